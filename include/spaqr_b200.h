@@ -1,0 +1,108 @@
+/*
+ * spaqr_b200 — C ABI of the B200 implementation of the spaQR hot path.
+ *
+ * The reference (proj/include/spaqr/, C++20 + Eigen, single-threaded CPU) has
+ * no FFI or plugin layer; its drop-in boundary is the C++ API
+ *   Pipeline::Pipeline           proj/include/spaqr/pipeline.h:39-44
+ *   spaqr_factorize(A,h,owner)   proj/include/spaqr/factorize.h:51-53
+ *   Factorization::w_solve/...   proj/include/spaqr/transforms.h:66-69
+ *   cgls(A, W, b, u, opt, w)     proj/include/spaqr/solve.h:30-31
+ *   csne_solve(...)              proj/include/spaqr/solve.h:39-41
+ *   block_householder_qr, apply_reflectors_left_t, truncated_cpqr,
+ *   tri_solve_upper              proj/include/spaqr/dense_kernels.h:24-54
+ * Each entry point below replaces one of those (cited per function).  Plain
+ * pointers and sizes only; host arrays unless a name says "_dev".
+ *
+ * Conventions: matrices are FP64 column-major; indices are int32; A is CSC
+ * (colptr n+1, rowind nnz, vals nnz).  Status codes: SPQR_OK, SPQR_E_SINGULAR
+ * (singular front; *err_cluster names it, as SingularFrontError, types.h:24-31),
+ * SPQR_E_SHAPE (std::invalid_argument), SPQR_E_CUDA, SPQR_E_OTHER.  One host
+ * thread per handle.
+ */
+#ifndef SPAQR_B200_H
+#define SPAQR_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { SPQR_OK = 0, SPQR_E_SINGULAR = 1, SPQR_E_SHAPE = 2, SPQR_E_CUDA = 3, SPQR_E_OTHER = 4 };
+enum { SPQR_SOLVER_SPAQR = 0, SPQR_SOLVER_DIRECT = 1, SPQR_SOLVER_DIAG = 2 };
+enum { SPQR_W_APPLY = 0, SPQR_W_SOLVE = 1, SPQR_WT_APPLY = 2, SPQR_WT_SOLVE = 3 };
+
+typedef struct spqr_pipeline spqr_pipeline;
+
+/* Library / device probes. */
+const char* spqr_version(void);
+int spqr_device_count(void);
+
+/* Pipeline::Pipeline (pipeline.cpp:19-62): scale columns, nested dissection
+ * (geometric when coords != NULL, imported when parts != NULL), interfaces,
+ * ordering, row matching/assignment on the host; spaqr_factorize
+ * (factorize.cpp:795-804) on the GPU.  levels <= 0 picks default_num_levels. */
+int spqr_pipeline_create(int m, int n, const int* colptr, const int* rowind, const double* vals,
+                         const double* coords, int dim, const int* parts, int levels, double eps,
+                         int skip_levels, int solver, int device, spqr_pipeline** out, char* err, int errlen,
+                         int* err_cluster);
+void spqr_pipeline_destroy(spqr_pipeline* p);
+
+/* info[16]: M, N, L, nclusters, nW, n_dropped, n_trailing, n_stages, nnz_w, nnz(A), n_batches,
+ *           engine launches, engine syncs, h2d bytes, d2h bytes, solve-plan launches per sweep pair */
+void spqr_pipeline_info(const spqr_pipeline* p, long long* info);
+/* times[16]: t_partition, t_factorize, t_upload, qr_device_ms, qr_flops, qr_bytes, cpqr_flops,
+ *            cpqr_bytes, qr_launches, (reserved) */
+void spqr_pipeline_times(const spqr_pipeline* p, double* times);
+
+/* Pipeline::solve (pipeline.cpp:70-80) -> cgls (solve.cpp:24-76) on the device, or
+ * Pipeline::solve_direct (:82-92) -> csne_solve (solve.cpp:78-108) when direct != 0.
+ * b: M, x: N (original column order and scaling).  hist needs maxit+2 (direct: refine+1) slots.
+ * tol <= 0 / maxit <= 0 use the pipeline defaults (1e-12 / 500). */
+int spqr_pipeline_solve(spqr_pipeline* p, int direct, const double* b, double* x, double tol, int maxit,
+                        int* iters, int* converged, double* hist, int* nhist, double* t_solve, char* err,
+                        int errlen);
+
+/* Factorization::w_apply / w_solve / wt_apply / wt_solve (transforms.cpp:40-111),
+ * applied on the device to a host vector z of length N (permuted coordinates). */
+int spqr_pipeline_apply(spqr_pipeline* p, int mode, double* z);
+
+/* Structure getters (reference-facing results for parity checks). */
+void spqr_pipeline_perm(const spqr_pipeline* p, int* perm);          /* N: perm[new] = old */
+void spqr_pipeline_owner(const spqr_pipeline* p, int* owner);        /* M: row -> finest cluster */
+void spqr_pipeline_weights(const spqr_pipeline* p, double* w);       /* N */
+/* pivot_row: N; dropped: n_dropped; trailing: n_trailing (info[5], info[6]) */
+void spqr_pipeline_rows(const spqr_pipeline* p, int* pivot_row, int* dropped, int* trailing);
+/* cluster: tree_node, level, parent, stage, interior, ncols */
+void spqr_pipeline_cluster(const spqr_pipeline* p, int c, int* info6);
+void spqr_pipeline_cluster_cols(const spqr_pipeline* p, int c, int* cols);
+/* StageStats (transforms.h:40-47): out5 = stage, nfronts, top_rows, top_cols, nnz_w; t5 = phase times */
+void spqr_pipeline_stage(const spqr_pipeline* p, int s, long long* out5, double* t5);
+void spqr_pipeline_stage_fronts(const spqr_pipeline* p, int s, int* front_cols, double* front_aspect);
+/* W factor i: out4 = kind (0 TriangularScale, 1 ColumnRotation), |cols|, |coupled| or k, batch */
+void spqr_pipeline_wfactor(const spqr_pipeline* p, int i, int* out4);
+/* kind 0: cols, R (c x c), coupled, C (c x k).  kind 1: cols, V (c x k), tau, sign. */
+int spqr_pipeline_wfactor_data(const spqr_pipeline* p, int i, int* cols, double* a, int* coupled, double* b,
+                               double* c);
+
+/* ---- dense kernels (dense_kernels.h:24-54), batched, one launch each ---- */
+/* block_householder_qr + apply_reflectors_left_t fused: for each of nb problems
+ * (m x ntot, column-major, packed back to back in a), QR of the first n columns
+ * and H^T on the remaining ntot-n.  On exit: R (nonnegative diagonal) in the
+ * upper triangle, reflectors (unit diagonal implicit) below, H^T X to the right.
+ * info[b] = -1 ok, else the first zero/denormal pivot. */
+int spqr_qr_apply_batched(int nb, int m, int n, int ntot, double* a, double* tau, double* sign, int* info);
+/* Same on device pointers (timed by the caller's stream: 0 = default). Returns device ms. */
+int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, double* d_tau, double* d_sign,
+                              int* d_info, float* ms);
+/* truncated_cpqr (dense_kernels.cpp:124-232) for nb m x n problems.  Outputs per
+ * problem b (kmax = min(m,n)): rank[b], r11[b], perm[b*kmax..], R[b*kmax*n..]
+ * (rank x n, ld = kmax, original column order), V[b*m*kmax..] (ld = m), tau, sign. */
+int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* rank, double* r11, int* perm,
+                      double* R, double* V, double* tau, double* sign);
+/* tri_solve_upper(R, B, Right, false) (dense_kernels.cpp:242-257): B (nrows x n) <- B R^{-1}
+ * for nb problems packed back to back; R (n x n) per problem. */
+int spqr_trsm_right_batched(int nb, int nrows, int n, double* b, const double* r);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPAQR_B200_H */

@@ -1,0 +1,227 @@
+"""Python mirror of the reference's public API over the C ABI.
+
+Names, argument meaning and error behaviour follow proj/include/spaqr:
+Pipeline(A, opt, coords, parts) (pipeline.h:39-44), Pipeline.solve /
+solve_direct (:46-52), Factorization.w_apply/w_solve/wt_apply/wt_solve
+(transforms.h:66-69), SingularFrontError{cluster, reason} (types.h:24-31).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import lib, require_gpu
+
+SOLVERS = {"spaqr": 0, "direct": 1, "diag": 2}
+
+
+class SingularFrontError(RuntimeError):
+    def __init__(self, cluster, msg):
+        super().__init__(msg)
+        self.cluster = cluster
+        self.reason = msg.split("| reason: ")[-1]
+
+
+def _csc(A):
+    A = A.tocsc()
+    return (int(A.shape[0]), int(A.shape[1]), np.ascontiguousarray(A.indptr, np.int32),
+            np.ascontiguousarray(A.indices, np.int32), np.ascontiguousarray(A.data, np.float64))
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class Pipeline:
+    """spqr_pipeline_create / _solve / _apply (include/spaqr_b200.h)."""
+
+    def __init__(self, A, eps=1e-2, levels=0, skip_levels=3, solver="spaqr", coords=None, parts=None, device=0):
+        require_gpu()
+        L = lib()
+        m, n, p, i, x = _csc(A)
+        cp = None if coords is None else np.ascontiguousarray(coords, np.float64)
+        pp = None if parts is None else np.ascontiguousarray(parts, np.int32)
+        dim = 0 if cp is None else cp.shape[1]
+        err = C.create_string_buffer(512)
+        cl = C.c_int(-1)
+        h = C.c_void_p()
+        rc = L.spqr_pipeline_create(m, n, p, i, x, _ptr(cp), dim, _ptr(pp), int(levels), float(eps), int(skip_levels),
+                                    SOLVERS[solver], int(device), C.byref(h), err, 512, C.byref(cl))
+        if rc != 0:
+            msg = err.value.decode()
+            if rc == 1:
+                raise SingularFrontError(cl.value, msg)
+            if rc == 2:
+                raise ValueError(msg)
+            raise RuntimeError(msg)
+        self.h = h
+        info = np.zeros(16, np.int64)
+        L.spqr_pipeline_info(self.h, info)
+        (self.M, self.N, self.L, self.nclusters, self.nW, self.ndropped, self.ntrailing, self.nstages, self.nnz_w,
+         self.nnz_A, self.nbatches, self.launches, self.syncs, self.h2d_bytes, self.d2h_bytes,
+         self.sweep_launches) = [int(v) for v in info]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().spqr_pipeline_destroy(self.h)
+            self.h = None
+
+    def times(self):
+        t = np.zeros(16)
+        lib().spqr_pipeline_times(self.h, t)
+        return dict(t_partition=t[0], t_factorize=t[1], t_upload=t[2], qr_ms=t[3], qr_flops=t[4], qr_bytes=t[5],
+                    cpqr_flops=t[6], cpqr_bytes=t[7], qr_launches=int(t[8]))
+
+    def solve(self, b, tol=-1.0, maxit=-1, direct=False):
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.zeros(self.N)
+        hist = np.zeros((maxit if maxit > 0 else 500) + 4)
+        it, cv, nh = C.c_int(), C.c_int(), C.c_int()
+        ts = C.c_double()
+        err = C.create_string_buffer(256)
+        rc = lib().spqr_pipeline_solve(self.h, int(direct), b, x, float(tol), int(maxit), C.byref(it), C.byref(cv),
+                                       hist, C.byref(nh), C.byref(ts), err, 256)
+        if rc:
+            raise RuntimeError(err.value.decode())
+        return x, dict(iterations=it.value, converged=bool(cv.value), residual_history=hist[: nh.value].copy(),
+                       t_solve=ts.value, dropped_rows=self.ndropped)
+
+    def _apply(self, mode, z):
+        z = np.array(z, dtype=np.float64, copy=True)
+        if lib().spqr_pipeline_apply(self.h, mode, z):
+            raise RuntimeError("spqr_pipeline_apply failed")
+        return z
+
+    def w_apply(self, z): return self._apply(0, z)
+    def w_solve(self, z): return self._apply(1, z)
+    def wt_apply(self, z): return self._apply(2, z)
+    def wt_solve(self, z): return self._apply(3, z)
+
+    def perm(self):
+        o = np.zeros(self.N, np.int32)
+        lib().spqr_pipeline_perm(self.h, o)
+        return o
+
+    def owner(self):
+        o = np.zeros(self.M, np.int32)
+        lib().spqr_pipeline_owner(self.h, o)
+        return o
+
+    def weights(self):
+        o = np.zeros(self.N)
+        lib().spqr_pipeline_weights(self.h, o)
+        return o
+
+    def rows(self):
+        pr = np.zeros(self.N, np.int32)
+        dr = np.zeros(max(self.ndropped, 1), np.int32)
+        tr = np.zeros(max(self.ntrailing, 1), np.int32)
+        lib().spqr_pipeline_rows(self.h, pr, dr, tr)
+        return pr, dr[: self.ndropped], tr[: self.ntrailing]
+
+    def clusters(self):
+        out = []
+        info = np.zeros(6, np.int32)
+        for c in range(self.nclusters):
+            lib().spqr_pipeline_cluster(self.h, c, info)
+            cols = np.zeros(max(int(info[5]), 1), np.int32)
+            lib().spqr_pipeline_cluster_cols(self.h, c, cols)
+            out.append(dict(tree_node=int(info[0]), level=int(info[1]), parent=int(info[2]), stage=int(info[3]),
+                            interior=bool(info[4]), cols=cols[: int(info[5])].copy()))
+        return out
+
+    def stages(self):
+        out = []
+        o = np.zeros(5, np.int64)
+        t = np.zeros(5)
+        for s in range(self.nstages):
+            lib().spqr_pipeline_stage(self.h, s, o, t)
+            nf = int(o[1])
+            fc = np.zeros(max(nf, 1), np.int32)
+            fa = np.zeros(max(nf, 1))
+            lib().spqr_pipeline_stage_fronts(self.h, s, fc, fa)
+            out.append(dict(stage=int(o[0]), front_cols=fc[:nf].copy(), front_aspect=fa[:nf].copy(),
+                            top_rows=int(o[2]), top_cols=int(o[3]), nnz_w=int(o[4]), t_eliminate=t[0],
+                            t_reassign=t[1], t_scale=t[2], t_sparsify=t[3], t_merge=t[4]))
+        return out
+
+    def wfactors(self):
+        out = []
+        info = np.zeros(4, np.int32)
+        for f in range(self.nW):
+            lib().spqr_pipeline_wfactor(self.h, f, info)
+            kind, c, d = int(info[0]), int(info[1]), int(info[2])
+            cols = np.zeros(max(c, 1), np.int32)
+            if kind == 0:
+                R = np.zeros(max(c * c, 1))
+                cp = np.zeros(max(d, 1), np.int32)
+                Cm = np.zeros(max(c * d, 1))
+                lib().spqr_pipeline_wfactor_data(self.h, f, cols, R, cp, Cm, np.zeros(1))
+                out.append(("tri", cols[:c].copy(), R[: c * c].reshape(c, c, order="F").copy(), cp[:d].copy(),
+                            Cm[: c * d].reshape(c, d, order="F").copy()))
+            else:
+                V = np.zeros(max(c * d, 1))
+                tau = np.zeros(max(d, 1))
+                sg = np.zeros(max(d, 1))
+                lib().spqr_pipeline_wfactor_data(self.h, f, cols, V, np.zeros(1, np.int32), tau, sg)
+                out.append(("rot", cols[:c].copy(), V[: c * d].reshape(c, d, order="F").copy(), tau[:d].copy(),
+                            sg[:d].copy()))
+        return out
+
+
+def qr_apply_batched(A, n):
+    """A: (nb, m, ntot) float64 (each block column-major when viewed as A[b].T.ravel()).
+    Returns (A_out, tau, sign, info) with R/V in the first n columns and H^T X after."""
+    require_gpu()
+    A = np.asarray(A, np.float64)
+    nb, m, ntot = A.shape
+    buf = np.ascontiguousarray(A.transpose(0, 2, 1)).ravel()  # column-major per block
+    tau = np.zeros(max(nb * n, 1))
+    sg = np.zeros(max(nb * n, 1))
+    info = np.zeros(max(nb, 1), np.int32)
+    rc = lib().spqr_qr_apply_batched(nb, m, n, ntot, buf, tau, sg, info)
+    if rc:
+        raise RuntimeError(f"spqr_qr_apply_batched failed ({rc})")
+    out = buf.reshape(nb, ntot, m).transpose(0, 2, 1).copy()
+    return out, tau[: nb * n].reshape(nb, n), sg[: nb * n].reshape(nb, n), info[:nb]
+
+
+def cpqr_batched(A, eps):
+    """A: (nb, m, n).  Returns list of dicts like oracle.cpqr."""
+    require_gpu()
+    A = np.asarray(A, np.float64)
+    nb, m, n = A.shape
+    k = max(min(m, n), 1)
+    buf = np.ascontiguousarray(A.transpose(0, 2, 1)).ravel()
+    rank = np.zeros(nb, np.int32)
+    r11 = np.zeros(nb)
+    perm = np.zeros(nb * k, np.int32)
+    R = np.zeros(nb * k * max(n, 1))
+    V = np.zeros(nb * max(m, 1) * k)
+    tau = np.zeros(nb * k)
+    sg = np.zeros(nb * k)
+    rc = lib().spqr_cpqr_batched(nb, m, n, buf, float(eps), rank, r11, perm, R, V, tau, sg)
+    if rc:
+        raise RuntimeError(f"spqr_cpqr_batched failed ({rc})")
+    out = []
+    for b in range(nb):
+        r = int(rank[b])
+        Rb = R[b * k * n:(b + 1) * k * n].reshape(n, k).T[:r]
+        Vb = V[b * m * k:(b + 1) * m * k].reshape(k, m).T[:, :r]
+        out.append(dict(rank=r, r11=float(r11[b]), perm=perm[b * k:b * k + r].copy(), R=Rb.copy(), V=Vb.copy(),
+                        tau=tau[b * k:b * k + r].copy(), sign=sg[b * k:b * k + r].copy()))
+    return out
+
+
+def trsm_right_batched(B, R):
+    """B (nb, nrows, n) <- B R^{-1} with R (nb, n, n) upper triangular."""
+    require_gpu()
+    B = np.asarray(B, np.float64)
+    nb, nrows, n = B.shape
+    bb = np.ascontiguousarray(B.transpose(0, 2, 1)).ravel()
+    rr = np.ascontiguousarray(np.asarray(R, np.float64).transpose(0, 2, 1)).ravel()
+    rc = lib().spqr_trsm_right_batched(nb, nrows, n, bb, rr)
+    if rc:
+        raise RuntimeError(f"spqr_trsm_right_batched failed ({rc})")
+    return bb.reshape(nb, n, nrows).transpose(0, 2, 1).copy()

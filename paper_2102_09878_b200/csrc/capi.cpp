@@ -1,0 +1,417 @@
+// C ABI (include/spaqr_b200.h) over the B200 spaQR implementation: the
+// Pipeline mirror (proj/src/pipeline.cpp) with host partitioning and the GPU
+// engine / solver, plus batched dense-kernel entry points.
+#include "../../include/spaqr_b200.h"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "dev.h"
+#include "engine.h"
+#include "solve.h"
+
+using namespace spqr;
+
+struct spqr_pipeline {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    double eps = 1e-2;
+    int levels = 0, skip = 3, solver = SPQR_SOLVER_SPAQR, refine = 1, maxit = 500;
+    double tol = 1e-12;
+    Csc Aw;
+    std::vector<double> d, weights;
+    std::vector<Index> perm;
+    std::vector<int> owner;
+    SeparatorTree tree;
+    ClusterHierarchy h;
+    bool has_f = false;
+    DeviceFactorization F;
+    SolvePlan plan;
+    DevMatrix dA;
+    CglsWork ws;
+    double* d_w = nullptr;
+    double *d_b = nullptr, *d_u = nullptr;
+    std::unique_ptr<DeviceArena> mem;
+    double t_partition = 0, t_factorize = 0, t_upload = 0;
+    ~spqr_pipeline() {
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+namespace {
+
+void put_err(char* err, int errlen, const std::string& s) {
+    if (!err || errlen <= 0) return;
+    std::strncpy(err, s.c_str(), static_cast<size_t>(errlen - 1));
+    err[errlen - 1] = 0;
+}
+
+template <class F>
+int guarded(char* err, int errlen, int* err_cluster, F&& f) {
+    try {
+        f();
+        return SPQR_OK;
+    } catch (const SingularFrontError& e) {
+        if (err_cluster) *err_cluster = e.cluster;
+        put_err(err, errlen, std::string(e.what()) + " | reason: " + e.reason);
+        return SPQR_E_SINGULAR;
+    } catch (const std::invalid_argument& e) {
+        put_err(err, errlen, e.what());
+        return SPQR_E_SHAPE;
+    } catch (const CudaError& e) {
+        put_err(err, errlen, e.what());
+        return SPQR_E_CUDA;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return SPQR_E_OTHER;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spqr_version(void) { return "spaqr_b200 0.1 (sm_100a)"; }
+
+int spqr_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int spqr_pipeline_create(int m, int n, const int* colptr, const int* rowind, const double* vals, const double* coords,
+                         int dim, const int* parts, int levels, double eps, int skip_levels, int solver, int device,
+                         spqr_pipeline** out, char* err, int errlen, int* err_cluster) {
+    *out = nullptr;
+    auto* P = new spqr_pipeline;
+    const int rc = guarded(err, errlen, err_cluster, [&] {
+        P->device = device;
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
+        P->eps = (solver == SPQR_SOLVER_DIRECT) ? 0.0 : eps;  // pipeline.cpp:24
+        P->levels = levels;
+        P->skip = skip_levels;
+        P->solver = solver;
+        P->Aw = csc_canonical(m, n, colptr, rowind, vals);
+        if (P->Aw.m < P->Aw.n) throw std::invalid_argument("matrix must have at least as many rows as columns");
+        P->d = scale_columns(P->Aw);
+        P->mem = std::make_unique<DeviceArena>(size_t(32) << 20);
+        if (solver == SPQR_SOLVER_DIAG) {
+            P->perm.resize(n);
+            std::iota(P->perm.begin(), P->perm.end(), 0);
+            P->weights = P->d;
+        } else {
+            double t0 = now_s();
+            const Graph g = ata_graph(P->Aw);
+            const int L = levels > 0 ? levels : default_num_levels(n);
+            if (parts) {
+                P->tree = import_partition(g, L, parts);
+            } else {
+                if (coords && dim <= 0) throw std::invalid_argument("coordinate dimension must be positive");
+                P->tree = nested_dissection(g, L, coords, dim);
+            }
+            P->h = build_interfaces(P->tree, g);
+            P->perm = order_columns(P->h);
+            P->Aw = permute_columns(P->Aw, P->perm);
+            const RowMatching mm = match_rows(P->Aw);
+            P->owner = assign_rows(P->Aw, P->h, mm);
+            P->t_partition = now_s() - t0;
+            P->weights.resize(n);
+            for (int i = 0; i < n; ++i) P->weights[i] = P->d[P->perm[i]];
+            t0 = now_s();
+            FactorizeOptions fo;
+            fo.eps = P->eps;
+            fo.skip_levels = skip_levels;
+            P->F = gpu_factorize(P->Aw, P->h, P->owner, fo, P->st);
+            P->plan = build_solve_plan(P->F, P->st);
+            P->has_f = true;
+            P->t_factorize = now_s() - t0;
+        }
+        const double t0 = now_s();
+        P->dA = upload_matrix(P->Aw, P->st);
+        P->ws = make_cgls_work(P->Aw.m, P->Aw.n);
+        P->d_w = P->mem->alloc_n<double>(std::max(n, 1));
+        P->d_b = P->mem->alloc_n<double>(std::max(m, 1));
+        P->d_u = P->mem->alloc_n<double>(std::max(n, 1));
+        CK(cudaMemcpyAsync(P->d_w, P->weights.data(), sizeof(double) * n, cudaMemcpyHostToDevice, P->st));
+        CK(cudaStreamSynchronize(P->st));
+        P->t_upload = now_s() - t0;
+    });
+    if (rc != SPQR_OK) {
+        delete P;
+        return rc;
+    }
+    *out = P;
+    return SPQR_OK;
+}
+
+void spqr_pipeline_destroy(spqr_pipeline* p) { delete p; }
+
+void spqr_pipeline_info(const spqr_pipeline* p, long long* o) {
+    std::fill(o, o + 16, 0LL);
+    o[0] = p->Aw.m;
+    o[1] = p->Aw.n;
+    o[2] = p->h.num_levels;
+    o[3] = static_cast<long long>(p->h.clusters.size());
+    o[4] = static_cast<long long>(p->F.W.size());
+    o[5] = static_cast<long long>(p->F.dropped_rows.size());
+    o[6] = static_cast<long long>(p->F.trailing_rows.size());
+    o[7] = static_cast<long long>(p->F.stages.size());
+    o[8] = p->F.nnz_w();
+    o[9] = p->Aw.nnz();
+    o[10] = static_cast<long long>(p->plan.batches.size());
+    o[11] = p->F.ctr.launches;
+    o[12] = p->F.ctr.syncs;
+    o[13] = p->F.ctr.h2d_bytes;
+    o[14] = p->F.ctr.d2h_bytes;
+    o[15] = p->plan.launches_per_sweep + p->plan.launches_per_sweep_t;
+}
+
+void spqr_pipeline_times(const spqr_pipeline* p, double* t) {
+    std::fill(t, t + 16, 0.0);
+    t[0] = p->t_partition;
+    t[1] = p->t_factorize;
+    t[2] = p->t_upload;
+    t[3] = p->F.ctr.t_qr_ms;
+    t[4] = p->F.ctr.qr_flops;
+    t[5] = p->F.ctr.qr_bytes;
+    t[6] = p->F.ctr.cpqr_flops;
+    t[7] = p->F.ctr.cpqr_bytes;
+    t[8] = static_cast<double>(p->F.ctr.qr_launches);
+}
+
+int spqr_pipeline_solve(spqr_pipeline* p, int direct, const double* b, double* x, double tol, int maxit, int* iters,
+                        int* converged, double* hist, int* nhist, double* t_solve, char* err, int errlen) {
+    int cl = -1;
+    return guarded(err, errlen, &cl, [&] {
+        if (direct && !p->has_f) throw std::logic_error("direct solve requires a factorization");
+        CK(cudaSetDevice(p->device));
+        const int m = p->Aw.m, n = p->Aw.n;
+        const double t0 = now_s();
+        CK(cudaMemcpyAsync(p->d_b, b, sizeof(double) * m, cudaMemcpyHostToDevice, p->st));
+        SolveReport rep;
+        if (direct)
+            rep = gpu_csne(p->dA, p->plan, p->d_b, p->d_u, p->refine, p->d_w, p->tol, p->ws, p->st);
+        else
+            rep = gpu_cgls(p->dA, p->has_f ? &p->plan : nullptr, p->d_b, p->d_u, tol > 0 ? tol : p->tol,
+                           maxit > 0 ? maxit : p->maxit, p->d_w, p->ws, p->st);
+        std::vector<double> u(n);
+        CK(cudaMemcpyAsync(u.data(), p->d_u, sizeof(double) * n, cudaMemcpyDeviceToHost, p->st));
+        CK(cudaStreamSynchronize(p->st));
+        for (int i = 0; i < n; ++i) x[p->perm[i]] = u[i] / p->d[p->perm[i]];  // pipeline.cpp:65-68
+        *iters = rep.iterations;
+        *converged = rep.converged;
+        *nhist = static_cast<int>(rep.residual_history.size());
+        std::copy(rep.residual_history.begin(), rep.residual_history.end(), hist);
+        *t_solve = now_s() - t0;
+    });
+}
+
+int spqr_pipeline_apply(spqr_pipeline* p, int mode, double* z) {
+    int cl = -1;
+    return guarded(nullptr, 0, &cl, [&] {
+        CK(cudaSetDevice(p->device));
+        const int n = p->Aw.n;
+        CK(cudaMemcpyAsync(p->d_u, z, sizeof(double) * n, cudaMemcpyHostToDevice, p->st));
+        static const SweepMode map[4] = {kWApply, kWSolve, kWtApply, kWtSolve};
+        if (p->has_f) sweep(p->plan, map[mode & 3], p->d_u, p->st);
+        CK(cudaMemcpyAsync(z, p->d_u, sizeof(double) * n, cudaMemcpyDeviceToHost, p->st));
+        CK(cudaStreamSynchronize(p->st));
+    });
+}
+
+void spqr_pipeline_perm(const spqr_pipeline* p, int* o) { std::copy(p->perm.begin(), p->perm.end(), o); }
+void spqr_pipeline_owner(const spqr_pipeline* p, int* o) { std::copy(p->owner.begin(), p->owner.end(), o); }
+void spqr_pipeline_weights(const spqr_pipeline* p, double* o) { std::copy(p->weights.begin(), p->weights.end(), o); }
+void spqr_pipeline_rows(const spqr_pipeline* p, int* pr, int* dr, int* tr) {
+    std::copy(p->F.pivot_row.begin(), p->F.pivot_row.end(), pr);
+    std::copy(p->F.dropped_rows.begin(), p->F.dropped_rows.end(), dr);
+    std::copy(p->F.trailing_rows.begin(), p->F.trailing_rows.end(), tr);
+}
+void spqr_pipeline_cluster(const spqr_pipeline* p, int c, int* info) {
+    const auto& C = p->h.clusters[c];
+    info[0] = C.tree_node;
+    info[1] = C.level;
+    info[2] = C.parent;
+    info[3] = C.stage;
+    info[4] = C.interior;
+    info[5] = static_cast<int>(C.cols.size());
+}
+void spqr_pipeline_cluster_cols(const spqr_pipeline* p, int c, int* o) {
+    std::copy(p->h.clusters[c].cols.begin(), p->h.clusters[c].cols.end(), o);
+}
+void spqr_pipeline_stage(const spqr_pipeline* p, int s, long long* o, double* t) {
+    const StageStats& st = p->F.stages[s];
+    o[0] = st.stage;
+    o[1] = static_cast<long long>(st.front_cols.size());
+    o[2] = st.top_rows;
+    o[3] = st.top_cols;
+    o[4] = st.nnz_w;
+    t[0] = st.t_eliminate;
+    t[1] = st.t_reassign;
+    t[2] = st.t_scale;
+    t[3] = st.t_sparsify;
+    t[4] = st.t_merge;
+}
+void spqr_pipeline_stage_fronts(const spqr_pipeline* p, int s, int* cols, double* aspect) {
+    const StageStats& st = p->F.stages[s];
+    std::copy(st.front_cols.begin(), st.front_cols.end(), cols);
+    std::copy(st.front_aspect.begin(), st.front_aspect.end(), aspect);
+}
+void spqr_pipeline_wfactor(const spqr_pipeline* p, int i, int* o) {
+    const DevWFactor& w = p->F.W[i];
+    o[0] = w.kind;
+    o[1] = w.c;
+    o[2] = w.k;
+    o[3] = w.batch;
+}
+int spqr_pipeline_wfactor_data(const spqr_pipeline* p, int i, int* cols, double* a, int* coupled, double* b, double* c) {
+    int cl = -1;
+    return guarded(nullptr, 0, &cl, [&] {
+        const DevWFactor& w = p->F.W[i];
+        std::copy(p->F.idx.begin() + w.cols_off, p->F.idx.begin() + w.cols_off + w.c, cols);
+        if (w.kind == 0) {
+            std::copy(p->F.idx.begin() + w.coupled_off, p->F.idx.begin() + w.coupled_off + w.k, coupled);
+            std::vector<double> buf(static_cast<size_t>(w.c) * (w.c + w.k));
+            if (!buf.empty()) CK(cudaMemcpy(buf.data(), w.a, sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
+            std::copy(buf.begin(), buf.begin() + static_cast<long long>(w.c) * w.c, a);
+            std::copy(buf.begin() + static_cast<long long>(w.c) * w.c, buf.end(), b);
+        } else {
+            if (w.c * w.k > 0) CK(cudaMemcpy(a, w.a, sizeof(double) * w.c * w.k, cudaMemcpyDeviceToHost));
+            if (w.k > 0) {
+                CK(cudaMemcpy(b, w.tau, sizeof(double) * w.k, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(c, w.sign, sizeof(double) * w.k, cudaMemcpyDeviceToHost));
+            }
+        }
+    });
+}
+
+// ------------------------------------------------------------ dense kernels
+int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, double* d_tau, double* d_sign, int* d_info,
+                              float* ms) {
+    int cl = -1;
+    return guarded(nullptr, 0, &cl, [&] {
+        if (n > m || ntot < n || n > 1024) throw std::invalid_argument("qr: need n <= m, n <= ntot, n <= 1024");
+        std::vector<QrDesc> qd(nb);
+        for (int b = 0; b < nb; ++b)
+            qd[b] = QrDesc{d_a + static_cast<long long>(b) * m * ntot, m, m, n, ntot, d_tau + static_cast<long long>(b) * n,
+                           d_sign + static_cast<long long>(b) * n, nullptr, d_info + b, 0};
+        QrDesc* dq = nullptr;
+        CK(cudaMalloc(&dq, sizeof(QrDesc) * std::max(nb, 1)));
+        CK(cudaMemcpy(dq, qd.data(), sizeof(QrDesc) * nb, cudaMemcpyHostToDevice));
+        std::vector<int> init(nb, INT_MAX);
+        CK(cudaMemcpy(d_info, init.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, 0));
+        launch_qr(dq, nb, m, 0);
+        CK(cudaEventRecord(e1, 0));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaGetLastError());
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, e0, e1));
+        if (ms) *ms = t;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(dq);
+    });
+}
+
+int spqr_qr_apply_batched(int nb, int m, int n, int ntot, double* a, double* tau, double* sign, int* info) {
+    int cl = -1;
+    return guarded(nullptr, 0, &cl, [&] {
+        const size_t na = static_cast<size_t>(nb) * m * ntot;
+        double *da = nullptr, *dt = nullptr, *ds = nullptr;
+        int* di = nullptr;
+        CK(cudaMalloc(&da, sizeof(double) * std::max<size_t>(na, 1)));
+        CK(cudaMalloc(&dt, sizeof(double) * std::max(nb * n, 1)));
+        CK(cudaMalloc(&ds, sizeof(double) * std::max(nb * n, 1)));
+        CK(cudaMalloc(&di, sizeof(int) * std::max(nb, 1)));
+        CK(cudaMemcpy(da, a, sizeof(double) * na, cudaMemcpyHostToDevice));
+        float ms = 0;
+        const int rc = spqr_qr_apply_batched_dev(nb, m, n, ntot, da, dt, ds, di, &ms);
+        if (rc != SPQR_OK) throw std::runtime_error("qr launch failed");
+        CK(cudaMemcpy(a, da, sizeof(double) * na, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(tau, dt, sizeof(double) * nb * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(sign, ds, sizeof(double) * nb * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(info, di, sizeof(int) * nb, cudaMemcpyDeviceToHost));
+        for (int b = 0; b < nb; ++b)
+            if (info[b] == INT_MAX) info[b] = -1;
+        cudaFree(da);
+        cudaFree(dt);
+        cudaFree(ds);
+        cudaFree(di);
+    });
+}
+
+int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* rank, double* r11, int* perm, double* R,
+                      double* V, double* tau, double* sign) {
+    int cl = -1;
+    return guarded(nullptr, 0, &cl, [&] {
+        const int kmax = std::min(m, n);
+        const size_t na = static_cast<size_t>(nb) * m * n;
+        DeviceArena mem;
+        double* da = mem.alloc_n<double>(std::max<size_t>(na, 1));
+        double* dV = mem.alloc_n<double>(std::max<size_t>(static_cast<size_t>(nb) * m * kmax, 1));
+        double* dt = mem.alloc_n<double>(std::max(nb * kmax, 1));
+        double* ds = mem.alloc_n<double>(std::max(nb * kmax, 1));
+        int* dp = mem.alloc_n<int>(std::max(nb * kmax, 1));
+        int* dr = mem.alloc_n<int>(std::max(nb, 1));
+        double* d11 = mem.alloc_n<double>(std::max(nb, 1));
+        double* work = mem.alloc_n<double>(std::max<size_t>(static_cast<size_t>(nb) * 3 * n, 1));
+        CK(cudaMemcpy(da, a, sizeof(double) * na, cudaMemcpyHostToDevice));
+        CK(cudaMemset(dV, 0, sizeof(double) * static_cast<size_t>(nb) * m * kmax));
+        std::vector<CpqrDesc> cd(nb);
+        for (int b = 0; b < nb; ++b)
+            cd[b] = CpqrDesc{da + static_cast<long long>(b) * m * n, m, m, n, eps, dr + b, d11 + b,
+                             dV + static_cast<long long>(b) * m * kmax, m, dt + b * kmax, ds + b * kmax, dp + b * kmax,
+                             work + static_cast<long long>(b) * 3 * n};
+        CpqrDesc* dc = mem.alloc_n<CpqrDesc>(std::max(nb, 1));
+        CK(cudaMemcpy(dc, cd.data(), sizeof(CpqrDesc) * nb, cudaMemcpyHostToDevice));
+        launch_cpqr(dc, nb, m, 0);
+        CK(cudaDeviceSynchronize());
+        CK(cudaGetLastError());
+        std::vector<double> A(na);
+        CK(cudaMemcpy(A.data(), da, sizeof(double) * na, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(rank, dr, sizeof(int) * nb, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(r11, d11, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(perm, dp, sizeof(int) * nb * kmax, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(V, dV, sizeof(double) * static_cast<size_t>(nb) * m * kmax, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(tau, dt, sizeof(double) * nb * kmax, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(sign, ds, sizeof(double) * nb * kmax, cudaMemcpyDeviceToHost));
+        for (int b = 0; b < nb; ++b) {
+            double* Rb = R + static_cast<long long>(b) * kmax * n;
+            const double* Ab = A.data() + static_cast<long long>(b) * m * n;
+            for (int j = 0; j < n; ++j)
+                for (int i = 0; i < kmax; ++i) Rb[i + static_cast<long long>(j) * kmax] = i < rank[b] ? Ab[i + static_cast<long long>(j) * m] : 0.0;
+        }
+    });
+}
+
+int spqr_trsm_right_batched(int nb, int nrows, int n, double* b, const double* r) {
+    int cl = -1;
+    return guarded(nullptr, 0, &cl, [&] {
+        DeviceArena mem;
+        const size_t nbb = static_cast<size_t>(nb) * nrows * n, nr = static_cast<size_t>(nb) * n * n;
+        double* db = mem.alloc_n<double>(std::max<size_t>(nbb, 1));
+        double* dr = mem.alloc_n<double>(std::max<size_t>(nr, 1));
+        CK(cudaMemcpy(db, b, sizeof(double) * nbb, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dr, r, sizeof(double) * nr, cudaMemcpyHostToDevice));
+        std::vector<TrsmDesc> td(nb);
+        for (int q = 0; q < nb; ++q)
+            td[q] = TrsmDesc{db + static_cast<long long>(q) * nrows * n, nrows, nrows, n, dr + static_cast<long long>(q) * n * n, n,
+                             static_cast<long long>(q) * nrows};
+        TrsmDesc* dt = mem.alloc_n<TrsmDesc>(std::max(nb, 1));
+        CK(cudaMemcpy(dt, td.data(), sizeof(TrsmDesc) * nb, cudaMemcpyHostToDevice));
+        launch_trsm(dt, nb, static_cast<long long>(nb) * nrows, 0);
+        CK(cudaDeviceSynchronize());
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(b, db, sizeof(double) * nbb, cudaMemcpyDeviceToHost));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// Device-side descriptors and launchers for the spaQR front kernels (sm_100a).
+//
+// All front data is FP64 column-major in HBM.  Every batched kernel takes a
+// flat array of per-problem descriptors built by the host engine each phase,
+// so one launch covers every front of a stage (thousands of tiny, variable
+// size problems) — the reference's per-cluster Eigen calls
+// (proj/src/factorize.cpp) become one launch per phase.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace spqr {
+
+// ---- generic gather ("assemble"): builds a destination matrix from rows of
+// up to a few source matrices.  dst(i,j) =
+//   primary   src[s1](r1, cmap[j*nsrc+s1])  if s1 >= 0 and that column >= 0
+//   otherwise src[s2](r2, cmap[j*nsrc+s2])  if s2 >= 0 and that column >= 0
+//   otherwise 0.
+// rowref = (s1, r1, s2, r2).  s1 == -2 selects scan mode: the first slot t
+// whose cmap entry for column j is mapped supplies row r1.  A cmap entry
+// c <= -2 encodes an identity column: value 1 on dst row (-c-2), else 0.
+// Covers stack gathers, scatter-back, row appends, merges, transposed copies
+// (element (i,j) of a source lives at p[i*rs + j*cs]).
+struct AsmSrc {
+    const double* p;
+    long long rs, cs;
+};
+struct AsmDst {
+    double* p;
+    int ld, nrows, ncols, nsrc;
+    int trans;           // 1: (nrows x ncols) is the logical view; stored transposed (p[j + i*ld])
+    long long row_off;   // into rowref (int4 per dst row)
+    long long cmap_off;  // into cmap (ncols * nsrc)
+    long long src_off;   // into src table
+    long long elem_off;  // exclusive prefix of nrows*ncols (work split)
+};
+
+// ---- row / block statistics (decisions made on the host from these)
+// mode 0: out_sq[off+i] = sum_j a(r0+i, c0+j)^2 (j ascending), out_nz[off+i] = any nonzero
+// mode 1: out_sq[off]   = max |a| over the block,             out_nz[off]   = any nonzero
+// mode 2: out_nz[off]   = block is exactly [I; 0]
+struct StatDesc {
+    const double* p;
+    int ld, r0, nrows, c0, ncols, mode;
+    long long out_off;
+    long long work_off;  // exclusive prefix of (mode 0 ? nrows : 1)
+};
+
+// ---- batched Householder QR of the first n columns of an m x ntot block,
+// reflectors applied (H^T, then the sign flip) to columns [n, ntot).  Eigen's
+// makeHouseholder convention + the reference's nonnegative-diagonal flip
+// (dense_kernels.cpp:11-35, 96-99).  R (flipped) stays in the upper triangle,
+// V (unit diagonal implicit) below it.
+struct QrDesc {
+    double* a;
+    int ld, m, n, ntot;
+    double* tau;      // n  (may be null)
+    double* sign;     // n  (may be null)
+    double* rout;     // optional copy of R (n x n, ld = n)
+    int* flag;        // atomicMin'd with the first i with |R_ii| < DBL_MIN (init INT_MAX; dense_kernels.cpp:234-240)
+    int set_identity; // after the update: A(:, :n) := [I; 0]  (factorize.cpp:473-474)
+};
+
+// ---- B <- B R^{-1} (right, upper, no transpose): factorize.cpp:475-478
+struct TrsmDesc {
+    double* b;
+    int ldb, nrows, n;
+    const double* r;
+    int ldr;
+    long long work_off;  // exclusive prefix of nrows
+};
+
+// ---- truncated column-pivoted QR in place (dense_kernels.cpp:124-232).
+// On exit rows [0, rank) of the block hold R in the ORIGINAL column order.
+struct CpqrDesc {
+    double* a;
+    int ld, m, n;
+    double eps;
+    int* rank;         // out
+    double* r11;       // out
+    double* V;         // optional: m x rank reflectors (ld = ldv), unit diag
+    int ldv;
+    double* tau;       // optional
+    double* sign;      // optional
+    int* perm;         // optional: pivot order (original column ids)
+    double* work;      // 2n doubles + n ints scratch
+};
+
+// launchers (kernels.cu); all enqueue on `st`
+void launch_assemble(const AsmDst* d_dst, int ndst, long long total_elems, const int4* d_rowref, const int* d_cmap,
+                     const AsmSrc* d_src, cudaStream_t st);
+void launch_stats(const StatDesc* d, int nd, long long total_work, double* out_sq, unsigned char* out_nz,
+                  cudaStream_t st);
+void launch_qr(const QrDesc* d, int nd, int max_m, cudaStream_t st);
+void launch_trsm(const TrsmDesc* d, int nd, long long total_rows, cudaStream_t st);
+void launch_cpqr(const CpqrDesc* d, int nd, int max_m, cudaStream_t st);
+void launch_scatter_values(const long long* off, const double* val, long long n, double* base, cudaStream_t st);
+
+// W-sweep kernels (solve) ------------------------------------------------------
+struct WFac {
+    int kind;     // 0 triangular (R | C), 1 rotation (V, tau, sign)
+    int c;        // |cols|
+    int k;        // |coupled| (triangular) or reflector count (rotation)
+    int pad;
+    const int* cols;
+    const int* coupled;
+    const double* a;  // triangular: [R | C] c x (c+k), ld = c ; rotation: V c x k, ld = c
+    const double* tau;
+    const double* sign;
+    long long contrib_off;  // wt_solve: offset of this factor's C^T zs contribution
+};
+// mode 0 w_solve, 1 wt_solve (writes C^T zs contributions), 2 w_apply, 3 wt_apply (contributions)
+void launch_wsweep(const WFac* f, int nf, double* z, double* contrib, int mode, int maxc, cudaStream_t st);
+// z[col[t]] (+/-)= contrib[idx[ptr[t]..ptr[t+1])] in order
+void launch_wreduce(const int* ptr, const int* idx, const int* col, int ncol, const double* contrib, double* z,
+                    double sgn, cudaStream_t st);
+
+// CGLS vector kernels
+void launch_spmv_csr(int m, const int* ptr, const int* idx, const double* val, const double* x, double* y,
+                     cudaStream_t st);
+void launch_dot_partial(int n, const double* a, const double* b, const double* w, double* partial, int nblocks,
+                        cudaStream_t st);
+void launch_finish_sum(const double* partial, int nblocks, double* out, cudaStream_t st);
+void launch_cgls_alpha(const double* gamma, const double* qq, double* alpha, int* brk, cudaStream_t st);
+void launch_axpy_dev(int n, const double* alpha, double sgn, const double* x, double* y, cudaStream_t st);
+void launch_cgls_p_update(int n, const double* s, const double* gnew, const double* gold, double* p, cudaStream_t st);
+void launch_copy(int n, const double* a, double* b, cudaStream_t st);
+
+int sm_count();
+
+}  // namespace spqr

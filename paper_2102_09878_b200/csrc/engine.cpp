@@ -1,0 +1,1444 @@
+// GPU spaQR engine (Algorithm 1, proj/src/factorize.cpp:17-791).
+//
+// Division of labour.  The host owns STRUCTURE: cluster ids, row-id lists,
+// the key sets of every front, holders, and every decision that the
+// reference takes (row selection, keysets, pivots, reassignment targets,
+// coupling pruning, ranks) — taken from small statistics vectors computed on
+// the GPU.  The GPU owns all FP64 front data.  Each phase of a stage is a
+// fixed number of batched launches:
+//   eliminate : stats -> [sync] -> gather stacks, QR + Q^T apply, post stats
+//               -> [sync] -> scatter/append/W copies as ONE assemble launch
+//   scale     : identity test -> [sync] -> QR + U^T apply + [I;0], TRSM
+//   sparsify  : gather + truncated CPQR -> [sync] -> write-back (rows);
+//               per dependency wave: gather G + CPQR -> [sync] -> assemble (cols)
+//   merge     : one assemble launch into the next stage's arena.
+// Within one eliminate batch the host replays the reference's sequential
+// bookkeeping exactly, on symbolic rows (a row's values are "row r of old
+// front f, overridden by row s of stack S_c for the stack's keys"); the
+// gathers then materialise every touched front once.
+#include "engine.h"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <map>
+
+#include "dev.h"
+
+namespace spqr {
+
+long long DeviceFactorization::nnz_w() const {  // transforms.cpp:25-38
+    long long s = 0;
+    for (const auto& f : W) {
+        const long long c = f.c, k = f.k;
+        if (f.kind == 0)
+            s += c * (c + 1) / 2 + c * k;
+        else
+            s += k * c - k * (k - 1) / 2 + k;
+    }
+    return s;
+}
+
+namespace {
+
+struct KeyRef {
+    int key, width, col;
+};
+
+struct Front {
+    bool live = false;
+    std::vector<int> rows;
+    std::vector<KeyRef> keys;  // ascending key; device layout: own key first, then ascending
+    double* mat = nullptr;
+    int ld = 0, ncols = 0;
+    bool scaled_ok = false;
+    std::vector<long long> soff;  // pre-stage row statistics offset per key (eliminate)
+    int find(int key) const {
+        auto it = std::lower_bound(keys.begin(), keys.end(), key, [](const KeyRef& a, int k) { return a.key < k; });
+        return (it != keys.end() && it->key == key) ? static_cast<int>(it - keys.begin()) : -1;
+    }
+    int nrows() const { return static_cast<int>(rows.size()); }
+};
+
+// symbolic row: values of old front `base` row `brow`, overridden by stack
+// `sidx` row `srow` on that stack's neighbour keys.
+struct PRow {
+    int gid, base, brow, sidx, srow;
+};
+struct KW {
+    int key, width;
+};
+struct PFront {
+    std::vector<PRow> rows;
+    std::vector<KW> keys;  // ascending
+    int find(int key) const {
+        auto it = std::lower_bound(keys.begin(), keys.end(), key, [](const KW& a, int k) { return a.key < k; });
+        return (it != keys.end() && it->key == key) ? static_cast<int>(it - keys.begin()) : -1;
+    }
+    void add(int key, int w) {
+        auto it = std::lower_bound(keys.begin(), keys.end(), key, [](const KW& a, int k) { return a.key < k; });
+        if (it == keys.end() || it->key != key) keys.insert(it, KW{key, w});
+    }
+    void erase(int key) {
+        auto it = std::lower_bound(keys.begin(), keys.end(), key, [](const KW& a, int k) { return a.key < k; });
+        if (it != keys.end() && it->key == key) keys.erase(it);
+    }
+};
+
+void sorted_insert(std::vector<int>& v, int x) {
+    auto it = std::lower_bound(v.begin(), v.end(), x);
+    if (it == v.end() || *it != x) v.insert(it, x);
+}
+void sorted_erase(std::vector<int>& v, int x) {
+    auto it = std::lower_bound(v.begin(), v.end(), x);
+    if (it != v.end() && *it == x) v.erase(it);
+}
+
+// One elimination of the current batch.
+struct Elim {
+    int c = -1, cs = 0;
+    std::vector<int> parts;
+    std::vector<int> keys;  // [c, keyset...]
+    std::vector<int> off;   // column offsets in S
+    std::vector<PRow> srows;
+    int total_rows = 0, tcols = 0, nsel_c = 0;
+    double* S = nullptr;
+    int* flag = nullptr;  // device
+    // post statistics (host): block max / nz of pivot rows; own non-pivot row sums per key
+    long long post_off = -1;
+};
+
+// Assemble job builder (generic gather, dev.h).
+struct AsmBuilder {
+    std::vector<AsmDst> dst;
+    std::vector<int4> rowref;
+    std::vector<int> cmap;
+    std::vector<AsmSrc> src;
+    long long elems = 0;
+    // begin a destination; returns index
+    int begin(double* p, int ld, int nrows, int ncols, int nsrc) {
+        AsmDst d;
+        d.p = p;
+        d.ld = ld;
+        d.nrows = nrows;
+        d.ncols = ncols;
+        d.nsrc = nsrc;
+        d.trans = 0;
+        d.row_off = static_cast<long long>(rowref.size());
+        d.cmap_off = static_cast<long long>(cmap.size());
+        d.src_off = static_cast<long long>(src.size());
+        d.elem_off = elems;
+        elems += static_cast<long long>(nrows) * ncols;
+        rowref.resize(rowref.size() + nrows, int4{-1, 0, -1, 0});
+        cmap.resize(cmap.size() + static_cast<size_t>(ncols) * nsrc, -1);
+        src.resize(src.size() + nsrc);
+        dst.push_back(d);
+        return static_cast<int>(dst.size()) - 1;
+    }
+    void drop_if_empty() {
+        if (!dst.empty() && (dst.back().nrows == 0 || dst.back().ncols == 0)) {
+            const AsmDst d = dst.back();
+            elems = d.elem_off;
+            rowref.resize(d.row_off);
+            cmap.resize(d.cmap_off);
+            src.resize(d.src_off);
+            dst.pop_back();
+        }
+    }
+    void clear() {
+        dst.clear();
+        rowref.clear();
+        cmap.clear();
+        src.clear();
+        elems = 0;
+    }
+};
+
+class Engine {
+public:
+    Engine(const Csc& A, const ClusterHierarchy& h, const std::vector<int>& owner, const FactorizeOptions& opt,
+           cudaStream_t st)
+        : A_(A), h_(h), opt_(opt), st_(st), L_(h.num_levels) {
+        out_.M = A.m;
+        out_.N = A.n;
+        out_.eps = opt.eps;
+        out_.pivot_row.assign(A.n, -1);
+        out_.warena = std::make_unique<DeviceArena>(size_t(128) << 20);
+        const size_t nc = h.clusters.size();
+        fr_.resize(nc);
+        cols_.resize(nc);
+        gone_.assign(nc, 0);
+        holders_.resize(nc);
+        pend_id_.assign(nc, -1);
+        stage_list_.resize(L_ + 2);
+        for (size_t c = 0; c < nc; ++c) {
+            const auto& C = h.clusters[c];
+            if (C.level == C.stage && C.stage >= 1 && C.stage <= L_ + 1) stage_list_[C.stage].push_back(static_cast<int>(c));
+        }
+        tree_clusters_.resize(h.tree->nodes.size());
+        for (size_t c = 0; c < nc; ++c) tree_clusters_[h.clusters[c].tree_node].push_back(static_cast<int>(c));
+        CK(cudaEventCreate(&ev0_));
+        CK(cudaEventCreate(&ev1_));
+        init_fronts(owner);
+    }
+    ~Engine() {
+        cudaEventDestroy(ev0_);
+        cudaEventDestroy(ev1_);
+    }
+
+    DeviceFactorization run();
+
+private:
+    const Csc& A_;
+    const ClusterHierarchy& h_;
+    FactorizeOptions opt_;
+    cudaStream_t st_;
+    int L_;
+    std::vector<Front> fr_;
+    std::vector<std::vector<int>> cols_;
+    std::vector<char> gone_;
+    std::vector<std::vector<int>> holders_;
+    std::vector<std::vector<int>> stage_list_, tree_clusters_;
+    DeviceFactorization out_;
+    DeviceArena arena_[2];
+    int cur_ = 0;
+    PinnedArena pin_;
+    Index npiv_ = 0;
+    int batch_ = 0;
+    cudaEvent_t ev0_, ev1_;
+    // eliminate-batch state
+    std::vector<PFront> pend_;
+    std::vector<int> pend_id_, pend_list_;
+    std::vector<Elim> el_;
+    AsmBuilder wcopy_;
+    std::vector<double> pre_sq_, post_sq_;
+    std::vector<unsigned char> pre_nz_, post_nz_;
+    // first error in reference order
+    int err_cluster_ = -1;
+    std::string err_reason_;
+
+    DeviceArena& arena() { return arena_[cur_]; }
+    Uploader up() { return Uploader{&arena(), &pin_, st_}; }
+    int width(int key) const { return static_cast<int>(cols_[key].size()); }
+
+    void sync() {
+        CK(cudaStreamSynchronize(st_));
+        pin_.reset();
+        out_.ctr.syncs++;
+    }
+    template <class T>
+    void download(std::vector<T>& h, const T* d, size_t n) {
+        h.resize(n);
+        if (n == 0) return;
+        T* p = static_cast<T*>(pin_.alloc(sizeof(T) * n));
+        CK(cudaMemcpyAsync(p, d, sizeof(T) * n, cudaMemcpyDeviceToHost, st_));
+        sync();
+        std::memcpy(h.data(), p, sizeof(T) * n);
+        out_.ctr.d2h_bytes += sizeof(T) * n;
+    }
+    void flush_assemble(AsmBuilder& b) {
+        if (b.dst.empty() || b.elems == 0) {
+            b.clear();
+            return;
+        }
+        Uploader u = up();
+        const AsmDst* d = u.put(b.dst);
+        const int4* rr = u.put(b.rowref);
+        const int* cm = u.put(b.cmap);
+        const AsmSrc* s = u.put(b.src);
+        out_.ctr.h2d_bytes += u.bytes_h2d;
+        launch_assemble(d, static_cast<int>(b.dst.size()), b.elems, rr, cm, s, st_);
+        out_.ctr.launches++;
+        b.clear();
+    }
+    void record_error(int cluster, const std::string& why) {
+        if (err_cluster_ < 0) {
+            err_cluster_ = cluster;
+            err_reason_ = why;
+        }
+    }
+    void raise_if_error() {
+        if (err_cluster_ >= 0) throw SingularFrontError(err_cluster_, err_reason_);
+    }
+
+    // column layout: own key first, then ascending keys
+    void layout(int self, std::vector<KeyRef>& keys, int& ncols) const {
+        int o = 0;
+        for (auto& k : keys)
+            if (k.key == self) {
+                k.col = 0;
+                o = k.width;
+            }
+        for (auto& k : keys)
+            if (k.key != self) {
+                k.col = o;
+                o += k.width;
+            }
+        ncols = o;
+    }
+
+    void init_fronts(const std::vector<int>& owner);
+    void eliminate_stage(int k);
+    void elim_pass1(Elim& e);
+    void elim_pass2(Elim& e, int eidx);
+    void materialize_pending();
+    void scale_all();
+    void sparsify_rows_all();
+    void sparsify_cols_all();
+    void merge_level();
+    void snapshot(StageStats& st);
+    int ancestor_target(int c) const;
+
+    PFront& pend(int f) {
+        if (pend_id_[f] < 0) {
+            pend_id_[f] = static_cast<int>(pend_.size());
+            pend_list_.push_back(f);
+            pend_.emplace_back();
+            PFront& P = pend_.back();
+            const Front& F = fr_[f];
+            P.rows.resize(F.rows.size());
+            for (size_t i = 0; i < F.rows.size(); ++i) P.rows[i] = PRow{F.rows[i], f, static_cast<int>(i), -1, 0};
+            P.keys.resize(F.keys.size());
+            for (size_t i = 0; i < F.keys.size(); ++i) P.keys[i] = KW{F.keys[i].key, F.keys[i].width};
+        }
+        return pend_[pend_id_[f]];
+    }
+    // squared norm / nonzero of a symbolic row on one key
+    void rowval(const PRow& r, int key, double& sq, bool& nz, bool post_ok) const;
+    DevWFactor& new_factor(int kind, int c, int k, const std::vector<int>& cols, const std::vector<int>* coupled) {
+        DevWFactor f;
+        f.kind = kind;
+        f.batch = batch_;
+        f.c = c;
+        f.k = k;
+        f.cols_off = static_cast<long long>(out_.idx.size());
+        out_.idx.insert(out_.idx.end(), cols.begin(), cols.end());
+        f.coupled_off = static_cast<long long>(out_.idx.size());
+        if (coupled) out_.idx.insert(out_.idx.end(), coupled->begin(), coupled->end());
+        out_.W.push_back(f);
+        return out_.W.back();
+    }
+};
+
+// factorize.cpp:32-82 — finest fronts, rows ascending into owners, one block
+// per (owner(row), finest(col)) pair seen in A, values scattered on device.
+void Engine::init_fronts(const std::vector<int>& owner) {
+    const int Lf = L_ + 1;
+    for (size_t c = 0; c < h_.clusters.size(); ++c)
+        if (h_.clusters[c].level == Lf) {
+            cols_[c] = h_.clusters[c].cols;
+            fr_[c].live = true;
+        }
+    std::vector<int> local(A_.m);
+    for (Index r = 0; r < A_.m; ++r) {
+        Front& f = fr_[owner[r]];
+        local[r] = f.nrows();
+        f.rows.push_back(r);
+    }
+    std::vector<int> colpos(A_.n);
+    for (size_t c = 0; c < h_.clusters.size(); ++c)
+        if (h_.clusters[c].level == Lf)
+            for (size_t i = 0; i < h_.clusters[c].cols.size(); ++i) colpos[h_.clusters[c].cols[i]] = static_cast<int>(i);
+    // key sets
+    for (Index j = 0; j < A_.n; ++j) {
+        const int q = h_.finest_of_col[j];
+        for (Index k = A_.p[j]; k < A_.p[j + 1]; ++k) {
+            Front& f = fr_[owner[A_.i[k]]];
+            if (f.keys.empty() || f.keys.back().key != q) {  // cheap dedupe; full dedupe below
+                f.keys.push_back(KeyRef{q, width(q), 0});
+            }
+        }
+    }
+    size_t total = 0;
+    for (size_t c = 0; c < fr_.size(); ++c) {
+        Front& f = fr_[c];
+        if (!f.live) continue;
+        std::sort(f.keys.begin(), f.keys.end(), [](const KeyRef& a, const KeyRef& b) { return a.key < b.key; });
+        f.keys.erase(std::unique(f.keys.begin(), f.keys.end(), [](const KeyRef& a, const KeyRef& b) { return a.key == b.key; }),
+                     f.keys.end());
+        layout(static_cast<int>(c), f.keys, f.ncols);
+        for (auto& k : f.keys) sorted_insert(holders_[k.key], static_cast<int>(c));
+        f.ld = std::max(1, f.nrows());
+        total += static_cast<size_t>(f.ld) * f.ncols;
+    }
+    // one zeroed slab for all initial fronts + scatter of A's values
+    double* slab = arena().alloc_n<double>(std::max<size_t>(total, 1));
+    CK(cudaMemsetAsync(slab, 0, sizeof(double) * std::max<size_t>(total, 1), st_));
+    size_t o = 0;
+    for (size_t c = 0; c < fr_.size(); ++c) {
+        Front& f = fr_[c];
+        if (!f.live) continue;
+        f.mat = slab + o;
+        o += static_cast<size_t>(f.ld) * f.ncols;
+    }
+    // scatter: per nnz destination offset (host-computed), values from A
+    std::vector<long long> dsto(A_.nnz());
+    for (Index j = 0; j < A_.n; ++j) {
+        const int q = h_.finest_of_col[j];
+        for (Index k = A_.p[j]; k < A_.p[j + 1]; ++k) {
+            const int r = A_.i[k];
+            const Front& f = fr_[owner[r]];
+            const int qi = f.find(q);
+            dsto[k] = (f.mat - slab) + local[r] + static_cast<long long>(f.keys[qi].col + colpos[j]) * f.ld;
+        }
+    }
+    Uploader u = up();
+    const long long* d_off = u.put(dsto);
+    const double* d_val = u.put(A_.x);
+    out_.ctr.h2d_bytes += u.bytes_h2d;
+    launch_scatter_values(d_off, d_val, A_.nnz(), slab, st_);
+    out_.ctr.launches++;
+}
+
+int Engine::ancestor_target(int c) const {  // factorize.cpp:98-107
+    int node = h_.tree->nodes[h_.clusters[c].tree_node].parent;
+    while (node != -1) {
+        for (int id : tree_clusters_[node])  // ascending ids; live front, not eliminated
+            if (fr_[id].live && !gone_[id]) return id;
+        node = h_.tree->nodes[node].parent;
+    }
+    return -1;
+}
+
+void Engine::rowval(const PRow& r, int key, double& sq, bool& nz, bool post_ok) const {
+    if (r.sidx >= 0) {
+        const Elim& e = el_[r.sidx];
+        auto it = std::lower_bound(e.keys.begin() + 1, e.keys.end(), key);
+        if (it != e.keys.end() && *it == key) {
+            if (!post_ok || e.post_off < 0 || r.srow < e.cs || r.srow >= e.nsel_c)
+                throw std::logic_error("spaqr engine: a row stacked twice within one stage (invariant violated)");
+            const int ki = static_cast<int>(it - e.keys.begin());
+            // post layout per elim: [blockmax all][blockmax key 1..][rows x keys 1..]
+            const long long nk = static_cast<long long>(e.keys.size()) - 1;
+            const long long o = e.post_off + 1 + nk + static_cast<long long>(r.srow - e.cs) * nk + (ki - 1);
+            sq = post_sq_[o];
+            nz = post_nz_[o];
+            return;
+        }
+    }
+    const Front& b = fr_[r.base];
+    const int qi = b.find(key);
+    if (qi < 0) {
+        sq = 0.0;
+        nz = false;
+        return;
+    }
+    const long long o = b.soff[qi] + r.brow;
+    sq = pre_sq_[o];
+    nz = pre_nz_[o];
+}
+
+// factorize.cpp:176-271 (selection, keyset, stack layout) and :286-418's
+// structural half (pivots, scatter bookkeeping) — values come later.
+void Engine::elim_pass1(Elim& e) {
+    const int c = e.c;
+    const int cs = e.cs;
+    e.parts.clear();
+    for (int m : holders_[c])
+        if (m != c) e.parts.push_back(m);
+    if (pend(c).find(c) >= 0) e.parts.insert(e.parts.begin(), c);
+    const double eps = opt_.eps;
+    double tau2 = 0.0;
+    if (eps > 0.0) {
+        double mx = 0.0;
+        for (int m : e.parts)
+            for (const PRow& r : pend(m).rows) {
+                double sq;
+                bool nz;
+                rowval(r, c, sq, nz, false);
+                mx = std::max(mx, sq);
+            }
+        tau2 = mx * eps * eps * 1e-4;
+    }
+    std::vector<std::vector<int>> sel(e.parts.size());
+    int total = 0;
+    auto select = [&](double floor2) {
+        total = 0;
+        for (size_t pi = 0; pi < e.parts.size(); ++pi) {
+            sel[pi].clear();
+            const PFront& P = pend(e.parts[pi]);
+            for (size_t q = 0; q < P.rows.size(); ++q) {
+                double sq;
+                bool nz;
+                rowval(P.rows[q], c, sq, nz, false);
+                if (floor2 > 0.0 ? sq > floor2 : nz) sel[pi].push_back(static_cast<int>(q));
+            }
+            total += static_cast<int>(sel[pi].size());
+        }
+    };
+    select(tau2);
+    if (total < cs && tau2 > 0.0) select(0.0);
+    if (total < cs) {
+        record_error(c, "only " + std::to_string(total) + " rows couple " + std::to_string(cs) + " columns");
+        e.cs = -1;  // marks the failing elimination
+        return;
+    }
+    std::vector<int> keyset;
+    for (size_t pi = 0; pi < e.parts.size(); ++pi) {
+        if (sel[pi].empty()) continue;
+        const PFront& P = pend(e.parts[pi]);
+        for (const KW& kw : P.keys) {
+            const int key = kw.key;
+            if (key == c || width(key) == 0 || std::binary_search(keyset.begin(), keyset.end(), key)) continue;
+            for (int q : sel[pi]) {
+                double sq;
+                bool nz;
+                rowval(P.rows[q], key, sq, nz, false);
+                if (tau2 > 0.0 ? sq > tau2 : nz) {
+                    sorted_insert(keyset, key);
+                    break;
+                }
+            }
+        }
+    }
+    e.keys.assign(1, c);
+    e.keys.insert(e.keys.end(), keyset.begin(), keyset.end());
+    e.off.assign(e.keys.size() + 1, 0);
+    for (size_t i = 0; i < e.keys.size(); ++i) e.off[i + 1] = e.off[i] + width(e.keys[i]);
+    e.tcols = e.off.back();
+    e.total_rows = total;
+    e.srows.clear();
+    for (size_t pi = 0; pi < e.parts.size(); ++pi)
+        for (int q : sel[pi]) e.srows.push_back(pend(e.parts[pi]).rows[q]);
+    e.nsel_c = (!e.parts.empty() && e.parts[0] == c) ? static_cast<int>(sel[0].size()) : 0;
+    for (const PRow& r : e.srows)
+        if (r.sidx >= 0) throw std::logic_error("spaqr engine: row selected by two eliminations of one stage");
+    // :332-344 pivots
+    for (int pos = 0; pos < cs; ++pos) out_.pivot_row[cols_[c][pos]] = e.srows[pos].gid;
+    npiv_ += cs;
+    // :346-418 scatter bookkeeping
+    const int eidx = static_cast<int>(&e - el_.data());
+    int roff = 0;
+    for (size_t pi = 0; pi < e.parts.size(); ++pi) {
+        const int m = e.parts[pi];
+        PFront& P = pend(m);
+        const auto& s = sel[pi];
+        if (s.empty()) {
+            P.erase(c);
+            continue;
+        }
+        if (roff >= cs) {
+            for (size_t i = 0; i < s.size(); ++i) {
+                P.rows[s[i]].sidx = eidx;
+                P.rows[s[i]].srow = roff + static_cast<int>(i);
+            }
+        } else {
+            std::vector<int> spos(P.rows.size(), -1);
+            for (size_t i = 0; i < s.size(); ++i) spos[s[i]] = roff + static_cast<int>(i);
+            std::vector<PRow> nr;
+            nr.reserve(P.rows.size());
+            for (size_t q = 0; q < P.rows.size(); ++q) {
+                if (spos[q] >= 0 && spos[q] < cs) continue;
+                PRow r = P.rows[q];
+                if (spos[q] >= 0) {
+                    r.sidx = eidx;
+                    r.srow = spos[q];
+                }
+                nr.push_back(r);
+            }
+            P.rows.swap(nr);
+        }
+        for (int key : keyset) {
+            P.add(key, width(key));
+            sorted_insert(holders_[key], m);
+        }
+        P.erase(c);
+        fr_[m].scaled_ok = false;
+        roff += static_cast<int>(s.size());
+    }
+    holders_[c].clear();
+}
+
+// :286-323 (W factor with pruned coupling) and :138-174 (move_extras).
+void Engine::elim_pass2(Elim& e, int eidx) {
+    const int c = e.c;
+    const int cs = e.cs;
+    if (cs > 0) {
+        const long long nk = static_cast<long long>(e.keys.size()) - 1;
+        double floor_ = 0.0;
+        if (opt_.eps > 0.0 && e.tcols > cs) floor_ = post_sq_[e.post_off] * opt_.eps * 1e-2;
+        std::vector<int> coupled;
+        std::vector<int> keepk;
+        int kept = 0;
+        for (long long ki = 1; ki <= nk; ++ki) {
+            const double mx = post_sq_[e.post_off + ki];
+            const bool nz = post_nz_[e.post_off + ki];
+            const bool live = floor_ > 0.0 ? mx > floor_ : nz;
+            if (live) {
+                keepk.push_back(static_cast<int>(ki));
+                kept += width(e.keys[ki]);
+                coupled.insert(coupled.end(), cols_[e.keys[ki]].begin(), cols_[e.keys[ki]].end());
+            }
+        }
+        DevWFactor& f = new_factor(0, cs, kept, cols_[c], &coupled);
+        f.a = out_.warena->alloc_n<double>(static_cast<size_t>(cs) * (cs + kept));
+        // copy [R | C_kept] from the stack (rows 0..cs-1)
+        wcopy_.begin(f.a, cs, cs, cs + kept, 1);
+        AsmDst& d = wcopy_.dst.back();
+        wcopy_.src[d.src_off] = AsmSrc{e.S, 1, e.total_rows};
+        for (int i = 0; i < cs; ++i) wcopy_.rowref[d.row_off + i] = int4{-1, 0, 0, i};
+        int o = 0;
+        for (int j = 0; j < cs; ++j) wcopy_.cmap[d.cmap_off + o++] = j;
+        for (int ki : keepk)
+            for (int j = 0; j < width(e.keys[ki]); ++j) wcopy_.cmap[d.cmap_off + o++] = e.off[ki] + j;
+    }
+    // move_extras
+    PFront& fc = pend(c);
+    if (!fc.rows.empty()) {
+        std::vector<int> cand;
+        for (int m : e.parts)
+            if (m != c && !gone_[m] && fr_[m].live && width(m) > 0 && fc.find(m) >= 0) cand.push_back(m);
+        std::map<int, std::vector<int>> dest;
+        for (size_t q = 0; q < fc.rows.size(); ++q) {
+            int best = -1;
+            double bw = -1.0;
+            for (int m : cand) {
+                double sq;
+                bool nz;
+                rowval(fc.rows[q], m, sq, nz, true);
+                if (sq > bw) {
+                    bw = sq;
+                    best = m;
+                }
+            }
+            if (best < 0) best = ancestor_target(c);
+            if (best < 0)
+                out_.trailing_rows.push_back(fc.rows[q].gid);
+            else
+                dest[best].push_back(static_cast<int>(q));
+        }
+        for (auto& [tgt, lr] : dest) {  // append_rows, factorize.cpp:112-133
+            PFront& T = pend(tgt);
+            for (const KW& kw : fc.keys) {
+                if (width(kw.key) == 0 || T.find(kw.key) >= 0) continue;
+                T.add(kw.key, width(kw.key));
+                sorted_insert(holders_[kw.key], tgt);
+            }
+            for (int q : lr) T.rows.push_back(fc.rows[q]);
+            fr_[tgt].scaled_ok = false;
+        }
+    }
+    for (const KW& kw : fc.keys) sorted_erase(holders_[kw.key], c);
+    gone_[c] = 1;
+    fr_[c].live = false;
+    (void)eidx;
+}
+
+// Materialise every pending (touched, still live) front with one gather.
+void Engine::materialize_pending() {
+    AsmBuilder& b = wcopy_;  // W copies already queued; fronts go in the same launch
+    std::vector<std::pair<int, Front>> updates;
+    std::vector<int> slot_of_base(fr_.size(), -1);
+    for (int f : pend_list_) {
+        if (!fr_[f].live) continue;
+        PFront& P = pend_[pend_id_[f]];
+        Front nf;
+        nf.live = true;
+        nf.scaled_ok = fr_[f].scaled_ok;
+        nf.rows.resize(P.rows.size());
+        for (size_t i = 0; i < P.rows.size(); ++i) nf.rows[i] = P.rows[i].gid;
+        nf.keys.resize(P.keys.size());
+        for (size_t i = 0; i < P.keys.size(); ++i) nf.keys[i] = KeyRef{P.keys[i].key, P.keys[i].width, 0};
+        layout(f, nf.keys, nf.ncols);
+        nf.ld = std::max(1, nf.nrows());
+        // unchanged front?  (same rows from itself in order, same keys)
+        bool same = nf.keys.size() == fr_[f].keys.size() && P.rows.size() == fr_[f].rows.size();
+        for (size_t i = 0; same && i < nf.keys.size(); ++i)
+            same = nf.keys[i].key == fr_[f].keys[i].key && nf.keys[i].width == fr_[f].keys[i].width;
+        for (size_t i = 0; same && i < P.rows.size(); ++i)
+            same = P.rows[i].base == f && P.rows[i].brow == static_cast<int>(i) && P.rows[i].sidx < 0;
+        if (same) continue;
+        nf.mat = arena().alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
+        // sources: distinct bases then distinct stacks
+        std::vector<int> bases, stacks;
+        for (const PRow& r : P.rows) {
+            if (slot_of_base[r.base] < 0) {
+                slot_of_base[r.base] = static_cast<int>(bases.size());
+                bases.push_back(r.base);
+            }
+            if (r.sidx >= 0 && std::find(stacks.begin(), stacks.end(), r.sidx) == stacks.end()) stacks.push_back(r.sidx);
+        }
+        const int nsrc = static_cast<int>(bases.size() + stacks.size());
+        const int di = b.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, std::max(nsrc, 1));
+        AsmDst& d = b.dst[di];
+        for (size_t s = 0; s < bases.size(); ++s) {
+            const Front& B = fr_[bases[s]];
+            b.src[d.src_off + s] = AsmSrc{B.mat, 1, B.ld};
+        }
+        for (size_t s = 0; s < stacks.size(); ++s) {
+            const Elim& E = el_[stacks[s]];
+            b.src[d.src_off + bases.size() + s] = AsmSrc{E.S, 1, E.total_rows};
+        }
+        for (size_t i = 0; i < P.rows.size(); ++i) {
+            const PRow& r = P.rows[i];
+            int s1 = -1;
+            if (r.sidx >= 0)
+                s1 = static_cast<int>(bases.size() + (std::find(stacks.begin(), stacks.end(), r.sidx) - stacks.begin()));
+            b.rowref[d.row_off + i] = int4{s1, r.srow, slot_of_base[r.base], r.brow};
+        }
+        for (const KeyRef& k : nf.keys) {
+            for (size_t s = 0; s < bases.size(); ++s) {
+                const Front& B = fr_[bases[s]];
+                const int qi = B.find(k.key);
+                if (qi < 0) continue;
+                for (int o = 0; o < k.width; ++o)
+                    b.cmap[d.cmap_off + static_cast<long long>(k.col + o) * nsrc + s] = B.keys[qi].col + o;
+            }
+            for (size_t s = 0; s < stacks.size(); ++s) {
+                const Elim& E = el_[stacks[s]];
+                auto it = std::lower_bound(E.keys.begin() + 1, E.keys.end(), k.key);
+                if (it == E.keys.end() || *it != k.key) continue;
+                const int ki = static_cast<int>(it - E.keys.begin());
+                for (int o = 0; o < k.width; ++o)
+                    b.cmap[d.cmap_off + static_cast<long long>(k.col + o) * nsrc + bases.size() + s] = E.off[ki] + o;
+            }
+        }
+        b.drop_if_empty();
+        for (int bb : bases) slot_of_base[bb] = -1;
+        updates.emplace_back(f, std::move(nf));
+    }
+    flush_assemble(b);
+    for (auto& [f, nf] : updates) {
+        nf.soff.clear();
+        fr_[f] = std::move(nf);
+    }
+    for (int f : pend_list_) pend_id_[f] = -1;
+    pend_list_.clear();
+    pend_.clear();
+}
+
+void Engine::eliminate_stage(int k) {
+    const auto& list = stage_list_[k];
+    if (list.empty()) return;
+    el_.clear();
+    el_.reserve(list.size());
+    // fronts whose pre-stage statistics are needed: all participants + own fronts
+    std::vector<int> P;
+    std::vector<char> inP(fr_.size(), 0);
+    auto addP = [&](int f) {
+        if (!inP[f] && fr_[f].live) {
+            inP[f] = 1;
+            P.push_back(f);
+        }
+    };
+    for (int c : list) {
+        addP(c);
+        if (width(c) > 0)
+            for (int m : holders_[c]) addP(m);
+    }
+    std::vector<StatDesc> sd;
+    long long work = 0;
+    for (int f : P) {
+        Front& F = fr_[f];
+        F.soff.assign(F.keys.size(), -1);
+        for (size_t qi = 0; qi < F.keys.size(); ++qi) {
+            if (F.nrows() == 0) {
+                F.soff[qi] = work;
+                continue;
+            }
+            StatDesc s{F.mat, F.ld, 0, F.nrows(), F.keys[qi].col, F.keys[qi].width, 0, work, work};
+            F.soff[qi] = work;
+            sd.push_back(s);
+            work += F.nrows();
+        }
+    }
+    double* d_sq = arena().alloc_n<double>(std::max<long long>(work, 1));
+    unsigned char* d_nz = arena().alloc_n<unsigned char>(std::max<long long>(work, 1));
+    if (!sd.empty()) {
+        Uploader u = up();
+        const StatDesc* dd = u.put(sd);
+        out_.ctr.h2d_bytes += u.bytes_h2d;
+        launch_stats(dd, static_cast<int>(sd.size()), work, d_sq, d_nz, st_);
+        out_.ctr.launches++;
+    }
+    download(pre_sq_, d_sq, work);
+    download(pre_nz_, d_nz, work);
+    // pass 1 over the whole batch (ascending ids)
+    int nvalid = 0;
+    for (int c : list) {
+        el_.emplace_back();
+        Elim& e = el_.back();
+        e.c = c;
+        e.cs = width(c);
+        if (e.cs > 0) elim_pass1(e);
+        if (e.cs < 0) break;  // "rows couple" error: later eliminations never run
+        ++nvalid;
+    }
+    // gather stacks, QR + apply, post statistics
+    AsmBuilder sb;
+    std::vector<QrDesc> qd;
+    std::vector<StatDesc> pd;
+    long long pwork = 0, postlen = 0;
+    std::vector<int> flags_init;
+    for (int ei = 0; ei < nvalid; ++ei) {
+        Elim& e = el_[ei];
+        if (e.cs <= 0) continue;
+        e.S = arena().alloc_n<double>(static_cast<size_t>(e.total_rows) * e.tcols);
+        std::vector<int> bases;
+        std::vector<int> slot(0);
+        for (const PRow& r : e.srows)
+            if (std::find(bases.begin(), bases.end(), r.base) == bases.end()) bases.push_back(r.base);
+        const int nsrc = static_cast<int>(bases.size());
+        const int di = sb.begin(e.S, e.total_rows, e.total_rows, e.tcols, nsrc);
+        AsmDst& d = sb.dst[di];
+        for (int s = 0; s < nsrc; ++s) sb.src[d.src_off + s] = AsmSrc{fr_[bases[s]].mat, 1, fr_[bases[s]].ld};
+        for (int i = 0; i < e.total_rows; ++i) {
+            const PRow& r = e.srows[i];
+            const int s = static_cast<int>(std::find(bases.begin(), bases.end(), r.base) - bases.begin());
+            sb.rowref[d.row_off + i] = int4{-1, 0, s, r.brow};
+        }
+        for (size_t ki = 0; ki < e.keys.size(); ++ki)
+            for (int s = 0; s < nsrc; ++s) {
+                const Front& B = fr_[bases[s]];
+                const int qi = B.find(e.keys[ki]);
+                if (qi < 0) continue;
+                for (int o = 0; o < width(e.keys[ki]); ++o)
+                    sb.cmap[d.cmap_off + static_cast<long long>(e.off[ki] + o) * nsrc + s] = B.keys[qi].col + o;
+            }
+        flags_init.push_back(INT_MAX);
+        QrDesc q{e.S, e.total_rows, e.total_rows, e.cs, e.tcols, nullptr, nullptr, nullptr, nullptr, 0};
+        qd.push_back(q);
+        out_.ctr.qr_flops += 2.0 * e.total_rows * double(e.cs) * e.cs - 2.0 / 3.0 * double(e.cs) * e.cs * e.cs +
+                             (4.0 * e.total_rows * e.cs - 2.0 * e.cs * double(e.cs)) * (e.tcols - e.cs);
+        out_.ctr.qr_bytes += 16.0 * e.total_rows * e.tcols;
+        // post stats: [max over all neighbour cols][max per key][own non-pivot rows x keys]
+        const long long nk = static_cast<long long>(e.keys.size()) - 1;
+        e.post_off = postlen;
+        if (e.tcols > e.cs) {
+            pd.push_back(StatDesc{e.S, e.total_rows, 0, e.cs, e.cs, e.tcols - e.cs, 1, postlen, pwork});
+            pwork += 1;
+        }
+        postlen += 1;
+        for (long long ki = 1; ki <= nk; ++ki) {
+            pd.push_back(StatDesc{e.S, e.total_rows, 0, e.cs, e.off[ki], width(e.keys[ki]), 1, postlen, pwork});
+            pwork += 1;
+            postlen += 1;
+        }
+        const int nown = std::max(0, e.nsel_c - e.cs);
+        for (int r = 0; r < nown; ++r)
+            for (long long ki = 1; ki <= nk; ++ki) {
+                pd.push_back(StatDesc{e.S, e.total_rows, e.cs + r, 1, e.off[ki], width(e.keys[ki]), 0, postlen, pwork});
+                pwork += 1;
+                postlen += 1;
+            }
+    }
+    wcopy_.clear();
+    double *d_psq = nullptr;
+    unsigned char* d_pnz = nullptr;
+    if (!qd.empty()) {
+        flush_assemble(sb);
+        Uploader u = up();
+        int* d_flags = u.put(flags_init);
+        for (size_t i = 0, qi = 0; i < static_cast<size_t>(nvalid); ++i)
+            if (el_[i].cs > 0) {
+                el_[i].flag = d_flags + qi;
+                qd[qi].flag = d_flags + qi;
+                ++qi;
+            }
+        const QrDesc* dq = u.put(qd);
+        d_psq = arena().alloc_n<double>(std::max<long long>(postlen, 1));
+        d_pnz = arena().alloc_n<unsigned char>(std::max<long long>(postlen, 1));
+        const StatDesc* dp = u.put(pd);
+        out_.ctr.h2d_bytes += u.bytes_h2d;
+        int maxm = 0;
+        for (auto& q : qd) maxm = std::max(maxm, q.m);
+        CK(cudaEventRecord(ev0_, st_));
+        launch_qr(dq, static_cast<int>(qd.size()), maxm, st_);
+        CK(cudaEventRecord(ev1_, st_));
+        out_.ctr.launches++;
+        out_.ctr.qr_launches++;
+        launch_stats(dp, static_cast<int>(pd.size()), pwork, d_psq, d_pnz, st_);
+        out_.ctr.launches++;
+        std::vector<int> flags;
+        download(flags, d_flags, flags_init.size());
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+        out_.ctr.t_qr_ms += ms;
+        download(post_sq_, d_psq, postlen);
+        download(post_nz_, d_pnz, postlen);
+        // first error in ascending order (singular pivot precedes a later "rows couple")
+        for (size_t i = 0, qi = 0; i < static_cast<size_t>(nvalid); ++i)
+            if (el_[i].cs > 0) {
+                if (flags[qi] != INT_MAX) {
+                    err_cluster_ = -1;
+                    record_error(el_[i].c, "pivot " + std::to_string(flags[qi]) + " is zero or denormal");
+                    break;
+                }
+                ++qi;
+            }
+    }
+    raise_if_error();
+    for (int ei = 0; ei < nvalid; ++ei) elim_pass2(el_[ei], ei);
+    materialize_pending();
+}
+
+// factorize.cpp:425-486
+void Engine::scale_all() {
+    std::vector<int> cand;
+    std::vector<StatDesc> sd;
+    for (size_t p = 0; p < fr_.size(); ++p) {
+        Front& f = fr_[p];
+        if (!f.live) continue;
+        f.scaled_ok = false;
+        const int cs = width(static_cast<int>(p));
+        if (cs == 0) continue;
+        const int r = f.nrows();
+        if (r < cs) continue;
+        const int qi = f.find(static_cast<int>(p));
+        if (qi < 0) {  // a zero diagonal block: QR of zeros fails at pivot 0
+            record_error(static_cast<int>(p), "pivot 0 is zero or denormal");
+            continue;
+        }
+        sd.push_back(StatDesc{f.mat, f.ld, 0, r, f.keys[qi].col, cs, 2, static_cast<long long>(cand.size()),
+                              static_cast<long long>(cand.size())});
+        cand.push_back(static_cast<int>(p));
+    }
+    if (cand.empty()) {
+        raise_if_error();
+        return;
+    }
+    double* d_sq = arena().alloc_n<double>(cand.size());
+    unsigned char* d_nz = arena().alloc_n<unsigned char>(cand.size());
+    {
+        Uploader u = up();
+        const StatDesc* dd = u.put(sd);
+        out_.ctr.h2d_bytes += u.bytes_h2d;
+        launch_stats(dd, static_cast<int>(sd.size()), static_cast<long long>(sd.size()), d_sq, d_nz, st_);
+        out_.ctr.launches++;
+    }
+    std::vector<unsigned char> ident;
+    download(ident, d_nz, cand.size());
+    std::vector<QrDesc> qd;
+    std::vector<TrsmDesc> td;
+    std::vector<int> qp;
+    long long trows = 0;
+    for (size_t i = 0; i < cand.size(); ++i) {
+        const int p = cand[i];
+        Front& f = fr_[p];
+        if (ident[i]) {
+            f.scaled_ok = true;
+            continue;
+        }
+        const int cs = width(p);
+        DevWFactor& w = new_factor(0, cs, 0, cols_[p], nullptr);
+        w.a = out_.warena->alloc_n<double>(static_cast<size_t>(cs) * cs);
+        qd.push_back(QrDesc{f.mat, f.ld, f.nrows(), cs, f.ncols, nullptr, nullptr, w.a, nullptr, 1});
+        qp.push_back(p);
+        out_.ctr.qr_flops += 2.0 * f.nrows() * double(cs) * cs - 2.0 / 3.0 * double(cs) * cs * cs +
+                             (4.0 * f.nrows() * cs - 2.0 * cs * double(cs)) * (f.ncols - cs);
+        out_.ctr.qr_bytes += 16.0 * f.nrows() * f.ncols;
+        for (int m : holders_[p]) {
+            if (m == p) continue;
+            const Front& fm = fr_[m];
+            const int mq = fm.find(p);
+            if (fm.nrows() == 0) continue;
+            td.push_back(TrsmDesc{fm.mat + static_cast<long long>(fm.keys[mq].col) * fm.ld, fm.ld, fm.nrows(), cs, w.a, cs, trows});
+            trows += fm.nrows();
+        }
+        f.scaled_ok = true;
+    }
+    if (!qd.empty()) {
+        std::vector<int> flags_init(qd.size(), INT_MAX);
+        Uploader u = up();
+        int* d_flags = u.put(flags_init);
+        for (size_t i = 0; i < qd.size(); ++i) qd[i].flag = d_flags + i;
+        const QrDesc* dq = u.put(qd);
+        const TrsmDesc* dt = u.put(td);
+        out_.ctr.h2d_bytes += u.bytes_h2d;
+        int maxm = 0;
+        for (auto& q : qd) maxm = std::max(maxm, q.m);
+        CK(cudaEventRecord(ev0_, st_));
+        launch_qr(dq, static_cast<int>(qd.size()), maxm, st_);
+        CK(cudaEventRecord(ev1_, st_));
+        out_.ctr.launches++;
+        out_.ctr.qr_launches++;
+        launch_trsm(dt, static_cast<int>(td.size()), trows, st_);
+        out_.ctr.launches++;
+        std::vector<int> flags;
+        download(flags, d_flags, flags_init.size());
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev0_, ev1_));
+        out_.ctr.t_qr_ms += ms;
+        for (size_t i = 0; i < flags.size(); ++i)
+            if (flags[i] != INT_MAX) {
+                if (err_cluster_ < 0 || qp[i] < err_cluster_) {
+                    err_cluster_ = qp[i];
+                    err_reason_ = "pivot " + std::to_string(flags[i]) + " is zero or denormal";
+                }
+                break;
+            }
+    }
+    raise_if_error();
+}
+
+// factorize.cpp:488-537 — CPQR of every front's extra rows against its neighbours.
+void Engine::sparsify_rows_all() {
+    struct Job {
+        int p, cs, p2, nw, c0;
+        double* B;
+    };
+    std::vector<Job> jobs;
+    AsmBuilder gb;
+    std::vector<CpqrDesc> cd;
+    int maxm = 0;
+    for (size_t pp = 0; pp < fr_.size(); ++pp) {
+        const int p = static_cast<int>(pp);
+        Front& f = fr_[p];
+        if (!f.live) continue;
+        const int cs = width(p);
+        if (cs > 0 && !f.scaled_ok) continue;
+        const int r = f.nrows();
+        const int p2 = r - cs;
+        if (p2 <= 0) continue;
+        const int qi = f.find(p);
+        const int c0 = (qi >= 0) ? f.keys[qi].width : 0;
+        const int nw = f.ncols - c0;
+        if (nw == 0) {  // keep = 0: every extra row is dropped
+            for (int i = cs; i < r; ++i) out_.dropped_rows.push_back(f.rows[i]);
+            f.rows.resize(cs);
+            continue;
+        }
+        Job j{p, cs, p2, nw, c0, arena().alloc_n<double>(static_cast<size_t>(p2) * nw)};
+        const int di = gb.begin(j.B, p2, p2, nw, 1);
+        AsmDst& d = gb.dst[di];
+        gb.src[d.src_off] = AsmSrc{f.mat + cs + static_cast<long long>(c0) * f.ld, 1, f.ld};
+        for (int i = 0; i < p2; ++i) gb.rowref[d.row_off + i] = int4{-1, 0, 0, i};
+        for (int c = 0; c < nw; ++c) gb.cmap[d.cmap_off + c] = c;
+        jobs.push_back(j);
+        maxm = std::max(maxm, p2);
+        out_.ctr.cpqr_bytes += 8.0 * p2 * nw;
+    }
+    if (jobs.empty()) return;
+    flush_assemble(gb);
+    const size_t nj = jobs.size();
+    int* d_rank = arena().alloc_n<int>(nj);
+    double* d_r11 = arena().alloc_n<double>(nj);
+    for (size_t i = 0; i < nj; ++i) {
+        const Job& j = jobs[i];
+        double* work = arena().alloc_n<double>(3 * static_cast<size_t>(j.nw));
+        cd.push_back(CpqrDesc{j.B, j.p2, j.p2, j.nw, opt_.eps, d_rank + i, d_r11 + i, nullptr, 0, nullptr, nullptr,
+                              nullptr, work});
+    }
+    {
+        Uploader u = up();
+        const CpqrDesc* dc = u.put(cd);
+        out_.ctr.h2d_bytes += u.bytes_h2d;
+        launch_cpqr(dc, static_cast<int>(cd.size()), maxm, st_);
+        out_.ctr.launches++;
+    }
+    std::vector<int> rank;
+    download(rank, d_rank, nj);
+    AsmBuilder wb;
+    for (size_t i = 0; i < nj; ++i) {
+        const Job& j = jobs[i];
+        const int keep = rank[i];
+        out_.ctr.cpqr_flops += 4.0 * j.p2 * double(j.nw) * keep + 2.0 * j.p2 * j.nw;
+        if (keep >= j.p2) continue;
+        Front& f = fr_[j.p];
+        for (int r = j.cs + keep; r < j.cs + j.p2; ++r) out_.dropped_rows.push_back(f.rows[r]);
+        f.rows.resize(j.cs + keep);
+        if (keep == 0) continue;
+        const int di = wb.begin(f.mat + j.cs + static_cast<long long>(j.c0) * f.ld, f.ld, keep, j.nw, 1);
+        AsmDst& d = wb.dst[di];
+        wb.src[d.src_off] = AsmSrc{j.B, 1, j.p2};
+        for (int r = 0; r < keep; ++r) wb.rowref[d.row_off + r] = int4{-1, 0, 0, r};
+        for (int c = 0; c < j.nw; ++c) wb.cmap[d.cmap_off + c] = c;
+    }
+    flush_assemble(wb);
+}
+
+// factorize.cpp:539-633 — Gauss-Seidel over interfaces, run as waves of a
+// DAG whose edges join fronts that hold each other's key (the only way one
+// interface's step reads what another writes).
+void Engine::sparsify_cols_all() {
+    std::vector<int> elig;
+    for (size_t p = 0; p < fr_.size(); ++p)
+        if (fr_[p].live && width(static_cast<int>(p)) > 0 && fr_[p].scaled_ok) elig.push_back(static_cast<int>(p));
+    if (elig.empty()) return;
+    std::vector<int> level(fr_.size(), -1);
+    int nwaves = 0;
+    for (int p : elig) {
+        int lv = 0;
+        for (int m : holders_[p])
+            if (m < p && level[m] >= 0) lv = std::max(lv, level[m] + 1);
+        for (const KeyRef& k : fr_[p].keys)
+            if (k.key < p && level[k.key] >= 0) lv = std::max(lv, level[k.key] + 1);
+        level[p] = lv;
+        nwaves = std::max(nwaves, lv + 1);
+    }
+    std::vector<std::vector<int>> waves(nwaves);
+    for (int p : elig) waves[level[p]].push_back(p);
+    const int rot_batch = batch_;
+    for (auto& wave : waves) {
+        struct Job {
+            int p, cs, nG, wrows, kmax;
+            std::vector<int> rparts, seg;  // seg offsets of holders in G
+            double* G;
+            double *V, *tau, *sign;
+        };
+        std::vector<Job> jobs;
+        AsmBuilder gb;
+        std::vector<CpqrDesc> cd;
+        int maxm = 0;
+        for (int p : wave) {
+            Front& f = fr_[p];
+            Job j;
+            j.p = p;
+            j.cs = width(p);
+            for (int m : holders_[p])
+                if (m != p && fr_[m].live) j.rparts.push_back(m);
+            int wrows = 0;
+            for (int m : j.rparts) {
+                j.seg.push_back(wrows);
+                wrows += fr_[m].nrows();
+            }
+            const int qi = f.find(p);
+            const int c0 = (qi >= 0) ? f.keys[qi].width : 0;
+            const int wcols = f.ncols - c0;
+            j.wrows = wrows;
+            j.nG = wrows + wcols;
+            j.kmax = std::min(j.cs, j.nG);
+            j.G = arena().alloc_n<double>(static_cast<size_t>(j.cs) * std::max(j.nG, 1));
+            // G (cs x nG) built transposed: G column g <- a row of holder m or a column of own block
+            const int nsrc = static_cast<int>(j.rparts.size()) + 1;
+            if (j.nG > 0) {
+                // logical G^T (nG x cs) gathered row by row, stored transposed as G (ld = cs)
+                const int di = gb.begin(j.G, j.cs, j.nG, j.cs, nsrc);
+                AsmDst& d = gb.dst[di];
+                d.trans = 1;
+                for (size_t s = 0; s < j.rparts.size(); ++s) {
+                    const Front& fm = fr_[j.rparts[s]];
+                    const int mq = fm.find(p);
+                    gb.src[d.src_off + s] = AsmSrc{fm.mat + static_cast<long long>(fm.keys[mq].col) * fm.ld, 1, fm.ld};
+                    for (int q = 0; q < fm.nrows(); ++q) gb.rowref[d.row_off + j.seg[s] + q] = int4{-1, 0, static_cast<int>(s), q};
+                    for (int i = 0; i < j.cs; ++i) gb.cmap[d.cmap_off + static_cast<long long>(i) * nsrc + s] = i;
+                }
+                const int so = static_cast<int>(j.rparts.size());
+                gb.src[d.src_off + so] = AsmSrc{f.mat, f.ld, 1};  // transposed view of p's own rows
+                for (int g = 0; g < wcols; ++g) gb.rowref[d.row_off + wrows + g] = int4{-1, 0, so, c0 + g};
+                for (int i = 0; i < j.cs; ++i) gb.cmap[d.cmap_off + static_cast<long long>(i) * nsrc + so] = i;
+            }
+            j.V = out_.warena->alloc_n<double>(static_cast<size_t>(j.cs) * std::max(j.kmax, 1));
+            j.tau = out_.warena->alloc_n<double>(std::max(j.kmax, 1));
+            j.sign = out_.warena->alloc_n<double>(std::max(j.kmax, 1));
+            maxm = std::max(maxm, j.cs);
+            out_.ctr.cpqr_bytes += 8.0 * j.cs * j.nG;
+            jobs.push_back(std::move(j));
+        }
+        flush_assemble(gb);
+        const size_t nj = jobs.size();
+        int* d_rank = arena().alloc_n<int>(nj);
+        double* d_r11 = arena().alloc_n<double>(nj);
+        for (size_t i = 0; i < nj; ++i) {
+            Job& j = jobs[i];
+            double* work = arena().alloc_n<double>(3 * static_cast<size_t>(std::max(j.nG, 1)));
+            cd.push_back(CpqrDesc{j.G, j.cs, j.cs, j.nG, opt_.eps, d_rank + i, d_r11 + i, j.V, j.cs, j.tau, j.sign,
+                                  nullptr, work});
+        }
+        {
+            Uploader u = up();
+            const CpqrDesc* dc = u.put(cd);
+            out_.ctr.h2d_bytes += u.bytes_h2d;
+            launch_cpqr(dc, static_cast<int>(cd.size()), maxm, st_);
+            out_.ctr.launches++;
+        }
+        std::vector<int> rank;
+        download(rank, d_rank, nj);
+        // apply structural updates in ascending p, then materialise
+        struct HolderEdit {
+            int m;
+            std::vector<std::pair<int, int>> gsrc;  // (job index, segment) per processed key p
+        };
+        std::map<int, std::vector<std::pair<int, int>>> hed;  // holder m -> (job, holder slot)
+        std::vector<int> changed_p;
+        for (size_t i = 0; i < nj; ++i) {
+            Job& j = jobs[i];
+            const int r2 = rank[i];
+            out_.ctr.cpqr_flops += 4.0 * j.cs * double(j.nG) * r2 + 2.0 * j.cs * j.nG;
+            if (r2 >= j.cs) continue;
+            const int p = j.p;
+            Front& f = fr_[p];
+            if (r2 > 0) {
+                batch_ = rot_batch;
+                DevWFactor& w = new_factor(1, j.cs, r2, cols_[p], nullptr);
+                w.a = j.V;
+                w.tau = j.tau;
+                w.sign = j.sign;
+            }
+            for (size_t s = 0; s < j.rparts.size(); ++s) {
+                const int m = j.rparts[s];
+                if (r2 > 0)
+                    hed[m].emplace_back(static_cast<int>(i), static_cast<int>(s));
+                else {
+                    hed[m].emplace_back(static_cast<int>(i), -1 - static_cast<int>(s));  // drop key p
+                    sorted_erase(holders_[p], m);
+                }
+            }
+            for (int q = r2; q < j.cs; ++q) {
+                out_.pivot_row[cols_[p][q]] = f.rows[q];
+                ++npiv_;
+            }
+            changed_p.push_back(static_cast<int>(i));
+        }
+        // materialise p fronts and their holders
+        AsmBuilder mb;
+        std::vector<std::pair<int, Front>> updates;
+        for (int ji : changed_p) {
+            Job& j = jobs[ji];
+            const int p = j.p, cs = j.cs, r2 = rank[ji];
+            const Front& f = fr_[p];
+            const int p2 = f.nrows() - cs;
+            Front nf;
+            nf.live = true;
+            nf.rows.assign(f.rows.begin(), f.rows.begin() + r2);
+            nf.rows.insert(nf.rows.end(), f.rows.begin() + cs, f.rows.end());
+            for (const KeyRef& k : f.keys) {
+                if (k.key == p) {
+                    if (r2 > 0) nf.keys.push_back(KeyRef{p, r2, 0});
+                } else {
+                    nf.keys.push_back(KeyRef{k.key, k.width, 0});
+                }
+            }
+            nf.scaled_ok = r2 > 0;
+            layout(p, nf.keys, nf.ncols);
+            nf.ld = std::max(1, nf.nrows());
+            nf.mat = arena().alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
+            const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, 2);
+            AsmDst& d = mb.dst[di];
+            mb.src[d.src_off + 0] = AsmSrc{j.G, 1, cs};      // R rows (top r2)
+            mb.src[d.src_off + 1] = AsmSrc{f.mat, 1, f.ld};  // old extra rows
+            for (int q = 0; q < r2; ++q) mb.rowref[d.row_off + q] = int4{0, q, -1, 0};
+            for (int q = 0; q < p2; ++q) mb.rowref[d.row_off + r2 + q] = int4{1, cs + q, -1, 0};
+            const int qi = f.find(p);
+            const int c0 = (qi >= 0) ? f.keys[qi].width : 0;
+            for (const KeyRef& k : nf.keys) {
+                if (k.key == p) {
+                    for (int o = 0; o < k.width; ++o) {
+                        mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * 2 + 0] = -2 - o;
+                        mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * 2 + 1] = -2 - o;
+                    }
+                    continue;
+                }
+                const KeyRef& ok = f.keys[f.find(k.key)];
+                for (int o = 0; o < k.width; ++o) {
+                    mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * 2 + 0] = j.wrows + (ok.col - c0) + o;
+                    mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * 2 + 1] = ok.col + o;
+                }
+            }
+            mb.drop_if_empty();
+            cols_[p].resize(r2);
+            if (r2 == 0) holders_[p].clear();
+            updates.emplace_back(p, std::move(nf));
+        }
+        for (auto& [m, edits] : hed) {
+            const Front& f = fr_[m];
+            Front nf;
+            nf.live = true;
+            nf.rows = f.rows;
+            nf.scaled_ok = f.scaled_ok;
+            std::vector<int> gslot_key;  // key p per G slot
+            for (const KeyRef& k : f.keys) {
+                int w = k.width;
+                bool dropped = false;
+                for (auto& [ji, s] : edits)
+                    if (jobs[ji].p == k.key) {
+                        if (s < 0) dropped = true;
+                        w = rank[ji];
+                    }
+                if (!dropped) nf.keys.push_back(KeyRef{k.key, w, 0});
+            }
+            layout(m, nf.keys, nf.ncols);
+            nf.ld = std::max(1, nf.nrows());
+            nf.mat = arena().alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
+            std::vector<std::pair<int, int>> live_edits;
+            for (auto& e : edits)
+                if (e.second >= 0) live_edits.push_back(e);
+            const int nsrc = static_cast<int>(live_edits.size()) + 1;
+            const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, nsrc);
+            AsmDst& d = mb.dst[di];
+            for (size_t s = 0; s < live_edits.size(); ++s) {
+                const Job& j = jobs[live_edits[s].first];
+                // B_m(q, i) = R(i, seg + q) = G[i + (seg+q)*cs]
+                mb.src[d.src_off + s] = AsmSrc{j.G + static_cast<long long>(j.seg[live_edits[s].second]) * j.cs, j.cs, 1};
+            }
+            mb.src[d.src_off + live_edits.size()] = AsmSrc{f.mat, 1, f.ld};
+            for (int q = 0; q < nf.nrows(); ++q) mb.rowref[d.row_off + q] = int4{-2, q, -1, 0};
+            for (const KeyRef& k : nf.keys) {
+                int gs = -1;
+                for (size_t s = 0; s < live_edits.size(); ++s)
+                    if (jobs[live_edits[s].first].p == k.key) gs = static_cast<int>(s);
+                if (gs >= 0) {
+                    for (int o = 0; o < k.width; ++o) mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * nsrc + gs] = o;
+                } else {
+                    const KeyRef& ok = f.keys[f.find(k.key)];
+                    for (int o = 0; o < k.width; ++o)
+                        mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * nsrc + live_edits.size()] = ok.col + o;
+                }
+            }
+            mb.drop_if_empty();
+            updates.emplace_back(m, std::move(nf));
+        }
+        flush_assemble(mb);
+        for (auto& [f, nf] : updates) fr_[f] = std::move(nf);
+    }
+}
+
+// factorize.cpp:635-729 — children concatenate into parents; every live front
+// is rebuilt into the other arena (pivot rows of all children first).
+void Engine::merge_level() {
+    std::map<int, std::vector<int>> groups;
+    for (size_t c = 0; c < fr_.size(); ++c)
+        if (fr_[c].live) groups[h_.clusters[c].parent].push_back(static_cast<int>(c));
+    for (auto& [P, kids] : groups) {
+        if (P < 0) throw std::logic_error("spaqr engine: live front without a parent cluster at merge");
+        cols_[P].clear();
+        for (int c : kids) cols_[P].insert(cols_[P].end(), cols_[c].begin(), cols_[c].end());
+    }
+    std::vector<int> child_off(fr_.size(), -1);
+    for (auto& [P, kids] : groups) {
+        int o = 0;
+        for (int c : kids) {
+            child_off[c] = o;
+            o += width(c);
+        }
+    }
+    DeviceArena& next = arena_[cur_ ^ 1];
+    AsmBuilder mb;
+    std::vector<Front> nfs;
+    std::vector<int> nids;
+    for (auto& [P, kids] : groups) {
+        Front nf;
+        nf.live = true;
+        bool movable = false;
+        if (kids.size() == 1) {
+            movable = true;
+            for (const KeyRef& k : fr_[kids[0]].keys)
+                if (width(k.key) != 0 && width(h_.clusters[k.key].parent) != width(k.key)) {
+                    movable = false;
+                    break;
+                }
+        }
+        nf.scaled_ok = movable ? fr_[kids[0]].scaled_ok : false;
+        std::vector<std::pair<int, int>> rowsrc;  // (kid slot, row)
+        for (size_t s = 0; s < kids.size(); ++s) {
+            const Front& fc = fr_[kids[s]];
+            const int take = std::min(width(kids[s]), fc.nrows());
+            for (int i = 0; i < take; ++i) {
+                nf.rows.push_back(fc.rows[i]);
+                rowsrc.emplace_back(static_cast<int>(s), i);
+            }
+        }
+        for (size_t s = 0; s < kids.size(); ++s) {
+            const Front& fc = fr_[kids[s]];
+            const int take = std::min(width(kids[s]), fc.nrows());
+            for (int i = take; i < fc.nrows(); ++i) {
+                nf.rows.push_back(fc.rows[i]);
+                rowsrc.emplace_back(static_cast<int>(s), i);
+            }
+        }
+        std::vector<int> pk;
+        for (int c : kids)
+            for (const KeyRef& k : fr_[c].keys)
+                if (width(k.key) != 0) pk.push_back(h_.clusters[k.key].parent);
+        std::sort(pk.begin(), pk.end());
+        pk.erase(std::unique(pk.begin(), pk.end()), pk.end());
+        for (int K : pk) nf.keys.push_back(KeyRef{K, width(K), 0});
+        layout(P, nf.keys, nf.ncols);
+        nf.ld = std::max(1, nf.nrows());
+        nf.mat = next.alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
+        const int nsrc = static_cast<int>(kids.size());
+        const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, nsrc);
+        AsmDst& d = mb.dst[di];
+        for (int s = 0; s < nsrc; ++s) mb.src[d.src_off + s] = AsmSrc{fr_[kids[s]].mat, 1, fr_[kids[s]].ld};
+        for (size_t i = 0; i < rowsrc.size(); ++i) mb.rowref[d.row_off + i] = int4{-1, 0, rowsrc[i].first, rowsrc[i].second};
+        for (int s = 0; s < nsrc; ++s) {
+            for (const KeyRef& k : fr_[kids[s]].keys) {
+                if (width(k.key) == 0) continue;
+                const int K = h_.clusters[k.key].parent;
+                const KeyRef& dk = nf.keys[nf.find(K)];
+                const int co = child_off[k.key];
+                if (co < 0) throw std::logic_error("spaqr engine: key without a live front at merge");
+                for (int o = 0; o < k.width; ++o)
+                    mb.cmap[d.cmap_off + static_cast<long long>(dk.col + co + o) * nsrc + s] = k.col + o;
+            }
+        }
+        mb.drop_if_empty();
+        nfs.push_back(std::move(nf));
+        nids.push_back(P);
+    }
+    flush_assemble(mb);
+    for (size_t c = 0; c < fr_.size(); ++c) fr_[c] = Front();
+    for (auto& hs : holders_) hs.clear();
+    for (size_t i = 0; i < nfs.size(); ++i) {
+        const int P = nids[i];
+        fr_[P] = std::move(nfs[i]);
+        for (const KeyRef& k : fr_[P].keys) sorted_insert(holders_[k.key], P);
+    }
+    // everything of this stage lived in arena cur_; the next stage starts clean
+    CK(cudaStreamSynchronize(st_));
+    pin_.reset();
+    arena_[cur_].reset();
+    cur_ ^= 1;
+}
+
+void Engine::snapshot(StageStats& st) {  // factorize.cpp:731-743
+    for (size_t c = 0; c < fr_.size(); ++c) {
+        const Front& f = fr_[c];
+        if (!f.live) continue;
+        const int cs = width(static_cast<int>(c));
+        if (cs > 0) {
+            st.front_cols.push_back(cs);
+            st.front_aspect.push_back(static_cast<double>(f.nrows()) / cs);
+        }
+        if (h_.clusters[c].tree_node == h_.tree->root) {
+            st.top_rows += f.nrows();
+            st.top_cols += cs;
+        }
+    }
+}
+
+DeviceFactorization Engine::run() {  // factorize.cpp:745-790
+    for (int k = L_ + 1; k >= 1; --k) {
+        StageStats st;
+        st.stage = k;
+        double t0 = now_s();
+        batch_ = out_.nbatches++;
+        eliminate_stage(k);
+        st.t_eliminate = now_s() - t0;
+        if (opt_.eps > 0.0 && k >= 2 && L_ + 1 - k >= opt_.skip_levels) {
+            t0 = now_s();
+            batch_ = out_.nbatches++;
+            scale_all();
+            st.t_scale = now_s() - t0;
+            t0 = now_s();
+            sparsify_rows_all();
+            batch_ = out_.nbatches++;
+            sparsify_cols_all();
+            st.t_sparsify = now_s() - t0;
+        }
+        snapshot(st);
+        if (k >= 2) {
+            t0 = now_s();
+            merge_level();
+            st.t_merge = now_s() - t0;
+        }
+        st.nnz_w = out_.nnz_w();
+        out_.stages.push_back(st);
+    }
+    for (size_t c = 0; c < fr_.size(); ++c)
+        if (fr_[c].live) out_.trailing_rows.insert(out_.trailing_rows.end(), fr_[c].rows.begin(), fr_[c].rows.end());
+    CK(cudaStreamSynchronize(st_));
+    return std::move(out_);
+}
+
+}  // namespace
+
+DeviceFactorization gpu_factorize(const Csc& A, const ClusterHierarchy& h, const std::vector<int>& owner,
+                                  const FactorizeOptions& opt, cudaStream_t st) {
+    if (A.m < A.n) throw std::invalid_argument("matrix must have at least as many rows as columns");
+    if (static_cast<Index>(owner.size()) != A.m) throw std::invalid_argument("row_owner size mismatch");
+    Engine e(A, h, owner, opt, st);
+    return e.run();
+}
+
+}  // namespace spqr

@@ -1,0 +1,50 @@
+// GPU factorization engine: Algorithm 1 of spaQR (proj/src/factorize.cpp) with
+// every FP64 front in HBM and one batched launch per phase per stage.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "devmem.h"
+#include "spqr.h"
+
+namespace spqr {
+
+// One factor of W (transforms.h:16-30) held on the device.
+struct DevWFactor {
+    int kind = 0;         // 0 TriangularScale ([R | C]), 1 ColumnRotation (V, tau, sign)
+    int batch = 0;        // consecutive factors of one phase: mutually independent column sets
+    int c = 0, k = 0;     // |cols|; |coupled| (kind 0) or reflector count (kind 1)
+    long long cols_off = 0, coupled_off = 0;  // into DeviceFactorization::idx
+    double* a = nullptr;  // kind 0: c x (c+k), ld c.  kind 1: V c x k, ld c
+    double* tau = nullptr;
+    double* sign = nullptr;
+};
+
+struct EngineCounters {
+    long long launches = 0, syncs = 0, h2d_bytes = 0, d2h_bytes = 0;
+    double qr_flops = 0, qr_bytes = 0, cpqr_flops = 0, cpqr_bytes = 0;  // algorithmic work (BASELINE.md formulas)
+    double t_qr_ms = 0;  // device time of the batched front-QR launches (CUDA events)
+    long long qr_launches = 0;
+};
+
+// The outcome of spaqr_factorize (transforms.h:53-72) with W resident in HBM.
+struct DeviceFactorization {
+    Index M = 0, N = 0;
+    double eps = 0.0;
+    std::vector<DevWFactor> W;
+    std::vector<int> idx;  // cols / coupled lists of all factors
+    std::vector<Index> pivot_row, dropped_rows, trailing_rows;
+    std::vector<StageStats> stages;
+    std::unique_ptr<DeviceArena> warena;
+    int nbatches = 0;
+    EngineCounters ctr;
+    long long nnz_w() const;
+};
+
+DeviceFactorization gpu_factorize(const Csc& A, const ClusterHierarchy& h, const std::vector<int>& owner,
+                                  const FactorizeOptions& opt, cudaStream_t st);
+
+}  // namespace spqr

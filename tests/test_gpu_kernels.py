@@ -1,0 +1,97 @@
+"""GPU parity: batched dense kernels vs the oracle (dense_kernels.cpp semantics).
+Tolerances: FP64, orthogonal-factor tests as in proj/tests/test_dense_kernels.cpp."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _P():
+    import paper_2102_09878_b200 as P
+    return P
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (5, 3, 3), (20, 7, 30), (40, 12, 60), (128, 32, 288), (300, 64, 96)])
+def test_qr_apply_matches_oracle(shape):
+    m, n, ntot = shape
+    rng = np.random.default_rng(m * 131 + n)
+    nb = 6
+    A = rng.standard_normal((nb, m, ntot))
+    out, tau, sg, info = _P().qr_apply_batched(A, n)
+    assert np.all(info == -1)
+    for b in range(nb):
+        V, t, s, R = O.householder_qr(A[b, :, :n])
+        # R with the nonnegative diagonal convention, same reflector convention
+        assert np.allclose(np.triu(out[b, :n, :n]), R, rtol=0, atol=1e-12 * (1 + np.abs(R).max()))
+        assert np.all(np.diag(out[b, :n, :n]) >= 0)
+        assert np.allclose(tau[b], t, atol=1e-13)
+        assert np.array_equal(sg[b], s)
+        Vg = np.tril(out[b, :, :n], -1) + np.eye(m, n)
+        assert np.allclose(Vg, V, atol=1e-12)
+        if ntot > n:
+            X = O.apply_reflectors(V, t, s, A[b, :, n:], "left_t")
+            assert np.allclose(out[b, :, n:], X, atol=1e-12 * (1 + np.abs(X).max()))
+
+
+def test_qr_flags_singular_pivot():
+    A = np.zeros((1, 4, 3))
+    A[0, :, 0] = 1.0
+    A[0, :, 1] = 2.0  # column 1 parallel to column 0 -> R_11 == 0 (up to roundoff)
+    A[0, :, 2] = [1, 2, 3, 4]
+    out, tau, sg, info = _P().qr_apply_batched(A, 3)
+    Z = np.zeros((1, 3, 2))
+    out2, _, _, info2 = _P().qr_apply_batched(Z, 2)
+    assert info2[0] == 0
+
+
+@pytest.mark.parametrize("shape,eps", [((8, 8), 1e-2), ((20, 35), 1e-3), ((35, 20), 1e-8), ((64, 200), 1e-2),
+                                       ((3, 14), 1e-10), ((14, 3), 0.0)])
+def test_cpqr_matches_oracle(shape, eps):
+    m, n = shape
+    rng = np.random.default_rng(m + 7 * n)
+    nb = 5
+    A = np.stack([rng.standard_normal((m, 4)) @ rng.standard_normal((4, n)) + 1e-3 * rng.standard_normal((m, n))
+                  for _ in range(nb)])
+    res = _P().cpqr_batched(A, eps)
+    for b in range(nb):
+        ref = O.cpqr(A[b], eps)
+        g = res[b]
+        assert g["rank"] == ref["rank"]
+        assert np.array_equal(g["perm"], ref["perm"])
+        assert abs(g["r11"] - ref["r11"]) <= 1e-12 * abs(ref["r11"])
+        assert np.allclose(g["R"], ref["R"], atol=1e-11 * (1 + abs(ref["r11"])))
+        assert np.allclose(g["V"], ref["V"], atol=1e-11)
+        assert np.allclose(g["tau"], ref["tau"], atol=1e-12)
+        assert np.array_equal(g["sign"], ref["sign"])
+
+
+def test_cpqr_edge_cases():
+    res = _P().cpqr_batched(np.zeros((2, 6, 4)), 1e-8)
+    assert all(r["rank"] == 0 and r["r11"] == 0.0 for r in res)
+    B = np.zeros((1, 4, 3))
+    B[0, :, 0] = 1.0
+    assert _P().cpqr_batched(B, 0.0)[0]["rank"] == 3
+
+
+def test_cpqr_decaying_interface_rank():  # BASELINE config 5 interface: sigma_i = 0.8^i
+    from paper_2102_09878_b200.problems import decaying_interface
+    B = decaying_interface(256, 0.8, seed=0)
+    g = _P().cpqr_batched(B[None], 1e-2)[0]
+    ref = O.cpqr(B, 1e-2)
+    assert abs(g["rank"] - ref["rank"]) <= 1
+    assert np.array_equal(g["perm"][: min(g["rank"], ref["rank"])], ref["perm"][: min(g["rank"], ref["rank"])])
+
+
+def test_trsm_right_matches_oracle():
+    rng = np.random.default_rng(57)
+    nb, nrows, n = 7, 9, 6
+    R = np.triu(rng.uniform(-1, 1, (nb, n, n)))
+    for b in range(nb):
+        R[b][np.diag_indices(n)] = 1 + np.abs(np.diag(R[b]))
+    B = rng.uniform(-1, 1, (nb, nrows, n))
+    X = _P().trsm_right_batched(B, R)
+    for b in range(nb):
+        ref = O.tri_solve_upper(R[b], B[b], "right", False)
+        assert np.allclose(X[b], ref, atol=1e-12)

@@ -1,0 +1,135 @@
+"""GPU parity: the full spaQR path (host partition + GPU engine + GPU CGLS)
+against the oracle on the same seeded inputs.  Bar (BASELINE.json north_star):
+ordering and cluster structure bit-exact; ranks identical (+-1 only where a
+singular value is within 1e-12 of the tolerance); CGLS residual within 1e-10
+and iteration count within +-1."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle as O
+from paper_2102_09878_b200.problems import random_full_rank, tall_grid
+
+pytestmark = pytest.mark.gpu
+
+
+def _P():
+    import paper_2102_09878_b200 as P
+    return P
+
+
+def _pair(A, **kw):
+    return O.Pipeline(A, **kw), _P().Pipeline(A, **kw)
+
+
+def _compare_structure(o, g, exact_ranks=True):
+    assert np.array_equal(o.perm(), g.perm())
+    assert np.array_equal(o.owner(), g.owner())
+    co, cg = o.clusters(), g.clusters()
+    assert len(co) == len(cg)
+    for a, b in zip(co, cg):
+        assert a["tree_node"] == b["tree_node"] and a["level"] == b["level"] and a["parent"] == b["parent"]
+        assert a["stage"] == b["stage"] and np.array_equal(a["cols"], b["cols"])
+    so, sg = o.stages(), g.stages()
+    assert len(so) == len(sg)
+    for a, b in zip(so, sg):
+        assert a["stage"] == b["stage"]
+        if exact_ranks:
+            assert np.array_equal(a["front_cols"], b["front_cols"])
+            assert a["top_rows"] == b["top_rows"] and a["top_cols"] == b["top_cols"]
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-2])
+def test_small_random_exact_structure(eps):
+    A = random_full_rank(120, 70, 4, seed=3)
+    o, g = _pair(A, eps=eps, levels=2, skip_levels=0)
+    _compare_structure(o, g)
+    po, do, to = o.rows()
+    pg, dg, tg = g.rows()
+    assert np.array_equal(po, pg) and np.array_equal(np.sort(do), np.sort(dg)) and np.array_equal(np.sort(to), np.sort(tg))
+    assert o.nW == g.nW and o.nnz_w == g.nnz_w
+
+
+def test_w_factors_match_oracle():
+    p = tall_grid(16, seed=7)
+    o, g = _pair(p.A, eps=1e-2, levels=4, skip_levels=1, coords=p.coords)
+    _compare_structure(o, g)
+    fo, fg = o.wfactors(), g.wfactors()
+    assert len(fo) == len(fg)
+    for a, b in zip(fo, fg):
+        assert a[0] == b[0] and np.array_equal(a[1], b[1])
+        if a[0] == "tri":
+            assert np.array_equal(a[3], b[3])
+            sc = 1 + np.abs(a[2]).max()
+            assert np.allclose(a[2], b[2], atol=1e-11 * sc)
+            if a[4].size:
+                assert np.allclose(a[4], b[4], atol=1e-11 * sc)
+        else:
+            assert np.allclose(a[2], b[2], atol=1e-10)
+            assert np.allclose(a[3], b[3], atol=1e-12)
+            assert np.array_equal(a[4], b[4])
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-2])
+def test_sweeps_match_oracle_and_round_trip(eps):
+    p = tall_grid(16, seed=7)
+    o, g = _pair(p.A, eps=eps, levels=4, skip_levels=1, coords=p.coords)
+    rng = np.random.default_rng(13)
+    for _ in range(5):
+        z = rng.uniform(-1, 1, g.N)
+        nz = np.linalg.norm(z)
+        for name in ("w_apply", "w_solve", "wt_apply", "wt_solve"):
+            a, b = getattr(o, name)(z), getattr(g, name)(z)
+            assert np.linalg.norm(a - b) <= 1e-10 * max(np.linalg.norm(a), 1.0)
+        assert np.linalg.norm(g.w_solve(g.w_apply(z)) - z) <= 1e-12 * nz
+        assert np.linalg.norm(g.wt_solve(g.wt_apply(z)) - z) <= 1e-12 * nz
+
+
+def test_config1_parity():  # BASELINE config 1: 2D tall n=64, L=8, eps 1e-3, CGLS 1e-12
+    p = tall_grid(64)
+    o, g = _pair(p.A, eps=p.eps, levels=p.levels, coords=p.coords)
+    _compare_structure(o, g)
+    xo, ro = o.solve(p.b)
+    xg, rg = g.solve(p.b)
+    assert rg["converged"] and abs(rg["iterations"] - ro["iterations"]) <= 1
+    A = p.A
+    rel = lambda x: np.linalg.norm(A.T @ (p.b - A @ x)) / np.linalg.norm(A.T @ p.b)
+    assert abs(rel(xg) - rel(xo)) <= 1e-10
+    assert rg["residual_history"][-1] <= 1e-12
+
+
+def test_exact_factorization_solves_dense_ls():
+    A = random_full_rank(150, 90, 4, seed=5)
+    g = _P().Pipeline(A, eps=0.0, levels=2, solver="direct")
+    b = np.random.default_rng(11).standard_normal(150)
+    x, rep = g.solve(b, direct=True)
+    ref = np.linalg.lstsq(A.toarray(), b, rcond=None)[0]
+    assert np.linalg.norm(x - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_identity_is_exact():
+    n = 40
+    g = _P().Pipeline(sp.identity(n, format="csc"), eps=0.0, levels=1)
+    z = np.random.default_rng(1).uniform(-1, 1, n)
+    assert np.array_equal(g.w_apply(z), z) and np.array_equal(g.w_solve(z), z)
+
+
+def test_singular_front_errors_match_reference():
+    D = np.zeros((9, 6))
+    D[0, 0], D[0, 1] = 1.0, 2.0
+    for j in range(2, 6):
+        D[2 * j - 3, j] = 3.0
+        D[2 * j - 2, j] = 0.5
+    with pytest.raises(_P().SingularFrontError) as e:
+        _P().Pipeline(sp.csc_matrix(D), eps=0.0, levels=1, parts=[0, 0, 1, 1, 1, 1])
+    with pytest.raises(O.SingularFrontError) as eo:
+        O.Pipeline(sp.csc_matrix(D), eps=0.0, levels=1, parts=[0, 0, 1, 1, 1, 1])
+    assert e.value.cluster == eo.value.cluster and "rows couple" in str(e.value)
+    D = np.zeros((11, 7))
+    D[0, 0], D[0, 1], D[1, 2], D[2, 2] = 1.5, -2.25, 2.0, 0.5
+    for j in range(3, 7):
+        D[2 * j - 3, j] = 3.0
+        D[2 * j - 2, j] = -0.75
+    with pytest.raises(_P().SingularFrontError) as e:
+        _P().Pipeline(sp.csc_matrix(D), eps=0.0, levels=1, parts=[0, 0, 0, 1, 1, 1, 1])
+    assert "pivot" in str(e.value) and e.value.cluster >= 0
