@@ -176,7 +176,7 @@ def qr_apply_batched(A, n):
     require_gpu()
     A = np.asarray(A, np.float64)
     nb, m, ntot = A.shape
-    buf = np.ascontiguousarray(A.transpose(0, 2, 1)).ravel()  # column-major per block
+    buf = np.array(A.transpose(0, 2, 1), dtype=np.float64, order='C', copy=True).ravel()  # column-major per block
     tau = np.zeros(max(nb * n, 1))
     sg = np.zeros(max(nb * n, 1))
     info = np.zeros(max(nb, 1), np.int32)
@@ -193,7 +193,7 @@ def cpqr_batched(A, eps):
     A = np.asarray(A, np.float64)
     nb, m, n = A.shape
     k = max(min(m, n), 1)
-    buf = np.ascontiguousarray(A.transpose(0, 2, 1)).ravel()
+    buf = np.array(A.transpose(0, 2, 1), dtype=np.float64, order='C', copy=True).ravel()
     rank = np.zeros(nb, np.int32)
     r11 = np.zeros(nb)
     perm = np.zeros(nb * k, np.int32)
@@ -219,7 +219,7 @@ def trsm_right_batched(B, R):
     require_gpu()
     B = np.asarray(B, np.float64)
     nb, nrows, n = B.shape
-    bb = np.ascontiguousarray(B.transpose(0, 2, 1)).ravel()
+    bb = np.array(B.transpose(0, 2, 1), dtype=np.float64, order='C', copy=True).ravel()
     rr = np.ascontiguousarray(np.asarray(R, np.float64).transpose(0, 2, 1)).ravel()
     rc = lib().spqr_trsm_right_batched(nb, nrows, n, bb, rr)
     if rc:

@@ -298,7 +298,7 @@ int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, doubl
         std::vector<QrDesc> qd(nb);
         for (int b = 0; b < nb; ++b)
             qd[b] = QrDesc{d_a + static_cast<long long>(b) * m * ntot, m, m, n, ntot, d_tau + static_cast<long long>(b) * n,
-                           d_sign + static_cast<long long>(b) * n, nullptr, d_info + b, 0};
+                           d_sign + static_cast<long long>(b) * n, nullptr, d_info + b, 0, 0};
         QrDesc* dq = nullptr;
         CK(cudaMalloc(&dq, sizeof(QrDesc) * std::max(nb, 1)));
         CK(cudaMemcpy(dq, qd.data(), sizeof(QrDesc) * nb, cudaMemcpyHostToDevice));

@@ -62,6 +62,7 @@ struct QrDesc {
     double* rout;     // optional copy of R (n x n, ld = n)
     int* flag;        // atomicMin'd with the first i with |R_ii| < DBL_MIN (init INT_MAX; dense_kernels.cpp:234-240)
     int set_identity; // after the update: A(:, :n) := [I; 0]  (factorize.cpp:473-474)
+    int zero_lower;   // after the update: clear V below the diagonal (R alone remains)
 };
 
 // ---- B <- B R^{-1} (right, upper, no transpose): factorize.cpp:475-478

@@ -53,6 +53,7 @@ struct Front {
     int ld = 0, ncols = 0;
     bool scaled_ok = false;
     std::vector<long long> soff;  // pre-stage row statistics offset per key (eliminate)
+    std::vector<int> tag;         // per row append tag within the current stage (empty: all -1)
     int find(int key) const {
         auto it = std::lower_bound(keys.begin(), keys.end(), key, [](const KeyRef& a, int k) { return a.key < k; });
         return (it != keys.end() && it->key == key) ? static_cast<int>(it - keys.begin()) : -1;
@@ -63,7 +64,7 @@ struct Front {
 // symbolic row: values of old front `base` row `brow`, overridden by stack
 // `sidx` row `srow` on that stack's neighbour keys.
 struct PRow {
-    int gid, base, brow, sidx, srow;
+    int gid, base, brow, sidx, srow, tag;  // tag: cluster whose move_extras appended the row this stage (-1: none)
 };
 struct KW {
     int key, width;
@@ -170,6 +171,9 @@ public:
         gone_.assign(nc, 0);
         holders_.resize(nc);
         pend_id_.assign(nc, -1);
+        mark_.assign(nc, 0);
+        stage_of_.assign(nc, 0);
+        for (size_t c = 0; c < nc; ++c) stage_of_[c] = (h.clusters[c].level == h.clusters[c].stage) ? h.clusters[c].stage : 0;
         stage_list_.resize(L_ + 2);
         for (size_t c = 0; c < nc; ++c) {
             const auto& C = h.clusters[c];
@@ -210,6 +214,9 @@ private:
     std::vector<PFront> pend_;
     std::vector<int> pend_id_, pend_list_;
     std::vector<Elim> el_;
+    std::vector<char> mark_;
+    std::vector<int> stage_of_;
+    std::vector<std::pair<int, int>> dep_;
     AsmBuilder wcopy_;
     std::vector<double> pre_sq_, post_sq_;
     std::vector<unsigned char> pre_nz_, post_nz_;
@@ -279,6 +286,9 @@ private:
 
     void init_fronts(const std::vector<int>& owner);
     void eliminate_stage(int k);
+    void eliminate_wave(const std::vector<int>& list);
+    void compute_stats(const std::vector<int>& P);
+    std::vector<int> stage_fronts(const std::vector<int>& list);
     void elim_pass1(Elim& e);
     void elim_pass2(Elim& e, int eidx);
     void materialize_pending();
@@ -297,7 +307,8 @@ private:
             PFront& P = pend_.back();
             const Front& F = fr_[f];
             P.rows.resize(F.rows.size());
-            for (size_t i = 0; i < F.rows.size(); ++i) P.rows[i] = PRow{F.rows[i], f, static_cast<int>(i), -1, 0};
+            for (size_t i = 0; i < F.rows.size(); ++i)
+                P.rows[i] = PRow{F.rows[i], f, static_cast<int>(i), -1, 0, F.tag.empty() ? -1 : F.tag[i]};
             P.keys.resize(F.keys.size());
             for (size_t i = 0; i < F.keys.size(); ++i) P.keys[i] = KW{F.keys[i].key, F.keys[i].width};
         }
@@ -305,10 +316,11 @@ private:
     }
     // squared norm / nonzero of a symbolic row on one key
     void rowval(const PRow& r, int key, double& sq, bool& nz, bool post_ok) const;
-    DevWFactor& new_factor(int kind, int c, int k, const std::vector<int>& cols, const std::vector<int>* coupled) {
+    DevWFactor& new_factor(int kind, int cluster, int c, int k, const std::vector<int>& cols, const std::vector<int>* coupled) {
         DevWFactor f;
         f.kind = kind;
         f.batch = batch_;
+        f.cluster = cluster;
         f.c = c;
         f.k = k;
         f.cols_off = static_cast<long long>(out_.idx.size());
@@ -570,7 +582,7 @@ void Engine::elim_pass2(Elim& e, int eidx) {
                 coupled.insert(coupled.end(), cols_[e.keys[ki]].begin(), cols_[e.keys[ki]].end());
             }
         }
-        DevWFactor& f = new_factor(0, cs, kept, cols_[c], &coupled);
+        DevWFactor& f = new_factor(0, c, cs, kept, cols_[c], &coupled);
         f.a = out_.warena->alloc_n<double>(static_cast<size_t>(cs) * (cs + kept));
         // copy [R | C_kept] from the stack (rows 0..cs-1)
         wcopy_.begin(f.a, cs, cs, cs + kept, 1);
@@ -614,7 +626,16 @@ void Engine::elim_pass2(Elim& e, int eidx) {
                 T.add(kw.key, width(kw.key));
                 sorted_insert(holders_[kw.key], tgt);
             }
-            for (int q : lr) T.rows.push_back(fc.rows[q]);
+            // sequential order appends in ascending c: keep groups sorted by their source cluster
+            auto pos = std::upper_bound(T.rows.begin(), T.rows.end(), c, [](int cc, const PRow& r) { return cc < r.tag; });
+            std::vector<PRow> grp;
+            grp.reserve(lr.size());
+            for (int q : lr) {
+                PRow r = fc.rows[q];
+                r.tag = c;
+                grp.push_back(r);
+            }
+            T.rows.insert(pos, grp.begin(), grp.end());
             fr_[tgt].scaled_ok = false;
         }
     }
@@ -637,6 +658,8 @@ void Engine::materialize_pending() {
         nf.scaled_ok = fr_[f].scaled_ok;
         nf.rows.resize(P.rows.size());
         for (size_t i = 0; i < P.rows.size(); ++i) nf.rows[i] = P.rows[i].gid;
+        nf.tag.resize(P.rows.size());
+        for (size_t i = 0; i < P.rows.size(); ++i) nf.tag[i] = P.rows[i].tag;
         nf.keys.resize(P.keys.size());
         for (size_t i = 0; i < P.keys.size(); ++i) nf.keys[i] = KeyRef{P.keys[i].key, P.keys[i].width, 0};
         layout(f, nf.keys, nf.ncols);
@@ -707,38 +730,17 @@ void Engine::materialize_pending() {
     pend_.clear();
 }
 
-void Engine::eliminate_stage(int k) {
-    const auto& list = stage_list_[k];
-    if (list.empty()) return;
-    el_.clear();
-    el_.reserve(list.size());
-    // fronts whose pre-stage statistics are needed: all participants + own fronts
-    std::vector<int> P;
-    std::vector<char> inP(fr_.size(), 0);
-    auto addP = [&](int f) {
-        if (!inP[f] && fr_[f].live) {
-            inP[f] = 1;
-            P.push_back(f);
-        }
-    };
-    for (int c : list) {
-        addP(c);
-        if (width(c) > 0)
-            for (int m : holders_[c]) addP(m);
-    }
+// pre-stage row statistics (sum of squares, any-nonzero) of every block of the fronts in P
+void Engine::compute_stats(const std::vector<int>& P) {
     std::vector<StatDesc> sd;
     long long work = 0;
     for (int f : P) {
         Front& F = fr_[f];
         F.soff.assign(F.keys.size(), -1);
         for (size_t qi = 0; qi < F.keys.size(); ++qi) {
-            if (F.nrows() == 0) {
-                F.soff[qi] = work;
-                continue;
-            }
-            StatDesc s{F.mat, F.ld, 0, F.nrows(), F.keys[qi].col, F.keys[qi].width, 0, work, work};
             F.soff[qi] = work;
-            sd.push_back(s);
+            if (F.nrows() == 0) continue;
+            sd.push_back(StatDesc{F.mat, F.ld, 0, F.nrows(), F.keys[qi].col, F.keys[qi].width, 0, work, work});
             work += F.nrows();
         }
     }
@@ -753,7 +755,83 @@ void Engine::eliminate_stage(int k) {
     }
     download(pre_sq_, d_sq, work);
     download(pre_nz_, d_nz, work);
-    // pass 1 over the whole batch (ascending ids)
+}
+
+std::vector<int> Engine::stage_fronts(const std::vector<int>& list) {
+    std::vector<int> P;
+    for (int c : list) {
+        if (fr_[c].live && !mark_[c]) {
+            mark_[c] = 1;
+            P.push_back(c);
+        }
+        if (width(c) > 0)
+            for (int m : holders_[c])
+                if (fr_[m].live && !mark_[m]) {
+                    mark_[m] = 1;
+                    P.push_back(m);
+                }
+    }
+    for (int f : P) mark_[f] = 0;
+    return P;
+}
+
+// Eliminations of one stage touch disjoint rows in exact mode, but once
+// scale_all has mixed a shared front's rows, two clusters of the same stage
+// can couple to the same row: the later one must see the earlier one's
+// transformed values (the reference runs them in ascending id order).  The
+// stage is split into dependency waves (edge c1 -> c2, c1 < c2, when some row
+// is nonzero in both blocks); each wave is one batched round.
+void Engine::eliminate_stage(int k) {
+    const auto& list = stage_list_[k];
+    if (list.empty()) return;
+    for (size_t f = 0; f < fr_.size(); ++f) fr_[f].tag.clear();
+    std::vector<int> P = stage_fronts(list);
+    compute_stats(P);
+    std::vector<int> lvl(fr_.size(), -1);
+    for (int c : list) lvl[c] = 0;
+    {
+        std::vector<int> last;
+        for (int f : P) {
+            const Front& F = fr_[f];
+            last.assign(F.nrows(), -1);
+            for (size_t qi = 0; qi < F.keys.size(); ++qi) {  // ascending keys
+                const int c = F.keys[qi].key;
+                if (lvl[c] < 0 || stage_of_[c] != k) continue;
+                for (int r = 0; r < F.nrows(); ++r)
+                    if (pre_nz_[F.soff[qi] + r]) {
+                        if (last[r] >= 0) dep_.emplace_back(last[r], c);
+                        last[r] = c;
+                    }
+            }
+        }
+        std::sort(dep_.begin(), dep_.end(), [](const auto& a, const auto& b) { return a.second < b.second; });
+        size_t q = 0;
+        for (int c : list) {  // ascending: every edge points to a larger id
+            for (; q < dep_.size() && dep_[q].second == c; ++q) lvl[c] = std::max(lvl[c], lvl[dep_[q].first] + 1);
+        }
+        dep_.clear();
+    }
+    int nw = 0;
+    for (int c : list) nw = std::max(nw, lvl[c] + 1);
+    std::vector<std::vector<int>> waves(nw);
+    for (int c : list) waves[lvl[c]].push_back(c);
+    out_.ctr.elim_waves += nw;
+    const size_t w0 = out_.W.size();
+    for (int w = 0; w < nw; ++w) {
+        if (w > 0) compute_stats(stage_fronts(waves[w]));
+        batch_ = out_.nbatches++;  // a wave's factors touch independent column sets
+        eliminate_wave(waves[w]);
+    }
+    // W in the reference's chronological order (ascending cluster); the solve
+    // plan regroups by batch, which only reorders independent factors
+    std::stable_sort(out_.W.begin() + w0, out_.W.end(),
+                     [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
+}
+
+void Engine::eliminate_wave(const std::vector<int>& list) {
+    el_.clear();
+    el_.reserve(list.size());
+    // pass 1 over the wave (ascending ids)
     int nvalid = 0;
     for (int c : list) {
         el_.emplace_back();
@@ -796,7 +874,7 @@ void Engine::eliminate_stage(int k) {
                     sb.cmap[d.cmap_off + static_cast<long long>(e.off[ki] + o) * nsrc + s] = B.keys[qi].col + o;
             }
         flags_init.push_back(INT_MAX);
-        QrDesc q{e.S, e.total_rows, e.total_rows, e.cs, e.tcols, nullptr, nullptr, nullptr, nullptr, 0};
+        QrDesc q{e.S, e.total_rows, e.total_rows, e.cs, e.tcols, nullptr, nullptr, nullptr, nullptr, 0, 1};
         qd.push_back(q);
         out_.ctr.qr_flops += 2.0 * e.total_rows * double(e.cs) * e.cs - 2.0 / 3.0 * double(e.cs) * e.cs * e.cs +
                              (4.0 * e.total_rows * e.cs - 2.0 * e.cs * double(e.cs)) * (e.tcols - e.cs);
@@ -920,9 +998,9 @@ void Engine::scale_all() {
             continue;
         }
         const int cs = width(p);
-        DevWFactor& w = new_factor(0, cs, 0, cols_[p], nullptr);
+        DevWFactor& w = new_factor(0, p, cs, 0, cols_[p], nullptr);
         w.a = out_.warena->alloc_n<double>(static_cast<size_t>(cs) * cs);
-        qd.push_back(QrDesc{f.mat, f.ld, f.nrows(), cs, f.ncols, nullptr, nullptr, w.a, nullptr, 1});
+        qd.push_back(QrDesc{f.mat, f.ld, f.nrows(), cs, f.ncols, nullptr, nullptr, w.a, nullptr, 1, 0});
         qp.push_back(p);
         out_.ctr.qr_flops += 2.0 * f.nrows() * double(cs) * cs - 2.0 / 3.0 * double(cs) * cs * cs +
                              (4.0 * f.nrows() * cs - 2.0 * cs * double(cs)) * (f.ncols - cs);
@@ -1069,6 +1147,7 @@ void Engine::sparsify_cols_all() {
     std::vector<std::vector<int>> waves(nwaves);
     for (int p : elig) waves[level[p]].push_back(p);
     const int rot_batch = batch_;
+    const size_t w0 = out_.W.size();
     for (auto& wave : waves) {
         struct Job {
             int p, cs, nG, wrows, kmax;
@@ -1160,7 +1239,7 @@ void Engine::sparsify_cols_all() {
             Front& f = fr_[p];
             if (r2 > 0) {
                 batch_ = rot_batch;
-                DevWFactor& w = new_factor(1, j.cs, r2, cols_[p], nullptr);
+                DevWFactor& w = new_factor(1, p, j.cs, r2, cols_[p], nullptr);
                 w.a = j.V;
                 w.tau = j.tau;
                 w.sign = j.sign;
@@ -1281,6 +1360,8 @@ void Engine::sparsify_cols_all() {
         flush_assemble(mb);
         for (auto& [f, nf] : updates) fr_[f] = std::move(nf);
     }
+    std::stable_sort(out_.W.begin() + w0, out_.W.end(),
+                     [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
 }
 
 // factorize.cpp:635-729 — children concatenate into parents; every live front
@@ -1402,7 +1483,6 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         StageStats st;
         st.stage = k;
         double t0 = now_s();
-        batch_ = out_.nbatches++;
         eliminate_stage(k);
         st.t_eliminate = now_s() - t0;
         if (opt_.eps > 0.0 && k >= 2 && L_ + 1 - k >= opt_.skip_levels) {

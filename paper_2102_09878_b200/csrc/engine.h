@@ -15,7 +15,8 @@ namespace spqr {
 // One factor of W (transforms.h:16-30) held on the device.
 struct DevWFactor {
     int kind = 0;         // 0 TriangularScale ([R | C]), 1 ColumnRotation (V, tau, sign)
-    int batch = 0;        // consecutive factors of one phase: mutually independent column sets
+    int batch = 0;        // factors of one batch act on mutually independent column sets
+    int cluster = -1;     // cluster whose step produced the factor
     int c = 0, k = 0;     // |cols|; |coupled| (kind 0) or reflector count (kind 1)
     long long cols_off = 0, coupled_off = 0;  // into DeviceFactorization::idx
     double* a = nullptr;  // kind 0: c x (c+k), ld c.  kind 1: V c x k, ld c
@@ -28,6 +29,7 @@ struct EngineCounters {
     double qr_flops = 0, qr_bytes = 0, cpqr_flops = 0, cpqr_bytes = 0;  // algorithmic work (BASELINE.md formulas)
     double t_qr_ms = 0;  // device time of the batched front-QR launches (CUDA events)
     long long qr_launches = 0;
+    long long elim_waves = 0;  // dependency waves of eliminations summed over stages
 };
 
 // The outcome of spaqr_factorize (transforms.h:53-72) with W resident in HBM.

@@ -219,6 +219,11 @@ __global__ void __launch_bounds__(kQrThreads) k_qr(const QrDesc* __restrict__ ds
             const int i = e % n, j = e / n;
             d.rout[e] = (i <= j) ? A[i + static_cast<long long>(j) * ld] : 0.0;
         }
+    if (d.zero_lower && !d.set_identity) {
+        __syncthreads();
+        for (int j = 0; j < n; ++j)
+            for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) A[i + static_cast<long long>(j) * ld] = 0.0;
+    }
     if (d.set_identity) {
         __syncthreads();
         for (int e = threadIdx.x; e < m * n; e += blockDim.x) {

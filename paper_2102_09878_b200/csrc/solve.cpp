@@ -14,18 +14,22 @@ SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
     PinnedArena pin;
     Uploader up{P.mem.get(), &pin, st};
     const int* d_idx = up.put(F.idx);
-    // group consecutive factors of equal batch id
+    // group factors by batch (batch ids increase chronologically; within a
+    // batch the factors commute)
+    std::vector<size_t> ord(F.W.size());
+    for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return F.W[a].batch < F.W[b].batch; });
     long long maxcontrib = 1;
     size_t i = 0;
-    while (i < F.W.size()) {
+    while (i < ord.size()) {
         size_t j = i;
-        while (j < F.W.size() && F.W[j].batch == F.W[i].batch) ++j;
+        while (j < ord.size() && F.W[ord[j]].batch == F.W[ord[i]].batch) ++j;
         std::vector<WFac> fac;
         long long contrib = 0;
         std::map<int, std::vector<int>> lists;  // coupled column -> contribution indices (chronological)
         int maxc = 1;
         for (size_t q = i; q < j; ++q) {
-            const DevWFactor& w = F.W[q];
+            const DevWFactor& w = F.W[ord[q]];
             WFac f{};
             f.kind = w.kind;
             f.c = w.c;
