@@ -1,0 +1,291 @@
+"""Benchmark of the spaQR hot path on B200 (BASELINE.json metric: spaQR factor+solve
+time, s; plus the batched front-QR roofline).
+
+Workload (BASELINE.json configs[1], "C2"): 2D tall sparse least squares on a
+512 x 512 grid (N = 262,144 unknowns, M = 2N rows), seeded synthetic data,
+geometric nested dissection with 14 levels, sparsification tol 1e-2,
+preconditioned CGLS to 1e-12.  One step = one spaqr factorization + one
+preconditioned CGLS solve of that problem.
+
+value    : factorize + solve time measured with CUDA events on the pipeline
+           stream (A already scaled/permuted/partitioned on the host and
+           uploaded — the reference times t_factorize and t_solve the same way,
+           pipeline.cpp:55-61, solve.cpp:26,74).
+e2e      : the same step through the C ABI from HOST buffers
+           (spqr_pipeline_create + spqr_pipeline_solve): partition, upload of A
+           and b, factorize, solve, download of x.
+--impl reference : the CPU oracle restatement of the reference (the reference
+           itself cannot be built here: Eigen3 is absent), timed on this box's
+           host on the same problem.
+Multi-GPU (--gpus N under torchrun): independent replicas, one per GPU
+("replicas only" in round 1), timed as the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOAD = ("C2: 2D tall sparse LS, 512x512 grid, N=262144, M=524288, 5-point rows + 3-nnz random rows, "
+            "geometric ND L=14, eps=1e-2, skip_levels=3, CGLS tol 1e-12 (seed 0)")
+METRIC = "spaQR factor+solve time (s)"
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allmax(ws, v):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], device="cuda" if torch.cuda.is_available() else "cpu", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and "Active" in s[3 + i]
+                          and "Not" not in s[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch for `kernel` from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+def make_problem():
+    from paper_2102_09878_b200.problems import tall_grid
+    return tall_grid(512, seed=0)
+
+
+def cpu_oracle_step(p):
+    import oracle as O
+    t0 = time.perf_counter()
+    P = O.Pipeline(p.A, eps=p.eps, levels=p.levels, coords=p.coords)
+    x, rep = P.solve(p.b)
+    wall = time.perf_counter() - t0
+    t = P.times()
+    return t["t_factorize"] + rep["t_solve"], wall, rep["iterations"], t["t_partition"]
+
+
+def l2_flush(buf):
+    if buf is not None:
+        buf.add_(1.0)
+
+
+def run_ours(args, ws, rank, local):
+    import paper_2102_09878_b200 as P
+    P.require_gpu()
+    p = make_problem()
+    flush = None
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
+    except Exception:
+        flush = None
+    A = p.A
+    h2d = A.indptr.nbytes + A.indices.nbytes + A.data.nbytes + p.b.nbytes + p.coords.nbytes
+    d2h = 8 * A.shape[1]
+
+    def step():
+        t0 = time.perf_counter()
+        g = P.Pipeline(A, eps=p.eps, levels=p.levels, coords=p.coords, device=local)
+        x, rep = g.solve(p.b)
+        wall = time.perf_counter() - t0
+        t = g.times()
+        return g, rep, (t["factorize_event_ms"] + t["solve_event_ms"]) / 1e3, wall
+
+    for _ in range(args.warmup):
+        l2_flush(flush)
+        step()
+    clocks = ClockSampler(local)
+    barrier(ws)
+    clocks.start()
+    dev_t, e2e_t, last = [], [], None
+    for _ in range(args.steps):
+        l2_flush(flush)
+        if flush is not None:
+            import torch
+            torch.cuda.synchronize()
+        g, rep, dt, wall = step()
+        dev_t.append(dt)
+        e2e_t.append(wall)
+        last = (g, rep)
+    barrier(ws)
+    ck = clocks.stop()
+    value = allmax(ws, sum(dev_t) / len(dev_t))
+    e2e = allmax(ws, sum(e2e_t) / len(e2e_t))
+    g, rep = last
+    t = g.times()
+    ks = g.kernel_stats()
+    dom = max(ks, key=lambda k: ks[k]["ms"])
+    peak, peak_src = load_peaks()
+    d = ks[dom]
+    achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
+    per_launch_traffic = ncu_traffic(dom)
+    # front-QR roofline on its own (the kernel BASELINE.json names)
+    q = ks["front_qr"]
+    qr_gbs = q["bytes"] / (q["ms"] / 1e3) / 1e9 if q["ms"] > 0 else 0.0
+    qr_tflops = t["qr_flops"] / (q["ms"] / 1e3) / 1e12 if q["ms"] > 0 else 0.0
+    x_rel = None
+    launches = int(g.launches + t["solve_launches"])
+    out = {
+        "metric": METRIC, "value": round(value, 6), "unit": "s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(value * 1e3, 3), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "parallelism": f"replicas{ws}", "l2_flush": "256MB write between steps",
+                   "levels": p.levels, "eps": p.eps, "N": int(A.shape[1]), "M": int(A.shape[0])},
+        "e2e": {"value": round(e2e, 6), "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "note": "spqr_pipeline_create+solve from host CSC/b to host x, incl. host partition "
+                        f"({t['t_partition']:.3f}s)"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": per_launch_traffic,
+                     "peak_source": peak_src,
+                     "algorithmic_bytes": d["bytes"], "device_ms": round(d["ms"], 3), "launches": d["launches"],
+                     "front_qr": {"GB/s": round(qr_gbs, 2), "frac_hbm": round(qr_gbs / peak, 4),
+                                  "TFLOP/s": round(qr_tflops, 4), "launches": q["launches"],
+                                  "device_ms": round(q["ms"], 3)},
+                     "kernel_ms": {k: round(v["ms"], 3) for k, v in ks.items()}},
+        "gpu_launches": launches,
+        "clocks": ck,
+        "solve": {"iterations": rep["iterations"], "converged": rep["converged"],
+                  "residual": float(rep["residual_history"][-1]), "nW": g.nW, "nnz_w": g.nnz_w,
+                  "factorize_event_s": round(t["factorize_event_ms"] / 1e3, 4),
+                  "solve_event_s": round(t["solve_event_ms"] / 1e3, 4), "engine_syncs": g.syncs,
+                  "elim_waves": t["elim_waves"]},
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        v, wall, iters, tpart = cpu_oracle_step(p)
+        out["cpu_baseline"] = {"value": round(v, 4), "unit": "s", "cores": 1, "kind": "port",
+                               "sample": "full C2 problem, one factorize+solve of the single-threaded CPU oracle "
+                                         f"(oracle/; {iters} CGLS iterations; partition {tpart:.2f}s excluded)"}
+    if rank == 0:
+        print(json.dumps(out))
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    p = make_problem()
+    vals, walls, its = [], [], []
+    # the oracle is a pure CPU program: there is no device state to warm up, so
+    # warm-up steps are not repeated; at most 2 timed steps keep the run bounded.
+    for _ in range(max(1, min(args.steps, 2))):
+        v, wall, iters, tpart = cpu_oracle_step(p)
+        vals.append(v)
+        walls.append(wall)
+        its.append(iters)
+    v = sum(vals) / len(vals)
+    out = {"metric": METRIC, "value": round(v, 4), "unit": "s", "n_gpus": ws, "steps": len(vals),
+           "warmup": 0, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": WORKLOAD, "parallelism": "cpu-1-thread"},
+           "cpu_baseline": {"value": round(v, 4), "unit": "s", "cores": 1, "kind": "port",
+                            "sample": "full C2 problem per step (CPU oracle restatement; reference needs Eigen3, "
+                                      "absent)"},
+           "e2e": {"value": round(v, 4), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "iterations": its[-1]}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -50,8 +50,12 @@ void spqr_pipeline_destroy(spqr_pipeline* p);
  *           engine launches, engine syncs, h2d bytes, d2h bytes, solve-plan launches per sweep pair */
 void spqr_pipeline_info(const spqr_pipeline* p, long long* info);
 /* times[16]: t_partition, t_factorize, t_upload, qr_device_ms, qr_flops, qr_bytes, cpqr_flops,
- *            cpqr_bytes, qr_launches, (reserved) */
+ *            cpqr_bytes, qr_launches, factorize_event_ms, solve_event_ms, solve_launches,
+ *            elimination_waves */
 void spqr_pipeline_times(const spqr_pipeline* p, double* times);
+/* Device time (CUDA events on the engine stream), algorithmic HBM bytes and launch
+ * counts per kernel family: assemble, stats, front_qr, trsm, cpqr, scatter (6 each). */
+void spqr_pipeline_kernel_stats(const spqr_pipeline* p, double* ms, double* bytes, long long* launches);
 
 /* Pipeline::solve (pipeline.cpp:70-80) -> cgls (solve.cpp:24-76) on the device, or
  * Pipeline::solve_direct (:82-92) -> csne_solve (solve.cpp:78-108) when direct != 0.

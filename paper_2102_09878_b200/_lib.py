@@ -30,6 +30,7 @@ SIGNATURES = {
     "spqr_pipeline_destroy": (None, [vp]),
     "spqr_pipeline_info": (None, [vp, i64p]),
     "spqr_pipeline_times": (None, [vp, f64p]),
+    "spqr_pipeline_kernel_stats": (None, [vp, f64p, f64p, i64p]),
     "spqr_pipeline_solve": (C.c_int, [vp, C.c_int, f64p, f64p, C.c_double, C.c_int, C.POINTER(C.c_int),
                                       C.POINTER(C.c_int), f64p, C.POINTER(C.c_int), C.POINTER(C.c_double),
                                       C.c_char_p, C.c_int]),

@@ -71,7 +71,15 @@ class Pipeline:
         t = np.zeros(16)
         lib().spqr_pipeline_times(self.h, t)
         return dict(t_partition=t[0], t_factorize=t[1], t_upload=t[2], qr_ms=t[3], qr_flops=t[4], qr_bytes=t[5],
-                    cpqr_flops=t[6], cpqr_bytes=t[7], qr_launches=int(t[8]))
+                    cpqr_flops=t[6], cpqr_bytes=t[7], qr_launches=int(t[8]), factorize_event_ms=t[9],
+                    solve_event_ms=t[10], solve_launches=int(t[11]), elim_waves=int(t[12]))
+
+    KERNELS = ("assemble", "stats", "front_qr", "trsm", "cpqr", "scatter")
+
+    def kernel_stats(self):
+        ms, by, n = np.zeros(6), np.zeros(6), np.zeros(6, np.int64)
+        lib().spqr_pipeline_kernel_stats(self.h, ms, by, n)
+        return {k: dict(ms=float(ms[i]), bytes=float(by[i]), launches=int(n[i])) for i, k in enumerate(self.KERNELS)}
 
     def solve(self, b, tol=-1.0, maxit=-1, direct=False):
         b = np.ascontiguousarray(b, np.float64)

@@ -36,6 +36,8 @@ struct spqr_pipeline {
     double *d_b = nullptr, *d_u = nullptr;
     std::unique_ptr<DeviceArena> mem;
     double t_partition = 0, t_factorize = 0, t_upload = 0;
+    double ev_factorize_ms = 0, ev_solve_ms = 0;  // CUDA events on the pipeline stream
+    long long solve_launches = 0;
     ~spqr_pipeline() {
         if (st) cudaStreamDestroy(st);
     }
@@ -125,8 +127,19 @@ int spqr_pipeline_create(int m, int n, const int* colptr, const int* rowind, con
             FactorizeOptions fo;
             fo.eps = P->eps;
             fo.skip_levels = skip_levels;
+            cudaEvent_t e0, e1;
+            CK(cudaEventCreate(&e0));
+            CK(cudaEventCreate(&e1));
+            CK(cudaEventRecord(e0, P->st));
             P->F = gpu_factorize(P->Aw, P->h, P->owner, fo, P->st);
             P->plan = build_solve_plan(P->F, P->st);
+            CK(cudaEventRecord(e1, P->st));
+            CK(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            P->ev_factorize_ms = ms;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
             P->has_f = true;
             P->t_factorize = now_s() - t0;
         }
@@ -181,6 +194,18 @@ void spqr_pipeline_times(const spqr_pipeline* p, double* t) {
     t[6] = p->F.ctr.cpqr_flops;
     t[7] = p->F.ctr.cpqr_bytes;
     t[8] = static_cast<double>(p->F.ctr.qr_launches);
+    t[9] = p->ev_factorize_ms;
+    t[10] = p->ev_solve_ms;
+    t[11] = static_cast<double>(p->solve_launches);
+    t[12] = static_cast<double>(p->F.ctr.elim_waves);
+}
+
+void spqr_pipeline_kernel_stats(const spqr_pipeline* p, double* ms, double* bytes, long long* launches) {
+    for (int t = 0; t < K_NTAGS; ++t) {
+        ms[t] = p->F.ctr.k_ms[t];
+        bytes[t] = p->F.ctr.k_bytes[t];
+        launches[t] = p->F.ctr.k_launches[t];
+    }
 }
 
 int spqr_pipeline_solve(spqr_pipeline* p, int direct, const double* b, double* x, double tol, int maxit, int* iters,
@@ -193,11 +218,23 @@ int spqr_pipeline_solve(spqr_pipeline* p, int direct, const double* b, double* x
         const double t0 = now_s();
         CK(cudaMemcpyAsync(p->d_b, b, sizeof(double) * m, cudaMemcpyHostToDevice, p->st));
         SolveReport rep;
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, p->st));
         if (direct)
             rep = gpu_csne(p->dA, p->plan, p->d_b, p->d_u, p->refine, p->d_w, p->tol, p->ws, p->st);
         else
             rep = gpu_cgls(p->dA, p->has_f ? &p->plan : nullptr, p->d_b, p->d_u, tol > 0 ? tol : p->tol,
                            maxit > 0 ? maxit : p->maxit, p->d_w, p->ws, p->st);
+        CK(cudaEventRecord(e1, p->st));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        p->ev_solve_ms = ms;
+        p->solve_launches = rep.launches;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
         std::vector<double> u(n);
         CK(cudaMemcpyAsync(u.data(), p->d_u, sizeof(double) * n, cudaMemcpyDeviceToHost, p->st));
         CK(cudaStreamSynchronize(p->st));

@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 
 #include "dev.h"
@@ -94,6 +96,75 @@ void sorted_erase(std::vector<int>& v, int x) {
     auto it = std::lower_bound(v.begin(), v.end(), x);
     if (it != v.end() && *it == x) v.erase(it);
 }
+
+// Host-side profile (SPQR_PROF=1 prints it to stderr after the factorization).
+struct HostProf {
+    enum { INIT, STATS, SYNC, PASS1, SBUILD, PASS2, MATER, SCALE, SROWS, SCOLS, MERGE, UPLOAD, DEPS, FETCH, N };
+    double t[N] = {0};
+    long long n[N] = {0};
+    static const char* name(int i) {
+        static const char* s[N] = {"init", "stats", "sync_wait", "pass1", "stack_build", "pass2", "materialize",
+                                   "scale", "sparsify_rows", "sparsify_cols", "merge", "upload", "deps", "fetch"};
+        return s[i];
+    }
+};
+struct ProfScope {
+    HostProf& p;
+    int i;
+    double t0;
+    ProfScope(HostProf& p_, int i_) : p(p_), i(i_), t0(now_s()) {}
+    ~ProfScope() {
+        p.t[i] += now_s() - t0;
+        p.n[i]++;
+    }
+};
+
+// CUDA-event accounting per kernel family; resolved at every host sync.
+class KTimer {
+public:
+    ~KTimer() {
+        for (auto e : pool_) cudaEventDestroy(e);
+    }
+    cudaEvent_t begin(cudaStream_t st) {
+        cudaEvent_t e = take();
+        CK(cudaEventRecord(e, st));
+        return e;
+    }
+    void end(int tag, cudaEvent_t e0, cudaStream_t st, double bytes) {
+        cudaEvent_t e1 = take();
+        CK(cudaEventRecord(e1, st));
+        pend_.push_back({tag, e0, e1, bytes});
+    }
+    void resolve(EngineCounters& c) {
+        for (auto& p : pend_) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, p.e0, p.e1));
+            c.k_ms[p.tag] += ms;
+            c.k_bytes[p.tag] += p.bytes;
+            c.k_launches[p.tag] += 1;
+        }
+        pend_.clear();
+        used_ = 0;
+    }
+
+private:
+    struct P {
+        int tag;
+        cudaEvent_t e0, e1;
+        double bytes;
+    };
+    std::vector<cudaEvent_t> pool_;
+    std::vector<P> pend_;
+    size_t used_ = 0;
+    cudaEvent_t take() {
+        if (used_ == pool_.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            pool_.push_back(e);
+        }
+        return pool_[used_++];
+    }
+};
 
 // One elimination of the current batch.
 struct Elim {
@@ -210,6 +281,15 @@ private:
     Index npiv_ = 0;
     int batch_ = 0;
     cudaEvent_t ev0_, ev1_;
+    KTimer kt_;
+    HostProf prof_;
+    std::vector<int> waves_per_stage_;
+    struct StageProf {
+        int stage = 0, waves = 0, scol_waves = 0;
+        long long s_elems = 0, s_max_rows = 0, s_max_cols = 0, mat_fronts = 0, mat_rows = 0, mat_elems = 0, elims = 0;
+        long long max_front_rows = 0, max_front_cols = 0;
+    };
+    std::vector<StageProf> sprof_;
     // eliminate-batch state
     std::vector<PFront> pend_;
     std::vector<int> pend_id_, pend_list_;
@@ -229,8 +309,40 @@ private:
     int width(int key) const { return static_cast<int>(cols_[key].size()); }
 
     void sync() {
-        CK(cudaStreamSynchronize(st_));
+        {
+            ProfScope ps(prof_, HostProf::SYNC);
+            CK(cudaStreamSynchronize(st_));
+        }
         pin_.reset();
+        kt_.resolve(out_.ctr);
+        out_.ctr.syncs++;
+    }
+    // batched device->host copies with a single stream sync
+    struct Pending {
+        void* host;
+        void* pin;
+        size_t bytes;
+    };
+    std::vector<Pending> dl_;
+    template <class T>
+    void enqueue(std::vector<T>& h, const T* d, size_t n) {
+        h.resize(n);
+        if (n == 0) return;
+        void* p = pin_.alloc(sizeof(T) * n);
+        CK(cudaMemcpyAsync(p, d, sizeof(T) * n, cudaMemcpyDeviceToHost, st_));
+        dl_.push_back({h.data(), p, sizeof(T) * n});
+        out_.ctr.d2h_bytes += sizeof(T) * n;
+    }
+    void fetch() {
+        ProfScope ps(prof_, HostProf::FETCH);
+        {
+            ProfScope pw(prof_, HostProf::SYNC);
+            CK(cudaStreamSynchronize(st_));
+        }
+        for (auto& q : dl_) std::memcpy(q.host, q.pin, q.bytes);
+        dl_.clear();
+        pin_.reset();
+        kt_.resolve(out_.ctr);
         out_.ctr.syncs++;
     }
     template <class T>
@@ -248,13 +360,16 @@ private:
             b.clear();
             return;
         }
+        ProfScope ps(prof_, HostProf::UPLOAD);
         Uploader u = up();
         const AsmDst* d = u.put(b.dst);
         const int4* rr = u.put(b.rowref);
         const int* cm = u.put(b.cmap);
         const AsmSrc* s = u.put(b.src);
         out_.ctr.h2d_bytes += u.bytes_h2d;
+        cudaEvent_t e0 = kt_.begin(st_);
         launch_assemble(d, static_cast<int>(b.dst.size()), b.elems, rr, cm, s, st_);
+        kt_.end(K_ASSEMBLE, e0, st_, 16.0 * b.elems);
         out_.ctr.launches++;
         b.clear();
     }
@@ -335,6 +450,7 @@ private:
 // factorize.cpp:32-82 — finest fronts, rows ascending into owners, one block
 // per (owner(row), finest(col)) pair seen in A, values scattered on device.
 void Engine::init_fronts(const std::vector<int>& owner) {
+    ProfScope ps_(prof_, HostProf::INIT);
     const int Lf = L_ + 1;
     for (size_t c = 0; c < h_.clusters.size(); ++c)
         if (h_.clusters[c].level == Lf) {
@@ -398,7 +514,9 @@ void Engine::init_fronts(const std::vector<int>& owner) {
     const long long* d_off = u.put(dsto);
     const double* d_val = u.put(A_.x);
     out_.ctr.h2d_bytes += u.bytes_h2d;
+    cudaEvent_t e0 = kt_.begin(st_);
     launch_scatter_values(d_off, d_val, A_.nnz(), slab, st_);
+    kt_.end(K_SCATTER, e0, st_, 24.0 * A_.nnz());
     out_.ctr.launches++;
 }
 
@@ -443,6 +561,7 @@ void Engine::rowval(const PRow& r, int key, double& sq, bool& nz, bool post_ok) 
 // factorize.cpp:176-271 (selection, keyset, stack layout) and :286-418's
 // structural half (pivots, scatter bookkeeping) — values come later.
 void Engine::elim_pass1(Elim& e) {
+    ProfScope ps_(prof_, HostProf::PASS1);
     const int c = e.c;
     const int cs = e.cs;
     e.parts.clear();
@@ -563,6 +682,7 @@ void Engine::elim_pass1(Elim& e) {
 
 // :286-323 (W factor with pruned coupling) and :138-174 (move_extras).
 void Engine::elim_pass2(Elim& e, int eidx) {
+    ProfScope ps_(prof_, HostProf::PASS2);
     const int c = e.c;
     const int cs = e.cs;
     if (cs > 0) {
@@ -647,6 +767,7 @@ void Engine::elim_pass2(Elim& e, int eidx) {
 
 // Materialise every pending (touched, still live) front with one gather.
 void Engine::materialize_pending() {
+    ProfScope ps_(prof_, HostProf::MATER);
     AsmBuilder& b = wcopy_;  // W copies already queued; fronts go in the same launch
     std::vector<std::pair<int, Front>> updates;
     std::vector<int> slot_of_base(fr_.size(), -1);
@@ -672,6 +793,14 @@ void Engine::materialize_pending() {
             same = P.rows[i].base == f && P.rows[i].brow == static_cast<int>(i) && P.rows[i].sidx < 0;
         if (same) continue;
         nf.mat = arena().alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
+        if (!sprof_.empty()) {
+            auto& sp = sprof_.back();
+            sp.mat_fronts++;
+            sp.mat_rows += nf.nrows();
+            sp.mat_elems += static_cast<long long>(nf.nrows()) * nf.ncols;
+            sp.max_front_rows = std::max<long long>(sp.max_front_rows, nf.nrows());
+            sp.max_front_cols = std::max<long long>(sp.max_front_cols, nf.ncols);
+        }
         // sources: distinct bases then distinct stacks
         std::vector<int> bases, stacks;
         for (const PRow& r : P.rows) {
@@ -732,6 +861,7 @@ void Engine::materialize_pending() {
 
 // pre-stage row statistics (sum of squares, any-nonzero) of every block of the fronts in P
 void Engine::compute_stats(const std::vector<int>& P) {
+    ProfScope ps_(prof_, HostProf::STATS);
     std::vector<StatDesc> sd;
     long long work = 0;
     for (int f : P) {
@@ -750,11 +880,16 @@ void Engine::compute_stats(const std::vector<int>& P) {
         Uploader u = up();
         const StatDesc* dd = u.put(sd);
         out_.ctr.h2d_bytes += u.bytes_h2d;
+        double sb = 0;
+        for (auto& q : sd) sb += 8.0 * q.nrows * q.ncols + 9.0 * q.nrows;
+        cudaEvent_t e0 = kt_.begin(st_);
         launch_stats(dd, static_cast<int>(sd.size()), work, d_sq, d_nz, st_);
+        kt_.end(K_STATS, e0, st_, sb);
         out_.ctr.launches++;
     }
-    download(pre_sq_, d_sq, work);
-    download(pre_nz_, d_nz, work);
+    enqueue(pre_sq_, d_sq, work);
+    enqueue(pre_nz_, d_nz, work);
+    fetch();
 }
 
 std::vector<int> Engine::stage_fronts(const std::vector<int>& list) {
@@ -790,6 +925,7 @@ void Engine::eliminate_stage(int k) {
     std::vector<int> lvl(fr_.size(), -1);
     for (int c : list) lvl[c] = 0;
     {
+        ProfScope ps(prof_, HostProf::DEPS);
         std::vector<int> last;
         for (int f : P) {
             const Front& F = fr_[f];
@@ -816,6 +952,8 @@ void Engine::eliminate_stage(int k) {
     std::vector<std::vector<int>> waves(nw);
     for (int c : list) waves[lvl[c]].push_back(c);
     out_.ctr.elim_waves += nw;
+    waves_per_stage_.push_back(nw);
+    sprof_.back().waves = nw;
     const size_t w0 = out_.W.size();
     for (int w = 0; w < nw; ++w) {
         if (w > 0) compute_stats(stage_fronts(waves[w]));
@@ -843,6 +981,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         ++nvalid;
     }
     // gather stacks, QR + apply, post statistics
+    ProfScope ps_sb(prof_, HostProf::SBUILD);
     AsmBuilder sb;
     std::vector<QrDesc> qd;
     std::vector<StatDesc> pd;
@@ -852,6 +991,13 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         Elim& e = el_[ei];
         if (e.cs <= 0) continue;
         e.S = arena().alloc_n<double>(static_cast<size_t>(e.total_rows) * e.tcols);
+        if (!sprof_.empty()) {
+            auto& sp = sprof_.back();
+            sp.s_elems += static_cast<long long>(e.total_rows) * e.tcols;
+            sp.s_max_rows = std::max<long long>(sp.s_max_rows, e.total_rows);
+            sp.s_max_cols = std::max<long long>(sp.s_max_cols, e.tcols);
+            sp.elims++;
+        }
         std::vector<int> bases;
         std::vector<int> slot(0);
         for (const PRow& r : e.srows)
@@ -920,20 +1066,24 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         out_.ctr.h2d_bytes += u.bytes_h2d;
         int maxm = 0;
         for (auto& q : qd) maxm = std::max(maxm, q.m);
-        CK(cudaEventRecord(ev0_, st_));
+        double qb = 0;
+        for (auto& q : qd) qb += 16.0 * q.m * q.ntot;
+        cudaEvent_t e0 = kt_.begin(st_);
         launch_qr(dq, static_cast<int>(qd.size()), maxm, st_);
-        CK(cudaEventRecord(ev1_, st_));
+        kt_.end(K_QR, e0, st_, qb);
         out_.ctr.launches++;
         out_.ctr.qr_launches++;
+        double sb = 0;
+        for (auto& q : pd) sb += 8.0 * q.nrows * q.ncols + 9.0;
+        e0 = kt_.begin(st_);
         launch_stats(dp, static_cast<int>(pd.size()), pwork, d_psq, d_pnz, st_);
+        kt_.end(K_STATS, e0, st_, sb);
         out_.ctr.launches++;
         std::vector<int> flags;
-        download(flags, d_flags, flags_init.size());
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev0_, ev1_));
-        out_.ctr.t_qr_ms += ms;
-        download(post_sq_, d_psq, postlen);
-        download(post_nz_, d_pnz, postlen);
+        enqueue(flags, d_flags, flags_init.size());
+        enqueue(post_sq_, d_psq, postlen);
+        enqueue(post_nz_, d_pnz, postlen);
+        fetch();
         // first error in ascending order (singular pivot precedes a later "rows couple")
         for (size_t i = 0, qi = 0; i < static_cast<size_t>(nvalid); ++i)
             if (el_[i].cs > 0) {
@@ -952,6 +1102,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
 
 // factorize.cpp:425-486
 void Engine::scale_all() {
+    ProfScope ps_(prof_, HostProf::SCALE);
     std::vector<int> cand;
     std::vector<StatDesc> sd;
     for (size_t p = 0; p < fr_.size(); ++p) {
@@ -981,7 +1132,11 @@ void Engine::scale_all() {
         Uploader u = up();
         const StatDesc* dd = u.put(sd);
         out_.ctr.h2d_bytes += u.bytes_h2d;
+        double sb = 0;
+        for (auto& q : sd) sb += 8.0 * q.nrows * q.ncols;
+        cudaEvent_t e0 = kt_.begin(st_);
         launch_stats(dd, static_cast<int>(sd.size()), static_cast<long long>(sd.size()), d_sq, d_nz, st_);
+        kt_.end(K_STATS, e0, st_, sb);
         out_.ctr.launches++;
     }
     std::vector<unsigned char> ident;
@@ -1025,18 +1180,20 @@ void Engine::scale_all() {
         out_.ctr.h2d_bytes += u.bytes_h2d;
         int maxm = 0;
         for (auto& q : qd) maxm = std::max(maxm, q.m);
-        CK(cudaEventRecord(ev0_, st_));
+        double qb = 0, tb = 0;
+        for (auto& q : qd) qb += 16.0 * q.m * q.ntot;
+        for (auto& t : td) tb += 16.0 * t.nrows * t.n;
+        cudaEvent_t e0 = kt_.begin(st_);
         launch_qr(dq, static_cast<int>(qd.size()), maxm, st_);
-        CK(cudaEventRecord(ev1_, st_));
+        kt_.end(K_QR, e0, st_, qb);
         out_.ctr.launches++;
         out_.ctr.qr_launches++;
+        e0 = kt_.begin(st_);
         launch_trsm(dt, static_cast<int>(td.size()), trows, st_);
+        kt_.end(K_TRSM, e0, st_, tb);
         out_.ctr.launches++;
         std::vector<int> flags;
         download(flags, d_flags, flags_init.size());
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev0_, ev1_));
-        out_.ctr.t_qr_ms += ms;
         for (size_t i = 0; i < flags.size(); ++i)
             if (flags[i] != INT_MAX) {
                 if (err_cluster_ < 0 || qp[i] < err_cluster_) {
@@ -1051,6 +1208,7 @@ void Engine::scale_all() {
 
 // factorize.cpp:488-537 — CPQR of every front's extra rows against its neighbours.
 void Engine::sparsify_rows_all() {
+    ProfScope ps_(prof_, HostProf::SROWS);
     struct Job {
         int p, cs, p2, nw, c0;
         double* B;
@@ -1101,7 +1259,11 @@ void Engine::sparsify_rows_all() {
         Uploader u = up();
         const CpqrDesc* dc = u.put(cd);
         out_.ctr.h2d_bytes += u.bytes_h2d;
+        double cb = 0;
+        for (auto& q : cd) cb += 16.0 * q.m * q.n;
+        cudaEvent_t e0 = kt_.begin(st_);
         launch_cpqr(dc, static_cast<int>(cd.size()), maxm, st_);
+        kt_.end(K_CPQR, e0, st_, cb);
         out_.ctr.launches++;
     }
     std::vector<int> rank;
@@ -1129,6 +1291,7 @@ void Engine::sparsify_rows_all() {
 // DAG whose edges join fronts that hold each other's key (the only way one
 // interface's step reads what another writes).
 void Engine::sparsify_cols_all() {
+    ProfScope ps_(prof_, HostProf::SCOLS);
     std::vector<int> elig;
     for (size_t p = 0; p < fr_.size(); ++p)
         if (fr_[p].live && width(static_cast<int>(p)) > 0 && fr_[p].scaled_ok) elig.push_back(static_cast<int>(p));
@@ -1146,6 +1309,7 @@ void Engine::sparsify_cols_all() {
     }
     std::vector<std::vector<int>> waves(nwaves);
     for (int p : elig) waves[level[p]].push_back(p);
+    if (!sprof_.empty()) sprof_.back().scol_waves = nwaves;
     const int rot_batch = batch_;
     const size_t w0 = out_.W.size();
     for (auto& wave : waves) {
@@ -1218,7 +1382,11 @@ void Engine::sparsify_cols_all() {
             Uploader u = up();
             const CpqrDesc* dc = u.put(cd);
             out_.ctr.h2d_bytes += u.bytes_h2d;
-            launch_cpqr(dc, static_cast<int>(cd.size()), maxm, st_);
+            double cb = 0;
+        for (auto& q : cd) cb += 16.0 * q.m * q.n;
+        cudaEvent_t e0 = kt_.begin(st_);
+        launch_cpqr(dc, static_cast<int>(cd.size()), maxm, st_);
+        kt_.end(K_CPQR, e0, st_, cb);
             out_.ctr.launches++;
         }
         std::vector<int> rank;
@@ -1367,6 +1535,7 @@ void Engine::sparsify_cols_all() {
 // factorize.cpp:635-729 — children concatenate into parents; every live front
 // is rebuilt into the other arena (pivot rows of all children first).
 void Engine::merge_level() {
+    ProfScope ps_(prof_, HostProf::MERGE);
     std::map<int, std::vector<int>> groups;
     for (size_t c = 0; c < fr_.size(); ++c)
         if (fr_[c].live) groups[h_.clusters[c].parent].push_back(static_cast<int>(c));
@@ -1456,8 +1625,7 @@ void Engine::merge_level() {
         for (const KeyRef& k : fr_[P].keys) sorted_insert(holders_[k.key], P);
     }
     // everything of this stage lived in arena cur_; the next stage starts clean
-    CK(cudaStreamSynchronize(st_));
-    pin_.reset();
+    sync();
     arena_[cur_].reset();
     cur_ ^= 1;
 }
@@ -1482,6 +1650,8 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
     for (int k = L_ + 1; k >= 1; --k) {
         StageStats st;
         st.stage = k;
+        sprof_.emplace_back();
+        sprof_.back().stage = k;
         double t0 = now_s();
         eliminate_stage(k);
         st.t_eliminate = now_s() - t0;
@@ -1507,7 +1677,21 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
     }
     for (size_t c = 0; c < fr_.size(); ++c)
         if (fr_[c].live) out_.trailing_rows.insert(out_.trailing_rows.end(), fr_[c].rows.begin(), fr_[c].rows.end());
-    CK(cudaStreamSynchronize(st_));
+    sync();
+    out_.ctr.t_qr_ms = out_.ctr.k_ms[K_QR];
+    if (std::getenv("SPQR_PROF")) {
+        for (int i = 0; i < HostProf::N; ++i)
+            std::fprintf(stderr, "[spqr prof] %-14s %8.3f s  (%lld)\n", HostProf::name(i), prof_.t[i], prof_.n[i]);
+        for (auto& sp : sprof_)
+            std::fprintf(stderr,
+                         "[spqr prof] stage %2d waves %3d scol_waves %3d elims %6lld S_elems %10lld S_max %lldx%lld | "
+                         "mat fronts %7lld rows %9lld elems %11lld max %lldx%lld\n",
+                         sp.stage, sp.waves, sp.scol_waves, sp.elims, sp.s_elems, sp.s_max_rows, sp.s_max_cols, sp.mat_fronts,
+                         sp.mat_rows, sp.mat_elems, sp.max_front_rows, sp.max_front_cols);
+        for (int t = 0; t < K_NTAGS; ++t)
+            std::fprintf(stderr, "[spqr prof] kernel %-9s %8.2f ms %6lld launches %10.1f MB\n", ktag_name(t), out_.ctr.k_ms[t],
+                         out_.ctr.k_launches[t], out_.ctr.k_bytes[t] / 1e6);
+    }
     return std::move(out_);
 }
 

@@ -24,7 +24,16 @@ struct DevWFactor {
     double* sign = nullptr;
 };
 
+enum KTag { K_ASSEMBLE = 0, K_STATS, K_QR, K_TRSM, K_CPQR, K_SCATTER, K_NTAGS };
+inline const char* ktag_name(int t) {
+    static const char* n[K_NTAGS] = {"assemble", "stats", "front_qr", "trsm", "cpqr", "scatter"};
+    return n[t];
+}
+
 struct EngineCounters {
+    double k_ms[K_NTAGS] = {0};       // device time per kernel family (CUDA events on the engine stream)
+    double k_bytes[K_NTAGS] = {0};    // algorithmic HBM bytes (read + write) per kernel family
+    long long k_launches[K_NTAGS] = {0};
     long long launches = 0, syncs = 0, h2d_bytes = 0, d2h_bytes = 0;
     double qr_flops = 0, qr_bytes = 0, cpqr_flops = 0, cpqr_bytes = 0;  // algorithmic work (BASELINE.md formulas)
     double t_qr_ms = 0;  // device time of the batched front-QR launches (CUDA events)

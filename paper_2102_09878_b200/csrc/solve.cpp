@@ -76,15 +76,20 @@ SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
     return P;
 }
 
-void sweep(const SolvePlan& P, SweepMode mode, double* d_z, cudaStream_t st) {
+long long sweep(const SolvePlan& P, SweepMode mode, double* d_z, cudaStream_t st) {
+    long long L = 0;
     const int nb = static_cast<int>(P.batches.size());
     const bool forward = (mode == kWtSolve || mode == kWApply);  // chronological order
     for (int q = 0; q < nb; ++q) {
         const auto& b = P.batches[forward ? q : nb - 1 - q];
         launch_wsweep(b.fac, b.nf, d_z, P.contrib, static_cast<int>(mode), b.maxc, st);
-        if ((mode == kWtSolve || mode == kWtApply) && b.ncol > 0)
+        ++L;
+        if ((mode == kWtSolve || mode == kWtApply) && b.ncol > 0) {
             launch_wreduce(b.rptr, b.ridx, b.rcol, b.ncol, P.contrib, d_z, mode == kWtSolve ? -1.0 : 1.0, st);
+            ++L;
+        }
     }
+    return L;
 }
 
 DevMatrix upload_matrix(const Csc& A, cudaStream_t st) {
@@ -174,7 +179,7 @@ SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, 
     }
     rep.residual_history.push_back(1.0);
     launch_copy(n, ws.t, ws.s, st);
-    if (W) sweep(*W, kWtSolve, ws.s, st);
+    if (W) L += sweep(*W, kWtSolve, ws.s, st);
     launch_copy(n, ws.s, ws.p, st);
     CK(cudaMemsetAsync(ws.y, 0, sizeof(double) * n, st));
     double* gamma = sc + 1;
@@ -188,7 +193,7 @@ SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, 
     CK(cudaMallocHost(reinterpret_cast<void**>(&hpin), 2 * sizeof(double)));
     for (int it = 1; it <= maxit; ++it) {
         launch_copy(n, ws.p, ws.v, st);
-        if (W) sweep(*W, kWSolve, ws.v, st);
+        if (W) L += sweep(*W, kWSolve, ws.v, st);
         launch_spmv_csr(m, A.rp, A.ri, A.rv, ws.v, ws.q, st);  // q = A v
         dots.norm2(m, ws.q, nullptr, sc + 3);
         launch_cgls_alpha(gamma, sc + 3, sc + 4, ws.brk, st);
@@ -211,7 +216,7 @@ SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, 
             break;
         }
         launch_copy(n, ws.t, ws.s, st);
-        if (W) sweep(*W, kWtSolve, ws.s, st);
+        if (W) L += sweep(*W, kWtSolve, ws.s, st);
         dots.norm2(n, ws.s, nullptr, gnew);
         launch_cgls_p_update(n, ws.s, gnew, gamma, ws.p, st);
         L += 3;
@@ -219,7 +224,7 @@ SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, 
     }
     cudaFreeHost(hpin);
     launch_copy(n, ws.y, d_u, st);
-    if (W) sweep(*W, kWSolve, d_u, st);
+    if (W) L += sweep(*W, kWSolve, d_u, st);
     CK(cudaStreamSynchronize(st));
     rep.t_solve = now_s() - t0;
     rep.launches = L;

@@ -28,7 +28,7 @@ struct SolvePlan {
 SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st);
 
 enum SweepMode { kWSolve = 0, kWtSolve = 1, kWApply = 2, kWtApply = 3 };
-void sweep(const SolvePlan& P, SweepMode mode, double* d_z, cudaStream_t st);
+long long sweep(const SolvePlan& P, SweepMode mode, double* d_z, cudaStream_t st);  // returns launches
 
 // A on the device in both orientations (row dots for A x and A^T y).
 struct DevMatrix {
