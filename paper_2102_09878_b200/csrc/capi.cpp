@@ -409,7 +409,15 @@ int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* ra
                              work + static_cast<long long>(b) * 3 * n};
         CpqrDesc* dc = mem.alloc_n<CpqrDesc>(std::max(nb, 1));
         CK(cudaMemcpy(dc, cd.data(), sizeof(CpqrDesc) * nb, cudaMemcpyHostToDevice));
-        launch_cpqr(dc, nb, m, 0);
+        std::vector<int> all(nb);
+        for (int b = 0; b < nb; ++b) all[b] = b;
+        int* didx = mem.alloc_n<int>(std::max(nb, 1));
+        CK(cudaMemcpy(didx, all.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
+        const size_t sm = cpqr_smem_bytes(m, n);
+        if (sm <= kSmemBudget)
+            launch_cpqr_split(dc, didx, nb, sm, nullptr, 0, m, 0);
+        else
+            launch_cpqr_split(dc, nullptr, 0, 0, didx, nb, m, 0);
         CK(cudaDeviceSynchronize());
         CK(cudaGetLastError());
         std::vector<double> A(na);

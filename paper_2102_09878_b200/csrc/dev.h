@@ -15,25 +15,26 @@
 namespace spqr {
 
 // ---- generic gather ("assemble"): builds a destination matrix from rows of
-// up to a few source matrices.  dst(i,j) =
-//   primary   src[s1](r1, cmap[j*nsrc+s1])  if s1 >= 0 and that column >= 0
-//   otherwise src[s2](r2, cmap[j*nsrc+s2])  if s2 >= 0 and that column >= 0
-//   otherwise 0.
-// rowref = (s1, r1, s2, r2).  s1 == -2 selects scan mode: the first slot t
-// whose cmap entry for column j is mapped supplies row r1.  A cmap entry
-// c <= -2 encodes an identity column: value 1 on dst row (-c-2), else 0.
-// Covers stack gathers, scatter-back, row appends, merges, transposed copies
-// (element (i,j) of a source lives at p[i*rs + j*cs]).
+// up to a few source matrices.  The destination's columns are split into
+// segments (seg_off[q] <= j < seg_off[q+1]); kmap[q*nsrc + t] gives the
+// first source column of segment q in source slot t (-1: unmapped, -2: the
+// segment is an identity block, value 1 on dst row == offset in segment).
+// rowref = (s1, r1, s2, r2): dst(i,j) comes from slot s1 row r1 if that
+// slot maps j's segment, else from slot s2 row r2, else 0.  s1 == -2 selects
+// scan mode: the first slot mapping the segment supplies row r1.
+// Covers stack gathers, scatter-back, row appends, merges and transposed
+// copies (element (r,c) of a source lives at p[r*rs + c*cs]).
 struct AsmSrc {
     const double* p;
     long long rs, cs;
 };
 struct AsmDst {
     double* p;
-    int ld, nrows, ncols, nsrc;
+    int ld, nrows, ncols, nsrc, nseg;
     int trans;           // 1: (nrows x ncols) is the logical view; stored transposed (p[j + i*ld])
-    long long row_off;   // into rowref (int4 per dst row)
-    long long cmap_off;  // into cmap (ncols * nsrc)
+    long long row_off;   // into rowref (int4 per logical row)
+    long long seg_off;   // into segoff (nseg + 1 ints)
+    long long kmap_off;  // into kmap (nseg * nsrc)
     long long src_off;   // into src table
     long long elem_off;  // exclusive prefix of nrows*ncols (work split)
 };
@@ -91,13 +92,21 @@ struct CpqrDesc {
 };
 
 // launchers (kernels.cu); all enqueue on `st`
-void launch_assemble(const AsmDst* d_dst, int ndst, long long total_elems, const int4* d_rowref, const int* d_cmap,
-                     const AsmSrc* d_src, cudaStream_t st);
+void launch_assemble(const AsmDst* d_dst, int ndst, long long total_elems, const int4* d_rowref, const int* d_segoff,
+                     const int* d_kmap, const AsmSrc* d_src, cudaStream_t st);
 void launch_stats(const StatDesc* d, int nd, long long total_work, double* out_sq, unsigned char* out_nz,
                   cudaStream_t st);
 void launch_qr(const QrDesc* d, int nd, int max_m, cudaStream_t st);
+// Size-split launches: problems listed in d_small are staged in shared memory
+// (smem_small = the largest staged footprint), the rest run in place in HBM.
+constexpr size_t kSmemBudget = 100 * 1024;  // two CTAs per SM
+inline size_t qr_smem_bytes(int m, int n, int ntot) { return 8ull * (static_cast<size_t>(m) * ntot + n); }
+inline size_t cpqr_smem_bytes(int m, int n) { return 8ull * (static_cast<size_t>(m) * n + 2ull * n + m) + 4ull * n + 16; }
+void launch_qr_split(const QrDesc* d_desc, const int* d_small, int n_small, size_t smem_small, const int* d_large,
+                     int n_large, cudaStream_t st);
+void launch_cpqr_split(const CpqrDesc* d_desc, const int* d_small, int n_small, size_t smem_small, const int* d_large,
+                       int n_large, int max_m_large, cudaStream_t st);
 void launch_trsm(const TrsmDesc* d, int nd, long long total_rows, cudaStream_t st);
-void launch_cpqr(const CpqrDesc* d, int nd, int max_m, cudaStream_t st);
 void launch_scatter_values(const long long* off, const double* val, long long n, double* base, cudaStream_t st);
 
 // W-sweep kernels (solve) ------------------------------------------------------

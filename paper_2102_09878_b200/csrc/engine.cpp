@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <iterator>
 #include <map>
 
 #include "dev.h"
@@ -108,6 +109,22 @@ struct HostProf {
         return s[i];
     }
 };
+// named fine-grained scopes (string literals as keys)
+struct NamedProf {
+    std::vector<std::pair<const char*, double>> v;
+    double& slot(const char* n) {
+        for (auto& p : v)
+            if (p.first == n) return p.second;
+        v.emplace_back(n, 0.0);
+        return v.back().second;
+    }
+};
+struct NScope {
+    double& t;
+    double t0;
+    NScope(NamedProf& p, const char* n) : t(p.slot(n)), t0(now_s()) {}
+    ~NScope() { t += now_s() - t0; }
+};
 struct ProfScope {
     HostProf& p;
     int i;
@@ -184,35 +201,43 @@ struct Elim {
 struct AsmBuilder {
     std::vector<AsmDst> dst;
     std::vector<int4> rowref;
-    std::vector<int> cmap;
+    std::vector<int> segoff, kmap;
     std::vector<AsmSrc> src;
     long long elems = 0;
-    // begin a destination; returns index
-    int begin(double* p, int ld, int nrows, int ncols, int nsrc) {
+    int begin(double* p, int ld, int nrows, int ncols, int nsrc, int nseg) {
         AsmDst d;
         d.p = p;
         d.ld = ld;
         d.nrows = nrows;
         d.ncols = ncols;
         d.nsrc = nsrc;
+        d.nseg = std::max(nseg, 1);
         d.trans = 0;
         d.row_off = static_cast<long long>(rowref.size());
-        d.cmap_off = static_cast<long long>(cmap.size());
+        d.seg_off = static_cast<long long>(segoff.size());
+        d.kmap_off = static_cast<long long>(kmap.size());
         d.src_off = static_cast<long long>(src.size());
         d.elem_off = elems;
         elems += static_cast<long long>(nrows) * ncols;
         rowref.resize(rowref.size() + nrows, int4{-1, 0, -1, 0});
-        cmap.resize(cmap.size() + static_cast<size_t>(ncols) * nsrc, -1);
+        segoff.resize(segoff.size() + d.nseg + 1, 0);
+        segoff[d.seg_off + d.nseg] = ncols;
+        kmap.resize(kmap.size() + static_cast<size_t>(d.nseg) * nsrc, -1);
         src.resize(src.size() + nsrc);
         dst.push_back(d);
         return static_cast<int>(dst.size()) - 1;
     }
+    void seg(int di, int q, int start) { segoff[dst[di].seg_off + q] = start; }
+    int& km(int di, int q, int s) { return kmap[dst[di].kmap_off + static_cast<long long>(q) * dst[di].nsrc + s]; }
+    int4& row(int di, int i) { return rowref[dst[di].row_off + i]; }
+    AsmSrc& source(int di, int s) { return src[dst[di].src_off + s]; }
     void drop_if_empty() {
         if (!dst.empty() && (dst.back().nrows == 0 || dst.back().ncols == 0)) {
             const AsmDst d = dst.back();
             elems = d.elem_off;
             rowref.resize(d.row_off);
-            cmap.resize(d.cmap_off);
+            segoff.resize(d.seg_off);
+            kmap.resize(d.kmap_off);
             src.resize(d.src_off);
             dst.pop_back();
         }
@@ -220,11 +245,19 @@ struct AsmBuilder {
     void clear() {
         dst.clear();
         rowref.clear();
-        cmap.clear();
+        segoff.clear();
+        kmap.clear();
         src.clear();
         elems = 0;
     }
 };
+
+// key indices of a front in physical column order
+inline void phys_order(const std::vector<KeyRef>& keys, std::vector<int>& ord) {
+    ord.resize(keys.size());
+    for (size_t i = 0; i < keys.size(); ++i) ord[i] = static_cast<int>(i);
+    std::sort(ord.begin(), ord.end(), [&](int a, int b) { return keys[a].col < keys[b].col; });
+}
 
 class Engine {
 public:
@@ -283,6 +316,7 @@ private:
     cudaEvent_t ev0_, ev1_;
     KTimer kt_;
     HostProf prof_;
+    NamedProf nprof_;
     std::vector<int> waves_per_stage_;
     struct StageProf {
         int stage = 0, waves = 0, scol_waves = 0;
@@ -290,6 +324,7 @@ private:
         long long max_front_rows = 0, max_front_cols = 0;
     };
     std::vector<StageProf> sprof_;
+    int spec_depth_ = std::getenv("SPQR_SPEC_DEPTH") ? std::atoi(std::getenv("SPQR_SPEC_DEPTH")) : 3;
     // eliminate-batch state
     std::vector<PFront> pend_;
     std::vector<int> pend_id_, pend_list_;
@@ -364,11 +399,12 @@ private:
         Uploader u = up();
         const AsmDst* d = u.put(b.dst);
         const int4* rr = u.put(b.rowref);
-        const int* cm = u.put(b.cmap);
+        const int* so = u.put(b.segoff);
+        const int* km = u.put(b.kmap);
         const AsmSrc* s = u.put(b.src);
         out_.ctr.h2d_bytes += u.bytes_h2d;
         cudaEvent_t e0 = kt_.begin(st_);
-        launch_assemble(d, static_cast<int>(b.dst.size()), b.elems, rr, cm, s, st_);
+        launch_assemble(d, static_cast<int>(b.dst.size()), b.elems, rr, so, km, s, st_);
         kt_.end(K_ASSEMBLE, e0, st_, 16.0 * b.elems);
         out_.ctr.launches++;
         b.clear();
@@ -400,6 +436,49 @@ private:
     }
 
     void init_fronts(const std::vector<int>& owner);
+    // size-split batched launches (shared-memory staged when the block fits)
+    void run_qr(const std::vector<QrDesc>& qd, const QrDesc* dq, Uploader& u) {
+        std::vector<int> small, large;
+        size_t smem = 0;
+        for (size_t i = 0; i < qd.size(); ++i) {
+            const size_t b = qr_smem_bytes(qd[i].m, qd[i].n, qd[i].ntot);
+            if (b <= kSmemBudget && qd[i].n <= 1024) {
+                small.push_back(static_cast<int>(i));
+                smem = std::max(smem, b);
+            } else {
+                large.push_back(static_cast<int>(i));
+            }
+        }
+        const int* ds = u.put(small);
+        const int* dl = u.put(large);
+        double qb = 0;
+        for (auto& q : qd) qb += 16.0 * q.m * q.ntot;
+        cudaEvent_t e0 = kt_.begin(st_);
+        launch_qr_split(dq, ds, static_cast<int>(small.size()), smem, dl, static_cast<int>(large.size()), st_);
+        kt_.end(K_QR, e0, st_, qb);
+    }
+    void run_cpqr(const std::vector<CpqrDesc>& cd, const CpqrDesc* dc, Uploader& u) {
+        std::vector<int> small, large;
+        size_t smem = 0;
+        int maxm = 1;
+        for (size_t i = 0; i < cd.size(); ++i) {
+            const size_t b = cpqr_smem_bytes(cd[i].m, cd[i].n);
+            if (b <= kSmemBudget) {
+                small.push_back(static_cast<int>(i));
+                smem = std::max(smem, b);
+            } else {
+                large.push_back(static_cast<int>(i));
+                maxm = std::max(maxm, cd[i].m);
+            }
+        }
+        const int* ds = u.put(small);
+        const int* dl = u.put(large);
+        double cb = 0;
+        for (auto& q : cd) cb += 16.0 * q.m * q.n;
+        cudaEvent_t e0 = kt_.begin(st_);
+        launch_cpqr_split(dc, ds, static_cast<int>(small.size()), smem, dl, static_cast<int>(large.size()), maxm, st_);
+        kt_.end(K_CPQR, e0, st_, cb);
+    }
     void eliminate_stage(int k);
     void eliminate_wave(const std::vector<int>& list);
     void compute_stats(const std::vector<int>& P);
@@ -538,9 +617,10 @@ void Engine::rowval(const PRow& r, int key, double& sq, bool& nz, bool post_ok) 
             if (!post_ok || e.post_off < 0 || r.srow < e.cs || r.srow >= e.nsel_c)
                 throw std::logic_error("spaqr engine: a row stacked twice within one stage (invariant violated)");
             const int ki = static_cast<int>(it - e.keys.begin());
-            // post layout per elim: [blockmax all][blockmax key 1..][rows x keys 1..]
+            // post layout per elim: [blockmax all][blockmax key 1..nk][key 1..nk x own non-pivot rows]
             const long long nk = static_cast<long long>(e.keys.size()) - 1;
-            const long long o = e.post_off + 1 + nk + static_cast<long long>(r.srow - e.cs) * nk + (ki - 1);
+            const long long nown = e.nsel_c - e.cs;
+            const long long o = e.post_off + 1 + nk + static_cast<long long>(ki - 1) * nown + (r.srow - e.cs);
             sq = post_sq_[o];
             nz = post_nz_[o];
             return;
@@ -705,14 +785,17 @@ void Engine::elim_pass2(Elim& e, int eidx) {
         DevWFactor& f = new_factor(0, c, cs, kept, cols_[c], &coupled);
         f.a = out_.warena->alloc_n<double>(static_cast<size_t>(cs) * (cs + kept));
         // copy [R | C_kept] from the stack (rows 0..cs-1)
-        wcopy_.begin(f.a, cs, cs, cs + kept, 1);
-        AsmDst& d = wcopy_.dst.back();
-        wcopy_.src[d.src_off] = AsmSrc{e.S, 1, e.total_rows};
-        for (int i = 0; i < cs; ++i) wcopy_.rowref[d.row_off + i] = int4{-1, 0, 0, i};
-        int o = 0;
-        for (int j = 0; j < cs; ++j) wcopy_.cmap[d.cmap_off + o++] = j;
-        for (int ki : keepk)
-            for (int j = 0; j < width(e.keys[ki]); ++j) wcopy_.cmap[d.cmap_off + o++] = e.off[ki] + j;
+        const int di = wcopy_.begin(f.a, cs, cs, cs + kept, 1, 1 + static_cast<int>(keepk.size()));
+        wcopy_.source(di, 0) = AsmSrc{e.S, 1, e.total_rows};
+        for (int i = 0; i < cs; ++i) wcopy_.row(di, i) = int4{-1, 0, 0, i};
+        wcopy_.seg(di, 0, 0);
+        wcopy_.km(di, 0, 0) = 0;
+        int o = cs;
+        for (size_t q = 0; q < keepk.size(); ++q) {
+            wcopy_.seg(di, static_cast<int>(q) + 1, o);
+            wcopy_.km(di, static_cast<int>(q) + 1, 0) = e.off[keepk[q]];
+            o += width(e.keys[keepk[q]]);
+        }
     }
     // move_extras
     PFront& fc = pend(c);
@@ -768,6 +851,7 @@ void Engine::elim_pass2(Elim& e, int eidx) {
 // Materialise every pending (touched, still live) front with one gather.
 void Engine::materialize_pending() {
     ProfScope ps_(prof_, HostProf::MATER);
+    std::unique_ptr<NScope> mt1 = std::make_unique<NScope>(nprof_, "mat.descriptors");
     AsmBuilder& b = wcopy_;  // W copies already queued; fronts go in the same launch
     std::vector<std::pair<int, Front>> updates;
     std::vector<int> slot_of_base(fr_.size(), -1);
@@ -811,45 +895,48 @@ void Engine::materialize_pending() {
             if (r.sidx >= 0 && std::find(stacks.begin(), stacks.end(), r.sidx) == stacks.end()) stacks.push_back(r.sidx);
         }
         const int nsrc = static_cast<int>(bases.size() + stacks.size());
-        const int di = b.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, std::max(nsrc, 1));
-        AsmDst& d = b.dst[di];
+        std::vector<int> ord;
+        phys_order(nf.keys, ord);
+        const int di = b.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, std::max(nsrc, 1), static_cast<int>(ord.size()));
         for (size_t s = 0; s < bases.size(); ++s) {
             const Front& B = fr_[bases[s]];
-            b.src[d.src_off + s] = AsmSrc{B.mat, 1, B.ld};
+            b.source(di, static_cast<int>(s)) = AsmSrc{B.mat, 1, B.ld};
         }
         for (size_t s = 0; s < stacks.size(); ++s) {
             const Elim& E = el_[stacks[s]];
-            b.src[d.src_off + bases.size() + s] = AsmSrc{E.S, 1, E.total_rows};
+            b.source(di, static_cast<int>(bases.size() + s)) = AsmSrc{E.S, 1, E.total_rows};
         }
         for (size_t i = 0; i < P.rows.size(); ++i) {
             const PRow& r = P.rows[i];
             int s1 = -1;
             if (r.sidx >= 0)
                 s1 = static_cast<int>(bases.size() + (std::find(stacks.begin(), stacks.end(), r.sidx) - stacks.begin()));
-            b.rowref[d.row_off + i] = int4{s1, r.srow, slot_of_base[r.base], r.brow};
+            b.row(di, static_cast<int>(i)) = int4{s1, r.srow, slot_of_base[r.base], r.brow};
         }
-        for (const KeyRef& k : nf.keys) {
+        for (size_t q = 0; q < ord.size(); ++q) {
+            const KeyRef& k = nf.keys[ord[q]];
+            b.seg(di, static_cast<int>(q), k.col);
             for (size_t s = 0; s < bases.size(); ++s) {
                 const Front& B = fr_[bases[s]];
                 const int qi = B.find(k.key);
-                if (qi < 0) continue;
-                for (int o = 0; o < k.width; ++o)
-                    b.cmap[d.cmap_off + static_cast<long long>(k.col + o) * nsrc + s] = B.keys[qi].col + o;
+                if (qi >= 0) b.km(di, static_cast<int>(q), static_cast<int>(s)) = B.keys[qi].col;
             }
             for (size_t s = 0; s < stacks.size(); ++s) {
                 const Elim& E = el_[stacks[s]];
                 auto it = std::lower_bound(E.keys.begin() + 1, E.keys.end(), k.key);
                 if (it == E.keys.end() || *it != k.key) continue;
-                const int ki = static_cast<int>(it - E.keys.begin());
-                for (int o = 0; o < k.width; ++o)
-                    b.cmap[d.cmap_off + static_cast<long long>(k.col + o) * nsrc + bases.size() + s] = E.off[ki] + o;
+                b.km(di, static_cast<int>(q), static_cast<int>(bases.size() + s)) = E.off[it - E.keys.begin()];
             }
         }
         b.drop_if_empty();
         for (int bb : bases) slot_of_base[bb] = -1;
         updates.emplace_back(f, std::move(nf));
     }
+    mt1.reset();
+    std::unique_ptr<NScope> mt2 = std::make_unique<NScope>(nprof_, "mat.flush");
     flush_assemble(b);
+    mt2.reset();
+    NScope mt3(nprof_, "mat.swap");
     for (auto& [f, nf] : updates) {
         nf.soff.clear();
         fr_[f] = std::move(nf);
@@ -982,6 +1069,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
     }
     // gather stacks, QR + apply, post statistics
     ProfScope ps_sb(prof_, HostProf::SBUILD);
+    std::unique_ptr<NScope> sb_desc = std::make_unique<NScope>(nprof_, "sb.descriptors");
     AsmBuilder sb;
     std::vector<QrDesc> qd;
     std::vector<StatDesc> pd;
@@ -999,26 +1087,24 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
             sp.elims++;
         }
         std::vector<int> bases;
-        std::vector<int> slot(0);
         for (const PRow& r : e.srows)
             if (std::find(bases.begin(), bases.end(), r.base) == bases.end()) bases.push_back(r.base);
         const int nsrc = static_cast<int>(bases.size());
-        const int di = sb.begin(e.S, e.total_rows, e.total_rows, e.tcols, nsrc);
-        AsmDst& d = sb.dst[di];
-        for (int s = 0; s < nsrc; ++s) sb.src[d.src_off + s] = AsmSrc{fr_[bases[s]].mat, 1, fr_[bases[s]].ld};
+        const int di = sb.begin(e.S, e.total_rows, e.total_rows, e.tcols, nsrc, static_cast<int>(e.keys.size()));
+        for (int s = 0; s < nsrc; ++s) sb.source(di, s) = AsmSrc{fr_[bases[s]].mat, 1, fr_[bases[s]].ld};
         for (int i = 0; i < e.total_rows; ++i) {
             const PRow& r = e.srows[i];
             const int s = static_cast<int>(std::find(bases.begin(), bases.end(), r.base) - bases.begin());
-            sb.rowref[d.row_off + i] = int4{-1, 0, s, r.brow};
+            sb.row(di, i) = int4{-1, 0, s, r.brow};
         }
-        for (size_t ki = 0; ki < e.keys.size(); ++ki)
+        for (size_t ki = 0; ki < e.keys.size(); ++ki) {
+            sb.seg(di, static_cast<int>(ki), e.off[ki]);
             for (int s = 0; s < nsrc; ++s) {
                 const Front& B = fr_[bases[s]];
                 const int qi = B.find(e.keys[ki]);
-                if (qi < 0) continue;
-                for (int o = 0; o < width(e.keys[ki]); ++o)
-                    sb.cmap[d.cmap_off + static_cast<long long>(e.off[ki] + o) * nsrc + s] = B.keys[qi].col + o;
+                if (qi >= 0) sb.km(di, static_cast<int>(ki), s) = B.keys[qi].col;
             }
+        }
         flags_init.push_back(INT_MAX);
         QrDesc q{e.S, e.total_rows, e.total_rows, e.cs, e.tcols, nullptr, nullptr, nullptr, nullptr, 0, 1};
         qd.push_back(q);
@@ -1039,17 +1125,19 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
             postlen += 1;
         }
         const int nown = std::max(0, e.nsel_c - e.cs);
-        for (int r = 0; r < nown; ++r)
-            for (long long ki = 1; ki <= nk; ++ki) {
-                pd.push_back(StatDesc{e.S, e.total_rows, e.cs + r, 1, e.off[ki], width(e.keys[ki]), 0, postlen, pwork});
-                pwork += 1;
-                postlen += 1;
+        if (nown > 0)
+            for (long long ki = 1; ki <= nk; ++ki) {  // own non-pivot rows, one descriptor per key
+                pd.push_back(StatDesc{e.S, e.total_rows, e.cs, nown, e.off[ki], width(e.keys[ki]), 0, postlen, pwork});
+                pwork += nown;
+                postlen += nown;
             }
     }
     wcopy_.clear();
     double *d_psq = nullptr;
     unsigned char* d_pnz = nullptr;
     if (!qd.empty()) {
+        sb_desc.reset();
+        NScope sx(nprof_, "sb.upload+launch+fetch");
         flush_assemble(sb);
         Uploader u = up();
         int* d_flags = u.put(flags_init);
@@ -1066,16 +1154,12 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         out_.ctr.h2d_bytes += u.bytes_h2d;
         int maxm = 0;
         for (auto& q : qd) maxm = std::max(maxm, q.m);
-        double qb = 0;
-        for (auto& q : qd) qb += 16.0 * q.m * q.ntot;
-        cudaEvent_t e0 = kt_.begin(st_);
-        launch_qr(dq, static_cast<int>(qd.size()), maxm, st_);
-        kt_.end(K_QR, e0, st_, qb);
+        run_qr(qd, dq, u);
         out_.ctr.launches++;
         out_.ctr.qr_launches++;
         double sb = 0;
         for (auto& q : pd) sb += 8.0 * q.nrows * q.ncols + 9.0;
-        e0 = kt_.begin(st_);
+        cudaEvent_t e0 = kt_.begin(st_);
         launch_stats(dp, static_cast<int>(pd.size()), pwork, d_psq, d_pnz, st_);
         kt_.end(K_STATS, e0, st_, sb);
         out_.ctr.launches++;
@@ -1180,15 +1264,12 @@ void Engine::scale_all() {
         out_.ctr.h2d_bytes += u.bytes_h2d;
         int maxm = 0;
         for (auto& q : qd) maxm = std::max(maxm, q.m);
-        double qb = 0, tb = 0;
-        for (auto& q : qd) qb += 16.0 * q.m * q.ntot;
+        double tb = 0;
         for (auto& t : td) tb += 16.0 * t.nrows * t.n;
-        cudaEvent_t e0 = kt_.begin(st_);
-        launch_qr(dq, static_cast<int>(qd.size()), maxm, st_);
-        kt_.end(K_QR, e0, st_, qb);
+        run_qr(qd, dq, u);
         out_.ctr.launches++;
         out_.ctr.qr_launches++;
-        e0 = kt_.begin(st_);
+        cudaEvent_t e0 = kt_.begin(st_);
         launch_trsm(dt, static_cast<int>(td.size()), trows, st_);
         kt_.end(K_TRSM, e0, st_, tb);
         out_.ctr.launches++;
@@ -1235,11 +1316,10 @@ void Engine::sparsify_rows_all() {
             continue;
         }
         Job j{p, cs, p2, nw, c0, arena().alloc_n<double>(static_cast<size_t>(p2) * nw)};
-        const int di = gb.begin(j.B, p2, p2, nw, 1);
-        AsmDst& d = gb.dst[di];
-        gb.src[d.src_off] = AsmSrc{f.mat + cs + static_cast<long long>(c0) * f.ld, 1, f.ld};
-        for (int i = 0; i < p2; ++i) gb.rowref[d.row_off + i] = int4{-1, 0, 0, i};
-        for (int c = 0; c < nw; ++c) gb.cmap[d.cmap_off + c] = c;
+        const int di = gb.begin(j.B, p2, p2, nw, 1, 1);
+        gb.source(di, 0) = AsmSrc{f.mat + cs + static_cast<long long>(c0) * f.ld, 1, f.ld};
+        for (int i = 0; i < p2; ++i) gb.row(di, i) = int4{-1, 0, 0, i};
+        gb.km(di, 0, 0) = 0;
         jobs.push_back(j);
         maxm = std::max(maxm, p2);
         out_.ctr.cpqr_bytes += 8.0 * p2 * nw;
@@ -1259,11 +1339,7 @@ void Engine::sparsify_rows_all() {
         Uploader u = up();
         const CpqrDesc* dc = u.put(cd);
         out_.ctr.h2d_bytes += u.bytes_h2d;
-        double cb = 0;
-        for (auto& q : cd) cb += 16.0 * q.m * q.n;
-        cudaEvent_t e0 = kt_.begin(st_);
-        launch_cpqr(dc, static_cast<int>(cd.size()), maxm, st_);
-        kt_.end(K_CPQR, e0, st_, cb);
+        run_cpqr(cd, dc, u);
         out_.ctr.launches++;
     }
     std::vector<int> rank;
@@ -1278,11 +1354,10 @@ void Engine::sparsify_rows_all() {
         for (int r = j.cs + keep; r < j.cs + j.p2; ++r) out_.dropped_rows.push_back(f.rows[r]);
         f.rows.resize(j.cs + keep);
         if (keep == 0) continue;
-        const int di = wb.begin(f.mat + j.cs + static_cast<long long>(j.c0) * f.ld, f.ld, keep, j.nw, 1);
-        AsmDst& d = wb.dst[di];
-        wb.src[d.src_off] = AsmSrc{j.B, 1, j.p2};
-        for (int r = 0; r < keep; ++r) wb.rowref[d.row_off + r] = int4{-1, 0, 0, r};
-        for (int c = 0; c < j.nw; ++c) wb.cmap[d.cmap_off + c] = c;
+        const int di = wb.begin(f.mat + j.cs + static_cast<long long>(j.c0) * f.ld, f.ld, keep, j.nw, 1, 1);
+        wb.source(di, 0) = AsmSrc{j.B, 1, j.p2};
+        for (int r = 0; r < keep; ++r) wb.row(di, r) = int4{-1, 0, 0, r};
+        wb.km(di, 0, 0) = 0;
     }
     flush_assemble(wb);
 }
@@ -1296,23 +1371,53 @@ void Engine::sparsify_cols_all() {
     for (size_t p = 0; p < fr_.size(); ++p)
         if (fr_[p].live && width(static_cast<int>(p)) > 0 && fr_[p].scaled_ok) elig.push_back(static_cast<int>(p));
     if (elig.empty()) return;
-    std::vector<int> level(fr_.size(), -1);
-    int nwaves = 0;
-    for (int p : elig) {
-        int lv = 0;
+    // Speculative rounds: every pending interface is factored from the
+    // current data; in ascending order a result is accepted unless a lower
+    // neighbour (an interface holding its key or whose key it holds) was
+    // rejected or changed (rank < width) in the same round.  Accepted
+    // results are exactly those of the reference's sequential sweep, since an
+    // unchanged neighbour leaves every input untouched.
+    std::vector<std::vector<int>> lower(elig.size());
+    std::vector<int> eidx(fr_.size(), -1);
+    for (size_t i = 0; i < elig.size(); ++i) eidx[elig[i]] = static_cast<int>(i);
+    for (size_t i = 0; i < elig.size(); ++i) {
+        const int p = elig[i];
         for (int m : holders_[p])
-            if (m < p && level[m] >= 0) lv = std::max(lv, level[m] + 1);
+            if (m < p && eidx[m] >= 0) lower[i].push_back(m);
         for (const KeyRef& k : fr_[p].keys)
-            if (k.key < p && level[k.key] >= 0) lv = std::max(lv, level[k.key] + 1);
-        level[p] = lv;
-        nwaves = std::max(nwaves, lv + 1);
+            if (k.key < p && eidx[k.key] >= 0) lower[i].push_back(k.key);
     }
-    std::vector<std::vector<int>> waves(nwaves);
-    for (int p : elig) waves[level[p]].push_back(p);
-    if (!sprof_.empty()) sprof_.back().scol_waves = nwaves;
+    std::vector<char> bad(fr_.size(), 0), changed(fr_.size(), 0);
+    std::vector<int> pending = elig;
+    int rounds = 0;
     const int rot_batch = batch_;
     const size_t w0 = out_.W.size();
-    for (auto& wave : waves) {
+    std::vector<int> depth(fr_.size(), -1);  // speculation depth of interfaces included in this round
+    std::vector<char> done(fr_.size(), 0);
+    const int kmax_depth = spec_depth_;
+    while (!pending.empty()) {
+        ++rounds;
+        // include p when every lower neighbour is done or included, at a
+        // bounded speculation depth
+        std::vector<int> wave, later;
+        for (int p : pending) {
+            int dp = 0;
+            bool ok = true;
+            for (int q : lower[eidx[p]]) {
+                if (done[q]) continue;
+                if (depth[q] < 0) {
+                    ok = false;
+                    break;
+                }
+                dp = std::max(dp, depth[q] + 1);
+            }
+            if (ok && dp <= kmax_depth) {
+                depth[p] = dp;
+                wave.push_back(p);
+            } else {
+                later.push_back(p);
+            }
+        }
         struct Job {
             int p, cs, nG, wrows, kmax;
             std::vector<int> rparts, seg;  // seg offsets of holders in G
@@ -1320,6 +1425,7 @@ void Engine::sparsify_cols_all() {
             double *V, *tau, *sign;
         };
         std::vector<Job> jobs;
+        std::unique_ptr<NScope> sc1 = std::make_unique<NScope>(nprof_, "scols.G_descriptors");
         AsmBuilder gb;
         std::vector<CpqrDesc> cd;
         int maxm = 0;
@@ -1346,20 +1452,19 @@ void Engine::sparsify_cols_all() {
             const int nsrc = static_cast<int>(j.rparts.size()) + 1;
             if (j.nG > 0) {
                 // logical G^T (nG x cs) gathered row by row, stored transposed as G (ld = cs)
-                const int di = gb.begin(j.G, j.cs, j.nG, j.cs, nsrc);
-                AsmDst& d = gb.dst[di];
-                d.trans = 1;
+                const int di = gb.begin(j.G, j.cs, j.nG, j.cs, nsrc, 1);
+                gb.dst[di].trans = 1;
                 for (size_t s = 0; s < j.rparts.size(); ++s) {
                     const Front& fm = fr_[j.rparts[s]];
                     const int mq = fm.find(p);
-                    gb.src[d.src_off + s] = AsmSrc{fm.mat + static_cast<long long>(fm.keys[mq].col) * fm.ld, 1, fm.ld};
-                    for (int q = 0; q < fm.nrows(); ++q) gb.rowref[d.row_off + j.seg[s] + q] = int4{-1, 0, static_cast<int>(s), q};
-                    for (int i = 0; i < j.cs; ++i) gb.cmap[d.cmap_off + static_cast<long long>(i) * nsrc + s] = i;
+                    gb.source(di, static_cast<int>(s)) = AsmSrc{fm.mat + static_cast<long long>(fm.keys[mq].col) * fm.ld, 1, fm.ld};
+                    for (int q = 0; q < fm.nrows(); ++q) gb.row(di, j.seg[s] + q) = int4{-1, 0, static_cast<int>(s), q};
+                    gb.km(di, 0, static_cast<int>(s)) = 0;
                 }
                 const int so = static_cast<int>(j.rparts.size());
-                gb.src[d.src_off + so] = AsmSrc{f.mat, f.ld, 1};  // transposed view of p's own rows
-                for (int g = 0; g < wcols; ++g) gb.rowref[d.row_off + wrows + g] = int4{-1, 0, so, c0 + g};
-                for (int i = 0; i < j.cs; ++i) gb.cmap[d.cmap_off + static_cast<long long>(i) * nsrc + so] = i;
+                gb.source(di, so) = AsmSrc{f.mat, f.ld, 1};  // transposed view of p's own rows
+                for (int g = 0; g < wcols; ++g) gb.row(di, wrows + g) = int4{-1, 0, so, c0 + g};
+                gb.km(di, 0, so) = 0;
             }
             j.V = out_.warena->alloc_n<double>(static_cast<size_t>(j.cs) * std::max(j.kmax, 1));
             j.tau = out_.warena->alloc_n<double>(std::max(j.kmax, 1));
@@ -1368,6 +1473,8 @@ void Engine::sparsify_cols_all() {
             out_.ctr.cpqr_bytes += 8.0 * j.cs * j.nG;
             jobs.push_back(std::move(j));
         }
+        sc1.reset();
+        std::unique_ptr<NScope> sc2 = std::make_unique<NScope>(nprof_, "scols.upload+cpqr+fetch");
         flush_assemble(gb);
         const size_t nj = jobs.size();
         int* d_rank = arena().alloc_n<int>(nj);
@@ -1382,27 +1489,35 @@ void Engine::sparsify_cols_all() {
             Uploader u = up();
             const CpqrDesc* dc = u.put(cd);
             out_.ctr.h2d_bytes += u.bytes_h2d;
-            double cb = 0;
-        for (auto& q : cd) cb += 16.0 * q.m * q.n;
-        cudaEvent_t e0 = kt_.begin(st_);
-        launch_cpqr(dc, static_cast<int>(cd.size()), maxm, st_);
-        kt_.end(K_CPQR, e0, st_, cb);
+        run_cpqr(cd, dc, u);
             out_.ctr.launches++;
         }
         std::vector<int> rank;
         download(rank, d_rank, nj);
-        // apply structural updates in ascending p, then materialise
-        struct HolderEdit {
-            int m;
-            std::vector<std::pair<int, int>> gsrc;  // (job index, segment) per processed key p
-        };
+        sc2.reset();
+        std::unique_ptr<NScope> sc3 = std::make_unique<NScope>(nprof_, "scols.apply+rebuild_descr");
+        // acceptance (ascending p), then structural updates of accepted changes
         std::map<int, std::vector<std::pair<int, int>>> hed;  // holder m -> (job, holder slot)
         std::vector<int> changed_p;
+        std::vector<int> rejected;
         for (size_t i = 0; i < nj; ++i) {
             Job& j = jobs[i];
             const int r2 = rank[i];
             out_.ctr.cpqr_flops += 4.0 * j.cs * double(j.nG) * r2 + 2.0 * j.cs * j.nG;
+            bool ok = true;
+            for (int q : lower[eidx[j.p]])
+                if (bad[q] || changed[q]) {
+                    ok = false;
+                    break;
+                }
+            if (!ok) {
+                bad[j.p] = 1;
+                rejected.push_back(j.p);
+                continue;
+            }
+            done[j.p] = 1;
             if (r2 >= j.cs) continue;
+            changed[j.p] = 1;
             const int p = j.p;
             Front& f = fr_[p];
             if (r2 > 0) {
@@ -1450,27 +1565,26 @@ void Engine::sparsify_cols_all() {
             layout(p, nf.keys, nf.ncols);
             nf.ld = std::max(1, nf.nrows());
             nf.mat = arena().alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
-            const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, 2);
-            AsmDst& d = mb.dst[di];
-            mb.src[d.src_off + 0] = AsmSrc{j.G, 1, cs};      // R rows (top r2)
-            mb.src[d.src_off + 1] = AsmSrc{f.mat, 1, f.ld};  // old extra rows
-            for (int q = 0; q < r2; ++q) mb.rowref[d.row_off + q] = int4{0, q, -1, 0};
-            for (int q = 0; q < p2; ++q) mb.rowref[d.row_off + r2 + q] = int4{1, cs + q, -1, 0};
+            std::vector<int> ord;
+            phys_order(nf.keys, ord);
+            const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, 2, static_cast<int>(ord.size()));
+            mb.source(di, 0) = AsmSrc{j.G, 1, cs};      // R rows (top r2)
+            mb.source(di, 1) = AsmSrc{f.mat, 1, f.ld};  // old extra rows
+            for (int q = 0; q < r2; ++q) mb.row(di, q) = int4{0, q, -1, 0};
+            for (int q = 0; q < p2; ++q) mb.row(di, r2 + q) = int4{1, cs + q, -1, 0};
             const int qi = f.find(p);
             const int c0 = (qi >= 0) ? f.keys[qi].width : 0;
-            for (const KeyRef& k : nf.keys) {
-                if (k.key == p) {
-                    for (int o = 0; o < k.width; ++o) {
-                        mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * 2 + 0] = -2 - o;
-                        mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * 2 + 1] = -2 - o;
-                    }
+            for (size_t q = 0; q < ord.size(); ++q) {
+                const KeyRef& k = nf.keys[ord[q]];
+                mb.seg(di, static_cast<int>(q), k.col);
+                if (k.key == p) {  // D = [I; 0]
+                    mb.km(di, static_cast<int>(q), 0) = -2;
+                    mb.km(di, static_cast<int>(q), 1) = -2;
                     continue;
                 }
                 const KeyRef& ok = f.keys[f.find(k.key)];
-                for (int o = 0; o < k.width; ++o) {
-                    mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * 2 + 0] = j.wrows + (ok.col - c0) + o;
-                    mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * 2 + 1] = ok.col + o;
-                }
+                mb.km(di, static_cast<int>(q), 0) = j.wrows + (ok.col - c0);
+                mb.km(di, static_cast<int>(q), 1) = ok.col;
             }
             mb.drop_if_empty();
             cols_[p].resize(r2);
@@ -1501,33 +1615,46 @@ void Engine::sparsify_cols_all() {
             for (auto& e : edits)
                 if (e.second >= 0) live_edits.push_back(e);
             const int nsrc = static_cast<int>(live_edits.size()) + 1;
-            const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, nsrc);
-            AsmDst& d = mb.dst[di];
+            std::vector<int> ord;
+            phys_order(nf.keys, ord);
+            const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, nsrc, static_cast<int>(ord.size()));
             for (size_t s = 0; s < live_edits.size(); ++s) {
                 const Job& j = jobs[live_edits[s].first];
                 // B_m(q, i) = R(i, seg + q) = G[i + (seg+q)*cs]
-                mb.src[d.src_off + s] = AsmSrc{j.G + static_cast<long long>(j.seg[live_edits[s].second]) * j.cs, j.cs, 1};
+                mb.source(di, static_cast<int>(s)) =
+                    AsmSrc{j.G + static_cast<long long>(j.seg[live_edits[s].second]) * j.cs, j.cs, 1};
             }
-            mb.src[d.src_off + live_edits.size()] = AsmSrc{f.mat, 1, f.ld};
-            for (int q = 0; q < nf.nrows(); ++q) mb.rowref[d.row_off + q] = int4{-2, q, -1, 0};
-            for (const KeyRef& k : nf.keys) {
+            mb.source(di, static_cast<int>(live_edits.size())) = AsmSrc{f.mat, 1, f.ld};
+            for (int q = 0; q < nf.nrows(); ++q) mb.row(di, q) = int4{-2, q, -1, 0};
+            for (size_t q = 0; q < ord.size(); ++q) {
+                const KeyRef& k = nf.keys[ord[q]];
+                mb.seg(di, static_cast<int>(q), k.col);
                 int gs = -1;
                 for (size_t s = 0; s < live_edits.size(); ++s)
                     if (jobs[live_edits[s].first].p == k.key) gs = static_cast<int>(s);
-                if (gs >= 0) {
-                    for (int o = 0; o < k.width; ++o) mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * nsrc + gs] = o;
-                } else {
-                    const KeyRef& ok = f.keys[f.find(k.key)];
-                    for (int o = 0; o < k.width; ++o)
-                        mb.cmap[d.cmap_off + static_cast<long long>(k.col + o) * nsrc + live_edits.size()] = ok.col + o;
-                }
+                if (gs >= 0)
+                    mb.km(di, static_cast<int>(q), gs) = 0;
+                else
+                    mb.km(di, static_cast<int>(q), static_cast<int>(live_edits.size())) = f.keys[f.find(k.key)].col;
             }
             mb.drop_if_empty();
             updates.emplace_back(m, std::move(nf));
         }
-        flush_assemble(mb);
+        sc3.reset();
+        {
+            NScope sc4(nprof_, "scols.rebuild_flush");
+            flush_assemble(mb);
+        }
         for (auto& [f, nf] : updates) fr_[f] = std::move(nf);
+        for (const Job& j : jobs) {
+            bad[j.p] = 0;
+            changed[j.p] = 0;
+            depth[j.p] = -1;
+        }
+        pending.clear();
+        std::merge(rejected.begin(), rejected.end(), later.begin(), later.end(), std::back_inserter(pending));
     }
+    if (!sprof_.empty()) sprof_.back().scol_waves = rounds;
     std::stable_sort(out_.W.begin() + w0, out_.W.end(),
                      [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
 }
@@ -1553,6 +1680,7 @@ void Engine::merge_level() {
         }
     }
     DeviceArena& next = arena_[cur_ ^ 1];
+    std::unique_ptr<NScope> m1 = std::make_unique<NScope>(nprof_, "merge.descriptors");
     AsmBuilder mb;
     std::vector<Front> nfs;
     std::vector<int> nids;
@@ -1597,25 +1725,33 @@ void Engine::merge_level() {
         nf.ld = std::max(1, nf.nrows());
         nf.mat = next.alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
         const int nsrc = static_cast<int>(kids.size());
-        const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, nsrc);
-        AsmDst& d = mb.dst[di];
-        for (int s = 0; s < nsrc; ++s) mb.src[d.src_off + s] = AsmSrc{fr_[kids[s]].mat, 1, fr_[kids[s]].ld};
-        for (size_t i = 0; i < rowsrc.size(); ++i) mb.rowref[d.row_off + i] = int4{-1, 0, rowsrc[i].first, rowsrc[i].second};
-        for (int s = 0; s < nsrc; ++s) {
-            for (const KeyRef& k : fr_[kids[s]].keys) {
-                if (width(k.key) == 0) continue;
-                const int K = h_.clusters[k.key].parent;
-                const KeyRef& dk = nf.keys[nf.find(K)];
-                const int co = child_off[k.key];
-                if (co < 0) throw std::logic_error("spaqr engine: key without a live front at merge");
-                for (int o = 0; o < k.width; ++o)
-                    mb.cmap[d.cmap_off + static_cast<long long>(dk.col + co + o) * nsrc + s] = k.col + o;
+        // segments: each parent key K splits into its children's column ranges
+        std::vector<int> ord;
+        phys_order(nf.keys, ord);
+        int nseg = 0;
+        for (int q : ord) nseg += static_cast<int>(groups.at(nf.keys[q].key).size());
+        const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, nsrc, nseg);
+        for (int s = 0; s < nsrc; ++s) mb.source(di, s) = AsmSrc{fr_[kids[s]].mat, 1, fr_[kids[s]].ld};
+        for (size_t i = 0; i < rowsrc.size(); ++i) mb.row(di, static_cast<int>(i)) = int4{-1, 0, rowsrc[i].first, rowsrc[i].second};
+        int sg = 0;
+        for (int q : ord) {
+            const KeyRef& dk = nf.keys[q];
+            for (int ck : groups.at(dk.key)) {
+                mb.seg(di, sg, dk.col + child_off[ck]);
+                for (int s = 0; s < nsrc; ++s) {
+                    const Front& fc = fr_[kids[s]];
+                    const int ci = fc.find(ck);
+                    if (ci >= 0) mb.km(di, sg, s) = fc.keys[ci].col;
+                }
+                ++sg;
             }
         }
         mb.drop_if_empty();
         nfs.push_back(std::move(nf));
         nids.push_back(P);
     }
+    m1.reset();
+    std::unique_ptr<NScope> m2 = std::make_unique<NScope>(nprof_, "merge.flush+rebuild_host");
     flush_assemble(mb);
     for (size_t c = 0; c < fr_.size(); ++c) fr_[c] = Front();
     for (auto& hs : holders_) hs.clear();
@@ -1682,6 +1818,7 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
     if (std::getenv("SPQR_PROF")) {
         for (int i = 0; i < HostProf::N; ++i)
             std::fprintf(stderr, "[spqr prof] %-14s %8.3f s  (%lld)\n", HostProf::name(i), prof_.t[i], prof_.n[i]);
+        for (auto& p : nprof_.v) std::fprintf(stderr, "[spqr prof]   %-28s %8.3f s\n", p.first, p.second);
         for (auto& sp : sprof_)
             std::fprintf(stderr,
                          "[spqr prof] stage %2d waves %3d scol_waves %3d elims %6lld S_elems %10lld S_max %lldx%lld | "

@@ -16,7 +16,6 @@ namespace spqr {
 
 namespace {
 
-constexpr int kQrThreads = 128;
 constexpr int kCpqrThreads = 256;
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -39,7 +38,7 @@ __device__ double block_sum(double v, double* red) {
 
 // ------------------------------------------------------------------ assemble
 __global__ void k_assemble(const AsmDst* __restrict__ dst, int ndst, long long total, const int4* __restrict__ rowref,
-                           const int* __restrict__ cmap, const AsmSrc* __restrict__ src) {
+                           const int* __restrict__ segoff, const int* __restrict__ kmap, const AsmSrc* __restrict__ src) {
     const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (e >= total) return;
     int lo = 0, hi = ndst - 1;
@@ -54,39 +53,41 @@ __global__ void k_assemble(const AsmDst* __restrict__ dst, int ndst, long long t
     const long long loc = e - d.elem_off;
     const int i = static_cast<int>(loc % d.nrows);
     const int j = static_cast<int>(loc / d.nrows);
+    const int* so = segoff + d.seg_off;
+    int q = 0, qh = d.nseg - 1;
+    while (q < qh) {
+        const int mid = (q + qh + 1) >> 1;
+        if (so[mid] <= j)
+            q = mid;
+        else
+            qh = mid - 1;
+    }
+    const int o = j - so[q];
+    const int* km = kmap + d.kmap_off + static_cast<long long>(q) * d.nsrc;
     const int4 rr = rowref[d.row_off + i];
-    const int* cm = cmap + d.cmap_off + static_cast<long long>(j) * d.nsrc;
+    int t = -1, r = 0;
+    if (rr.x == -2) {  // scan mode
+        for (int s = 0; s < d.nsrc; ++s)
+            if (km[s] != -1) {
+                t = s;
+                r = rr.y;
+                break;
+            }
+    } else if (rr.x >= 0 && km[rr.x] != -1) {
+        t = rr.x;
+        r = rr.y;
+    } else if (rr.z >= 0 && km[rr.z] != -1) {
+        t = rr.z;
+        r = rr.w;
+    }
     double v = 0.0;
-    if (rr.x == -2) {  // scan mode: first slot with a mapping for column j, row rr.y in every slot
-        for (int t = 0; t < d.nsrc; ++t) {
-            const int c = cm[t];
-            if (c >= 0) {
-                const AsmSrc s = src[d.src_off + t];
-                v = s.p[rr.y * s.rs + c * s.cs];
-                break;
-            }
-            if (c <= -2) {  // identity column: 1 on row (-c-2)
-                v = (i == -c - 2) ? 1.0 : 0.0;
-                break;
-            }
-        }
-    } else {
-        int c = -1, t = -1, r = 0;
-        if (rr.x >= 0 && cm[rr.x] != -1) {
-            t = rr.x;
-            r = rr.y;
-        } else if (rr.z >= 0 && cm[rr.z] != -1) {
-            t = rr.z;
-            r = rr.w;
-        }
-        if (t >= 0) {
-            c = cm[t];
-            if (c >= 0) {
-                const AsmSrc s = src[d.src_off + t];
-                v = s.p[r * s.rs + c * s.cs];
-            } else {
-                v = (i == -c - 2) ? 1.0 : 0.0;
-            }
+    if (t >= 0) {
+        const int c = km[t];
+        if (c >= 0) {
+            const AsmSrc s = src[d.src_off + t];
+            v = s.p[r * s.rs + static_cast<long long>(c + o) * s.cs];
+        } else {
+            v = (i == o) ? 1.0 : 0.0;  // identity segment
         }
     }
     if (d.trans)
@@ -155,14 +156,13 @@ __global__ void k_stats(const StatDesc* __restrict__ ds, int nd, long long total
 // dense_kernels.cpp:11-35 + apply_reflectors_left_t (:96-99) on the trailing
 // columns, fused: reflector k is applied to every column right of k (the QR
 // trailing columns and the neighbour block X) in one right-looking sweep.
-__global__ void __launch_bounds__(kQrThreads) k_qr(const QrDesc* __restrict__ ds) {
-    const QrDesc d = ds[blockIdx.x];
-    __shared__ double red[32];
-    __shared__ double s_tau, s_den;
-    __shared__ signed char s_neg[1024];
-    const int m = d.m, n = d.n, nt = d.ntot, ld = d.ld;
-    double* A = d.a;
+// The body runs on a block that is either staged in shared memory (most
+// fronts: the whole m x ntot block fits) or addressed in place in HBM.
+// Column updates are warp-per-column when m >= 32, else thread-per-column.
+__device__ void qr_body(double* A, int ld, int m, int n, int nt, double* tau_out, double* s_neg_f, double* red,
+                        double* s_sc) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const bool wide = m < 32;
     for (int k = 0; k < n; ++k) {
         double* ak = A + static_cast<long long>(k) * ld;
         double part = 0.0;
@@ -171,65 +171,121 @@ __global__ void __launch_bounds__(kQrThreads) k_qr(const QrDesc* __restrict__ ds
         if (threadIdx.x == 0) {
             const double c0 = ak[k];
             if (tail2 <= DBL_MIN) {  // Eigen makeHouseholder: tau = 0, beta = c0
-                s_tau = 0.0;
-                s_den = 0.0;
+                s_sc[0] = 0.0;
+                s_sc[1] = 0.0;
             } else {
                 double beta = sqrt(c0 * c0 + tail2);
                 if (c0 >= 0.0) beta = -beta;
-                s_den = c0 - beta;
-                s_tau = (beta - c0) / beta;
+                s_sc[1] = c0 - beta;
+                s_sc[0] = (beta - c0) / beta;
                 ak[k] = beta;
             }
         }
         __syncthreads();
-        const double tau = s_tau, den = s_den;
+        const double tau = s_sc[0], den = s_sc[1];
         for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) ak[i] = (tau == 0.0) ? 0.0 : ak[i] / den;
         __syncthreads();
         if (tau != 0.0) {
-            for (int j = k + 1 + wid; j < nt; j += nw) {
-                double* aj = A + static_cast<long long>(j) * ld;
-                double w = 0.0;
-                for (int i = k + 1 + lane; i < m; i += 32) w = fma(ak[i], aj[i], w);
-                w = warp_sum(w) + aj[k];
-                const double tw = tau * w;
-                for (int i = k + 1 + lane; i < m; i += 32) aj[i] = fma(-tw, ak[i], aj[i]);
-                if (lane == 0) aj[k] -= tw;
+            if (wide) {
+                for (int j = k + 1 + threadIdx.x; j < nt; j += blockDim.x) {
+                    double* aj = A + static_cast<long long>(j) * ld;
+                    double w = aj[k];
+                    for (int i = k + 1; i < m; ++i) w = fma(ak[i], aj[i], w);
+                    const double tw = tau * w;
+                    aj[k] -= tw;
+                    for (int i = k + 1; i < m; ++i) aj[i] = fma(-tw, ak[i], aj[i]);
+                }
+            } else {
+                for (int j = k + 1 + wid; j < nt; j += nw) {
+                    double* aj = A + static_cast<long long>(j) * ld;
+                    double w = 0.0;
+                    for (int i = k + 1 + lane; i < m; i += 32) w = fma(ak[i], aj[i], w);
+                    w = warp_sum(w) + aj[k];
+                    const double tw = tau * w;
+                    for (int i = k + 1 + lane; i < m; i += 32) aj[i] = fma(-tw, ak[i], aj[i]);
+                    if (lane == 0) aj[k] -= tw;
+                }
             }
         }
-        if (threadIdx.x == 0 && d.tau) d.tau[k] = tau;
+        if (threadIdx.x == 0 && tau_out) tau_out[k] = tau;
         __syncthreads();
     }
     // nonnegative diagonal: flip row i of R and of the updated neighbour block
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const double r = A[i + static_cast<long long>(i) * ld];
-        s_neg[i] = (r < 0.0);
-        if (d.sign) d.sign[i] = (r < 0.0) ? -1.0 : 1.0;
-        if (d.flag && !(fabs(r) >= DBL_MIN)) atomicMin(d.flag, i);  // first singular pivot
-    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s_neg_f[i] = (A[i + static_cast<long long>(i) * ld] < 0.0) ? -1.0 : 1.0;
     __syncthreads();
     for (int j = threadIdx.x; j < nt; j += blockDim.x) {
         double* aj = A + static_cast<long long>(j) * ld;
         const int top = j < n ? j + 1 : n;
         for (int i = 0; i < top; ++i)
-            if (s_neg[i]) aj[i] = -aj[i];
+            if (s_neg_f[i] < 0.0) aj[i] = -aj[i];
     }
     __syncthreads();
+}
+
+__device__ void qr_epilogue(const QrDesc& d, double* A, int ld, const double* s_neg_f) {
+    const int m = d.m, n = d.n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double r = A[i + static_cast<long long>(i) * ld];
+        if (d.sign) d.sign[i] = s_neg_f[i];
+        if (d.flag && !(fabs(r) >= DBL_MIN)) atomicMin(d.flag, i);  // first singular pivot
+    }
     if (d.rout)
         for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
             const int i = e % n, j = e / n;
             d.rout[e] = (i <= j) ? A[i + static_cast<long long>(j) * ld] : 0.0;
         }
-    if (d.zero_lower && !d.set_identity) {
-        __syncthreads();
+    __syncthreads();
+    if (d.zero_lower && !d.set_identity)
         for (int j = 0; j < n; ++j)
             for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) A[i + static_cast<long long>(j) * ld] = 0.0;
-    }
-    if (d.set_identity) {
-        __syncthreads();
+    if (d.set_identity)
         for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
             const int i = e % m, j = e / m;
             A[i + static_cast<long long>(j) * ld] = (i == j) ? 1.0 : 0.0;
         }
+    __syncthreads();
+}
+
+constexpr int kQrMaxN = 1024;
+
+// in place in HBM (large fronts)
+__global__ void __launch_bounds__(256) k_qr(const QrDesc* __restrict__ ds) {
+    const QrDesc d = ds[blockIdx.x];
+    __shared__ double red[32];
+    __shared__ double s_sc[2];
+    __shared__ double s_neg[kQrMaxN];
+    qr_body(d.a, d.ld, d.m, d.n, d.ntot, d.tau, s_neg, red, s_sc);
+    qr_epilogue(d, d.a, d.ld, s_neg);
+}
+
+__global__ void __launch_bounds__(256) k_qr_idx(const QrDesc* __restrict__ ds, const int* __restrict__ idx) {
+    const QrDesc d = ds[idx[blockIdx.x]];
+    __shared__ double red[32];
+    __shared__ double s_sc[2];
+    __shared__ double s_neg[kQrMaxN];
+    qr_body(d.a, d.ld, d.m, d.n, d.ntot, d.tau, s_neg, red, s_sc);
+    qr_epilogue(d, d.a, d.ld, s_neg);
+}
+
+// staged in shared memory (block + sign buffer), written back once
+__global__ void __launch_bounds__(256) k_qr_smem(const QrDesc* __restrict__ ds, const int* __restrict__ idx) {
+    const QrDesc d = ds[idx[blockIdx.x]];
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    __shared__ double s_sc[2];
+    const int m = d.m, nt = d.ntot;
+    double* A = sm;
+    double* s_neg = sm + static_cast<long long>(m) * nt;
+    for (long long e = threadIdx.x; e < static_cast<long long>(m) * nt; e += blockDim.x) {
+        const int i = static_cast<int>(e % m), j = static_cast<int>(e / m);
+        A[e] = d.a[i + static_cast<long long>(j) * d.ld];
+    }
+    __syncthreads();
+    qr_body(A, m, m, d.n, nt, d.tau, s_neg, red, s_sc);
+    qr_epilogue(d, A, m, s_neg);
+    for (long long e = threadIdx.x; e < static_cast<long long>(m) * nt; e += blockDim.x) {
+        const int i = static_cast<int>(e % m), j = static_cast<int>(e / m);
+        d.a[i + static_cast<long long>(j) * d.ld] = A[e];
     }
 }
 
@@ -255,110 +311,123 @@ __global__ void k_trsm(const TrsmDesc* __restrict__ ds, int nd, long long total)
 }
 
 // ---------------------------------------------------------------------- CPQR
-__device__ double col_norm_from(const double* a, int r0, int m) {  // per warp
+// dense_kernels.cpp:124-232.  Logical column order is kept in ph[] (no data
+// swaps); physical column = original column, so rows [0, rank) are R in the
+// original order on exit.  First-max argmax (strict >) reproduces the
+// reference's lowest-index tie break.  Column norms and updates are
+// thread-per-column when m < 32 (interfaces are a few rows tall), else
+// warp-per-column.
+struct CpqrShared {
+    double red[32];
+    int redi[32];
+    double r11, exact;
+    int piv, stop;
+};
+
+__device__ double colnorm_seq(const double* a, int r0, int m) {
+    double s = 0.0;
+    for (int i = r0; i < m; ++i) s = fma(a[i], a[i], s);
+    return sqrt(s);
+}
+__device__ double colnorm_warp(const double* a, int r0, int m) {
     double s = 0.0;
     for (int i = r0 + (threadIdx.x & 31); i < m; i += 32) s = fma(a[i], a[i], s);
     return sqrt(warp_sum(s));
 }
 
-// dense_kernels.cpp:124-232.  Logical column order is kept in ph[] (no data
-// swaps); physical column = original column, so rows [0, rank) are R in the
-// original order on exit.  First-max argmax (strict >) reproduces the
-// reference's lowest-index tie break.
-__global__ void __launch_bounds__(kCpqrThreads) k_cpqr(const CpqrDesc* __restrict__ ds) {
-    const CpqrDesc d = ds[blockIdx.x];
-    extern __shared__ double sv[];  // reflector vector, m entries
-    __shared__ double red[32];
-    __shared__ int redi[32];
-    __shared__ double s_r11, s_exact;
-    __shared__ int s_piv, s_stop;
-    const int m = d.m, n = d.n, ld = d.ld, kmax = min(m, n);
+__device__ int cpqr_argmax(const double* vn1, int k, int n, CpqrShared& S) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double* A = d.a;
-    double* vn1 = d.work;
-    double* vn2 = d.work + n;
-    int* ph = reinterpret_cast<int*>(d.work + 2 * n);
-    if (kmax == 0) {
-        if (threadIdx.x == 0) {
-            *d.rank = 0;
-            *d.r11 = 0.0;
+    double bv = -1.0;
+    int bj = n;
+    for (int j = k + threadIdx.x; j < n; j += blockDim.x) {
+        const double v = vn1[j];
+        if (v > bv) {
+            bv = v;
+            bj = j;
         }
-        return;
     }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ov > bv || (ov == bv && oj < bj)) {
+            bv = ov;
+            bj = oj;
+        }
+    }
+    __syncthreads();
+    if (lane == 0) {
+        S.red[wid] = bv;
+        S.redi[wid] = bj;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = -1.0;
+        int jj = n;
+        for (int w = 0; w < nw; ++w)
+            if (S.red[w] > b || (S.red[w] == b && S.redi[w] < jj)) {
+                b = S.red[w];
+                jj = S.redi[w];
+            }
+        S.piv = jj;
+    }
+    __syncthreads();
+    return S.piv;
+}
+
+// A: m x n (ld), vn1/vn2/ph: n, sv: m.  Returns rank; R in rows [0, rank).
+__device__ int cpqr_body(const CpqrDesc& d, double* A, int ld, double* vn1, double* vn2, int* ph, double* sv,
+                         CpqrShared& S) {
+    const int m = d.m, n = d.n, kmax = min(m, n);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const bool wide = m < 32;
     const double tol3z = sqrt(DBL_EPSILON);
-    for (int j = wid; j < n; j += nw) {
-        const double nr = col_norm_from(A + static_cast<long long>(j) * ld, 0, m);
-        if (lane == 0) {
-            vn1[j] = vn2[j] = nr;
+    if (wide) {
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            vn1[j] = vn2[j] = colnorm_seq(A + static_cast<long long>(j) * ld, 0, m);
             ph[j] = j;
         }
+    } else {
+        for (int j = wid; j < n; j += nw) {
+            const double nr = colnorm_warp(A + static_cast<long long>(j) * ld, 0, m);
+            if (lane == 0) {
+                vn1[j] = vn2[j] = nr;
+                ph[j] = j;
+            }
+        }
     }
-    if (threadIdx.x == 0) s_r11 = 0.0;
+    if (threadIdx.x == 0) S.r11 = 0.0;
     __syncthreads();
-
-    auto argmax_from = [&](int k) {  // first maximum of vn1[k..n)
-        double bv = -1.0;
-        int bj = n;
-        for (int j = k + threadIdx.x; j < n; j += blockDim.x) {
-            const double v = vn1[j];
-            if (v > bv || (v == bv && j < bj)) {
-                bv = v;
-                bj = j;
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-            if (ov > bv || (ov == bv && oj < bj)) {
-                bv = ov;
-                bj = oj;
-            }
-        }
-        __syncthreads();
-        if (lane == 0) {
-            red[wid] = bv;
-            redi[wid] = bj;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double b = -1.0;
-            int jj = n;
-            for (int w = 0; w < nw; ++w)
-                if (red[w] > b || (red[w] == b && redi[w] < jj)) {
-                    b = red[w];
-                    jj = redi[w];
-                }
-            s_piv = jj;
-        }
-        __syncthreads();
-        return s_piv;
-    };
-
     int k = 0;
     while (k < kmax) {
-        int piv = argmax_from(k);
-        if (wid == 0) {
-            const double ex = col_norm_from(A + static_cast<long long>(ph[piv]) * ld, k, m);
-            if (lane == 0) {
-                s_exact = ex;
-                s_stop = (k == 0) ? !(ex > 0.0) : (d.eps > 0.0 && ex < d.eps * s_r11);
+        int piv = cpqr_argmax(vn1, k, n, S);
+        if (threadIdx.x < 32) {
+            const double* ap = A + static_cast<long long>(ph[piv]) * ld;
+            const double ex = wide ? colnorm_seq(ap, k, m) : colnorm_warp(ap, k, m);
+            if (threadIdx.x == 0) {
+                S.exact = ex;
+                S.stop = (k == 0) ? !(ex > 0.0) : (d.eps > 0.0 && ex < d.eps * S.r11);
             }
         }
         __syncthreads();
-        if (s_stop && k > 0) {  // refresh every trailing norm and retry once
-            for (int j = k + wid; j < n; j += nw) {
-                const double nr = col_norm_from(A + static_cast<long long>(ph[j]) * ld, k, m);
-                if (lane == 0) vn1[j] = vn2[j] = nr;
+        if (S.stop && k > 0) {  // refresh every trailing norm and retry once
+            if (wide) {
+                for (int j = k + threadIdx.x; j < n; j += blockDim.x)
+                    vn1[j] = vn2[j] = colnorm_seq(A + static_cast<long long>(ph[j]) * ld, k, m);
+            } else {
+                for (int j = k + wid; j < n; j += nw) {
+                    const double nr = colnorm_warp(A + static_cast<long long>(ph[j]) * ld, k, m);
+                    if (lane == 0) vn1[j] = vn2[j] = nr;
+                }
             }
             __syncthreads();
-            piv = argmax_from(k);
+            piv = cpqr_argmax(vn1, k, n, S);
             if (threadIdx.x == 0) {
-                s_exact = vn1[piv];
-                s_stop = d.eps > 0.0 && s_exact < d.eps * s_r11;
+                S.exact = vn1[piv];
+                S.stop = d.eps > 0.0 && S.exact < d.eps * S.r11;
             }
             __syncthreads();
         }
-        if (s_stop) break;
+        if (S.stop) break;
         if (threadIdx.x == 0 && piv != k) {
             const int t = ph[piv];
             ph[piv] = ph[k];
@@ -375,7 +444,7 @@ __global__ void __launch_bounds__(kCpqrThreads) k_cpqr(const CpqrDesc* __restric
         double* ap = A + static_cast<long long>(pc) * ld;
         const int len = m - k;
         // Householder: alpha = -sign+(x0)||x||, v = x - alpha e1, tau = 2/||v||^2
-        double alpha = s_exact;
+        double alpha = S.exact;
         const double x0 = ap[k];
         if (x0 > 0.0) alpha = -alpha;
         double part = 0.0;
@@ -384,7 +453,7 @@ __global__ void __launch_bounds__(kCpqrThreads) k_cpqr(const CpqrDesc* __restric
             sv[i] = vi;
             part = fma(vi, vi, part);
         }
-        const double vns = block_sum(part, red);  // syncs: sv visible
+        const double vns = block_sum(part, S.red);
         const double v0 = sv[0];
         if (d.V) {
             double* vk = d.V + static_cast<long long>(k) * d.ldv;
@@ -393,12 +462,22 @@ __global__ void __launch_bounds__(kCpqrThreads) k_cpqr(const CpqrDesc* __restric
         }
         if (vns > 0.0) {
             const double t = 2.0 / vns;
-            for (int jl = k + 1 + wid; jl < n; jl += nw) {
-                double* aj = A + static_cast<long long>(ph[jl]) * ld + k;
-                double w = 0.0;
-                for (int i = lane; i < len; i += 32) w = fma(aj[i], sv[i], w);
-                const double tw = t * warp_sum(w);
-                for (int i = lane; i < len; i += 32) aj[i] = fma(-tw, sv[i], aj[i]);
+            if (wide) {
+                for (int jl = k + 1 + threadIdx.x; jl < n; jl += blockDim.x) {
+                    double* aj = A + static_cast<long long>(ph[jl]) * ld + k;
+                    double w = 0.0;
+                    for (int i = 0; i < len; ++i) w = fma(aj[i], sv[i], w);
+                    const double tw = t * w;
+                    for (int i = 0; i < len; ++i) aj[i] = fma(-tw, sv[i], aj[i]);
+                }
+            } else {
+                for (int jl = k + 1 + wid; jl < n; jl += nw) {
+                    double* aj = A + static_cast<long long>(ph[jl]) * ld + k;
+                    double w = 0.0;
+                    for (int i = lane; i < len; i += 32) w = fma(aj[i], sv[i], w);
+                    const double tw = t * warp_sum(w);
+                    for (int i = lane; i < len; i += 32) aj[i] = fma(-tw, sv[i], aj[i]);
+                }
             }
             __syncthreads();
             for (int i = threadIdx.x; i < len; i += blockDim.x) ap[k + i] = (i == 0) ? alpha : 0.0;
@@ -416,32 +495,99 @@ __global__ void __launch_bounds__(kCpqrThreads) k_cpqr(const CpqrDesc* __restric
         __syncthreads();
         if (threadIdx.x == 0) {
             if (d.sign) d.sign[k] = neg ? -1.0 : 1.0;
-            if (k == 0) s_r11 = ap[0];
+            if (k == 0) S.r11 = ap[0];
             if (d.perm) d.perm[k] = pc;
         }
         ++k;
         __syncthreads();
         if (k < kmax) {  // LAPACK-style downdate, recompute on cancellation
-            for (int jl = k + wid; jl < n; jl += nw) {
-                const double v1 = vn1[jl];
-                if (v1 == 0.0) continue;
-                double* aj = A + static_cast<long long>(ph[jl]) * ld;
-                double tt = fabs(aj[k - 1]) / v1;
-                tt = fmax(0.0, (1.0 - tt) * (1.0 + tt));
-                const double ratio = v1 / vn2[jl];
-                if (tt * ratio * ratio <= tol3z) {
-                    const double nr = col_norm_from(aj, k, m);
-                    if (lane == 0) vn1[jl] = vn2[jl] = nr;
-                } else if (lane == 0) {
-                    vn1[jl] = v1 * sqrt(tt);
+            if (wide) {
+                for (int jl = k + threadIdx.x; jl < n; jl += blockDim.x) {
+                    const double v1 = vn1[jl];
+                    if (v1 == 0.0) continue;
+                    const double* aj = A + static_cast<long long>(ph[jl]) * ld;
+                    double tt = fabs(aj[k - 1]) / v1;
+                    tt = fmax(0.0, (1.0 - tt) * (1.0 + tt));
+                    const double ratio = v1 / vn2[jl];
+                    if (tt * ratio * ratio <= tol3z)
+                        vn1[jl] = vn2[jl] = colnorm_seq(aj, k, m);
+                    else
+                        vn1[jl] = v1 * sqrt(tt);
+                }
+            } else {
+                for (int jl = k + wid; jl < n; jl += nw) {
+                    const double v1 = vn1[jl];
+                    if (v1 == 0.0) continue;
+                    const double* aj = A + static_cast<long long>(ph[jl]) * ld;
+                    double tt = fabs(aj[k - 1]) / v1;
+                    tt = fmax(0.0, (1.0 - tt) * (1.0 + tt));
+                    const double ratio = v1 / vn2[jl];
+                    if (tt * ratio * ratio <= tol3z) {
+                        const double nr = colnorm_warp(aj, k, m);
+                        if (lane == 0) vn1[jl] = vn2[jl] = nr;
+                    } else if (lane == 0) {
+                        vn1[jl] = v1 * sqrt(tt);
+                    }
                 }
             }
             __syncthreads();
         }
     }
+    return k;
+}
+
+// in place in HBM; scratch from d.work, reflector vector in dynamic smem
+__global__ void __launch_bounds__(kCpqrThreads) k_cpqr(const CpqrDesc* __restrict__ ds, const int* __restrict__ idx) {
+    const CpqrDesc d = ds[idx[blockIdx.x]];
+    extern __shared__ double sv[];
+    __shared__ CpqrShared S;
+    const int n = d.n;
+    if (min(d.m, n) == 0) {
+        if (threadIdx.x == 0) {
+            *d.rank = 0;
+            *d.r11 = 0.0;
+        }
+        return;
+    }
+    const int r = cpqr_body(d, d.a, d.ld, d.work, d.work + n, reinterpret_cast<int*>(d.work + 2 * n), sv, S);
     if (threadIdx.x == 0) {
-        *d.rank = k;
-        *d.r11 = s_r11;
+        *d.rank = r;
+        *d.r11 = S.r11;
+    }
+}
+
+// staged: A (m x n), vn1, vn2 (n), ph (n ints), v (m) all in shared memory;
+// rows [0, rank) written back (the rest is never read by the engine)
+__global__ void __launch_bounds__(kCpqrThreads) k_cpqr_smem(const CpqrDesc* __restrict__ ds, const int* __restrict__ idx) {
+    const CpqrDesc d = ds[idx[blockIdx.x]];
+    extern __shared__ double sm[];
+    __shared__ CpqrShared S;
+    const int m = d.m, n = d.n;
+    if (min(m, n) == 0) {
+        if (threadIdx.x == 0) {
+            *d.rank = 0;
+            *d.r11 = 0.0;
+        }
+        return;
+    }
+    double* A = sm;
+    double* vn1 = A + static_cast<long long>(m) * n;
+    double* vn2 = vn1 + n;
+    double* sv = vn2 + n;
+    int* ph = reinterpret_cast<int*>(sv + m);
+    for (long long e = threadIdx.x; e < static_cast<long long>(m) * n; e += blockDim.x) {
+        const int i = static_cast<int>(e % m), j = static_cast<int>(e / m);
+        A[e] = d.a[i + static_cast<long long>(j) * d.ld];
+    }
+    __syncthreads();
+    const int r = cpqr_body(d, A, m, vn1, vn2, ph, sv, S);
+    for (long long e = threadIdx.x; e < static_cast<long long>(r) * n; e += blockDim.x) {
+        const int i = static_cast<int>(e % r), j = static_cast<int>(e / r);
+        d.a[i + static_cast<long long>(j) * d.ld] = A[i + static_cast<long long>(j) * m];
+    }
+    if (threadIdx.x == 0) {
+        *d.rank = r;
+        *d.r11 = S.r11;
     }
 }
 
@@ -458,11 +604,12 @@ int sm_count() {
     return n;
 }
 
-void launch_assemble(const AsmDst* d_dst, int ndst, long long total, const int4* d_rowref, const int* d_cmap,
-                     const AsmSrc* d_src, cudaStream_t st) {
+void launch_assemble(const AsmDst* d_dst, int ndst, long long total, const int4* d_rowref, const int* d_segoff,
+                     const int* d_kmap, const AsmSrc* d_src, cudaStream_t st) {
     if (total <= 0 || ndst <= 0) return;
     const int bs = 256;
-    k_assemble<<<static_cast<unsigned>((total + bs - 1) / bs), bs, 0, st>>>(d_dst, ndst, total, d_rowref, d_cmap, d_src);
+    k_assemble<<<static_cast<unsigned>((total + bs - 1) / bs), bs, 0, st>>>(d_dst, ndst, total, d_rowref, d_segoff, d_kmap,
+                                                                          d_src);
 }
 
 void launch_scatter_values(const long long* off, const double* val, long long n, double* base, cudaStream_t st) {
@@ -476,9 +623,19 @@ void launch_stats(const StatDesc* d, int nd, long long total, double* out_sq, un
     k_stats<<<static_cast<unsigned>((total + bs - 1) / bs), bs, 0, st>>>(d, nd, total, out_sq, out_nz);
 }
 
-void launch_qr(const QrDesc* d, int nd, int /*max_m*/, cudaStream_t st) {
+void launch_qr(const QrDesc* d, int nd, int /*max_m*/, cudaStream_t st) {  // all in place in HBM
     if (nd <= 0) return;
-    k_qr<<<nd, kQrThreads, 0, st>>>(d);
+    k_qr<<<nd, 256, 0, st>>>(d);
+}
+
+void launch_qr_split(const QrDesc* d_desc, const int* d_small, int n_small, size_t smem_small, const int* d_large,
+                     int n_large, cudaStream_t st) {
+    if (n_small > 0) {
+        if (smem_small > 48 * 1024)
+            cudaFuncSetAttribute(k_qr_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_small));
+        k_qr_smem<<<n_small, 256, smem_small, st>>>(d_desc, d_small);
+    }
+    if (n_large > 0) k_qr_idx<<<n_large, 256, 0, st>>>(d_desc, d_large);
 }
 
 void launch_trsm(const TrsmDesc* d, int nd, long long total, cudaStream_t st) {
@@ -487,11 +644,18 @@ void launch_trsm(const TrsmDesc* d, int nd, long long total, cudaStream_t st) {
     k_trsm<<<static_cast<unsigned>((total + bs - 1) / bs), bs, 0, st>>>(d, nd, total);
 }
 
-void launch_cpqr(const CpqrDesc* d, int nd, int max_m, cudaStream_t st) {
-    if (nd <= 0) return;
-    const size_t smem = sizeof(double) * static_cast<size_t>(max_m > 0 ? max_m : 1);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_cpqr, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_cpqr<<<nd, kCpqrThreads, smem, st>>>(d);
+void launch_cpqr_split(const CpqrDesc* d_desc, const int* d_small, int n_small, size_t smem_small, const int* d_large,
+                       int n_large, int max_m_large, cudaStream_t st) {
+    if (n_small > 0) {
+        if (smem_small > 48 * 1024)
+            cudaFuncSetAttribute(k_cpqr_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_small));
+        k_cpqr_smem<<<n_small, kCpqrThreads, smem_small, st>>>(d_desc, d_small);
+    }
+    if (n_large > 0) {
+        const size_t smem = sizeof(double) * static_cast<size_t>(max_m_large > 0 ? max_m_large : 1);
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k_cpqr, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k_cpqr<<<n_large, kCpqrThreads, smem, st>>>(d_desc, d_large);
+    }
 }
 
 }  // namespace spqr
