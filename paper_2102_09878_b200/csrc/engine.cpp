@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <iterator>
+#include <deque>
 #include <map>
 
 #include "dev.h"
@@ -86,6 +87,36 @@ struct PFront {
     void erase(int key) {
         auto it = std::lower_bound(keys.begin(), keys.end(), key, [](const KW& a, int k) { return a.key < k; });
         if (it != keys.end() && it->key == key) keys.erase(it);
+    }
+};
+
+// holders[key]: fronts holding a block of key.  Appends are O(1); the set is
+// sorted/deduplicated lazily when read (reads need ascending order).
+struct HolderSet {
+    std::vector<int> v;
+    bool dirty = false;
+    void add(int x) {
+        v.push_back(x);
+        dirty = true;
+    }
+    void remove(int x) {
+        norm();
+        auto it = std::lower_bound(v.begin(), v.end(), x);
+        if (it != v.end() && *it == x) v.erase(it);
+    }
+    void clear() {
+        v.clear();
+        dirty = false;
+    }
+    const std::vector<int>& get() {
+        norm();
+        return v;
+    }
+    void norm() {
+        if (!dirty) return;
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        dirty = false;
     }
 };
 
@@ -193,6 +224,18 @@ struct Elim {
     int total_rows = 0, tcols = 0, nsel_c = 0;
     double* S = nullptr;
     int* flag = nullptr;  // device
+    void reset(int c_, int cs_) {
+        c = c_;
+        cs = cs_;
+        parts.clear();
+        keys.clear();
+        off.clear();
+        srows.clear();
+        total_rows = tcols = nsel_c = 0;
+        S = nullptr;
+        flag = nullptr;
+        post_off = -1;
+    }
     // post statistics (host): block max / nz of pivot rows; own non-pivot row sums per key
     long long post_off = -1;
 };
@@ -305,7 +348,7 @@ private:
     std::vector<Front> fr_;
     std::vector<std::vector<int>> cols_;
     std::vector<char> gone_;
-    std::vector<std::vector<int>> holders_;
+    std::vector<HolderSet> holders_;
     std::vector<std::vector<int>> stage_list_, tree_clusters_;
     DeviceFactorization out_;
     DeviceArena arena_[2];
@@ -326,7 +369,8 @@ private:
     std::vector<StageProf> sprof_;
     int spec_depth_ = std::getenv("SPQR_SPEC_DEPTH") ? std::atoi(std::getenv("SPQR_SPEC_DEPTH")) : 3;
     // eliminate-batch state
-    std::vector<PFront> pend_;
+    std::deque<PFront> pend_;  // deque: references stay valid while new fronts become pending
+    size_t npend_ = 0;
     std::vector<int> pend_id_, pend_list_;
     std::vector<Elim> el_;
     std::vector<char> mark_;
@@ -495,10 +539,10 @@ private:
 
     PFront& pend(int f) {
         if (pend_id_[f] < 0) {
-            pend_id_[f] = static_cast<int>(pend_.size());
+            if (npend_ == pend_.size()) pend_.emplace_back();
+            pend_id_[f] = static_cast<int>(npend_);
             pend_list_.push_back(f);
-            pend_.emplace_back();
-            PFront& P = pend_.back();
+            PFront& P = pend_[npend_++];
             const Front& F = fr_[f];
             P.rows.resize(F.rows.size());
             for (size_t i = 0; i < F.rows.size(); ++i)
@@ -510,6 +554,37 @@ private:
     }
     // squared norm / nonzero of a symbolic row on one key
     void rowval(const PRow& r, int key, double& sq, bool& nz, bool post_ok) const;
+    // rowval for every row of a pending front, with a fast path for rows still
+    // in their own front's old matrix
+    void row_vals(const PFront& P, int self, int key, double* sq, unsigned char* nz, bool post_ok) const {
+        const Front& B = fr_[self];
+        const int qi = B.find(key);
+        const long long off = (qi >= 0 && !B.soff.empty()) ? B.soff[qi] : -1;
+        for (size_t q = 0; q < P.rows.size(); ++q) {
+            const PRow& r = P.rows[q];
+            if (r.base == self && r.sidx < 0) {
+                if (off < 0) {
+                    sq[q] = 0.0;
+                    nz[q] = 0;
+                } else {
+                    sq[q] = pre_sq_[off + r.brow];
+                    nz[q] = pre_nz_[off + r.brow];
+                }
+            } else {
+                bool b;
+                rowval(r, key, sq[q], b, post_ok);
+                nz[q] = b;
+            }
+        }
+    }
+    std::vector<size_t> rv_off_;
+    std::vector<double> rv_sq_;
+    std::vector<unsigned char> rv_nz_;
+    std::vector<std::vector<int>> sel_;
+    std::vector<int> scr_cand_, scr_best_, scr_keyset_, scr_spos_;
+    std::vector<double> scr_bw_;
+    std::vector<std::pair<int, int>> scr_dest_;
+    std::vector<PRow> scr_rows_;
     DevWFactor& new_factor(int kind, int cluster, int c, int k, const std::vector<int>& cols, const std::vector<int>* coupled) {
         DevWFactor f;
         f.kind = kind;
@@ -564,7 +639,7 @@ void Engine::init_fronts(const std::vector<int>& owner) {
         f.keys.erase(std::unique(f.keys.begin(), f.keys.end(), [](const KeyRef& a, const KeyRef& b) { return a.key == b.key; }),
                      f.keys.end());
         layout(static_cast<int>(c), f.keys, f.ncols);
-        for (auto& k : f.keys) sorted_insert(holders_[k.key], static_cast<int>(c));
+        for (auto& k : f.keys) holders_[k.key].add(static_cast<int>(c));
         f.ld = std::max(1, f.nrows());
         total += static_cast<size_t>(f.ld) * f.ncols;
     }
@@ -645,35 +720,33 @@ void Engine::elim_pass1(Elim& e) {
     const int c = e.c;
     const int cs = e.cs;
     e.parts.clear();
-    for (int m : holders_[c])
+    for (int m : holders_[c].get())
         if (m != c) e.parts.push_back(m);
     if (pend(c).find(c) >= 0) e.parts.insert(e.parts.begin(), c);
     const double eps = opt_.eps;
-    double tau2 = 0.0;
-    if (eps > 0.0) {
-        double mx = 0.0;
-        for (int m : e.parts)
-            for (const PRow& r : pend(m).rows) {
-                double sq;
-                bool nz;
-                rowval(r, c, sq, nz, false);
-                mx = std::max(mx, sq);
-            }
-        tau2 = mx * eps * eps * 1e-4;
+    // row statistics of the c block of every participant, computed once
+    const size_t np = e.parts.size();
+    rv_off_.assign(np + 1, 0);
+    for (size_t pi = 0; pi < np; ++pi) rv_off_[pi + 1] = rv_off_[pi] + pend(e.parts[pi]).rows.size();
+    rv_sq_.resize(rv_off_[np]);
+    rv_nz_.resize(rv_off_[np]);
+    double mx = 0.0;
+    for (size_t pi = 0; pi < np; ++pi) {
+        const PFront& P = pend(e.parts[pi]);
+        row_vals(P, e.parts[pi], c, rv_sq_.data() + rv_off_[pi], rv_nz_.data() + rv_off_[pi], false);
+        for (size_t q = rv_off_[pi]; q < rv_off_[pi + 1]; ++q) mx = std::max(mx, rv_sq_[q]);
     }
-    std::vector<std::vector<int>> sel(e.parts.size());
+    const double tau2 = eps > 0.0 ? mx * eps * eps * 1e-4 : 0.0;
+    std::vector<std::vector<int>>& sel = sel_;
+    if (sel.size() < np) sel.resize(np);
     int total = 0;
     auto select = [&](double floor2) {
         total = 0;
-        for (size_t pi = 0; pi < e.parts.size(); ++pi) {
+        for (size_t pi = 0; pi < np; ++pi) {
             sel[pi].clear();
-            const PFront& P = pend(e.parts[pi]);
-            for (size_t q = 0; q < P.rows.size(); ++q) {
-                double sq;
-                bool nz;
-                rowval(P.rows[q], c, sq, nz, false);
-                if (floor2 > 0.0 ? sq > floor2 : nz) sel[pi].push_back(static_cast<int>(q));
-            }
+            const size_t o = rv_off_[pi], n = rv_off_[pi + 1] - o;
+            for (size_t q = 0; q < n; ++q)
+                if (floor2 > 0.0 ? rv_sq_[o + q] > floor2 : rv_nz_[o + q]) sel[pi].push_back(static_cast<int>(q));
             total += static_cast<int>(sel[pi].size());
         }
     };
@@ -684,7 +757,8 @@ void Engine::elim_pass1(Elim& e) {
         e.cs = -1;  // marks the failing elimination
         return;
     }
-    std::vector<int> keyset;
+    std::vector<int>& keyset = scr_keyset_;
+    keyset.clear();
     for (size_t pi = 0; pi < e.parts.size(); ++pi) {
         if (sel[pi].empty()) continue;
         const PFront& P = pend(e.parts[pi]);
@@ -734,10 +808,11 @@ void Engine::elim_pass1(Elim& e) {
                 P.rows[s[i]].srow = roff + static_cast<int>(i);
             }
         } else {
-            std::vector<int> spos(P.rows.size(), -1);
+            std::vector<int>& spos = scr_spos_;
+            spos.assign(P.rows.size(), -1);
             for (size_t i = 0; i < s.size(); ++i) spos[s[i]] = roff + static_cast<int>(i);
-            std::vector<PRow> nr;
-            nr.reserve(P.rows.size());
+            std::vector<PRow>& nr = scr_rows_;
+            nr.clear();
             for (size_t q = 0; q < P.rows.size(); ++q) {
                 if (spos[q] >= 0 && spos[q] < cs) continue;
                 PRow r = P.rows[q];
@@ -751,7 +826,7 @@ void Engine::elim_pass1(Elim& e) {
         }
         for (int key : keyset) {
             P.add(key, width(key));
-            sorted_insert(holders_[key], m);
+            holders_[key].add(m);
         }
         P.erase(c);
         fr_[m].scaled_ok = false;
@@ -800,49 +875,64 @@ void Engine::elim_pass2(Elim& e, int eidx) {
     // move_extras
     PFront& fc = pend(c);
     if (!fc.rows.empty()) {
-        std::vector<int> cand;
+        std::vector<int>& cand = scr_cand_;
+        cand.clear();
         for (int m : e.parts)
             if (m != c && !gone_[m] && fr_[m].live && width(m) > 0 && fc.find(m) >= 0) cand.push_back(m);
-        std::map<int, std::vector<int>> dest;
-        for (size_t q = 0; q < fc.rows.size(); ++q) {
-            int best = -1;
-            double bw = -1.0;
-            for (int m : cand) {
-                double sq;
-                bool nz;
-                rowval(fc.rows[q], m, sq, nz, true);
-                if (sq > bw) {
-                    bw = sq;
-                    best = m;
+        std::vector<std::pair<int, int>>& dest = scr_dest_;  // (target, row), grouped by target below
+        dest.clear();
+        const size_t nr = fc.rows.size();
+        std::vector<double>& best_w = scr_bw_;
+        std::vector<int>& best = scr_best_;
+        best_w.assign(nr, -1.0);
+        best.assign(nr, -1);
+        rv_sq_.resize(nr);
+        rv_nz_.resize(nr);
+        for (int m : cand) {  // strict > in candidate order == the reference's per-row loop
+            row_vals(fc, c, m, rv_sq_.data(), rv_nz_.data(), true);
+            for (size_t q = 0; q < nr; ++q)
+                if (rv_sq_[q] > best_w[q]) {
+                    best_w[q] = rv_sq_[q];
+                    best[q] = m;
                 }
+        }
+        int anc = -2;
+        for (size_t q = 0; q < nr; ++q) {
+            int b = best[q];
+            if (b < 0) {
+                if (anc == -2) anc = ancestor_target(c);
+                b = anc;
             }
-            if (best < 0) best = ancestor_target(c);
-            if (best < 0)
+            if (b < 0)
                 out_.trailing_rows.push_back(fc.rows[q].gid);
             else
-                dest[best].push_back(static_cast<int>(q));
+                dest.emplace_back(b, static_cast<int>(q));
         }
-        for (auto& [tgt, lr] : dest) {  // append_rows, factorize.cpp:112-133
+        std::stable_sort(dest.begin(), dest.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (size_t a = 0; a < dest.size();) {  // append_rows, factorize.cpp:112-133 (ascending targets)
+            size_t b = a;
+            while (b < dest.size() && dest[b].first == dest[a].first) ++b;
+            const int tgt = dest[a].first;
             PFront& T = pend(tgt);
             for (const KW& kw : fc.keys) {
                 if (width(kw.key) == 0 || T.find(kw.key) >= 0) continue;
                 T.add(kw.key, width(kw.key));
-                sorted_insert(holders_[kw.key], tgt);
+                holders_[kw.key].add(tgt);
             }
             // sequential order appends in ascending c: keep groups sorted by their source cluster
             auto pos = std::upper_bound(T.rows.begin(), T.rows.end(), c, [](int cc, const PRow& r) { return cc < r.tag; });
-            std::vector<PRow> grp;
-            grp.reserve(lr.size());
-            for (int q : lr) {
-                PRow r = fc.rows[q];
+            const size_t at = static_cast<size_t>(pos - T.rows.begin());
+            T.rows.insert(pos, b - a, PRow{});
+            for (size_t t = a; t < b; ++t) {
+                PRow r = fc.rows[dest[t].second];
                 r.tag = c;
-                grp.push_back(r);
+                T.rows[at + (t - a)] = r;
             }
-            T.rows.insert(pos, grp.begin(), grp.end());
             fr_[tgt].scaled_ok = false;
+            a = b;
         }
     }
-    for (const KW& kw : fc.keys) sorted_erase(holders_[kw.key], c);
+    for (const KW& kw : fc.keys) holders_[kw.key].remove(c);
     gone_[c] = 1;
     fr_[c].live = false;
     (void)eidx;
@@ -853,29 +943,57 @@ void Engine::materialize_pending() {
     ProfScope ps_(prof_, HostProf::MATER);
     std::unique_ptr<NScope> mt1 = std::make_unique<NScope>(nprof_, "mat.descriptors");
     AsmBuilder& b = wcopy_;  // W copies already queued; fronts go in the same launch
-    std::vector<std::pair<int, Front>> updates;
-    std::vector<int> slot_of_base(fr_.size(), -1);
-    for (int f : pend_list_) {
-        if (!fr_[f].live) continue;
-        PFront& P = pend_[pend_id_[f]];
+    struct Plan {
+        int f = -1;
+        bool same = false;
         Front nf;
+        std::vector<int> bases, stacks, ord;
+        int di = -1;
+    };
+    std::vector<Plan> plans(pend_list_.size());
+    // phase A (parallel): new row / key lists, layout, sources
+#pragma omp parallel for schedule(dynamic, 32)
+    for (long long t = 0; t < static_cast<long long>(pend_list_.size()); ++t) {
+        const int f = pend_list_[t];
+        Plan& pl = plans[t];
+        if (!fr_[f].live) continue;
+        pl.f = f;
+        const PFront& P = pend_[pend_id_[f]];
+        Front& nf = pl.nf;
         nf.live = true;
         nf.scaled_ok = fr_[f].scaled_ok;
         nf.rows.resize(P.rows.size());
-        for (size_t i = 0; i < P.rows.size(); ++i) nf.rows[i] = P.rows[i].gid;
-        nf.tag.resize(P.rows.size());
-        for (size_t i = 0; i < P.rows.size(); ++i) nf.tag[i] = P.rows[i].tag;
+        bool tagged = false;
+        for (size_t i = 0; i < P.rows.size(); ++i) {
+            nf.rows[i] = P.rows[i].gid;
+            tagged |= P.rows[i].tag >= 0;
+        }
+        if (tagged) {
+            nf.tag.resize(P.rows.size());
+            for (size_t i = 0; i < P.rows.size(); ++i) nf.tag[i] = P.rows[i].tag;
+        }
         nf.keys.resize(P.keys.size());
         for (size_t i = 0; i < P.keys.size(); ++i) nf.keys[i] = KeyRef{P.keys[i].key, P.keys[i].width, 0};
         layout(f, nf.keys, nf.ncols);
         nf.ld = std::max(1, nf.nrows());
-        // unchanged front?  (same rows from itself in order, same keys)
         bool same = nf.keys.size() == fr_[f].keys.size() && P.rows.size() == fr_[f].rows.size();
         for (size_t i = 0; same && i < nf.keys.size(); ++i)
             same = nf.keys[i].key == fr_[f].keys[i].key && nf.keys[i].width == fr_[f].keys[i].width;
         for (size_t i = 0; same && i < P.rows.size(); ++i)
             same = P.rows[i].base == f && P.rows[i].brow == static_cast<int>(i) && P.rows[i].sidx < 0;
+        pl.same = same;
         if (same) continue;
+        for (const PRow& r : P.rows) {
+            if (std::find(pl.bases.begin(), pl.bases.end(), r.base) == pl.bases.end()) pl.bases.push_back(r.base);
+            if (r.sidx >= 0 && std::find(pl.stacks.begin(), pl.stacks.end(), r.sidx) == pl.stacks.end())
+                pl.stacks.push_back(r.sidx);
+        }
+        phys_order(nf.keys, pl.ord);
+    }
+    // phase B (sequential): allocation and descriptor reservation
+    for (Plan& pl : plans) {
+        if (pl.f < 0 || pl.same) continue;
+        Front& nf = pl.nf;
         nf.mat = arena().alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
         if (!sprof_.empty()) {
             auto& sp = sprof_.back();
@@ -885,80 +1003,94 @@ void Engine::materialize_pending() {
             sp.max_front_rows = std::max<long long>(sp.max_front_rows, nf.nrows());
             sp.max_front_cols = std::max<long long>(sp.max_front_cols, nf.ncols);
         }
-        // sources: distinct bases then distinct stacks
-        std::vector<int> bases, stacks;
-        for (const PRow& r : P.rows) {
-            if (slot_of_base[r.base] < 0) {
-                slot_of_base[r.base] = static_cast<int>(bases.size());
-                bases.push_back(r.base);
-            }
-            if (r.sidx >= 0 && std::find(stacks.begin(), stacks.end(), r.sidx) == stacks.end()) stacks.push_back(r.sidx);
+        if (nf.nrows() == 0 || nf.ncols == 0) continue;
+        const int nsrc = static_cast<int>(pl.bases.size() + pl.stacks.size());
+        pl.di = b.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, std::max(nsrc, 1), static_cast<int>(pl.ord.size()));
+    }
+    // phase C (parallel): fill
+#pragma omp parallel for schedule(dynamic, 32)
+    for (long long t = 0; t < static_cast<long long>(plans.size()); ++t) {
+        Plan& pl = plans[t];
+        if (pl.di < 0) continue;
+        const int di = pl.di;
+        const PFront& P = pend_[pend_id_[pl.f]];
+        const Front& nf = pl.nf;
+        const int nb = static_cast<int>(pl.bases.size());
+        for (int s = 0; s < nb; ++s) {
+            const Front& B = fr_[pl.bases[s]];
+            b.source(di, s) = AsmSrc{B.mat, 1, B.ld};
         }
-        const int nsrc = static_cast<int>(bases.size() + stacks.size());
-        std::vector<int> ord;
-        phys_order(nf.keys, ord);
-        const int di = b.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, std::max(nsrc, 1), static_cast<int>(ord.size()));
-        for (size_t s = 0; s < bases.size(); ++s) {
-            const Front& B = fr_[bases[s]];
-            b.source(di, static_cast<int>(s)) = AsmSrc{B.mat, 1, B.ld};
+        for (size_t s = 0; s < pl.stacks.size(); ++s) {
+            const Elim& E = el_[pl.stacks[s]];
+            b.source(di, nb + static_cast<int>(s)) = AsmSrc{E.S, 1, E.total_rows};
         }
-        for (size_t s = 0; s < stacks.size(); ++s) {
-            const Elim& E = el_[stacks[s]];
-            b.source(di, static_cast<int>(bases.size() + s)) = AsmSrc{E.S, 1, E.total_rows};
-        }
+        int lastb = -1, lastslot = 0;
         for (size_t i = 0; i < P.rows.size(); ++i) {
             const PRow& r = P.rows[i];
+            if (r.base != lastb) {
+                lastb = r.base;
+                lastslot = static_cast<int>(std::find(pl.bases.begin(), pl.bases.end(), r.base) - pl.bases.begin());
+            }
             int s1 = -1;
             if (r.sidx >= 0)
-                s1 = static_cast<int>(bases.size() + (std::find(stacks.begin(), stacks.end(), r.sidx) - stacks.begin()));
-            b.row(di, static_cast<int>(i)) = int4{s1, r.srow, slot_of_base[r.base], r.brow};
+                s1 = nb + static_cast<int>(std::find(pl.stacks.begin(), pl.stacks.end(), r.sidx) - pl.stacks.begin());
+            b.row(di, static_cast<int>(i)) = int4{s1, r.srow, lastslot, r.brow};
         }
-        for (size_t q = 0; q < ord.size(); ++q) {
-            const KeyRef& k = nf.keys[ord[q]];
+        for (size_t q = 0; q < pl.ord.size(); ++q) {
+            const KeyRef& k = nf.keys[pl.ord[q]];
             b.seg(di, static_cast<int>(q), k.col);
-            for (size_t s = 0; s < bases.size(); ++s) {
-                const Front& B = fr_[bases[s]];
+            for (int s = 0; s < nb; ++s) {
+                const Front& B = fr_[pl.bases[s]];
                 const int qi = B.find(k.key);
-                if (qi >= 0) b.km(di, static_cast<int>(q), static_cast<int>(s)) = B.keys[qi].col;
+                if (qi >= 0) b.km(di, static_cast<int>(q), s) = B.keys[qi].col;
             }
-            for (size_t s = 0; s < stacks.size(); ++s) {
-                const Elim& E = el_[stacks[s]];
+            for (size_t s = 0; s < pl.stacks.size(); ++s) {
+                const Elim& E = el_[pl.stacks[s]];
                 auto it = std::lower_bound(E.keys.begin() + 1, E.keys.end(), k.key);
                 if (it == E.keys.end() || *it != k.key) continue;
-                b.km(di, static_cast<int>(q), static_cast<int>(bases.size() + s)) = E.off[it - E.keys.begin()];
+                b.km(di, static_cast<int>(q), nb + static_cast<int>(s)) = E.off[it - E.keys.begin()];
             }
         }
-        b.drop_if_empty();
-        for (int bb : bases) slot_of_base[bb] = -1;
-        updates.emplace_back(f, std::move(nf));
     }
     mt1.reset();
     std::unique_ptr<NScope> mt2 = std::make_unique<NScope>(nprof_, "mat.flush");
     flush_assemble(b);
     mt2.reset();
     NScope mt3(nprof_, "mat.swap");
-    for (auto& [f, nf] : updates) {
-        nf.soff.clear();
-        fr_[f] = std::move(nf);
+    for (Plan& pl : plans) {
+        if (pl.f < 0 || pl.same) continue;
+        fr_[pl.f] = std::move(pl.nf);
     }
     for (int f : pend_list_) pend_id_[f] = -1;
     pend_list_.clear();
-    pend_.clear();
+    npend_ = 0;
 }
 
 // pre-stage row statistics (sum of squares, any-nonzero) of every block of the fronts in P
 void Engine::compute_stats(const std::vector<int>& P) {
     ProfScope ps_(prof_, HostProf::STATS);
-    std::vector<StatDesc> sd;
-    long long work = 0;
-    for (int f : P) {
-        Front& F = fr_[f];
+    // two-phase (count, parallel fill) descriptor build
+    const size_t nP = P.size();
+    std::vector<long long> dcount(nP + 1, 0), wcount(nP + 1, 0);
+    for (size_t t = 0; t < nP; ++t) {
+        const Front& F = fr_[P[t]];
+        const int nk = F.nrows() > 0 ? static_cast<int>(F.keys.size()) : 0;
+        dcount[t + 1] = dcount[t] + nk;
+        wcount[t + 1] = wcount[t] + static_cast<long long>(nk) * F.nrows();
+    }
+    const long long work = wcount[nP];
+    std::vector<StatDesc> sd(dcount[nP]);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (long long t = 0; t < static_cast<long long>(nP); ++t) {
+        Front& F = fr_[P[t]];
         F.soff.assign(F.keys.size(), -1);
+        long long w = wcount[t];
+        long long dd = dcount[t];
         for (size_t qi = 0; qi < F.keys.size(); ++qi) {
-            F.soff[qi] = work;
+            F.soff[qi] = w;
             if (F.nrows() == 0) continue;
-            sd.push_back(StatDesc{F.mat, F.ld, 0, F.nrows(), F.keys[qi].col, F.keys[qi].width, 0, work, work});
-            work += F.nrows();
+            sd[dd++] = StatDesc{F.mat, F.ld, 0, F.nrows(), F.keys[qi].col, F.keys[qi].width, 0, w, w};
+            w += F.nrows();
         }
     }
     double* d_sq = arena().alloc_n<double>(std::max<long long>(work, 1));
@@ -987,7 +1119,7 @@ std::vector<int> Engine::stage_fronts(const std::vector<int>& list) {
             P.push_back(c);
         }
         if (width(c) > 0)
-            for (int m : holders_[c])
+            for (int m : holders_[c].get())
                 if (fr_[m].live && !mark_[m]) {
                     mark_[m] = 1;
                     P.push_back(m);
@@ -1054,15 +1186,13 @@ void Engine::eliminate_stage(int k) {
 }
 
 void Engine::eliminate_wave(const std::vector<int>& list) {
-    el_.clear();
-    el_.reserve(list.size());
+    if (el_.size() < list.size()) el_.resize(list.size());  // pool: Elim objects keep their capacity
     // pass 1 over the wave (ascending ids)
     int nvalid = 0;
-    for (int c : list) {
-        el_.emplace_back();
-        Elim& e = el_.back();
-        e.c = c;
-        e.cs = width(c);
+    for (size_t t = 0; t < list.size(); ++t) {
+        const int c = list[t];
+        Elim& e = el_[t];
+        e.reset(c, width(c));
         if (e.cs > 0) elim_pass1(e);
         if (e.cs < 0) break;  // "rows couple" error: later eliminations never run
         ++nvalid;
@@ -1244,7 +1374,7 @@ void Engine::scale_all() {
         out_.ctr.qr_flops += 2.0 * f.nrows() * double(cs) * cs - 2.0 / 3.0 * double(cs) * cs * cs +
                              (4.0 * f.nrows() * cs - 2.0 * cs * double(cs)) * (f.ncols - cs);
         out_.ctr.qr_bytes += 16.0 * f.nrows() * f.ncols;
-        for (int m : holders_[p]) {
+        for (int m : holders_[p].get()) {
             if (m == p) continue;
             const Front& fm = fr_[m];
             const int mq = fm.find(p);
@@ -1382,7 +1512,7 @@ void Engine::sparsify_cols_all() {
     for (size_t i = 0; i < elig.size(); ++i) eidx[elig[i]] = static_cast<int>(i);
     for (size_t i = 0; i < elig.size(); ++i) {
         const int p = elig[i];
-        for (int m : holders_[p])
+        for (int m : holders_[p].get())
             if (m < p && eidx[m] >= 0) lower[i].push_back(m);
         for (const KeyRef& k : fr_[p].keys)
             if (k.key < p && eidx[k.key] >= 0) lower[i].push_back(k.key);
@@ -1434,7 +1564,7 @@ void Engine::sparsify_cols_all() {
             Job j;
             j.p = p;
             j.cs = width(p);
-            for (int m : holders_[p])
+            for (int m : holders_[p].get())
                 if (m != p && fr_[m].live) j.rparts.push_back(m);
             int wrows = 0;
             for (int m : j.rparts) {
@@ -1533,7 +1663,7 @@ void Engine::sparsify_cols_all() {
                     hed[m].emplace_back(static_cast<int>(i), static_cast<int>(s));
                 else {
                     hed[m].emplace_back(static_cast<int>(i), -1 - static_cast<int>(s));  // drop key p
-                    sorted_erase(holders_[p], m);
+                    holders_[p].remove(m);
                 }
             }
             for (int q = r2; q < j.cs; ++q) {
@@ -1663,18 +1793,36 @@ void Engine::sparsify_cols_all() {
 // is rebuilt into the other arena (pivot rows of all children first).
 void Engine::merge_level() {
     ProfScope ps_(prof_, HostProf::MERGE);
-    std::map<int, std::vector<int>> groups;
-    for (size_t c = 0; c < fr_.size(); ++c)
-        if (fr_[c].live) groups[h_.clusters[c].parent].push_back(static_cast<int>(c));
-    for (auto& [P, kids] : groups) {
-        if (P < 0) throw std::logic_error("spaqr engine: live front without a parent cluster at merge");
-        cols_[P].clear();
-        for (int c : kids) cols_[P].insert(cols_[P].end(), cols_[c].begin(), cols_[c].end());
+    // groups of live fronts by parent cluster (ascending parents, ascending kids)
+    std::vector<int> gp;       // parent per group
+    std::vector<int> gstart;   // kids of group g: gkids[gstart[g] .. gstart[g+1])
+    std::vector<int> gkids;
+    std::vector<int> group_of(fr_.size(), -1);
+    {
+        std::vector<std::pair<int, int>> pk;  // (parent, kid)
+        for (size_t c = 0; c < fr_.size(); ++c)
+            if (fr_[c].live) pk.emplace_back(h_.clusters[c].parent, static_cast<int>(c));
+        std::sort(pk.begin(), pk.end());
+        for (size_t i = 0; i < pk.size(); ++i) {
+            if (pk[i].first < 0) throw std::logic_error("spaqr engine: live front without a parent cluster at merge");
+            if (i == 0 || pk[i].first != pk[i - 1].first) {
+                gp.push_back(pk[i].first);
+                gstart.push_back(static_cast<int>(gkids.size()));
+                group_of[pk[i].first] = static_cast<int>(gp.size()) - 1;
+            }
+            gkids.push_back(pk[i].second);
+        }
+        gstart.push_back(static_cast<int>(gkids.size()));
     }
+    const int ng = static_cast<int>(gp.size());
     std::vector<int> child_off(fr_.size(), -1);
-    for (auto& [P, kids] : groups) {
+    for (int g = 0; g < ng; ++g) {
+        const int P = gp[g];
+        cols_[P].clear();
         int o = 0;
-        for (int c : kids) {
+        for (int t = gstart[g]; t < gstart[g + 1]; ++t) {
+            const int c = gkids[t];
+            cols_[P].insert(cols_[P].end(), cols_[c].begin(), cols_[c].end());
             child_off[c] = o;
             o += width(c);
         }
@@ -1682,83 +1830,100 @@ void Engine::merge_level() {
     DeviceArena& next = arena_[cur_ ^ 1];
     std::unique_ptr<NScope> m1 = std::make_unique<NScope>(nprof_, "merge.descriptors");
     AsmBuilder mb;
-    std::vector<Front> nfs;
-    std::vector<int> nids;
-    for (auto& [P, kids] : groups) {
+    struct Plan {
         Front nf;
+        std::vector<int2> rowsrc;  // (kid slot, row)
+        std::vector<int> ord;
+        int nseg = 0, di = -1;
+    };
+    std::vector<Plan> plans(ng);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int g = 0; g < ng; ++g) {
+        const int P = gp[g];
+        const int k0 = gstart[g], k1 = gstart[g + 1];
+        Plan& pl = plans[g];
+        Front& nf = pl.nf;
         nf.live = true;
         bool movable = false;
-        if (kids.size() == 1) {
+        if (k1 - k0 == 1) {
             movable = true;
-            for (const KeyRef& k : fr_[kids[0]].keys)
+            for (const KeyRef& k : fr_[gkids[k0]].keys)
                 if (width(k.key) != 0 && width(h_.clusters[k.key].parent) != width(k.key)) {
                     movable = false;
                     break;
                 }
         }
-        nf.scaled_ok = movable ? fr_[kids[0]].scaled_ok : false;
-        std::vector<std::pair<int, int>> rowsrc;  // (kid slot, row)
-        for (size_t s = 0; s < kids.size(); ++s) {
-            const Front& fc = fr_[kids[s]];
-            const int take = std::min(width(kids[s]), fc.nrows());
-            for (int i = 0; i < take; ++i) {
-                nf.rows.push_back(fc.rows[i]);
-                rowsrc.emplace_back(static_cast<int>(s), i);
+        nf.scaled_ok = movable ? fr_[gkids[k0]].scaled_ok : false;
+        size_t nr = 0;
+        for (int t = k0; t < k1; ++t) nr += fr_[gkids[t]].rows.size();
+        nf.rows.reserve(nr);
+        pl.rowsrc.reserve(nr);
+        for (int pass = 0; pass < 2; ++pass)  // pivot rows of all children first, then remainders
+            for (int t = k0; t < k1; ++t) {
+                const Front& fc = fr_[gkids[t]];
+                const int take = std::min(width(gkids[t]), fc.nrows());
+                const int i0 = pass == 0 ? 0 : take, i1 = pass == 0 ? take : fc.nrows();
+                for (int i = i0; i < i1; ++i) {
+                    nf.rows.push_back(fc.rows[i]);
+                    pl.rowsrc.push_back(int2{t - k0, i});
+                }
             }
-        }
-        for (size_t s = 0; s < kids.size(); ++s) {
-            const Front& fc = fr_[kids[s]];
-            const int take = std::min(width(kids[s]), fc.nrows());
-            for (int i = take; i < fc.nrows(); ++i) {
-                nf.rows.push_back(fc.rows[i]);
-                rowsrc.emplace_back(static_cast<int>(s), i);
-            }
-        }
-        std::vector<int> pk;
-        for (int c : kids)
-            for (const KeyRef& k : fr_[c].keys)
-                if (width(k.key) != 0) pk.push_back(h_.clusters[k.key].parent);
-        std::sort(pk.begin(), pk.end());
-        pk.erase(std::unique(pk.begin(), pk.end()), pk.end());
-        for (int K : pk) nf.keys.push_back(KeyRef{K, width(K), 0});
+        std::vector<int> pkeys;
+        for (int t = k0; t < k1; ++t)
+            for (const KeyRef& k : fr_[gkids[t]].keys)
+                if (width(k.key) != 0) pkeys.push_back(h_.clusters[k.key].parent);
+        std::sort(pkeys.begin(), pkeys.end());
+        pkeys.erase(std::unique(pkeys.begin(), pkeys.end()), pkeys.end());
+        nf.keys.reserve(pkeys.size());
+        for (int K : pkeys) nf.keys.push_back(KeyRef{K, width(K), 0});
         layout(P, nf.keys, nf.ncols);
         nf.ld = std::max(1, nf.nrows());
+        phys_order(nf.keys, pl.ord);
+        for (int q : pl.ord) {
+            const int gk = group_of[nf.keys[q].key];
+            pl.nseg += gstart[gk + 1] - gstart[gk];
+        }
+    }
+    for (int g = 0; g < ng; ++g) {
+        Plan& pl = plans[g];
+        Front& nf = pl.nf;
         nf.mat = next.alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
-        const int nsrc = static_cast<int>(kids.size());
-        // segments: each parent key K splits into its children's column ranges
-        std::vector<int> ord;
-        phys_order(nf.keys, ord);
-        int nseg = 0;
-        for (int q : ord) nseg += static_cast<int>(groups.at(nf.keys[q].key).size());
-        const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, nsrc, nseg);
-        for (int s = 0; s < nsrc; ++s) mb.source(di, s) = AsmSrc{fr_[kids[s]].mat, 1, fr_[kids[s]].ld};
-        for (size_t i = 0; i < rowsrc.size(); ++i) mb.row(di, static_cast<int>(i)) = int4{-1, 0, rowsrc[i].first, rowsrc[i].second};
+        if (nf.nrows() == 0 || nf.ncols == 0) continue;
+        pl.di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, gstart[g + 1] - gstart[g], pl.nseg);
+    }
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int g = 0; g < ng; ++g) {
+        Plan& pl = plans[g];
+        if (pl.di < 0) continue;
+        const int di = pl.di, k0 = gstart[g], nsrc = gstart[g + 1] - k0;
+        for (int s = 0; s < nsrc; ++s) mb.source(di, s) = AsmSrc{fr_[gkids[k0 + s]].mat, 1, fr_[gkids[k0 + s]].ld};
+        for (size_t i = 0; i < pl.rowsrc.size(); ++i) mb.row(di, static_cast<int>(i)) = int4{-1, 0, pl.rowsrc[i].x, pl.rowsrc[i].y};
         int sg = 0;
-        for (int q : ord) {
-            const KeyRef& dk = nf.keys[q];
-            for (int ck : groups.at(dk.key)) {
+        for (int q : pl.ord) {  // each parent key splits into its children's column ranges
+            const KeyRef& dk = pl.nf.keys[q];
+            const int gk = group_of[dk.key];
+            for (int t = gstart[gk]; t < gstart[gk + 1]; ++t) {
+                const int ck = gkids[t];
                 mb.seg(di, sg, dk.col + child_off[ck]);
                 for (int s = 0; s < nsrc; ++s) {
-                    const Front& fc = fr_[kids[s]];
+                    const Front& fc = fr_[gkids[k0 + s]];
                     const int ci = fc.find(ck);
                     if (ci >= 0) mb.km(di, sg, s) = fc.keys[ci].col;
                 }
                 ++sg;
             }
         }
-        mb.drop_if_empty();
-        nfs.push_back(std::move(nf));
-        nids.push_back(P);
     }
     m1.reset();
     std::unique_ptr<NScope> m2 = std::make_unique<NScope>(nprof_, "merge.flush+rebuild_host");
     flush_assemble(mb);
-    for (size_t c = 0; c < fr_.size(); ++c) fr_[c] = Front();
+    for (size_t c = 0; c < fr_.size(); ++c)
+        if (fr_[c].live) fr_[c] = Front();
     for (auto& hs : holders_) hs.clear();
-    for (size_t i = 0; i < nfs.size(); ++i) {
-        const int P = nids[i];
-        fr_[P] = std::move(nfs[i]);
-        for (const KeyRef& k : fr_[P].keys) sorted_insert(holders_[k.key], P);
+    for (int g = 0; g < ng; ++g) {
+        const int P = gp[g];
+        fr_[P] = std::move(plans[g].nf);
+        for (const KeyRef& k : fr_[P].keys) holders_[k.key].add(P);
     }
     // everything of this stage lived in arena cur_; the next stage starts clean
     sync();
@@ -1834,12 +1999,18 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
 
 }  // namespace
 
+void sampler_start();
+void sampler_stop();
+
 DeviceFactorization gpu_factorize(const Csc& A, const ClusterHierarchy& h, const std::vector<int>& owner,
                                   const FactorizeOptions& opt, cudaStream_t st) {
     if (A.m < A.n) throw std::invalid_argument("matrix must have at least as many rows as columns");
     if (static_cast<Index>(owner.size()) != A.m) throw std::invalid_argument("row_owner size mismatch");
+    sampler_start();
     Engine e(A, h, owner, opt, st);
-    return e.run();
+    DeviceFactorization F = e.run();
+    sampler_stop();
+    return F;
 }
 
 }  // namespace spqr

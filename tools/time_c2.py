@@ -5,7 +5,7 @@ from paper_2102_09878_b200.problems import tall_grid
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 p = tall_grid(n)
 L = p.levels or None
-for rep in range(2):
+for rep in range(int(os.environ.get("REPS", "2"))):
     t0 = time.time()
     g = P.Pipeline(p.A, eps=p.eps, levels=p.levels, coords=p.coords)
     t1 = time.time()
