@@ -25,6 +25,9 @@
 #include <cstdlib>
 #include <iterator>
 #include <deque>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <map>
 
 #include "dev.h"
@@ -124,10 +127,6 @@ void sorted_insert(std::vector<int>& v, int x) {
     auto it = std::lower_bound(v.begin(), v.end(), x);
     if (it == v.end() || *it != x) v.insert(it, x);
 }
-void sorted_erase(std::vector<int>& v, int x) {
-    auto it = std::lower_bound(v.begin(), v.end(), x);
-    if (it != v.end() && *it == x) v.erase(it);
-}
 
 // Host-side profile (SPQR_PROF=1 prints it to stderr after the factorization).
 struct HostProf {
@@ -224,9 +223,26 @@ struct Elim {
     int total_rows = 0, tcols = 0, nsel_c = 0;
     double* S = nullptr;
     int* flag = nullptr;  // device
+    // deferred effects of the parallel host passes
+    std::vector<std::pair<int, int>> hadd;  // holders_[key].add(front)
+    std::string err;                        // error text raised inside a parallel pass
+    bool logic = false;                     // err is an internal logic error
+    std::vector<int> keepk, coupled;        // pruned coupling (W factor)
+    int kept = 0;
+    std::vector<std::pair<int, int>> dest;  // move_extras: (target, local row), ascending target
+    std::vector<int> trail;                 // move_extras: rows to the trailing set
+    int color = 0;
     void reset(int c_, int cs_) {
         c = c_;
         cs = cs_;
+        hadd.clear();
+        err.clear();
+        logic = false;
+        keepk.clear();
+        coupled.clear();
+        kept = 0;
+        dest.clear();
+        trail.clear();
         parts.clear();
         keys.clear();
         off.clear();
@@ -238,6 +254,16 @@ struct Elim {
     }
     // post statistics (host): block max / nz of pivot rows; own non-pivot row sums per key
     long long post_off = -1;
+};
+
+// Per-thread scratch of the parallel elimination passes.
+struct Scratch {
+    std::vector<size_t> rv_off;
+    std::vector<double> rv_sq, bw;
+    std::vector<unsigned char> rv_nz;
+    std::vector<std::vector<int>> sel;
+    std::vector<int> keyset, spos, best, cand;
+    std::vector<PRow> rows;
 };
 
 // Assemble job builder (generic gather, dev.h).
@@ -319,6 +345,7 @@ public:
         holders_.resize(nc);
         pend_id_.assign(nc, -1);
         mark_.assign(nc, 0);
+        colmask_.assign(nc, 0);
         stage_of_.assign(nc, 0);
         for (size_t c = 0; c < nc; ++c) stage_of_[c] = (h.clusters[c].level == h.clusters[c].stage) ? h.clusters[c].stage : 0;
         stage_list_.resize(L_ + 2);
@@ -365,6 +392,7 @@ private:
         int stage = 0, waves = 0, scol_waves = 0;
         long long s_elems = 0, s_max_rows = 0, s_max_cols = 0, mat_fronts = 0, mat_rows = 0, mat_elems = 0, elims = 0;
         long long max_front_rows = 0, max_front_cols = 0;
+        double t[HostProf::N] = {0};
     };
     std::vector<StageProf> sprof_;
     int spec_depth_ = std::getenv("SPQR_SPEC_DEPTH") ? std::atoi(std::getenv("SPQR_SPEC_DEPTH")) : 3;
@@ -527,8 +555,11 @@ private:
     void eliminate_wave(const std::vector<int>& list);
     void compute_stats(const std::vector<int>& P);
     std::vector<int> stage_fronts(const std::vector<int>& list);
-    void elim_pass1(Elim& e);
-    void elim_pass2(Elim& e, int eidx);
+    void elim_pass1(Elim& e, Scratch& S);
+    void elim_prep2(Elim& e, Scratch& S);
+    void elim_commit2(Elim& e);
+    std::vector<Scratch> tscr_;
+    std::vector<uint64_t> colmask_;
     void materialize_pending();
     void scale_all();
     void sparsify_rows_all();
@@ -714,54 +745,50 @@ void Engine::rowval(const PRow& r, int key, double& sq, bool& nz, bool post_ok) 
 }
 
 // factorize.cpp:176-271 (selection, keyset, stack layout) and :286-418's
-// structural half (pivots, scatter bookkeeping) — values come later.
-void Engine::elim_pass1(Elim& e) {
-    ProfScope ps_(prof_, HostProf::PASS1);
+// structural half (pivots, scatter bookkeeping) — values come later.  Runs in
+// parallel over eliminations that share no participant front; effects on
+// shared state (holders, npiv) are deferred to the caller.
+void Engine::elim_pass1(Elim& e, Scratch& S) {
     const int c = e.c;
     const int cs = e.cs;
-    e.parts.clear();
-    for (int m : holders_[c].get())
-        if (m != c) e.parts.push_back(m);
-    if (pend(c).find(c) >= 0) e.parts.insert(e.parts.begin(), c);
     const double eps = opt_.eps;
-    // row statistics of the c block of every participant, computed once
     const size_t np = e.parts.size();
-    rv_off_.assign(np + 1, 0);
-    for (size_t pi = 0; pi < np; ++pi) rv_off_[pi + 1] = rv_off_[pi] + pend(e.parts[pi]).rows.size();
-    rv_sq_.resize(rv_off_[np]);
-    rv_nz_.resize(rv_off_[np]);
+    S.rv_off.assign(np + 1, 0);
+    for (size_t pi = 0; pi < np; ++pi) S.rv_off[pi + 1] = S.rv_off[pi] + pend_[pend_id_[e.parts[pi]]].rows.size();
+    S.rv_sq.resize(S.rv_off[np]);
+    S.rv_nz.resize(S.rv_off[np]);
     double mx = 0.0;
     for (size_t pi = 0; pi < np; ++pi) {
-        const PFront& P = pend(e.parts[pi]);
-        row_vals(P, e.parts[pi], c, rv_sq_.data() + rv_off_[pi], rv_nz_.data() + rv_off_[pi], false);
-        for (size_t q = rv_off_[pi]; q < rv_off_[pi + 1]; ++q) mx = std::max(mx, rv_sq_[q]);
+        const PFront& P = pend_[pend_id_[e.parts[pi]]];
+        row_vals(P, e.parts[pi], c, S.rv_sq.data() + S.rv_off[pi], S.rv_nz.data() + S.rv_off[pi], false);
+        for (size_t q = S.rv_off[pi]; q < S.rv_off[pi + 1]; ++q) mx = std::max(mx, S.rv_sq[q]);
     }
     const double tau2 = eps > 0.0 ? mx * eps * eps * 1e-4 : 0.0;
-    std::vector<std::vector<int>>& sel = sel_;
-    if (sel.size() < np) sel.resize(np);
+    if (S.sel.size() < np) S.sel.resize(np);
+    auto& sel = S.sel;
     int total = 0;
     auto select = [&](double floor2) {
         total = 0;
         for (size_t pi = 0; pi < np; ++pi) {
             sel[pi].clear();
-            const size_t o = rv_off_[pi], n = rv_off_[pi + 1] - o;
+            const size_t o = S.rv_off[pi], n = S.rv_off[pi + 1] - o;
             for (size_t q = 0; q < n; ++q)
-                if (floor2 > 0.0 ? rv_sq_[o + q] > floor2 : rv_nz_[o + q]) sel[pi].push_back(static_cast<int>(q));
+                if (floor2 > 0.0 ? S.rv_sq[o + q] > floor2 : S.rv_nz[o + q]) sel[pi].push_back(static_cast<int>(q));
             total += static_cast<int>(sel[pi].size());
         }
     };
     select(tau2);
     if (total < cs && tau2 > 0.0) select(0.0);
     if (total < cs) {
-        record_error(c, "only " + std::to_string(total) + " rows couple " + std::to_string(cs) + " columns");
+        e.err = "only " + std::to_string(total) + " rows couple " + std::to_string(cs) + " columns";
         e.cs = -1;  // marks the failing elimination
         return;
     }
-    std::vector<int>& keyset = scr_keyset_;
+    auto& keyset = S.keyset;
     keyset.clear();
-    for (size_t pi = 0; pi < e.parts.size(); ++pi) {
+    for (size_t pi = 0; pi < np; ++pi) {
         if (sel[pi].empty()) continue;
-        const PFront& P = pend(e.parts[pi]);
+        const PFront& P = pend_[pend_id_[e.parts[pi]]];
         for (const KW& kw : P.keys) {
             const int key = kw.key;
             if (key == c || width(key) == 0 || std::binary_search(keyset.begin(), keyset.end(), key)) continue;
@@ -783,20 +810,19 @@ void Engine::elim_pass1(Elim& e) {
     e.tcols = e.off.back();
     e.total_rows = total;
     e.srows.clear();
-    for (size_t pi = 0; pi < e.parts.size(); ++pi)
-        for (int q : sel[pi]) e.srows.push_back(pend(e.parts[pi]).rows[q]);
-    e.nsel_c = (!e.parts.empty() && e.parts[0] == c) ? static_cast<int>(sel[0].size()) : 0;
+    for (size_t pi = 0; pi < np; ++pi)
+        for (int q : sel[pi]) e.srows.push_back(pend_[pend_id_[e.parts[pi]]].rows[q]);
+    e.nsel_c = (np > 0 && e.parts[0] == c) ? static_cast<int>(sel[0].size()) : 0;
     for (const PRow& r : e.srows)
         if (r.sidx >= 0) throw std::logic_error("spaqr engine: row selected by two eliminations of one stage");
-    // :332-344 pivots
+    // :332-344 pivots (disjoint columns per elimination)
     for (int pos = 0; pos < cs; ++pos) out_.pivot_row[cols_[c][pos]] = e.srows[pos].gid;
-    npiv_ += cs;
-    // :346-418 scatter bookkeeping
+    // :346-418 scatter bookkeeping (participants are exclusive within a colour)
     const int eidx = static_cast<int>(&e - el_.data());
     int roff = 0;
-    for (size_t pi = 0; pi < e.parts.size(); ++pi) {
+    for (size_t pi = 0; pi < np; ++pi) {
         const int m = e.parts[pi];
-        PFront& P = pend(m);
+        PFront& P = pend_[pend_id_[m]];
         const auto& s = sel[pi];
         if (s.empty()) {
             P.erase(c);
@@ -808,10 +834,10 @@ void Engine::elim_pass1(Elim& e) {
                 P.rows[s[i]].srow = roff + static_cast<int>(i);
             }
         } else {
-            std::vector<int>& spos = scr_spos_;
+            auto& spos = S.spos;
             spos.assign(P.rows.size(), -1);
             for (size_t i = 0; i < s.size(); ++i) spos[s[i]] = roff + static_cast<int>(i);
-            std::vector<PRow>& nr = scr_rows_;
+            auto& nr = S.rows;
             nr.clear();
             for (size_t q = 0; q < P.rows.size(); ++q) {
                 if (spos[q] >= 0 && spos[q] < cs) continue;
@@ -826,116 +852,114 @@ void Engine::elim_pass1(Elim& e) {
         }
         for (int key : keyset) {
             P.add(key, width(key));
-            holders_[key].add(m);
+            e.hadd.emplace_back(key, m);
         }
         P.erase(c);
         fr_[m].scaled_ok = false;
         roff += static_cast<int>(s.size());
     }
-    holders_[c].clear();
 }
 
-// :286-323 (W factor with pruned coupling) and :138-174 (move_extras).
-void Engine::elim_pass2(Elim& e, int eidx) {
-    ProfScope ps_(prof_, HostProf::PASS2);
+// :286-323 coupling pruning and :138-174 move_extras decisions (parallel,
+// read-only on shared state).
+void Engine::elim_prep2(Elim& e, Scratch& S) {
     const int c = e.c;
     const int cs = e.cs;
     if (cs > 0) {
         const long long nk = static_cast<long long>(e.keys.size()) - 1;
         double floor_ = 0.0;
         if (opt_.eps > 0.0 && e.tcols > cs) floor_ = post_sq_[e.post_off] * opt_.eps * 1e-2;
-        std::vector<int> coupled;
-        std::vector<int> keepk;
-        int kept = 0;
         for (long long ki = 1; ki <= nk; ++ki) {
             const double mx = post_sq_[e.post_off + ki];
             const bool nz = post_nz_[e.post_off + ki];
-            const bool live = floor_ > 0.0 ? mx > floor_ : nz;
-            if (live) {
-                keepk.push_back(static_cast<int>(ki));
-                kept += width(e.keys[ki]);
-                coupled.insert(coupled.end(), cols_[e.keys[ki]].begin(), cols_[e.keys[ki]].end());
+            if (floor_ > 0.0 ? mx > floor_ : nz) {
+                e.keepk.push_back(static_cast<int>(ki));
+                e.kept += width(e.keys[ki]);
+                e.coupled.insert(e.coupled.end(), cols_[e.keys[ki]].begin(), cols_[e.keys[ki]].end());
             }
         }
-        DevWFactor& f = new_factor(0, c, cs, kept, cols_[c], &coupled);
+    }
+    const PFront& fc = pend_[pend_id_[c]];
+    if (fc.rows.empty()) return;
+    auto& cand = S.cand;
+    cand.clear();
+    for (int m : e.parts)
+        if (m != c && !gone_[m] && fr_[m].live && width(m) > 0 && fc.find(m) >= 0) cand.push_back(m);
+    const size_t nr = fc.rows.size();
+    S.bw.assign(nr, -1.0);
+    S.best.assign(nr, -1);
+    S.rv_sq.resize(nr);
+    S.rv_nz.resize(nr);
+    for (int m : cand) {  // strict > in candidate order == the reference's per-row loop
+        row_vals(fc, c, m, S.rv_sq.data(), S.rv_nz.data(), true);
+        for (size_t q = 0; q < nr; ++q)
+            if (S.rv_sq[q] > S.bw[q]) {
+                S.bw[q] = S.rv_sq[q];
+                S.best[q] = m;
+            }
+    }
+    int anc = -2;
+    for (size_t q = 0; q < nr; ++q) {
+        int b = S.best[q];
+        if (b < 0) {
+            if (anc == -2) anc = ancestor_target(c);
+            b = anc;
+        }
+        if (b < 0)
+            e.trail.push_back(static_cast<int>(q));
+        else
+            e.dest.emplace_back(b, static_cast<int>(q));
+    }
+    std::stable_sort(e.dest.begin(), e.dest.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+}
+
+// W factor + appends, in ascending cluster order (sequential).
+void Engine::elim_commit2(Elim& e) {
+    const int c = e.c;
+    const int cs = e.cs;
+    if (cs > 0) {
+        const int kept = e.kept;
+        DevWFactor& f = new_factor(0, c, cs, kept, cols_[c], &e.coupled);
         f.a = out_.warena->alloc_n<double>(static_cast<size_t>(cs) * (cs + kept));
-        // copy [R | C_kept] from the stack (rows 0..cs-1)
-        const int di = wcopy_.begin(f.a, cs, cs, cs + kept, 1, 1 + static_cast<int>(keepk.size()));
+        const int di = wcopy_.begin(f.a, cs, cs, cs + kept, 1, 1 + static_cast<int>(e.keepk.size()));
         wcopy_.source(di, 0) = AsmSrc{e.S, 1, e.total_rows};
         for (int i = 0; i < cs; ++i) wcopy_.row(di, i) = int4{-1, 0, 0, i};
         wcopy_.seg(di, 0, 0);
         wcopy_.km(di, 0, 0) = 0;
         int o = cs;
-        for (size_t q = 0; q < keepk.size(); ++q) {
+        for (size_t q = 0; q < e.keepk.size(); ++q) {
             wcopy_.seg(di, static_cast<int>(q) + 1, o);
-            wcopy_.km(di, static_cast<int>(q) + 1, 0) = e.off[keepk[q]];
-            o += width(e.keys[keepk[q]]);
+            wcopy_.km(di, static_cast<int>(q) + 1, 0) = e.off[e.keepk[q]];
+            o += width(e.keys[e.keepk[q]]);
         }
     }
-    // move_extras
-    PFront& fc = pend(c);
-    if (!fc.rows.empty()) {
-        std::vector<int>& cand = scr_cand_;
-        cand.clear();
-        for (int m : e.parts)
-            if (m != c && !gone_[m] && fr_[m].live && width(m) > 0 && fc.find(m) >= 0) cand.push_back(m);
-        std::vector<std::pair<int, int>>& dest = scr_dest_;  // (target, row), grouped by target below
-        dest.clear();
-        const size_t nr = fc.rows.size();
-        std::vector<double>& best_w = scr_bw_;
-        std::vector<int>& best = scr_best_;
-        best_w.assign(nr, -1.0);
-        best.assign(nr, -1);
-        rv_sq_.resize(nr);
-        rv_nz_.resize(nr);
-        for (int m : cand) {  // strict > in candidate order == the reference's per-row loop
-            row_vals(fc, c, m, rv_sq_.data(), rv_nz_.data(), true);
-            for (size_t q = 0; q < nr; ++q)
-                if (rv_sq_[q] > best_w[q]) {
-                    best_w[q] = rv_sq_[q];
-                    best[q] = m;
-                }
+    PFront& fc = pend_[pend_id_[c]];
+    for (int q : e.trail) out_.trailing_rows.push_back(fc.rows[q].gid);
+    for (size_t a = 0; a < e.dest.size();) {  // append_rows, factorize.cpp:112-133 (ascending targets)
+        size_t b = a;
+        while (b < e.dest.size() && e.dest[b].first == e.dest[a].first) ++b;
+        const int tgt = e.dest[a].first;
+        PFront& T = pend(tgt);
+        for (const KW& kw : fc.keys) {
+            if (width(kw.key) == 0 || T.find(kw.key) >= 0) continue;
+            T.add(kw.key, width(kw.key));
+            holders_[kw.key].add(tgt);
         }
-        int anc = -2;
-        for (size_t q = 0; q < nr; ++q) {
-            int b = best[q];
-            if (b < 0) {
-                if (anc == -2) anc = ancestor_target(c);
-                b = anc;
-            }
-            if (b < 0)
-                out_.trailing_rows.push_back(fc.rows[q].gid);
-            else
-                dest.emplace_back(b, static_cast<int>(q));
+        // sequential order appends in ascending c: keep groups sorted by their source cluster
+        auto pos = std::upper_bound(T.rows.begin(), T.rows.end(), c, [](int cc, const PRow& r) { return cc < r.tag; });
+        const size_t at = static_cast<size_t>(pos - T.rows.begin());
+        T.rows.insert(pos, b - a, PRow{});
+        for (size_t t = a; t < b; ++t) {
+            PRow r = fc.rows[e.dest[t].second];
+            r.tag = c;
+            T.rows[at + (t - a)] = r;
         }
-        std::stable_sort(dest.begin(), dest.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-        for (size_t a = 0; a < dest.size();) {  // append_rows, factorize.cpp:112-133 (ascending targets)
-            size_t b = a;
-            while (b < dest.size() && dest[b].first == dest[a].first) ++b;
-            const int tgt = dest[a].first;
-            PFront& T = pend(tgt);
-            for (const KW& kw : fc.keys) {
-                if (width(kw.key) == 0 || T.find(kw.key) >= 0) continue;
-                T.add(kw.key, width(kw.key));
-                holders_[kw.key].add(tgt);
-            }
-            // sequential order appends in ascending c: keep groups sorted by their source cluster
-            auto pos = std::upper_bound(T.rows.begin(), T.rows.end(), c, [](int cc, const PRow& r) { return cc < r.tag; });
-            const size_t at = static_cast<size_t>(pos - T.rows.begin());
-            T.rows.insert(pos, b - a, PRow{});
-            for (size_t t = a; t < b; ++t) {
-                PRow r = fc.rows[dest[t].second];
-                r.tag = c;
-                T.rows[at + (t - a)] = r;
-            }
-            fr_[tgt].scaled_ok = false;
-            a = b;
-        }
+        fr_[tgt].scaled_ok = false;
+        a = b;
     }
     for (const KW& kw : fc.keys) holders_[kw.key].remove(c);
     gone_[c] = 1;
     fr_[c].live = false;
-    (void)eidx;
 }
 
 // Materialise every pending (touched, still live) front with one gather.
@@ -1186,16 +1210,78 @@ void Engine::eliminate_stage(int k) {
 }
 
 void Engine::eliminate_wave(const std::vector<int>& list) {
-    if (el_.size() < list.size()) el_.resize(list.size());  // pool: Elim objects keep their capacity
-    // pass 1 over the wave (ascending ids)
+    const size_t n = list.size();
+    if (el_.size() < n) el_.resize(n);  // pool: Elim objects keep their capacity
+    int nth = 1;
+#ifdef _OPENMP
+    nth = omp_get_max_threads();
+#endif
+    if (static_cast<int>(tscr_.size()) < nth) tscr_.resize(nth);
+    // prepass (sequential): participants, pending fronts, conflict colouring
+    // (eliminations of one colour share no participant front)
+    std::vector<std::vector<int>> colour_lists;
+    {
+        ProfScope ps(prof_, HostProf::PASS1);
+        for (size_t t = 0; t < n; ++t) {
+            const int c = list[t];
+            Elim& e = el_[t];
+            e.reset(c, width(c));
+            pend(c);
+            if (e.cs <= 0) continue;
+            for (int m : holders_[c].get())
+                if (m != c) e.parts.push_back(m);
+            if (pend(c).find(c) >= 0) e.parts.insert(e.parts.begin(), c);
+            for (int m : e.parts) pend(m);
+            uint64_t used = 0;
+            for (int m : e.parts) used |= colmask_[m];
+            int col = 0;
+            while (col < 63 && ((used >> col) & 1)) ++col;
+            e.color = col;  // colour 63 collects overflow; it is run sequentially
+            for (int m : e.parts) colmask_[m] |= (uint64_t(1) << col);
+            if (static_cast<int>(colour_lists.size()) <= col) colour_lists.resize(col + 1);
+            colour_lists[col].push_back(static_cast<int>(t));
+        }
+        for (size_t t = 0; t < n; ++t)
+            for (int m : el_[t].parts) colmask_[m] = 0;
+        // pass 1, colour by colour
+        for (size_t col = 0; col < colour_lists.size(); ++col) {
+            const auto& cl = colour_lists[col];
+            const bool par = col < 63 && cl.size() > 16;
+#pragma omp parallel for schedule(dynamic, 8) if (par)
+            for (long long q = 0; q < static_cast<long long>(cl.size()); ++q) {
+                Elim& e = el_[cl[q]];
+                if (e.cs <= 0) continue;
+                int tid = 0;
+#ifdef _OPENMP
+                tid = omp_get_thread_num();
+#endif
+                try {
+                    elim_pass1(e, tscr_[tid]);
+                } catch (const std::exception& x) {
+                    e.logic = true;
+                    e.err = x.what();
+                }
+            }
+        }
+    }
+    for (size_t t = 0; t < n; ++t)
+        if (el_[t].logic) throw std::logic_error(el_[t].err);
+    // the first failing elimination in ascending order stops the sequence
     int nvalid = 0;
-    for (size_t t = 0; t < list.size(); ++t) {
-        const int c = list[t];
-        Elim& e = el_[t];
-        e.reset(c, width(c));
-        if (e.cs > 0) elim_pass1(e);
-        if (e.cs < 0) break;  // "rows couple" error: later eliminations never run
+    for (size_t t = 0; t < n; ++t) {
+        if (el_[t].cs < 0) {
+            record_error(el_[t].c, el_[t].err);
+            break;
+        }
         ++nvalid;
+    }
+    for (int t = 0; t < nvalid; ++t) {
+        Elim& e = el_[t];
+        for (auto& hk : e.hadd) holders_[hk.first].add(hk.second);
+        if (e.cs > 0) {
+            npiv_ += e.cs;
+            holders_[e.c].clear();
+        }
     }
     // gather stacks, QR + apply, post statistics
     ProfScope ps_sb(prof_, HostProf::SBUILD);
@@ -1310,7 +1396,25 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
             }
     }
     raise_if_error();
-    for (int ei = 0; ei < nvalid; ++ei) elim_pass2(el_[ei], ei);
+    {
+        ProfScope ps(prof_, HostProf::PASS2);
+#pragma omp parallel for schedule(dynamic, 8) if (nvalid > 32)
+        for (int t = 0; t < nvalid; ++t) {
+            int tid = 0;
+#ifdef _OPENMP
+            tid = omp_get_thread_num();
+#endif
+            try {
+                elim_prep2(el_[t], tscr_[tid]);
+            } catch (const std::exception& x) {
+                el_[t].logic = true;
+                el_[t].err = x.what();
+            }
+        }
+        for (int t = 0; t < nvalid; ++t)
+            if (el_[t].logic) throw std::logic_error(el_[t].err);
+        for (int t = 0; t < nvalid; ++t) elim_commit2(el_[t]);
+    }
     materialize_pending();
 }
 
@@ -1439,17 +1543,35 @@ void Engine::sparsify_rows_all() {
         if (p2 <= 0) continue;
         const int qi = f.find(p);
         const int c0 = (qi >= 0) ? f.keys[qi].width : 0;
-        const int nw = f.ncols - c0;
+        int nw = 0, nseg = 0;
+        for (const KeyRef& k : f.keys)
+            if (k.key != p && k.width > 0) {
+                nw += k.width;
+                ++nseg;
+            }
         if (nw == 0) {  // keep = 0: every extra row is dropped
             for (int i = cs; i < r; ++i) out_.dropped_rows.push_back(f.rows[i]);
             f.rows.resize(cs);
             continue;
         }
         Job j{p, cs, p2, nw, c0, arena().alloc_n<double>(static_cast<size_t>(p2) * nw)};
-        const int di = gb.begin(j.B, p2, p2, nw, 1, 1);
-        gb.source(di, 0) = AsmSrc{f.mat + cs + static_cast<long long>(c0) * f.ld, 1, f.ld};
+        // B = extra rows x live neighbour columns, ascending keys (physical order)
+        const int di = gb.begin(j.B, p2, p2, nw, 1, nseg);
+        gb.source(di, 0) = AsmSrc{f.mat + cs, 1, f.ld};
         for (int i = 0; i < p2; ++i) gb.row(di, i) = int4{-1, 0, 0, i};
-        gb.km(di, 0, 0) = 0;
+        {
+            std::vector<int> ord;
+            phys_order(f.keys, ord);
+            int sg = 0, bo = 0;
+            for (int q : ord) {
+                const KeyRef& k = f.keys[q];
+                if (k.key == p || k.width == 0) continue;
+                gb.seg(di, sg, bo);
+                gb.km(di, sg, 0) = k.col;
+                bo += k.width;
+                ++sg;
+            }
+        }
         jobs.push_back(j);
         maxm = std::max(maxm, p2);
         out_.ctr.cpqr_bytes += 8.0 * p2 * nw;
@@ -1484,10 +1606,27 @@ void Engine::sparsify_rows_all() {
         for (int r = j.cs + keep; r < j.cs + j.p2; ++r) out_.dropped_rows.push_back(f.rows[r]);
         f.rows.resize(j.cs + keep);
         if (keep == 0) continue;
-        const int di = wb.begin(f.mat + j.cs + static_cast<long long>(j.c0) * f.ld, f.ld, keep, j.nw, 1, 1);
+        // write R back into the live neighbour columns (dead gaps get zeros)
+        std::vector<int> ord;
+        phys_order(f.keys, ord);
+        std::vector<std::pair<int, int>> segs{{0, -1}};  // (dst col relative to c0, B col or -1)
+        int bo = 0;
+        for (size_t t = 0; t < ord.size(); ++t) {
+            const KeyRef& k = f.keys[ord[t]];
+            if (k.key == j.p || k.width == 0) continue;
+            segs.emplace_back(k.col - j.c0, bo);
+            segs.emplace_back(k.col + k.width - j.c0, -1);
+            bo += k.width;
+        }
+        const int dcols = f.ncols - j.c0;
+        const int di = wb.begin(f.mat + j.cs + static_cast<long long>(j.c0) * f.ld, f.ld, keep, dcols, 1,
+                                static_cast<int>(segs.size()));
         wb.source(di, 0) = AsmSrc{j.B, 1, j.p2};
         for (int r = 0; r < keep; ++r) wb.row(di, r) = int4{-1, 0, 0, r};
-        wb.km(di, 0, 0) = 0;
+        for (size_t s = 0; s < segs.size(); ++s) {
+            wb.seg(di, static_cast<int>(s), std::min(segs[s].first, dcols));
+            wb.km(di, static_cast<int>(s), 0) = segs[s].second;
+        }
     }
     flush_assemble(wb);
 }
@@ -1551,6 +1690,7 @@ void Engine::sparsify_cols_all() {
         struct Job {
             int p, cs, nG, wrows, kmax;
             std::vector<int> rparts, seg;  // seg offsets of holders in G
+            std::vector<std::pair<int, int>> kg;  // (neighbour key, its first column in G's own part)
             double* G;
             double *V, *tau, *sign;
         };
@@ -1571,9 +1711,12 @@ void Engine::sparsify_cols_all() {
                 j.seg.push_back(wrows);
                 wrows += fr_[m].nrows();
             }
-            const int qi = f.find(p);
-            const int c0 = (qi >= 0) ? f.keys[qi].width : 0;
-            const int wcols = f.ncols - c0;
+            int wcols = 0;
+            for (const KeyRef& k : f.keys)  // ascending keys = physical order of the neighbour blocks
+                if (k.key != p && k.width > 0) {
+                    j.kg.emplace_back(k.key, wcols);
+                    wcols += k.width;
+                }
             j.wrows = wrows;
             j.nG = wrows + wcols;
             j.kmax = std::min(j.cs, j.nG);
@@ -1593,7 +1736,10 @@ void Engine::sparsify_cols_all() {
                 }
                 const int so = static_cast<int>(j.rparts.size());
                 gb.source(di, so) = AsmSrc{f.mat, f.ld, 1};  // transposed view of p's own rows
-                for (int g = 0; g < wcols; ++g) gb.row(di, wrows + g) = int4{-1, 0, so, c0 + g};
+                for (const auto& kg : j.kg) {
+                    const KeyRef& k = f.keys[f.find(kg.first)];
+                    for (int o = 0; o < k.width; ++o) gb.row(di, wrows + kg.second + o) = int4{-1, 0, so, k.col + o};
+                }
                 gb.km(di, 0, so) = 0;
             }
             j.V = out_.warena->alloc_n<double>(static_cast<size_t>(j.cs) * std::max(j.kmax, 1));
@@ -1702,8 +1848,6 @@ void Engine::sparsify_cols_all() {
             mb.source(di, 1) = AsmSrc{f.mat, 1, f.ld};  // old extra rows
             for (int q = 0; q < r2; ++q) mb.row(di, q) = int4{0, q, -1, 0};
             for (int q = 0; q < p2; ++q) mb.row(di, r2 + q) = int4{1, cs + q, -1, 0};
-            const int qi = f.find(p);
-            const int c0 = (qi >= 0) ? f.keys[qi].width : 0;
             for (size_t q = 0; q < ord.size(); ++q) {
                 const KeyRef& k = nf.keys[ord[q]];
                 mb.seg(di, static_cast<int>(q), k.col);
@@ -1713,7 +1857,10 @@ void Engine::sparsify_cols_all() {
                     continue;
                 }
                 const KeyRef& ok = f.keys[f.find(k.key)];
-                mb.km(di, static_cast<int>(q), 0) = j.wrows + (ok.col - c0);
+                int gofs = -1;
+                for (const auto& kg : j.kg)
+                    if (kg.first == k.key) gofs = kg.second;
+                if (gofs >= 0) mb.km(di, static_cast<int>(q), 0) = j.wrows + gofs;
                 mb.km(di, static_cast<int>(q), 1) = ok.col;
             }
             mb.drop_if_empty();
@@ -1721,54 +1868,28 @@ void Engine::sparsify_cols_all() {
             if (r2 == 0) holders_[p].clear();
             updates.emplace_back(p, std::move(nf));
         }
+        // holders: B_m = (R seg_m)^T written in place into the first r2 columns of
+        // m's p block (the rest of the block becomes dead columns), or the key is
+        // dropped when r2 == 0 — no rebuild of m
         for (auto& [m, edits] : hed) {
-            const Front& f = fr_[m];
-            Front nf;
-            nf.live = true;
-            nf.rows = f.rows;
-            nf.scaled_ok = f.scaled_ok;
-            std::vector<int> gslot_key;  // key p per G slot
-            for (const KeyRef& k : f.keys) {
-                int w = k.width;
-                bool dropped = false;
-                for (auto& [ji, s] : edits)
-                    if (jobs[ji].p == k.key) {
-                        if (s < 0) dropped = true;
-                        w = rank[ji];
-                    }
-                if (!dropped) nf.keys.push_back(KeyRef{k.key, w, 0});
+            Front& fm = fr_[m];
+            for (auto& [ji, s] : edits) {
+                const Job& j = jobs[ji];
+                const int mq = fm.find(j.p);
+                if (s < 0) {
+                    fm.keys.erase(fm.keys.begin() + mq);
+                    continue;
+                }
+                const int r2 = rank[ji];
+                if (fm.nrows() > 0) {
+                    const int di = mb.begin(fm.mat + static_cast<long long>(fm.keys[mq].col) * fm.ld, fm.ld, fm.nrows(), r2,
+                                            1, 1);
+                    mb.source(di, 0) = AsmSrc{j.G + static_cast<long long>(j.seg[s]) * j.cs, j.cs, 1};
+                    for (int q = 0; q < fm.nrows(); ++q) mb.row(di, q) = int4{-1, 0, 0, q};
+                    mb.km(di, 0, 0) = 0;
+                }
+                fm.keys[mq].width = r2;
             }
-            layout(m, nf.keys, nf.ncols);
-            nf.ld = std::max(1, nf.nrows());
-            nf.mat = arena().alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
-            std::vector<std::pair<int, int>> live_edits;
-            for (auto& e : edits)
-                if (e.second >= 0) live_edits.push_back(e);
-            const int nsrc = static_cast<int>(live_edits.size()) + 1;
-            std::vector<int> ord;
-            phys_order(nf.keys, ord);
-            const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, nsrc, static_cast<int>(ord.size()));
-            for (size_t s = 0; s < live_edits.size(); ++s) {
-                const Job& j = jobs[live_edits[s].first];
-                // B_m(q, i) = R(i, seg + q) = G[i + (seg+q)*cs]
-                mb.source(di, static_cast<int>(s)) =
-                    AsmSrc{j.G + static_cast<long long>(j.seg[live_edits[s].second]) * j.cs, j.cs, 1};
-            }
-            mb.source(di, static_cast<int>(live_edits.size())) = AsmSrc{f.mat, 1, f.ld};
-            for (int q = 0; q < nf.nrows(); ++q) mb.row(di, q) = int4{-2, q, -1, 0};
-            for (size_t q = 0; q < ord.size(); ++q) {
-                const KeyRef& k = nf.keys[ord[q]];
-                mb.seg(di, static_cast<int>(q), k.col);
-                int gs = -1;
-                for (size_t s = 0; s < live_edits.size(); ++s)
-                    if (jobs[live_edits[s].first].p == k.key) gs = static_cast<int>(s);
-                if (gs >= 0)
-                    mb.km(di, static_cast<int>(q), gs) = 0;
-                else
-                    mb.km(di, static_cast<int>(q), static_cast<int>(live_edits.size())) = f.keys[f.find(k.key)].col;
-            }
-            mb.drop_if_empty();
-            updates.emplace_back(m, std::move(nf));
         }
         sc3.reset();
         {
@@ -1953,6 +2074,7 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         st.stage = k;
         sprof_.emplace_back();
         sprof_.back().stage = k;
+        const HostProf before = prof_;
         double t0 = now_s();
         eliminate_stage(k);
         st.t_eliminate = now_s() - t0;
@@ -1975,6 +2097,7 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         }
         st.nnz_w = out_.nnz_w();
         out_.stages.push_back(st);
+        for (int i = 0; i < HostProf::N; ++i) sprof_.back().t[i] = prof_.t[i] - before.t[i];
     }
     for (size_t c = 0; c < fr_.size(); ++c)
         if (fr_[c].live) out_.trailing_rows.insert(out_.trailing_rows.end(), fr_[c].rows.begin(), fr_[c].rows.end());
@@ -1984,6 +2107,14 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         for (int i = 0; i < HostProf::N; ++i)
             std::fprintf(stderr, "[spqr prof] %-14s %8.3f s  (%lld)\n", HostProf::name(i), prof_.t[i], prof_.n[i]);
         for (auto& p : nprof_.v) std::fprintf(stderr, "[spqr prof]   %-28s %8.3f s\n", p.first, p.second);
+        std::fprintf(stderr, "[spqr prof] per stage:");
+        for (int i = 0; i < HostProf::N; ++i) std::fprintf(stderr, " %s", HostProf::name(i));
+        std::fprintf(stderr, "\n");
+        for (auto& sp : sprof_) {
+            std::fprintf(stderr, "[spqr prof] stage %2d", sp.stage);
+            for (int i = 0; i < HostProf::N; ++i) std::fprintf(stderr, " %6.3f", sp.t[i]);
+            std::fprintf(stderr, "\n");
+        }
         for (auto& sp : sprof_)
             std::fprintf(stderr,
                          "[spqr prof] stage %2d waves %3d scol_waves %3d elims %6lld S_elems %10lld S_max %lldx%lld | "
