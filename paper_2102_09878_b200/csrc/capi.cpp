@@ -7,7 +7,11 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <numeric>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #include "dev.h"
 #include "engine.h"
@@ -90,6 +94,14 @@ int spqr_pipeline_create(int m, int n, const int* colptr, const int* rowind, con
     *out = nullptr;
     auto* P = new spqr_pipeline;
     const int rc = guarded(err, errlen, err_cluster, [&] {
+#ifdef _OPENMP
+        // host bookkeeping threads: leave headroom for the CUDA driver and the
+        // orchestrating thread unless the user chose a count
+        if (!std::getenv("OMP_NUM_THREADS")) {
+            const int np = omp_get_num_procs();
+            omp_set_num_threads(std::max(1, std::min(12, np - 2)));
+        }
+#endif
         P->device = device;
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
