@@ -343,21 +343,35 @@ int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, doubl
                               float* ms) {
     int cl = -1;
     return guarded(nullptr, 0, &cl, [&] {
-        if (n > m || ntot < n || n > 1024) throw std::invalid_argument("qr: need n <= m, n <= ntot, n <= 1024");
-        std::vector<QrDesc> qd(nb);
-        for (int b = 0; b < nb; ++b)
-            qd[b] = QrDesc{d_a + static_cast<long long>(b) * m * ntot, m, m, n, ntot, d_tau + static_cast<long long>(b) * n,
-                           d_sign + static_cast<long long>(b) * n, nullptr, d_info + b, 0, 0};
-        QrDesc* dq = nullptr;
-        CK(cudaMalloc(&dq, sizeof(QrDesc) * std::max(nb, 1)));
-        CK(cudaMemcpy(dq, qd.data(), sizeof(QrDesc) * nb, cudaMemcpyHostToDevice));
+        if (n > m || ntot < n) throw std::invalid_argument("qr: need n <= m and n <= ntot");
         std::vector<int> init(nb, INT_MAX);
         CK(cudaMemcpy(d_info, init.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
+        const bool staged = qr_smem_bytes(m, n, ntot) <= kSmemBudget && n <= 1024;
+        QrDesc* dq = nullptr;
+        int* didx = nullptr;
+        double* dT = nullptr;
+        if (staged) {
+            std::vector<QrDesc> qd(nb);
+            for (int b = 0; b < nb; ++b)
+                qd[b] = QrDesc{d_a + static_cast<long long>(b) * m * ntot, m, m, n, ntot, d_tau + static_cast<long long>(b) * n,
+                               d_sign + static_cast<long long>(b) * n, nullptr, d_info + b, 0, 0};
+            std::vector<int> all(nb);
+            for (int b = 0; b < nb; ++b) all[b] = b;
+            CK(cudaMalloc(&dq, sizeof(QrDesc) * std::max(nb, 1)));
+            CK(cudaMalloc(&didx, sizeof(int) * std::max(nb, 1)));
+            CK(cudaMemcpy(dq, qd.data(), sizeof(QrDesc) * nb, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(didx, all.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
+        } else {
+            CK(cudaMalloc(&dT, sizeof(double) * 32 * 32 * std::max(nb, 1)));
+        }
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, 0));
-        launch_qr(dq, nb, m, 0);
+        if (staged)
+            launch_qr_split(dq, didx, nb, qr_smem_bytes(m, n, ntot), nullptr, 0, 0);
+        else
+            blocked_qr_apply(nb, m, n, ntot, d_a, d_tau, d_sign, d_info, dT, 0);
         CK(cudaEventRecord(e1, 0));
         CK(cudaEventSynchronize(e1));
         CK(cudaGetLastError());
@@ -366,7 +380,9 @@ int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, doubl
         if (ms) *ms = t;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        cudaFree(dq);
+        if (dq) cudaFree(dq);
+        if (didx) cudaFree(didx);
+        if (dT) cudaFree(dT);
     });
 }
 

@@ -139,6 +139,11 @@ void launch_axpy_dev(int n, const double* alpha, double sgn, const double* x, do
 void launch_cgls_p_update(int n, const double* s, const double* gnew, const double* gold, double* p, cudaStream_t st);
 void launch_copy(int n, const double* a, double* b, cudaStream_t st);
 
+// blocked batched QR + compact-WY apply (mbqr.cu) for fronts too large to stage:
+// d_T needs nbatch * 32 * 32 doubles of scratch
+void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d_tau, double* d_sign, int* d_info,
+                      double* d_T, cudaStream_t st);
+
 int sm_count();
 
 }  // namespace spqr

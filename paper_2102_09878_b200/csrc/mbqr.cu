@@ -1,0 +1,348 @@
+// Blocked batched Householder QR + compact-WY apply for large fronts on B200.
+//
+// Reference semantics: block_householder_qr (Eigen HouseholderQR, makeHouseholder
+// convention) + apply_reflectors_left_t on the neighbour block
+// (proj/src/dense_kernels.cpp:11-99).  The reference applies Q^T to the
+// neighbour block through the compact-WY form H = I - V T V^T with T built by
+// accumulate_wy (:41-53); here every panel of NB columns is factored once,
+// its T is built the same way, and the panel's block reflector is applied to
+// all trailing columns (the rest of the front and the neighbour block) as
+// DMMA (mma.sync.m8n8k4.f64) GEMMs:  W = V^T C,  W = T^T W,  C -= V W.
+// The final nonnegative-diagonal flip (dense_kernels.cpp:29-34, 89-92) is a
+// separate row-flip pass.
+#include <cfloat>
+#include <climits>
+#include <cmath>
+
+#include "dev.h"
+
+namespace spqr {
+
+namespace {
+
+constexpr int NB = 32;      // panel width
+constexpr int CH = 64;      // row chunk staged per step
+// padded leading dims: every DMMA fragment load (t4 + 4g or g + 8t4 patterns
+// mod 16 doubles) touches 16 distinct bank pairs, i.e. the 2-wavefront minimum
+constexpr int LDV = CH + 4;   // V chunk, (row, col) at row + col*LDV      (pass 1: A = V^T)
+constexpr int LDVT = NB + 4;  // V chunk transposed, (row, col) at col + row*LDVT (pass 2: A = V)
+constexpr int LDC = CH + 4;
+constexpr int LDW = NB + 4;
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// Panel factorisation: columns [j0, j0+w) of problem b, rows [j0, m).
+// Lane j of every warp owns panel column j; the NWP warps split the rows.  The
+// panel lives in shared memory (ld = rows + 1, conflict-free column walks) when
+// it fits, else in place in HBM.  Writes V below the diagonal, beta on it,
+// tau, and the compact-WY factor T (w x w, accumulate_wy order).
+template <int NWP>
+__global__ void __launch_bounds__(32 * NWP) k_panel(double* __restrict__ a, int ld, long long stride, int m, int j0,
+                                                    int w, double* __restrict__ tau_all, int tau_stride,
+                                                    double* __restrict__ T_all, int smem_rows) {
+    const int b = blockIdx.x;
+    double* A = a + b * stride;
+    double* tau = tau_all + static_cast<long long>(b) * tau_stride;
+    double* T = T_all + static_cast<long long>(b) * NB * NB;
+    extern __shared__ double sm[];
+    __shared__ double part[NWP][NB + 1];
+    __shared__ double G[NB * NB];
+    __shared__ double s_tau, s_den;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int rows = m - j0;
+    const bool staged = rows <= smem_rows;
+    double* P;
+    int pld;
+    if (staged) {
+        P = sm;
+        pld = rows + 1;
+        for (int e = threadIdx.x; e < rows * w; e += blockDim.x) {
+            const int i = e % rows, j = e / rows;
+            P[i + j * pld] = A[(j0 + i) + static_cast<long long>(j0 + j) * ld];
+        }
+        __syncthreads();
+    } else {
+        P = A + j0 + static_cast<long long>(j0) * ld;
+        pld = ld;
+    }
+    // row range of this warp
+    const int per = (rows + NWP - 1) / NWP;
+    const int r_lo = wid * per, r_hi = min(rows, r_lo + per);
+    double* pj = P + static_cast<long long>(lane) * pld;  // this lane's column
+    for (int k = 0; k < w; ++k) {
+        const double* pk = P + static_cast<long long>(k) * pld;
+        // tail norm^2 of column k over rows > k: lane-strided within the warp's range
+        double s = 0.0;
+        for (int i = max(r_lo, k + 1) + lane; i < r_hi; i += 32) s = fma(pk[i], pk[i], s);
+        s = wsum(s);
+        if (NWP > 1) {
+            if (lane == 0) part[wid][0] = s;
+            __syncthreads();
+            s = 0.0;
+            for (int q = 0; q < NWP; ++q) s += part[q][0];
+        }
+        if (threadIdx.x == 0) {
+            const double c0 = pk[k];
+            double t = 0.0, den = 0.0;
+            if (!(s <= DBL_MIN)) {
+                double beta = sqrt(c0 * c0 + s);
+                if (c0 >= 0.0) beta = -beta;
+                den = c0 - beta;
+                t = (beta - c0) / beta;
+                P[k + static_cast<long long>(k) * pld] = beta;
+            }
+            s_tau = t;
+            s_den = den;
+            tau[j0 + k] = t;
+        }
+        __syncthreads();
+        const double t = s_tau, den = s_den;
+        double* pkw = P + static_cast<long long>(k) * pld;
+        for (int i = max(r_lo, k + 1) + lane; i < r_hi; i += 32) pkw[i] = (t == 0.0) ? 0.0 : pkw[i] / den;
+        __syncthreads();
+        if (t != 0.0) {
+            // dots of v_k with every later column (lane = column), rows of this warp
+            double d = 0.0;
+            const double pjk = (lane > k && lane < w) ? pj[k] : 0.0;  // read before anyone updates row k
+            if (lane > k && lane < w)
+                for (int i = max(r_lo, k + 1); i < r_hi; ++i) d = fma(pkw[i], pj[i], d);
+            if (NWP > 1) {
+                part[wid][lane] = d;
+                __syncthreads();
+                d = 0.0;
+                for (int q = 0; q < NWP; ++q) d += part[q][lane];
+            }
+            if (lane > k && lane < w) {
+                const double tw = t * (d + pjk);
+                if (r_lo <= k && k < r_hi) pj[k] -= tw;
+                for (int i = max(r_lo, k + 1); i < r_hi; ++i) pj[i] = fma(-tw, pkw[i], pj[i]);
+            }
+        }
+        __syncthreads();
+    }
+    // Gram matrix of the unit-lower V (dense_kernels.cpp:41-53 needs V^T v_j): lane = column j
+    for (int i = 0; i < w; ++i) {
+        double g = 0.0;
+        if (lane > i && lane < w)
+            for (int r = max(r_lo, lane); r < r_hi; ++r) {
+                const double vi = P[r + static_cast<long long>(i) * pld];  // r >= lane > i
+                const double vj = (r == lane) ? 1.0 : pj[r];
+                g = fma(vi, vj, g);
+            }
+        if (NWP > 1) {
+            part[wid][lane] = g;
+            __syncthreads();
+            if (wid == 0) {
+                g = 0.0;
+                for (int q = 0; q < NWP; ++q) g += part[q][lane];
+            }
+            __syncthreads();
+        }
+        if (wid == 0 && lane > i && lane < w) G[i + lane * NB] = g;
+    }
+    __syncthreads();
+    if (wid == 0) {  // T column by column (upper triangular); lane i computes T(i, j)
+        for (int e = lane; e < NB * NB; e += 32) T[e] = 0.0;
+        __syncwarp();
+        for (int j = 0; j < w; ++j) {
+            const double tj = tau[j0 + j];
+            if (tj == 0.0) continue;
+            double s = 0.0;
+            if (lane < j)
+                for (int q = lane; q < j; ++q) s = fma(T[lane + q * NB], G[q + j * NB], s);
+            __syncwarp();
+            if (lane < j) T[lane + j * NB] = -tj * s;
+            if (lane == 0) T[j + j * NB] = tj;
+            __syncwarp();
+        }
+    }
+    if (staged) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < rows * w; e += blockDim.x) {
+            const int i = e % rows, j = e / rows;
+            A[(j0 + i) + static_cast<long long>(j0 + j) * ld] = P[i + j * pld];
+        }
+    }
+}
+
+// Block reflector on a TC-column tile of the trailing matrix:
+//   W = V^T C (w x TC), W = T^T W, C -= V W.   16 warps, DMMA 8x8x4.
+constexpr int TC2 = 128;
+__global__ void __launch_bounds__(512) k_wy(double* __restrict__ a, int ld, long long stride, int m, int ntot, int j0,
+                                            int w, const double* __restrict__ T_all) {
+    const int b = blockIdx.y;
+    double* A = a + b * stride;
+    const double* T = T_all + static_cast<long long>(b) * NB * NB;
+    const int c0 = j0 + w + blockIdx.x * TC2;  // first column of this tile
+    const int nc = min(TC2, ntot - c0);
+    if (nc <= 0) return;
+    extern __shared__ double dsm[];
+    double* sV = dsm;                  // V chunk (CH x NB), column-major, ld LDV
+    double* sC = sV + NB * LDV;        // C chunk (CH x TC2), column-major, ld LDC
+    double* sW = sC + TC2 * LDC;       // W (NB x TC2), column-major, ld LDW
+    double* sT = sW + TC2 * LDW;
+    double* sVt = sT + NB * LDW;       // V chunk transposed (pass 2)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+        const int i = e % NB, j = e / NB;
+        sT[i + j * LDW] = (i < w && j < w) ? T[e] : 0.0;
+    }
+    const int rows = m - j0;
+    auto load_chunk = [&](int r0, int rc, bool transposed) {
+        for (int e = threadIdx.x; e < CH * NB; e += blockDim.x) {
+            const int i = e % CH, j = e / CH;
+            const int r = r0 + i;
+            double v = 0.0;
+            if (i < rc && j < w) v = (r > j) ? A[(j0 + r) + static_cast<long long>(j0 + j) * ld] : (r == j ? 1.0 : 0.0);
+            if (transposed)
+                sVt[j + i * LDVT] = v;
+            else
+                sV[i + j * LDV] = v;
+        }
+        for (int e = threadIdx.x; e < CH * TC2; e += blockDim.x) {
+            const int i = e % CH, j = e / CH;
+            sC[i + j * LDC] = (i < rc && j < nc) ? A[(j0 + r0 + i) + static_cast<long long>(c0 + j) * ld] : 0.0;
+        }
+    };
+    // ---- pass 1: W = V^T C; warp: W rows (wid&3)*8.., cols (wid>>2)*32.. (4 tiles)
+    double acc[4][2] = {};
+    const int mr = (wid & 3) * 8, nc0 = (wid >> 2) * 32;
+    for (int r0 = 0; r0 < rows; r0 += CH) {
+        const int rc = min(CH, rows - r0);
+        __syncthreads();
+        load_chunk(r0, rc, false);
+        __syncthreads();
+#pragma unroll 4
+        for (int k0 = 0; k0 < CH; k0 += 4) {
+            const double av = sV[(k0 + t4) + (mr + g) * LDV];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dmma(acc[q][0], acc[q][1], av, sC[(k0 + t4) + (nc0 + q * 8 + g) * LDC]);
+        }
+    }
+    __syncthreads();
+    for (int q = 0; q < 4; ++q) {
+        sW[(mr + g) + (nc0 + q * 8 + 2 * t4) * LDW] = acc[q][0];
+        sW[(mr + g) + (nc0 + q * 8 + 2 * t4 + 1) * LDW] = acc[q][1];
+    }
+    __syncthreads();
+    // ---- W2 = T^T W
+    double acc2[4][2] = {};
+#pragma unroll
+    for (int k0 = 0; k0 < NB; k0 += 4) {
+        const double av = sT[(k0 + t4) + (mr + g) * LDW];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dmma(acc2[q][0], acc2[q][1], av, sW[(k0 + t4) + (nc0 + q * 8 + g) * LDW]);
+    }
+    __syncthreads();
+    for (int q = 0; q < 4; ++q) {
+        sW[(mr + g) + (nc0 + q * 8 + 2 * t4) * LDW] = acc2[q][0];
+        sW[(mr + g) + (nc0 + q * 8 + 2 * t4 + 1) * LDW] = acc2[q][1];
+    }
+    // ---- pass 2: C -= V W2; warp: chunk rows (wid&7)*8.., cols (wid>>3)*64.. (8 tiles)
+    const int rr = (wid & 7) * 8, cc0 = (wid >> 3) * 64;
+    for (int r0 = 0; r0 < rows; r0 += CH) {
+        const int rc = min(CH, rows - r0);
+        __syncthreads();
+        load_chunk(r0, rc, true);
+        __syncthreads();
+        double o[8][2];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            o[q][0] = -sC[(rr + g) + (cc0 + q * 8 + 2 * t4) * LDC];
+            o[q][1] = -sC[(rr + g) + (cc0 + q * 8 + 2 * t4 + 1) * LDC];
+        }
+#pragma unroll
+        for (int k0 = 0; k0 < NB; k0 += 4) {
+            const double av = sVt[(k0 + t4) + (rr + g) * LDVT];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) dmma(o[q][0], o[q][1], av, sW[(k0 + t4) + (cc0 + q * 8 + g) * LDW]);
+        }
+        const int i = rr + g;
+        if (i < rc)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int ja = cc0 + q * 8 + 2 * t4, jb = ja + 1;
+                if (ja < nc) A[(j0 + r0 + i) + static_cast<long long>(c0 + ja) * ld] = -o[q][0];
+                if (jb < nc) A[(j0 + r0 + i) + static_cast<long long>(c0 + jb) * ld] = -o[q][1];
+            }
+    }
+}
+
+// nonnegative diagonal: flip rows of R (cols i..) and of the neighbour block;
+// sign and first zero/denormal pivot per problem
+__global__ void k_flip(double* __restrict__ a, int ld, long long stride, int n, int ntot, double* __restrict__ sign_all,
+                       int* __restrict__ info) {
+    const int b = blockIdx.y;
+    double* A = a + b * stride;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ntot; j += gridDim.x * blockDim.x) {
+        const int top = j < n ? j + 1 : n;
+        for (int i = 0; i < top; ++i)
+            if (A[i + static_cast<long long>(i) * ld] < 0.0 && i != j) A[i + static_cast<long long>(j) * ld] = -A[i + static_cast<long long>(j) * ld];
+    }
+    __syncthreads();
+    if (blockIdx.x == 0) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const double r = A[i + static_cast<long long>(i) * ld];
+            sign_all[static_cast<long long>(b) * n + i] = r < 0.0 ? -1.0 : 1.0;
+            if (!(fabs(r) >= DBL_MIN)) atomicMin(info + b, i);
+        }
+    }
+}
+
+__global__ void k_flip_diag(double* __restrict__ a, int ld, long long stride, int n) {
+    const int b = blockIdx.x;
+    double* A = a + b * stride;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double* d = A + i + static_cast<long long>(i) * ld;
+        if (*d < 0.0) *d = -*d;
+    }
+}
+
+}  // namespace
+
+// nb problems, each m x ntot column-major (ld = m, packed), QR of the first n
+// columns + H^T applied to the rest; tau/sign n per problem; info per problem.
+void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d_tau, double* d_sign, int* d_info,
+                      double* d_T, cudaStream_t st) {
+    const long long stride = static_cast<long long>(m) * ntot;
+    const size_t smem_cap = 160 * 1024;
+    for (int j0 = 0; j0 < n; j0 += NB) {
+        const int w = std::min(NB, n - j0);
+        const int rows = m - j0;
+        const int smem_rows = static_cast<int>(smem_cap / (sizeof(double) * NB)) - 1;
+        const size_t smem = rows <= smem_rows ? sizeof(double) * (rows + 1) * w : 0;
+        if (rows <= 256) {
+            if (smem > 48 * 1024) cudaFuncSetAttribute(k_panel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k_panel<1><<<nbatch, 32, smem, st>>>(d_a, m, stride, m, j0, w, d_tau, n, d_T, smem_rows);
+        } else if (rows <= 1024) {
+            if (smem > 48 * 1024) cudaFuncSetAttribute(k_panel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k_panel<4><<<nbatch, 128, smem, st>>>(d_a, m, stride, m, j0, w, d_tau, n, d_T, smem_rows);
+        } else {
+            if (smem > 48 * 1024) cudaFuncSetAttribute(k_panel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k_panel<16><<<nbatch, 512, smem, st>>>(d_a, m, stride, m, j0, w, d_tau, n, d_T, smem_rows);
+        }
+        const int trail = ntot - (j0 + w);
+        if (trail > 0) {
+            dim3 grid((trail + TC2 - 1) / TC2, nbatch);
+            const size_t wsm = sizeof(double) * (NB * LDV + TC2 * LDC + TC2 * LDW + NB * LDW + CH * LDVT);
+            cudaFuncSetAttribute(k_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm));
+            k_wy<<<grid, 512, wsm, st>>>(d_a, m, stride, m, ntot, j0, w, d_T);
+        }
+    }
+    dim3 g2((ntot + 255) / 256, nbatch);
+    k_flip<<<g2, 256, 0, st>>>(d_a, m, stride, n, ntot, d_sign, d_info);
+    k_flip_diag<<<nbatch, 256, 0, st>>>(d_a, m, stride, n);
+}
+
+}  // namespace spqr

@@ -13,7 +13,9 @@ def _P():
     return P
 
 
-@pytest.mark.parametrize("shape", [(1, 1, 1), (5, 3, 3), (20, 7, 30), (40, 12, 60), (128, 32, 288), (300, 64, 96)])
+@pytest.mark.parametrize("shape", [(1, 1, 1), (5, 3, 3), (20, 7, 30), (40, 12, 60), (128, 32, 288), (300, 64, 96),
+                                   # blocked compact-WY path (block too large to stage on chip)
+                                   (300, 40, 140), (513, 70, 200), (512, 128, 384)])
 def test_qr_apply_matches_oracle(shape):
     m, n, ntot = shape
     rng = np.random.default_rng(m * 131 + n)
