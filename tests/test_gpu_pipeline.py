@@ -133,3 +133,51 @@ def test_singular_front_errors_match_reference():
     with pytest.raises(_P().SingularFrontError) as e:
         _P().Pipeline(sp.csc_matrix(D), eps=0.0, levels=1, parts=[0, 0, 0, 1, 1, 1, 1])
     assert "pivot" in str(e.value) and e.value.cluster >= 0
+
+
+def _solve_parity(o, g, p):
+    xo, ro = o.solve(p.b)
+    xg, rg = g.solve(p.b)
+    assert rg["converged"] == ro["converged"]
+    assert abs(rg["iterations"] - ro["iterations"]) <= 1
+    A = p.A
+    rel = lambda x: np.linalg.norm(A.T @ (p.b - A @ x)) / np.linalg.norm(A.T @ p.b)
+    assert abs(rel(xg) - rel(xo)) <= 1e-10
+    return rg
+
+
+def test_config3_3d_small_parity():  # BASELINE config 3 construction at n=16 (4096 unknowns, M=3N)
+    from paper_2102_09878_b200.problems import tall_grid as tg
+    p = tg(16, dim=3, seed=3)
+    kw = dict(eps=1e-2, levels=6, coords=p.coords)
+    o, g = _pair(p.A, **kw)
+    _compare_structure(o, g)
+    assert o.nnz_w == g.nnz_w and o.nW == g.nW
+    _solve_parity(o, g, p)
+
+
+def test_config4_knn_small_parity():  # BASELINE config 4 construction at N=4096 (M=4N, 4 exact NNs)
+    from paper_2102_09878_b200.problems import knn_geometric
+    p = knn_geometric(4096, seed=4, levels=6)
+    kw = dict(eps=1e-2, levels=6, coords=p.coords)
+    o, g = _pair(p.A, **kw)
+    _compare_structure(o, g)
+    assert o.nnz_w == g.nnz_w and o.nW == g.nW
+    _solve_parity(o, g, p)
+
+
+@pytest.mark.timeout(900)
+def test_config2_full_size_parity():  # the headline problem at full size (oracle ~25-60 s)
+    p = tall_grid(512)
+    o, g = _pair(p.A, eps=p.eps, levels=p.levels, coords=p.coords)
+    _compare_structure(o, g)
+    assert o.nnz_w == g.nnz_w and o.nW == g.nW
+    po, do, to = o.rows()
+    pg, dg, tg_ = g.rows()
+    assert np.array_equal(po, pg) and np.array_equal(np.sort(do), np.sort(dg))
+    rg = _solve_parity(o, g, p)
+    assert rg["residual_history"][-1] <= 1e-12
+    # size-independent properties of W at full size
+    z = np.random.default_rng(0).uniform(-1, 1, g.N)
+    assert np.linalg.norm(g.w_solve(g.w_apply(z)) - z) <= 1e-12 * np.linalg.norm(z)
+    assert np.linalg.norm(g.wt_solve(g.wt_apply(z)) - z) <= 1e-12 * np.linalg.norm(z)
