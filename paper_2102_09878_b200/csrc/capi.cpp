@@ -427,14 +427,16 @@ int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* ra
         int* dp = mem.alloc_n<int>(std::max(nb * kmax, 1));
         int* dr = mem.alloc_n<int>(std::max(nb, 1));
         double* d11 = mem.alloc_n<double>(std::max(nb, 1));
-        double* work = mem.alloc_n<double>(std::max<size_t>(static_cast<size_t>(nb) * 3 * n, 1));
+        const bool big = 8ull * m * n > kBigCpqrBytes && m >= 32 && 8ull * n <= 200 * 1024;
+        const size_t wstride = big ? cpqr_big_work_doubles(n) : 3 * static_cast<size_t>(n);
+        double* work = mem.alloc_n<double>(std::max<size_t>(static_cast<size_t>(nb) * wstride, 1));
         CK(cudaMemcpy(da, a, sizeof(double) * na, cudaMemcpyHostToDevice));
         CK(cudaMemset(dV, 0, sizeof(double) * static_cast<size_t>(nb) * m * kmax));
         std::vector<CpqrDesc> cd(nb);
         for (int b = 0; b < nb; ++b)
             cd[b] = CpqrDesc{da + static_cast<long long>(b) * m * n, m, m, n, eps, dr + b, d11 + b,
                              dV + static_cast<long long>(b) * m * kmax, m, dt + b * kmax, ds + b * kmax, dp + b * kmax,
-                             work + static_cast<long long>(b) * 3 * n};
+                             work + static_cast<long long>(b) * wstride};
         CpqrDesc* dc = mem.alloc_n<CpqrDesc>(std::max(nb, 1));
         CK(cudaMemcpy(dc, cd.data(), sizeof(CpqrDesc) * nb, cudaMemcpyHostToDevice));
         std::vector<int> all(nb);
@@ -442,7 +444,9 @@ int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* ra
         int* didx = mem.alloc_n<int>(std::max(nb, 1));
         CK(cudaMemcpy(didx, all.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
         const size_t sm = cpqr_smem_bytes(m, n);
-        if (sm <= kSmemBudget)
+        if (big)
+            for (int b = 0; b < nb; ++b) launch_cpqr_big(cd[b], 0);
+        else if (sm <= kSmemBudget)
             launch_cpqr_split(dc, didx, nb, sm, nullptr, 0, m, 0);
         else
             launch_cpqr_split(dc, nullptr, 0, 0, didx, nb, m, 0);

@@ -47,8 +47,26 @@ struct StatDesc {
     const double* p;
     int ld, r0, nrows, c0, ncols, mode;
     long long out_off;
-    long long work_off;  // exclusive prefix of (mode 0 ? nrows : 1)
+    long long work_off;  // see layout_stats
 };
+
+// Assigns work_off: mode 0 = one thread per row; modes 1/2 = warps of 32
+// threads, 256 elements per warp, starting 32-aligned.  Returns the total.
+inline long long layout_stats(StatDesc* v, size_t n) {
+    long long w = 0;
+    for (size_t i = 0; i < n; ++i) {
+        StatDesc& d = v[i];
+        if (d.mode == 0) {
+            d.work_off = w;
+            w += d.nrows;
+        } else {
+            w = (w + 31) & ~31LL;
+            d.work_off = w;
+            w += 32 * ((static_cast<long long>(d.nrows) * d.ncols + 255) / 256);
+        }
+    }
+    return w;
+}
 
 // ---- batched Householder QR of the first n columns of an m x ntot block,
 // reflectors applied (H^T, then the sign flip) to columns [n, ntot).  Eigen's
@@ -142,7 +160,15 @@ void launch_copy(int n, const double* a, double* b, cudaStream_t st);
 // blocked batched QR + compact-WY apply (mbqr.cu) for fronts too large to stage:
 // d_T needs nbatch * 32 * 32 doubles of scratch
 void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d_tau, double* d_sign, int* d_info,
-                      double* d_T, cudaStream_t st);
+                      double* d_T, cudaStream_t st, int ld = 0);
+void blocked_qr_post(double* a, int ld, int m, int n, double* rout, int set_identity, int zero_lower, cudaStream_t st);
+constexpr size_t kBlockedQrBytes = size_t(2) << 20;  // fronts above this use the blocked DMMA path
+
+// grid-cooperative CPQR of one large problem (cpqr_big.cu); d.work needs
+// cpqr_big_work_doubles(n) doubles
+void launch_cpqr_big(const CpqrDesc& d, cudaStream_t st);
+inline size_t cpqr_big_work_doubles(int n) { return 3 * static_cast<size_t>(n) + 2 * 512 + 16; }
+constexpr size_t kBigCpqrBytes = size_t(2) << 20;
 
 int sm_count();
 

@@ -57,6 +57,7 @@ struct Front {
     std::vector<int> rows;
     std::vector<KeyRef> keys;  // ascending key; device layout: own key first, then ascending
     double* mat = nullptr;
+    bool big = false;  // mat from cudaMallocAsync (released stream-ordered when superseded)
     int ld = 0, ncols = 0;
     bool scaled_ok = false;
     std::vector<long long> soff;  // pre-stage row statistics offset per key (eliminate)
@@ -222,6 +223,7 @@ struct Elim {
     std::vector<PRow> srows;
     int total_rows = 0, tcols = 0, nsel_c = 0;
     double* S = nullptr;
+    bool sbig = false;
     int* flag = nullptr;  // device
     // deferred effects of the parallel host passes
     std::vector<std::pair<int, int>> hadd;  // holders_[key].add(front)
@@ -249,6 +251,7 @@ struct Elim {
         srows.clear();
         total_rows = tcols = nsel_c = 0;
         S = nullptr;
+        sbig = false;
         flag = nullptr;
         post_off = -1;
     }
@@ -355,6 +358,14 @@ public:
         }
         tree_clusters_.resize(h.tree->nodes.size());
         for (size_t c = 0; c < nc; ++c) tree_clusters_[h.clusters[c].tree_node].push_back(static_cast<int>(c));
+        {
+            int dev = 0;
+            CK(cudaGetDevice(&dev));
+            cudaMemPool_t pool;
+            CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+            uint64_t thr = UINT64_MAX;
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        }
         CK(cudaEventCreate(&ev0_));
         CK(cudaEventCreate(&ev1_));
         init_fronts(owner);
@@ -412,6 +423,21 @@ private:
     std::string err_reason_;
 
     DeviceArena& arena() { return arena_[cur_]; }
+    // Large matrices (3D fronts, big stacks) are allocated stream-ordered and
+    // released as soon as the launch that consumes them is enqueued, so a
+    // stage's peak footprint is its live data, not everything it rebuilt.
+    static constexpr size_t kBig = size_t(4) << 20;
+    double* dalloc(DeviceArena& ar, size_t n, bool& big) {
+        const size_t bytes = sizeof(double) * std::max<size_t>(n, 1);
+        big = bytes >= kBig;
+        if (!big) return ar.alloc_n<double>(std::max<size_t>(n, 1));
+        void* p = nullptr;
+        CK(cudaMallocAsync(&p, bytes, st_));
+        return static_cast<double*>(p);
+    }
+    void dfree(double* p, bool big) {
+        if (big && p) CK(cudaFreeAsync(p, st_));
+    }
     Uploader up() { return Uploader{&arena(), &pin_, st_}; }
     int width(int key) const { return static_cast<int>(cols_[key].size()); }
 
@@ -510,16 +536,27 @@ private:
     void init_fronts(const std::vector<int>& owner);
     // size-split batched launches (shared-memory staged when the block fits)
     void run_qr(const std::vector<QrDesc>& qd, const QrDesc* dq, Uploader& u) {
-        std::vector<int> small, large;
+        std::vector<int> small, large, huge;
         size_t smem = 0;
         for (size_t i = 0; i < qd.size(); ++i) {
             const size_t b = qr_smem_bytes(qd[i].m, qd[i].n, qd[i].ntot);
             if (b <= kSmemBudget && qd[i].n <= 1024) {
                 small.push_back(static_cast<int>(i));
                 smem = std::max(smem, b);
+            } else if (b > kBlockedQrBytes && qd[i].n >= 16) {
+                huge.push_back(static_cast<int>(i));
             } else {
                 large.push_back(static_cast<int>(i));
             }
+        }
+        // big fronts: panel factorisation + compact-WY trailing updates on DMMA (mbqr.cu)
+        for (int i : huge) {
+            const QrDesc& q = qd[i];
+            cudaEvent_t e0 = kt_.begin(st_);
+            double* scratch = arena().alloc_n<double>(2 * static_cast<size_t>(q.n) + 32 * 32);
+            blocked_qr_apply(1, q.m, q.n, q.ntot, q.a, scratch, scratch + q.n, q.flag, scratch + 2 * q.n, st_, q.ld);
+            blocked_qr_post(q.a, q.ld, q.m, q.n, q.rout, q.set_identity, q.zero_lower, st_);
+            kt_.end(K_QR, e0, st_, 16.0 * q.m * q.ntot);
         }
         const int* ds = u.put(small);
         const int* dl = u.put(large);
@@ -535,6 +572,33 @@ private:
         int maxm = 1;
         for (size_t i = 0; i < cd.size(); ++i) {
             const size_t b = cpqr_smem_bytes(cd[i].m, cd[i].n);
+            if (8ull * cd[i].m * cd[i].n > kBigCpqrBytes && cd[i].m >= 32 && 8ull * cd[i].n <= 200 * 1024) {
+                // large interface: the whole GPU cooperates on it (cpqr_big.cu)
+                CpqrDesc d = cd[i];
+                d.work = arena().alloc_n<double>(cpqr_big_work_doubles(d.n));
+                cudaEvent_t e0 = kt_.begin(st_);
+                static const bool biglog = std::getenv("SPQR_BIGLOG") != nullptr;
+                cudaEvent_t b0 = nullptr, b1 = nullptr;
+                if (biglog) {
+                    cudaEventCreate(&b0);
+                    cudaEventCreate(&b1);
+                    cudaEventRecord(b0, st_);
+                }
+                launch_cpqr_big(d, st_);
+                if (biglog) {
+                    cudaEventRecord(b1, st_);
+                    cudaEventSynchronize(b1);
+                    float ms = 0;
+                    cudaEventElapsedTime(&ms, b0, b1);
+                    int rk = 0;
+                    cudaMemcpy(&rk, d.rank, sizeof(int), cudaMemcpyDeviceToHost);
+                    std::fprintf(stderr, "[spqr big cpqr] m %d n %d rank %d  %.3f ms\n", d.m, d.n, rk, ms);
+                    cudaEventDestroy(b0);
+                    cudaEventDestroy(b1);
+                }
+                kt_.end(K_CPQR, e0, st_, 16.0 * d.m * d.n);
+                continue;
+            }
             if (b <= kSmemBudget) {
                 small.push_back(static_cast<int>(i));
                 smem = std::max(smem, b);
@@ -1018,7 +1082,7 @@ void Engine::materialize_pending() {
     for (Plan& pl : plans) {
         if (pl.f < 0 || pl.same) continue;
         Front& nf = pl.nf;
-        nf.mat = arena().alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
+        nf.mat = dalloc(arena(), static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1), nf.big);
         if (!sprof_.empty()) {
             auto& sp = sprof_.back();
             sp.mat_fronts++;
@@ -1083,8 +1147,22 @@ void Engine::materialize_pending() {
     NScope mt3(nprof_, "mat.swap");
     for (Plan& pl : plans) {
         if (pl.f < 0 || pl.same) continue;
+        dfree(fr_[pl.f].mat, fr_[pl.f].big);  // the gather reading it is already enqueued
         fr_[pl.f] = std::move(pl.nf);
     }
+    // eliminated fronts and this wave's stacks are no longer referenced
+    for (int f : pend_list_)
+        if (!fr_[f].live && fr_[f].big) {
+            dfree(fr_[f].mat, true);
+            fr_[f].mat = nullptr;
+            fr_[f].big = false;
+        }
+    for (size_t t = 0; t < el_.size(); ++t)
+        if (el_[t].sbig) {
+            dfree(el_[t].S, true);
+            el_[t].S = nullptr;
+            el_[t].sbig = false;
+        }
     for (int f : pend_list_) pend_id_[f] = -1;
     pend_list_.clear();
     npend_ = 0;
@@ -1294,7 +1372,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
     for (int ei = 0; ei < nvalid; ++ei) {
         Elim& e = el_[ei];
         if (e.cs <= 0) continue;
-        e.S = arena().alloc_n<double>(static_cast<size_t>(e.total_rows) * e.tcols);
+        e.S = dalloc(arena(), static_cast<size_t>(e.total_rows) * e.tcols, e.sbig);
         if (!sprof_.empty()) {
             auto& sp = sprof_.back();
             sp.s_elems += static_cast<long long>(e.total_rows) * e.tcols;
@@ -1366,6 +1444,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         const QrDesc* dq = u.put(qd);
         d_psq = arena().alloc_n<double>(std::max<long long>(postlen, 1));
         d_pnz = arena().alloc_n<unsigned char>(std::max<long long>(postlen, 1));
+        pwork = layout_stats(pd.data(), pd.size());
         const StatDesc* dp = u.put(pd);
         out_.ctr.h2d_bytes += u.bytes_h2d;
         int maxm = 0;
@@ -1448,12 +1527,13 @@ void Engine::scale_all() {
     unsigned char* d_nz = arena().alloc_n<unsigned char>(cand.size());
     {
         Uploader u = up();
+        const long long swork = layout_stats(sd.data(), sd.size());
         const StatDesc* dd = u.put(sd);
         out_.ctr.h2d_bytes += u.bytes_h2d;
         double sb = 0;
         for (auto& q : sd) sb += 8.0 * q.nrows * q.ncols;
         cudaEvent_t e0 = kt_.begin(st_);
-        launch_stats(dd, static_cast<int>(sd.size()), static_cast<long long>(sd.size()), d_sq, d_nz, st_);
+        launch_stats(dd, static_cast<int>(sd.size()), swork, d_sq, d_nz, st_);
         kt_.end(K_STATS, e0, st_, sb);
         out_.ctr.launches++;
     }
@@ -1527,6 +1607,7 @@ void Engine::sparsify_rows_all() {
     struct Job {
         int p, cs, p2, nw, c0;
         double* B;
+        bool big;
     };
     std::vector<Job> jobs;
     AsmBuilder gb;
@@ -1554,7 +1635,8 @@ void Engine::sparsify_rows_all() {
             f.rows.resize(cs);
             continue;
         }
-        Job j{p, cs, p2, nw, c0, arena().alloc_n<double>(static_cast<size_t>(p2) * nw)};
+        bool bbig = false;
+        Job j{p, cs, p2, nw, c0, dalloc(arena(), static_cast<size_t>(p2) * nw, bbig), bbig};
         // B = extra rows x live neighbour columns, ascending keys (physical order)
         const int di = gb.begin(j.B, p2, p2, nw, 1, nseg);
         gb.source(di, 0) = AsmSrc{f.mat + cs, 1, f.ld};
@@ -1629,6 +1711,7 @@ void Engine::sparsify_rows_all() {
         }
     }
     flush_assemble(wb);
+    for (const Job& j : jobs) dfree(j.B, j.big);
 }
 
 // factorize.cpp:539-633 — Gauss-Seidel over interfaces, run as waves of a
@@ -1691,6 +1774,7 @@ void Engine::sparsify_cols_all() {
             int p, cs, nG, wrows, kmax;
             std::vector<int> rparts, seg;  // seg offsets of holders in G
             std::vector<std::pair<int, int>> kg;  // (neighbour key, its first column in G's own part)
+            bool gbig = false;
             double* G;
             double *V, *tau, *sign;
         };
@@ -1720,7 +1804,7 @@ void Engine::sparsify_cols_all() {
             j.wrows = wrows;
             j.nG = wrows + wcols;
             j.kmax = std::min(j.cs, j.nG);
-            j.G = arena().alloc_n<double>(static_cast<size_t>(j.cs) * std::max(j.nG, 1));
+            j.G = dalloc(arena(), static_cast<size_t>(j.cs) * std::max(j.nG, 1), j.gbig);
             // G (cs x nG) built transposed: G column g <- a row of holder m or a column of own block
             const int nsrc = static_cast<int>(j.rparts.size()) + 1;
             if (j.nG > 0) {
@@ -1840,7 +1924,7 @@ void Engine::sparsify_cols_all() {
             nf.scaled_ok = r2 > 0;
             layout(p, nf.keys, nf.ncols);
             nf.ld = std::max(1, nf.nrows());
-            nf.mat = arena().alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
+            nf.mat = dalloc(arena(), static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1), nf.big);
             std::vector<int> ord;
             phys_order(nf.keys, ord);
             const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, 2, static_cast<int>(ord.size()));
@@ -1896,7 +1980,11 @@ void Engine::sparsify_cols_all() {
             NScope sc4(nprof_, "scols.rebuild_flush");
             flush_assemble(mb);
         }
-        for (auto& [f, nf] : updates) fr_[f] = std::move(nf);
+        for (auto& [f, nf] : updates) {
+            dfree(fr_[f].mat, fr_[f].big);
+            fr_[f] = std::move(nf);
+        }
+        for (const Job& j : jobs) dfree(j.G, j.gbig);
         for (const Job& j : jobs) {
             bad[j.p] = 0;
             changed[j.p] = 0;
@@ -2008,7 +2096,7 @@ void Engine::merge_level() {
     for (int g = 0; g < ng; ++g) {
         Plan& pl = plans[g];
         Front& nf = pl.nf;
-        nf.mat = next.alloc_n<double>(static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1));
+        nf.mat = dalloc(next, static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1), nf.big);
         if (nf.nrows() == 0 || nf.ncols == 0) continue;
         pl.di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, gstart[g + 1] - gstart[g], pl.nseg);
     }
@@ -2039,7 +2127,10 @@ void Engine::merge_level() {
     std::unique_ptr<NScope> m2 = std::make_unique<NScope>(nprof_, "merge.flush+rebuild_host");
     flush_assemble(mb);
     for (size_t c = 0; c < fr_.size(); ++c)
-        if (fr_[c].live) fr_[c] = Front();
+        if (fr_[c].live) {
+            dfree(fr_[c].mat, fr_[c].big);
+            fr_[c] = Front();
+        }
     for (auto& hs : holders_) hs.clear();
     for (int g = 0; g < ng; ++g) {
         const int P = gp[g];
@@ -2101,6 +2192,7 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
     }
     for (size_t c = 0; c < fr_.size(); ++c)
         if (fr_[c].live) out_.trailing_rows.insert(out_.trailing_rows.end(), fr_[c].rows.begin(), fr_[c].rows.end());
+    for (size_t c = 0; c < fr_.size(); ++c) dfree(fr_[c].mat, fr_[c].big);
     sync();
     out_.ctr.t_qr_ms = out_.ctr.k_ms[K_QR];
     if (std::getenv("SPQR_PROF")) {

@@ -103,6 +103,24 @@ __global__ void k_scatter(const long long* __restrict__ off, const double* __res
 }
 
 // --------------------------------------------------------------------- stats
+__global__ void k_stats_init(const StatDesc* __restrict__ ds, int nd, double* __restrict__ out_sq,
+                             unsigned char* __restrict__ out_nz) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nd || ds[i].mode == 0) return;
+    out_sq[ds[i].out_off] = 0.0;
+    out_nz[ds[i].out_off] = ds[i].mode == 2 ? 1 : 0;
+}
+
+// byte-wide atomic OR / AND-NOT through the containing 32-bit word
+__device__ __forceinline__ void byte_or(unsigned char* p, unsigned v) {
+    const size_t a = reinterpret_cast<size_t>(p);
+    atomicOr(reinterpret_cast<unsigned*>(a & ~size_t(3)), v << (8 * (a & 3)));
+}
+__device__ __forceinline__ void byte_clear(unsigned char* p) {
+    const size_t a = reinterpret_cast<size_t>(p);
+    atomicAnd(reinterpret_cast<unsigned*>(a & ~size_t(3)), ~(0xFFu << (8 * (a & 3))));
+}
+
 __global__ void k_stats(const StatDesc* __restrict__ ds, int nd, long long total, double* __restrict__ out_sq,
                         unsigned char* __restrict__ out_nz) {
     const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -117,7 +135,8 @@ __global__ void k_stats(const StatDesc* __restrict__ ds, int nd, long long total
     }
     const StatDesc d = ds[lo];
     if (d.mode == 0) {
-        const int i = static_cast<int>(e - d.work_off);
+        const long long i = e - d.work_off;
+        if (i >= d.nrows) return;  // alignment padding of a following warp-mode descriptor
         const double* a = d.p + (d.r0 + i) + static_cast<long long>(d.c0) * d.ld;
         double s = 0.0;
         unsigned char nz = 0;
@@ -128,27 +147,39 @@ __global__ void k_stats(const StatDesc* __restrict__ ds, int nd, long long total
         }
         out_sq[d.out_off + i] = s;
         out_nz[d.out_off + i] = nz;
-    } else if (d.mode == 2) {  // exactly [I; 0]?  (Eigen isIdentity(0) / isZero(0), factorize.cpp:435)
-        unsigned char ok = 1;
-        for (int j = 0; j < d.ncols && ok; ++j)
-            for (int i = 0; i < d.nrows; ++i)
-                if (d.p[(d.r0 + i) + static_cast<long long>(d.c0 + j) * d.ld] != (i == j ? 1.0 : 0.0)) {
-                    ok = 0;
-                    break;
-                }
-        out_sq[d.out_off] = 0.0;
-        out_nz[d.out_off] = ok;
-    } else {
-        double mx = 0.0;
-        unsigned char nz = 0;
-        for (int j = 0; j < d.ncols; ++j)
-            for (int i = 0; i < d.nrows; ++i) {
-                const double x = d.p[(d.r0 + i) + static_cast<long long>(d.c0 + j) * d.ld];
-                mx = fmax(mx, fabs(x));
-                nz |= (x != 0.0);
-            }
-        out_sq[d.out_off] = mx;
-        out_nz[d.out_off] = nz;
+        return;
+    }
+    // modes 1/2: the warp owns 256 consecutive elements (column-major in the block)
+    const long long u = e - d.work_off;
+    const long long nel = static_cast<long long>(d.nrows) * d.ncols;
+    const long long base = (u >> 5) * 256;
+    const int lane = static_cast<int>(u & 31);
+    double mx = 0.0;
+    bool nz = false, bad = false;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const long long t = base + lane + 32 * q;
+        if (t >= nel) break;
+        const int j = static_cast<int>(t / d.nrows), i = static_cast<int>(t - static_cast<long long>(j) * d.nrows);
+        const double x = d.p[(d.r0 + i) + static_cast<long long>(d.c0 + j) * d.ld];
+        mx = fmax(mx, fabs(x));
+        nz |= (x != 0.0);
+        bad |= (x != (i == j ? 1.0 : 0.0));  // exactly [I; 0]?  (Eigen isIdentity(0) / isZero(0), factorize.cpp:435)
+    }
+    // the whole warp belongs to this descriptor (32-aligned work_off)
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    nz = __any_sync(0xffffffffu, nz);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+        if (d.mode == 1) {
+            if (mx > 0.0)
+                atomicMax(reinterpret_cast<unsigned long long*>(out_sq + d.out_off), __double_as_longlong(mx));
+            if (nz) byte_or(out_nz + d.out_off, 1u);
+        } else if (bad) {
+            byte_clear(out_nz + d.out_off);
+        }
     }
 }
 
@@ -620,6 +651,7 @@ void launch_scatter_values(const long long* off, const double* val, long long n,
 void launch_stats(const StatDesc* d, int nd, long long total, double* out_sq, unsigned char* out_nz, cudaStream_t st) {
     if (total <= 0 || nd <= 0) return;
     const int bs = 128;
+    k_stats_init<<<(nd + 255) / 256, 256, 0, st>>>(d, nd, out_sq, out_nz);
     k_stats<<<static_cast<unsigned>((total + bs - 1) / bs), bs, 0, st>>>(d, nd, total, out_sq, out_nz);
 }
 

@@ -309,13 +309,37 @@ __global__ void k_flip_diag(double* __restrict__ a, int ld, long long stride, in
     }
 }
 
+// epilogue for engine fronts factored by the blocked path: R copy (upper n x n),
+// optional [I;0] overwrite of the factored columns, or clearing V below the diagonal
+__global__ void k_qr_post(double* __restrict__ a, int ld, int m, int n, double* __restrict__ rout, int set_identity,
+                          int zero_lower) {
+    const long long total = static_cast<long long>(m) * n;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e % m), j = static_cast<int>(e / m);
+        double* x = a + i + static_cast<long long>(j) * ld;
+        if (rout && i < n) rout[i + static_cast<long long>(j) * n] = (i <= j) ? *x : 0.0;
+        if (set_identity)
+            *x = (i == j) ? 1.0 : 0.0;
+        else if (zero_lower && i > j)
+            *x = 0.0;
+    }
+}
+
 }  // namespace
+
+void blocked_qr_post(double* a, int ld, int m, int n, double* rout, int set_identity, int zero_lower, cudaStream_t st) {
+    const long long total = static_cast<long long>(m) * n;
+    const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 4096));
+    if (total > 0) k_qr_post<<<grid, 256, 0, st>>>(a, ld, m, n, rout, set_identity, zero_lower);
+}
 
 // nb problems, each m x ntot column-major (ld = m, packed), QR of the first n
 // columns + H^T applied to the rest; tau/sign n per problem; info per problem.
 void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d_tau, double* d_sign, int* d_info,
-                      double* d_T, cudaStream_t st) {
-    const long long stride = static_cast<long long>(m) * ntot;
+                      double* d_T, cudaStream_t st, int ld_in) {
+    const int ldA = ld_in > 0 ? ld_in : m;
+    const long long stride = static_cast<long long>(ldA) * ntot;
     const size_t smem_cap = 160 * 1024;
     for (int j0 = 0; j0 < n; j0 += NB) {
         const int w = std::min(NB, n - j0);
@@ -324,25 +348,25 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
         const size_t smem = rows <= smem_rows ? sizeof(double) * (rows + 1) * w : 0;
         if (rows <= 256) {
             if (smem > 48 * 1024) cudaFuncSetAttribute(k_panel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            k_panel<1><<<nbatch, 32, smem, st>>>(d_a, m, stride, m, j0, w, d_tau, n, d_T, smem_rows);
+            k_panel<1><<<nbatch, 32, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
         } else if (rows <= 1024) {
             if (smem > 48 * 1024) cudaFuncSetAttribute(k_panel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            k_panel<4><<<nbatch, 128, smem, st>>>(d_a, m, stride, m, j0, w, d_tau, n, d_T, smem_rows);
+            k_panel<4><<<nbatch, 128, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
         } else {
             if (smem > 48 * 1024) cudaFuncSetAttribute(k_panel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            k_panel<16><<<nbatch, 512, smem, st>>>(d_a, m, stride, m, j0, w, d_tau, n, d_T, smem_rows);
+            k_panel<16><<<nbatch, 512, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
         }
         const int trail = ntot - (j0 + w);
         if (trail > 0) {
             dim3 grid((trail + TC2 - 1) / TC2, nbatch);
             const size_t wsm = sizeof(double) * (NB * LDV + TC2 * LDC + TC2 * LDW + NB * LDW + CH * LDVT);
             cudaFuncSetAttribute(k_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm));
-            k_wy<<<grid, 512, wsm, st>>>(d_a, m, stride, m, ntot, j0, w, d_T);
+            k_wy<<<grid, 512, wsm, st>>>(d_a, ldA, stride, m, ntot, j0, w, d_T);
         }
     }
     dim3 g2((ntot + 255) / 256, nbatch);
-    k_flip<<<g2, 256, 0, st>>>(d_a, m, stride, n, ntot, d_sign, d_info);
-    k_flip_diag<<<nbatch, 256, 0, st>>>(d_a, m, stride, n);
+    k_flip<<<g2, 256, 0, st>>>(d_a, ldA, stride, n, ntot, d_sign, d_info);
+    k_flip_diag<<<nbatch, 256, 0, st>>>(d_a, ldA, stride, n);
 }
 
 }  // namespace spqr

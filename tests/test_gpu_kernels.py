@@ -69,6 +69,28 @@ def test_cpqr_matches_oracle(shape, eps):
         assert np.array_equal(g["sign"], ref["sign"])
 
 
+@pytest.mark.parametrize("shape,eps,decay", [((600, 1200), 1e-2, 0.97), ((1500, 400), 1e-3, 0.98),
+                                             ((700, 900), 0.0, 0.99)])
+def test_cpqr_large_cooperative_matches_oracle(shape, eps, decay):
+    """Problems above 2 MB take the grid-cooperative kernel (cpqr_big.cu)."""
+    m, n = shape
+    rng = np.random.default_rng(m + n)
+    r = min(m, n)
+    U, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    W, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    A = (U * decay ** np.arange(r)) @ W.T
+    g = _P().cpqr_batched(A[None], eps)[0]
+    ref = O.cpqr(A, eps)
+    assert g["rank"] == ref["rank"]
+    k = ref["rank"]
+    assert np.array_equal(g["perm"][:k], ref["perm"][:k])
+    assert abs(g["r11"] - ref["r11"]) <= 1e-12 * abs(ref["r11"])
+    assert np.allclose(g["R"], ref["R"], atol=1e-10 * abs(ref["r11"]))
+    assert np.allclose(g["V"], ref["V"], atol=1e-9)
+    assert np.allclose(g["tau"], ref["tau"], atol=1e-12)
+    assert np.array_equal(g["sign"][:k], ref["sign"][:k])
+
+
 def test_cpqr_edge_cases():
     res = _P().cpqr_batched(np.zeros((2, 6, 4)), 1e-8)
     assert all(r["rank"] == 0 and r["r11"] == 0.0 for r in res)
