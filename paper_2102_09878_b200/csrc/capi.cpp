@@ -427,7 +427,7 @@ int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* ra
         int* dp = mem.alloc_n<int>(std::max(nb * kmax, 1));
         int* dr = mem.alloc_n<int>(std::max(nb, 1));
         double* d11 = mem.alloc_n<double>(std::max(nb, 1));
-        const bool big = 8ull * m * n > kBigCpqrBytes && m >= 32 && 8ull * n <= 200 * 1024;
+        const bool big = 8ull * m * n > kBigCpqrBytes && m >= 32 && cpqr_big_smem_bytes(m, n) <= 200 * 1024;
         const size_t wstride = big ? cpqr_big_work_doubles(n) : 3 * static_cast<size_t>(n);
         double* work = mem.alloc_n<double>(std::max<size_t>(static_cast<size_t>(nb) * wstride, 1));
         CK(cudaMemcpy(da, a, sizeof(double) * na, cudaMemcpyHostToDevice));

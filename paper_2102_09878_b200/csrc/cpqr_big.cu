@@ -1,14 +1,19 @@
 // Grid-cooperative truncated CPQR for large interfaces (3D top levels).
 //
 // Semantics: truncated_cpqr (proj/src/dense_kernels.cpp:124-232) — greedy
-// column-norm pivoting (first maximum), exact-norm stop rule with one refresh
-// and retry, Householder alpha = -sign+(x0)||x||, LAPACK-style norm downdate.
-// One problem per launch, all CTAs of the GPU cooperate: CTA c owns physical
-// columns c, c+G, ... .  Per pivot step there is one grid-wide barrier (argmax
-// partials); every CTA then reduces the same partials and recomputes the same
-// pivot norm and Householder scalars, so decisions are identical everywhere
-// without further synchronisation.  The pivot column is finalised (alpha e1,
-// V column) by its owner one step later, after every CTA has used it.
+// column-norm pivoting (first maximum by logical position), exact-norm stop
+// rule with one refresh and retry, Householder alpha = -sign+(x0)||x||,
+// LAPACK-style norm downdate with recompute below sqrt(eps).
+//
+// One problem per launch; one CTA per SM cooperates on it.  CTA c owns the
+// physical columns c, c+G, c+2G, ...; their logical positions and downdated
+// norms live in the CTA's shared memory, the matrix stays in place in HBM/L2.
+// Per pivot step there is exactly one grid-wide barrier (the argmax partials).
+// After it every CTA reduces the same partials, stages the same pivot column
+// into shared memory and computes the same Householder scalars, so all
+// decisions agree without further synchronisation.  The pivot column itself
+// (alpha e1 and the V column) is finalised by its owner one step later, after
+// every CTA is past the barrier that proves nobody still reads it.
 #include <cooperative_groups.h>
 
 #include <cfloat>
@@ -22,63 +27,134 @@ namespace spqr {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 1024;
 
-__device__ __forceinline__ double wsum2(double v) {
+__device__ __forceinline__ double wsum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
 struct BigScratch {
-    double* vn1;   // n, indexed by physical column
-    double* vn2;   // n
-    double* pval;  // G partial argmax values
-    int* pidx;     // G partial argmax logical positions
-    int* pos;      // n: logical position of physical column (global mirror)
-    int* ph;       // n: physical column at logical position
+    double* vn1;   // n: refreshed norms (global mirror used by the retry)
+    double* pval;  // G argmax partials: value
+    int* pidx;     // G: logical position
+    int* pphys;    // G: physical column
 };
 
-// block-wide norm of column `col` rows [r0, m) (all threads; result to all)
-__device__ double block_colnorm(const double* A, long long ld, int col, int r0, int m, double* red) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double s = 0.0;
-    const double* c = A + static_cast<long long>(col) * ld;
-    for (int i = r0 + threadIdx.x; i < m; i += blockDim.x) s = fma(c[i], c[i], s);
-    s = wsum2(s);
+// better candidate: larger norm, then smaller logical position (first max)
+__device__ __forceinline__ bool better(double v, int j, double bv, int bj) { return v > bv || (v == bv && j < bj); }
+
+// block-wide sum, result in every thread
+__device__ __forceinline__ double block_sum(double s, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    s = wsum(s);
     __syncthreads();
     if (lane == 0) red[wid] = s;
     __syncthreads();
     double t = 0.0;
-    for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) t += red[q];
-    return sqrt(t);
+    for (int q = 0; q < nw; ++q) t += red[q];
+    return t;
 }
 
-__global__ void __launch_bounds__(kThreads) k_cpqr_big(CpqrDesc d, BigScratch S) {
+// Trailing update of U owned columns per warp at a time (ILP over columns).
+// xs holds the pivot column rows [k, m); column j gets a_j -= t (v^T a_j) v,
+// then the row-k flip and the norm downdate.
+template <int U>
+__device__ void trailing(double* A, long long ld, int m, int k, int kmax, int G, int cta, int nown, const int* lpos,
+                         double* lv1, double* lv2, const double* xs, double v0, double t, bool reflect, bool flip,
+                         double tol3z) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int t0 = wid * U; t0 < nown; t0 += nw * U) {
+        double* a[U];
+        bool act[U];
+#pragma unroll
+        for (int c = 0; c < U; ++c) {
+            const int tt = t0 + c;
+            act[c] = tt < nown && lpos[tt] > k;
+            a[c] = A + static_cast<long long>(cta + G * tt) * ld;
+        }
+        double akk[U];
+        if (reflect) {
+            double w[U];
+#pragma unroll
+            for (int c = 0; c < U; ++c) w[c] = (lane == 0 && act[c]) ? v0 * a[c][k] : 0.0;
+            for (int i = k + 1 + lane; i < m; i += 32) {
+                const double x = xs[i];
+#pragma unroll
+                for (int c = 0; c < U; ++c)
+                    if (act[c]) w[c] = fma(x, a[c][i], w[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < U; ++c) w[c] = wsum(w[c]) * t;
+            for (int i = k + 1 + lane; i < m; i += 32) {
+                const double x = xs[i];
+#pragma unroll
+                for (int c = 0; c < U; ++c)
+                    if (act[c]) a[c][i] = fma(-w[c], x, a[c][i]);
+            }
+#pragma unroll
+            for (int c = 0; c < U; ++c) akk[c] = (lane == 0 && act[c]) ? fma(-w[c], v0, a[c][k]) : 0.0;
+        } else {
+#pragma unroll
+            for (int c = 0; c < U; ++c) akk[c] = (lane == 0 && act[c]) ? a[c][k] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < U; ++c) {
+            if (!act[c]) continue;
+            if (flip) akk[c] = -akk[c];
+            if (lane == 0 && (reflect || flip)) a[c][k] = akk[c];
+            if (k + 1 >= kmax) continue;
+            int recompute = 0;
+            if (lane == 0) {
+                const double v1 = lv1[t0 + c];
+                if (v1 != 0.0) {
+                    double q = fabs(akk[c]) / v1;
+                    q = fmax(0.0, (1.0 - q) * (1.0 + q));
+                    const double ratio = v1 / lv2[t0 + c];
+                    if (q * ratio * ratio <= tol3z)
+                        recompute = 1;
+                    else
+                        lv1[t0 + c] = v1 * sqrt(q);
+                }
+            }
+            recompute = __shfl_sync(0xffffffffu, recompute, 0);
+            if (recompute) {
+                __syncwarp();  // other lanes' stores of this column are visible
+                double s = 0.0;
+                for (int i = k + 1 + lane; i < m; i += 32) s = fma(a[c][i], a[c][i], s);
+                s = sqrt(wsum(s));
+                if (lane == 0) lv1[t0 + c] = lv2[t0 + c] = s;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_cpqr_big(CpqrDesc d, BigScratch S) {
     cg::grid_group grid = cg::this_grid();
     const int G = gridDim.x, cta = blockIdx.x;
     const int m = d.m, n = d.n, kmax = min(m, n);
     const long long ld = d.ld;
     double* A = d.a;
+    const int nown = n > cta ? (n - cta + G - 1) / G : 0;
+    extern __shared__ double smem[];
+    double* xs = smem;      // m: staged pivot column
+    double* lv1 = xs + m;   // nown: downdated norms of owned columns
+    double* lv2 = lv1 + nown;
+    int* lpos = reinterpret_cast<int*>(lv2 + nown);  // nown: logical positions
     __shared__ double red[32];
-    __shared__ int redi[32];
-    __shared__ int spiv;
-    extern __shared__ int sh[];  // ph (n) and pos (n), CTA-local copies
-    int* ph = sh;
-    int* pos = sh + n;
+    __shared__ int redi[32], redp[32];
+    __shared__ int s_piv, s_pc;
     const double tol3z = sqrt(DBL_EPSILON);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        ph[j] = j;
-        pos[j] = j;
-    }
-    // initial norms of owned columns (warp per column)
-    for (int p = cta + G * wid; p < n; p += G * nw) {
+
+    for (int t = threadIdx.x; t < nown; t += blockDim.x) lpos[t] = cta + G * t;
+    for (int t = wid; t < nown; t += nw) {
+        const double* c = A + static_cast<long long>(cta + G * t) * ld;
         double s = 0.0;
-        const double* c = A + p * ld;
         for (int i = lane; i < m; i += 32) s = fma(c[i], c[i], s);
-        s = sqrt(wsum2(s));
-        if (lane == 0) S.vn1[p] = S.vn2[p] = s;
+        s = sqrt(wsum(s));
+        if (lane == 0) lv1[t] = lv2[t] = s;
     }
     if (kmax == 0) {
         if (cta == 0 && threadIdx.x == 0) {
@@ -87,191 +163,191 @@ __global__ void __launch_bounds__(kThreads) k_cpqr_big(CpqrDesc d, BigScratch S)
         }
         return;
     }
-    double r11 = 0.0;
-    int k = 0;
-    int prev_pc = -1;
-    double prev_alpha = 0.0, prev_v0 = 0.0, prev_vns = 0.0;
-    bool prev_flip = false;
-    auto argmax = [&](int k0) {  // over logical positions >= k0: (vn1[ph[j]], j), first max
+
+    // grid-wide first max over logical positions >= k0; sets s_piv / s_pc
+    auto argmax = [&](int k0) {
         double bv = -1.0;
-        int bj = n;
-        for (int p = cta + G * static_cast<int>(threadIdx.x); p < n; p += G * blockDim.x) {
-            const int j = pos[p];
+        int bj = n, bp = -1;
+        for (int t = threadIdx.x; t < nown; t += blockDim.x) {
+            const int j = lpos[t];
             if (j < k0) continue;
-            const double v = S.vn1[p];
-            if (v > bv || (v == bv && j < bj)) {
-                bv = v;
+            if (better(lv1[t], j, bv, bj)) {
+                bv = lv1[t];
                 bj = j;
+                bp = cta + G * t;
             }
         }
         for (int o = 16; o > 0; o >>= 1) {
             const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
             const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-            if (ov > bv || (ov == bv && oj < bj)) {
+            const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+            if (better(ov, oj, bv, bj)) {
                 bv = ov;
                 bj = oj;
+                bp = op;
             }
         }
         __syncthreads();
         if (lane == 0) {
             red[wid] = bv;
             redi[wid] = bj;
+            redp[wid] = bp;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            double b = -1.0;
-            int jj = n;
-            for (int q = 0; q < nw; ++q)
-                if (red[q] > b || (red[q] == b && redi[q] < jj)) {
-                    b = red[q];
-                    jj = redi[q];
+        if (wid == 0) {
+            bv = lane < nw ? red[lane] : -1.0;
+            bj = lane < nw ? redi[lane] : n;
+            bp = lane < nw ? redp[lane] : -1;
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                if (better(ov, oj, bv, bj)) {
+                    bv = ov;
+                    bj = oj;
+                    bp = op;
                 }
-            S.pval[cta] = b;
-            S.pidx[cta] = jj;
+            }
+            if (lane == 0) {
+                S.pval[cta] = bv;
+                S.pidx[cta] = bj;
+                S.pphys[cta] = bp;
+            }
         }
         grid.sync();
-        if (threadIdx.x == 0) {  // every CTA reduces the same partials in the same order
-            double b = -1.0;
-            int jj = n;
-            for (int q = 0; q < G; ++q)
-                if (S.pval[q] > b || (S.pval[q] == b && S.pidx[q] < jj)) {
-                    b = S.pval[q];
-                    jj = S.pidx[q];
+        if (wid == 0) {  // every CTA reduces the same partials to the same answer
+            bv = -1.0;
+            bj = n;
+            bp = -1;
+            for (int q = lane; q < G; q += 32) {
+                const double v = __ldcg(S.pval + q);
+                const int j = __ldcg(S.pidx + q);
+                if (better(v, j, bv, bj)) {
+                    bv = v;
+                    bj = j;
+                    bp = __ldcg(S.pphys + q);
                 }
-            spiv = jj;
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                if (better(ov, oj, bv, bj)) {
+                    bv = ov;
+                    bj = oj;
+                    bp = op;
+                }
+            }
+            if (lane == 0) {
+                s_piv = bj;
+                s_pc = bp;
+            }
         }
         __syncthreads();
-        return spiv;
     };
-    while (k < kmax) {
-        __syncthreads();  // norms written by other warps of this CTA
-        int piv = argmax(k);
-        // the previous pivot column is final now (every CTA has passed the barrier)
-        if (prev_pc >= 0 && prev_pc % G == cta) {
-            double* ap = A + prev_pc * ld;
-            const int kk = k - 1;
-            for (int i = threadIdx.x; i < m - kk; i += blockDim.x) {
-                if (d.V) {
-                    double* vk = d.V + static_cast<long long>(kk) * d.ldv;
-                    vk[kk + i] = (i == 0) ? 1.0 : (prev_vns > 0.0 ? ap[kk + i] / prev_v0 : 0.0);
-                }
-            }
-            if (d.V)
-                for (int i = threadIdx.x; i < kk; i += blockDim.x) d.V[static_cast<long long>(kk) * d.ldv + i] = 0.0;
-            __syncthreads();
-            if (prev_vns > 0.0)
-                for (int i = threadIdx.x; i < m - kk; i += blockDim.x) ap[kk + i] = (i == 0) ? (prev_flip ? -prev_alpha : prev_alpha) : 0.0;
-            else if (prev_flip && threadIdx.x == 0)
-                ap[kk] = -ap[kk];
-        }
-        prev_pc = -1;  // finalised; a stop below must not finalise it again
-        double exact = block_colnorm(A, ld, ph[piv], k, m, red);
-        bool stop = (k == 0) ? !(exact > 0.0) : (d.eps > 0.0 && exact < d.eps * r11);
-        if (stop && k > 0) {  // refresh all trailing norms, retry once
-            grid.sync();
-            for (int p = cta + G * wid; p < n; p += G * nw) {
-                if (pos[p] < k) continue;
-                double s = 0.0;
-                const double* c = A + p * ld;
-                for (int i = k + lane; i < m; i += 32) s = fma(c[i], c[i], s);
-                s = sqrt(wsum2(s));
-                if (lane == 0) S.vn1[p] = S.vn2[p] = s;
-            }
-            grid.sync();
-            piv = argmax(k);
-            exact = S.vn1[ph[piv]];
-            stop = d.eps > 0.0 && exact < d.eps * r11;
-        }
-        if (stop) break;
-        // logical swap k <-> piv (every CTA, local copies)
-        __syncthreads();
-        if (threadIdx.x == 0 && piv != k) {
-            const int a = ph[k], b = ph[piv];
-            ph[k] = b;
-            ph[piv] = a;
-            pos[b] = k;
-            pos[a] = piv;
-        }
-        __syncthreads();
-        const int pc = ph[k];
-        const double* ap = A + pc * ld;
-        double alpha = exact;
-        const double x0 = ap[k];
-        if (x0 > 0.0) alpha = -alpha;
-        const double v0 = x0 - alpha;
-        // ||v||^2 = v0^2 + sum_{i>k} x_i^2 (block reduction, identical in every CTA)
+    // stage rows [k, m) of column pc into xs; returns sum_{i>k} x_i^2 (same in every CTA)
+    auto stage = [&](int pc, int k) {
+        const double* c = A + static_cast<long long>(pc) * ld;
         double s = 0.0;
-        for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) s = fma(ap[i], ap[i], s);
-        s = wsum2(s);
-        __syncthreads();
-        if (lane == 0) red[wid] = s;
-        __syncthreads();
-        double tail = 0.0;
-        for (int q = 0; q < nw; ++q) tail += red[q];
-        const double vns = fma(v0, v0, tail);
-        const double t = vns > 0.0 ? 2.0 / vns : 0.0;
-        const bool flip = alpha < 0.0;  // sign of R(k,k) after the update (A(k,k) = alpha)
-        if (cta == 0 && threadIdx.x == 0) {
-            if (d.tau) d.tau[k] = vns > 0.0 ? t * v0 * v0 : 0.0;
-            if (d.sign) d.sign[k] = flip ? -1.0 : 1.0;
-            if (d.perm) d.perm[k] = pc;
+        for (int i = k + threadIdx.x; i < m; i += blockDim.x) {
+            const double x = __ldcg(c + i);
+            xs[i] = x;
+            if (i > k) s = fma(x, x, s);
         }
-        if (k == 0) r11 = flip ? -alpha : alpha;
-        // trailing update of owned columns (warp per column), row-k flip, downdate
-        for (int p = cta + G * wid; p < n; p += G * nw) {
-            const int j = pos[p];
-            if (j <= k) continue;
-            double* aj = A + p * ld;
-            if (vns > 0.0) {
-                double w = (lane == 0) ? v0 * aj[k] : 0.0;
-                for (int i = k + 1 + lane; i < m; i += 32) w = fma(ap[i], aj[i], w);
-                w = wsum2(w);
-                const double tw = t * w;
-                for (int i = k + 1 + lane; i < m; i += 32) aj[i] = fma(-tw, ap[i], aj[i]);
-                if (lane == 0) aj[k] = fma(-tw, v0, aj[k]);
-            }
-            __syncwarp();
-            if (lane == 0 && flip) aj[k] = -aj[k];
-            __syncwarp();
-            if (k + 1 < kmax) {
-                const double v1 = S.vn1[p];
-                if (v1 != 0.0) {
-                    double tt = fabs(aj[k]) / v1;
-                    tt = fmax(0.0, (1.0 - tt) * (1.0 + tt));
-                    const double ratio = v1 / S.vn2[p];
-                    if (tt * ratio * ratio <= tol3z) {
-                        double q = 0.0;
-                        for (int i = k + 1 + lane; i < m; i += 32) q = fma(aj[i], aj[i], q);
-                        q = sqrt(wsum2(q));
-                        if (lane == 0) S.vn1[p] = S.vn2[p] = q;
-                    } else if (lane == 0) {
-                        S.vn1[p] = v1 * sqrt(tt);
-                    }
-                }
-            }
-        }
-        prev_pc = pc;
-        prev_alpha = alpha;
-        prev_v0 = v0;
-        prev_vns = vns;
-        prev_flip = flip;
-        ++k;
-    }
-    // finalise the last pivot column
-    grid.sync();
-    if (prev_pc >= 0 && prev_pc % G == cta) {
-        double* ap = A + prev_pc * ld;
-        const int kk = k - 1;
+        return block_sum(s, red);  // its barriers also publish xs
+    };
+    // owner writes V(:, kk) and alpha e1 into the (previous) pivot column
+    auto finalise = [&](int pc, int kk, double alpha, double v0, bool reflect, bool flip) {
+        if (pc % G != cta) return;
+        double* ap = A + static_cast<long long>(pc) * ld;
         if (d.V) {
             double* vk = d.V + static_cast<long long>(kk) * d.ldv;
             for (int i = threadIdx.x; i < m; i += blockDim.x)
-                vk[i] = (i < kk) ? 0.0 : (i == kk ? 1.0 : (prev_vns > 0.0 ? ap[i] / prev_v0 : 0.0));
+                vk[i] = i < kk ? 0.0 : (i == kk ? 1.0 : (reflect ? xs[i] / v0 : 0.0));
         }
-        __syncthreads();
-        if (prev_vns > 0.0)
-            for (int i = threadIdx.x; i < m - kk; i += blockDim.x) ap[kk + i] = (i == 0) ? (prev_flip ? -prev_alpha : prev_alpha) : 0.0;
-        else if (prev_flip && threadIdx.x == 0)
+        if (reflect) {
+            for (int i = kk + threadIdx.x; i < m; i += blockDim.x) ap[i] = i == kk ? (flip ? -alpha : alpha) : 0.0;
+        } else if (flip && threadIdx.x == 0) {
             ap[kk] = -ap[kk];
+        }
+    };
+
+    double r11 = 0.0;
+    int k = 0;
+    int prev_pc = -1;
+    double prev_alpha = 0.0, prev_v0 = 0.0;
+    bool prev_reflect = false, prev_flip = false;
+    while (k < kmax) {
+        __syncthreads();
+        argmax(k);
+        if (prev_pc >= 0) finalise(prev_pc, k - 1, prev_alpha, prev_v0, prev_reflect, prev_flip);
+        prev_pc = -1;
+        __syncthreads();  // xs is free again
+        int piv = s_piv, pc = s_pc;
+        double tail = stage(pc, k);
+        double x0 = xs[k];
+        double exact = sqrt(fma(x0, x0, tail));
+        bool stop = (k == 0) ? !(exact > 0.0) : (d.eps > 0.0 && exact < d.eps * r11);
+        if (stop && k > 0) {  // refresh every trailing norm and retry once
+            for (int t = wid; t < nown; t += nw) {
+                if (lpos[t] < k) continue;
+                const double* c = A + static_cast<long long>(cta + G * t) * ld;
+                double s = 0.0;
+                for (int i = k + lane; i < m; i += 32) s = fma(c[i], c[i], s);
+                s = sqrt(wsum(s));
+                if (lane == 0) {
+                    lv1[t] = lv2[t] = s;
+                    S.vn1[cta + G * t] = s;
+                }
+            }
+            __syncthreads();
+            argmax(k);  // its grid barrier publishes S.vn1
+            piv = s_piv;
+            pc = s_pc;
+            exact = __ldcg(S.vn1 + pc);
+            stop = d.eps > 0.0 && exact < d.eps * r11;
+            if (!stop) {
+                tail = stage(pc, k);
+                x0 = xs[k];
+            }
+        }
+        if (stop) break;
+        // logical swap k <-> piv on the owned columns
+        for (int t = threadIdx.x; t < nown; t += blockDim.x) {
+            const int p = cta + G * t;
+            lpos[t] = p == pc ? k : (lpos[t] == k ? piv : lpos[t]);
+        }
+        double alpha = sqrt(fma(x0, x0, tail));
+        if (x0 > 0.0) alpha = -alpha;
+        const double v0 = x0 - alpha;
+        const double vns = fma(v0, v0, tail);
+        const bool reflect = vns > 0.0;
+        const double tt = reflect ? 2.0 / vns : 0.0;
+        const bool flip = (reflect ? alpha : x0) < 0.0;  // sign of A(k,k) after the step
+        if (cta == 0 && threadIdx.x == 0) {
+            if (d.tau) d.tau[k] = reflect ? tt * v0 * v0 : 0.0;
+            if (d.sign) d.sign[k] = flip ? -1.0 : 1.0;
+            if (d.perm) d.perm[k] = pc;
+        }
+        if (k == 0) r11 = reflect ? fabs(alpha) : fabs(x0);
+        __syncthreads();  // lpos
+        const int per_warp = (nown + nw - 1) / nw;
+        if (per_warp >= 4)
+            trailing<4>(A, ld, m, k, kmax, G, cta, nown, lpos, lv1, lv2, xs, v0, tt, reflect, flip, tol3z);
+        else if (per_warp >= 2)
+            trailing<2>(A, ld, m, k, kmax, G, cta, nown, lpos, lv1, lv2, xs, v0, tt, reflect, flip, tol3z);
+        else
+            trailing<1>(A, ld, m, k, kmax, G, cta, nown, lpos, lv1, lv2, xs, v0, tt, reflect, flip, tol3z);
+        prev_pc = pc;
+        prev_alpha = alpha;
+        prev_v0 = v0;
+        prev_reflect = reflect;
+        prev_flip = flip;
+        ++k;
+    }
+    if (prev_pc >= 0) {  // loop ran to kmax: the last pivot column is still pending
+        grid.sync();
+        finalise(prev_pc, k - 1, prev_alpha, prev_v0, prev_reflect, prev_flip);
     }
     if (cta == 0 && threadIdx.x == 0) {
         *d.rank = k;
@@ -281,26 +357,39 @@ __global__ void __launch_bounds__(kThreads) k_cpqr_big(CpqrDesc d, BigScratch S)
 
 }  // namespace
 
+int cpqr_big_grid() {
+    static int g = 0;
+    if (!g) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return g;
+}
+
+size_t cpqr_big_smem_bytes(int m, int n) {
+    const size_t G = static_cast<size_t>(cpqr_big_grid());
+    const size_t nown = (static_cast<size_t>(n) + G - 1) / G;
+    return sizeof(double) * (static_cast<size_t>(m) + 2 * nown) + sizeof(int) * nown;
+}
+
 // d.work: cpqr_big_work_doubles(n) doubles; one problem, whole GPU.
 void launch_cpqr_big(const CpqrDesc& d, cudaStream_t st) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem = sizeof(int) * 2 * static_cast<size_t>(d.n);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_cpqr_big, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cpqr_big, kThreads, smem);
-    const int G = sms * std::max(1, std::min(per, 2));
+    const int G = cpqr_big_grid();
+    const size_t smem = cpqr_big_smem_bytes(d.m, d.n);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(k_cpqr_big, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        configured = smem;
+    }
     BigScratch S;
     S.vn1 = d.work;
-    S.vn2 = d.work + d.n;
-    S.pval = d.work + 2 * d.n;
-    S.pidx = reinterpret_cast<int*>(d.work + 2 * d.n + G);
-    S.pos = S.pidx + G;
-    S.ph = S.pos + d.n;
+    S.pval = d.work + d.n;
+    S.pidx = reinterpret_cast<int*>(S.pval + G);
+    S.pphys = S.pidx + G;
     CpqrDesc dd = d;
     void* args[] = {&dd, &S};
     cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_cpqr_big), G, kThreads, args, smem, st);
 }
-
 
 }  // namespace spqr

@@ -167,6 +167,7 @@ constexpr size_t kBlockedQrBytes = size_t(2) << 20;  // fronts above this use th
 // grid-cooperative CPQR of one large problem (cpqr_big.cu); d.work needs
 // cpqr_big_work_doubles(n) doubles
 void launch_cpqr_big(const CpqrDesc& d, cudaStream_t st);
+size_t cpqr_big_smem_bytes(int m, int n);  // dynamic smem of one launch (<= 200 KB to be eligible)
 inline size_t cpqr_big_work_doubles(int n) { return 3 * static_cast<size_t>(n) + 2 * 512 + 16; }
 constexpr size_t kBigCpqrBytes = size_t(2) << 20;
 

@@ -570,10 +570,44 @@ private:
         std::vector<int> small, large;
         size_t smem = 0;
         int maxm = 1;
+        // Problems too big for one CTA's shared memory either run one CTA each
+        // (k_cpqr, in parallel) or one at a time on the whole GPU (cpqr_big.cu).
+        // Cost model (measured): one CTA streams ~20 GB/s; the cooperative
+        // kernel costs ~8 us per pivot plus the trailing traffic at ~6 TB/s.
+        // Move the largest problems to the cooperative kernel while that lowers
+        // the estimated batch time.
+        std::vector<int> glob;
+        for (size_t i = 0; i < cd.size(); ++i)
+            if (cpqr_smem_bytes(cd[i].m, cd[i].n) > kSmemBudget) glob.push_back(static_cast<int>(i));
+        std::vector<char> coop(cd.size(), 0);
+        if (!glob.empty()) {
+            auto single = [&](int i) { return 16.0 * std::min(cd[i].m, cd[i].n) * double(cd[i].m) * cd[i].n / 20e9; };
+            auto cost = [&](int i) {
+                return std::min(cd[i].m, cd[i].n) * (8e-6 + 16.0 * double(cd[i].m) * cd[i].n / 6e12);
+            };
+            std::sort(glob.begin(), glob.end(), [&](int a, int b) { return single(a) > single(b); });
+            const double lanes = 2.0 * sm_count();
+            std::vector<double> suf(glob.size() + 1, 0.0);
+            for (size_t j = glob.size(); j-- > 0;) suf[j] = suf[j + 1] + single(glob[j]);
+            double best = 1e300, ccum = 0.0;
+            size_t bj = 0;
+            for (size_t j = 0; j <= glob.size(); ++j) {
+                const double rest = j < glob.size() ? std::max(single(glob[j]), suf[j] / lanes) : 0.0;
+                if (ccum + rest < best) {
+                    best = ccum + rest;
+                    bj = j;
+                }
+                if (j < glob.size()) {
+                    const int i = glob[j];
+                    if (cpqr_big_smem_bytes(cd[i].m, cd[i].n) > 200 * 1024 || cd[i].m < 32) break;
+                    ccum += cost(i);
+                }
+            }
+            for (size_t j = 0; j < bj; ++j) coop[glob[j]] = 1;
+        }
         for (size_t i = 0; i < cd.size(); ++i) {
             const size_t b = cpqr_smem_bytes(cd[i].m, cd[i].n);
-            if (8ull * cd[i].m * cd[i].n > kBigCpqrBytes && cd[i].m >= 32 && 8ull * cd[i].n <= 200 * 1024) {
-                // large interface: the whole GPU cooperates on it (cpqr_big.cu)
+            if (coop[i]) {
                 CpqrDesc d = cd[i];
                 d.work = arena().alloc_n<double>(cpqr_big_work_doubles(d.n));
                 cudaEvent_t e0 = kt_.begin(st_);
@@ -612,7 +646,36 @@ private:
         double cb = 0;
         for (auto& q : cd) cb += 16.0 * q.m * q.n;
         cudaEvent_t e0 = kt_.begin(st_);
+        static const bool biglog = std::getenv("SPQR_BIGLOG") != nullptr;
+        cudaEvent_t b0 = nullptr, b1 = nullptr;
+        if (biglog) {
+            cudaEventCreate(&b0);
+            cudaEventCreate(&b1);
+            cudaEventRecord(b0, st_);
+        }
         launch_cpqr_split(dc, ds, static_cast<int>(small.size()), smem, dl, static_cast<int>(large.size()), maxm, st_);
+        if (biglog) {
+            cudaEventRecord(b1, st_);
+            cudaEventSynchronize(b1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, b0, b1);
+            long long sm_mn = 0, lg_mn = 0;
+            int sm_m = 0, sm_n = 0, lg_m = 0, lg_n = 0;
+            for (int i : small) {
+                sm_mn = std::max<long long>(sm_mn, 1LL * cd[i].m * cd[i].n);
+                sm_m = std::max(sm_m, cd[i].m);
+                sm_n = std::max(sm_n, cd[i].n);
+            }
+            for (int i : large) {
+                lg_mn += 1LL * cd[i].m * cd[i].n;
+                lg_m = std::max(lg_m, cd[i].m);
+                lg_n = std::max(lg_n, cd[i].n);
+            }
+            std::fprintf(stderr, "[spqr cpqr batch] small %zu (max m %d n %d mn %lld) large %zu (max m %d n %d sum mn %lld)  %.3f ms\n",
+                         small.size(), sm_m, sm_n, sm_mn, large.size(), lg_m, lg_n, lg_mn, ms);
+            cudaEventDestroy(b0);
+            cudaEventDestroy(b1);
+        }
         kt_.end(K_CPQR, e0, st_, cb);
     }
     void eliminate_stage(int k);
