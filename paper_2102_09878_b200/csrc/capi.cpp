@@ -9,6 +9,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <numeric>
+#include <string>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -346,11 +347,33 @@ int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, doubl
         if (n > m || ntot < n) throw std::invalid_argument("qr: need n <= m and n <= ntot");
         std::vector<int> init(nb, INT_MAX);
         CK(cudaMemcpy(d_info, init.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
-        const bool staged = qr_smem_bytes(m, n, ntot) <= kSmemBudget && n <= 1024;
+        // path: column-tiled (default when the panel fits), smem-staged, or blocked DMMA;
+        // SPQR_QR_PATH=tile|smem|blocked forces one (comparisons, tests)
+        const char* force = std::getenv("SPQR_QR_PATH");
+        const std::string fp = force ? force : "";
+        const int tcls = qr_tile_class(m, n);
+        const bool tile = (fp.empty() || fp == "tile") && tcls >= 0;
+        const bool staged = !tile && fp != "blocked" && qr_smem_bytes(m, n, ntot) <= kSmemBudget && n <= 1024;
         QrDesc* dq = nullptr;
+        int4* dwork = nullptr;
+        int nwork = 0;
         int* didx = nullptr;
         double* dT = nullptr;
-        if (staged) {
+        if (tile) {
+            std::vector<QrDesc> qd(nb);
+            for (int b = 0; b < nb; ++b)
+                qd[b] = QrDesc{d_a + static_cast<long long>(b) * m * ntot, m, m, n, ntot, d_tau + static_cast<long long>(b) * n,
+                               d_sign + static_cast<long long>(b) * n, nullptr, d_info + b, 0, 0};
+            std::vector<int> all(nb);
+            for (int b = 0; b < nb; ++b) all[b] = b;
+            const std::vector<int4> wk = qr_tile_plan(qd.data(), all.data(), nb, sm_count());
+            nwork = static_cast<int>(wk.size());
+            CK(cudaMalloc(&dq, sizeof(QrDesc) * std::max(nb, 1)));
+            CK(cudaMalloc(&dwork, sizeof(int4) * std::max(nwork, 1) + sizeof(int) * std::max(nb, 1)));
+            CK(cudaMemset(dwork, 0, sizeof(int4) * std::max(nwork, 1) + sizeof(int) * std::max(nb, 1)));
+            CK(cudaMemcpy(dq, qd.data(), sizeof(QrDesc) * nb, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dwork, wk.data(), sizeof(int4) * nwork, cudaMemcpyHostToDevice));
+        } else if (staged) {
             std::vector<QrDesc> qd(nb);
             for (int b = 0; b < nb; ++b)
                 qd[b] = QrDesc{d_a + static_cast<long long>(b) * m * ntot, m, m, n, ntot, d_tau + static_cast<long long>(b) * n,
@@ -368,7 +391,9 @@ int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, doubl
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, 0));
-        if (staged)
+        if (tile)
+            launch_qr_tile(tcls, dq, dwork, nwork, 8ull * m * n, reinterpret_cast<int*>(dwork + std::max(nwork, 1)), 0);
+        else if (staged)
             launch_qr_split(dq, didx, nb, qr_smem_bytes(m, n, ntot), nullptr, 0, 0);
         else
             blocked_qr_apply(nb, m, n, ntot, d_a, d_tau, d_sign, d_info, dT, 0);
@@ -381,6 +406,7 @@ int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, doubl
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (dq) cudaFree(dq);
+        if (dwork) cudaFree(dwork);
         if (didx) cudaFree(didx);
         if (dT) cudaFree(dT);
     });

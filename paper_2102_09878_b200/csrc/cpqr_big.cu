@@ -378,10 +378,7 @@ void launch_cpqr_big(const CpqrDesc& d, cudaStream_t st) {
     const int G = cpqr_big_grid();
     const size_t smem = cpqr_big_smem_bytes(d.m, d.n);
     static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_cpqr_big, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = smem;
-    }
+    smem_optin(reinterpret_cast<const void*>(k_cpqr_big), smem, configured);
     BigScratch S;
     S.vn1 = d.work;
     S.pval = d.work + d.n;

@@ -12,7 +12,20 @@
 
 #include <cuda_runtime.h>
 
+#include <vector>
+
 namespace spqr {
+
+// Opt in to `bytes` of dynamic shared memory for `func`.  The 48 KB default
+// limit covers static + dynamic shared memory together, so the attribute is
+// raised whenever a launch needs more than any earlier one (`configured` is a
+// per-call-site static).
+inline void smem_optin(const void* func, size_t bytes, size_t& configured) {
+    if (bytes > configured) {
+        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+        configured = bytes;
+    }
+}
 
 // ---- generic gather ("assemble"): builds a destination matrix from rows of
 // up to a few source matrices.  The destination's columns are split into
@@ -163,6 +176,19 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
                       double* d_T, cudaStream_t st, int ld = 0);
 void blocked_qr_post(double* a, int ld, int m, int n, double* rout, int set_identity, int zero_lower, cudaStream_t st);
 constexpr size_t kBlockedQrBytes = size_t(2) << 20;  // fronts above this use the blocked DMMA path
+
+// column-tiled QR (qr_tile.cu): panel m x n staged in shared memory, trailing
+// columns in tiles [work.y, work.z) of front work.x; work.w = number of tiles of
+// that front.  Class -1 = not eligible.
+constexpr int kQrTileMaxN = 128;
+constexpr size_t kQrTileSmem = 200 * 1024;
+int qr_tile_class(int m, int n);
+// d_count: one int per descriptor, zero on entry (left zero on exit)
+void launch_qr_tile(int cls, const QrDesc* d_desc, const int4* d_work, int nwork, size_t smem, int* d_count,
+                    cudaStream_t st);
+// work list for the fronts idx[] of one class (host); tiles sized so the launch
+// has about two CTAs per SM
+std::vector<int4> qr_tile_plan(const QrDesc* hq, const int* idx, int cnt, int sms);
 
 // grid-cooperative CPQR of one large problem (cpqr_big.cu); d.work needs
 // cpqr_big_work_doubles(n) doubles

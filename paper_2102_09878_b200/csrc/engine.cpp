@@ -29,6 +29,7 @@
 #include <omp.h>
 #endif
 #include <map>
+#include <string>
 
 #include "dev.h"
 
@@ -446,6 +447,7 @@ private:
             ProfScope ps(prof_, HostProf::SYNC);
             CK(cudaStreamSynchronize(st_));
         }
+        CK(cudaGetLastError());  // a failed launch must not pass silently
         pin_.reset();
         kt_.resolve(out_.ctr);
         out_.ctr.syncs++;
@@ -472,6 +474,7 @@ private:
             ProfScope pw(prof_, HostProf::SYNC);
             CK(cudaStreamSynchronize(st_));
         }
+        CK(cudaGetLastError());  // a failed launch must not pass silently
         for (auto& q : dl_) std::memcpy(q.host, q.pin, q.bytes);
         dl_.clear();
         pin_.reset();
@@ -538,7 +541,81 @@ private:
     void run_qr(const std::vector<QrDesc>& qd, const QrDesc* dq, Uploader& u) {
         std::vector<int> small, large, huge;
         size_t smem = 0;
+        // column-tiled path (qr_tile.cu) for every front whose panel fits in shared memory
+        std::vector<int> cls(qd.size(), -1);
+        size_t tsmem[5] = {0, 0, 0, 0, 0};
+        int tcount[5] = {0, 0, 0, 0, 0};
+        int* qcount = nullptr;
+        static const bool no_tile = std::getenv("SPQR_QR_PATH") && std::string(std::getenv("SPQR_QR_PATH")) != "tile";
         for (size_t i = 0; i < qd.size(); ++i) {
+            cls[i] = no_tile ? -1 : qr_tile_class(qd[i].m, qd[i].n);
+            if (cls[i] < 0) continue;
+            tsmem[cls[i]] = std::max<size_t>(tsmem[cls[i]], 8ull * qd[i].m * qd[i].n);
+            ++tcount[cls[i]];
+        }
+        for (int c = 0; c < 5; ++c) {
+            if (!tcount[c]) continue;
+            std::vector<int> ids;
+            for (size_t i = 0; i < qd.size(); ++i)
+                if (cls[i] == c) ids.push_back(static_cast<int>(i));
+            const std::vector<int4> wk = qr_tile_plan(qd.data(), ids.data(), static_cast<int>(ids.size()), sm_count());
+            const int4* dw = u.put(wk);
+            double qb = 0;
+            for (size_t i = 0; i < qd.size(); ++i)
+                if (cls[i] == c) qb += 16.0 * qd[i].m * qd[i].ntot;
+            cudaEvent_t e0 = kt_.begin(st_);
+            if (!qcount) {
+                qcount = arena().alloc_n<int>(qd.size());
+                cudaMemsetAsync(qcount, 0, sizeof(int) * qd.size(), st_);
+            }
+            static const bool check = std::getenv("SPQR_QR_CHECK") != nullptr;
+            std::vector<std::vector<double>> before;
+            if (check) {
+                cudaStreamSynchronize(st_);
+                for (int i : ids) {
+                    const QrDesc& q = qd[i];
+                    before.emplace_back(static_cast<size_t>(q.m) * q.ntot);
+                    cudaMemcpy2D(before.back().data(), 8 * q.m, q.a, 8 * q.ld, 8 * q.m, q.ntot, cudaMemcpyDeviceToHost);
+                }
+            }
+            launch_qr_tile(c, dq, dw, static_cast<int>(wk.size()), tsmem[c], qcount, st_);
+            kt_.end(K_QR, e0, st_, qb);
+            if (check) {
+                cudaStreamSynchronize(st_);
+                const cudaError_t le = cudaGetLastError();
+                if (le != cudaSuccess) std::fprintf(stderr, "[qr check] cls %d launch error %s (smem %zu)\n", c, cudaGetErrorString(le), tsmem[c]);
+                int* didx = nullptr;
+                cudaMalloc(&didx, sizeof(int));
+                for (size_t t = 0; t < ids.size(); ++t) {
+                    const QrDesc& q = qd[ids[t]];
+                    std::vector<double> tile(static_cast<size_t>(q.m) * q.ntot), old(tile.size());
+                    cudaMemcpy2D(tile.data(), 8 * q.m, q.a, 8 * q.ld, 8 * q.m, q.ntot, cudaMemcpyDeviceToHost);
+                    cudaMemcpy2D(q.a, 8 * q.ld, before[t].data(), 8 * q.m, 8 * q.m, q.ntot, cudaMemcpyHostToDevice);
+                    cudaMemcpy(didx, &ids[t], sizeof(int), cudaMemcpyHostToDevice);
+                    launch_qr_split(dq, nullptr, 0, 0, didx, 1, st_);
+                    cudaStreamSynchronize(st_);
+                    cudaMemcpy2D(old.data(), 8 * q.m, q.a, 8 * q.ld, 8 * q.m, q.ntot, cudaMemcpyDeviceToHost);
+                    double md = 0, mx = 0;
+                    long long arg = -1;
+                    for (size_t z = 0; z < old.size(); ++z) {
+                        mx = std::max(mx, std::fabs(old[z]));
+                        if (std::fabs(old[z] - tile[z]) > md) {
+                            md = std::fabs(old[z] - tile[z]);
+                            arg = static_cast<long long>(z);
+                        }
+                    }
+                    if (md > 1e-9 * (1 + mx))
+                        std::fprintf(stderr, "[qr check] cls %d desc %d m %d n %d ntot %d ld %d set_id %d zl %d rout %d: max diff %.3e at (%lld,%lld) of %.3e\n",
+                                     c, ids[t], q.m, q.n, q.ntot, q.ld, q.set_identity, q.zero_lower, q.rout != nullptr, md,
+                                     arg % q.m, arg / q.m, mx);
+                    if (md > 1e-9 * (1 + mx))
+                        std::fprintf(stderr, "    before %.6e tile %.6e old %.6e\n", before[t][arg], tile[arg], old[arg]);
+                }
+                cudaFree(didx);
+            }
+        }
+        for (size_t i = 0; i < qd.size(); ++i) {
+            if (cls[i] >= 0) continue;
             const size_t b = qr_smem_bytes(qd[i].m, qd[i].n, qd[i].ntot);
             if (b <= kSmemBudget && qd[i].n <= 1024) {
                 small.push_back(static_cast<int>(i));
@@ -558,12 +635,46 @@ private:
             blocked_qr_post(q.a, q.ld, q.m, q.n, q.rout, q.set_identity, q.zero_lower, st_);
             kt_.end(K_QR, e0, st_, 16.0 * q.m * q.ntot);
         }
+        if (small.empty() && large.empty()) return;
         const int* ds = u.put(small);
         const int* dl = u.put(large);
         double qb = 0;
-        for (auto& q : qd) qb += 16.0 * q.m * q.ntot;
+        for (int i : small) qb += 16.0 * qd[i].m * qd[i].ntot;
+        for (int i : large) qb += 16.0 * qd[i].m * qd[i].ntot;
         cudaEvent_t e0 = kt_.begin(st_);
+        static const bool qrlog = std::getenv("SPQR_QRLOG") != nullptr;
+        cudaEvent_t b0 = nullptr, b1 = nullptr;
+        if (qrlog) {
+            cudaEventCreate(&b0);
+            cudaEventCreate(&b1);
+            cudaEventRecord(b0, st_);
+        }
         launch_qr_split(dq, ds, static_cast<int>(small.size()), smem, dl, static_cast<int>(large.size()), st_);
+        if (qrlog) {
+            cudaEventRecord(b1, st_);
+            cudaEventSynchronize(b1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, b0, b1);
+            int sm_m = 0, sm_n = 0, sm_t = 0, lg_m = 0, lg_n = 0, lg_t = 0;
+            double sbytes = 0, lbytes = 0;
+            for (int i : small) {
+                sm_m = std::max(sm_m, qd[i].m);
+                sm_n = std::max(sm_n, qd[i].n);
+                sm_t = std::max(sm_t, qd[i].ntot);
+                sbytes += 16.0 * qd[i].m * qd[i].ntot;
+            }
+            for (int i : large) {
+                lg_m = std::max(lg_m, qd[i].m);
+                lg_n = std::max(lg_n, qd[i].n);
+                lg_t = std::max(lg_t, qd[i].ntot);
+                lbytes += 16.0 * qd[i].m * qd[i].ntot;
+            }
+            std::fprintf(stderr, "[spqr qr batch] small %zu (max %dx%d/%d, %.1f MB) large %zu (max %dx%d/%d, %.1f MB) huge %zu  %.3f ms\n",
+                         small.size(), sm_m, sm_n, sm_t, sbytes / 1e6, large.size(), lg_m, lg_n, lg_t, lbytes / 1e6,
+                         huge.size(), ms);
+            cudaEventDestroy(b0);
+            cudaEventDestroy(b1);
+        }
         kt_.end(K_QR, e0, st_, qb);
     }
     void run_cpqr(const std::vector<CpqrDesc>& cd, const CpqrDesc* dc, Uploader& u) {

@@ -663,8 +663,8 @@ void launch_qr(const QrDesc* d, int nd, int /*max_m*/, cudaStream_t st) {  // al
 void launch_qr_split(const QrDesc* d_desc, const int* d_small, int n_small, size_t smem_small, const int* d_large,
                      int n_large, cudaStream_t st) {
     if (n_small > 0) {
-        if (smem_small > 48 * 1024)
-            cudaFuncSetAttribute(k_qr_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_small));
+        static size_t cfg = 0;
+        smem_optin(reinterpret_cast<const void*>(k_qr_smem), smem_small, cfg);
         k_qr_smem<<<n_small, 256, smem_small, st>>>(d_desc, d_small);
     }
     if (n_large > 0) k_qr_idx<<<n_large, 256, 0, st>>>(d_desc, d_large);
@@ -679,13 +679,14 @@ void launch_trsm(const TrsmDesc* d, int nd, long long total, cudaStream_t st) {
 void launch_cpqr_split(const CpqrDesc* d_desc, const int* d_small, int n_small, size_t smem_small, const int* d_large,
                        int n_large, int max_m_large, cudaStream_t st) {
     if (n_small > 0) {
-        if (smem_small > 48 * 1024)
-            cudaFuncSetAttribute(k_cpqr_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_small));
+        static size_t cfg = 0;
+        smem_optin(reinterpret_cast<const void*>(k_cpqr_smem), smem_small, cfg);
         k_cpqr_smem<<<n_small, kCpqrThreads, smem_small, st>>>(d_desc, d_small);
     }
     if (n_large > 0) {
         const size_t smem = sizeof(double) * static_cast<size_t>(max_m_large > 0 ? max_m_large : 1);
-        if (smem > 48 * 1024) cudaFuncSetAttribute(k_cpqr, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        static size_t cfg = 0;
+        smem_optin(reinterpret_cast<const void*>(k_cpqr), smem, cfg);
         k_cpqr<<<n_large, kCpqrThreads, smem, st>>>(d_desc, d_large);
     }
 }

@@ -295,7 +295,7 @@ __global__ void k_flip(double* __restrict__ a, int ld, long long stride, int n, 
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             const double r = A[i + static_cast<long long>(i) * ld];
             sign_all[static_cast<long long>(b) * n + i] = r < 0.0 ? -1.0 : 1.0;
-            if (!(fabs(r) >= DBL_MIN)) atomicMin(info + b, i);
+            if (info && !(fabs(r) >= DBL_MIN)) atomicMin(info + b, i);
         }
     }
 }
@@ -347,20 +347,24 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
         const int smem_rows = static_cast<int>(smem_cap / (sizeof(double) * NB)) - 1;
         const size_t smem = rows <= smem_rows ? sizeof(double) * (rows + 1) * w : 0;
         if (rows <= 256) {
-            if (smem > 48 * 1024) cudaFuncSetAttribute(k_panel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            static size_t cfg = 0;
+            smem_optin(reinterpret_cast<const void*>(k_panel<1>), smem, cfg);
             k_panel<1><<<nbatch, 32, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
         } else if (rows <= 1024) {
-            if (smem > 48 * 1024) cudaFuncSetAttribute(k_panel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            static size_t cfg = 0;
+            smem_optin(reinterpret_cast<const void*>(k_panel<4>), smem, cfg);
             k_panel<4><<<nbatch, 128, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
         } else {
-            if (smem > 48 * 1024) cudaFuncSetAttribute(k_panel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            static size_t cfg = 0;
+            smem_optin(reinterpret_cast<const void*>(k_panel<16>), smem, cfg);
             k_panel<16><<<nbatch, 512, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
         }
         const int trail = ntot - (j0 + w);
         if (trail > 0) {
             dim3 grid((trail + TC2 - 1) / TC2, nbatch);
             const size_t wsm = sizeof(double) * (NB * LDV + TC2 * LDC + TC2 * LDW + NB * LDW + CH * LDVT);
-            cudaFuncSetAttribute(k_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm));
+            static size_t cfg = 0;
+            smem_optin(reinterpret_cast<const void*>(k_wy), wsm, cfg);
             k_wy<<<grid, 512, wsm, st>>>(d_a, ldA, stride, m, ntot, j0, w, d_T);
         }
     }

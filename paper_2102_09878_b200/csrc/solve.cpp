@@ -73,6 +73,7 @@ SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
         P.launches_per_sweep_t += 1 + (b.ncol > 0 ? 1 : 0);
     }
     CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
     return P;
 }
 
@@ -118,6 +119,7 @@ DevMatrix upload_matrix(const Csc& A, cudaStream_t st) {
     D.ci = up.put(A.i);
     D.cv = up.put(A.x);
     CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
     return D;
 }
 
@@ -169,6 +171,7 @@ SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, 
     double h0 = 0.0;
     CK(cudaMemcpyAsync(&h0, sc + 0, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
     const double nres0 = std::sqrt(h0);
     CK(cudaMemsetAsync(d_u, 0, sizeof(double) * n, st));
     if (nres0 == 0.0) {
@@ -205,6 +208,7 @@ SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, 
         CK(cudaMemcpyAsync(hpin, sc + 5, sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(hpin + 1, ws.brk, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        CK(cudaGetLastError());
         hres.tn2 = hpin[0];
         std::memcpy(&hres.brk, hpin + 1, sizeof(int));
         if (hres.brk) break;
@@ -226,6 +230,7 @@ SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, 
     launch_copy(n, ws.y, d_u, st);
     if (W) L += sweep(*W, kWSolve, d_u, st);
     CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
     rep.t_solve = now_s() - t0;
     rep.launches = L;
     return rep;
@@ -243,6 +248,7 @@ SolveReport gpu_csne(const DevMatrix& A, const SolvePlan& W, const double* d_b, 
         double h = 0.0;
         CK(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        CK(cudaGetLastError());
         return h;
     };
     launch_spmv_csr(n, A.cp, A.ci, A.cv, d_b, ws.t, st);
@@ -280,6 +286,7 @@ SolveReport gpu_csne(const DevMatrix& A, const SolvePlan& W, const double* d_b, 
         record();
     }
     CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
     rep.iterations = refine;
     rep.converged = rep.residual_history.back() <= tol;
     rep.t_solve = now_s() - t0;

@@ -210,7 +210,8 @@ __global__ void k_copy(int n, const double* __restrict__ a, double* __restrict__
 static void wsweep(const WFac* f, int nf, double* z, double* contrib, int mode, int maxc, cudaStream_t st) {
     if (nf <= 0) return;
     const size_t smem = sizeof(double) * static_cast<size_t>(maxc > 0 ? maxc : 1) * kWarpsPerBlock;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_wsweep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    static size_t cfg = 0;
+    smem_optin(reinterpret_cast<const void*>(k_wsweep), smem, cfg);
     k_wsweep<<<(nf + kWarpsPerBlock - 1) / kWarpsPerBlock, 32 * kWarpsPerBlock, smem, st>>>(f, nf, z, contrib, mode, maxc);
 }
 

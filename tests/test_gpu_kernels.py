@@ -13,16 +13,28 @@ def _P():
     return P
 
 
+@pytest.mark.parametrize("path", ["auto", "smem", "blocked"])
 @pytest.mark.parametrize("shape", [(1, 1, 1), (5, 3, 3), (20, 7, 30), (40, 12, 60), (128, 32, 288), (300, 64, 96),
-                                   # blocked compact-WY path (block too large to stage on chip)
-                                   (300, 40, 140), (513, 70, 200), (512, 128, 384)])
-def test_qr_apply_matches_oracle(shape):
+                                   (300, 40, 140), (513, 70, 200), (512, 128, 384),
+                                   # column-tiled path: many tiles, panel only, square panel, m > 256
+                                   (33, 5, 1000), (200, 100, 100), (64, 64, 200), (480, 20, 300),
+                                   # dynamic smem just under 48 KB: static + dynamic needs the opt-in
+                                   (129, 47, 150)])
+def test_qr_apply_matches_oracle(shape, path, monkeypatch):
+    """auto = column-tiled kernel where the panel fits in shared memory (qr_tile.cu);
+    smem = whole block staged per CTA (kernels.cu); blocked = panel + DMMA compact-WY (mbqr.cu)."""
+    if path != "auto":
+        monkeypatch.setenv("SPQR_QR_PATH", path)
     m, n, ntot = shape
     rng = np.random.default_rng(m * 131 + n)
     nb = 6
     A = rng.standard_normal((nb, m, ntot))
+    if m > 3:
+        A[1, :, min(2, n - 1)] = 0.0  # a zero column: tau = 0 (Eigen makeHouseholder)
     out, tau, sg, info = _P().qr_apply_batched(A, n)
-    assert np.all(info == -1)
+    zc = min(2, n - 1) if m > 3 else None
+    for b in range(nb):
+        assert info[b] == (zc if (b == 1 and zc is not None) else -1)
     for b in range(nb):
         V, t, s, R = O.householder_qr(A[b, :, :n])
         # R with the nonnegative diagonal convention, same reflector convention
@@ -35,6 +47,21 @@ def test_qr_apply_matches_oracle(shape):
         if ntot > n:
             X = O.apply_reflectors(V, t, s, A[b, :, n:], "left_t")
             assert np.allclose(out[b, :, n:], X, atol=1e-12 * (1 + np.abs(X).max()))
+
+
+def test_qr_tiled_many_ctas_per_front():
+    """More tiles than resident CTAs: the panel must not be overwritten while a
+    later tile of the same front still stages it (qr_tile.cu writer election)."""
+    m, n, ntot, nb = 128, 32, 2000, 120
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((nb, m, ntot))
+    out, tau, sg, info = _P().qr_apply_batched(A, n)
+    assert np.all(info == -1)
+    for b in range(0, nb, 7):
+        V, t, s, R = O.householder_qr(A[b, :, :n])
+        assert np.allclose(np.triu(out[b, :n, :n]), R, atol=1e-12 * (1 + np.abs(R).max()))
+        X = O.apply_reflectors(V, t, s, A[b, :, n:], "left_t")
+        assert np.allclose(out[b, :, n:], X, atol=1e-12 * (1 + np.abs(X).max()))
 
 
 def test_qr_flags_singular_pivot():
