@@ -183,6 +183,7 @@ constexpr size_t kBlockedQrBytes = size_t(2) << 20;  // fronts above this use th
 constexpr int kQrTileMaxN = 128;
 constexpr size_t kQrTileSmem = 200 * 1024;
 int qr_tile_class(int m, int n);
+size_t qr_tile_smem(int cls, int n);  // dynamic smem of class cls (rows padded to 32 << cls)
 // d_count: one int per descriptor, zero on entry (left zero on exit)
 void launch_qr_tile(int cls, const QrDesc* d_desc, const int4* d_work, int nwork, size_t smem, int* d_count,
                     cudaStream_t st);

@@ -550,7 +550,7 @@ private:
         for (size_t i = 0; i < qd.size(); ++i) {
             cls[i] = no_tile ? -1 : qr_tile_class(qd[i].m, qd[i].n);
             if (cls[i] < 0) continue;
-            tsmem[cls[i]] = std::max<size_t>(tsmem[cls[i]], 8ull * qd[i].m * qd[i].n);
+            tsmem[cls[i]] = std::max<size_t>(tsmem[cls[i]], qr_tile_smem(cls[i], qd[i].n));
             ++tcount[cls[i]];
         }
         for (int c = 0; c < 5; ++c) {
