@@ -146,6 +146,46 @@ def cpu_oracle_step(p):
     return t["t_factorize"] + rep["t_solve"], wall, rep["iterations"], t["t_partition"]
 
 
+FP64_PEAK_TFLOPS = 37.1  # DMMA m8n8k4 on this pool's B200, tools/fp64_peak.cu -> profiles/r01_fp64_peak.txt
+
+
+def front_qr_microbench(local):
+    """BASELINE config 5: batched front QR + Q^T on a 256-column neighbour block,
+    through spqr_qr_apply_batched_dev (device buffers, CUDA events inside the call),
+    best of 3 after one warm-up; FP64 TFLOP/s against the measured DMMA peak."""
+    import ctypes as C
+    import torch
+    import paper_2102_09878_b200 as P
+    L = P.lib()
+    rows = []
+    for (m, n, nb) in ((128, 32, 4096), (512, 128, 1024), (4096, 1024, 64)):
+        k = 256
+        ntot = n + k
+        g = torch.Generator(device="cuda").manual_seed(0)
+        A0 = torch.randn(nb, ntot, m, dtype=torch.float64, device=f"cuda:{local}", generator=g)
+        tau = torch.empty(nb, n, dtype=torch.float64, device=A0.device)
+        sg = torch.empty(nb, n, dtype=torch.float64, device=A0.device)
+        info = torch.empty(nb, dtype=torch.int32, device=A0.device)
+        best = 1e30
+        for r in range(4):
+            A = A0.clone()
+            torch.cuda.synchronize()
+            ms = C.c_float()
+            rc = L.spqr_qr_apply_batched_dev(nb, m, n, ntot, C.c_void_p(A.data_ptr()), C.c_void_p(tau.data_ptr()),
+                                             C.c_void_p(sg.data_ptr()), C.c_void_p(info.data_ptr()), C.byref(ms))
+            if rc != 0:
+                raise RuntimeError("spqr_qr_apply_batched_dev failed")
+            if r > 0:
+                best = min(best, ms.value)
+        fl = (2 * m * n * n - 2 / 3 * n ** 3 + 4 * m * n * k - 2 * n * n * k) * nb
+        by = 16.0 * m * ntot * nb
+        rows.append({"shape": f"{m}x{n}+{k}", "batch": nb, "ms": round(best, 3),
+                     "TFLOP/s": round(fl / best / 1e9, 2), "frac_fp64": round(fl / best / 1e9 / FP64_PEAK_TFLOPS, 3),
+                     "GB/s": round(by / best / 1e6, 1)})
+        del A0, A
+    return {"peak_tflops": FP64_PEAK_TFLOPS, "peak_source": "measured DMMA (tools/fp64_peak.cu)", "shapes": rows}
+
+
 def l2_flush(buf):
     if buf is not None:
         buf.add_(1.0)
@@ -234,6 +274,11 @@ def run_ours(args, ws, rank, local):
                   "solve_event_s": round(t["solve_event_ms"] / 1e3, 4), "engine_syncs": g.syncs,
                   "elim_waves": t["elim_waves"]},
     }
+    if rank == 0 and not args.no_microbench:
+        try:
+            out["front_qr_microbench"] = front_qr_microbench(local)
+        except Exception as e:  # reported, never fatal for the headline line
+            out["front_qr_microbench"] = {"error": str(e)[:200]}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         v, wall, iters, tpart = cpu_oracle_step(p)
         out["cpu_baseline"] = {"value": round(v, 4), "unit": "s", "cores": 1, "kind": "port",
@@ -275,6 +320,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-microbench", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_init()

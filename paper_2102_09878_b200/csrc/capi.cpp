@@ -470,7 +470,12 @@ int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* ra
         int* didx = mem.alloc_n<int>(std::max(nb, 1));
         CK(cudaMemcpy(didx, all.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
         const size_t sm = cpqr_smem_bytes(m, n);
-        if (big)
+        const char* force = std::getenv("SPQR_CPQR_PATH");  // narrow|smem|big (comparisons, tests)
+        const std::string fp = force ? force : "";
+        const bool narrow = (fp.empty() || fp == "narrow") && cpqr_narrow_ok(m, n);
+        if (narrow)
+            launch_cpqr_narrow(dc, didx, nb, m, cpqr_narrow_smem(m, n), 0);
+        else if (big)
             for (int b = 0; b < nb; ++b) launch_cpqr_big(cd[b], 0);
         else if (sm <= kSmemBudget)
             launch_cpqr_split(dc, didx, nb, sm, nullptr, 0, m, 0);

@@ -1,0 +1,269 @@
+// Truncated CPQR for short-wide interface blocks (m <= 64 rows, n <= 1024).
+//
+// Semantics: truncated_cpqr (proj/src/dense_kernels.cpp:124-232), exactly as
+// cpqr_body in kernels.cu — greedy column-norm pivoting (first maximum by
+// logical position), exact-norm stop rule with one refresh and retry,
+// Householder alpha = -sign+(x0)||x||, nonnegative diagonal flip, LAPACK-style
+// norm downdate with recompute below sqrt(eps).
+//
+// The sparsify_cols blocks G = [B^T | own rows] are a few interface columns
+// tall and hundreds of rows wide; one CTA per problem, the block staged in
+// shared memory (odd leading dimension: conflict-free column walks).  Thread t
+// owns physical columns t, t+256, ...; their logical positions and downdated
+// norms live in registers.  Per pivot step there is one block barrier (argmax
+// partials, double-buffered); every warp then recomputes the same pivot norm
+// and Householder vector from shared memory with warp shuffles (lane = row),
+// so no further block synchronisation is needed.  Each thread updates its own
+// trailing columns serially over the m rows.  The pivot column is finalised
+// by its owner one step later, after the barrier that proves every warp has
+// read it.
+#include <cfloat>
+#include <climits>
+#include <cmath>
+
+#include "dev.h"
+
+namespace spqr {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kNW = kThreads / 32;
+constexpr int NC = 4;  // owned columns per thread (n <= 1024)
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ bool better(double v, int j, double bv, int bj) { return v > bv || (v == bv && j < bj); }
+
+template <int RPL>
+__global__ void __launch_bounds__(kThreads) k_cpqr_narrow(const CpqrDesc* __restrict__ ds, const int* __restrict__ idx) {
+    const CpqrDesc d = ds[idx[blockIdx.x]];
+    const int m = d.m, n = d.n, kmax = min(m, n);
+    const int ldm = m | 1;
+    extern __shared__ double A[];  // ldm x n
+    __shared__ double vbuf[kNW][32 * RPL];
+    __shared__ double pv[2][kNW];
+    __shared__ int pj[2][kNW], pp[2][kNW];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (kmax == 0) {
+        if (tid == 0) {
+            *d.rank = 0;
+            *d.r11 = 0.0;
+        }
+        return;
+    }
+    for (int e = tid; e < m * n; e += kThreads) {
+        const int j = e / m, i = e - j * m;
+        A[i + j * ldm] = d.a[i + static_cast<long long>(j) * d.ld];
+    }
+    __syncthreads();
+    const double tol3z = sqrt(DBL_EPSILON);
+    double vn1[NC], vn2[NC];
+    int lpos[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int p = tid + kThreads * c;
+        lpos[c] = p < n ? p : INT_MAX;
+        double s = 0.0;
+        if (p < n)
+            for (int i = 0; i < m; ++i) s = fma(A[i + p * ldm], A[i + p * ldm], s);
+        vn1[c] = vn2[c] = p < n ? sqrt(s) : -1.0;
+    }
+    int buf = 0;
+    // grid of the CTA: first max of vn1 over logical positions >= k0 -> (value, position, physical)
+    auto argmax = [&](int k0, double& bv, int& bj, int& bp) {
+        bv = -1.0;
+        bj = INT_MAX;
+        bp = -1;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (lpos[c] >= k0 && lpos[c] != INT_MAX && better(vn1[c], lpos[c], bv, bj)) {
+                bv = vn1[c];
+                bj = lpos[c];
+                bp = tid + kThreads * c;
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+            if (better(ov, oj, bv, bj)) {
+                bv = ov;
+                bj = oj;
+                bp = op;
+            }
+        }
+        if (lane == 0) {
+            pv[buf][wid] = bv;
+            pj[buf][wid] = bj;
+            pp[buf][wid] = bp;
+        }
+        __syncthreads();
+        bv = -1.0;
+        bj = INT_MAX;
+        bp = -1;
+#pragma unroll
+        for (int w = 0; w < kNW; ++w)
+            if (better(pv[buf][w], pj[buf][w], bv, bj)) {
+                bv = pv[buf][w];
+                bj = pj[buf][w];
+                bp = pp[buf][w];
+            }
+        buf ^= 1;
+    };
+    // sum over rows [r0, m) of column p squared, lane = row (every warp the same)
+    auto tail_sumsq = [&](int p, int r0) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int i = lane + 32 * q;
+            if (i >= r0 && i < m) s = fma(A[i + p * ldm], A[i + p * ldm], s);
+        }
+        return wsum(s);
+    };
+
+    double r11 = 0.0;
+    int k = 0;
+    int prev_pc = -1, prev_k = -1;
+    double prev_alpha = 0.0;
+    bool prev_reflect = false, prev_flip = false;
+    auto finalise = [&]() {  // owner thread writes alpha e1 into the previous pivot column
+        if (prev_pc >= 0 && prev_pc % kThreads == tid) {
+            double* ap = A + prev_pc * ldm;
+            if (prev_reflect) {
+                ap[prev_k] = prev_flip ? -prev_alpha : prev_alpha;
+                for (int i = prev_k + 1; i < m; ++i) ap[i] = 0.0;
+            } else if (prev_flip) {
+                ap[prev_k] = -ap[prev_k];
+            }
+        }
+        prev_pc = -1;
+    };
+    while (k < kmax) {
+        double bv;
+        int piv, pc;
+        argmax(k, bv, piv, pc);
+        finalise();
+        double exact = sqrt(tail_sumsq(pc, k));
+        bool stop = (k == 0) ? !(exact > 0.0) : (d.eps > 0.0 && exact < d.eps * r11);
+        if (stop && k > 0) {  // refresh every trailing norm and retry once
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                if (lpos[c] == INT_MAX || lpos[c] < k) continue;
+                const double* a = A + (tid + kThreads * c) * ldm;
+                double s = 0.0;
+                for (int i = k; i < m; ++i) s = fma(a[i], a[i], s);
+                vn1[c] = vn2[c] = sqrt(s);
+            }
+            argmax(k, bv, piv, pc);
+            exact = bv;
+            stop = d.eps > 0.0 && exact < d.eps * r11;
+        }
+        if (stop) break;
+        // Householder on rows [k, m) of the pivot column (every warp, lane = row)
+        const double x0 = A[k + pc * ldm];
+        const double tail = tail_sumsq(pc, k + 1);
+        double alpha = sqrt(fma(x0, x0, tail));
+        if (x0 > 0.0) alpha = -alpha;
+        const double v0 = x0 - alpha;
+        const double vns = fma(v0, v0, tail);
+        const bool reflect = vns > 0.0;
+        const double t = reflect ? 2.0 / vns : 0.0;
+        const bool flip = (reflect ? alpha : x0) < 0.0;
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int i = lane + 32 * q;
+            vbuf[wid][i] = (i < k || i >= m) ? 0.0 : (i == k ? v0 : A[i + pc * ldm]);
+        }
+        __syncwarp();
+        if (wid == 0 && d.V) {
+            double* vk = d.V + static_cast<long long>(k) * d.ldv;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+                const int i = lane + 32 * q;
+                if (i < m) vk[i] = i < k ? 0.0 : (i == k ? 1.0 : (reflect ? vbuf[0][i] / v0 : 0.0));
+            }
+        }
+        if (tid == 0) {
+            if (d.tau) d.tau[k] = reflect ? t * v0 * v0 : 0.0;
+            if (d.sign) d.sign[k] = flip ? -1.0 : 1.0;
+            if (d.perm) d.perm[k] = pc;
+        }
+        if (k == 0) r11 = fabs(reflect ? alpha : x0);
+        // logical swap k <-> piv, then the owned trailing columns
+        const double* v = vbuf[wid];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const int p = tid + kThreads * c;
+            if (lpos[c] == INT_MAX) continue;
+            lpos[c] = p == pc ? k : (lpos[c] == k ? piv : lpos[c]);
+            if (lpos[c] <= k) continue;
+            double* a = A + p * ldm;
+            if (reflect) {
+                double w = 0.0;
+                for (int i = k; i < m; ++i) w = fma(v[i], a[i], w);
+                const double tw = t * w;
+                for (int i = k; i < m; ++i) a[i] = fma(-tw, v[i], a[i]);
+            }
+            double akk = a[k];
+            if (flip) a[k] = akk = -akk;
+            if (k + 1 < kmax && vn1[c] != 0.0) {
+                double qq = fabs(akk) / vn1[c];
+                qq = fmax(0.0, (1.0 - qq) * (1.0 + qq));
+                const double ratio = vn1[c] / vn2[c];
+                if (qq * ratio * ratio <= tol3z) {
+                    double s = 0.0;
+                    for (int i = k + 1; i < m; ++i) s = fma(a[i], a[i], s);
+                    vn1[c] = vn2[c] = sqrt(s);
+                } else {
+                    vn1[c] *= sqrt(qq);
+                }
+            }
+        }
+        prev_pc = pc;
+        prev_k = k;
+        prev_alpha = alpha;
+        prev_reflect = reflect;
+        prev_flip = flip;
+        ++k;
+    }
+    __syncthreads();  // every warp has read the last pivot column
+    finalise();
+    __syncthreads();
+    for (int e = tid; e < k * n; e += kThreads) {
+        const int j = e / k, i = e - j * k;
+        d.a[i + static_cast<long long>(j) * d.ld] = A[i + j * ldm];
+    }
+    if (tid == 0) {
+        *d.rank = k;
+        *d.r11 = r11;
+    }
+}
+
+template <int RPL>
+void launch_narrow(const CpqrDesc* d, const int* idx, int cnt, size_t smem, cudaStream_t st) {
+    static size_t configured = 0;
+    smem_optin(reinterpret_cast<const void*>(k_cpqr_narrow<RPL>), smem, configured);
+    k_cpqr_narrow<RPL><<<cnt, kThreads, smem, st>>>(d, idx);
+}
+
+}  // namespace
+
+size_t cpqr_narrow_smem(int m, int n) { return sizeof(double) * static_cast<size_t>(m | 1) * n; }
+
+bool cpqr_narrow_ok(int m, int n) { return m >= 1 && m <= 64 && n <= kThreads * NC && cpqr_narrow_smem(m, n) <= 200 * 1024; }
+
+void launch_cpqr_narrow(const CpqrDesc* d_desc, const int* d_idx, int cnt, int max_m, size_t smem, cudaStream_t st) {
+    if (cnt <= 0) return;
+    if (max_m <= 32)
+        launch_narrow<1>(d_desc, d_idx, cnt, smem, st);
+    else
+        launch_narrow<2>(d_desc, d_idx, cnt, smem, st);
+}
+
+}  // namespace spqr

@@ -687,10 +687,48 @@ private:
         // kernel costs ~8 us per pivot plus the trailing traffic at ~6 TB/s.
         // Move the largest problems to the cooperative kernel while that lowers
         // the estimated batch time.
-        std::vector<int> glob;
-        for (size_t i = 0; i < cd.size(); ++i)
-            if (cpqr_smem_bytes(cd[i].m, cd[i].n) > kSmemBudget) glob.push_back(static_cast<int>(i));
-        std::vector<char> coop(cd.size(), 0);
+        std::vector<int> glob, narrow;
+        std::vector<char> coop(cd.size(), 0), nar(cd.size(), 0);
+        static const bool no_narrow = std::getenv("SPQR_NO_NARROW") != nullptr;
+        size_t nsmem = 0;
+        int nmaxm = 1;
+        for (size_t i = 0; i < cd.size(); ++i) {
+            if (!no_narrow && cpqr_narrow_ok(cd[i].m, cd[i].n)) {
+                narrow.push_back(static_cast<int>(i));
+                nar[i] = 1;
+                nsmem = std::max(nsmem, cpqr_narrow_smem(cd[i].m, cd[i].n));
+                nmaxm = std::max(nmaxm, cd[i].m);
+            } else if (cpqr_smem_bytes(cd[i].m, cd[i].n) > kSmemBudget) {
+                glob.push_back(static_cast<int>(i));
+            }
+        }
+        if (!narrow.empty()) {
+            const int* dn = u.put(narrow);
+            double nb = 0;
+            for (int i : narrow) nb += 16.0 * cd[i].m * cd[i].n;
+            cudaEvent_t e0 = kt_.begin(st_);
+            static const bool nlog = std::getenv("SPQR_BIGLOG") != nullptr;
+            cudaEvent_t b0 = nullptr, b1 = nullptr;
+            if (nlog) {
+                cudaEventCreate(&b0);
+                cudaEventCreate(&b1);
+                cudaEventRecord(b0, st_);
+            }
+            launch_cpqr_narrow(dc, dn, static_cast<int>(narrow.size()), nmaxm, nsmem, st_);
+            if (nlog) {
+                cudaEventRecord(b1, st_);
+                cudaEventSynchronize(b1);
+                float ms = 0;
+                cudaEventElapsedTime(&ms, b0, b1);
+                int mn_n = 0;
+                for (int i : narrow) mn_n = std::max(mn_n, cd[i].n);
+                std::fprintf(stderr, "[spqr cpqr narrow] %zu (max m %d n %d)  %.3f ms\n", narrow.size(), nmaxm, mn_n, ms);
+                cudaEventDestroy(b0);
+                cudaEventDestroy(b1);
+            }
+            kt_.end(K_CPQR, e0, st_, nb);
+        }
+        if (narrow.size() == cd.size()) return;
         if (!glob.empty()) {
             auto single = [&](int i) { return 16.0 * std::min(cd[i].m, cd[i].n) * double(cd[i].m) * cd[i].n / 20e9; };
             auto cost = [&](int i) {
@@ -717,6 +755,7 @@ private:
             for (size_t j = 0; j < bj; ++j) coop[glob[j]] = 1;
         }
         for (size_t i = 0; i < cd.size(); ++i) {
+            if (nar[i]) continue;
             const size_t b = cpqr_smem_bytes(cd[i].m, cd[i].n);
             if (coop[i]) {
                 CpqrDesc d = cd[i];
@@ -755,7 +794,8 @@ private:
         const int* ds = u.put(small);
         const int* dl = u.put(large);
         double cb = 0;
-        for (auto& q : cd) cb += 16.0 * q.m * q.n;
+        for (int i : small) cb += 16.0 * cd[i].m * cd[i].n;
+        for (int i : large) cb += 16.0 * cd[i].m * cd[i].n;
         cudaEvent_t e0 = kt_.begin(st_);
         static const bool biglog = std::getenv("SPQR_BIGLOG") != nullptr;
         cudaEvent_t b0 = nullptr, b1 = nullptr;
