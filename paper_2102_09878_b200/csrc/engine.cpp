@@ -413,6 +413,7 @@ private:
     size_t npend_ = 0;
     std::vector<int> pend_id_, pend_list_;
     std::vector<Elim> el_;
+    std::vector<std::vector<int>> sb_bases_;  // per-elimination source fronts (pool)
     std::vector<char> mark_;
     std::vector<int> stage_of_;
     std::vector<std::pair<int, int>> dep_;
@@ -1583,6 +1584,19 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
     std::vector<StatDesc> pd;
     long long pwork = 0, postlen = 0;
     std::vector<int> flags_init;
+    // stack descriptors in three phases: source fronts per elimination
+    // (parallel), allocation + descriptor reservation (sequential, cheap),
+    // row / segment maps (parallel, disjoint ranges of the builder)
+    if (sb_bases_.size() < static_cast<size_t>(nvalid)) sb_bases_.resize(nvalid);
+    std::vector<int> edi(nvalid, -1);
+#pragma omp parallel for schedule(dynamic, 16) if (nvalid > 64)
+    for (int ei = 0; ei < nvalid; ++ei) {
+        std::vector<int>& bases = sb_bases_[ei];
+        bases.clear();
+        if (el_[ei].cs <= 0) continue;
+        for (const PRow& r : el_[ei].srows)
+            if (std::find(bases.begin(), bases.end(), r.base) == bases.end()) bases.push_back(r.base);
+    }
     for (int ei = 0; ei < nvalid; ++ei) {
         Elim& e = el_[ei];
         if (e.cs <= 0) continue;
@@ -1594,25 +1608,8 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
             sp.s_max_cols = std::max<long long>(sp.s_max_cols, e.tcols);
             sp.elims++;
         }
-        std::vector<int> bases;
-        for (const PRow& r : e.srows)
-            if (std::find(bases.begin(), bases.end(), r.base) == bases.end()) bases.push_back(r.base);
-        const int nsrc = static_cast<int>(bases.size());
-        const int di = sb.begin(e.S, e.total_rows, e.total_rows, e.tcols, nsrc, static_cast<int>(e.keys.size()));
-        for (int s = 0; s < nsrc; ++s) sb.source(di, s) = AsmSrc{fr_[bases[s]].mat, 1, fr_[bases[s]].ld};
-        for (int i = 0; i < e.total_rows; ++i) {
-            const PRow& r = e.srows[i];
-            const int s = static_cast<int>(std::find(bases.begin(), bases.end(), r.base) - bases.begin());
-            sb.row(di, i) = int4{-1, 0, s, r.brow};
-        }
-        for (size_t ki = 0; ki < e.keys.size(); ++ki) {
-            sb.seg(di, static_cast<int>(ki), e.off[ki]);
-            for (int s = 0; s < nsrc; ++s) {
-                const Front& B = fr_[bases[s]];
-                const int qi = B.find(e.keys[ki]);
-                if (qi >= 0) sb.km(di, static_cast<int>(ki), s) = B.keys[qi].col;
-            }
-        }
+        const int nsrc = static_cast<int>(sb_bases_[ei].size());
+        edi[ei] = sb.begin(e.S, e.total_rows, e.total_rows, e.tcols, nsrc, static_cast<int>(e.keys.size()));
         flags_init.push_back(INT_MAX);
         QrDesc q{e.S, e.total_rows, e.total_rows, e.cs, e.tcols, nullptr, nullptr, nullptr, nullptr, 0, 1};
         qd.push_back(q);
@@ -1639,6 +1636,28 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
                 pwork += nown;
                 postlen += nown;
             }
+    }
+#pragma omp parallel for schedule(dynamic, 16) if (nvalid > 64)
+    for (int ei = 0; ei < nvalid; ++ei) {
+        const Elim& e = el_[ei];
+        const int di = edi[ei];
+        if (di < 0) continue;
+        const std::vector<int>& bases = sb_bases_[ei];
+        const int nsrc = static_cast<int>(bases.size());
+        for (int s = 0; s < nsrc; ++s) sb.source(di, s) = AsmSrc{fr_[bases[s]].mat, 1, fr_[bases[s]].ld};
+        for (int i = 0; i < e.total_rows; ++i) {
+            const PRow& r = e.srows[i];
+            const int s = static_cast<int>(std::find(bases.begin(), bases.end(), r.base) - bases.begin());
+            sb.row(di, i) = int4{-1, 0, s, r.brow};
+        }
+        for (size_t ki = 0; ki < e.keys.size(); ++ki) {
+            sb.seg(di, static_cast<int>(ki), e.off[ki]);
+            for (int s = 0; s < nsrc; ++s) {
+                const Front& B = fr_[bases[s]];
+                const int qi = B.find(e.keys[ki]);
+                if (qi >= 0) sb.km(di, static_cast<int>(ki), s) = B.keys[qi].col;
+            }
+        }
     }
     wcopy_.clear();
     double *d_psq = nullptr;
@@ -1989,6 +2008,7 @@ void Engine::sparsify_cols_all() {
             std::vector<int> rparts, seg;  // seg offsets of holders in G
             std::vector<std::pair<int, int>> kg;  // (neighbour key, its first column in G's own part)
             bool gbig = false;
+            int di = -1;
             double* G;
             double *V, *tau, *sign;
         };
@@ -2019,26 +2039,14 @@ void Engine::sparsify_cols_all() {
             j.nG = wrows + wcols;
             j.kmax = std::min(j.cs, j.nG);
             j.G = dalloc(arena(), static_cast<size_t>(j.cs) * std::max(j.nG, 1), j.gbig);
-            // G (cs x nG) built transposed: G column g <- a row of holder m or a column of own block
+            // G (cs x nG) built transposed: G column g <- a row of holder m or a column of own block;
+            // logical G^T (nG x cs) gathered row by row, stored transposed as G (ld = cs).  The
+            // row maps are filled in parallel below.
             const int nsrc = static_cast<int>(j.rparts.size()) + 1;
+            j.di = -1;
             if (j.nG > 0) {
-                // logical G^T (nG x cs) gathered row by row, stored transposed as G (ld = cs)
-                const int di = gb.begin(j.G, j.cs, j.nG, j.cs, nsrc, 1);
-                gb.dst[di].trans = 1;
-                for (size_t s = 0; s < j.rparts.size(); ++s) {
-                    const Front& fm = fr_[j.rparts[s]];
-                    const int mq = fm.find(p);
-                    gb.source(di, static_cast<int>(s)) = AsmSrc{fm.mat + static_cast<long long>(fm.keys[mq].col) * fm.ld, 1, fm.ld};
-                    for (int q = 0; q < fm.nrows(); ++q) gb.row(di, j.seg[s] + q) = int4{-1, 0, static_cast<int>(s), q};
-                    gb.km(di, 0, static_cast<int>(s)) = 0;
-                }
-                const int so = static_cast<int>(j.rparts.size());
-                gb.source(di, so) = AsmSrc{f.mat, f.ld, 1};  // transposed view of p's own rows
-                for (const auto& kg : j.kg) {
-                    const KeyRef& k = f.keys[f.find(kg.first)];
-                    for (int o = 0; o < k.width; ++o) gb.row(di, wrows + kg.second + o) = int4{-1, 0, so, k.col + o};
-                }
-                gb.km(di, 0, so) = 0;
+                j.di = gb.begin(j.G, j.cs, j.nG, j.cs, nsrc, 1);
+                gb.dst[j.di].trans = 1;
             }
             j.V = out_.warena->alloc_n<double>(static_cast<size_t>(j.cs) * std::max(j.kmax, 1));
             j.tau = out_.warena->alloc_n<double>(std::max(j.kmax, 1));
@@ -2046,6 +2054,27 @@ void Engine::sparsify_cols_all() {
             maxm = std::max(maxm, j.cs);
             out_.ctr.cpqr_bytes += 8.0 * j.cs * j.nG;
             jobs.push_back(std::move(j));
+        }
+#pragma omp parallel for schedule(dynamic, 4) if (jobs.size() > 16)
+        for (long long ji = 0; ji < static_cast<long long>(jobs.size()); ++ji) {
+            const Job& j = jobs[ji];
+            if (j.di < 0) continue;
+            const int di = j.di, p = j.p;
+            const Front& f = fr_[p];
+            for (size_t s = 0; s < j.rparts.size(); ++s) {
+                const Front& fm = fr_[j.rparts[s]];
+                const int mq = fm.find(p);
+                gb.source(di, static_cast<int>(s)) = AsmSrc{fm.mat + static_cast<long long>(fm.keys[mq].col) * fm.ld, 1, fm.ld};
+                for (int q = 0; q < fm.nrows(); ++q) gb.row(di, j.seg[s] + q) = int4{-1, 0, static_cast<int>(s), q};
+                gb.km(di, 0, static_cast<int>(s)) = 0;
+            }
+            const int so = static_cast<int>(j.rparts.size());
+            gb.source(di, so) = AsmSrc{f.mat, f.ld, 1};  // transposed view of p's own rows
+            for (const auto& kg : j.kg) {
+                const KeyRef& k = f.keys[f.find(kg.first)];
+                for (int o = 0; o < k.width; ++o) gb.row(di, j.wrows + kg.second + o) = int4{-1, 0, so, k.col + o};
+            }
+            gb.km(di, 0, so) = 0;
         }
         sc1.reset();
         std::unique_ptr<NScope> sc2 = std::make_unique<NScope>(nprof_, "scols.upload+cpqr+fetch");
