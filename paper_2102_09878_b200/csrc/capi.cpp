@@ -472,9 +472,9 @@ int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* ra
         const size_t sm = cpqr_smem_bytes(m, n);
         const char* force = std::getenv("SPQR_CPQR_PATH");  // narrow|smem|big (comparisons, tests)
         const std::string fp = force ? force : "";
-        const bool narrow = (fp.empty() || fp == "narrow") && cpqr_narrow_ok(m, n);
-        if (narrow)
-            launch_cpqr_narrow(dc, didx, nb, m, cpqr_narrow_smem(m, n), 0);
+        const int ncls = (fp.empty() || fp == "narrow") ? cpqr_narrow_class(m, n) : -1;
+        if (ncls >= 0)
+            launch_cpqr_narrow(ncls, dc, didx, nb, cpqr_narrow_smem(m, n), 0);
         else if (big)
             for (int b = 0; b < nb; ++b) launch_cpqr_big(cd[b], 0);
         else if (sm <= kSmemBudget)

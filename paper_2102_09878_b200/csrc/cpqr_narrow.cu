@@ -1,4 +1,4 @@
-// Truncated CPQR for short-wide interface blocks (m <= 64 rows, n <= 1024).
+// Truncated CPQR for short-wide interface blocks (m <= 128 rows, n <= 2048).
 //
 // Semantics: truncated_cpqr (proj/src/dense_kernels.cpp:124-232), exactly as
 // cpqr_body in kernels.cu — greedy column-norm pivoting (first maximum by
@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kNW = kThreads / 32;
-constexpr int NC = 4;  // owned columns per thread (n <= 1024)
+constexpr size_t kNarrowSmem = 216 * 1024;  // dynamic smem cap (227 KB minus the static arrays)
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -39,12 +39,16 @@ __device__ __forceinline__ double wsum(double v) {
 
 __device__ __forceinline__ bool better(double v, int j, double bv, int bj) { return v > bv || (v == bv && j < bj); }
 
-template <int RPL>
+// GLB: the block stays in place in global memory (L1/L2 serve the per-thread
+// column walks) when it is too large to stage in shared memory.
+// NC: owned columns per thread (n <= 256 NC)
+template <int RPL, bool GLB, int NC>
 __global__ void __launch_bounds__(kThreads) k_cpqr_narrow(const CpqrDesc* __restrict__ ds, const int* __restrict__ idx) {
     const CpqrDesc d = ds[idx[blockIdx.x]];
     const int m = d.m, n = d.n, kmax = min(m, n);
-    const int ldm = m | 1;
-    extern __shared__ double A[];  // ldm x n
+    const long long ldm = GLB ? d.ld : (m | 1);
+    extern __shared__ double sA[];  // ldm x n when staged
+    double* A = GLB ? d.a : sA;
     __shared__ double vbuf[kNW][32 * RPL];
     __shared__ double pv[2][kNW];
     __shared__ int pj[2][kNW], pp[2][kNW];
@@ -56,11 +60,13 @@ __global__ void __launch_bounds__(kThreads) k_cpqr_narrow(const CpqrDesc* __rest
         }
         return;
     }
-    for (int e = tid; e < m * n; e += kThreads) {
-        const int j = e / m, i = e - j * m;
-        A[i + j * ldm] = d.a[i + static_cast<long long>(j) * d.ld];
+    if (!GLB) {
+        for (int e = tid; e < m * n; e += kThreads) {
+            const int j = e / m, i = e - j * m;
+            A[i + j * ldm] = d.a[i + static_cast<long long>(j) * d.ld];
+        }
+        __syncthreads();
     }
-    __syncthreads();
     const double tol3z = sqrt(DBL_EPSILON);
     double vn1[NC], vn2[NC];
     int lpos[NC];
@@ -204,11 +210,19 @@ __global__ void __launch_bounds__(kThreads) k_cpqr_narrow(const CpqrDesc* __rest
             lpos[c] = p == pc ? k : (lpos[c] == k ? piv : lpos[c]);
             if (lpos[c] <= k) continue;
             double* a = A + p * ldm;
-            if (reflect) {
-                double w = 0.0;
-                for (int i = k; i < m; ++i) w = fma(v[i], a[i], w);
-                const double tw = t * w;
-                for (int i = k; i < m; ++i) a[i] = fma(-tw, v[i], a[i]);
+            if (reflect) {  // four independent chains: latency, not issue, bounds one thread
+                double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+                int i = k;
+                for (; i + 3 < m; i += 4) {
+                    w0 = fma(v[i], a[i], w0);
+                    w1 = fma(v[i + 1], a[i + 1], w1);
+                    w2 = fma(v[i + 2], a[i + 2], w2);
+                    w3 = fma(v[i + 3], a[i + 3], w3);
+                }
+                for (; i < m; ++i) w0 = fma(v[i], a[i], w0);
+                const double tw = -t * ((w0 + w1) + (w2 + w3));
+#pragma unroll 4
+                for (i = k; i < m; ++i) a[i] = fma(tw, v[i], a[i]);
             }
             double akk = a[k];
             if (flip) a[k] = akk = -akk;
@@ -235,35 +249,54 @@ __global__ void __launch_bounds__(kThreads) k_cpqr_narrow(const CpqrDesc* __rest
     __syncthreads();  // every warp has read the last pivot column
     finalise();
     __syncthreads();
-    for (int e = tid; e < k * n; e += kThreads) {
-        const int j = e / k, i = e - j * k;
-        d.a[i + static_cast<long long>(j) * d.ld] = A[i + j * ldm];
-    }
+    if (!GLB)
+        for (int e = tid; e < k * n; e += kThreads) {
+            const int j = e / k, i = e - j * k;
+            d.a[i + static_cast<long long>(j) * d.ld] = A[i + j * ldm];
+        }
     if (tid == 0) {
         *d.rank = k;
         *d.r11 = r11;
     }
 }
 
-template <int RPL>
+template <int RPL, bool GLB, int NC>
 void launch_narrow(const CpqrDesc* d, const int* idx, int cnt, size_t smem, cudaStream_t st) {
     static size_t configured = 0;
-    smem_optin(reinterpret_cast<const void*>(k_cpqr_narrow<RPL>), smem, configured);
-    k_cpqr_narrow<RPL><<<cnt, kThreads, smem, st>>>(d, idx);
+    if (!GLB) smem_optin(reinterpret_cast<const void*>(k_cpqr_narrow<RPL, GLB, NC>), smem, configured);
+    k_cpqr_narrow<RPL, GLB, NC><<<cnt, kThreads, GLB ? 0 : smem, st>>>(d, idx);
+}
+
+template <int NC>
+void launch_nc(int cls, const CpqrDesc* d, const int* idx, int cnt, size_t smem, cudaStream_t st) {
+    switch (cls) {
+        case 0: launch_narrow<1, false, NC>(d, idx, cnt, smem, st); break;
+        case 1: launch_narrow<2, false, NC>(d, idx, cnt, smem, st); break;
+        case 2: launch_narrow<4, false, NC>(d, idx, cnt, smem, st); break;
+        case 3: launch_narrow<1, true, NC>(d, idx, cnt, smem, st); break;
+        case 4: launch_narrow<2, true, NC>(d, idx, cnt, smem, st); break;
+        default: launch_narrow<4, true, NC>(d, idx, cnt, smem, st); break;
+    }
 }
 
 }  // namespace
 
 size_t cpqr_narrow_smem(int m, int n) { return sizeof(double) * static_cast<size_t>(m | 1) * n; }
 
-bool cpqr_narrow_ok(int m, int n) { return m >= 1 && m <= 64 && n <= kThreads * NC && cpqr_narrow_smem(m, n) <= 200 * 1024; }
+// classes 0..5: NC = 4 (n <= 1024); 6..11: NC = 8 (n <= 2048).  Within each
+// half: 0..2 staged (m <= 32 / 64 / 128), 3..5 in place in global memory.
+int cpqr_narrow_class(int m, int n) {
+    if (m < 1 || m > 128 || n > 2048) return -1;
+    const int r = m <= 32 ? 0 : (m <= 64 ? 1 : 2);
+    return (n > 1024 ? 6 : 0) + (cpqr_narrow_smem(m, n) <= kNarrowSmem ? r : 3 + r);
+}
 
-void launch_cpqr_narrow(const CpqrDesc* d_desc, const int* d_idx, int cnt, int max_m, size_t smem, cudaStream_t st) {
+void launch_cpqr_narrow(int cls, const CpqrDesc* d_desc, const int* d_idx, int cnt, size_t smem, cudaStream_t st) {
     if (cnt <= 0) return;
-    if (max_m <= 32)
-        launch_narrow<1>(d_desc, d_idx, cnt, smem, st);
+    if (cls < 6)
+        launch_nc<4>(cls, d_desc, d_idx, cnt, smem, st);
     else
-        launch_narrow<2>(d_desc, d_idx, cnt, smem, st);
+        launch_nc<8>(cls - 6, d_desc, d_idx, cnt, smem, st);
 }
 
 }  // namespace spqr

@@ -193,10 +193,11 @@ std::vector<int4> qr_tile_plan(const QrDesc* hq, const int* idx, int cnt, int sm
 
 // grid-cooperative CPQR of one large problem (cpqr_big.cu); d.work needs
 // cpqr_big_work_doubles(n) doubles
-// short-wide CPQR (cpqr_narrow.cu): m <= 64, n <= 1024, block staged in smem
-bool cpqr_narrow_ok(int m, int n);
+// short-wide CPQR (cpqr_narrow.cu): m <= 128, n <= 2048
+// class 0..11 (see cpqr_narrow.cu); -1 not eligible
+int cpqr_narrow_class(int m, int n);
 size_t cpqr_narrow_smem(int m, int n);
-void launch_cpqr_narrow(const CpqrDesc* d_desc, const int* d_idx, int cnt, int max_m, size_t smem, cudaStream_t st);
+void launch_cpqr_narrow(int cls, const CpqrDesc* d_desc, const int* d_idx, int cnt, size_t smem, cudaStream_t st);
 void launch_cpqr_big(const CpqrDesc& d, cudaStream_t st);
 size_t cpqr_big_smem_bytes(int m, int n);  // dynamic smem of one launch (<= 200 KB to be eligible)
 inline size_t cpqr_big_work_doubles(int n) { return 3 * static_cast<size_t>(n) + 2 * 512 + 16; }

@@ -688,25 +688,28 @@ private:
         // kernel costs ~8 us per pivot plus the trailing traffic at ~6 TB/s.
         // Move the largest problems to the cooperative kernel while that lowers
         // the estimated batch time.
-        std::vector<int> glob, narrow;
+        std::vector<int> glob;
+        std::vector<std::vector<int>> narrow(12);
         std::vector<char> coop(cd.size(), 0), nar(cd.size(), 0);
         static const bool no_narrow = std::getenv("SPQR_NO_NARROW") != nullptr;
-        size_t nsmem = 0;
-        int nmaxm = 1;
+        size_t nsmem[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        size_t nnar = 0;
         for (size_t i = 0; i < cd.size(); ++i) {
-            if (!no_narrow && cpqr_narrow_ok(cd[i].m, cd[i].n)) {
-                narrow.push_back(static_cast<int>(i));
+            const int nc = no_narrow ? -1 : cpqr_narrow_class(cd[i].m, cd[i].n);
+            if (nc >= 0) {
+                narrow[nc].push_back(static_cast<int>(i));
                 nar[i] = 1;
-                nsmem = std::max(nsmem, cpqr_narrow_smem(cd[i].m, cd[i].n));
-                nmaxm = std::max(nmaxm, cd[i].m);
+                ++nnar;
+                if (nc % 6 < 3) nsmem[nc] = std::max(nsmem[nc], cpqr_narrow_smem(cd[i].m, cd[i].n));
             } else if (cpqr_smem_bytes(cd[i].m, cd[i].n) > kSmemBudget) {
                 glob.push_back(static_cast<int>(i));
             }
         }
-        if (!narrow.empty()) {
-            const int* dn = u.put(narrow);
+        for (int c = 0; c < 12; ++c) {
+            if (narrow[c].empty()) continue;
+            const int* dn = u.put(narrow[c]);
             double nb = 0;
-            for (int i : narrow) nb += 16.0 * cd[i].m * cd[i].n;
+            for (int i : narrow[c]) nb += 16.0 * cd[i].m * cd[i].n;
             cudaEvent_t e0 = kt_.begin(st_);
             static const bool nlog = std::getenv("SPQR_BIGLOG") != nullptr;
             cudaEvent_t b0 = nullptr, b1 = nullptr;
@@ -715,21 +718,25 @@ private:
                 cudaEventCreate(&b1);
                 cudaEventRecord(b0, st_);
             }
-            launch_cpqr_narrow(dc, dn, static_cast<int>(narrow.size()), nmaxm, nsmem, st_);
+            launch_cpqr_narrow(c, dc, dn, static_cast<int>(narrow[c].size()), nsmem[c], st_);
             if (nlog) {
                 cudaEventRecord(b1, st_);
                 cudaEventSynchronize(b1);
                 float ms = 0;
                 cudaEventElapsedTime(&ms, b0, b1);
-                int mn_n = 0;
-                for (int i : narrow) mn_n = std::max(mn_n, cd[i].n);
-                std::fprintf(stderr, "[spqr cpqr narrow] %zu (max m %d n %d)  %.3f ms\n", narrow.size(), nmaxm, mn_n, ms);
+                int mm = 0, mn = 0;
+                for (int i : narrow[c]) {
+                    mm = std::max(mm, cd[i].m);
+                    mn = std::max(mn, cd[i].n);
+                }
+                std::fprintf(stderr, "[spqr cpqr narrow] cls %d count %zu max m %d max n %d  %.3f ms\n", c,
+                             narrow[c].size(), mm, mn, ms);
                 cudaEventDestroy(b0);
                 cudaEventDestroy(b1);
             }
             kt_.end(K_CPQR, e0, st_, nb);
         }
-        if (narrow.size() == cd.size()) return;
+        if (nnar == cd.size()) return;
         if (!glob.empty()) {
             auto single = [&](int i) { return 16.0 * std::min(cd[i].m, cd[i].n) * double(cd[i].m) * cd[i].n / 20e9; };
             auto cost = [&](int i) {

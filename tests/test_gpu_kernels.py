@@ -79,7 +79,9 @@ def test_qr_flags_singular_pivot():
 @pytest.mark.parametrize("shape,eps", [((8, 8), 1e-2), ((20, 35), 1e-3), ((35, 20), 1e-8), ((64, 200), 1e-2),
                                        ((3, 14), 1e-10), ((14, 3), 0.0),
                                        # short-wide sparsify_cols blocks (cpqr_narrow.cu)
-                                       ((11, 475), 1e-2), ((33, 1000), 1e-2), ((1, 50), 1e-2), ((64, 300), 0.0)])
+                                       ((11, 475), 1e-2), ((33, 1000), 1e-2), ((1, 50), 1e-2), ((64, 300), 0.0),
+                                       ((100, 200), 1e-2), ((84, 448), 1e-2), ((128, 700), 1e-3),
+                                       ((20, 1500), 1e-2), ((90, 1800), 1e-2)])
 def test_cpqr_matches_oracle(shape, eps, path, monkeypatch):
     """auto = short-wide kernel where eligible (cpqr_narrow.cu); smem = one CTA per block (kernels.cu)."""
     if path != "auto":
