@@ -122,11 +122,13 @@ def load_peaks():
 
 
 def ncu_traffic(kernel):
-    """dram bytes per launch for `kernel` from the committed ncu --set full summary, if any."""
+    """dram bytes (read + write) of one launch of kernel family `kernel` from the committed
+    ncu --set full summary (profiles/ncu_traffic.json), if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(kernel)
+            v = json.load(f).get(kernel)
+        return v.get("dram_bytes") if isinstance(v, dict) else v
     except Exception:
         return None
 
