@@ -151,10 +151,18 @@ def cpu_oracle_step(p):
 FP64_PEAK_TFLOPS = 37.1  # DMMA m8n8k4 on this pool's B200, tools/fp64_peak.cu -> profiles/r01_fp64_peak.txt
 
 
-def front_qr_microbench(local):
+def microbench_shard(nb, ws, rank):
+    """Rows of a batch owned by `rank`: contiguous, sizes differ by at most one (no exchange)."""
+    base, rem = divmod(nb, ws)
+    return base + (1 if rank < rem else 0)
+
+
+def front_qr_microbench(local, ws=1, rank=0):
     """BASELINE config 5: batched front QR + Q^T on a 256-column neighbour block,
     through spqr_qr_apply_batched_dev (device buffers, CUDA events inside the call),
-    best of 3 after one warm-up; FP64 TFLOP/s against the measured DMMA peak."""
+    best of 3 after one warm-up; FP64 TFLOP/s against the measured DMMA peak.
+    With N ranks the batch is split across GPUs (independent fronts, no exchange;
+    SURVEY 8(e)) and the time is the max over ranks."""
     import ctypes as C
     import torch
     import paper_2102_09878_b200 as P
@@ -163,29 +171,34 @@ def front_qr_microbench(local):
     for (m, n, nb) in ((128, 32, 4096), (512, 128, 1024), (4096, 1024, 64)):
         k = 256
         ntot = n + k
-        g = torch.Generator(device="cuda").manual_seed(0)
-        A0 = torch.randn(nb, ntot, m, dtype=torch.float64, device=f"cuda:{local}", generator=g)
-        tau = torch.empty(nb, n, dtype=torch.float64, device=A0.device)
-        sg = torch.empty(nb, n, dtype=torch.float64, device=A0.device)
-        info = torch.empty(nb, dtype=torch.int32, device=A0.device)
+        mine = microbench_shard(nb, ws, rank)
+        g = torch.Generator(device=f"cuda:{local}").manual_seed(1000 * rank)
+        A0 = torch.randn(max(mine, 1), ntot, m, dtype=torch.float64, device=f"cuda:{local}", generator=g)
+        tau = torch.empty(max(mine, 1), n, dtype=torch.float64, device=A0.device)
+        sg = torch.empty(max(mine, 1), n, dtype=torch.float64, device=A0.device)
+        info = torch.empty(max(mine, 1), dtype=torch.int32, device=A0.device)
         best = 1e30
         for r in range(4):
             A = A0.clone()
             torch.cuda.synchronize()
+            barrier(ws)
             ms = C.c_float()
-            rc = L.spqr_qr_apply_batched_dev(nb, m, n, ntot, C.c_void_p(A.data_ptr()), C.c_void_p(tau.data_ptr()),
-                                             C.c_void_p(sg.data_ptr()), C.c_void_p(info.data_ptr()), C.byref(ms))
-            if rc != 0:
-                raise RuntimeError("spqr_qr_apply_batched_dev failed")
+            if mine > 0:
+                rc = L.spqr_qr_apply_batched_dev(mine, m, n, ntot, C.c_void_p(A.data_ptr()), C.c_void_p(tau.data_ptr()),
+                                                 C.c_void_p(sg.data_ptr()), C.c_void_p(info.data_ptr()), C.byref(ms))
+                if rc != 0:
+                    raise RuntimeError("spqr_qr_apply_batched_dev failed")
             if r > 0:
-                best = min(best, ms.value)
+                best = min(best, allmax(ws, ms.value))
         fl = (2 * m * n * n - 2 / 3 * n ** 3 + 4 * m * n * k - 2 * n * n * k) * nb
         by = 16.0 * m * ntot * nb
-        rows.append({"shape": f"{m}x{n}+{k}", "batch": nb, "ms": round(best, 3),
-                     "TFLOP/s": round(fl / best / 1e9, 2), "frac_fp64": round(fl / best / 1e9 / FP64_PEAK_TFLOPS, 3),
+        rows.append({"shape": f"{m}x{n}+{k}", "batch": nb, "n_gpus": ws, "ms": round(best, 3),
+                     "TFLOP/s": round(fl / best / 1e9, 2),
+                     "frac_fp64": round(fl / best / 1e9 / (FP64_PEAK_TFLOPS * ws), 3),
                      "GB/s": round(by / best / 1e6, 1)})
         del A0, A
-    return {"peak_tflops": FP64_PEAK_TFLOPS, "peak_source": "measured DMMA (tools/fp64_peak.cu)", "shapes": rows}
+    return {"peak_tflops_per_gpu": FP64_PEAK_TFLOPS, "peak_source": "measured DMMA (tools/fp64_peak.cu)",
+            "sharding": "batch split across ranks, no exchange; time = max over ranks", "shapes": rows}
 
 
 def l2_flush(buf):
@@ -276,11 +289,13 @@ def run_ours(args, ws, rank, local):
                   "solve_event_s": round(t["solve_event_ms"] / 1e3, 4), "engine_syncs": g.syncs,
                   "elim_waves": t["elim_waves"]},
     }
-    if rank == 0 and not args.no_microbench:
+    if not args.no_microbench:
         try:
-            out["front_qr_microbench"] = front_qr_microbench(local)
+            mb = front_qr_microbench(local, ws, rank)
         except Exception as e:  # reported, never fatal for the headline line
-            out["front_qr_microbench"] = {"error": str(e)[:200]}
+            mb = {"error": str(e)[:200]}
+        if rank == 0:
+            out["front_qr_microbench"] = mb
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         v, wall, iters, tpart = cpu_oracle_step(p)
         out["cpu_baseline"] = {"value": round(v, 4), "unit": "s", "cores": 1, "kind": "port",

@@ -1,6 +1,7 @@
 """N>1 plumbing of bench.py on CPU (gloo, world_size 2): process-group init from
 torchrun-style env, barrier, max-over-ranks timing, and rank-0-only reporting of
-the reference arm.  The GPU path itself is "replicas only" in round 1."""
+the reference arm, and the split of the C5 microbenchmark batch across ranks.  The C2
+factorization is "replicas only"."""
 import os
 import socket
 import subprocess
@@ -19,7 +20,12 @@ assert ws == 2 and rank == int(os.environ["RANK"])
 bench.barrier(ws)
 v = bench.allmax(ws, 1.5 + rank)          # per-rank step time
 assert v == 2.5, v
-import torch.distributed as dist
+import torch, torch.distributed as dist
+# the C5 microbenchmark batch is split across ranks with no overlap and nothing dropped
+for nb in (4096, 1024, 64, 3):
+    t = torch.tensor([bench.microbench_shard(nb, ws, rank)], dtype=torch.int64)
+    dist.all_reduce(t)
+    assert int(t.item()) == nb, (nb, int(t.item()))
 # rank != 0 must not run the CPU reference arm
 class A: steps = 1; warmup = 0
 if rank != 0:
