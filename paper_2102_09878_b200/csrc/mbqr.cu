@@ -175,6 +175,144 @@ __global__ void __launch_bounds__(32 * NWP) k_panel(double* __restrict__ a, int 
     }
 }
 
+// Panel factorisation, row-group layout: warp g owns a contiguous chunk of
+// rows of the w <= 32 panel columns; within a warp, lanes stride the rows
+// (coalesced in HBM or shared memory alike).  Per reflector: warps reduce the
+// tail norm of column k over their rows (barrier), every thread forms the same
+// Householder scalars (Eigen makeHouseholder), the warps scale their rows of
+// column k and publish v (barrier), then each warp accumulates v^T a_j for all
+// 32 columns in registers and folds them with a 31-shuffle transpose reduction
+// (lane j ends with column j); per-warp partials are reduced (barrier) before
+// the rank-1 update.  Lanes left of k carry v_j^T v_k from the same pass, which
+// builds the compact-WY factor T column by column (accumulate_wy,
+// dense_kernels.cpp:41-53).  The panel is staged in shared memory when it
+// fits, else it is walked in place.
+template <int NWP>
+__global__ void __launch_bounds__(32 * NWP) k_panel2(double* __restrict__ a, int ld, long long stride, int m, int j0,
+                                                     int w, double* __restrict__ tau_all, int tau_stride,
+                                                     double* __restrict__ T_all, int smem_rows) {
+    const int b = blockIdx.x;
+    double* A = a + b * stride;
+    double* tau = tau_all + static_cast<long long>(b) * tau_stride;
+    double* T = T_all + static_cast<long long>(b) * NB * NB;
+    extern __shared__ double sm[];
+    __shared__ double red[NWP], part[NWP][32], Ts[NB * NB], gv[NB];
+    __shared__ double s_c0;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int rows = m - j0;
+    const bool staged = rows <= smem_rows;
+    double* P;
+    long long pld;
+    double* vsh;
+    if (staged) {
+        pld = rows;
+        P = sm;
+        vsh = sm + pld * w;
+        for (int e = threadIdx.x; e < rows * w; e += blockDim.x) {
+            const int j = e / rows, i = e - j * rows;
+            P[i + j * pld] = A[(j0 + i) + static_cast<long long>(j0 + j) * ld];
+        }
+    } else {
+        pld = ld;
+        P = A + j0 + static_cast<long long>(j0) * ld;
+        vsh = sm;
+    }
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) Ts[e] = 0.0;
+    __syncthreads();
+    const int per = (((rows + NWP - 1) / NWP) + 31) & ~31;  // whole warps of rows
+    const int r_lo = min(rows, wid * per), r_hi = min(rows, r_lo + per);
+    const int kmax = min(w, rows);
+    for (int k = 0; k < kmax; ++k) {
+        double* pk = P + static_cast<long long>(k) * pld;
+        double s = 0.0;
+        for (int r = max(r_lo, k + 1) + lane; r < r_hi; r += 32) s = fma(pk[r], pk[r], s);
+        s = wsum(s);
+        if (lane == 0) red[wid] = s;
+        if (lane == 0 && r_lo <= k && k < r_hi) s_c0 = pk[k];
+        __syncthreads();
+        double tail2 = 0.0;
+#pragma unroll
+        for (int g = 0; g < NWP; ++g) tail2 += red[g];
+        const double c0 = s_c0;
+        double t = 0.0, den = 0.0, beta = c0;
+        if (!(tail2 <= DBL_MIN)) {
+            beta = sqrt(c0 * c0 + tail2);
+            if (c0 >= 0.0) beta = -beta;
+            den = c0 - beta;
+            t = (beta - c0) / beta;
+        }
+        for (int r = max(r_lo, k + 1) + lane; r < r_hi; r += 32) {
+            const double v = (t == 0.0) ? 0.0 : pk[r] / den;
+            pk[r] = v;
+            vsh[r] = v;
+        }
+        if (lane == 0 && r_lo <= k && k < r_hi) {
+            pk[k] = beta;
+            vsh[k] = 1.0;
+        }
+        if (threadIdx.x == 0) tau[j0 + k] = t;
+        __syncthreads();
+        if (t != 0.0) {
+            // acc[j] = sum over this warp's rows >= k of v * a_j (all 32 columns)
+            double acc[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+            for (int r = max(r_lo, k) + lane; r < r_hi; r += 32) {
+                const double v = vsh[r];
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < w) acc[j] = fma(v, P[r + j * pld], acc[j]);
+            }
+            // transpose reduction: lane j ends with column j's warp total
+#pragma unroll
+            for (int o = 16, cnt = 16; o >= 1; o >>= 1, cnt >>= 1) {
+                const bool up = lane & o;
+#pragma unroll
+                for (int i = 0; i < cnt; ++i) {
+                    const double send = up ? acc[i] : acc[i + cnt];
+                    const double keep = up ? acc[i + cnt] : acc[i];
+                    acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            part[wid][lane] = acc[0];
+        }
+        __syncthreads();
+        if (t != 0.0) {
+            double wl = 0.0;
+#pragma unroll
+            for (int g = 0; g < NWP; ++g) wl += part[g][lane];
+            const double twl = (lane > k && lane < w) ? -t * wl : 0.0;
+            double tws[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tws[j] = __shfl_sync(0xffffffffu, twl, j);
+            for (int r = max(r_lo, k) + lane; r < r_hi; r += 32) {
+                const double v = vsh[r];
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j > k && j < w) P[r + j * pld] = fma(tws[j], v, P[r + j * pld]);
+            }
+            if (wid == 0) {  // T(:, k) = -t T(0:k, 0:k) (V^T v_k),  T(k, k) = t
+                if (lane < k) gv[lane] = wl;
+                __syncwarp();
+                if (lane < k) {
+                    double sacc = 0.0;
+                    for (int l = lane; l < k; ++l) sacc = fma(Ts[lane + l * NB], gv[l], sacc);
+                    Ts[lane + k * NB] = -t * sacc;
+                }
+                if (lane == 0) Ts[k + k * NB] = t;
+                __syncwarp();
+            }
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) T[e] = Ts[e];
+    if (staged)
+        for (int e = threadIdx.x; e < rows * w; e += blockDim.x) {
+            const int j = e / rows, i = e - j * rows;
+            A[(j0 + i) + static_cast<long long>(j0 + j) * ld] = P[i + j * pld];
+        }
+}
+
 // Block reflector on a TC-column tile of the trailing matrix:
 //   W = V^T C (w x TC), W = T^T W, C -= V W.   16 warps, DMMA 8x8x4.
 constexpr int TC2 = 128;
@@ -344,20 +482,18 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
     for (int j0 = 0; j0 < n; j0 += NB) {
         const int w = std::min(NB, n - j0);
         const int rows = m - j0;
-        const int smem_rows = static_cast<int>(smem_cap / (sizeof(double) * NB)) - 1;
-        const size_t smem = rows <= smem_rows ? sizeof(double) * (rows + 1) * w : 0;
-        if (rows <= 256) {
+        // staged panel: (rows|1) x w plus v (rows); else in place with v in shared memory
+        const int smem_rows = static_cast<int>(smem_cap / (sizeof(double) * (NB + 1))) - 2;
+        const size_t smem = rows <= smem_rows ? sizeof(double) * (rows * static_cast<size_t>(w) + rows)
+                                              : sizeof(double) * static_cast<size_t>(rows);
+        if (rows <= 512) {
             static size_t cfg = 0;
-            smem_optin(reinterpret_cast<const void*>(k_panel<1>), smem, cfg);
-            k_panel<1><<<nbatch, 32, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
-        } else if (rows <= 1024) {
-            static size_t cfg = 0;
-            smem_optin(reinterpret_cast<const void*>(k_panel<4>), smem, cfg);
-            k_panel<4><<<nbatch, 128, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
+            smem_optin(reinterpret_cast<const void*>(k_panel2<8>), smem, cfg);
+            k_panel2<8><<<nbatch, 256, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
         } else {
             static size_t cfg = 0;
-            smem_optin(reinterpret_cast<const void*>(k_panel<16>), smem, cfg);
-            k_panel<16><<<nbatch, 512, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
+            smem_optin(reinterpret_cast<const void*>(k_panel2<16>), smem, cfg);
+            k_panel2<16><<<nbatch, 512, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
         }
         const int trail = ntot - (j0 + w);
         if (trail > 0) {
