@@ -316,6 +316,19 @@ __global__ void __launch_bounds__(32 * NWP) k_panel2(double* __restrict__ a, int
 // Block reflector on a TC-column tile of the trailing matrix:
 //   W = V^T C (w x TC), W = T^T W, C -= V W.   16 warps, DMMA 8x8x4.
 constexpr int TC2 = 128;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// The C chunks stream through two shared-memory buffers: the copy of chunk
+// c+1 (cp.async, zero-filled outside the block) is in flight while the DMMA
+// tiles of chunk c run.  Pass 2 writes the updated chunk back through shared
+// memory so the global stores are coalesced column runs.
 __global__ void __launch_bounds__(512) k_wy(double* __restrict__ a, int ld, long long stride, int m, int ntot, int j0,
                                             int w, const double* __restrict__ T_all) {
     const int b = blockIdx.y;
@@ -325,11 +338,12 @@ __global__ void __launch_bounds__(512) k_wy(double* __restrict__ a, int ld, long
     const int nc = min(TC2, ntot - c0);
     if (nc <= 0) return;
     extern __shared__ double dsm[];
-    double* sV = dsm;                  // V chunk (CH x NB), column-major, ld LDV
-    double* sC = sV + NB * LDV;        // C chunk (CH x TC2), column-major, ld LDC
-    double* sW = sC + TC2 * LDC;       // W (NB x TC2), column-major, ld LDW
+    // V chunks (pass 1: CH x NB column-major, ld LDV; pass 2 transposed, ld LDVT)
+    constexpr int VSZ = (NB * LDV > CH * LDVT) ? NB * LDV : CH * LDVT;
+    double* sVb[2] = {dsm, dsm + VSZ};
+    double* sCb[2] = {dsm + 2 * VSZ, dsm + 2 * VSZ + TC2 * LDC};  // C chunks, ld LDC
+    double* sW = sCb[1] + TC2 * LDC;   // W (NB x TC2), column-major, ld LDW
     double* sT = sW + TC2 * LDW;
-    double* sVt = sT + NB * LDW;       // V chunk transposed (pass 2)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = lane >> 2, t4 = lane & 3;
     for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
@@ -337,38 +351,52 @@ __global__ void __launch_bounds__(512) k_wy(double* __restrict__ a, int ld, long
         sT[i + j * LDW] = (i < w && j < w) ? T[e] : 0.0;
     }
     const int rows = m - j0;
-    auto load_chunk = [&](int r0, int rc, bool transposed) {
-        for (int e = threadIdx.x; e < CH * NB; e += blockDim.x) {
-            const int i = e % CH, j = e / CH;
-            const int r = r0 + i;
-            double v = 0.0;
-            if (i < rc && j < w) v = (r > j) ? A[(j0 + r) + static_cast<long long>(j0 + j) * ld] : (r == j ? 1.0 : 0.0);
-            if (transposed)
-                sVt[j + i * LDVT] = v;
-            else
-                sV[i + j * LDV] = v;
-        }
+    const int nchunk = (rows + CH - 1) / CH;
+    // chunk c of C and of V (unit lower trapezoid: the rows at or above the
+    // diagonal are written directly, the rest streams in with cp.async)
+    auto issue = [&](int c, bool transposed) {
+        const int r0 = c * CH, rc = min(CH, rows - r0);
+        double* cb = sCb[c & 1];
+        double* vb = sVb[c & 1];
         for (int e = threadIdx.x; e < CH * TC2; e += blockDim.x) {
             const int i = e % CH, j = e / CH;
-            sC[i + j * LDC] = (i < rc && j < nc) ? A[(j0 + r0 + i) + static_cast<long long>(c0 + j) * ld] : 0.0;
+            const bool ok = i < rc && j < nc;
+            cp_async8(cb + i + j * LDC, ok ? A + (j0 + r0 + i) + static_cast<long long>(c0 + j) * ld : A, ok);
         }
+        for (int e = threadIdx.x; e < CH * NB; e += blockDim.x) {
+            const int i = e % CH, j = e / CH, r = r0 + i;
+            double* dst = transposed ? vb + j + i * LDVT : vb + i + j * LDV;
+            if (i < rc && j < w && r <= j)
+                *dst = (r == j) ? 1.0 : 0.0;
+            else {
+                const bool ok = i < rc && j < w;
+                cp_async8(dst, ok ? A + (j0 + r) + static_cast<long long>(j0 + j) * ld : A, ok);
+            }
+        }
+        cp_commit();
     };
     // ---- pass 1: W = V^T C; warp: W rows (wid&3)*8.., cols (wid>>2)*32.. (4 tiles)
     double acc[4][2] = {};
     const int mr = (wid & 3) * 8, nc0 = (wid >> 2) * 32;
-    for (int r0 = 0; r0 < rows; r0 += CH) {
-        const int rc = min(CH, rows - r0);
+    issue(0, false);
+    for (int c = 0; c < nchunk; ++c) {
+        if (c + 1 < nchunk) issue(c + 1, false);
+        if (c + 1 < nchunk)
+            cp_wait<1>();
+        else
+            cp_wait<0>();
         __syncthreads();
-        load_chunk(r0, rc, false);
-        __syncthreads();
+        const double* sC = sCb[c & 1];
+        const double* sV = sVb[c & 1];
 #pragma unroll 4
         for (int k0 = 0; k0 < CH; k0 += 4) {
             const double av = sV[(k0 + t4) + (mr + g) * LDV];
 #pragma unroll
             for (int q = 0; q < 4; ++q) dmma(acc[q][0], acc[q][1], av, sC[(k0 + t4) + (nc0 + q * 8 + g) * LDC]);
         }
+        __syncthreads();
     }
-    __syncthreads();
+    issue(0, true);  // pass 2's first chunk streams in while W is finished
     for (int q = 0; q < 4; ++q) {
         sW[(mr + g) + (nc0 + q * 8 + 2 * t4) * LDW] = acc[q][0];
         sW[(mr + g) + (nc0 + q * 8 + 2 * t4 + 1) * LDW] = acc[q][1];
@@ -389,11 +417,16 @@ __global__ void __launch_bounds__(512) k_wy(double* __restrict__ a, int ld, long
     }
     // ---- pass 2: C -= V W2; warp: chunk rows (wid&7)*8.., cols (wid>>3)*64.. (8 tiles)
     const int rr = (wid & 7) * 8, cc0 = (wid >> 3) * 64;
-    for (int r0 = 0; r0 < rows; r0 += CH) {
-        const int rc = min(CH, rows - r0);
+    for (int c = 0; c < nchunk; ++c) {
+        const int r0 = c * CH, rc = min(CH, rows - r0);
+        if (c + 1 < nchunk) issue(c + 1, true);
+        if (c + 1 < nchunk)
+            cp_wait<1>();
+        else
+            cp_wait<0>();
         __syncthreads();
-        load_chunk(r0, rc, true);
-        __syncthreads();
+        double* sC = sCb[c & 1];
+        const double* sVt = sVb[c & 1];
         double o[8][2];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -406,14 +439,17 @@ __global__ void __launch_bounds__(512) k_wy(double* __restrict__ a, int ld, long
 #pragma unroll
             for (int q = 0; q < 8; ++q) dmma(o[q][0], o[q][1], av, sW[(k0 + t4) + (cc0 + q * 8 + g) * LDW]);
         }
-        const int i = rr + g;
-        if (i < rc)
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int ja = cc0 + q * 8 + 2 * t4, jb = ja + 1;
-                if (ja < nc) A[(j0 + r0 + i) + static_cast<long long>(c0 + ja) * ld] = -o[q][0];
-                if (jb < nc) A[(j0 + r0 + i) + static_cast<long long>(c0 + jb) * ld] = -o[q][1];
-            }
+        for (int q = 0; q < 8; ++q) {  // each element is read and written by its own thread only
+            sC[(rr + g) + (cc0 + q * 8 + 2 * t4) * LDC] = -o[q][0];
+            sC[(rr + g) + (cc0 + q * 8 + 2 * t4 + 1) * LDC] = -o[q][1];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < CH * TC2; e += blockDim.x) {
+            const int i = e % CH, j = e / CH;
+            if (i < rc && j < nc) A[(j0 + r0 + i) + static_cast<long long>(c0 + j) * ld] = sC[i + j * LDC];
+        }
+        __syncthreads();
     }
 }
 
@@ -498,7 +534,8 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
         const int trail = ntot - (j0 + w);
         if (trail > 0) {
             dim3 grid((trail + TC2 - 1) / TC2, nbatch);
-            const size_t wsm = sizeof(double) * (NB * LDV + TC2 * LDC + TC2 * LDW + NB * LDW + CH * LDVT);
+            const size_t vsz = std::max(NB * LDV, CH * LDVT);
+            const size_t wsm = sizeof(double) * (2 * vsz + 2 * TC2 * LDC + TC2 * LDW + NB * LDW);
             static size_t cfg = 0;
             smem_optin(reinterpret_cast<const void*>(k_wy), wsm, cfg);
             k_wy<<<grid, 512, wsm, st>>>(d_a, ldA, stride, m, ntot, j0, w, d_T);
