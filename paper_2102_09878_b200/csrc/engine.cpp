@@ -948,16 +948,21 @@ void Engine::init_fronts(const std::vector<int>& owner) {
             }
         }
     }
-    size_t total = 0;
-    for (size_t c = 0; c < fr_.size(); ++c) {
+#pragma omp parallel for schedule(dynamic, 256)
+    for (long long c = 0; c < static_cast<long long>(fr_.size()); ++c) {
         Front& f = fr_[c];
         if (!f.live) continue;
         std::sort(f.keys.begin(), f.keys.end(), [](const KeyRef& a, const KeyRef& b) { return a.key < b.key; });
         f.keys.erase(std::unique(f.keys.begin(), f.keys.end(), [](const KeyRef& a, const KeyRef& b) { return a.key == b.key; }),
                      f.keys.end());
         layout(static_cast<int>(c), f.keys, f.ncols);
-        for (auto& k : f.keys) holders_[k.key].add(static_cast<int>(c));
         f.ld = std::max(1, f.nrows());
+    }
+    size_t total = 0;
+    for (size_t c = 0; c < fr_.size(); ++c) {
+        Front& f = fr_[c];
+        if (!f.live) continue;
+        for (auto& k : f.keys) holders_[k.key].add(static_cast<int>(c));
         total += static_cast<size_t>(f.ld) * f.ncols;
     }
     // one zeroed slab for all initial fronts + scatter of A's values
@@ -972,6 +977,7 @@ void Engine::init_fronts(const std::vector<int>& owner) {
     }
     // scatter: per nnz destination offset (host-computed), values from A
     std::vector<long long> dsto(A_.nnz());
+#pragma omp parallel for schedule(dynamic, 1024)
     for (Index j = 0; j < A_.n; ++j) {
         const int q = h_.finest_of_col[j];
         for (Index k = A_.p[j]; k < A_.p[j + 1]; ++k) {
@@ -2377,11 +2383,12 @@ void Engine::merge_level() {
     std::unique_ptr<NScope> m2 = std::make_unique<NScope>(nprof_, "merge.flush+rebuild_host");
     flush_assemble(mb);
     for (size_t c = 0; c < fr_.size(); ++c)
-        if (fr_[c].live) {
-            dfree(fr_[c].mat, fr_[c].big);
-            fr_[c] = Front();
-        }
-    for (auto& hs : holders_) hs.clear();
+        if (fr_[c].live && fr_[c].big) dfree(fr_[c].mat, true);
+#pragma omp parallel for schedule(dynamic, 512)
+    for (long long c = 0; c < static_cast<long long>(fr_.size()); ++c)
+        if (fr_[c].live) fr_[c] = Front();
+#pragma omp parallel for schedule(dynamic, 512)
+    for (long long c = 0; c < static_cast<long long>(holders_.size()); ++c) holders_[c].clear();
     for (int g = 0; g < ng; ++g) {
         const int P = gp[g];
         fr_[P] = std::move(plans[g].nf);
