@@ -86,6 +86,11 @@ void spqr_pipeline_wfactor(const spqr_pipeline* p, int i, int* out4);
 /* kind 0: cols, R (c x c), coupled, C (c x k).  kind 1: cols, V (c x k), tau, sign. */
 int spqr_pipeline_wfactor_data(const spqr_pipeline* p, int i, int* cols, double* a, int* coupled, double* b,
                                double* c);
+/* save_factorization (proj/src/transforms.cpp:206-240; declared transforms.h:75): write the
+ * factorization (M, N, eps, pivot/dropped/trailing rows, W in chronological order) as an
+ * SPQRFW01 file readable by the reference's load_factorization (transforms.cpp:242-289).
+ * Returns SPQR_OK, or an error code with the message in err. */
+int spqr_pipeline_save(const spqr_pipeline* p, const char* path, char* err, int errlen);
 
 /* ---- dense kernels (dense_kernels.h:24-54), batched, one launch each ---- */
 /* block_householder_qr + apply_reflectors_left_t fused: for each of nb problems

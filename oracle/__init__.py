@@ -61,6 +61,8 @@ def lib():
         L.orc_pipeline_wfactor.argtypes = [vp, C.c_int, i32p]
         L.orc_pipeline_wfactor_data.argtypes = [vp, C.c_int, i32p, f64p, i32p, f64p, f64p]
         L.orc_pipeline_apply.argtypes = [vp, C.c_int, f64p, C.c_char_p, C.c_int]
+        L.orc_pipeline_save.argtypes = [vp, C.c_char_p, C.c_char_p, C.c_int]
+        L.orc_factor_file_apply.argtypes = [C.c_char_p, C.c_int, vp, C.c_longlong, i64p, C.c_char_p, C.c_int]
         L.orc_pipeline_solve.argtypes = [vp, C.c_int, f64p, f64p, C.c_double, C.c_int, C.POINTER(C.c_int),
                                          C.POINTER(C.c_int), f64p, C.POINTER(C.c_int), C.POINTER(C.c_double),
                                          C.c_char_p, C.c_int]
@@ -252,6 +254,12 @@ class Pipeline:
             raise RuntimeError(err.value.decode())
         return z
 
+    def save(self, path):
+        """save_factorization (transforms.cpp:206-240): SPQRFW01 file."""
+        err = C.create_string_buffer(512)
+        if lib().orc_pipeline_save(self.h, str(path).encode(), err, 512):
+            raise RuntimeError(err.value.decode())
+
     def w_apply(self, z): return self._apply(0, z)
     def w_solve(self, z): return self._apply(1, z)
     def wt_apply(self, z): return self._apply(2, z)
@@ -440,3 +448,18 @@ def match_rows(A):
     cr = np.zeros(m, np.int32)
     size = lib().orc_match_rows(m, n, p, i, x, rc, cr)
     return rc, cr, size
+
+
+def factor_file_apply(path, mode, z=None):
+    """load_factorization (transforms.cpp:242-289) of an SPQRFW01 file, then one sweep:
+    mode 'w_apply' | 'w_solve' | 'wt_apply' | 'wt_solve'.  Returns (M, N, nW) and the
+    transformed copy of z (None when z is None)."""
+    md = {"w_apply": 0, "w_solve": 1, "wt_apply": 2, "wt_solve": 3}[mode]
+    dims = np.zeros(3, np.int64)
+    err = C.create_string_buffer(512)
+    v = None if z is None else np.array(z, np.float64, copy=True)
+    rc = lib().orc_factor_file_apply(str(path).encode(), md, None if v is None else v.ctypes.data_as(C.c_void_p),
+                                     0 if v is None else len(v), dims, err, 512)
+    if rc:
+        raise RuntimeError(err.value.decode())
+    return tuple(int(d) for d in dims), v

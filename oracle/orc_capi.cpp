@@ -316,6 +316,38 @@ int orc_pipeline_apply(void* hv, int mode, double* z, char* err, int errlen) {
     });
 }
 
+// SPQRFW01 files (transforms.cpp:129-289): save this pipeline's factorization;
+// load a file and apply one W/Q sweep with it (mode as orc_pipeline_apply).
+int orc_pipeline_save(void* hv, const char* path, char* err, int errlen) {
+    const Pipeline& P = *static_cast<PipeH*>(hv)->p;
+    int cl = -1;
+    return guarded(err, errlen, &cl, [&] { save_factorization(P.F, path); });
+}
+
+int orc_factor_file_apply(const char* path, int mode, double* z, long long nz, long long* dims, char* err, int errlen) {
+    int cl = -1;
+    return guarded(err, errlen, &cl, [&] {
+        const Factorization F = load_factorization(path);
+        dims[0] = F.M;
+        dims[1] = F.N;
+        dims[2] = static_cast<long long>(F.W.size());
+        if (!z) return;
+        const size_t n = (mode >= 4) ? F.M : F.N;
+        if (static_cast<long long>(n) != nz) throw std::invalid_argument("vector length does not match the factorization");
+        Vec v(z, z + n);
+        switch (mode) {
+            case 0: F.w_apply(v); break;
+            case 1: F.w_solve(v); break;
+            case 2: F.wt_apply(v); break;
+            case 3: F.wt_solve(v); break;
+            case 4: F.q_apply_t(v); break;
+            case 5: F.q_apply(v); break;
+            default: throw std::invalid_argument("bad mode");
+        }
+        std::copy(v.begin(), v.end(), z);
+    });
+}
+
 // Pipeline::solve (direct=0) / solve_direct (direct=1). hist needs maxit+2 slots.
 int orc_pipeline_solve(void* hv, int direct, const double* b, double* x, double tol, int maxit, int* iters,
                        int* converged, double* hist, int* nhist, double* t_solve, char* err, int errlen) {

@@ -227,6 +227,10 @@ struct Factorization {  // transforms.h:53-72
     void q_apply_t(Vec& y) const;
     void q_apply(Vec& y) const;
 };
+// SPQRFW01 factor file (transforms.cpp:129-289), orc_serialize.cpp
+void save_factorization(const Factorization& f, const std::string& path);
+Factorization load_factorization(const std::string& path);
+
 
 // ------------------------------------------------------------- factorize ---
 struct FactorizeOptions { double eps = 1e-2; int skip_levels = 3; bool store_q = false; };  // factorize.h:13-17

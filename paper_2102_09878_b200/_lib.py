@@ -45,6 +45,7 @@ SIGNATURES = {
     "spqr_pipeline_stage_fronts": (None, [vp, C.c_int, i32p, f64p]),
     "spqr_pipeline_wfactor": (None, [vp, C.c_int, i32p]),
     "spqr_pipeline_wfactor_data": (C.c_int, [vp, C.c_int, i32p, f64p, i32p, f64p, f64p]),
+    "spqr_pipeline_save": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_int]),
     "spqr_qr_apply_batched": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, f64p, f64p, f64p, i32p]),
     "spqr_qr_apply_batched_dev": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp,
                                             C.POINTER(C.c_float)]),

@@ -154,6 +154,12 @@ class Pipeline:
                             t_reassign=t[1], t_scale=t[2], t_sparsify=t[3], t_merge=t[4]))
         return out
 
+    def save(self, path):
+        """save_factorization (transforms.cpp:206-240): SPQRFW01 file of this factorization."""
+        err = C.create_string_buffer(512)
+        if lib().spqr_pipeline_save(self.h, str(path).encode(), err, 512):
+            raise RuntimeError(err.value.decode())
+
     def wfactors(self):
         out = []
         info = np.zeros(4, np.int32)

@@ -7,7 +7,9 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
 #include <cstdlib>
+#include <memory>
 #include <numeric>
 #include <string>
 #ifdef _OPENMP
@@ -336,6 +338,80 @@ int spqr_pipeline_wfactor_data(const spqr_pipeline* p, int i, int* cols, double*
                 CK(cudaMemcpy(c, w.sign, sizeof(double) * w.k, cudaMemcpyDeviceToHost));
             }
         }
+    });
+}
+
+// save_factorization (transforms.cpp:206-240): the device-resident W written in
+// the reference's SPQRFW01 layout (little-endian int64 sizes and indices, IEEE
+// doubles; TriangularScale = tag 0: cols, R, coupled, C; ColumnRotation = tag
+// 1: cols, V, tau, sign; no Q part).  The W arena is mirrored to the host with
+// one copy per arena chunk.
+int spqr_pipeline_save(const spqr_pipeline* p, const char* path, char* err, int errlen) {
+    int cl = -1;
+    return guarded(err, errlen, &cl, [&] {
+        if (!p->has_f) throw std::logic_error("spqr_pipeline_save: no factorization (solver=direct)");
+        const DeviceFactorization& F = p->F;
+        std::vector<std::pair<const char*, std::vector<char>>> mirror;
+        F.warena->for_each_chunk([&](const char* base, size_t used) {
+            mirror.emplace_back(base, std::vector<char>(used));
+            if (used) CK(cudaMemcpy(mirror.back().second.data(), base, used, cudaMemcpyDeviceToHost));
+        });
+        auto host = [&](const double* d) -> const double* {
+            const char* c = reinterpret_cast<const char*>(d);
+            for (const auto& m : mirror)
+                if (c >= m.first && c < m.first + m.second.size())
+                    return reinterpret_cast<const double*>(m.second.data() + (c - m.first));
+            throw std::logic_error("spqr_pipeline_save: factor data outside the W arena");
+        };
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) throw std::runtime_error(std::string("cannot open ") + path + " for writing");
+        std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard(f, &std::fclose);
+        auto i64 = [&](long long v) {
+            const int64_t x = v;
+            std::fwrite(&x, 8, 1, f);
+        };
+        auto f64s = [&](const double* v, size_t n) {
+            if (n) std::fwrite(v, 8, n, f);
+        };
+        auto ivec = [&](const int* v, size_t n) {
+            i64(static_cast<long long>(n));
+            for (size_t i = 0; i < n; ++i) i64(v[i]);
+        };
+        std::fwrite("SPQRFW01", 1, 8, f);
+        i64(F.M);
+        i64(F.N);
+        f64s(&F.eps, 1);
+        ivec(F.pivot_row.data(), F.pivot_row.size());
+        ivec(F.dropped_rows.data(), F.dropped_rows.size());
+        ivec(F.trailing_rows.data(), F.trailing_rows.size());
+        i64(static_cast<long long>(F.W.size()));
+        for (const DevWFactor& w : F.W) {
+            const int* cols = F.idx.data() + w.cols_off;
+            if (w.kind == 0) {  // a = [R | C], c x (c + k), column-major
+                const double* a = w.c ? host(w.a) : nullptr;
+                i64(0);
+                ivec(cols, w.c);
+                i64(w.c);
+                i64(w.c);
+                f64s(a, static_cast<size_t>(w.c) * w.c);
+                ivec(F.idx.data() + w.coupled_off, w.k);
+                i64(w.scale_only ? 0 : w.c);  // scale_all's factor keeps the default-constructed C (0 x 0)
+                i64(w.k);
+                f64s(a ? a + static_cast<size_t>(w.c) * w.c : nullptr, static_cast<size_t>(w.c) * w.k);
+            } else {  // V c x k (unit diagonal explicit), tau k, sign k
+                i64(1);
+                ivec(cols, w.c);
+                i64(w.c);
+                i64(w.k);
+                f64s((w.c > 0 && w.k > 0) ? host(w.a) : nullptr, static_cast<size_t>(w.c) * w.k);
+                i64(w.k);
+                f64s(w.k ? host(w.tau) : nullptr, w.k);
+                i64(w.k);
+                f64s(w.k ? host(w.sign) : nullptr, w.k);
+            }
+        }
+        i64(0);  // has_q: the GPU engine does not store Q (store_q is a test-only option)
+        if (std::ferror(f)) throw std::runtime_error(std::string("write failed: ") + path);
     });
 }
 

@@ -57,6 +57,11 @@ public:
         in_use_ = 0;
     }
     size_t peak() const { return peak_; }
+    // (base, used bytes) of every chunk, e.g. to mirror the arena on the host in a few copies
+    template <class F>
+    void for_each_chunk(F f) const {
+        for (const auto& c : chunks_) f(c.base, c.used);
+    }
     size_t reserved() const {
         size_t s = 0;
         for (auto& c : chunks_) s += c.cap;

@@ -909,6 +909,7 @@ private:
         f.cluster = cluster;
         f.c = c;
         f.k = k;
+        f.scale_only = kind == 0 && coupled == nullptr;
         f.cols_off = static_cast<long long>(out_.idx.size());
         out_.idx.insert(out_.idx.end(), cols.begin(), cols.end());
         f.coupled_off = static_cast<long long>(out_.idx.size());

@@ -22,6 +22,7 @@ struct DevWFactor {
     double* a = nullptr;  // kind 0: c x (c+k), ld c.  kind 1: V c x k, ld c
     double* tau = nullptr;
     double* sign = nullptr;
+    bool scale_only = false;  // kind 0 from scale_all: no coupling, C is the empty 0 x 0 block (factorize.cpp:479-482)
 };
 
 enum KTag { K_ASSEMBLE = 0, K_STATS, K_QR, K_TRSM, K_CPQR, K_SCATTER, K_NTAGS };
