@@ -8,3 +8,4 @@ include/spaqr_b200.h); partitioning is host C++ inside the same library.
 from .api import (Pipeline, SingularFrontError, cpqr_batched, qr_apply_batched,  # noqa: F401
                   trsm_right_batched)
 from ._lib import LIB_PATH, build, lib, require_gpu  # noqa: F401
+from .profile import make_profile, validate_profile  # noqa: F401
