@@ -122,7 +122,11 @@ int spqr_pipeline_create(int m, int n, const int* colptr, const int* rowind, con
             P->weights = P->d;
         } else {
             double t0 = now_s();
+            double tp[8];
+            int np_ = 0;
+            tp[np_++] = now_s();
             const Graph g = ata_graph(P->Aw);
+            tp[np_++] = now_s();
             const int L = levels > 0 ? levels : default_num_levels(n);
             if (parts) {
                 P->tree = import_partition(g, L, parts);
@@ -130,12 +134,22 @@ int spqr_pipeline_create(int m, int n, const int* colptr, const int* rowind, con
                 if (coords && dim <= 0) throw std::invalid_argument("coordinate dimension must be positive");
                 P->tree = nested_dissection(g, L, coords, dim);
             }
+            tp[np_++] = now_s();
             P->h = build_interfaces(P->tree, g);
+            tp[np_++] = now_s();
             P->perm = order_columns(P->h);
             P->Aw = permute_columns(P->Aw, P->perm);
+            tp[np_++] = now_s();
             const RowMatching mm = match_rows(P->Aw);
+            tp[np_++] = now_s();
             P->owner = assign_rows(P->Aw, P->h, mm);
+            tp[np_++] = now_s();
             P->t_partition = now_s() - t0;
+            if (std::getenv("SPQR_PROF"))
+                std::fprintf(stderr,
+                             "[spqr prof] partition: ata_graph %.3f nested_dissection %.3f build_interfaces %.3f "
+                             "order+permute %.3f match_rows %.3f assign_rows %.3f s\n",
+                             tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5]);
             P->weights.resize(n);
             for (int i = 0; i < n; ++i) P->weights[i] = P->d[P->perm[i]];
             t0 = now_s();

@@ -84,30 +84,40 @@ Graph ata_graph(const Csc& A) {  // sparse.cpp:170-195: row cliques, sorted, uni
         for (Index j = 0; j < A.n; ++j)
             for (Index k = A.p[j]; k < A.p[j + 1]; ++k) rcol[pos[A.i[k]]++] = j;
     }
-    std::vector<long long> deg(A.n + 1, 0);
-    for (Index r = 0; r < A.m; ++r) {
-        const Index len = rptr[r + 1] - rptr[r];
-        for (Index k = rptr[r]; k < rptr[r + 1]; ++k) deg[rcol[k] + 1] += len - 1;
-    }
-    for (Index v = 0; v < A.n; ++v) deg[v + 1] += deg[v];
-    std::vector<Index> tmp(static_cast<size_t>(deg[A.n]));
-    {
-        std::vector<long long> pos(deg.begin(), deg.end() - 1);
-        for (Index r = 0; r < A.m; ++r)
-            for (Index a = rptr[r]; a < rptr[r + 1]; ++a)
-                for (Index b = rptr[r]; b < rptr[r + 1]; ++b)
-                    if (a != b) tmp[pos[rcol[a]]++] = rcol[b];
-    }
+    // adjacency of v = sorted unique columns sharing a row with v, minus v; built
+    // per column in parallel (count pass, then fill pass at the prefix offsets)
     Graph g;
     g.n = A.n;
     g.ptr.assign(A.n + 1, 0);
-    g.adj.reserve(tmp.size());
-    for (Index v = 0; v < A.n; ++v) {
-        auto b = tmp.begin() + deg[v], e = tmp.begin() + deg[v + 1];
-        std::sort(b, e);
-        auto u = std::unique(b, e);
-        g.adj.insert(g.adj.end(), b, u);
-        g.ptr[v + 1] = static_cast<Index>(g.adj.size());
+    auto neighbours = [&](Index v, std::vector<Index>& nb) {
+        nb.clear();
+        for (Index k = A.p[v]; k < A.p[v + 1]; ++k) {
+            const Index r = A.i[k];
+            for (Index a = rptr[r]; a < rptr[r + 1]; ++a)
+                if (rcol[a] != v) nb.push_back(rcol[a]);
+        }
+        std::sort(nb.begin(), nb.end());
+        nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+    };
+#pragma omp parallel
+    {
+        std::vector<Index> nb;
+#pragma omp for schedule(dynamic, 1024)
+        for (Index v = 0; v < A.n; ++v) {
+            neighbours(v, nb);
+            g.ptr[v + 1] = static_cast<Index>(nb.size());
+        }
+    }
+    for (Index v = 0; v < A.n; ++v) g.ptr[v + 1] += g.ptr[v];
+    g.adj.resize(static_cast<size_t>(g.ptr[A.n]));
+#pragma omp parallel
+    {
+        std::vector<Index> nb;
+#pragma omp for schedule(dynamic, 1024)
+        for (Index v = 0; v < A.n; ++v) {
+            neighbours(v, nb);
+            std::copy(nb.begin(), nb.end(), g.adj.begin() + g.ptr[v]);
+        }
     }
     return g;
 }
@@ -126,12 +136,15 @@ struct Builder {
     const int* parts;
     int L;
     SeparatorTree t;
-    std::vector<char> in;
+    // mark[v] = id of the tree node whose vertex set is being split (the serial
+    // algorithm's "in current set" flag; sibling subtrees run concurrently on
+    // disjoint vertex sets, so every per-vertex array is race-free)
+    std::vector<int> mark;
     std::vector<signed char> side;
     std::vector<int> dist;
 
     Builder(const Graph& g_, const double* x, int d, const int* p, int L_)
-        : g(g_), X(x), dim(d), parts(p), L(L_), in(g_.n, 0), side(g_.n, -1), dist(g_.n, -1) {}
+        : g(g_), X(x), dim(d), parts(p), L(L_), mark(g_.n, -1), side(g_.n, -1), dist(g_.n, -1) {}
 
     double coord(Index v, int a) const { return X[static_cast<size_t>(v) * dim + a]; }
 
@@ -161,7 +174,7 @@ struct Builder {
     }
 
     // partition.cpp:51-87
-    void split_bfs(const std::vector<Index>& s, std::vector<Index>& s1, std::vector<Index>& s2) {
+    void split_bfs(const std::vector<Index>& s, std::vector<Index>& s1, std::vector<Index>& s2, int id) {
         auto sweep = [&](Index src) {
             for (Index v : s) dist[v] = -1;
             std::deque<Index> q{src};
@@ -172,7 +185,7 @@ struct Builder {
                 q.pop_front();
                 if (dist[v] > dist[far] || (dist[v] == dist[far] && v < far)) far = v;
                 for (const Index* u = g.begin(v); u != g.end(v); ++u)
-                    if (in[*u] && dist[*u] < 0) {
+                    if (mark[*u] == id && dist[*u] < 0) {
                         dist[*u] = dist[v] + 1;
                         q.push_back(*u);
                     }
@@ -194,13 +207,13 @@ struct Builder {
     }
 
     // partition.cpp:103-147 (candidate order = side-2 order; in-pass updates)
-    void carve(std::vector<Index>& s1, std::vector<Index>& s2, std::vector<Index>& sep) {
+    void carve(std::vector<Index>& s1, std::vector<Index>& s2, std::vector<Index>& sep, int id) {
         for (Index v : s1) side[v] = 0;
         for (Index v : s2) side[v] = 1;
         std::vector<Index> cand;
         for (Index v : s2)
             for (const Index* u = g.begin(v); u != g.end(v); ++u)
-                if (in[*u] && side[*u] == 0) {
+                if (mark[*u] == id && side[*u] == 0) {
                     cand.push_back(v);
                     break;
                 }
@@ -211,7 +224,7 @@ struct Builder {
                 if (side[v] != 2) continue;
                 bool t1 = false, t2 = false;
                 for (const Index* u = g.begin(v); u != g.end(v); ++u) {
-                    if (!in[*u]) continue;
+                    if (mark[*u] != id) continue;
                     t1 |= side[*u] == 0;
                     t2 |= side[*u] == 1;
                 }
@@ -238,37 +251,47 @@ struct Builder {
         s2.swap(n2);
     }
 
-    int grow(std::vector<Index> s, int level, int parent) {
-        const int id = static_cast<int>(t.nodes.size());
-        t.nodes.emplace_back();
+    // nodes of a subtree rooted at `level` (every inner node has two children)
+    int subtree_size(int level) const { return (1 << (L + 2 - level)) - 1; }
+
+    // preorder ids: node id, then the left subtree, then the right one
+    void grow(std::vector<Index> s, int level, int parent, int id) {
         std::sort(s.begin(), s.end());
-        t.nodes[id].level = level;
-        t.nodes[id].parent = parent;
-        t.nodes[id].vertices = s;
-        if (level == L + 1) return id;
+        SeparatorTree::Node& nd = t.nodes[id];
+        nd.level = level;
+        nd.parent = parent;
+        nd.vertices = s;
+        if (level == L + 1) return;
         std::vector<Index> s1, s2, sep;
         if (parts) {
             const int bit = L - level;
             for (Index v : s) ((parts[v] >> bit) & 1 ? s2 : s1).push_back(v);
         } else if (!s.empty()) {
-            for (Index v : s) in[v] = 1;
+            for (Index v : s) mark[v] = id;
             if (X)
                 split_geo(s, s1, s2);
             else
-                split_bfs(s, s1, s2);
+                split_bfs(s, s1, s2, id);
         }
         if (!s.empty()) {
-            for (Index v : s) in[v] = 1;
-            carve(s1, s2, sep);
-            for (Index v : s) in[v] = 0;
+            for (Index v : s) mark[v] = id;
+            carve(s1, s2, sep, id);
         }
-        t.nodes[id].separator = sep;
+        nd.separator = sep;
         std::vector<Index>().swap(s);
-        const int a = grow(std::move(s1), level + 1, id);
-        const int b = grow(std::move(s2), level + 1, id);
-        t.nodes[id].child[0] = a;
-        t.nodes[id].child[1] = b;
-        return id;
+        const int a = id + 1, b = id + 1 + subtree_size(level + 1);
+        nd.child[0] = a;
+        nd.child[1] = b;
+        if (level <= 6) {  // the top levels fan out as tasks; deeper subtrees run in their task
+#pragma omp task default(shared) firstprivate(a, level, id) shared(s1)
+            grow(std::move(s1), level + 1, id, a);
+#pragma omp task default(shared) firstprivate(b, level, id) shared(s2)
+            grow(std::move(s2), level + 1, id, b);
+#pragma omp taskwait
+        } else {
+            grow(std::move(s1), level + 1, id, a);
+            grow(std::move(s2), level + 1, id, b);
+        }
     }
 };
 
@@ -280,7 +303,11 @@ SeparatorTree nested_dissection(const Graph& g, int L, const double* coords, int
     std::vector<Index> all(g.n);
     std::iota(all.begin(), all.end(), 0);
     b.t.num_levels = L;
-    b.t.root = b.grow(std::move(all), 1, -1);
+    b.t.nodes.resize(static_cast<size_t>(b.subtree_size(1)));
+    b.t.root = 0;
+#pragma omp parallel
+#pragma omp single
+    b.grow(std::move(all), 1, -1, 0);
     return std::move(b.t);
 }
 
@@ -292,7 +319,11 @@ SeparatorTree import_partition(const Graph& g, int L, const int* parts) {
     std::vector<Index> all(g.n);
     std::iota(all.begin(), all.end(), 0);
     b.t.num_levels = L;
-    b.t.root = b.grow(std::move(all), 1, -1);
+    b.t.nodes.resize(static_cast<size_t>(b.subtree_size(1)));
+    b.t.root = 0;
+#pragma omp parallel
+#pragma omp single
+    b.grow(std::move(all), 1, -1, 0);
     return std::move(b.t);
 }
 
