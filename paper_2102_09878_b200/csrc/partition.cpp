@@ -364,12 +364,19 @@ ClusterHierarchy build_interfaces(const SeparatorTree& t, const Graph& g) {
     std::stable_sort(seps.begin(), seps.end(), [&](int a, int b) {
         return t.nodes[a].level != t.nodes[b].level ? t.nodes[a].level > t.nodes[b].level : a < b;
     });
-    std::vector<int> piece_of(g.n, -1), grp(g.n, -1), mark(g.n, 0);
-    std::vector<std::vector<Index>> sigs;
-    for (int sid : seps) {
+    // pieces of every separator at every granularity, computed per separator in
+    // parallel (separators are disjoint vertex sets; mark[] carries the
+    // separator id so concurrent flood fills never see each other's vertices),
+    // then numbered sequentially in the reference's order (partition.cpp:284-339)
+    std::vector<int> grp(g.n, -1), mark(g.n, 0);
+    std::vector<std::vector<std::vector<std::vector<Index>>>> all_pieces(seps.size());
+#pragma omp parallel for schedule(dynamic, 1)
+    for (long long si = 0; si < static_cast<long long>(seps.size()); ++si) {
+        const int sid = seps[si];
         const auto& nd = t.nodes[sid];
         const int l = nd.level;
         const auto& S = nd.separator;
+        const int unvisited = sid + 1, visited = -(sid + 1);
         // per separator vertex: outside neighbours' owner nodes (fixed), climbed per k
         std::vector<Index> optr(S.size() + 1, 0), onode;
         for (size_t a = 0; a < S.size(); ++a) {
@@ -377,59 +384,70 @@ ClusterHierarchy build_interfaces(const SeparatorTree& t, const Graph& g) {
                 if (owner_node[*u] != sid) onode.push_back(owner_node[*u]);
             optr[a + 1] = static_cast<Index>(onode.size());
         }
+        std::vector<std::vector<Index>> sigs;
+        auto& per_k = all_pieces[si];
         for (int k = l; k <= L + 1; ++k) {
-            std::vector<std::vector<Index>> pieces;
+            per_k.emplace_back();
+            std::vector<std::vector<Index>>& pieces = per_k.back();
             if (k == l) {
                 pieces.push_back(S);
-            } else {
-                sigs.assign(S.size(), {});
-                for (size_t a = 0; a < S.size(); ++a) {
-                    auto& sig = sigs[a];
-                    for (Index q = optr[a]; q < optr[a + 1]; ++q) {
-                        int x = onode[q];
-                        while (t.nodes[x].level > k) x = t.nodes[x].parent;
-                        sig.push_back(x);
-                    }
-                    std::sort(sig.begin(), sig.end());
-                    sig.erase(std::unique(sig.begin(), sig.end()), sig.end());
-                }
-                std::vector<Index> ord(S.size());
-                std::iota(ord.begin(), ord.end(), 0);
-                std::sort(ord.begin(), ord.end(), [&](Index a, Index b) { return sigs[a] < sigs[b]; });
-                int gi = -1;
-                for (size_t q = 0; q < ord.size(); ++q) {
-                    if (q == 0 || sigs[ord[q]] != sigs[ord[q - 1]]) ++gi;
-                    grp[S[ord[q]]] = gi;
-                }
-                for (Index v : S) mark[v] = 1;  // 1 = unvisited separator vertex
-                for (Index s0 : S) {              // ascending seeds
-                    if (mark[s0] != 1) continue;
-                    mark[s0] = 2;
-                    std::vector<Index> comp{s0};
-                    for (size_t q = 0; q < comp.size(); ++q) {
-                        const Index v = comp[q];
-                        for (const Index* u = g.begin(v); u != g.end(v); ++u)
-                            if (mark[*u] == 1 && grp[*u] == grp[v]) {
-                                mark[*u] = 2;
-                                comp.push_back(*u);
-                            }
-                    }
-                    std::sort(comp.begin(), comp.end());
-                    pieces.push_back(std::move(comp));
-                }
-                for (Index v : S) mark[v] = 0;
-                std::sort(pieces.begin(), pieces.end(), [](const auto& a, const auto& b) { return a.front() < b.front(); });
+                continue;
             }
+            sigs.assign(S.size(), {});
+            for (size_t a = 0; a < S.size(); ++a) {
+                auto& sig = sigs[a];
+                for (Index q = optr[a]; q < optr[a + 1]; ++q) {
+                    int x = onode[q];
+                    while (t.nodes[x].level > k) x = t.nodes[x].parent;
+                    sig.push_back(x);
+                }
+                std::sort(sig.begin(), sig.end());
+                sig.erase(std::unique(sig.begin(), sig.end()), sig.end());
+            }
+            std::vector<Index> ord(S.size());
+            std::iota(ord.begin(), ord.end(), 0);
+            std::sort(ord.begin(), ord.end(), [&](Index a, Index b) { return sigs[a] < sigs[b]; });
+            int gi = -1;
+            for (size_t q = 0; q < ord.size(); ++q) {
+                if (q == 0 || sigs[ord[q]] != sigs[ord[q - 1]]) ++gi;
+                grp[S[ord[q]]] = gi;
+            }
+            for (Index v : S) mark[v] = unvisited;
+            for (Index s0 : S) {  // ascending seeds
+                if (mark[s0] != unvisited) continue;
+                mark[s0] = visited;
+                std::vector<Index> comp{s0};
+                for (size_t q = 0; q < comp.size(); ++q) {
+                    const Index v = comp[q];
+                    for (const Index* u = g.begin(v); u != g.end(v); ++u)
+                        if (mark[*u] == unvisited && grp[*u] == grp[v]) {
+                            mark[*u] = visited;
+                            comp.push_back(*u);
+                        }
+                }
+                std::sort(comp.begin(), comp.end());
+                pieces.push_back(std::move(comp));
+            }
+            for (Index v : S) mark[v] = 0;
+            std::sort(pieces.begin(), pieces.end(), [](const auto& a, const auto& b) { return a.front() < b.front(); });
+        }
+    }
+    std::vector<int> piece_of(g.n, -1);
+    for (size_t si = 0; si < seps.size(); ++si) {
+        const int sid = seps[si];
+        const int l = t.nodes[sid].level;
+        for (size_t kk = 0; kk < all_pieces[si].size(); ++kk) {
+            const int k = l + static_cast<int>(kk);
             std::vector<std::pair<Index, int>> next;
-            for (auto& pc : pieces) {
+            for (auto& pc : all_pieces[si][kk]) {
                 ClusterHierarchy::Cluster c;
                 const int cid = static_cast<int>(h.clusters.size());
                 c.tree_node = sid;
                 c.level = k;
                 c.stage = (k == l) ? l : 0;
                 c.parent = (k == l) ? -1 : piece_of[pc.front()];
-                c.cols = pc;
                 for (Index v : pc) next.emplace_back(v, cid);
+                c.cols = std::move(pc);
                 h.clusters.push_back(std::move(c));
             }
             for (auto& [v, cid] : next) piece_of[v] = cid;
