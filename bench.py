@@ -73,29 +73,63 @@ def allmax(ws, v):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in-process through
+    NVML (a cheap query every 0.25 s; spawning nvidia-smi would steal host cores from the
+    host-bound engine); falls back to nvidia-smi when NVML is unavailable."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons set)
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_reader(self):
+        import pynvml as N
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.device)
+        bits = {"hw_slowdown": N.nvmlClocksThrottleReasonHwSlowdown,
+                "hw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": N.nvmlClocksThrottleReasonSwPowerCap}
+
+        def read():
+            sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            return float(sm), float(mx), {k for k, v in bits.items() if r & v}
+        return read
+
+    def _smi_reader(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+        def read():
+            out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=5).stdout.strip()
+            s = [x.strip() for x in out.split(",")]
+            return float(s[0]), float(s[1]), {self.NAMES[i] for i in range(4)
+                                              if len(s) > 2 + i and "Active" in s[2 + i] and "Not" not in s[2 + i]}
+        return read
+
     def start(self):
+        try:
+            read = self._nvml_reader()
+            read()
+            self.source = "nvml"
+        except Exception:
+            read = self._smi_reader()
+            self.source = "nvidia-smi"
+
         def run():
-            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
+                    self.samples.append(read())
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.25)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -103,13 +137,11 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and "Active" in s[3 + i]
-                          and "Not" not in s[3 + i]})
+        sm = [s[0] for s in self.samples]
+        mx = [s[1] for s in self.samples]
+        reasons = sorted(set().union(*[s[2] for s in self.samples])) if self.samples else []
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples), "source": getattr(self, "source", None)}
 
 
 def load_peaks():
@@ -248,6 +280,7 @@ def run_ours(args, ws, rank, local):
         last = (g, rep)
     barrier(ws)
     ck = clocks.stop()
+    step_values = [round(v, 4) for v in dev_t]
     value = allmax(ws, sum(dev_t) / len(dev_t))
     e2e = allmax(ws, sum(e2e_t) / len(e2e_t))
     g, rep = last
@@ -281,6 +314,7 @@ def run_ours(args, ws, rank, local):
                                   "TFLOP/s": round(qr_tflops, 4), "launches": q["launches"],
                                   "device_ms": round(q["ms"], 3)},
                      "kernel_ms": {k: round(v["ms"], 3) for k, v in ks.items()}},
+        "step_values": step_values,
         "gpu_launches": launches,
         "clocks": ck,
         "solve": {"iterations": rep["iterations"], "converged": rep["converged"],
