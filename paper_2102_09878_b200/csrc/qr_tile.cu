@@ -170,6 +170,161 @@ __device__ void panel_regs(double* P, int m, int n, int kmax, double* s_tau) {
     __syncthreads();
 }
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// shared memory of the DMMA tile phase (doubles): X tile (MP x 32, ld MP+4; the
+// staged panel aliases it), explicit V (MP x 32, ld MP+4), T and W (32 x 32, ld 36)
+__host__ __device__ constexpr int dmma_tile_doubles(int MP) { return 2 * (MP + 4) * 32 + 2 * 36 * 32; }
+
+// Tile phase on FP64 tensor cores (n <= 32, MP <= 256): the panel's reflectors in
+// compact-WY form, H = I - V T V^T (T by accumulate_wy, dense_kernels.cpp:41-53),
+// applied to 32-column tiles as three DMMA m8n8k4 products: W = V^T X,
+// W = T^T W, X -= V W (apply_raw's blocked branch, dense_kernels.cpp:61-69).
+// Leading dimensions are = 4 (mod 16) doubles so every fragment load is two
+// conflict-free wavefronts.
+template <int MP>
+__device__ void tile_dmma(const QrDesc& d, const int4& wk, double* sm, int kmax, const double* s_tau,
+                          const unsigned char* s_neg) {
+    constexpr int LV = MP + 4, LT = 36;
+    const double* P = sm;  // factored panel (ld MP), consumed before sX is written
+    double* sX = sm;
+    double* sV = sm + LV * 32;
+    double* sT = sV + LV * 32;
+    double* sW = sT + LT * 32;
+    const int m = d.m;
+    const long long ld = d.ld;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+    for (int e = threadIdx.x; e < MP * 32; e += blockDim.x) {
+        const int j = e / MP, r = e - j * MP;
+        double v = 0.0;
+        if (j < kmax) v = r < j ? 0.0 : (r == j ? 1.0 : P[r + j * MP]);
+        sV[r + j * LV] = v;
+    }
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) sT[(e & 31) + (e >> 5) * LT] = 0.0;
+    __syncthreads();
+    // Gram matrix V^T V (strict upper part) into sW, then T column by column
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+        const int i = e & 31, j = e >> 5;
+        double s = 0.0;
+        if (i < j && j < kmax) {
+            const double* vi = sV + i * LV;
+            const double* vj = sV + j * LV;
+            double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int r = j;  // v_j is zero above row j
+            for (; r + 3 < MP; r += 4) {
+                s = fma(vi[r], vj[r], s);
+                s1 = fma(vi[r + 1], vj[r + 1], s1);
+                s2 = fma(vi[r + 2], vj[r + 2], s2);
+                s3 = fma(vi[r + 3], vj[r + 3], s3);
+            }
+            for (; r < MP; ++r) s = fma(vi[r], vj[r], s);
+            s = (s + s1) + (s2 + s3);
+        }
+        sW[i + j * LT] = s;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        for (int j = 0; j < kmax; ++j) {
+            const double tj = s_tau[j];
+            if (tj == 0.0) continue;
+            double s = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            if (lane < j) {
+                int q = lane;
+                for (; q + 3 < j; q += 4) {
+                    s = fma(sT[lane + q * LT], sW[q + j * LT], s);
+                    s1 = fma(sT[lane + (q + 1) * LT], sW[q + 1 + j * LT], s1);
+                    s2 = fma(sT[lane + (q + 2) * LT], sW[q + 2 + j * LT], s2);
+                    s3 = fma(sT[lane + (q + 3) * LT], sW[q + 3 + j * LT], s3);
+                }
+                for (; q < j; ++q) s = fma(sT[lane + q * LT], sW[q + j * LT], s);
+                s = (s + s1) + (s2 + s3);
+            }
+            __syncwarp();
+            if (lane < j) sT[lane + j * LT] = -tj * s;
+            if (lane == 0) sT[j + j * LT] = tj;
+            __syncwarp();
+        }
+    }
+    const int mt = wid & 3, nt = (wid >> 2) * 2;
+    for (int c0 = wk.y; c0 < wk.z; c0 += 32) {
+        const int nc = min(32, wk.z - c0);
+        __syncthreads();  // T ready / previous tile stored
+        {  // all loads of the tile in flight at once
+            constexpr int NL = MP * 32 / (32 * kNW);
+            double xv[NL];
+#pragma unroll
+            for (int u = 0; u < NL; ++u) {
+                const int e = threadIdx.x + u * 32 * kNW;
+                const int c = e / MP, r = e - c * MP;
+                xv[u] = (r < m && c < nc) ? d.a[r + static_cast<long long>(c0 + c) * ld] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < NL; ++u) {
+                const int e = threadIdx.x + u * 32 * kNW;
+                const int c = e / MP, r = e - c * MP;
+                sX[r + c * LV] = xv[u];
+            }
+        }
+        __syncthreads();
+        // W = V^T X  (32 x 32): warp -> W rows 8 mt.., columns 8 nt.. (two tiles)
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll 8
+        for (int k0 = 0; k0 < MP; k0 += 4) {
+            const double a = sV[(k0 + t4) + (8 * mt + g) * LV];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) dmma884(acc[q][0], acc[q][1], a, sX[(k0 + t4) + (8 * (nt + q) + g) * LV]);
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            sW[(8 * mt + g) + (8 * (nt + q) + 2 * t4) * LT] = acc[q][0];
+            sW[(8 * mt + g) + (8 * (nt + q) + 2 * t4 + 1) * LT] = acc[q][1];
+        }
+        __syncthreads();
+        // W = T^T W
+        double acc2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+            const double a = sT[(k0 + t4) + (8 * mt + g) * LT];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) dmma884(acc2[q][0], acc2[q][1], a, sW[(k0 + t4) + (8 * (nt + q) + g) * LT]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            sW[(8 * mt + g) + (8 * (nt + q) + 2 * t4) * LT] = acc2[q][0];
+            sW[(8 * mt + g) + (8 * (nt + q) + 2 * t4 + 1) * LT] = acc2[q][1];
+        }
+        __syncthreads();
+        // X -= V W: warp -> row tiles wid, wid + 8, ..., all four column tiles
+        for (int m8 = wid; m8 < MP / 8; m8 += 8) {
+            double o[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int k0 = 0; k0 < 32; k0 += 4) {
+                const double a = sV[(8 * m8 + g) + (k0 + t4) * LV];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) dmma884(o[q][0], o[q][1], a, sW[(k0 + t4) + (8 * q + g) * LT]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                sX[(8 * m8 + g) + (8 * q + 2 * t4) * LV] -= o[q][0];
+                sX[(8 * m8 + g) + (8 * q + 2 * t4 + 1) * LV] -= o[q][1];
+            }
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < MP * 32; e += blockDim.x) {
+            const int c = e / MP, r = e - c * MP;
+            if (r < m && c < nc) {
+                const double v = sX[r + c * LV];
+                d.a[r + static_cast<long long>(c0 + c) * ld] = (r < kmax && s_neg[r]) ? -v : v;
+            }
+        }
+    }
+}
+
 // work.x = descriptor, [work.y, work.z) = trailing columns, work.w = tiles of this front.
 // count[desc] (zero on entry, zero again on exit) elects the panel writer: the
 // last CTA of the front to finish staging, so no CTA can still be reading the
@@ -181,7 +336,7 @@ __device__ void panel_regs(double* P, int m, int n, int kmax, double* s_tau) {
 // log2(TPC) shuffles and 16 FMAs for the update, with no block barriers.
 // ~100 registers, so two CTAs share an SM and one's panel factorisation
 // overlaps the other's tile sweep.
-template <int TPC>
+template <int TPC, bool WY>
 __global__ void __launch_bounds__(32 * kNW, 2) k_qr_tile(const QrDesc* __restrict__ ds, const int4* __restrict__ work,
                                                       int* __restrict__ count) {
     constexpr int MP = 16 * TPC;  // padded rows (panel leading dimension)
@@ -266,6 +421,10 @@ __global__ void __launch_bounds__(32 * kNW, 2) k_qr_tile(const QrDesc* __restric
     }
     if (wk.z <= wk.y) return;
     __syncthreads();
+    if (WY && MP <= 256 && n <= 32) {  // compact-WY tile phase on DMMA (SPQR_TILE_DMMA=1)
+        tile_dmma<(MP <= 256 ? MP : 256)>(d, wk, P, kmax, s_tau, s_neg);
+        return;
+    }
     // ---- explicit reflectors: V(:, k) = [0; 1; v], zero rows >= m
     for (int e = threadIdx.x; e < MP * kmax; e += blockDim.x) {
         const int k = e / MP, i = e - k * MP;
@@ -341,11 +500,22 @@ __global__ void __launch_bounds__(32 * kNW, 2) k_qr_tile(const QrDesc* __restric
     }
 }
 
+// The register/FMA tile phase is the default: measured on C5 128x32+256 x 4096 it
+// takes 1.85 ms against 2.16 ms for the DMMA compact-WY variant (32-column
+// passes, five barriers each); SPQR_TILE_DMMA=1 selects the latter.
+bool tile_dmma_enabled() { return std::getenv("SPQR_TILE_DMMA") != nullptr; }
+
 template <int TPC>
 void launch_tile(const QrDesc* dd, const int4* dw, int nwork, size_t smem, int* count, cudaStream_t st) {
-    static size_t configured = 0;
-    smem_optin(reinterpret_cast<const void*>(k_qr_tile<TPC>), smem, configured);
-    k_qr_tile<TPC><<<nwork, 32 * kNW, smem, st>>>(dd, dw, count);
+    if (tile_dmma_enabled()) {
+        static size_t configured = 0;
+        smem_optin(reinterpret_cast<const void*>(k_qr_tile<TPC, true>), smem, configured);
+        k_qr_tile<TPC, true><<<nwork, 32 * kNW, smem, st>>>(dd, dw, count);
+    } else {
+        static size_t configured = 0;
+        smem_optin(reinterpret_cast<const void*>(k_qr_tile<TPC, false>), smem, configured);
+        k_qr_tile<TPC, false><<<nwork, 32 * kNW, smem, st>>>(dd, dw, count);
+    }
 }
 
 }  // namespace
@@ -359,7 +529,11 @@ int qr_tile_class(int m, int n) {
     return cls;
 }
 
-size_t qr_tile_smem(int cls, int n) { return sizeof(double) * (32u << cls) * static_cast<size_t>(n); }
+size_t qr_tile_smem(int cls, int n) {
+    const int MP = 32 << cls;
+    if (tile_dmma_enabled() && MP <= 256 && n <= 32) return sizeof(double) * static_cast<size_t>(dmma_tile_doubles(MP));
+    return sizeof(double) * static_cast<size_t>(MP) * n;
+}
 
 std::vector<int4> qr_tile_plan(const QrDesc* hq, const int* idx, int cnt, int sms) {
     long long trail = 0;

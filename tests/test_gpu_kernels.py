@@ -13,7 +13,7 @@ def _P():
     return P
 
 
-@pytest.mark.parametrize("path", ["auto", "smem", "blocked"])
+@pytest.mark.parametrize("path", ["auto", "smem", "blocked", "tile_dmma"])
 @pytest.mark.parametrize("shape", [(1, 1, 1), (5, 3, 3), (20, 7, 30), (40, 12, 60), (128, 32, 288), (300, 64, 96),
                                    (300, 40, 140), (513, 70, 200), (512, 128, 384),
                                    # column-tiled path: many tiles, panel only, square panel, m > 256
@@ -22,8 +22,11 @@ def _P():
                                    (129, 47, 150)])
 def test_qr_apply_matches_oracle(shape, path, monkeypatch):
     """auto = column-tiled kernel where the panel fits in shared memory (qr_tile.cu);
-    smem = whole block staged per CTA (kernels.cu); blocked = panel + DMMA compact-WY (mbqr.cu)."""
-    if path != "auto":
+    tile_dmma = the same with its DMMA compact-WY tile phase; smem = whole block staged per
+    CTA (kernels.cu); blocked = panel + DMMA compact-WY (mbqr.cu)."""
+    if path == "tile_dmma":
+        monkeypatch.setenv("SPQR_TILE_DMMA", "1")  # compact-WY DMMA tile phase (qr_tile.cu)
+    elif path != "auto":
         monkeypatch.setenv("SPQR_QR_PATH", path)
     m, n, ntot = shape
     rng = np.random.default_rng(m * 131 + n)
