@@ -45,6 +45,11 @@ def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # the engine's host bookkeeping is multi-threaded: replicas on one node split the
+    # host cores instead of oversubscribing them (one core left per replica's driver thread)
+    nloc = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    if nloc > 1 and "OMP_NUM_THREADS" not in os.environ:
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or nloc) // nloc - 1))
     if ws > 1:
         import torch
         import torch.distributed as dist
