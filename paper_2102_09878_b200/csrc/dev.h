@@ -127,7 +127,6 @@ void launch_assemble(const AsmDst* d_dst, int ndst, long long total_elems, const
                      const int* d_kmap, const AsmSrc* d_src, cudaStream_t st);
 void launch_stats(const StatDesc* d, int nd, long long total_work, double* out_sq, unsigned char* out_nz,
                   cudaStream_t st);
-void launch_qr(const QrDesc* d, int nd, int max_m, cudaStream_t st);
 // Size-split launches: problems listed in d_small are staged in shared memory
 // (smem_small = the largest staged footprint), the rest run in place in HBM.
 constexpr size_t kSmemBudget = 100 * 1024;  // two CTAs per SM

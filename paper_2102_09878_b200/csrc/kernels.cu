@@ -279,15 +279,6 @@ __device__ void qr_epilogue(const QrDesc& d, double* A, int ld, const double* s_
 
 constexpr int kQrMaxN = 1024;
 
-// in place in HBM (large fronts)
-__global__ void __launch_bounds__(256) k_qr(const QrDesc* __restrict__ ds) {
-    const QrDesc d = ds[blockIdx.x];
-    __shared__ double red[32];
-    __shared__ double s_sc[2];
-    __shared__ double s_neg[kQrMaxN];
-    qr_body(d.a, d.ld, d.m, d.n, d.ntot, d.tau, s_neg, red, s_sc);
-    qr_epilogue(d, d.a, d.ld, s_neg);
-}
 
 __global__ void __launch_bounds__(256) k_qr_idx(const QrDesc* __restrict__ ds, const int* __restrict__ idx) {
     const QrDesc d = ds[idx[blockIdx.x]];
@@ -655,10 +646,6 @@ void launch_stats(const StatDesc* d, int nd, long long total, double* out_sq, un
     k_stats<<<static_cast<unsigned>((total + bs - 1) / bs), bs, 0, st>>>(d, nd, total, out_sq, out_nz);
 }
 
-void launch_qr(const QrDesc* d, int nd, int /*max_m*/, cudaStream_t st) {  // all in place in HBM
-    if (nd <= 0) return;
-    k_qr<<<nd, 256, 0, st>>>(d);
-}
 
 void launch_qr_split(const QrDesc* d_desc, const int* d_small, int n_small, size_t smem_small, const int* d_large,
                      int n_large, cudaStream_t st) {

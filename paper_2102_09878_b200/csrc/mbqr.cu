@@ -41,140 +41,6 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-// Panel factorisation: columns [j0, j0+w) of problem b, rows [j0, m).
-// Lane j of every warp owns panel column j; the NWP warps split the rows.  The
-// panel lives in shared memory (ld = rows + 1, conflict-free column walks) when
-// it fits, else in place in HBM.  Writes V below the diagonal, beta on it,
-// tau, and the compact-WY factor T (w x w, accumulate_wy order).
-template <int NWP>
-__global__ void __launch_bounds__(32 * NWP) k_panel(double* __restrict__ a, int ld, long long stride, int m, int j0,
-                                                    int w, double* __restrict__ tau_all, int tau_stride,
-                                                    double* __restrict__ T_all, int smem_rows) {
-    const int b = blockIdx.x;
-    double* A = a + b * stride;
-    double* tau = tau_all + static_cast<long long>(b) * tau_stride;
-    double* T = T_all + static_cast<long long>(b) * NB * NB;
-    extern __shared__ double sm[];
-    __shared__ double part[NWP][NB + 1];
-    __shared__ double G[NB * NB];
-    __shared__ double s_tau, s_den;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int rows = m - j0;
-    const bool staged = rows <= smem_rows;
-    double* P;
-    int pld;
-    if (staged) {
-        P = sm;
-        pld = rows + 1;
-        for (int e = threadIdx.x; e < rows * w; e += blockDim.x) {
-            const int i = e % rows, j = e / rows;
-            P[i + j * pld] = A[(j0 + i) + static_cast<long long>(j0 + j) * ld];
-        }
-        __syncthreads();
-    } else {
-        P = A + j0 + static_cast<long long>(j0) * ld;
-        pld = ld;
-    }
-    // row range of this warp
-    const int per = (rows + NWP - 1) / NWP;
-    const int r_lo = wid * per, r_hi = min(rows, r_lo + per);
-    double* pj = P + static_cast<long long>(lane) * pld;  // this lane's column
-    for (int k = 0; k < w; ++k) {
-        const double* pk = P + static_cast<long long>(k) * pld;
-        // tail norm^2 of column k over rows > k: lane-strided within the warp's range
-        double s = 0.0;
-        for (int i = max(r_lo, k + 1) + lane; i < r_hi; i += 32) s = fma(pk[i], pk[i], s);
-        s = wsum(s);
-        if (NWP > 1) {
-            if (lane == 0) part[wid][0] = s;
-            __syncthreads();
-            s = 0.0;
-            for (int q = 0; q < NWP; ++q) s += part[q][0];
-        }
-        if (threadIdx.x == 0) {
-            const double c0 = pk[k];
-            double t = 0.0, den = 0.0;
-            if (!(s <= DBL_MIN)) {
-                double beta = sqrt(c0 * c0 + s);
-                if (c0 >= 0.0) beta = -beta;
-                den = c0 - beta;
-                t = (beta - c0) / beta;
-                P[k + static_cast<long long>(k) * pld] = beta;
-            }
-            s_tau = t;
-            s_den = den;
-            tau[j0 + k] = t;
-        }
-        __syncthreads();
-        const double t = s_tau, den = s_den;
-        double* pkw = P + static_cast<long long>(k) * pld;
-        for (int i = max(r_lo, k + 1) + lane; i < r_hi; i += 32) pkw[i] = (t == 0.0) ? 0.0 : pkw[i] / den;
-        __syncthreads();
-        if (t != 0.0) {
-            // dots of v_k with every later column (lane = column), rows of this warp
-            double d = 0.0;
-            const double pjk = (lane > k && lane < w) ? pj[k] : 0.0;  // read before anyone updates row k
-            if (lane > k && lane < w)
-                for (int i = max(r_lo, k + 1); i < r_hi; ++i) d = fma(pkw[i], pj[i], d);
-            if (NWP > 1) {
-                part[wid][lane] = d;
-                __syncthreads();
-                d = 0.0;
-                for (int q = 0; q < NWP; ++q) d += part[q][lane];
-            }
-            if (lane > k && lane < w) {
-                const double tw = t * (d + pjk);
-                if (r_lo <= k && k < r_hi) pj[k] -= tw;
-                for (int i = max(r_lo, k + 1); i < r_hi; ++i) pj[i] = fma(-tw, pkw[i], pj[i]);
-            }
-        }
-        __syncthreads();
-    }
-    // Gram matrix of the unit-lower V (dense_kernels.cpp:41-53 needs V^T v_j): lane = column j
-    for (int i = 0; i < w; ++i) {
-        double g = 0.0;
-        if (lane > i && lane < w)
-            for (int r = max(r_lo, lane); r < r_hi; ++r) {
-                const double vi = P[r + static_cast<long long>(i) * pld];  // r >= lane > i
-                const double vj = (r == lane) ? 1.0 : pj[r];
-                g = fma(vi, vj, g);
-            }
-        if (NWP > 1) {
-            part[wid][lane] = g;
-            __syncthreads();
-            if (wid == 0) {
-                g = 0.0;
-                for (int q = 0; q < NWP; ++q) g += part[q][lane];
-            }
-            __syncthreads();
-        }
-        if (wid == 0 && lane > i && lane < w) G[i + lane * NB] = g;
-    }
-    __syncthreads();
-    if (wid == 0) {  // T column by column (upper triangular); lane i computes T(i, j)
-        for (int e = lane; e < NB * NB; e += 32) T[e] = 0.0;
-        __syncwarp();
-        for (int j = 0; j < w; ++j) {
-            const double tj = tau[j0 + j];
-            if (tj == 0.0) continue;
-            double s = 0.0;
-            if (lane < j)
-                for (int q = lane; q < j; ++q) s = fma(T[lane + q * NB], G[q + j * NB], s);
-            __syncwarp();
-            if (lane < j) T[lane + j * NB] = -tj * s;
-            if (lane == 0) T[j + j * NB] = tj;
-            __syncwarp();
-        }
-    }
-    if (staged) {
-        __syncthreads();
-        for (int e = threadIdx.x; e < rows * w; e += blockDim.x) {
-            const int i = e % rows, j = e / rows;
-            A[(j0 + i) + static_cast<long long>(j0 + j) * ld] = P[i + j * pld];
-        }
-    }
-}
-
 // Panel factorisation, row-group layout: warp g owns a contiguous chunk of
 // rows of the w <= 32 panel columns; within a warp, lanes stride the rows
 // (coalesced in HBM or shared memory alike).  Per reflector: warps reduce the
