@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kNW = kThreads / 32;
-constexpr size_t kNarrowSmem = 216 * 1024;  // dynamic smem cap (227 KB minus the static arrays)
+constexpr size_t kNarrowSmem = 216 * 1024;  // dynamic smem cap (227 KB minus up to 9 KB of static arrays)
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -60,10 +60,22 @@ __global__ void __launch_bounds__(kThreads) k_cpqr_narrow(const CpqrDesc* __rest
         }
         return;
     }
-    if (!GLB) {
-        for (int e = tid; e < m * n; e += kThreads) {
-            const int j = e / m, i = e - j * m;
-            A[i + j * ldm] = d.a[i + static_cast<long long>(j) * d.ld];
+    if (!GLB) {  // stage the block, eight loads in flight per thread
+        const int tot = m * n;
+        for (int e0 = tid; e0 < tot; e0 += 8 * kThreads) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * kThreads;
+                const int j = e / m, i = e - j * m;
+                v[u] = e < tot ? d.a[i + static_cast<long long>(j) * d.ld] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * kThreads;
+                const int j = e / m, i = e - j * m;
+                if (e < tot) A[i + j * ldm] = v[u];
+            }
         }
         __syncthreads();
     }
@@ -154,7 +166,9 @@ __global__ void __launch_bounds__(kThreads) k_cpqr_narrow(const CpqrDesc* __rest
         int piv, pc;
         argmax(k, bv, piv, pc);
         finalise();
-        double exact = sqrt(tail_sumsq(pc, k));
+        double x0 = A[k + pc * ldm];
+        double tail = tail_sumsq(pc, k + 1);
+        double exact = sqrt(fma(x0, x0, tail));
         bool stop = (k == 0) ? !(exact > 0.0) : (d.eps > 0.0 && exact < d.eps * r11);
         if (stop && k > 0) {  // refresh every trailing norm and retry once
 #pragma unroll
@@ -168,11 +182,13 @@ __global__ void __launch_bounds__(kThreads) k_cpqr_narrow(const CpqrDesc* __rest
             argmax(k, bv, piv, pc);
             exact = bv;
             stop = d.eps > 0.0 && exact < d.eps * r11;
+            if (!stop) {
+                x0 = A[k + pc * ldm];
+                tail = tail_sumsq(pc, k + 1);
+            }
         }
         if (stop) break;
         // Householder on rows [k, m) of the pivot column (every warp, lane = row)
-        const double x0 = A[k + pc * ldm];
-        const double tail = tail_sumsq(pc, k + 1);
         double alpha = sqrt(fma(x0, x0, tail));
         if (x0 > 0.0) alpha = -alpha;
         const double v0 = x0 - alpha;
