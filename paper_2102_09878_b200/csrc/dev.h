@@ -154,6 +154,9 @@ struct WFac {
 };
 // mode 0 w_solve, 1 wt_solve (writes C^T zs contributions), 2 w_apply, 3 wt_apply (contributions)
 void launch_wsweep(const WFac* f, int nf, double* z, double* contrib, int mode, int maxc, cudaStream_t st);
+// factors with c >= kBigFactorCols: one CTA each (k_wsweep_big)
+constexpr int kBigFactorCols = 192;
+void launch_wsweep_big(const WFac* f, int nf, double* z, double* contrib, int mode, int maxc, cudaStream_t st);
 // z[col[t]] (+/-)= contrib[idx[ptr[t]..ptr[t+1])] in order
 void launch_wreduce(const int* ptr, const int* idx, const int* col, int ncol, const double* contrib, double* z,
                     double sgn, cudaStream_t st);

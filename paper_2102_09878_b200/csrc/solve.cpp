@@ -1,6 +1,8 @@
 // W sweep plan + device CGLS / CSNE drivers.
 #include "solve.h"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -20,14 +22,16 @@ SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
     for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;
     std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return F.W[a].batch < F.W[b].batch; });
     long long maxcontrib = 1;
+    // factors at least this wide run one per CTA (SPQR_BIG_FACTOR overrides, for tests)
+    const int big_cols = std::getenv("SPQR_BIG_FACTOR") ? std::atoi(std::getenv("SPQR_BIG_FACTOR")) : kBigFactorCols;
     size_t i = 0;
     while (i < ord.size()) {
         size_t j = i;
         while (j < ord.size() && F.W[ord[j]].batch == F.W[ord[i]].batch) ++j;
-        std::vector<WFac> fac;
+        std::vector<WFac> fac, bfac;
         long long contrib = 0;
         std::map<int, std::vector<int>> lists;  // coupled column -> contribution indices (chronological)
-        int maxc = 1;
+        int maxc = 1, bmaxc = 1;
         for (size_t q = i; q < j; ++q) {
             const DevWFactor& w = F.W[ord[q]];
             WFac f{};
@@ -44,13 +48,24 @@ SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
                 for (int t = 0; t < w.k; ++t) lists[F.idx[w.coupled_off + t]].push_back(static_cast<int>(contrib + t));
                 contrib += w.k;
             }
-            maxc = std::max(maxc, w.c);
-            fac.push_back(f);
+            // triangular factors: the warp path's back substitution is c sequential
+            // steps of c/32 work; rotations: the CTA path pays two block barriers per
+            // reflector, so only very tall ones move
+            if (w.kind == 0 ? w.c >= big_cols : w.c >= 8 * big_cols) {
+                bmaxc = std::max(bmaxc, w.c);
+                bfac.push_back(f);
+            } else {
+                maxc = std::max(maxc, w.c);
+                fac.push_back(f);
+            }
         }
         SolvePlan::Batch b;
         b.fac = up.put(fac);
         b.nf = static_cast<int>(fac.size());
         b.maxc = maxc;
+        b.bfac = up.put(bfac);
+        b.nbf = static_cast<int>(bfac.size());
+        b.bmaxc = bmaxc;
         if (!lists.empty()) {
             std::vector<int> ptr{0}, idx, col;
             for (auto& [c, l] : lists) {
@@ -69,8 +84,9 @@ SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
     }
     P.contrib = P.mem->alloc_n<double>(maxcontrib);
     for (const auto& b : P.batches) {
-        P.launches_per_sweep += 1;
-        P.launches_per_sweep_t += 1 + (b.ncol > 0 ? 1 : 0);
+        const int k = (b.nf > 0 ? 1 : 0) + (b.nbf > 0 ? 1 : 0);
+        P.launches_per_sweep += k;
+        P.launches_per_sweep_t += k + (b.ncol > 0 ? 1 : 0);
     }
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
@@ -83,8 +99,14 @@ long long sweep(const SolvePlan& P, SweepMode mode, double* d_z, cudaStream_t st
     const bool forward = (mode == kWtSolve || mode == kWApply);  // chronological order
     for (int q = 0; q < nb; ++q) {
         const auto& b = P.batches[forward ? q : nb - 1 - q];
-        launch_wsweep(b.fac, b.nf, d_z, P.contrib, static_cast<int>(mode), b.maxc, st);
-        ++L;
+        if (b.nf > 0) {
+            launch_wsweep(b.fac, b.nf, d_z, P.contrib, static_cast<int>(mode), b.maxc, st);
+            ++L;
+        }
+        if (b.nbf > 0) {  // same batch: the factors commute, the order of the two launches is free
+            launch_wsweep_big(b.bfac, b.nbf, d_z, P.contrib, static_cast<int>(mode), b.bmaxc, st);
+            ++L;
+        }
         if ((mode == kWtSolve || mode == kWtApply) && b.ncol > 0) {
             launch_wreduce(b.rptr, b.ridx, b.rcol, b.ncol, P.contrib, d_z, mode == kWtSolve ? -1.0 : 1.0, st);
             ++L;

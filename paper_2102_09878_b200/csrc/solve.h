@@ -15,8 +15,10 @@ namespace spqr {
 // Level schedule of W: one batch per engine phase, chronological.
 struct SolvePlan {
     struct Batch {
-        const WFac* fac = nullptr;
+        const WFac* fac = nullptr;  // warp per factor
         int nf = 0, maxc = 0;
+        const WFac* bfac = nullptr;  // CTA per factor (c >= kBigFactorCols)
+        int nbf = 0, bmaxc = 0;
         const int *rptr = nullptr, *ridx = nullptr, *rcol = nullptr;  // wt reduce lists
         int ncol = 0;
     };

@@ -119,6 +119,150 @@ __global__ void k_wsweep(const WFac* __restrict__ fs, int nf, double* __restrict
     for (int i = lane; i < c; i += 32) z[f.cols[i]] = x[i];
 }
 
+// One large factor per CTA (the top-level separators of the 3D and kNN
+// problems have factors thousands of columns wide; a warp per factor would
+// serialise them).  Same semantics as k_wsweep (transforms.cpp:40-111), work
+// spread over the CTA: products are thread-per-row GEMVs over the column-major
+// blocks (coalesced), triangular solves are blocked by 32 (one warp solves the
+// diagonal block, the CTA updates the rest), reflector dot products are block
+// reductions.
+constexpr int kBigThreads = 512;
+constexpr int kBigWarps = kBigThreads / 32;
+
+__device__ __forceinline__ double block_reduce(double v, double* red) {
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[wl] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kBigWarps; ++w) t += red[w];
+    return t;
+}
+
+__global__ void __launch_bounds__(kBigThreads) k_wsweep_big(const WFac* __restrict__ fs, double* __restrict__ z,
+                                                          double* __restrict__ contrib, int mode) {
+    extern __shared__ double x[];
+    __shared__ double red[kBigWarps];
+    const WFac f = fs[blockIdx.x];
+    const int c = f.c, tid = threadIdx.x, lane = tid & 31, wl = tid >> 5;
+    for (int i = tid; i < c; i += kBigThreads) x[i] = z[f.cols[i]];
+    __syncthreads();
+    if (f.kind == 0) {
+        const double* R = f.a;
+        const double* C = f.a + static_cast<long long>(c) * c;
+        // C^T x -> contributions, warp per coupled column (modes 1 and 3)
+        auto ctx = [&]() {
+            for (int j = wl; j < f.k; j += kBigWarps) {
+                const double* cj = C + static_cast<long long>(j) * c;
+                double s = 0.0;
+                for (int i = lane; i < c; i += 32) s = fma(cj[i], x[i], s);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                if (lane == 0) contrib[f.contrib_off + j] = s;
+            }
+        };
+        if (mode == 0) {  // zs = z[cols] - C z[coupled]; zs = R^{-1} zs
+            if (f.k > 0) {
+                for (int i = tid; i < c; i += kBigThreads) {
+                    double s = 0.0;
+                    for (int j = 0; j < f.k; ++j) s = fma(C[i + static_cast<long long>(j) * c], z[f.coupled[j]], s);
+                    x[i] -= s;
+                }
+                __syncthreads();
+            }
+            for (int i1 = c; i1 > 0; i1 -= 32) {  // backward, 32-row blocks
+                const int i0 = max(0, i1 - 32);
+                if (wl == 0) {
+                    for (int i = i1 - 1; i >= i0; --i) {
+                        const double xi = x[i] / R[i + static_cast<long long>(i) * c];
+                        __syncwarp();
+                        const int l = i0 + lane;
+                        if (l < i) x[l] = fma(-R[l + static_cast<long long>(i) * c], xi, x[l]);
+                        if (lane == 0) x[i] = xi;
+                        __syncwarp();
+                    }
+                }
+                __syncthreads();
+                for (int r = tid; r < i0; r += kBigThreads) {
+                    double s = 0.0;
+                    for (int i = i0; i < i1; ++i) s = fma(R[r + static_cast<long long>(i) * c], x[i], s);
+                    x[r] -= s;
+                }
+                __syncthreads();
+            }
+        } else if (mode == 1) {  // zs = R^{-T} z[cols]; contributions C^T zs
+            for (int i0 = 0; i0 < c; i0 += 32) {  // forward, 32-row blocks
+                const int i1 = min(c, i0 + 32);
+                if (wl == 0) {
+                    for (int i = i0; i < i1; ++i) {
+                        const double xi = x[i] / R[i + static_cast<long long>(i) * c];
+                        __syncwarp();
+                        const int l = i0 + lane;
+                        if (l > i && l < i1) x[l] = fma(-R[i + static_cast<long long>(l) * c], xi, x[l]);
+                        if (lane == 0) x[i] = xi;
+                        __syncwarp();
+                    }
+                }
+                __syncthreads();
+                for (int r = i1 + tid; r < c; r += kBigThreads) {
+                    const double* rr = R + static_cast<long long>(r) * c;  // column r: R(i0:i1, r) contiguous
+                    double s = 0.0;
+                    for (int i = i0; i < i1; ++i) s = fma(rr[i], x[i], s);
+                    x[r] -= s;
+                }
+                __syncthreads();
+            }
+            ctx();
+        } else if (mode == 2) {  // out = R zs + C z[coupled]
+            for (int i = tid; i < c; i += kBigThreads) {
+                double s = 0.0;
+                for (int j = i; j < c; ++j) s = fma(R[i + static_cast<long long>(j) * c], x[j], s);
+                double t = 0.0;
+                for (int j = 0; j < f.k; ++j) t = fma(C[i + static_cast<long long>(j) * c], z[f.coupled[j]], t);
+                z[f.cols[i]] = s + t;
+            }
+            return;
+        } else {  // mode 3: contributions C^T zs, out = R^T zs
+            ctx();
+            for (int i = tid; i < c; i += kBigThreads) {
+                const double* ri = R + static_cast<long long>(i) * c;
+                double s = 0.0;
+                for (int j = 0; j <= i; ++j) s = fma(ri[j], x[j], s);
+                z[f.cols[i]] = s;
+            }
+            return;
+        }
+    } else {
+        const double* V = f.a;
+        const bool transpose = (mode == 1 || mode == 2);
+        auto reflect = [&](int j) {
+            const double tj = f.tau[j];
+            if (tj == 0.0) return;
+            const double* v = V + static_cast<long long>(j) * c;
+            double w = 0.0;
+            for (int i = j + tid; i < c; i += kBigThreads) w = fma(x[i], v[i], w);
+            const double tw = tj * block_reduce(w, red);
+            for (int i = j + tid; i < c; i += kBigThreads) x[i] = fma(-tw, v[i], x[i]);
+            __syncthreads();
+        };
+        if (transpose) {
+            for (int j = 0; j < f.k; ++j) reflect(j);
+            for (int i = tid; i < f.k; i += kBigThreads)
+                if (f.sign[i] < 0.0) x[i] = -x[i];
+        } else {
+            for (int i = tid; i < f.k; i += kBigThreads)
+                if (f.sign[i] < 0.0) x[i] = -x[i];
+            __syncthreads();
+            for (int j = f.k - 1; j >= 0; --j) reflect(j);
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < c; i += kBigThreads) z[f.cols[i]] = x[i];
+}
+
 __global__ void k_wreduce(const int* __restrict__ ptr, const int* __restrict__ idx, const int* __restrict__ col, int ncol,
                           const double* __restrict__ contrib, double* __restrict__ z, double sgn) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -217,6 +361,14 @@ static void wsweep(const WFac* f, int nf, double* z, double* contrib, int mode, 
 
 void launch_wsweep(const WFac* f, int nf, double* z, double* contrib, int mode, int maxc, cudaStream_t st) {
     wsweep(f, nf, z, contrib, mode, maxc, st);
+}
+
+void launch_wsweep_big(const WFac* f, int nf, double* z, double* contrib, int mode, int maxc, cudaStream_t st) {
+    if (nf <= 0) return;
+    const size_t smem = sizeof(double) * static_cast<size_t>(maxc > 0 ? maxc : 1);
+    static size_t cfg = 0;
+    smem_optin(reinterpret_cast<const void*>(k_wsweep_big), smem, cfg);
+    k_wsweep_big<<<nf, kBigThreads, smem, st>>>(f, z, contrib, mode);
 }
 
 void launch_wreduce(const int* ptr, const int* idx, const int* col, int ncol, const double* contrib, double* z, double sgn,

@@ -70,8 +70,13 @@ def test_w_factors_match_oracle():
             assert np.array_equal(a[4], b[4])
 
 
+@pytest.mark.parametrize("big", [False, True])
 @pytest.mark.parametrize("eps", [0.0, 1e-2])
-def test_sweeps_match_oracle_and_round_trip(eps):
+def test_sweeps_match_oracle_and_round_trip(eps, big, monkeypatch):
+    """big=True routes every factor through the CTA-per-factor sweep kernel (k_wsweep_big),
+    which the solve plan otherwise uses only for factors >= 192 columns wide."""
+    if big:
+        monkeypatch.setenv("SPQR_BIG_FACTOR", "1")
     p = tall_grid(16, seed=7)
     o, g = _pair(p.A, eps=eps, levels=4, skip_levels=1, coords=p.coords)
     rng = np.random.default_rng(13)
