@@ -1183,8 +1183,14 @@ void Engine::elim_prep2(Elim& e, Scratch& S) {
     S.best.assign(nr, -1);
     S.rv_sq.resize(nr);
     S.rv_nz.resize(nr);
+    static const int trace_row = std::getenv("SPQR_TRACE_ROW") ? std::atoi(std::getenv("SPQR_TRACE_ROW")) : -1;
     for (int m : cand) {  // strict > in candidate order == the reference's per-row loop
         row_vals(fc, c, m, S.rv_sq.data(), S.rv_nz.data(), true);
+        if (trace_row >= 0)
+            for (size_t q = 0; q < nr; ++q)
+                if (fc.rows[q].gid == trace_row)
+                    std::fprintf(stderr, "[gpu row] c %d row %d cand %d sq %.17g (base %d sidx %d)\n", c, trace_row, m,
+                                 S.rv_sq[q], fc.rows[q].base, fc.rows[q].sidx);
         for (size_t q = 0; q < nr; ++q)
             if (S.rv_sq[q] > S.bw[q]) {
                 S.bw[q] = S.rv_sq[q];
@@ -1227,6 +1233,24 @@ void Engine::elim_commit2(Elim& e) {
         }
     }
     PFront& fc = pend_[pend_id_[c]];
+    if (const char* trace = std::getenv("SPQR_TRACE_SCOLS")) {  // diagnostics
+        std::string path(trace);
+        path = path.substr(0, path.find(':'));
+        if (FILE* tf = std::fopen(path.c_str(), "a")) {
+            if (cs > 0) std::fprintf(tf, "e %d rows %d tcols %d 0\n", c, e.total_rows, e.tcols);
+            static const int trace_c = std::getenv("SPQR_TRACE_ELIM") ? std::atoi(std::getenv("SPQR_TRACE_ELIM")) : -1;
+            if (c == trace_c && cs > 0) {
+                std::fprintf(tf, "S %d rows", c);
+                for (const PRow& r : e.srows) std::fprintf(tf, " %d", r.gid);
+                std::fprintf(tf, " keys");
+                for (int k : e.keys) std::fprintf(tf, " %d", k);
+                std::fprintf(tf, "\n");
+            }
+            for (const auto& d : e.dest) std::fprintf(tf, "m %d row %d tgt %d\n", c, fc.rows[d.second].gid, d.first);
+            for (int q : e.trail) std::fprintf(tf, "m %d row %d tgt -1\n", c, fc.rows[q].gid);
+            std::fclose(tf);
+        }
+    }
     for (int q : e.trail) out_.trailing_rows.push_back(fc.rows[q].gid);
     for (size_t a = 0; a < e.dest.size();) {  // append_rows, factorize.cpp:112-133 (ascending targets)
         size_t b = a;
@@ -1689,6 +1713,22 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
                 ++qi;
             }
         const QrDesc* dq = u.put(qd);
+        if (const char* dc = std::getenv("SPQR_TRACE_ELIM")) {  // diagnostics: the stack before its QR
+            const int want = std::atoi(dc);
+            for (int i = 0; i < nvalid; ++i)
+                if (el_[i].c == want && el_[i].cs > 0) {
+                    cudaStreamSynchronize(st_);
+                    const Elim& x = el_[i];
+                    std::vector<double> h(static_cast<size_t>(x.total_rows) * x.tcols);
+                    cudaMemcpy(h.data(), x.S, sizeof(double) * h.size(), cudaMemcpyDeviceToHost);
+                    if (FILE* df = std::fopen("gpurun_out/stack_gpu.bin", "wb")) {
+                        const int dims[3] = {x.total_rows, x.tcols, x.cs};
+                        std::fwrite(dims, 4, 3, df);
+                        std::fwrite(h.data(), 8, h.size(), df);
+                        std::fclose(df);
+                    }
+                }
+        }
         d_psq = arena().alloc_n<double>(std::max<long long>(postlen, 1));
         d_pnz = arena().alloc_n<unsigned char>(std::max<long long>(postlen, 1));
         pwork = layout_stats(pd.data(), pd.size());
@@ -1878,6 +1918,14 @@ void Engine::sparsify_rows_all() {
                 ++nseg;
             }
         if (nw == 0) {  // keep = 0: every extra row is dropped
+            if (const char* trace = std::getenv("SPQR_TRACE_SCOLS")) {  // diagnostics
+                std::string path(trace);
+                path = path.substr(0, path.find(':'));
+                if (FILE* tf = std::fopen(path.c_str(), "a")) {
+                    std::fprintf(tf, "r %d p2 %d nw 0 keep 0\n", static_cast<int>(p), p2);
+                    std::fclose(tf);
+                }
+            }
             for (int i = cs; i < r; ++i) out_.dropped_rows.push_back(f.rows[i]);
             f.rows.resize(cs);
             continue;
@@ -1930,6 +1978,14 @@ void Engine::sparsify_rows_all() {
         const Job& j = jobs[i];
         const int keep = rank[i];
         out_.ctr.cpqr_flops += 4.0 * j.p2 * double(j.nw) * keep + 2.0 * j.p2 * j.nw;
+        if (const char* trace = std::getenv("SPQR_TRACE_SCOLS")) {  // diagnostics
+            std::string path(trace);
+            path = path.substr(0, path.find(':'));
+            if (FILE* tf = std::fopen(path.c_str(), "a")) {
+                std::fprintf(tf, "r %d p2 %d nw %d keep %d\n", j.p, j.p2, j.nw, keep);
+                std::fclose(tf);
+            }
+        }
         if (keep >= j.p2) continue;
         Front& f = fr_[j.p];
         for (int r = j.cs + keep; r < j.cs + j.p2; ++r) out_.dropped_rows.push_back(f.rows[r]);
@@ -2133,6 +2189,29 @@ void Engine::sparsify_cols_all() {
                 continue;
             }
             done[j.p] = 1;
+            static const char* trace = std::getenv("SPQR_TRACE_SCOLS");  // diagnostics: "<path>[:cluster]"
+            if (trace) {
+                std::string tp(trace), path = tp;
+                int dump = -1;
+                if (auto cpos = tp.find(':'); cpos != std::string::npos) {
+                    path = tp.substr(0, cpos);
+                    dump = std::atoi(tp.c_str() + cpos + 1);
+                }
+                if (FILE* f = std::fopen(path.c_str(), "a")) {
+                    std::fprintf(f, "p %d cs %d nG %d rank %d\n", j.p, j.cs, j.nG, r2);
+                    std::fclose(f);
+                }
+                if (j.p == dump && j.nG > 0) {
+                    // G as it was factored: re-gather is not possible here, the CPQR overwrote it;
+                    // the dump therefore holds the factored block (rank rows of R in place)
+                    std::vector<double> h(static_cast<size_t>(j.cs) * j.nG);
+                    cudaMemcpy(h.data(), j.G, sizeof(double) * h.size(), cudaMemcpyDeviceToHost);
+                    if (FILE* f = std::fopen((path + ".R").c_str(), "wb")) {
+                        std::fwrite(h.data(), 8, h.size(), f);
+                        std::fclose(f);
+                    }
+                }
+            }
             if (r2 >= j.cs) continue;
             changed[j.p] = 1;
             const int p = j.p;
