@@ -2087,12 +2087,18 @@ void Engine::sparsify_cols_all() {
         AsmBuilder gb;
         std::vector<CpqrDesc> cd;
         int maxm = 0;
-        for (int p : wave) {
-            Front& f = fr_[p];
-            Job j;
+        // per-job shapes in parallel (holder sets normalised first: get() sorts lazily),
+        // then allocation and descriptor reservation in wave order
+        for (int p : wave) holders_[p].norm();
+        jobs.resize(wave.size());
+#pragma omp parallel for schedule(dynamic, 8) if (wave.size() > 64)
+        for (long long wi = 0; wi < static_cast<long long>(wave.size()); ++wi) {
+            const int p = wave[wi];
+            const Front& f = fr_[p];
+            Job& j = jobs[wi];
             j.p = p;
             j.cs = width(p);
-            for (int m : holders_[p].get())
+            for (int m : holders_[p].v)
                 if (m != p && fr_[m].live) j.rparts.push_back(m);
             int wrows = 0;
             for (int m : j.rparts) {
@@ -2108,6 +2114,8 @@ void Engine::sparsify_cols_all() {
             j.wrows = wrows;
             j.nG = wrows + wcols;
             j.kmax = std::min(j.cs, j.nG);
+        }
+        for (Job& j : jobs) {
             j.G = dalloc(arena(), static_cast<size_t>(j.cs) * std::max(j.nG, 1), j.gbig);
             // G (cs x nG) built transposed: G column g <- a row of holder m or a column of own block;
             // logical G^T (nG x cs) gathered row by row, stored transposed as G (ld = cs).  The
@@ -2123,8 +2131,9 @@ void Engine::sparsify_cols_all() {
             j.sign = out_.warena->alloc_n<double>(std::max(j.kmax, 1));
             maxm = std::max(maxm, j.cs);
             out_.ctr.cpqr_bytes += 8.0 * j.cs * j.nG;
-            jobs.push_back(std::move(j));
         }
+        sc1.reset();
+        sc1 = std::make_unique<NScope>(nprof_, "scols.G_fill");
 #pragma omp parallel for schedule(dynamic, 4) if (jobs.size() > 16)
         for (long long ji = 0; ji < static_cast<long long>(jobs.size()); ++ji) {
             const Job& j = jobs[ji];
