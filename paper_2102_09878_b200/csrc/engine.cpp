@@ -1435,7 +1435,7 @@ void Engine::compute_stats(const std::vector<int>& P) {
     }
     const long long work = wcount[nP];
     std::vector<StatDesc> sd(dcount[nP]);
-#pragma omp parallel for schedule(dynamic, 256) if (nP > 64)
+#pragma omp parallel for schedule(dynamic, 256)
     for (long long t = 0; t < static_cast<long long>(nP); ++t) {
         Front& F = fr_[P[t]];
         F.soff.assign(F.keys.size(), -1);
