@@ -13,6 +13,7 @@
 #include <cfloat>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 
 #include "dev.h"
 
@@ -195,8 +196,15 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // c+1 (cp.async, zero-filled outside the block) is in flight while the DMMA
 // tiles of chunk c run.  Pass 2 writes the updated chunk back through shared
 // memory so the global stores are coalesced column runs.
-__global__ void __launch_bounds__(512) k_wy(double* __restrict__ a, int ld, long long stride, int m, int ntot, int j0,
-                                            int w, const double* __restrict__ T_all) {
+// NWARP = 16: warp tiles 8x32 (W) and 8x64 (C chunk); NWARP = 8: 16x32 and 16x64,
+// half the fragment loads per DMMA and twice the accumulators per warp.
+template <int NWARP>
+__global__ void __launch_bounds__(32 * NWARP) k_wy(double* __restrict__ a, int ld, long long stride, int m, int ntot,
+                                                   int j0, int w, const double* __restrict__ T_all) {
+    constexpr int PM = 64 / (NWARP * 4), PN = 4;   // pass 1 / T^T W: m-tiles x n-tiles per warp
+    constexpr int MG = 4 / PM;                    // m-groups over the 4 W row tiles
+    constexpr int QM = 128 / (NWARP * 8), QN = 8;  // pass 2: m-tiles x n-tiles per warp
+    constexpr int QG = 8 / QM;                     // m-groups over the 8 chunk row tiles
     const int b = blockIdx.y;
     double* A = a + b * stride;
     const double* T = T_all + static_cast<long long>(b) * NB * NB;
@@ -241,9 +249,9 @@ __global__ void __launch_bounds__(512) k_wy(double* __restrict__ a, int ld, long
         }
         cp_commit();
     };
-    // ---- pass 1: W = V^T C; warp: W rows (wid&3)*8.., cols (wid>>2)*32.. (4 tiles)
-    double acc[4][2] = {};
-    const int mr = (wid & 3) * 8, nc0 = (wid >> 2) * 32;
+    // ---- pass 1: W = V^T C; warp: W row tiles mg*PM.., column tiles ng*PN..
+    const int mg = wid % MG, ng = wid / MG;
+    double acc[PM][PN][2] = {};
     issue(0, false);
     for (int c = 0; c < nchunk; ++c) {
         if (c + 1 < nchunk) issue(c + 1, false);
@@ -256,33 +264,51 @@ __global__ void __launch_bounds__(512) k_wy(double* __restrict__ a, int ld, long
         const double* sV = sVb[c & 1];
 #pragma unroll 4
         for (int k0 = 0; k0 < CH; k0 += 4) {
-            const double av = sV[(k0 + t4) + (mr + g) * LDV];
+            double av[PM], bv[PN];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) dmma(acc[q][0], acc[q][1], av, sC[(k0 + t4) + (nc0 + q * 8 + g) * LDC]);
+            for (int i = 0; i < PM; ++i) av[i] = sV[(k0 + t4) + ((mg * PM + i) * 8 + g) * LDV];
+#pragma unroll
+            for (int q = 0; q < PN; ++q) bv[q] = sC[(k0 + t4) + ((ng * PN + q) * 8 + g) * LDC];
+#pragma unroll
+            for (int i = 0; i < PM; ++i)
+#pragma unroll
+                for (int q = 0; q < PN; ++q) dmma(acc[i][q][0], acc[i][q][1], av[i], bv[q]);
         }
         __syncthreads();
     }
     issue(0, true);  // pass 2's first chunk streams in while W is finished
-    for (int q = 0; q < 4; ++q) {
-        sW[(mr + g) + (nc0 + q * 8 + 2 * t4) * LDW] = acc[q][0];
-        sW[(mr + g) + (nc0 + q * 8 + 2 * t4 + 1) * LDW] = acc[q][1];
-    }
+#pragma unroll
+    for (int i = 0; i < PM; ++i)
+#pragma unroll
+        for (int q = 0; q < PN; ++q) {
+            sW[((mg * PM + i) * 8 + g) + ((ng * PN + q) * 8 + 2 * t4) * LDW] = acc[i][q][0];
+            sW[((mg * PM + i) * 8 + g) + ((ng * PN + q) * 8 + 2 * t4 + 1) * LDW] = acc[i][q][1];
+        }
     __syncthreads();
     // ---- W2 = T^T W
-    double acc2[4][2] = {};
+    double acc2[PM][PN][2] = {};
 #pragma unroll
     for (int k0 = 0; k0 < NB; k0 += 4) {
-        const double av = sT[(k0 + t4) + (mr + g) * LDW];
+        double av[PM], bv[PN];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dmma(acc2[q][0], acc2[q][1], av, sW[(k0 + t4) + (nc0 + q * 8 + g) * LDW]);
+        for (int i = 0; i < PM; ++i) av[i] = sT[(k0 + t4) + ((mg * PM + i) * 8 + g) * LDW];
+#pragma unroll
+        for (int q = 0; q < PN; ++q) bv[q] = sW[(k0 + t4) + ((ng * PN + q) * 8 + g) * LDW];
+#pragma unroll
+        for (int i = 0; i < PM; ++i)
+#pragma unroll
+            for (int q = 0; q < PN; ++q) dmma(acc2[i][q][0], acc2[i][q][1], av[i], bv[q]);
     }
     __syncthreads();
-    for (int q = 0; q < 4; ++q) {
-        sW[(mr + g) + (nc0 + q * 8 + 2 * t4) * LDW] = acc2[q][0];
-        sW[(mr + g) + (nc0 + q * 8 + 2 * t4 + 1) * LDW] = acc2[q][1];
-    }
-    // ---- pass 2: C -= V W2; warp: chunk rows (wid&7)*8.., cols (wid>>3)*64.. (8 tiles)
-    const int rr = (wid & 7) * 8, cc0 = (wid >> 3) * 64;
+#pragma unroll
+    for (int i = 0; i < PM; ++i)
+#pragma unroll
+        for (int q = 0; q < PN; ++q) {
+            sW[((mg * PM + i) * 8 + g) + ((ng * PN + q) * 8 + 2 * t4) * LDW] = acc2[i][q][0];
+            sW[((mg * PM + i) * 8 + g) + ((ng * PN + q) * 8 + 2 * t4 + 1) * LDW] = acc2[i][q][1];
+        }
+    // ---- pass 2: C -= V W2; warp: chunk row tiles qg*QM.., column tiles qn*QN..
+    const int qg = wid % QG, qn = wid / QG;
     for (int c = 0; c < nchunk; ++c) {
         const int r0 = c * CH, rc = min(CH, rows - r0);
         if (c + 1 < nchunk) issue(c + 1, true);
@@ -293,23 +319,27 @@ __global__ void __launch_bounds__(512) k_wy(double* __restrict__ a, int ld, long
         __syncthreads();
         double* sC = sCb[c & 1];
         const double* sVt = sVb[c & 1];
-        double o[8][2];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            o[q][0] = -sC[(rr + g) + (cc0 + q * 8 + 2 * t4) * LDC];
-            o[q][1] = -sC[(rr + g) + (cc0 + q * 8 + 2 * t4 + 1) * LDC];
-        }
+        double o[QM][QN][2] = {};
 #pragma unroll
         for (int k0 = 0; k0 < NB; k0 += 4) {
-            const double av = sVt[(k0 + t4) + (rr + g) * LDVT];
+            double av[QM], bv[QN];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) dmma(o[q][0], o[q][1], av, sW[(k0 + t4) + (cc0 + q * 8 + g) * LDW]);
+            for (int i = 0; i < QM; ++i) av[i] = sVt[(k0 + t4) + ((qg * QM + i) * 8 + g) * LDVT];
+#pragma unroll
+            for (int q = 0; q < QN; ++q) bv[q] = sW[(k0 + t4) + ((qn * QN + q) * 8 + g) * LDW];
+#pragma unroll
+            for (int i = 0; i < QM; ++i)
+#pragma unroll
+                for (int q = 0; q < QN; ++q) dmma(o[i][q][0], o[i][q][1], av[i], bv[q]);
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {  // each element is read and written by its own thread only
-            sC[(rr + g) + (cc0 + q * 8 + 2 * t4) * LDC] = -o[q][0];
-            sC[(rr + g) + (cc0 + q * 8 + 2 * t4 + 1) * LDC] = -o[q][1];
-        }
+        for (int i = 0; i < QM; ++i)
+#pragma unroll
+            for (int q = 0; q < QN; ++q) {  // each element is read and written by its own thread only
+                const int row = (qg * QM + i) * 8 + g, col = (qn * QN + q) * 8 + 2 * t4;
+                sC[row + col * LDC] -= o[i][q][0];
+                sC[row + (col + 1) * LDC] -= o[i][q][1];
+            }
         __syncthreads();
         for (int e = threadIdx.x; e < CH * TC2; e += blockDim.x) {
             const int i = e % CH, j = e / CH;
@@ -402,9 +432,16 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
             dim3 grid((trail + TC2 - 1) / TC2, nbatch);
             const size_t vsz = std::max(NB * LDV, CH * LDVT);
             const size_t wsm = sizeof(double) * (2 * vsz + 2 * TC2 * LDC + TC2 * LDW + NB * LDW);
-            static size_t cfg = 0;
-            smem_optin(reinterpret_cast<const void*>(k_wy), wsm, cfg);
-            k_wy<<<grid, 512, wsm, st>>>(d_a, ldA, stride, m, ntot, j0, w, d_T);
+            static const bool wy8 = std::getenv("SPQR_WY8") != nullptr;  // 8-warp variant: measured no faster
+            if (wy8) {
+                static size_t cfg = 0;
+                smem_optin(reinterpret_cast<const void*>(k_wy<8>), wsm, cfg);
+                k_wy<8><<<grid, 256, wsm, st>>>(d_a, ldA, stride, m, ntot, j0, w, d_T);
+            } else {
+                static size_t cfg = 0;
+                smem_optin(reinterpret_cast<const void*>(k_wy<16>), wsm, cfg);
+                k_wy<16><<<grid, 512, wsm, st>>>(d_a, ldA, stride, m, ntot, j0, w, d_T);
+            }
         }
     }
     dim3 g2((ntot + 255) / 256, nbatch);
