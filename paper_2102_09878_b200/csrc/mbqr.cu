@@ -15,6 +15,8 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "dev.h"
 
 namespace spqr {
@@ -178,6 +180,147 @@ __global__ void __launch_bounds__(32 * NWP) k_panel2(double* __restrict__ a, int
             const int j = e / rows, i = e - j * rows;
             A[(j0 + i) + static_cast<long long>(j0 + j) * ld] = P[i + j * pld];
         }
+}
+
+// Tall panels (more rows than one SM's shared memory holds): a thread-block
+// cluster of kCS CTAs per panel, CTA r keeping rows [r R, (r+1) R) of the w <= 32
+// panel columns in its shared memory.  Per reflector there are two cluster
+// barriers: the per-CTA partial tail norms of column k are exchanged through
+// distributed shared memory (every CTA forms the same Householder scalars), then
+// the per-CTA partial dot products of v_k with all panel columns (lanes left of
+// k give V^T v_k for T).  Partials are double-buffered by step parity, so a
+// CTA can start the next step while slower ones still read the previous one.
+constexpr int kCS = 8;  // CTAs per cluster (portable maximum)
+
+__global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(256)
+    k_panel_cluster(double* __restrict__ a, int ld, long long stride, int m, int j0, int w,
+                    double* __restrict__ tau_all, int tau_stride, double* __restrict__ T_all, int R) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int b = blockIdx.x / kCS;
+    double* A = a + b * stride;
+    double* tau = tau_all + static_cast<long long>(b) * tau_stride;
+    double* T = T_all + static_cast<long long>(b) * NB * NB;
+    extern __shared__ double P[];  // R x w, column-major, ld R (this CTA's rows)
+    __shared__ double nrm[2][2];   // [parity][tail sumsq, c0 (owner only)]
+    __shared__ double dots[2][32]; // [parity][column]
+    __shared__ double red[8][33];
+    __shared__ double Ts[NB * NB], gv[NB];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int rows = m - j0;
+    const int g0 = rank * R;                       // first panel row of this CTA
+    const int nr = max(0, min(R, rows - g0));      // rows held here
+    for (int e = threadIdx.x; e < nr * w; e += blockDim.x) {
+        const int j = e / nr, i = e - j * nr;
+        P[i + j * R] = A[(j0 + g0 + i) + static_cast<long long>(j0 + j) * ld];
+    }
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) Ts[e] = 0.0;
+    __syncthreads();
+    const int kmax = min(w, rows);
+    for (int k = 0; k < kmax; ++k) {
+        const int par = k & 1;
+        double* pk = P + k * R;
+        // local rows > k of column k (global row index g0 + i)
+        const int lo = max(0, k + 1 - g0);
+        double s = 0.0;
+        for (int i = lo + threadIdx.x; i < nr; i += blockDim.x) s = fma(pk[i], pk[i], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) red[wid][0] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < 8; ++q) t += red[q][0];
+            nrm[par][0] = t;
+            nrm[par][1] = (k >= g0 && k < g0 + nr) ? pk[k - g0] : 0.0;
+        }
+        cluster.sync();
+        double tail2 = 0.0, c0 = 0.0;
+        for (int r = 0; r < kCS; ++r) {  // same order in every CTA
+            const double* rn = cluster.map_shared_rank(&nrm[par][0], r);
+            tail2 += rn[0];
+            c0 += rn[1];  // only the owner of row k contributes
+        }
+        double t = 0.0, den = 0.0, beta = c0;
+        if (!(tail2 <= DBL_MIN)) {
+            beta = sqrt(c0 * c0 + tail2);
+            if (c0 >= 0.0) beta = -beta;
+            den = c0 - beta;
+            t = (beta - c0) / beta;
+        }
+        for (int i = lo + threadIdx.x; i < nr; i += blockDim.x) pk[i] = (t == 0.0) ? 0.0 : pk[i] / den;
+        if (threadIdx.x == 0) {
+            if (k >= g0 && k < g0 + nr) pk[k - g0] = beta;
+            if (rank == 0) tau[j0 + k] = t;
+        }
+        __syncthreads();
+        // partial dots over local rows >= k: v_k^T a_j for every panel column j
+        const int lo2 = max(0, k - g0);
+        double acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+        if (t != 0.0) {
+            for (int i = lo2 + threadIdx.x; i < nr; i += blockDim.x) {
+                const double v = (g0 + i == k) ? 1.0 : pk[i];
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < w && j != k) acc[j] = fma(v, P[i + j * R], acc[j]);
+            }
+        }
+        // lane j ends with column j's warp total, then the CTA total
+#pragma unroll
+        for (int o = 16, cnt = 16; o >= 1; o >>= 1, cnt >>= 1) {
+            const bool up = lane & o;
+#pragma unroll
+            for (int i = 0; i < cnt; ++i) {
+                const double send = up ? acc[i] : acc[i + cnt];
+                const double keep = up ? acc[i + cnt] : acc[i];
+                acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        red[wid][lane] = acc[0];
+        __syncthreads();
+        if (wid == 0) {
+            double tsum = 0.0;
+            for (int q = 0; q < 8; ++q) tsum += red[q][lane];
+            dots[par][lane] = tsum;
+        }
+        cluster.sync();
+        double wl = 0.0;  // lane j: total v_k^T a_j over the cluster
+        for (int r = 0; r < kCS; ++r) wl += cluster.map_shared_rank(&dots[par][0], r)[lane];
+        if (t != 0.0) {
+            const double twl = (lane > k && lane < w) ? -t * wl : 0.0;
+            double tws[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tws[j] = __shfl_sync(0xffffffffu, twl, j);
+            for (int i = lo2 + threadIdx.x; i < nr; i += blockDim.x) {
+                const double v = (g0 + i == k) ? 1.0 : pk[i];
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j > k && j < w) P[i + j * R] = fma(tws[j], v, P[i + j * R]);
+            }
+            if (rank == 0 && wid == 0) {  // T(:, k) = -t T(0:k, 0:k) (V^T v_k),  T(k, k) = t
+                if (lane < k) gv[lane] = wl;
+                __syncwarp();
+                if (lane < k) {
+                    double sacc = 0.0;
+                    for (int l = lane; l < k; ++l) sacc = fma(Ts[lane + l * NB], gv[l], sacc);
+                    Ts[lane + k * NB] = -t * sacc;
+                }
+                if (lane == 0) Ts[k + k * NB] = t;
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+    }
+    cluster.sync();  // no CTA exits while another may still read its partials
+    if (rank == 0)
+        for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) T[e] = Ts[e];
+    for (int e = threadIdx.x; e < nr * w; e += blockDim.x) {
+        const int j = e / nr, i = e - j * nr;
+        A[(j0 + g0 + i) + static_cast<long long>(j0 + j) * ld] = P[i + j * R];
+    }
 }
 
 // Block reflector on a TC-column tile of the trailing matrix:
@@ -418,7 +561,15 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
         const int smem_rows = static_cast<int>(smem_cap / (sizeof(double) * (NB + 1))) - 2;
         const size_t smem = rows <= smem_rows ? sizeof(double) * (rows * static_cast<size_t>(w) + rows)
                                               : sizeof(double) * static_cast<size_t>(rows);
-        if (rows <= 512) {
+        // tall panels: a cluster of kCS CTAs holds the rows in distributed shared memory
+        const int Rc = ((rows + kCS - 1) / kCS + 31) & ~31;
+        if (rows > smem_rows && static_cast<size_t>(Rc) * w * sizeof(double) <= 200 * 1024 &&
+            !std::getenv("SPQR_NO_CLUSTER_PANEL")) {
+            const size_t csmem = sizeof(double) * static_cast<size_t>(Rc) * w;
+            static size_t cfg = 0;
+            smem_optin(reinterpret_cast<const void*>(k_panel_cluster), csmem, cfg);
+            k_panel_cluster<<<nbatch * kCS, 256, csmem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, Rc);
+        } else if (rows <= 512) {
             static size_t cfg = 0;
             smem_optin(reinterpret_cast<const void*>(k_panel2<8>), smem, cfg);
             k_panel2<8><<<nbatch, 256, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);

@@ -19,7 +19,9 @@ def _P():
                                    # column-tiled path: many tiles, panel only, square panel, m > 256
                                    (33, 5, 1000), (200, 100, 100), (64, 64, 200), (480, 20, 300),
                                    # dynamic smem just under 48 KB: static + dynamic needs the opt-in
-                                   (129, 47, 150)])
+                                   (129, 47, 150),
+                                   # tall panels: thread-block-cluster panel factorisation (mbqr.cu)
+                                   (1500, 40, 100), (4096, 33, 60)])
 def test_qr_apply_matches_oracle(shape, path, monkeypatch):
     """auto = column-tiled kernel where the panel fits in shared memory (qr_tile.cu);
     tile_dmma = the same with its DMMA compact-WY tile phase; smem = whole block staged per
