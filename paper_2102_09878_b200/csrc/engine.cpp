@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <iterator>
@@ -128,6 +129,36 @@ struct HolderSet {
 void sorted_insert(std::vector<int>& v, int x) {
     auto it = std::lower_bound(v.begin(), v.end(), x);
     if (it == v.end() || *it != x) v.insert(it, x);
+}
+
+// Parity diagnostics (off unless SPQR_TRACE_SCOLS=<path>): one text line per
+// elimination, row move and sparsify decision, in the format the oracle writes,
+// so tools/trace_scols.py can diff the two engines.  SPQR_TRACE_ELIM=<cluster>
+// adds that elimination's stack rows and dumps its stack before the QR;
+// SPQR_TRACE_ROW=<row> prints the move_extras candidates of that row.
+struct ParityTrace {
+    std::string path;
+    int elim = -1, row = -1;
+    ParityTrace() {
+        if (const char* t = std::getenv("SPQR_TRACE_SCOLS")) path = std::string(t).substr(0, std::string(t).find(':'));
+        if (const char* e = std::getenv("SPQR_TRACE_ELIM")) elim = std::atoi(e);
+        if (const char* r = std::getenv("SPQR_TRACE_ROW")) row = std::atoi(r);
+    }
+    bool on() const { return !path.empty(); }
+    void line(const char* fmt, ...) const {
+        if (!on()) return;
+        if (FILE* f = std::fopen(path.c_str(), "a")) {
+            va_list ap;
+            va_start(ap, fmt);
+            std::vfprintf(f, fmt, ap);
+            va_end(ap);
+            std::fclose(f);
+        }
+    }
+};
+const ParityTrace& ptrace() {
+    static const ParityTrace t;
+    return t;
 }
 
 // Host-side profile (SPQR_PROF=1 prints it to stderr after the factorization).
@@ -1183,7 +1214,7 @@ void Engine::elim_prep2(Elim& e, Scratch& S) {
     S.best.assign(nr, -1);
     S.rv_sq.resize(nr);
     S.rv_nz.resize(nr);
-    static const int trace_row = std::getenv("SPQR_TRACE_ROW") ? std::atoi(std::getenv("SPQR_TRACE_ROW")) : -1;
+    const int trace_row = ptrace().row;
     for (int m : cand) {  // strict > in candidate order == the reference's per-row loop
         row_vals(fc, c, m, S.rv_sq.data(), S.rv_nz.data(), true);
         if (trace_row >= 0)
@@ -1233,23 +1264,18 @@ void Engine::elim_commit2(Elim& e) {
         }
     }
     PFront& fc = pend_[pend_id_[c]];
-    if (const char* trace = std::getenv("SPQR_TRACE_SCOLS")) {  // diagnostics
-        std::string path(trace);
-        path = path.substr(0, path.find(':'));
-        if (FILE* tf = std::fopen(path.c_str(), "a")) {
-            if (cs > 0) std::fprintf(tf, "e %d rows %d tcols %d 0\n", c, e.total_rows, e.tcols);
-            static const int trace_c = std::getenv("SPQR_TRACE_ELIM") ? std::atoi(std::getenv("SPQR_TRACE_ELIM")) : -1;
-            if (c == trace_c && cs > 0) {
-                std::fprintf(tf, "S %d rows", c);
-                for (const PRow& r : e.srows) std::fprintf(tf, " %d", r.gid);
-                std::fprintf(tf, " keys");
-                for (int k : e.keys) std::fprintf(tf, " %d", k);
-                std::fprintf(tf, "\n");
-            }
-            for (const auto& d : e.dest) std::fprintf(tf, "m %d row %d tgt %d\n", c, fc.rows[d.second].gid, d.first);
-            for (int q : e.trail) std::fprintf(tf, "m %d row %d tgt -1\n", c, fc.rows[q].gid);
-            std::fclose(tf);
+    if (ptrace().on()) {
+        const ParityTrace& T = ptrace();
+        if (cs > 0) T.line("e %d rows %d tcols %d 0\n", c, e.total_rows, e.tcols);
+        if (c == T.elim && cs > 0) {
+            std::string l = "S " + std::to_string(c) + " rows";
+            for (const PRow& r : e.srows) l += " " + std::to_string(r.gid);
+            l += " keys";
+            for (int k : e.keys) l += " " + std::to_string(k);
+            T.line("%s\n", l.c_str());
         }
+        for (const auto& d : e.dest) T.line("m %d row %d tgt %d\n", c, fc.rows[d.second].gid, d.first);
+        for (int q : e.trail) T.line("m %d row %d tgt -1\n", c, fc.rows[q].gid);
     }
     for (int q : e.trail) out_.trailing_rows.push_back(fc.rows[q].gid);
     for (size_t a = 0; a < e.dest.size();) {  // append_rows, factorize.cpp:112-133 (ascending targets)
@@ -1713,8 +1739,8 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
                 ++qi;
             }
         const QrDesc* dq = u.put(qd);
-        if (const char* dc = std::getenv("SPQR_TRACE_ELIM")) {  // diagnostics: the stack before its QR
-            const int want = std::atoi(dc);
+        if (ptrace().elim >= 0) {  // diagnostics: the traced elimination's stack before its QR
+            const int want = ptrace().elim;
             for (int i = 0; i < nvalid; ++i)
                 if (el_[i].c == want && el_[i].cs > 0) {
                     cudaStreamSynchronize(st_);
@@ -1918,14 +1944,7 @@ void Engine::sparsify_rows_all() {
                 ++nseg;
             }
         if (nw == 0) {  // keep = 0: every extra row is dropped
-            if (const char* trace = std::getenv("SPQR_TRACE_SCOLS")) {  // diagnostics
-                std::string path(trace);
-                path = path.substr(0, path.find(':'));
-                if (FILE* tf = std::fopen(path.c_str(), "a")) {
-                    std::fprintf(tf, "r %d p2 %d nw 0 keep 0\n", static_cast<int>(p), p2);
-                    std::fclose(tf);
-                }
-            }
+            ptrace().line("r %d p2 %d nw 0 keep 0\n", static_cast<int>(p), p2);
             for (int i = cs; i < r; ++i) out_.dropped_rows.push_back(f.rows[i]);
             f.rows.resize(cs);
             continue;
@@ -1978,14 +1997,7 @@ void Engine::sparsify_rows_all() {
         const Job& j = jobs[i];
         const int keep = rank[i];
         out_.ctr.cpqr_flops += 4.0 * j.p2 * double(j.nw) * keep + 2.0 * j.p2 * j.nw;
-        if (const char* trace = std::getenv("SPQR_TRACE_SCOLS")) {  // diagnostics
-            std::string path(trace);
-            path = path.substr(0, path.find(':'));
-            if (FILE* tf = std::fopen(path.c_str(), "a")) {
-                std::fprintf(tf, "r %d p2 %d nw %d keep %d\n", j.p, j.p2, j.nw, keep);
-                std::fclose(tf);
-            }
-        }
+        ptrace().line("r %d p2 %d nw %d keep %d\n", j.p, j.p2, j.nw, keep);
         if (keep >= j.p2) continue;
         Front& f = fr_[j.p];
         for (int r = j.cs + keep; r < j.cs + j.p2; ++r) out_.dropped_rows.push_back(f.rows[r]);
@@ -2198,29 +2210,7 @@ void Engine::sparsify_cols_all() {
                 continue;
             }
             done[j.p] = 1;
-            static const char* trace = std::getenv("SPQR_TRACE_SCOLS");  // diagnostics: "<path>[:cluster]"
-            if (trace) {
-                std::string tp(trace), path = tp;
-                int dump = -1;
-                if (auto cpos = tp.find(':'); cpos != std::string::npos) {
-                    path = tp.substr(0, cpos);
-                    dump = std::atoi(tp.c_str() + cpos + 1);
-                }
-                if (FILE* f = std::fopen(path.c_str(), "a")) {
-                    std::fprintf(f, "p %d cs %d nG %d rank %d\n", j.p, j.cs, j.nG, r2);
-                    std::fclose(f);
-                }
-                if (j.p == dump && j.nG > 0) {
-                    // G as it was factored: re-gather is not possible here, the CPQR overwrote it;
-                    // the dump therefore holds the factored block (rank rows of R in place)
-                    std::vector<double> h(static_cast<size_t>(j.cs) * j.nG);
-                    cudaMemcpy(h.data(), j.G, sizeof(double) * h.size(), cudaMemcpyDeviceToHost);
-                    if (FILE* f = std::fopen((path + ".R").c_str(), "wb")) {
-                        std::fwrite(h.data(), 8, h.size(), f);
-                        std::fclose(f);
-                    }
-                }
-            }
+            ptrace().line("p %d cs %d nG %d rank %d\n", j.p, j.cs, j.nG, r2);
             if (r2 >= j.cs) continue;
             changed[j.p] = 1;
             const int p = j.p;

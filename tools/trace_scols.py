@@ -25,14 +25,22 @@ def load(f):
     d, order = {}, []
     for line in open(f):
         t = line.split()
-        key = (t[0], int(t[1])) if t[0] != "m" else ("m", int(t[1]), int(t[3]))
-        d.setdefault(key, []).append((int(t[3]), int(t[5]), int(t[7])) if t[0] != "m" else (int(t[5]),))
+        if t[0] == "S":
+            continue
+        if t[0] == "m":  # row move: m <cluster> row <row> tgt <front>
+            key, val = ("m", int(t[1]), int(t[3])), (int(t[5]),)
+        elif t[0] == "e":  # elimination: e <cluster> rows <n> tcols <n> 0
+            key, val = ("e", int(t[1])), (int(t[3]), int(t[5]))
+        else:  # r / p: <kind> <cluster> a <n> b <n> c <n>
+            key, val = (t[0], int(t[1])), (int(t[3]), int(t[5]), int(t[7]))
+        d.setdefault(key, []).append(val)
         order.append(key)
     return d, order
 (a, oa), (b, ob) = load(f"{out}/trace_gpu.txt"), load(f"{out}/trace_orc.txt")
 diff = [k for k in ob if a.get(k) != b.get(k)]
 print("records", len(a), len(b), "differing", len(set(diff)))
-print("first differences in the oracle's order (r = sparsify_rows p2/nw/keep, p = sparsify_cols cs/nG/rank):")
+print("first differences in the oracle's order (e = elimination rows/cols, m = row move target,\n"
+      "r = sparsify_rows p2/nw/keep, p = sparsify_cols cs/nG/rank):")
 seen = set()
 for k in diff:
     if k in seen:
