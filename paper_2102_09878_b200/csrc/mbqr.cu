@@ -14,6 +14,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdlib>
+#include <algorithm>
 
 #include <cooperative_groups.h>
 
@@ -539,6 +540,695 @@ __global__ void k_qr_post(double* __restrict__ a, int ld, int m, int n, double* 
     }
 }
 
+
+// Register-resident panel factorisation for the two-level path, row layout:
+// CTA rank r of a CS-CTA cluster holds panel rows [r NW 32 RR, (r+1) NW 32 RR);
+// thread (warp g, lane l) holds rows base + g 32 RR + l + 32 q (q < RR), all w <= 32
+// panel columns, in registers.  The reflector loop is fully unrolled, so column
+// indices are compile-time.  Per reflector: tail norm of column k (warp
+// shuffles, barrier), the same Householder scalars in every thread (Eigen
+// makeHouseholder), v formed in place, the dot products of v with all columns
+// (transpose reduction: lane j ends with column j, barrier), broadcast by
+// shuffles and the rank-1 update of the columns right of k.  Lanes left of k
+// carry V^T v_k, which builds the panel's compact-WY T (accumulate_wy,
+// dense_kernels.cpp:41-53).  With CS > 1 each CTA pushes its partial sums into
+// every CTA's shared memory (remote stores), one cluster barrier per reduction,
+// and every CTA adds the CS partials in rank order (double-buffered by parity).
+template <int NW, int RR, int CS>
+__device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, long long stride, int m, int j0, int w,
+                                               double* __restrict__ tau_all, int tau_stride,
+                                               double* __restrict__ T_all) {
+    namespace cg = cooperative_groups;
+    constexpr int R = NW * 32 * RR;
+    const int rank = CS > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+    const int b = blockIdx.x / CS;
+    double* A = a + b * stride;
+    __shared__ double red[NW], part[NW][32];
+    __shared__ double s_c0;
+    __shared__ double nrm[2][CS][2], dots[2][CS][32];
+    __shared__ double Ts[NB * NB], gv[NB];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int rows = m - j0;
+    int row[RR];
+#pragma unroll
+    for (int q = 0; q < RR; ++q) row[q] = rank * R + wid * 32 * RR + 32 * q + lane;
+    double x[RR][NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+#pragma unroll
+        for (int q = 0; q < RR; ++q)
+            x[q][j] = (row[q] < rows && j < w) ? A[(j0 + row[q]) + static_cast<long long>(j0 + j) * ld] : 0.0;
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) Ts[e] = 0.0;
+    const int kmax = min(w, rows);
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        if (k < kmax) {
+            const int par = k & 1;
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < RR; ++q) {
+                if (row[q] > k) s = fma(x[q][k], x[q][k], s);
+                if (row[q] == k) s_c0 = x[q][k];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) red[wid] = s;
+            __syncthreads();
+            double tail2 = 0.0, c0 = 0.0;
+            if constexpr (CS == 1) {
+#pragma unroll
+                for (int g = 0; g < NW; ++g) tail2 += red[g];
+                c0 = s_c0;
+            } else {
+                if (threadIdx.x < CS) {  // push this CTA's partials to rank threadIdx.x
+                    double t2 = 0.0;
+#pragma unroll
+                    for (int g = 0; g < NW; ++g) t2 += red[g];
+                    double* dst = cg::this_cluster().map_shared_rank(&nrm[par][rank][0], static_cast<int>(threadIdx.x));
+                    dst[0] = t2;
+                    dst[1] = rank == 0 ? s_c0 : 0.0;
+                }
+                cg::this_cluster().sync();
+#pragma unroll
+                for (int r = 0; r < CS; ++r) {
+                    tail2 += nrm[par][r][0];
+                    c0 += nrm[par][r][1];
+                }
+            }
+            double t = 0.0, den = 0.0, beta = c0;
+            if (!(tail2 <= DBL_MIN)) {
+                beta = sqrt(c0 * c0 + tail2);
+                if (c0 >= 0.0) beta = -beta;
+                den = c0 - beta;
+                t = (beta - c0) / beta;
+            }
+            const double rden = (t == 0.0) ? 0.0 : 1.0 / den;
+            double v[RR];
+#pragma unroll
+            for (int q = 0; q < RR; ++q) {
+                if (row[q] > k) x[q][k] *= rden;
+                if (row[q] == k) x[q][k] = beta;
+                v[q] = row[q] > k ? x[q][k] : (row[q] == k ? 1.0 : 0.0);
+            }
+            if (rank == 0 && threadIdx.x == 0) tau_all[static_cast<long long>(b) * tau_stride + j0 + k] = t;
+            // p[j] = sum over this thread's rows of v x_j (column k itself is not needed),
+            // then a transpose reduction: lane j ends with column j's warp total.  The
+            // first butterfly level is folded into the dot products so that only 16
+            // partials are live at a time.
+            double p[16];
+            const bool up16 = lane & 16;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                double lo = 0.0, hi = 0.0;
+#pragma unroll
+                for (int q = 0; q < RR; ++q) {
+                    if (i != k) lo = fma(v[q], x[q][i], lo);
+                    if (i + 16 != k) hi = fma(v[q], x[q][i + 16], hi);
+                }
+                const double send = up16 ? lo : hi;
+                const double keep = up16 ? hi : lo;
+                p[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+#pragma unroll
+            for (int o = 8, cnt = 8; o >= 1; o >>= 1, cnt >>= 1) {
+                const bool up = lane & o;
+#pragma unroll
+                for (int i = 0; i < cnt; ++i) {
+                    const double send = up ? p[i] : p[i + cnt];
+                    const double keep = up ? p[i + cnt] : p[i];
+                    p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            part[wid][lane] = p[0];
+            __syncthreads();
+            double wl = 0.0;
+            if constexpr (CS == 1) {
+#pragma unroll
+                for (int g = 0; g < NW; ++g) wl += part[g][lane];
+            } else {
+                if (wid < CS) {  // warp q pushes this CTA's column sums to ranks q, q + NW, ...
+                    double s2 = 0.0;
+#pragma unroll
+                    for (int g = 0; g < NW; ++g) s2 += part[g][lane];
+                    for (int r = wid; r < CS; r += NW) cg::this_cluster().map_shared_rank(&dots[par][rank][0], r)[lane] = s2;
+                }
+                cg::this_cluster().sync();
+#pragma unroll
+                for (int r = 0; r < CS; ++r) wl += dots[par][r][lane];
+            }
+            if (t != 0.0) {
+                const double twl = -t * wl;
+#pragma unroll
+                for (int j = k + 1; j < NB; ++j) {
+                    const double tw = __shfl_sync(0xffffffffu, twl, j);
+#pragma unroll
+                    for (int q = 0; q < RR; ++q) x[q][j] = fma(tw, v[q], x[q][j]);
+                }
+            }
+            if (rank == 0 && wid == 0) {  // T(:, k) = -t T(0:k, 0:k) (V^T v_k),  T(k, k) = t
+                if (lane < k) gv[lane] = wl;
+                __syncwarp();
+                if (lane < k) {
+                    double sacc = 0.0;
+                    for (int l = lane; l < k; ++l) sacc = fma(Ts[lane + l * NB], gv[l], sacc);
+                    Ts[lane + k * NB] = -t * sacc;
+                }
+                if (lane == 0) Ts[k + k * NB] = t;
+                __syncwarp();
+            }
+        }
+    }
+    if constexpr (CS > 1) cg::this_cluster().sync();  // no remote store may target an exited CTA
+    // store addresses formed here (an opaque copy of ld keeps the compiler from
+    // hoisting 32 column addresses across the reflector loop into registers)
+    long long ldo;
+    asm volatile("mov.b64 %0, %1;" : "=l"(ldo) : "l"(static_cast<long long>(ld)));
+    double* base = A + j0 + ldo * j0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+#pragma unroll
+        for (int q = 0; q < RR; ++q)
+            if (row[q] < rows && j < w) base[row[q] + ldo * j] = x[q][j];
+    __syncthreads();
+    if (rank == 0) {
+        double* T = T_all + static_cast<long long>(b) * NB * NB;
+        for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) T[e] = Ts[e];
+    }
+}
+
+template <int NW, int RR>
+__global__ void __launch_bounds__(32 * NW, NW * RR <= 8 ? 2 : 1) k_panel_row(double* a, int ld, long long stride,
+                                                                           int m, int j0, int w, double* tau_all,
+                                                                           int tau_stride, double* T_all) {
+    panel_row_body<NW, RR, 1>(a, ld, stride, m, j0, w, tau_all, tau_stride, T_all);
+}
+
+template <int NW, int RR>
+__global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(32 * NW, NW * RR <= 8 ? 2 : 1)
+    k_panel_rowc(double* a, int ld, long long stride, int m, int j0, int w, double* tau_all, int tau_stride,
+                 double* T_all) {
+    panel_row_body<NW, RR, kCS>(a, ld, stride, m, j0, w, tau_all, tau_stride, T_all);
+}
+
+// register-resident panel launch; false when the panel is too tall
+bool launch_panel_reg(int nbatch, int m, int ld, long long stride, double* d_a, int j0, int w, double* d_tau, int n,
+                      double* d_T, cudaStream_t st) {
+    const int rows = m - j0;
+    const bool cl = rows > 512;
+    const int per = cl ? (rows + kCS - 1) / kCS : rows;  // rows per CTA
+    if (per > 512) return false;
+    const int g = cl ? nbatch * kCS : nbatch;
+#define SPQR_PANEL(NW_, RR_)                                                                                    \
+    (cl ? k_panel_rowc<NW_, RR_><<<g, 32 * NW_, 0, st>>>(d_a, ld, stride, m, j0, w, d_tau, n, d_T)                \
+        : k_panel_row<NW_, RR_><<<g, 32 * NW_, 0, st>>>(d_a, ld, stride, m, j0, w, d_tau, n, d_T))
+    if (per <= 64) SPQR_PANEL(2, 1);
+    else if (per <= 128) SPQR_PANEL(4, 1);
+    else if (per <= 256) SPQR_PANEL(8, 1);
+    else if (std::getenv("SPQR_PANEL_RR2")) SPQR_PANEL(8, 2);
+    else SPQR_PANEL(16, 1);
+#undef SPQR_PANEL
+    return true;
+}
+
+// ---- two-level blocking for large fronts ------------------------------------
+// The NB = 32 panels of an outer block of KO = 128 columns are factored and
+// applied to the rest of that outer block (KB = 32); the outer block's 128
+// reflectors are then applied to every trailing column at once (KB = 128),
+// which lifts the trailing update from ~5 flop/B (below the FP64 ridge) to
+// ~21 flop/B.  Each block-reflector application  C -= V T^T-free form
+//   W = V^T C,  W2 = T^T W,  C -= V W2
+// runs as three kernels so that rows and columns are both split across CTAs:
+//   k_vtc  partial W over a row slice (deterministic per-slice partials),
+//   k_tw   sum of the partials in fixed order, then T^T (DMMA),
+//   k_cvw  C -= V W2 over (row tile, column tile).
+// The outer T (128 x 128) is built from the Gram matrix V^T V (k_vtc on the
+// panel's own columns) by accumulate_wy's recurrence (dense_kernels.cpp:41-53):
+//   T(0:k, k) = -tau_k T(0:k, 0:k) V(:, 0:k)^T v_k,  T(k, k) = tau_k.
+constexpr int KO = 128;   // outer block width
+constexpr int TCG = 64;   // trailing columns per CTA
+constexpr int CHG = 32;   // rows per staged chunk
+constexpr int LDS_ = CHG + 4;
+
+// V(i, j) of the block starting at panel row 0 / column J0 (i, j panel-relative):
+// unit lower trapezoidal, columns >= kw are zero
+__device__ __forceinline__ bool v_direct(int i, int j, int kw, double& val) {
+    if (j >= kw || i < j) { val = 0.0; return true; }
+    if (i == j) { val = 1.0; return true; }
+    return false;
+}
+
+// partial W[s] = V(rows of slice s)^T C(rows of slice s, column tile t)
+// gram = 1: C is V itself (columns 0..KB of the block), i.e. W = V^T V
+template <int KB>
+__global__ void __launch_bounds__(256) k_vtc(const double* __restrict__ a, int ld, long long stride, int m, int J0,
+                                             int kw, int cbeg, int cend, int rs, int gram,
+                                             double* __restrict__ wp) {
+    constexpr int PM = KB / 32, PN = TCG / 16;
+    const int t = blockIdx.x, s = blockIdx.y, b = blockIdx.z;
+    const int ntile = gridDim.x, nsl = gridDim.y;
+    const double* A = a + b * stride;
+    const int rows = m - J0;
+    const int c0 = cbeg + t * TCG, nc = min(TCG, cend - c0);
+    const int rlo = s * rs, rhi = min(rows, rlo + rs);
+    extern __shared__ double dsm[];
+    double* const sV0 = dsm;                     // two V chunks, KB * LDS_ each
+    double* const sC0 = dsm + 2 * KB * LDS_;     // two C chunks, TCG * LDS_ each
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int mw = wid & 3, nw = wid >> 2;
+    const int nchunk = rhi > rlo ? (rhi - rlo + CHG - 1) / CHG : 0;
+    auto issue = [&](int c) {
+        const int r0 = rlo + c * CHG, rc = min(CHG, rhi - r0);
+        double* vb = sV0 + (c & 1) * (KB * LDS_);
+        double* cb = sC0 + (c & 1) * (TCG * LDS_);
+        for (int e = threadIdx.x; e < CHG * KB; e += 256) {
+            const int i = e % CHG, j = e / CHG, r = r0 + i;
+            double* dst = vb + i + j * LDS_;
+            double v;
+            if (i >= rc) *dst = 0.0;
+            else if (v_direct(r, j, kw, v)) *dst = v;
+            else cp_async8(dst, A + (J0 + r) + static_cast<long long>(J0 + j) * ld, true);
+        }
+        for (int e = threadIdx.x; e < CHG * TCG; e += 256) {
+            const int i = e % CHG, j = e / CHG, r = r0 + i;
+            double* dst = cb + i + j * LDS_;
+            double v;
+            if (i >= rc || j >= nc) *dst = 0.0;
+            else if (gram && v_direct(r, c0 - cbeg + j, kw, v)) *dst = v;
+            else cp_async8(dst, A + (J0 + r) + static_cast<long long>(c0 + j) * ld, true);
+        }
+        cp_commit();
+    };
+    double acc[PM][PN][2] = {};
+    if (nchunk > 0) issue(0);
+    for (int c = 0; c < nchunk; ++c) {
+        if (c + 1 < nchunk) {
+            issue(c + 1);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        const double* sV = sV0 + (c & 1) * (KB * LDS_);
+        const double* sC = sC0 + (c & 1) * (TCG * LDS_);
+#pragma unroll
+        for (int k0 = 0; k0 < CHG; k0 += 4) {
+            double av[PM], bv[PN];
+#pragma unroll
+            for (int i = 0; i < PM; ++i) av[i] = sV[(k0 + t4) + ((mw * PM + i) * 8 + g) * LDS_];
+#pragma unroll
+            for (int q = 0; q < PN; ++q) bv[q] = sC[(k0 + t4) + ((nw * PN + q) * 8 + g) * LDS_];
+#pragma unroll
+            for (int i = 0; i < PM; ++i)
+#pragma unroll
+                for (int q = 0; q < PN; ++q) dmma(acc[i][q][0], acc[i][q][1], av[i], bv[q]);
+        }
+        __syncthreads();
+    }
+    double* W = wp + ((static_cast<long long>(b) * nsl + s) * ntile + t) * (KB * TCG);
+#pragma unroll
+    for (int i = 0; i < PM; ++i)
+#pragma unroll
+        for (int q = 0; q < PN; ++q) {
+            const int row = (mw * PM + i) * 8 + g, col = (nw * PN + q) * 8 + 2 * t4;
+            W[row + col * KB] = acc[i][q][0];
+            W[row + (col + 1) * KB] = acc[i][q][1];
+        }
+}
+
+// W2 = T^T (sum_s W[s]) for column tile t; written over slice 0's partial
+template <int KB>
+__global__ void __launch_bounds__(256) k_tw(double* __restrict__ wp, int nsl, const double* __restrict__ T_all,
+                                            int kw) {
+    constexpr int PM = KB / 32, PN = TCG / 16, LDW = KB + 4;
+    const int t = blockIdx.x, b = blockIdx.y, ntile = gridDim.x;
+    extern __shared__ double sW[];  // KB x TCG, ld LDW
+    const double* T = T_all + static_cast<long long>(b) * KB * KB;
+    double* W0 = wp + (static_cast<long long>(b) * nsl * ntile + t) * (KB * TCG);
+    for (int e = threadIdx.x; e < KB * TCG; e += 256) {
+        double v = 0.0;
+        for (int s = 0; s < nsl; ++s) v += W0[static_cast<long long>(s) * ntile * (KB * TCG) + e];
+        sW[(e % KB) + (e / KB) * LDW] = v;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int mw = wid & 3, nw = wid >> 2;
+    double acc[PM][PN][2] = {};
+    const int kend = min((mw + 1) * PM * 8, (kw + 3) & ~3);  // T^T lower triangular
+    for (int k0 = 0; k0 < kend; k0 += 4) {
+        double av[PM], bv[PN];
+#pragma unroll
+        for (int i = 0; i < PM; ++i) av[i] = __ldg(T + (k0 + t4) + ((mw * PM + i) * 8 + g) * KB);
+#pragma unroll
+        for (int q = 0; q < PN; ++q) bv[q] = sW[(k0 + t4) + ((nw * PN + q) * 8 + g) * LDW];
+#pragma unroll
+        for (int i = 0; i < PM; ++i)
+#pragma unroll
+            for (int q = 0; q < PN; ++q) dmma(acc[i][q][0], acc[i][q][1], av[i], bv[q]);
+    }
+#pragma unroll
+    for (int i = 0; i < PM; ++i)
+#pragma unroll
+        for (int q = 0; q < PN; ++q) {
+            const int row = (mw * PM + i) * 8 + g, col = (nw * PN + q) * 8 + 2 * t4;
+            W0[row + col * KB] = acc[i][q][0];
+            W0[row + (col + 1) * KB] = acc[i][q][1];
+        }
+}
+
+// C(row tile, column tile) -= V W2
+template <int KB>
+__global__ void __launch_bounds__(256) k_cvw(double* __restrict__ a, int ld, long long stride, int m, int J0, int kw,
+                                             int cbeg, int cend, int rt, const double* __restrict__ wp, int nsl) {
+    constexpr int LDV = KB + 4, LDW = KB + 4;
+    const int t = blockIdx.x, rtile = blockIdx.y, b = blockIdx.z, ntile = gridDim.x;
+    double* A = a + b * stride;
+    const int rows = m - J0;
+    const int c0 = cbeg + t * TCG, nc = min(TCG, cend - c0);
+    const int rlo = rtile * rt, rhi = min(rows, rlo + rt);
+    if (rlo >= rhi) return;
+    extern __shared__ double dsm[];
+    double* sW = dsm;                                  // KB x TCG, ld LDW
+    double* const sV0 = dsm + TCG * LDW;                  // two V chunks: (row, refl) at refl + row*LDV
+    double* const sC0 = dsm + TCG * LDW + 2 * CHG * LDV;  // two C chunks, TCG * LDS_ each
+    const double* W2 = wp + (static_cast<long long>(b) * nsl * ntile + t) * (KB * TCG);
+    const int kwr = (kw + 3) & ~3;
+    for (int e = threadIdx.x; e < KB * TCG; e += 256) cp_async8(sW + (e % KB) + (e / KB) * LDW, W2 + e, true);
+    const int nchunk = (rhi - rlo + CHG - 1) / CHG;
+    auto issue = [&](int c) {
+        const int r0 = rlo + c * CHG, rc = min(CHG, rhi - r0);
+        double* vb = sV0 + (c & 1) * (CHG * LDV);
+        double* cb = sC0 + (c & 1) * (TCG * LDS_);
+        for (int e = threadIdx.x; e < CHG * kwr; e += 256) {
+            const int i = e % CHG, j = e / CHG, r = r0 + i;
+            double* dst = vb + j + i * LDV;
+            double v;
+            if (i >= rc) *dst = 0.0;
+            else if (v_direct(r, j, kw, v)) *dst = v;
+            else cp_async8(dst, A + (J0 + r) + static_cast<long long>(J0 + j) * ld, true);
+        }
+        for (int e = threadIdx.x; e < CHG * TCG; e += 256) {
+            const int i = e % CHG, j = e / CHG;
+            const bool ok = i < rc && j < nc;
+            cp_async8(cb + i + j * LDS_, ok ? A + (J0 + r0 + i) + static_cast<long long>(c0 + j) * ld : A, ok);
+        }
+        cp_commit();
+    };
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int rw = wid & 1, cw = wid >> 1;  // warp: rows rw*16..+16, cols cw*16..+16 of the chunk
+    issue(0);
+    for (int c = 0; c < nchunk; ++c) {
+        const int r0 = rlo + c * CHG, rc = min(CHG, rhi - r0);
+        if (c + 1 < nchunk) {
+            issue(c + 1);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        const double* sV = sV0 + (c & 1) * (CHG * LDV);
+        double* sC = sC0 + (c & 1) * (TCG * LDS_);
+        double o[2][2][2] = {};
+#pragma unroll 4
+        for (int k0 = 0; k0 < kwr; k0 += 4) {
+            double av[2], bv[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) av[i] = sV[(k0 + t4) + ((rw * 2 + i) * 8 + g) * LDV];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) bv[q] = sW[(k0 + t4) + ((cw * 2 + q) * 8 + g) * LDW];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) dmma(o[i][q][0], o[i][q][1], av[i], bv[q]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int row = (rw * 2 + i) * 8 + g, col = (cw * 2 + q) * 8 + 2 * t4;
+                sC[row + col * LDS_] -= o[i][q][0];
+                sC[row + (col + 1) * LDS_] -= o[i][q][1];
+            }
+        __syncthreads();
+        for (int e = threadIdx.x; e < CHG * TCG; e += 256) {
+            const int i = e % CHG, j = e / CHG;
+            if (i < rc && j < nc) A[(J0 + r0 + i) + static_cast<long long>(c0 + j) * ld] = sC[i + j * LDS_];
+        }
+        __syncthreads();
+    }
+}
+
+// C(128-row tile, 64-column tile) -= V(tile rows, 0:kw) W2(0:kw, tile columns):
+// a plain GEMM tile with K = kw <= KB.  Warps 4 (rows) x 2 (columns), warp tile
+// 32 x 32 (4 x 4 DMMA m8n8k4 tiles: 8 fragment loads per 16 DMMA).  V and W2
+// stream through two shared-memory stages of 32 reflectors (cp.async); C is
+// read and written straight from/to global memory in the accumulator layout
+// (each warp access covers 8 rows x 4 column pairs: whole 32-byte sectors).
+constexpr int CM = 128;          // rows per CTA
+constexpr int KC = 32;           // reflectors per stage
+constexpr int LDM = CM + 4;      // V stage: (row, refl) at row + refl * LDM
+constexpr int LDK = KC + 4;      // W2 stage: (refl, col) at refl + col * LDK
+template <int KB>
+__global__ void __launch_bounds__(256, 2) k_cvw2(double* __restrict__ a, int ld, long long stride, int m, int J0,
+                                                 int kw, int cbeg, int cend, const double* __restrict__ wp, int nsl) {
+    const int t = blockIdx.x, rtile = blockIdx.y, b = blockIdx.z, ntile = gridDim.x;
+    double* A = a + b * stride;
+    const int rows = m - J0;
+    const int c0 = cbeg + t * TCG, nc = min(TCG, cend - c0);
+    const int r0 = rtile * CM;
+    const double* W2 = wp + (static_cast<long long>(b) * nsl * ntile + t) * (KB * TCG);
+    extern __shared__ double dsm[];
+    double* const sV0 = dsm;                  // two stages of CM x KC
+    double* const sW0 = dsm + 2 * KC * LDM;   // two stages of KC x TCG
+    const int nst = (kw + KC - 1) / KC;
+    auto issue = [&](int s) {
+        double* vb = sV0 + (s & 1) * (KC * LDM);
+        double* wb = sW0 + (s & 1) * (TCG * LDK);
+        const int k0 = s * KC;
+        for (int e = threadIdx.x; e < CM * KC; e += 256) {
+            const int i = e % CM, j = e / CM, r = r0 + i, jj = k0 + j;
+            double* dst = vb + i + j * LDM;
+            double v;
+            if (r >= rows) *dst = 0.0;
+            else if (v_direct(r, jj, kw, v)) *dst = v;
+            else cp_async8(dst, A + (J0 + r) + static_cast<long long>(J0 + jj) * ld, true);
+        }
+        for (int e = threadIdx.x; e < KC * TCG; e += 256) {
+            const int j = e % KC, c = e / KC;
+            cp_async8(wb + j + c * LDK, W2 + (k0 + j) + c * KB, true);
+        }
+        cp_commit();
+    };
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int mw = wid & 3, nw = wid >> 2;
+    double acc[4][4][2] = {};
+    issue(0);
+    for (int s = 0; s < nst; ++s) {
+        if (s + 1 < nst) {
+            issue(s + 1);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        const double* sV = sV0 + (s & 1) * (KC * LDM);
+        const double* sW = sW0 + (s & 1) * (TCG * LDK);
+        const int kend = min(KC, ((kw - s * KC) + 3) & ~3);
+#pragma unroll 2
+        for (int k0 = 0; k0 < kend; k0 += 4) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = sV[(mw * 32 + i * 8 + g) + (k0 + t4) * LDM];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) bv[q] = sW[(k0 + t4) + (nw * 32 + q * 8 + g) * LDK];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) dmma(acc[i][q][0], acc[i][q][1], av[i], bv[q]);
+        }
+        __syncthreads();
+    }
+    // epilogue: C -= acc, in the accumulator layout (one row tile of 8 at a time)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = r0 + mw * 32 + i * 8 + g;
+        double* crow = A + (J0 + r) + static_cast<long long>(c0) * ld;
+        double cv[4][2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = nw * 32 + q * 8 + 2 * t4 + h;
+                cv[q][h] = (r < rows && c < nc) ? crow[static_cast<long long>(c) * ld] : 0.0;
+            }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = nw * 32 + q * 8 + 2 * t4 + h;
+                if (r < rows && c < nc) crow[static_cast<long long>(c) * ld] = cv[q][h] - acc[i][q][h];
+            }
+    }
+}
+constexpr size_t kCvw2Smem = sizeof(double) * (2 * KC * LDM + 2 * TCG * LDK);
+
+// Outer T (KO x KO) of an outer block whose four NB-column panels have compact-WY
+// factors T_q (written by the panel kernels), composed pairwise:
+//   H_A H_B = I - [V_A V_B] [T_A, -T_A (V_A^T V_B) T_B; 0, T_B] [V_A V_B]^T
+// first (0,1) and (2,3), then (01, 23).  V_A^T V_B are blocks of the Gram matrix
+// V^T V, summed over the row-slice partials of k_vtc in fixed order.  Same
+// matrix as accumulate_wy's column recurrence (dense_kernels.cpp:41-53), in
+// blocked order.
+__global__ void __launch_bounds__(256) k_tmerge(const double* __restrict__ wp, int nsl,
+                                                const double* __restrict__ Tin, long long tin_slot, int nq,
+                                                double* __restrict__ T_all) {
+    constexpr int LDT = KO + 1, ntile = KO / TCG;
+    const int b = blockIdx.x;
+    extern __shared__ double sm[];
+    double* sT = sm;                    // KO x KO, ld LDT
+    double* G01 = sT + KO * LDT;        // 32 x 32: G(0:32, 32:64)
+    double* G23 = G01 + 32 * 32;        // 32 x 32: G(64:96, 96:128)
+    double* GAB = G23 + 32 * 32;        // 64 x 64: G(0:64, 64:128)
+    double* X = GAB + 64 * 64;          // 64 x 64 scratch
+    const double* G0 = wp + static_cast<long long>(b) * nsl * ntile * (KO * TCG);
+    auto gram = [&](int i, int j) {     // G(i, j), partials in fixed order
+        double v = 0.0;
+        for (int s = 0; s < nsl; ++s) v += G0[(static_cast<long long>(s) * ntile + j / TCG) * (KO * TCG) + i + (j % TCG) * KO];
+        return v;
+    };
+    for (int e = threadIdx.x; e < KO * KO; e += 256) {
+        const int i = e % KO, j = e / KO, q = i / NB;
+        double v = 0.0;
+        if (q == j / NB && q < nq) v = Tin[q * tin_slot + static_cast<long long>(b) * NB * NB + (i % NB) + (j % NB) * NB];
+        sT[i + j * LDT] = v;
+    }
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+        const int i = e % 32, j = e / 32;
+        G01[e] = gram(i, 32 + j);
+        G23[e] = gram(64 + i, 96 + j);
+    }
+    for (int e = threadIdx.x; e < 64 * 64; e += 256) GAB[e] = gram(e % 64, 64 + e / 64);
+    __syncthreads();
+    // level 1: T(o, o+32) = -T_o G T_{o+32} for o = 0 (threads 0..127) and o = 64 (128..255)
+    {
+        const int h = threadIdx.x >> 7, tl = threadIdx.x & 127, o = 64 * h;
+        const double* G = h ? G23 : G01;
+        double* Xh = X + h * 1024;
+        for (int e = tl; e < 1024; e += 128) {  // Xh = G T_{o+32}  (T upper: l <= j)
+            const int i = e % 32, j = e / 32;
+            double s = 0.0;
+            for (int l = 0; l <= j; ++l) s = fma(G[i + l * 32], sT[(o + 32 + l) + (o + 32 + j) * LDT], s);
+            Xh[i + j * 32] = s;
+        }
+        __syncthreads();
+        for (int e = tl; e < 1024; e += 128) {  // T(o.., o+32..) = -T_o Xh  (T_o upper: l >= i)
+            const int i = e % 32, j = e / 32;
+            double s = 0.0;
+            for (int l = i; l < 32; ++l) s = fma(sT[(o + i) + (o + l) * LDT], Xh[l + j * 32], s);
+            sT[(o + i) + (o + 32 + j) * LDT] = -s;
+        }
+    }
+    __syncthreads();
+    // level 2: T(0:64, 64:128) = -T_A (G_AB T_B)
+    for (int e = threadIdx.x; e < 4096; e += 256) {
+        const int i = e % 64, j = e / 64;
+        double s = 0.0;
+        for (int l = 0; l <= j; ++l) s = fma(GAB[i + l * 64], sT[(64 + l) + (64 + j) * LDT], s);
+        X[i + j * 64] = s;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 4096; e += 256) {
+        const int i = e % 64, j = e / 64;
+        double s = 0.0;
+        for (int l = i; l < 64; ++l) s = fma(sT[i + l * LDT], X[l + j * 64], s);
+        sT[i + (64 + j) * LDT] = -s;
+    }
+    __syncthreads();
+    double* T = T_all + static_cast<long long>(b) * KO * KO;
+    for (int e = threadIdx.x; e < KO * KO; e += 256) T[e] = sT[(e % KO) + (e / KO) * LDT];
+}
+constexpr size_t kTmergeSmem = sizeof(double) * (KO * (KO + 1) + 2 * 32 * 32 + 2 * 64 * 64);
+
+size_t vtc_smem(int kb) { return sizeof(double) * (2 * kb * LDS_ + 2 * TCG * LDS_); }
+size_t cvw_smem(int kb) { return sizeof(double) * (TCG * (kb + 4) + 2 * CHG * (kb + 4) + 2 * TCG * LDS_); }
+
+// workspace for the partial W tiles and the outer T (grow-only, per process)
+struct BigWs {
+    double* p = nullptr;
+    size_t cap = 0;
+    double* get(size_t n) {
+        if (n > cap) {
+            if (p) cudaFree(p);
+            cudaMalloc(&p, sizeof(double) * n);
+            cap = n;
+        }
+        return p;
+    }
+};
+BigWs g_ws_w, g_ws_t;
+
+// block reflector (KB columns at J0, kw valid, T in T_all with ld KB) applied
+// to columns [cbeg, cend) of every problem; gram != 0 computes V^T V instead
+template <int KB>
+void apply_block(int nbatch, int m, int ld, long long stride, double* d_a, int J0, int kw, int cbeg, int cend,
+                 const double* T_all, cudaStream_t st, double* wp_out = nullptr, int* nsl_out = nullptr, int gram = 0) {
+    const int rows = m - J0;
+    const int ntile = (cend - cbeg + TCG - 1) / TCG;
+    if (ntile <= 0 || rows <= 0) return;
+    const int sms = sm_count();
+    // row slices: minimise (waves of resident CTAs) x (chunks per slice), two
+    // k_vtc CTAs per SM; fewer slices on ties (less partial-sum traffic)
+    const long long resident = 2LL * sms;
+    const int nchunks = (rows + CHG - 1) / CHG;
+    int nsl = 1;
+    long long best = -1;
+    for (int cand = 1; cand <= std::min(64, std::max(1, nchunks / 2)); ++cand) {
+        const int per = (nchunks + cand - 1) / cand;
+        const long long waves = (static_cast<long long>(ntile) * cand * nbatch + resident - 1) / resident;
+        const long long cost = waves * (per + 2);  // +2: fixed cost per CTA (prologue, partial write)
+        if (best < 0 || cost < best) {
+            best = cost;
+            nsl = cand;
+        }
+    }
+    const int rs = ((nchunks + nsl - 1) / nsl) * CHG;
+    nsl = (rows + rs - 1) / rs;
+    double* wp = g_ws_w.get(static_cast<size_t>(nbatch) * nsl * ntile * KB * TCG);
+    {
+        static size_t cfg = 0;
+        smem_optin(reinterpret_cast<const void*>(k_vtc<KB>), vtc_smem(KB), cfg);
+        k_vtc<KB><<<dim3(ntile, nsl, nbatch), 256, vtc_smem(KB), st>>>(d_a, ld, stride, m, J0, kw, cbeg, cend, rs, gram,
+                                                                         wp);
+    }
+    if (gram) {
+        *nsl_out = nsl;
+        (void)wp_out;
+        return;
+    }
+    {
+        static size_t cfg = 0;
+        const size_t sm = sizeof(double) * KB * 0 + sizeof(double) * (KB + 4) * TCG;
+        smem_optin(reinterpret_cast<const void*>(k_tw<KB>), sm, cfg);
+        k_tw<KB><<<dim3(ntile, nbatch), 256, sm, st>>>(wp, nsl, T_all, kw);
+    }
+    if (!std::getenv("SPQR_CVW1")) {
+        static size_t cfg = 0;
+        smem_optin(reinterpret_cast<const void*>(k_cvw2<KB>), kCvw2Smem, cfg);
+        k_cvw2<KB><<<dim3(ntile, (rows + CM - 1) / CM, nbatch), 256, kCvw2Smem, st>>>(d_a, ld, stride, m, J0, kw, cbeg,
+                                                                                   cend, wp, nsl);
+    } else {
+        const int rt = rows <= 512 ? ((rows + 1) / 2 + CHG - 1) / CHG * CHG : 256;
+        const int nrt = (rows + rt - 1) / rt;
+        static size_t cfg = 0;
+        smem_optin(reinterpret_cast<const void*>(k_cvw<KB>), cvw_smem(KB), cfg);
+        k_cvw<KB><<<dim3(ntile, nrt, nbatch), 256, cvw_smem(KB), st>>>(d_a, ld, stride, m, J0, kw, cbeg, cend,
+                                                                         std::max(rt, CHG), wp, nsl);
+    }
+}
+
 }  // namespace
 
 void blocked_qr_post(double* a, int ld, int m, int n, double* rout, int set_identity, int zero_lower, cudaStream_t st) {
@@ -554,8 +1244,8 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
     const int ldA = ld_in > 0 ? ld_in : m;
     const long long stride = static_cast<long long>(ldA) * ntot;
     const size_t smem_cap = 160 * 1024;
-    for (int j0 = 0; j0 < n; j0 += NB) {
-        const int w = std::min(NB, n - j0);
+    // panel j0..j0+w: V, tau, and the panel's T (NB x NB per problem) in d_T
+    auto panel = [&](int j0, int w, double* d_T) {
         const int rows = m - j0;
         // staged panel: (rows|1) x w plus v (rows); else in place with v in shared memory
         const int smem_rows = static_cast<int>(smem_cap / (sizeof(double) * (NB + 1))) - 2;
@@ -578,21 +1268,52 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
             smem_optin(reinterpret_cast<const void*>(k_panel2<16>), smem, cfg);
             k_panel2<16><<<nbatch, 512, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
         }
-        const int trail = ntot - (j0 + w);
-        if (trail > 0) {
-            dim3 grid((trail + TC2 - 1) / TC2, nbatch);
-            const size_t vsz = std::max(NB * LDV, CH * LDVT);
-            const size_t wsm = sizeof(double) * (2 * vsz + 2 * TC2 * LDC + TC2 * LDW + NB * LDW);
-            static const bool wy8 = std::getenv("SPQR_WY8") != nullptr;  // 8-warp variant: measured no faster
-            if (wy8) {
-                static size_t cfg = 0;
-                smem_optin(reinterpret_cast<const void*>(k_wy<8>), wsm, cfg);
-                k_wy<8><<<grid, 256, wsm, st>>>(d_a, ldA, stride, m, ntot, j0, w, d_T);
-            } else {
+    };
+    // one level (SPQR_QR_L1=1, kept for comparison): every NB panel updates all
+    // trailing columns in one CTA per column tile (k_wy)
+    const bool one_level = std::getenv("SPQR_QR_L1") != nullptr;
+    if (one_level || n <= NB) {
+        for (int j0 = 0; j0 < n; j0 += NB) {
+            const int w = std::min(NB, n - j0);
+            panel(j0, w, d_T);
+            const int trail = ntot - (j0 + w);
+            if (trail > 0) {
+                dim3 grid((trail + TC2 - 1) / TC2, nbatch);
+                const size_t vsz = std::max(NB * LDV, CH * LDVT);
+                const size_t wsm = sizeof(double) * (2 * vsz + 2 * TC2 * LDC + TC2 * LDW + NB * LDW);
                 static size_t cfg = 0;
                 smem_optin(reinterpret_cast<const void*>(k_wy<16>), wsm, cfg);
                 k_wy<16><<<grid, 512, wsm, st>>>(d_a, ldA, stride, m, ntot, j0, w, d_T);
             }
+        }
+    } else {
+        // two levels: NB panels inside KO-wide outer blocks, one KO-wide block
+        // reflector per outer block for the trailing columns
+        double* T_outer = g_ws_t.get(static_cast<size_t>(nbatch) * (KO * KO + (KO / NB) * NB * NB));
+        double* T_in = T_outer + static_cast<size_t>(nbatch) * KO * KO;  // KO/NB panel T slots
+        const long long slot = static_cast<long long>(nbatch) * NB * NB;
+        const bool reg_panel = !std::getenv("SPQR_SMEM_PANEL");
+        for (int J0 = 0; J0 < n; J0 += KO) {
+            const int kw2 = std::min(KO, n - J0);
+            for (int j0 = J0; j0 < J0 + kw2; j0 += NB) {
+                const int w = std::min(NB, J0 + kw2 - j0);
+                double* Tq = T_in + ((j0 - J0) / NB) * slot;
+                if (!(reg_panel && launch_panel_reg(nbatch, m, ldA, stride, d_a, j0, w, d_tau, n, Tq, st)))
+                    panel(j0, w, Tq);
+                if (j0 + w < J0 + kw2)
+                    apply_block<NB>(nbatch, m, ldA, stride, d_a, j0, w, j0 + w, J0 + kw2, Tq, st);
+            }
+            if (J0 + kw2 >= ntot) continue;
+            if (kw2 <= NB) {
+                apply_block<NB>(nbatch, m, ldA, stride, d_a, J0, kw2, J0 + kw2, ntot, T_in, st);
+                continue;
+            }
+            int nsl = 1;
+            apply_block<KO>(nbatch, m, ldA, stride, d_a, J0, kw2, J0, J0 + KO, nullptr, st, nullptr, &nsl, 1);
+            static size_t cfg = 0;
+            smem_optin(reinterpret_cast<const void*>(k_tmerge), kTmergeSmem, cfg);
+            k_tmerge<<<nbatch, 256, kTmergeSmem, st>>>(g_ws_w.p, nsl, T_in, slot, (kw2 + NB - 1) / NB, T_outer);
+            apply_block<KO>(nbatch, m, ldA, stride, d_a, J0, kw2, J0 + kw2, ntot, T_outer, st);
         }
     }
     dim3 g2((ntot + 255) / 256, nbatch);

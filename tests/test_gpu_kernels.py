@@ -13,7 +13,7 @@ def _P():
     return P
 
 
-@pytest.mark.parametrize("path", ["auto", "smem", "blocked", "tile_dmma"])
+@pytest.mark.parametrize("path", ["auto", "smem", "blocked", "blocked_l1", "tile_dmma"])
 @pytest.mark.parametrize("shape", [(1, 1, 1), (5, 3, 3), (20, 7, 30), (40, 12, 60), (128, 32, 288), (300, 64, 96),
                                    (300, 40, 140), (513, 70, 200), (512, 128, 384),
                                    # column-tiled path: many tiles, panel only, square panel, m > 256
@@ -21,7 +21,10 @@ def _P():
                                    # dynamic smem just under 48 KB: static + dynamic needs the opt-in
                                    (129, 47, 150),
                                    # tall panels: thread-block-cluster panel factorisation (mbqr.cu)
-                                   (1500, 40, 100), (4096, 33, 60)])
+                                   (1500, 40, 100), (4096, 33, 60),
+                                   # two-level blocking: 128-wide outer blocks (ragged last block,
+                                   # a one-column outer block, no trailing columns, cluster panels)
+                                   (700, 200, 330), (520, 129, 140), (300, 160, 160), (1300, 140, 180)])
 def test_qr_apply_matches_oracle(shape, path, monkeypatch):
     """auto = column-tiled kernel where the panel fits in shared memory (qr_tile.cu);
     tile_dmma = the same with its DMMA compact-WY tile phase; smem = whole block staged per
