@@ -554,7 +554,7 @@ __global__ void k_qr_post(double* __restrict__ a, int ld, int m, int n, double* 
 // dense_kernels.cpp:41-53).  With CS > 1 each CTA pushes its partial sums into
 // every CTA's shared memory (remote stores), one cluster barrier per reduction,
 // and every CTA adds the CS partials in rank order (double-buffered by parity).
-template <int NW, int RR, int CS>
+template <int NW, int RR, int CS, bool UNR>
 __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, long long stride, int m, int j0, int w,
                                                double* __restrict__ tau_all, int tau_stride,
                                                double* __restrict__ T_all) {
@@ -580,15 +580,22 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
             x[q][j] = (row[q] < rows && j < w) ? A[(j0 + row[q]) + static_cast<long long>(j0 + j) * ld] : 0.0;
     for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) Ts[e] = 0.0;
     const int kmax = min(w, rows);
-#pragma unroll
+    // UNR: reflector loop fully unrolled (column k static).  Otherwise column k is
+    // read and written through select chains (a much smaller loop body: the
+    // unrolled one overflows the instruction cache)
+#pragma unroll UNR ? NB : 1
     for (int k = 0; k < NB; ++k) {
         if (k < kmax) {
             const int par = k & 1;
             double s = 0.0;
+            double xk[RR];
 #pragma unroll
             for (int q = 0; q < RR; ++q) {
-                if (row[q] > k) s = fma(x[q][k], x[q][k], s);
-                if (row[q] == k) s_c0 = x[q][k];
+                xk[q] = x[q][0];
+#pragma unroll
+                for (int j = 1; j < NB; ++j) xk[q] = (j == k) ? x[q][j] : xk[q];
+                if (row[q] > k) s = fma(xk[q], xk[q], s);
+                if (row[q] == k) s_c0 = xk[q];
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -626,9 +633,10 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
             double v[RR];
 #pragma unroll
             for (int q = 0; q < RR; ++q) {
-                if (row[q] > k) x[q][k] *= rden;
-                if (row[q] == k) x[q][k] = beta;
-                v[q] = row[q] > k ? x[q][k] : (row[q] == k ? 1.0 : 0.0);
+                const double nv = row[q] > k ? xk[q] * rden : (row[q] == k ? beta : xk[q]);
+#pragma unroll
+                for (int j = 0; j < NB; ++j) x[q][j] = (j == k) ? nv : x[q][j];
+                v[q] = row[q] > k ? nv : (row[q] == k ? 1.0 : 0.0);
             }
             if (rank == 0 && threadIdx.x == 0) tau_all[static_cast<long long>(b) * tau_stride + j0 + k] = t;
             // p[j] = sum over this thread's rows of v x_j (column k itself is not needed),
@@ -642,8 +650,8 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
                 double lo = 0.0, hi = 0.0;
 #pragma unroll
                 for (int q = 0; q < RR; ++q) {
-                    if (i != k) lo = fma(v[q], x[q][i], lo);
-                    if (i + 16 != k) hi = fma(v[q], x[q][i + 16], hi);
+                    lo = fma(v[q], x[q][i], lo);  // column k's own sum is never used
+                    hi = fma(v[q], x[q][i + 16], hi);
                 }
                 const double send = up16 ? lo : hi;
                 const double keep = up16 ? hi : lo;
@@ -677,9 +685,9 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
                 for (int r = 0; r < CS; ++r) wl += dots[par][r][lane];
             }
             if (t != 0.0) {
-                const double twl = -t * wl;
+                const double twl = lane > k ? -t * wl : 0.0;
 #pragma unroll
-                for (int j = k + 1; j < NB; ++j) {
+                for (int j = UNR ? k + 1 : 1; j < NB; ++j) {
                     const double tw = __shfl_sync(0xffffffffu, twl, j);
 #pragma unroll
                     for (int q = 0; q < RR; ++q) x[q][j] = fma(tw, v[q], x[q][j]);
@@ -720,14 +728,14 @@ template <int NW, int RR>
 __global__ void __launch_bounds__(32 * NW, NW * RR <= 8 ? 2 : 1) k_panel_row(double* a, int ld, long long stride,
                                                                            int m, int j0, int w, double* tau_all,
                                                                            int tau_stride, double* T_all) {
-    panel_row_body<NW, RR, 1>(a, ld, stride, m, j0, w, tau_all, tau_stride, T_all);
+    panel_row_body<NW, RR, 1, true>(a, ld, stride, m, j0, w, tau_all, tau_stride, T_all);
 }
 
 template <int NW, int RR>
 __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(32 * NW, NW * RR <= 8 ? 2 : 1)
     k_panel_rowc(double* a, int ld, long long stride, int m, int j0, int w, double* tau_all, int tau_stride,
                  double* T_all) {
-    panel_row_body<NW, RR, kCS>(a, ld, stride, m, j0, w, tau_all, tau_stride, T_all);
+    panel_row_body<NW, RR, kCS, true>(a, ld, stride, m, j0, w, tau_all, tau_stride, T_all);
 }
 
 // register-resident panel launch; false when the panel is too tall
@@ -744,8 +752,7 @@ bool launch_panel_reg(int nbatch, int m, int ld, long long stride, double* d_a, 
     if (per <= 64) SPQR_PANEL(2, 1);
     else if (per <= 128) SPQR_PANEL(4, 1);
     else if (per <= 256) SPQR_PANEL(8, 1);
-    else if (std::getenv("SPQR_PANEL_RR2")) SPQR_PANEL(8, 2);
-    else SPQR_PANEL(16, 1);
+    else SPQR_PANEL(8, 2);
 #undef SPQR_PANEL
     return true;
 }
@@ -1003,6 +1010,15 @@ __global__ void __launch_bounds__(256, 2) k_cvw2(double* __restrict__ a, int ld,
     double* const sV0 = dsm;                  // two stages of CM x KC
     double* const sW0 = dsm + 2 * KC * LDM;   // two stages of KC x TCG
     const int nst = (kw + KC - 1) / KC;
+    {  // pull this CTA's C tile into L2 while the stages run (read in the epilogue)
+        const int e = threadIdx.x;  // 256 threads: column e / 4, 32-row quarter e % 4
+        const int c = e >> 2, rq = (e & 3) * 32;
+        if (c < nc && r0 + rq < rows) {
+            const double* pc = A + (J0 + r0 + rq) + static_cast<long long>(c0 + c) * ld;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pc));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + 16));
+        }
+    }
     auto issue = [&](int s) {
         double* vb = sV0 + (s & 1) * (KC * LDM);
         double* wb = sW0 + (s & 1) * (TCG * LDK);
