@@ -107,6 +107,9 @@ int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, doubl
  * (rank x n, ld = kmax, original column order), V[b*m*kmax..] (ld = m), tau, sign. */
 int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* rank, double* r11, int* perm,
                       double* R, double* V, double* tau, double* sign);
+/* Same on device data, in place (R rows over the leading rank rows of each problem), ranks to
+ * d_rank; *ms = device time of the launches (the C5 microbenchmark's CPQR leg). */
+int spqr_cpqr_batched_dev(int nb, int m, int n, double* d_a, double eps, int* d_rank, float* ms);
 /* tri_solve_upper(R, B, Right, false) (dense_kernels.cpp:242-257): B (nrows x n) <- B R^{-1}
  * for nb problems packed back to back; R (n x n) per problem. */
 int spqr_trsm_right_batched(int nb, int nrows, int n, double* b, const double* r);

@@ -49,6 +49,7 @@ SIGNATURES = {
     "spqr_qr_apply_batched": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, f64p, f64p, f64p, i32p]),
     "spqr_qr_apply_batched_dev": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp,
                                             C.POINTER(C.c_float)]),
+    "spqr_cpqr_batched_dev": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, C.c_double, vp, C.POINTER(C.c_float)]),
     "spqr_cpqr_batched": (C.c_int, [C.c_int, C.c_int, C.c_int, f64p, C.c_double, i32p, f64p, i32p, f64p, f64p,
                                     f64p, f64p]),
     "spqr_trsm_right_batched": (C.c_int, [C.c_int, C.c_int, C.c_int, f64p, f64p]),

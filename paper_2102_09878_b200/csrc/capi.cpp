@@ -530,6 +530,62 @@ int spqr_qr_apply_batched(int nb, int m, int n, int ntot, double* a, double* tau
     });
 }
 
+namespace {
+// truncated CPQR of nb packed m x n problems already on the device (in place);
+// per-problem outputs into the caller's device buffers; device time of the
+// launches (events on the default stream) into *ms when given
+void cpqr_dev_run(DeviceArena& mem, int nb, int m, int n, double* da, double eps, int* dr, double* d11, int* dp,
+                  double* dV, double* dt, double* ds, float* ms) {
+    const int kmax = std::min(m, n);
+    const bool big = 8ull * m * n > kBigCpqrBytes && m >= 32 && cpqr_big_smem_bytes(m, n) <= 200 * 1024;
+    const size_t wstride = big ? cpqr_big_work_doubles(n) : 3 * static_cast<size_t>(n);
+    double* work = mem.alloc_n<double>(std::max<size_t>(static_cast<size_t>(nb) * wstride, 1));
+    CK(cudaMemset(dV, 0, sizeof(double) * static_cast<size_t>(nb) * m * kmax));
+    std::vector<CpqrDesc> cd(nb);
+    for (int b = 0; b < nb; ++b)
+        cd[b] = CpqrDesc{da + static_cast<long long>(b) * m * n, m, m, n, eps, dr + b, d11 + b,
+                         dV + static_cast<long long>(b) * m * kmax, m, dt + b * kmax, ds + b * kmax, dp + b * kmax,
+                         work + static_cast<long long>(b) * wstride};
+    CpqrDesc* dc = mem.alloc_n<CpqrDesc>(std::max(nb, 1));
+    CK(cudaMemcpy(dc, cd.data(), sizeof(CpqrDesc) * nb, cudaMemcpyHostToDevice));
+    std::vector<int> all(nb);
+    for (int b = 0; b < nb; ++b) all[b] = b;
+    int* didx = mem.alloc_n<int>(std::max(nb, 1));
+    CK(cudaMemcpy(didx, all.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
+    const size_t sm = cpqr_smem_bytes(m, n);
+    const char* force = std::getenv("SPQR_CPQR_PATH");  // narrow|smem|big (comparisons, tests)
+    const std::string fp = force ? force : "";
+    const int ncls = (fp.empty() || fp == "narrow") ? cpqr_narrow_class(m, n) : -1;
+    const int tcls = (fp.empty() || fp == "tall") ? cpqr_tall_class(m, n) : -1;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ms) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventRecord(e0, 0));
+    }
+    if (ncls >= 0)
+        launch_cpqr_narrow(ncls, dc, didx, nb, cpqr_narrow_smem(m, n), 0);
+    else if (tcls >= 0)
+        launch_cpqr_tall(tcls, dc, didx, nb, 0);
+    else if (big)
+        for (int b = 0; b < nb; ++b) launch_cpqr_big(cd[b], 0);
+    else if (sm <= kSmemBudget)
+        launch_cpqr_split(dc, didx, nb, sm, nullptr, 0, m, 0);
+    else
+        launch_cpqr_split(dc, nullptr, 0, 0, didx, nb, m, 0);
+    if (ms) {
+        CK(cudaEventRecord(e1, 0));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    CK(cudaDeviceSynchronize());
+    CK(cudaGetLastError());
+}
+}  // namespace
+
 int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* rank, double* r11, int* perm, double* R,
                       double* V, double* tau, double* sign) {
     int cl = -1;
@@ -544,36 +600,8 @@ int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* ra
         int* dp = mem.alloc_n<int>(std::max(nb * kmax, 1));
         int* dr = mem.alloc_n<int>(std::max(nb, 1));
         double* d11 = mem.alloc_n<double>(std::max(nb, 1));
-        const bool big = 8ull * m * n > kBigCpqrBytes && m >= 32 && cpqr_big_smem_bytes(m, n) <= 200 * 1024;
-        const size_t wstride = big ? cpqr_big_work_doubles(n) : 3 * static_cast<size_t>(n);
-        double* work = mem.alloc_n<double>(std::max<size_t>(static_cast<size_t>(nb) * wstride, 1));
         CK(cudaMemcpy(da, a, sizeof(double) * na, cudaMemcpyHostToDevice));
-        CK(cudaMemset(dV, 0, sizeof(double) * static_cast<size_t>(nb) * m * kmax));
-        std::vector<CpqrDesc> cd(nb);
-        for (int b = 0; b < nb; ++b)
-            cd[b] = CpqrDesc{da + static_cast<long long>(b) * m * n, m, m, n, eps, dr + b, d11 + b,
-                             dV + static_cast<long long>(b) * m * kmax, m, dt + b * kmax, ds + b * kmax, dp + b * kmax,
-                             work + static_cast<long long>(b) * wstride};
-        CpqrDesc* dc = mem.alloc_n<CpqrDesc>(std::max(nb, 1));
-        CK(cudaMemcpy(dc, cd.data(), sizeof(CpqrDesc) * nb, cudaMemcpyHostToDevice));
-        std::vector<int> all(nb);
-        for (int b = 0; b < nb; ++b) all[b] = b;
-        int* didx = mem.alloc_n<int>(std::max(nb, 1));
-        CK(cudaMemcpy(didx, all.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
-        const size_t sm = cpqr_smem_bytes(m, n);
-        const char* force = std::getenv("SPQR_CPQR_PATH");  // narrow|smem|big (comparisons, tests)
-        const std::string fp = force ? force : "";
-        const int ncls = (fp.empty() || fp == "narrow") ? cpqr_narrow_class(m, n) : -1;
-        if (ncls >= 0)
-            launch_cpqr_narrow(ncls, dc, didx, nb, cpqr_narrow_smem(m, n), 0);
-        else if (big)
-            for (int b = 0; b < nb; ++b) launch_cpqr_big(cd[b], 0);
-        else if (sm <= kSmemBudget)
-            launch_cpqr_split(dc, didx, nb, sm, nullptr, 0, m, 0);
-        else
-            launch_cpqr_split(dc, nullptr, 0, 0, didx, nb, m, 0);
-        CK(cudaDeviceSynchronize());
-        CK(cudaGetLastError());
+        cpqr_dev_run(mem, nb, m, n, da, eps, dr, d11, dp, dV, dt, ds, nullptr);
         std::vector<double> A(na);
         CK(cudaMemcpy(A.data(), da, sizeof(double) * na, cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(rank, dr, sizeof(int) * nb, cudaMemcpyDeviceToHost));
@@ -588,6 +616,22 @@ int spqr_cpqr_batched(int nb, int m, int n, const double* a, double eps, int* ra
             for (int j = 0; j < n; ++j)
                 for (int i = 0; i < kmax; ++i) Rb[i + static_cast<long long>(j) * kmax] = i < rank[b] ? Ab[i + static_cast<long long>(j) * m] : 0.0;
         }
+    });
+}
+
+int spqr_cpqr_batched_dev(int nb, int m, int n, double* d_a, double eps, int* d_rank, float* ms) {
+    int cl = -1;
+    return guarded(nullptr, 0, &cl, [&] {
+        const int kmax = std::min(m, n);
+        DeviceArena mem;
+        double* dV = mem.alloc_n<double>(std::max<size_t>(static_cast<size_t>(nb) * m * kmax, 1));
+        double* dt = mem.alloc_n<double>(std::max(nb * kmax, 1));
+        double* ds = mem.alloc_n<double>(std::max(nb * kmax, 1));
+        int* dp = mem.alloc_n<int>(std::max(nb * kmax, 1));
+        double* d11 = mem.alloc_n<double>(std::max(nb, 1));
+        float t = 0.f;
+        cpqr_dev_run(mem, nb, m, n, d_a, eps, d_rank, d11, dp, dV, dt, ds, &t);
+        if (ms) *ms = t;
     });
 }
 

@@ -276,6 +276,289 @@ __global__ void __launch_bounds__(kThreads) k_cpqr_narrow(const CpqrDesc* __rest
     }
 }
 
+// Truncated CPQR for taller blocks (128 < m <= 32 RPL, n <= 2048), in place in
+// global memory, one CTA per problem, warp per column.  Same semantics as
+// k_cpqr_narrow (first maximum by logical position, exact-norm stop rule with
+// one refresh and retry, Householder alpha = -sign+(x0)||x||, row flip, LAPACK
+// norm downdate with recompute below sqrt(eps)).  Column state (downdated
+// norms, logical positions) lives in shared memory; every warp recomputes the
+// pivot's Householder vector from the (L1-resident) pivot column with lane =
+// row, keeps v in registers, and sweeps columns w, w + 8, ...: coalesced
+// loads of the column, warp-shuffle dot product, update, store.  Two block
+// barriers per pivot (argmax partials; column data and state visible to the
+// next step).
+constexpr int kTallMaxN = 2048;
+template <int RPL, int CPW>
+__global__ void __launch_bounds__(kThreads, 2) k_cpqr_tall(const CpqrDesc* __restrict__ ds, const int* __restrict__ idx) {
+    const CpqrDesc d = ds[idx[blockIdx.x]];
+    const int m = d.m, n = d.n, kmax = min(m, n);
+    const long long ld = d.ld;
+    double* A = d.a;
+    __shared__ double s_vn1[kTallMaxN], s_vn2[kTallMaxN];
+    __shared__ int s_lpos[kTallMaxN];
+    __shared__ double pv[2][kNW];
+    __shared__ int pj[2][kNW], pp[2][kNW];
+    __shared__ double s_akk[kNW];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (kmax == 0) {
+        if (tid == 0) {
+            *d.rank = 0;
+            *d.r11 = 0.0;
+        }
+        return;
+    }
+    const double tol3z = sqrt(DBL_EPSILON);
+    // exact column norms, warp per column
+    for (int p = wid; p < n; p += kNW) {
+        const double* a = A + p * ld;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int i = lane + 32 * q;
+            if (i < m) s = fma(a[i], a[i], s);
+        }
+        s = wsum(s);
+        if (lane == 0) {
+            s_vn1[p] = s_vn2[p] = sqrt(s);
+            s_lpos[p] = p;
+        }
+    }
+    __syncthreads();
+    int buf = 0;
+    auto argmax = [&](int k0, double& bv, int& bj, int& bp) {
+        bv = -1.0;
+        bj = INT_MAX;
+        bp = -1;
+        for (int p = tid; p < n; p += kThreads) {
+            const int lp = s_lpos[p];
+            if (lp >= k0 && better(s_vn1[p], lp, bv, bj)) {
+                bv = s_vn1[p];
+                bj = lp;
+                bp = p;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+            if (better(ov, oj, bv, bj)) {
+                bv = ov;
+                bj = oj;
+                bp = op;
+            }
+        }
+        if (lane == 0) {
+            pv[buf][wid] = bv;
+            pj[buf][wid] = bj;
+            pp[buf][wid] = bp;
+        }
+        __syncthreads();
+        bv = -1.0;
+        bj = INT_MAX;
+        bp = -1;
+#pragma unroll
+        for (int g = 0; g < kNW; ++g)
+            if (better(pv[buf][g], pj[buf][g], bv, bj)) {
+                bv = pv[buf][g];
+                bj = pj[buf][g];
+                bp = pp[buf][g];
+            }
+        buf ^= 1;
+    };
+    auto tail_sumsq = [&](int p, int r0) {
+        const double* a = A + p * ld;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int i = lane + 32 * q;
+            if (i >= r0 && i < m) s = fma(a[i], a[i], s);
+        }
+        return wsum(s);
+    };
+    double r11 = 0.0;
+    int k = 0;
+    int prev_pc = -1, prev_k = -1;
+    double prev_alpha = 0.0;
+    bool prev_reflect = false, prev_flip = false;
+    auto finalise = [&]() {  // warp 0 writes alpha e1 into the previous pivot column
+        if (prev_pc >= 0 && wid == 0) {
+            double* ap = A + prev_pc * ld;
+            if (prev_reflect) {
+#pragma unroll
+                for (int q = 0; q < RPL; ++q) {
+                    const int i = lane + 32 * q;
+                    if (i == prev_k) ap[i] = prev_flip ? -prev_alpha : prev_alpha;
+                    else if (i > prev_k && i < m) ap[i] = 0.0;
+                }
+            } else if (prev_flip && lane == 0) {
+                ap[prev_k] = -ap[prev_k];
+            }
+        }
+        prev_pc = -1;
+    };
+    while (k < kmax) {
+        double bv;
+        int piv, pc;
+        argmax(k, bv, piv, pc);  // its barrier also orders the previous step's column updates
+        finalise();
+        double x0 = A[k + pc * ld];
+        double tail = tail_sumsq(pc, k + 1);
+        double exact = sqrt(fma(x0, x0, tail));
+        bool stop = (k == 0) ? !(exact > 0.0) : (d.eps > 0.0 && exact < d.eps * r11);
+        if (stop && k > 0) {  // refresh every trailing norm and retry once
+            __syncthreads();  // finalise() visible before the column walks
+            for (int p = wid; p < n; p += kNW) {
+                if (s_lpos[p] < k) continue;
+                const double* a = A + p * ld;
+                double s = 0.0;
+#pragma unroll
+                for (int q = 0; q < RPL; ++q) {
+                    const int i = lane + 32 * q;
+                    if (i >= k && i < m) s = fma(a[i], a[i], s);
+                }
+                s = wsum(s);
+                if (lane == 0) s_vn1[p] = s_vn2[p] = sqrt(s);
+            }
+            __syncthreads();
+            argmax(k, bv, piv, pc);
+            exact = bv;
+            stop = d.eps > 0.0 && exact < d.eps * r11;
+            if (!stop) {
+                x0 = A[k + pc * ld];
+                tail = tail_sumsq(pc, k + 1);
+            }
+        }
+        if (stop) break;
+        double alpha = sqrt(fma(x0, x0, tail));
+        if (x0 > 0.0) alpha = -alpha;
+        const double v0 = x0 - alpha;
+        const double vns = fma(v0, v0, tail);
+        const bool reflect = vns > 0.0;
+        const double t = reflect ? 2.0 / vns : 0.0;
+        const bool flip = (reflect ? alpha : x0) < 0.0;
+        double v[RPL];
+        {
+            const double* ap = A + pc * ld;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+                const int i = lane + 32 * q;
+                v[q] = (i < k || i >= m) ? 0.0 : (i == k ? v0 : ap[i]);
+            }
+        }
+        if (wid == 0 && d.V) {
+            double* vk = d.V + static_cast<long long>(k) * d.ldv;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+                const int i = lane + 32 * q;
+                if (i < m) vk[i] = i < k ? 0.0 : (i == k ? 1.0 : (reflect ? v[q] / v0 : 0.0));
+            }
+        }
+        if (tid == 0) {
+            if (d.tau) d.tau[k] = reflect ? t * v0 * v0 : 0.0;
+            if (d.sign) d.sign[k] = flip ? -1.0 : 1.0;
+            if (d.perm) d.perm[k] = pc;
+        }
+        if (k == 0) r11 = fabs(reflect ? alpha : x0);
+        // trailing columns (logical position > k after the swap k <-> piv), warp per column;
+        // the swap itself is written by the column's warp (the pivot's by warp 0)
+        if (tid == 0) s_lpos[pc] = k;
+        // CPW columns per warp iteration: their loads and reductions overlap
+        for (int p0 = wid; p0 < n; p0 += kNW * CPW) {
+            bool act[CPW];
+            double x[CPW][RPL];
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) {
+                const int p = p0 + kNW * c;
+                const int lp = p < n ? s_lpos[p] : -1;
+                act[c] = p < n && p != pc && lp >= k;
+                if (act[c] && lp == k && lane == 0) s_lpos[p] = piv;
+                const double* a = A + (act[c] ? p : 0) * ld;
+#pragma unroll
+                for (int q = 0; q < RPL; ++q) {
+                    const int i = lane + 32 * q;
+                    x[c][q] = (act[c] && i >= k && i < m) ? a[i] : 0.0;
+                }
+            }
+            if (reflect) {
+                double sc[CPW];
+#pragma unroll
+                for (int c = 0; c < CPW; ++c) {
+                    sc[c] = 0.0;
+#pragma unroll
+                    for (int q = 0; q < RPL; ++q) sc[c] = fma(v[q], x[c][q], sc[c]);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int c = 0; c < CPW; ++c) sc[c] += __shfl_xor_sync(0xffffffffu, sc[c], o);
+#pragma unroll
+                for (int c = 0; c < CPW; ++c) {
+                    const double tw = -t * sc[c];
+#pragma unroll
+                    for (int q = 0; q < RPL; ++q) x[c][q] = fma(tw, v[q], x[c][q]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) {
+                if (act[c]) {  // warp-uniform
+                const int p = p0 + kNW * c;
+                double* a = A + p * ld;
+                // row k (lane k % 32 of slot k / 32), flipped when the pivot's diagonal is negative
+                // (through shared memory: selecting x[c][k / 32] in registers turns into a
+                // dynamically indexed local array)
+#pragma unroll
+                for (int q = 0; q < RPL; ++q)
+                    if (lane + 32 * q == k) s_akk[wid] = x[c][q];
+                __syncwarp();
+                double akk = s_akk[wid];
+                __syncwarp();
+                if (flip) akk = -akk;
+#pragma unroll
+                for (int q = 0; q < RPL; ++q) {
+                    const int i = lane + 32 * q;
+                    if (i == k) x[c][q] = akk;
+                    if (i >= k && i < m && (reflect || i == k)) a[i] = x[c][q];
+                }
+                if (k + 1 < kmax) {
+                    const double vn1 = s_vn1[p];
+                    if (vn1 != 0.0) {
+                        double qq = fabs(akk) / vn1;
+                        qq = fmax(0.0, (1.0 - qq) * (1.0 + qq));
+                        const double ratio = vn1 / s_vn2[p];
+                        if (qq * ratio * ratio <= tol3z) {
+                            double s2 = 0.0;
+#pragma unroll
+                            for (int q = 0; q < RPL; ++q) {
+                                const int i = lane + 32 * q;
+                                if (i > k && i < m) s2 = fma(x[c][q], x[c][q], s2);
+                            }
+                            s2 = wsum(s2);
+                            if (lane == 0) s_vn1[p] = s_vn2[p] = sqrt(s2);
+                        } else if (lane == 0) {
+                            s_vn1[p] = vn1 * sqrt(qq);
+                        }
+                    }
+                }
+                }
+            }
+        }
+        prev_pc = pc;
+        prev_k = k;
+        prev_alpha = alpha;
+        prev_reflect = reflect;
+        prev_flip = flip;
+        ++k;
+        __syncthreads();  // column data and state visible to the next scan
+    }
+    __syncthreads();
+    finalise();
+    if (tid == 0) {
+        *d.rank = k;
+        *d.r11 = r11;
+    }
+}
+
 template <int RPL, bool GLB, int NC>
 void launch_narrow(const CpqrDesc* d, const int* idx, int cnt, size_t smem, cudaStream_t st) {
     static size_t configured = 0;
@@ -305,6 +588,20 @@ int cpqr_narrow_class(int m, int n) {
     if (m < 1 || m > 128 || n > 2048) return -1;
     const int r = m <= 32 ? 0 : (m <= 64 ? 1 : 2);
     return (n > 1024 ? 6 : 0) + (cpqr_narrow_smem(m, n) <= kNarrowSmem ? r : 3 + r);
+}
+
+// taller blocks, in place: class 0 (m <= 256), 1 (m <= 512); -1 not eligible
+int cpqr_tall_class(int m, int n) {
+    if (m <= 128 || m > 512 || n > kTallMaxN) return -1;
+    return m <= 256 ? 0 : 1;
+}
+
+void launch_cpqr_tall(int cls, const CpqrDesc* d_desc, const int* d_idx, int cnt, cudaStream_t st) {
+    if (cnt <= 0) return;
+    if (cls == 0)
+        k_cpqr_tall<8, 4><<<cnt, kThreads, 0, st>>>(d_desc, d_idx);
+    else
+        k_cpqr_tall<16, 2><<<cnt, kThreads, 0, st>>>(d_desc, d_idx);
 }
 
 void launch_cpqr_narrow(int cls, const CpqrDesc* d_desc, const int* d_idx, int cnt, size_t smem, cudaStream_t st) {

@@ -200,6 +200,9 @@ std::vector<int4> qr_tile_plan(const QrDesc* hq, const int* idx, int cnt, int sm
 int cpqr_narrow_class(int m, int n);
 size_t cpqr_narrow_smem(int m, int n);
 void launch_cpqr_narrow(int cls, const CpqrDesc* d_desc, const int* d_idx, int cnt, size_t smem, cudaStream_t st);
+// taller blocks (128 < m <= 512, n <= 2048), in place, warp per column (cpqr_narrow.cu)
+int cpqr_tall_class(int m, int n);
+void launch_cpqr_tall(int cls, const CpqrDesc* d_desc, const int* d_idx, int cnt, cudaStream_t st);
 void launch_cpqr_big(const CpqrDesc& d, cudaStream_t st);
 size_t cpqr_big_smem_bytes(int m, int n);  // dynamic smem of one launch (<= 200 KB to be eligible)
 inline size_t cpqr_big_work_doubles(int n) { return 3 * static_cast<size_t>(n) + 2 * 512 + 16; }

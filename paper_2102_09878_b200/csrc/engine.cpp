@@ -720,6 +720,7 @@ private:
         // Move the largest problems to the cooperative kernel while that lowers
         // the estimated batch time.
         std::vector<int> glob;
+        std::vector<int> tall[2];
         std::vector<std::vector<int>> narrow(12);
         std::vector<char> coop(cd.size(), 0), nar(cd.size(), 0);
         static const bool no_narrow = std::getenv("SPQR_NO_NARROW") != nullptr;
@@ -822,13 +823,26 @@ private:
                 kt_.end(K_CPQR, e0, st_, 16.0 * d.m * d.n);
                 continue;
             }
+            static const bool no_tall = std::getenv("SPQR_NO_TALL") != nullptr;
+            const int tc = no_tall ? -1 : cpqr_tall_class(cd[i].m, cd[i].n);
             if (b <= kSmemBudget) {
                 small.push_back(static_cast<int>(i));
                 smem = std::max(smem, b);
+            } else if (tc >= 0) {  // 128 < m <= 512: warp-per-column kernel, in place
+                tall[tc].push_back(static_cast<int>(i));
             } else {
                 large.push_back(static_cast<int>(i));
                 maxm = std::max(maxm, cd[i].m);
             }
+        }
+        for (int c = 0; c < 2; ++c) {
+            if (tall[c].empty()) continue;
+            const int* dt = u.put(tall[c]);
+            double tb = 0;
+            for (int i : tall[c]) tb += 16.0 * cd[i].m * cd[i].n;
+            cudaEvent_t e0 = kt_.begin(st_);
+            launch_cpqr_tall(c, dc, dt, static_cast<int>(tall[c].size()), st_);
+            kt_.end(K_CPQR, e0, st_, tb);
         }
         const int* ds = u.put(small);
         const int* dl = u.put(large);

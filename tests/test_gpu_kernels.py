@@ -89,9 +89,12 @@ def test_qr_flags_singular_pivot():
                                        # short-wide sparsify_cols blocks (cpqr_narrow.cu)
                                        ((11, 475), 1e-2), ((33, 1000), 1e-2), ((1, 50), 1e-2), ((64, 300), 0.0),
                                        ((100, 200), 1e-2), ((84, 448), 1e-2), ((128, 700), 1e-3),
-                                       ((20, 1500), 1e-2), ((90, 1800), 1e-2)])
+                                       ((20, 1500), 1e-2), ((90, 1800), 1e-2),
+                                       # 128 < m <= 512, in place, warp per column (the C5 256 x 256 interface)
+                                       ((256, 256), 1e-2), ((200, 1100), 1e-3), ((129, 40), 0.0),
+                                       ((300, 700), 1e-2), ((512, 64), 1e-8)])
 def test_cpqr_matches_oracle(shape, eps, path, monkeypatch):
-    """auto = short-wide kernel where eligible (cpqr_narrow.cu); smem = one CTA per block (kernels.cu)."""
+    """auto = short-wide or tall kernel where eligible (cpqr_narrow.cu); smem = one CTA per block (kernels.cu)."""
     if path != "auto":
         monkeypatch.setenv("SPQR_CPQR_PATH", path)
     m, n = shape
@@ -162,3 +165,24 @@ def test_trsm_right_matches_oracle():
     for b in range(nb):
         ref = O.tri_solve_upper(R[b], B[b], "right", False)
         assert np.allclose(X[b], ref, atol=1e-12)
+
+
+def test_cpqr_dev_entry_matches_host_entry():
+    """spqr_cpqr_batched_dev (device buffers, C5 microbenchmark leg) = spqr_cpqr_batched."""
+    import ctypes as C
+    import torch
+    from paper_2102_09878_b200.problems import decaying_interface
+    B = decaying_interface(256, 0.8, seed=0)
+    nb = 6
+    host = _P().cpqr_batched(np.stack([B] * nb), 1e-2)
+    A = torch.from_numpy(B.T.copy()).to("cuda").reshape(1, 256, 256).repeat(nb, 1, 1).contiguous()
+    rank = torch.empty(nb, dtype=torch.int32, device="cuda")
+    ms = C.c_float()
+    rc = _P().lib().spqr_cpqr_batched_dev(nb, 256, 256, C.c_void_p(A.data_ptr()), 1e-2, C.c_void_p(rank.data_ptr()),
+                                          C.byref(ms))
+    assert rc == 0 and ms.value > 0
+    Ad = A.cpu().numpy()
+    for b in range(nb):
+        k = host[b]["rank"]
+        assert int(rank[b]) == k == O.cpqr(B, 1e-2)["rank"]
+        assert np.array_equal(Ad[b].T[:k], host[b]["R"][:k])

@@ -47,6 +47,26 @@ def run_ours(m, n, k, nb, reps=3):
     return best
 
 
+def run_cpqr(B, nb, eps, reps=3):
+    """truncated CPQR of nb copies of B on the device (spqr_cpqr_batched_dev), best of reps"""
+    L = P.lib()
+    m, n = B.shape
+    A0 = torch.from_numpy(np.asfortranarray(B).T.copy()).to("cuda").reshape(1, n, m).repeat(nb, 1, 1).contiguous()
+    rank = torch.empty(nb, dtype=torch.int32, device="cuda")
+    best = 1e30
+    for r in range(reps + 1):
+        A = A0.clone()
+        torch.cuda.synchronize()
+        ms = C.c_float()
+        rc = L.spqr_cpqr_batched_dev(nb, m, n, C.c_void_p(A.data_ptr()), eps, C.c_void_p(rank.data_ptr()), C.byref(ms))
+        assert rc == 0
+        if r > 0:
+            best = min(best, ms.value)
+    rk = rank.cpu().numpy()
+    assert (rk == rk[0]).all()
+    return rk[0], best
+
+
 def run_torch(m, n, k, nb, reps=2):
     g = torch.Generator(device="cuda").manual_seed(0)
     A = torch.randn(nb, m, n, dtype=torch.float64, device="cuda", generator=g)
@@ -89,16 +109,20 @@ def main():
         print(row, flush=True)
     if os.environ.get("MB_ONLY") is not None:
         return
-    # CPQR 256x256, sigma_i = 0.8^i
+    # CPQR 256x256, sigma_i = 0.8^i, eps 1e-2: one interface per block of each batch size, device time
     from paper_2102_09878_b200.problems import decaying_interface
     B = decaying_interface(256, 0.8, seed=0)
-    for nb in (64, 512):
-        Bs = np.stack([B] * nb)
-        t0 = time.perf_counter()
-        res = P.cpqr_batched(Bs, 1e-2)
-        dt = time.perf_counter() - t0
-        out.setdefault("cpqr", []).append({"batch": nb, "rank": res[0]["rank"], "host_wall_s_incl_copies": round(dt, 4)})
-        print(out["cpqr"][-1], flush=True)
+    m = n = 256
+    for nb in (64, 1024, 4096):
+        rank, ms = run_cpqr(B, nb, 1e-2)
+        r = int(rank)
+        fl = sum(4.0 * (m - j) * (n - j - 1) for j in range(r)) + 2.0 * m * n
+        by = 8.0 * m * n + 8.0 * r * n  # single-pass ideal: read the block, write R
+        row = {"shape": "cpqr 256x256 eps 1e-2", "batch": nb, "rank": r, "ms": round(ms, 3),
+               "GFLOP/s": round(fl * nb / ms / 1e6, 1), "GB/s": round(by * nb / ms / 1e6, 1),
+               "frac_hbm": round(by * nb / ms / 1e6 / HBM, 4)}
+        out.setdefault("cpqr", []).append(row)
+        print(row, flush=True)
     print(json.dumps(out))
 
 
