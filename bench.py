@@ -234,6 +234,37 @@ def front_qr_microbench(local, ws=1, rank=0):
                      "frac_fp64": round(fl / best / 1e9 / (FP64_PEAK_TFLOPS * ws), 3),
                      "GB/s": round(by / best / 1e6, 1)})
         del A0, A
+    # truncated CPQR (eps 1e-2) of one 256 x 256 interface per block, sigma_i = 0.8^i
+    # (spqr_cpqr_batched_dev); bytes = single-pass ideal (read the block, write R)
+    import numpy as np
+    from paper_2102_09878_b200.problems import decaying_interface
+    B = decaying_interface(256, 0.8, seed=0)
+    cm = cn = 256
+    Bt = torch.from_numpy(np.ascontiguousarray(B.T)).to(f"cuda:{local}")
+    for nb in (4096, 1024, 64):
+        mine = microbench_shard(nb, ws, rank)
+        A0 = Bt.reshape(1, cn, cm).repeat(max(mine, 1), 1, 1).contiguous()
+        rk = torch.zeros(max(mine, 1), dtype=torch.int32, device=A0.device)
+        best = 1e30
+        for r in range(4):
+            A = A0.clone()
+            torch.cuda.synchronize()
+            barrier(ws)
+            ms = C.c_float()
+            if mine > 0:
+                rc = L.spqr_cpqr_batched_dev(mine, cm, cn, C.c_void_p(A.data_ptr()), 1e-2, C.c_void_p(rk.data_ptr()),
+                                             C.byref(ms))
+                if rc != 0:
+                    raise RuntimeError("spqr_cpqr_batched_dev failed")
+            if r > 0:
+                best = min(best, allmax(ws, ms.value))
+        rr = int(rk[0].item())
+        fl = (sum(4.0 * (cm - j) * (cn - j - 1) for j in range(rr)) + 2.0 * cm * cn) * nb
+        by = (8.0 * cm * cn + 8.0 * rr * cn) * nb
+        rows.append({"shape": "cpqr 256x256 eps 1e-2", "batch": nb, "n_gpus": ws, "rank": rr, "ms": round(best, 3),
+                     "GFLOP/s": round(fl / best / 1e6, 1), "GB/s": round(by / best / 1e6, 1),
+                     "frac_hbm": round(by / best / 1e6 / (load_peaks()[0] * ws), 4)})
+        del A0, A
     return {"peak_tflops_per_gpu": FP64_PEAK_TFLOPS, "peak_source": "measured DMMA (tools/fp64_peak.cu)",
             "sharding": "batch split across ranks, no exchange; time = max over ranks", "shapes": rows}
 
