@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <algorithm>
+#include <stdexcept>
 
 #include <cooperative_groups.h>
 
@@ -494,17 +495,25 @@ __global__ void __launch_bounds__(32 * NWARP) k_wy(double* __restrict__ a, int l
 }
 
 // nonnegative diagonal: flip rows of R (cols i..) and of the neighbour block;
-// sign and first zero/denormal pivot per problem
-__global__ void k_flip(double* __restrict__ a, int ld, long long stride, int n, int ntot, double* __restrict__ sign_all,
-                       int* __restrict__ info) {
+// sign and first zero/denormal pivot per problem.  CTA = 32 columns of one
+// problem: the diagonal's signs are staged in shared memory, then threads walk
+// the rows of each column (coalesced).  The diagonal itself is flipped by
+// k_flip_diag afterwards.
+constexpr int kFlipCols = 32, kFlipMaxN = 8192;
+__global__ void __launch_bounds__(256) k_flip(double* __restrict__ a, int ld, long long stride, int n, int ntot,
+                                              double* __restrict__ sign_all, int* __restrict__ info) {
     const int b = blockIdx.y;
     double* A = a + b * stride;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ntot; j += gridDim.x * blockDim.x) {
-        const int top = j < n ? j + 1 : n;
-        for (int i = 0; i < top; ++i)
-            if (A[i + static_cast<long long>(i) * ld] < 0.0 && i != j) A[i + static_cast<long long>(j) * ld] = -A[i + static_cast<long long>(j) * ld];
-    }
+    __shared__ unsigned char neg[kFlipMaxN];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) neg[i] = A[i + static_cast<long long>(i) * ld] < 0.0;
     __syncthreads();
+    const int c0 = blockIdx.x * kFlipCols;
+    for (int j = c0; j < min(ntot, c0 + kFlipCols); ++j) {
+        const int top = j < n ? j : n;  // rows i < top (the diagonal excluded)
+        double* col = A + static_cast<long long>(j) * ld;
+        for (int i = threadIdx.x; i < top; i += blockDim.x)
+            if (neg[i]) col[i] = -col[i];
+    }
     if (blockIdx.x == 0) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             const double r = A[i + static_cast<long long>(i) * ld];
@@ -1332,7 +1341,8 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
             apply_block<KO>(nbatch, m, ldA, stride, d_a, J0, kw2, J0 + kw2, ntot, T_outer, st);
         }
     }
-    dim3 g2((ntot + 255) / 256, nbatch);
+    if (n > kFlipMaxN) throw std::runtime_error("blocked_qr_apply: n above the flip kernel's limit");
+    dim3 g2((ntot + kFlipCols - 1) / kFlipCols, nbatch);
     k_flip<<<g2, 256, 0, st>>>(d_a, ldA, stride, n, ntot, d_sign, d_info);
     k_flip_diag<<<nbatch, 256, 0, st>>>(d_a, ldA, stride, n);
 }
