@@ -1193,13 +1193,13 @@ struct BigWs {
         return p;
     }
 };
-BigWs g_ws_w, g_ws_t;
+BigWs g_ws_w[2], g_ws_t[2];  // [0]: trailing updates (main stream), [1]: panel phase (side stream)
 
 // block reflector (KB columns at J0, kw valid, T in T_all with ld KB) applied
 // to columns [cbeg, cend) of every problem; gram != 0 computes V^T V instead
 template <int KB>
-void apply_block(int nbatch, int m, int ld, long long stride, double* d_a, int J0, int kw, int cbeg, int cend,
-                 const double* T_all, cudaStream_t st, double* wp_out = nullptr, int* nsl_out = nullptr, int gram = 0) {
+void apply_block(BigWs& ws, int nbatch, int m, int ld, long long stride, double* d_a, int J0, int kw, int cbeg,
+                 int cend, const double* T_all, cudaStream_t st, int* nsl_out = nullptr, int gram = 0) {
     const int rows = m - J0;
     const int ntile = (cend - cbeg + TCG - 1) / TCG;
     if (ntile <= 0 || rows <= 0) return;
@@ -1221,7 +1221,7 @@ void apply_block(int nbatch, int m, int ld, long long stride, double* d_a, int J
     }
     const int rs = ((nchunks + nsl - 1) / nsl) * CHG;
     nsl = (rows + rs - 1) / rs;
-    double* wp = g_ws_w.get(static_cast<size_t>(nbatch) * nsl * ntile * KB * TCG);
+    double* wp = ws.get(static_cast<size_t>(nbatch) * nsl * ntile * KB * TCG);
     {
         static size_t cfg = 0;
         smem_optin(reinterpret_cast<const void*>(k_vtc<KB>), vtc_smem(KB), cfg);
@@ -1230,7 +1230,6 @@ void apply_block(int nbatch, int m, int ld, long long stride, double* d_a, int J
     }
     if (gram) {
         *nsl_out = nsl;
-        (void)wp_out;
         return;
     }
     {
@@ -1270,7 +1269,7 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
     const long long stride = static_cast<long long>(ldA) * ntot;
     const size_t smem_cap = 160 * 1024;
     // panel j0..j0+w: V, tau, and the panel's T (NB x NB per problem) in d_T
-    auto panel = [&](int j0, int w, double* d_T) {
+    auto panel = [&](int j0, int w, double* d_T, cudaStream_t st) {
         const int rows = m - j0;
         // staged panel: (rows|1) x w plus v (rows); else in place with v in shared memory
         const int smem_rows = static_cast<int>(smem_cap / (sizeof(double) * (NB + 1))) - 2;
@@ -1300,7 +1299,7 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
     if (one_level || n <= NB) {
         for (int j0 = 0; j0 < n; j0 += NB) {
             const int w = std::min(NB, n - j0);
-            panel(j0, w, d_T);
+            panel(j0, w, d_T, st);
             const int trail = ntot - (j0 + w);
             if (trail > 0) {
                 dim3 grid((trail + TC2 - 1) / TC2, nbatch);
@@ -1313,32 +1312,74 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
         }
     } else {
         // two levels: NB panels inside KO-wide outer blocks, one KO-wide block
-        // reflector per outer block for the trailing columns
-        double* T_outer = g_ws_t.get(static_cast<size_t>(nbatch) * (KO * KO + (KO / NB) * NB * NB));
-        double* T_in = T_outer + static_cast<size_t>(nbatch) * KO * KO;  // KO/NB panel T slots
+        // reflector per outer block for the trailing columns.  Look-ahead: once
+        // block J has updated block J+1's columns, block J+1's panel phase runs on
+        // a side stream (high priority) while block J updates the columns beyond.
         const long long slot = static_cast<long long>(nbatch) * NB * NB;
+        const size_t tsz = static_cast<size_t>(nbatch) * (KO * KO + (KO / NB) * NB * NB);
+        double* Tb[2] = {g_ws_t[0].get(tsz), g_ws_t[1].get(tsz)};
         const bool reg_panel = !std::getenv("SPQR_SMEM_PANEL");
-        for (int J0 = 0; J0 < n; J0 += KO) {
+        const bool lookahead = !std::getenv("SPQR_NO_LOOKAHEAD");
+        static cudaStream_t side = nullptr;
+        static cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+        if (lookahead && !side) {
+            int lo = 0, hi = 0;
+            cudaDeviceGetStreamPriorityRange(&lo, &hi);
+            cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi);
+            cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming);
+        }
+        // panels + inner updates of block J0, its Gram matrix and merged T into Tout
+        auto panel_phase = [&](int J0, double* Tout, cudaStream_t s) {
             const int kw2 = std::min(KO, n - J0);
+            double* T_in = Tout + static_cast<size_t>(nbatch) * KO * KO;
             for (int j0 = J0; j0 < J0 + kw2; j0 += NB) {
                 const int w = std::min(NB, J0 + kw2 - j0);
                 double* Tq = T_in + ((j0 - J0) / NB) * slot;
-                if (!(reg_panel && launch_panel_reg(nbatch, m, ldA, stride, d_a, j0, w, d_tau, n, Tq, st)))
-                    panel(j0, w, Tq);
+                if (!(reg_panel && launch_panel_reg(nbatch, m, ldA, stride, d_a, j0, w, d_tau, n, Tq, s)))
+                    panel(j0, w, Tq, s);
                 if (j0 + w < J0 + kw2)
-                    apply_block<NB>(nbatch, m, ldA, stride, d_a, j0, w, j0 + w, J0 + kw2, Tq, st);
+                    apply_block<NB>(g_ws_w[1], nbatch, m, ldA, stride, d_a, j0, w, j0 + w, J0 + kw2, Tq, s);
             }
-            if (J0 + kw2 >= ntot) continue;
-            if (kw2 <= NB) {
-                apply_block<NB>(nbatch, m, ldA, stride, d_a, J0, kw2, J0 + kw2, ntot, T_in, st);
-                continue;
-            }
+            if (kw2 <= NB || J0 + kw2 >= ntot) return;
             int nsl = 1;
-            apply_block<KO>(nbatch, m, ldA, stride, d_a, J0, kw2, J0, J0 + KO, nullptr, st, nullptr, &nsl, 1);
+            apply_block<KO>(g_ws_w[1], nbatch, m, ldA, stride, d_a, J0, kw2, J0, J0 + KO, nullptr, s, &nsl, 1);
             static size_t cfg = 0;
             smem_optin(reinterpret_cast<const void*>(k_tmerge), kTmergeSmem, cfg);
-            k_tmerge<<<nbatch, 256, kTmergeSmem, st>>>(g_ws_w.p, nsl, T_in, slot, (kw2 + NB - 1) / NB, T_outer);
-            apply_block<KO>(nbatch, m, ldA, stride, d_a, J0, kw2, J0 + kw2, ntot, T_outer, st);
+            k_tmerge<<<nbatch, 256, kTmergeSmem, s>>>(g_ws_w[1].p, nsl, T_in, slot, (kw2 + NB - 1) / NB, Tout);
+        };
+        // block J0's reflectors applied to columns [c0, c1)
+        auto update = [&](int J0, const double* Tout, int c0, int c1) {
+            const int kw2 = std::min(KO, n - J0);
+            if (c1 <= c0) return;
+            if (kw2 <= NB)
+                apply_block<NB>(g_ws_w[0], nbatch, m, ldA, stride, d_a, J0, kw2, c0, c1,
+                                Tout + static_cast<size_t>(nbatch) * KO * KO, st);
+            else
+                apply_block<KO>(g_ws_w[0], nbatch, m, ldA, stride, d_a, J0, kw2, c0, c1, Tout, st);
+        };
+        panel_phase(0, Tb[0], st);
+        for (int bi = 0, J0 = 0; J0 < n; ++bi, J0 += KO) {
+            const int kw2 = std::min(KO, n - J0);
+            double* Tcur = Tb[bi & 1];
+            const int nJ = J0 + KO;  // next block
+            if (nJ >= n) {
+                update(J0, Tcur, J0 + kw2, ntot);
+                break;
+            }
+            const int nend = std::min(nJ + KO, n);
+            update(J0, Tcur, nJ, nend);  // the next block's columns first
+            if (lookahead) {
+                cudaEventRecord(ev_a, st);
+                cudaStreamWaitEvent(side, ev_a, 0);
+                panel_phase(nJ, Tb[(bi + 1) & 1], side);
+                cudaEventRecord(ev_b, side);
+                update(J0, Tcur, nend, ntot);
+                cudaStreamWaitEvent(st, ev_b, 0);
+            } else {
+                update(J0, Tcur, nend, ntot);
+                panel_phase(nJ, Tb[(bi + 1) & 1], st);
+            }
         }
     }
     if (n > kFlipMaxN) throw std::runtime_error("blocked_qr_apply: n above the flip kernel's limit");
