@@ -14,6 +14,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdlib>
+#include <cstdint>
 #include <algorithm>
 #include <stdexcept>
 
@@ -332,6 +333,10 @@ constexpr int TC2 = 128;
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -813,10 +818,30 @@ __global__ void __launch_bounds__(256) k_vtc(const double* __restrict__ a, int l
     const int g = lane >> 2, t4 = lane & 3;
     const int mw = wid & 3, nw = wid >> 2;
     const int nchunk = rhi > rlo ? (rhi - rlo + CHG - 1) / CHG : 0;
+    // 16-byte copies for chunks below the unit-triangular rows when row pairs are aligned
+    const bool vec = ((ld & 1) == 0) && ((J0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
     auto issue = [&](int c) {
         const int r0 = rlo + c * CHG, rc = min(CHG, rhi - r0);
         double* vb = sV0 + (c & 1) * (KB * LDS_);
         double* cb = sC0 + (c & 1) * (TCG * LDS_);
+        if (vec && rc == CHG && r0 >= KB) {
+            for (int e = threadIdx.x; e < CHG * KB / 2; e += 256) {
+                const int i = 2 * (e % (CHG / 2)), j = e / (CHG / 2);
+                if (j < kw)
+                    cp_async16(vb + i + j * LDS_, A + (J0 + r0 + i) + static_cast<long long>(J0 + j) * ld);
+                else
+                    vb[i + j * LDS_] = vb[i + 1 + j * LDS_] = 0.0;
+            }
+            for (int e = threadIdx.x; e < CHG * TCG / 2; e += 256) {
+                const int i = 2 * (e % (CHG / 2)), j = e / (CHG / 2);
+                if (j < nc && (!gram || c0 - cbeg + j < kw))  // Gram: V's columns beyond kw are zero
+                    cp_async16(cb + i + j * LDS_, A + (J0 + r0 + i) + static_cast<long long>(c0 + j) * ld);
+                else
+                    cb[i + j * LDS_] = cb[i + 1 + j * LDS_] = 0.0;
+            }
+            cp_commit();
+            return;
+        }
         for (int e = threadIdx.x; e < CHG * KB; e += 256) {
             const int i = e % CHG, j = e / CHG, r = r0 + i;
             double* dst = vb + i + j * LDS_;
@@ -1028,21 +1053,34 @@ __global__ void __launch_bounds__(256, 2) k_cvw2(double* __restrict__ a, int ld,
             asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + 16));
         }
     }
+    // 16-byte copies below the unit-triangular rows when row pairs are aligned (W2 always is)
+    const bool vec = ((ld & 1) == 0) && ((J0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+                     r0 >= KB && r0 + CM <= rows;
     auto issue = [&](int s) {
         double* vb = sV0 + (s & 1) * (KC * LDM);
         double* wb = sW0 + (s & 1) * (TCG * LDK);
         const int k0 = s * KC;
-        for (int e = threadIdx.x; e < CM * KC; e += 256) {
-            const int i = e % CM, j = e / CM, r = r0 + i, jj = k0 + j;
-            double* dst = vb + i + j * LDM;
-            double v;
-            if (r >= rows) *dst = 0.0;
-            else if (v_direct(r, jj, kw, v)) *dst = v;
-            else cp_async8(dst, A + (J0 + r) + static_cast<long long>(J0 + jj) * ld, true);
+        if (vec) {
+            for (int e = threadIdx.x; e < CM * KC / 2; e += 256) {
+                const int i = 2 * (e % (CM / 2)), j = e / (CM / 2), jj = k0 + j;
+                if (jj < kw)
+                    cp_async16(vb + i + j * LDM, A + (J0 + r0 + i) + static_cast<long long>(J0 + jj) * ld);
+                else
+                    vb[i + j * LDM] = vb[i + 1 + j * LDM] = 0.0;
+            }
+        } else {
+            for (int e = threadIdx.x; e < CM * KC; e += 256) {
+                const int i = e % CM, j = e / CM, r = r0 + i, jj = k0 + j;
+                double* dst = vb + i + j * LDM;
+                double v;
+                if (r >= rows) *dst = 0.0;
+                else if (v_direct(r, jj, kw, v)) *dst = v;
+                else cp_async8(dst, A + (J0 + r) + static_cast<long long>(J0 + jj) * ld, true);
+            }
         }
-        for (int e = threadIdx.x; e < KC * TCG; e += 256) {
-            const int j = e % KC, c = e / KC;
-            cp_async8(wb + j + c * LDK, W2 + (k0 + j) + c * KB, true);
+        for (int e = threadIdx.x; e < KC * TCG / 2; e += 256) {
+            const int j = 2 * (e % (KC / 2)), c = e / (KC / 2);
+            cp_async16(wb + j + c * LDK, W2 + (k0 + j) + c * KB);
         }
         cp_commit();
     };
