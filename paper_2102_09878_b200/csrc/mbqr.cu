@@ -707,16 +707,9 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
                     for (int q = 0; q < RR; ++q) x[q][j] = fma(tw, v[q], x[q][j]);
                 }
             }
-            if (rank == 0 && wid == 0) {  // T(:, k) = -t T(0:k, 0:k) (V^T v_k),  T(k, k) = t
-                if (lane < k) gv[lane] = wl;
-                __syncwarp();
-                if (lane < k) {
-                    double sacc = 0.0;
-                    for (int l = lane; l < k; ++l) sacc = fma(Ts[lane + l * NB], gv[l], sacc);
-                    Ts[lane + k * NB] = -t * sacc;
-                }
-                if (lane == 0) Ts[k + k * NB] = t;
-                __syncwarp();
+            if (rank == 0 && wid == 0) {  // V^T v_k and tau_k for T, built after the loop
+                if (lane < k) Ts[lane + k * NB] = wl;
+                if (lane == 0) gv[k] = t;
             }
         }
     }
@@ -731,6 +724,21 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
 #pragma unroll
         for (int q = 0; q < RR; ++q)
             if (row[q] < rows && j < w) base[row[q] + ldo * j] = x[q][j];
+    // compact-WY T from the recorded V^T v_k (strict upper part of Ts) and tau
+    // (accumulate_wy, dense_kernels.cpp:41-53): T(0:k, k) = -tau_k T(0:k, 0:k) (V^T v_k),
+    // T(k, k) = tau_k; one warp, off the per-reflector critical path
+    if (rank == 0 && wid == 0) {
+        __syncwarp();
+        for (int k = 0; k < kmax; ++k) {
+            double sacc = 0.0;
+            if (lane < k)
+                for (int l = lane; l < k; ++l) sacc = fma(Ts[lane + l * NB], Ts[l + k * NB], sacc);
+            __syncwarp();
+            if (lane < k) Ts[lane + k * NB] = -gv[k] * sacc;
+            if (lane == k) Ts[k + k * NB] = gv[k];
+            __syncwarp();
+        }
+    }
     __syncthreads();
     if (rank == 0) {
         double* T = T_all + static_cast<long long>(b) * NB * NB;
