@@ -811,7 +811,7 @@ __device__ __forceinline__ bool v_direct(int i, int j, int kw, double& val) {
 template <int KB>
 __global__ void __launch_bounds__(256) k_vtc(const double* __restrict__ a, int ld, long long stride, int m, int J0,
                                              int kw, int cbeg, int cend, int rs, int gram,
-                                             double* __restrict__ wp) {
+                                             double* __restrict__ wp, const double* __restrict__ T_all) {
     constexpr int PM = KB / 32, PN = TCG / 16;
     const int t = blockIdx.x, s = blockIdx.y, b = blockIdx.z;
     const int ntile = gridDim.x, nsl = gridDim.y;
@@ -895,6 +895,37 @@ __global__ void __launch_bounds__(256) k_vtc(const double* __restrict__ a, int l
         __syncthreads();
     }
     double* W = wp + ((static_cast<long long>(b) * nsl + s) * ntile + t) * (KB * TCG);
+    if (T_all != nullptr) {  // one row slice: W2 = T^T W here (k_tw's work, no W round trip)
+        constexpr int LDW = KB + 4;  // KB x TCG in the (free) staging buffers
+        double* sW = dsm;
+#pragma unroll
+        for (int i = 0; i < PM; ++i)
+#pragma unroll
+            for (int q = 0; q < PN; ++q) {
+                const int row = (mw * PM + i) * 8 + g, col = (nw * PN + q) * 8 + 2 * t4;
+                sW[row + col * LDW] = acc[i][q][0];
+                sW[row + (col + 1) * LDW] = acc[i][q][1];
+            }
+        __syncthreads();
+        const double* T = T_all + static_cast<long long>(b) * KB * KB;
+        double acc2[PM][PN][2] = {};
+        const int kend = min((mw + 1) * PM * 8, (kw + 3) & ~3);  // T^T lower triangular
+        for (int k0 = 0; k0 < kend; k0 += 4) {
+            double av[PM], bv[PN];
+#pragma unroll
+            for (int i = 0; i < PM; ++i) av[i] = __ldg(T + (k0 + t4) + ((mw * PM + i) * 8 + g) * KB);
+#pragma unroll
+            for (int q = 0; q < PN; ++q) bv[q] = sW[(k0 + t4) + ((nw * PN + q) * 8 + g) * LDW];
+#pragma unroll
+            for (int i = 0; i < PM; ++i)
+#pragma unroll
+                for (int q = 0; q < PN; ++q) dmma(acc2[i][q][0], acc2[i][q][1], av[i], bv[q]);
+        }
+#pragma unroll
+        for (int i = 0; i < PM; ++i)
+#pragma unroll
+            for (int q = 0; q < PN; ++q) acc[i][q][0] = acc2[i][q][0], acc[i][q][1] = acc2[i][q][1];
+    }
 #pragma unroll
     for (int i = 0; i < PM; ++i)
 #pragma unroll
@@ -1272,13 +1303,13 @@ void apply_block(BigWs& ws, int nbatch, int m, int ld, long long stride, double*
         static size_t cfg = 0;
         smem_optin(reinterpret_cast<const void*>(k_vtc<KB>), vtc_smem(KB), cfg);
         k_vtc<KB><<<dim3(ntile, nsl, nbatch), 256, vtc_smem(KB), st>>>(d_a, ld, stride, m, J0, kw, cbeg, cend, rs, gram,
-                                                                         wp);
+                                                                         wp, (nsl == 1 && !gram) ? T_all : nullptr);
     }
     if (gram) {
         *nsl_out = nsl;
         return;
     }
-    {
+    if (nsl > 1) {  // (one slice: fused into k_vtc)
         static size_t cfg = 0;
         const size_t sm = sizeof(double) * KB * 0 + sizeof(double) * (KB + 4) * TCG;
         smem_optin(reinterpret_cast<const void*>(k_tw<KB>), sm, cfg);
