@@ -1214,40 +1214,44 @@ __global__ void __launch_bounds__(256) k_tmerge(const double* __restrict__ wp, i
     }
     for (int e = threadIdx.x; e < 64 * 64; e += 256) GAB[e] = gram(e % 64, 64 + e / 64);
     __syncthreads();
+    // C = alpha A B (n x n, column-major, shared memory), 4 x 4 register blocks per thread
+    auto mm4 = [](double* C, int ldc, const double* A, int lda, const double* B, int ldb, int n, double alpha, int tid,
+                  int nthr) {
+        const int nb = n / 4;
+        for (int blk = tid; blk < nb * nb; blk += nthr) {
+            const int i0 = 4 * (blk % nb), j0 = 4 * (blk / nb);
+            double acc[4][4] = {};
+            for (int l = 0; l < n; ++l) {
+                double av[4], bv[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) av[r] = A[(i0 + r) + l * lda];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) bv[c] = B[l + (j0 + c) * ldb];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[r][c] = fma(av[r], bv[c], acc[r][c]);
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) C[(i0 + r) + (j0 + c) * ldc] = alpha * acc[r][c];
+        }
+    };
     // level 1: T(o, o+32) = -T_o G T_{o+32} for o = 0 (threads 0..127) and o = 64 (128..255)
     {
         const int h = threadIdx.x >> 7, tl = threadIdx.x & 127, o = 64 * h;
         const double* G = h ? G23 : G01;
         double* Xh = X + h * 1024;
-        for (int e = tl; e < 1024; e += 128) {  // Xh = G T_{o+32}  (T upper: l <= j)
-            const int i = e % 32, j = e / 32;
-            double s = 0.0;
-            for (int l = 0; l <= j; ++l) s = fma(G[i + l * 32], sT[(o + 32 + l) + (o + 32 + j) * LDT], s);
-            Xh[i + j * 32] = s;
-        }
+        mm4(Xh, 32, G, 32, sT + (o + 32) + (o + 32) * LDT, LDT, 32, 1.0, tl, 128);
         __syncthreads();
-        for (int e = tl; e < 1024; e += 128) {  // T(o.., o+32..) = -T_o Xh  (T_o upper: l >= i)
-            const int i = e % 32, j = e / 32;
-            double s = 0.0;
-            for (int l = i; l < 32; ++l) s = fma(sT[(o + i) + (o + l) * LDT], Xh[l + j * 32], s);
-            sT[(o + i) + (o + 32 + j) * LDT] = -s;
-        }
+        mm4(sT + o + (o + 32) * LDT, LDT, sT + o + o * LDT, LDT, Xh, 32, 32, -1.0, tl, 128);
     }
     __syncthreads();
     // level 2: T(0:64, 64:128) = -T_A (G_AB T_B)
-    for (int e = threadIdx.x; e < 4096; e += 256) {
-        const int i = e % 64, j = e / 64;
-        double s = 0.0;
-        for (int l = 0; l <= j; ++l) s = fma(GAB[i + l * 64], sT[(64 + l) + (64 + j) * LDT], s);
-        X[i + j * 64] = s;
-    }
+    mm4(X, 64, GAB, 64, sT + 64 + 64 * LDT, LDT, 64, 1.0, threadIdx.x, 256);
     __syncthreads();
-    for (int e = threadIdx.x; e < 4096; e += 256) {
-        const int i = e % 64, j = e / 64;
-        double s = 0.0;
-        for (int l = i; l < 64; ++l) s = fma(sT[i + l * LDT], X[l + j * 64], s);
-        sT[i + (64 + j) * LDT] = -s;
-    }
+    mm4(sT + 64 * LDT, LDT, sT, LDT, X, 64, 64, -1.0, threadIdx.x, 256);
     __syncthreads();
     double* T = T_all + static_cast<long long>(b) * KO * KO;
     for (int e = threadIdx.x; e < KO * KO; e += 256) T[e] = sT[(e % KO) + (e / KO) * LDT];
