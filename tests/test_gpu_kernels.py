@@ -13,7 +13,7 @@ def _P():
     return P
 
 
-@pytest.mark.parametrize("path", ["auto", "smem", "blocked", "blocked_l1", "tile_dmma"])
+@pytest.mark.parametrize("path", ["auto", "smem", "blocked", "blocked_l1", "blocked_nola", "blocked_alt", "tile_dmma"])
 @pytest.mark.parametrize("shape", [(1, 1, 1), (5, 3, 3), (20, 7, 30), (40, 12, 60), (128, 32, 288), (300, 64, 96),
                                    (300, 40, 140), (513, 70, 200), (512, 128, 384),
                                    # column-tiled path: many tiles, panel only, square panel, m > 256
@@ -55,6 +55,24 @@ def test_qr_apply_matches_oracle(shape, path, monkeypatch):
         if ntot > n:
             X = O.apply_reflectors(V, t, s, A[b, :, n:], "left_t")
             assert np.allclose(out[b, :, n:], X, atol=1e-12 * (1 + np.abs(X).max()))
+
+
+@pytest.mark.parametrize("shape", [(512, 128, 384), (1024, 256, 300)])
+def test_qr_blocked_large_batch(shape):
+    """Large batches: one row slice per trailing tile, so k_vtc applies T^T itself (mbqr.cu);
+    several outer blocks with the look-ahead side stream."""
+    m, n, ntot = shape
+    nb = 64
+    rng = np.random.default_rng(m + n)
+    A = rng.standard_normal((nb, m, ntot))
+    out, tau, sg, info = _P().qr_apply_batched(A, n)
+    assert np.all(info == -1)
+    for b in (0, 17, nb - 1):
+        V, t, s, R = O.householder_qr(A[b, :, :n])
+        assert np.allclose(np.triu(out[b, :n, :n]), R, atol=1e-12 * (1 + np.abs(R).max()))
+        assert np.allclose(tau[b], t, atol=1e-13)
+        X = O.apply_reflectors(V, t, s, A[b, :, n:], "left_t")
+        assert np.allclose(out[b, :, n:], X, atol=1e-12 * (1 + np.abs(X).max()))
 
 
 def test_qr_tiled_many_ctas_per_front():
