@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -112,6 +113,22 @@ private:
     size_t cur_ = 0, chunk_;
 };
 
+// Large host copies (pinned staging <-> host vectors) split over the OpenMP
+// threads: a single thread's memcpy is memory-latency bound far below DRAM speed.
+inline void par_memcpy(void* dst, const void* src, size_t bytes) {
+    constexpr size_t kChunk = size_t(256) << 10;
+    if (bytes < 4 * kChunk) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const long long n = static_cast<long long>((bytes + kChunk - 1) / kChunk);
+#pragma omp parallel for schedule(static)
+    for (long long c = 0; c < n; ++c) {
+        const size_t off = static_cast<size_t>(c) * kChunk;
+        std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, std::min(kChunk, bytes - off));
+    }
+}
+
 // Uploads host vectors through pinned memory into a device arena.
 struct Uploader {
     DeviceArena* dev;
@@ -123,7 +140,7 @@ struct Uploader {
         if (n == 0) return nullptr;
         T* d = dev->alloc_n<T>(n);
         void* p = pin->alloc(sizeof(T) * n);
-        std::memcpy(p, h, sizeof(T) * n);
+        par_memcpy(p, h, sizeof(T) * n);
         CK(cudaMemcpyAsync(d, p, sizeof(T) * n, cudaMemcpyHostToDevice, st));
         bytes_h2d += sizeof(T) * n;
         return d;

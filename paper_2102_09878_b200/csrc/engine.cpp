@@ -449,6 +449,11 @@ private:
     std::vector<int> stage_of_;
     std::vector<std::pair<int, int>> dep_;
     AsmBuilder wcopy_;
+    AsmBuilder asm_pool_[6];  // one per call site: vectors keep their capacity between waves
+    AsmBuilder& asm_slot(int i) {
+        asm_pool_[i].clear();
+        return asm_pool_[i];
+    }
     std::vector<double> pre_sq_, post_sq_;
     std::vector<unsigned char> pre_nz_, post_nz_;
     // first error in reference order
@@ -493,6 +498,10 @@ private:
     std::vector<Pending> dl_;
     template <class T>
     void enqueue(std::vector<T>& h, const T* d, size_t n) {
+        if (h.capacity() < n) {  // grow without copying the stale contents
+            h.clear();
+            h.reserve(n);
+        }
         h.resize(n);
         if (n == 0) return;
         void* p = pin_.alloc(sizeof(T) * n);
@@ -507,7 +516,7 @@ private:
             CK(cudaStreamSynchronize(st_));
         }
         CK(cudaGetLastError());  // a failed launch must not pass silently
-        for (auto& q : dl_) std::memcpy(q.host, q.pin, q.bytes);
+        for (auto& q : dl_) par_memcpy(q.host, q.pin, q.bytes);
         dl_.clear();
         pin_.reset();
         kt_.resolve(out_.ctr);
@@ -515,12 +524,16 @@ private:
     }
     template <class T>
     void download(std::vector<T>& h, const T* d, size_t n) {
+        if (h.capacity() < n) {
+            h.clear();
+            h.reserve(n);
+        }
         h.resize(n);
         if (n == 0) return;
         T* p = static_cast<T*>(pin_.alloc(sizeof(T) * n));
         CK(cudaMemcpyAsync(p, d, sizeof(T) * n, cudaMemcpyDeviceToHost, st_));
         sync();
-        std::memcpy(h.data(), p, sizeof(T) * n);
+        par_memcpy(h.data(), p, sizeof(T) * n);
         out_.ctr.d2h_bytes += sizeof(T) * n;
     }
     void flush_assemble(AsmBuilder& b) {
@@ -1657,7 +1670,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
     // gather stacks, QR + apply, post statistics
     ProfScope ps_sb(prof_, HostProf::SBUILD);
     std::unique_ptr<NScope> sb_desc = std::make_unique<NScope>(nprof_, "sb.descriptors");
-    AsmBuilder sb;
+    AsmBuilder& sb = asm_slot(0);  // keeps its capacity across calls
     std::vector<QrDesc> qd;
     std::vector<StatDesc> pd;
     long long pwork = 0, postlen = 0;
@@ -1937,7 +1950,7 @@ void Engine::sparsify_rows_all() {
         bool big;
     };
     std::vector<Job> jobs;
-    AsmBuilder gb;
+    AsmBuilder& gb = asm_slot(1);  // keeps its capacity across calls
     std::vector<CpqrDesc> cd;
     int maxm = 0;
     for (size_t pp = 0; pp < fr_.size(); ++pp) {
@@ -2006,7 +2019,7 @@ void Engine::sparsify_rows_all() {
     }
     std::vector<int> rank;
     download(rank, d_rank, nj);
-    AsmBuilder wb;
+    AsmBuilder& wb = asm_slot(2);  // keeps its capacity across calls
     for (size_t i = 0; i < nj; ++i) {
         const Job& j = jobs[i];
         const int keep = rank[i];
@@ -2110,7 +2123,7 @@ void Engine::sparsify_cols_all() {
         };
         std::vector<Job> jobs;
         std::unique_ptr<NScope> sc1 = std::make_unique<NScope>(nprof_, "scols.G_descriptors");
-        AsmBuilder gb;
+        AsmBuilder& gb = asm_slot(3);  // keeps its capacity across calls
         std::vector<CpqrDesc> cd;
         int maxm = 0;
         // per-job shapes in parallel (holder sets normalised first: get() sorts lazily),
@@ -2252,7 +2265,7 @@ void Engine::sparsify_cols_all() {
             changed_p.push_back(static_cast<int>(i));
         }
         // materialise p fronts and their holders
-        AsmBuilder mb;
+        AsmBuilder& mb = asm_slot(4);  // keeps its capacity across calls
         std::vector<std::pair<int, Front>> updates;
         for (int ji : changed_p) {
             Job& j = jobs[ji];
@@ -2387,7 +2400,7 @@ void Engine::merge_level() {
     }
     DeviceArena& next = arena_[cur_ ^ 1];
     std::unique_ptr<NScope> m1 = std::make_unique<NScope>(nprof_, "merge.descriptors");
-    AsmBuilder mb;
+    AsmBuilder& mb = asm_slot(5);  // keeps its capacity across calls
     struct Plan {
         Front nf;
         std::vector<int2> rowsrc;  // (kid slot, row)

@@ -1,12 +1,16 @@
 // Minimal in-process sampling profiler for the host side of the engine
 // (the GPU box has no perf).  SPQR_SAMPLE=<path> turns it on for one
-// factorization: SIGPROF every 100 us of CPU time records the call stack;
+// factorization: SIGPROF every 100 us of CPU time (SPQR_SAMPLE_MASTER=1: of
+// wall time, engine thread only) records the call stack;
 // on stop, each frame is written as "<object> <offset>" so it can be
 // symbolised offline (addr2line -f -C -e <object> <offset>).
 #include <dlfcn.h>
 #include <execinfo.h>
 #include <signal.h>
+#include <sys/syscall.h>
 #include <sys/time.h>
+#include <time.h>
+#include <unistd.h>
 
 #include <atomic>
 #include <cstdio>
@@ -24,6 +28,8 @@ constexpr int kMax = 400000;
 void* g_buf[kMax][kDepth];
 std::atomic<int> g_n{0};
 bool g_on = false;
+bool g_master = false;
+timer_t g_timer;
 
 void on_prof(int) {
     const int i = g_n.fetch_add(1);
@@ -44,15 +50,31 @@ void sampler_start() {
     sa.sa_handler = on_prof;
     sa.sa_flags = SA_RESTART;
     sigaction(SIGPROF, &sa, nullptr);
-    itimerval tv{{0, 100}, {0, 100}};
-    setitimer(ITIMER_PROF, &tv, nullptr);
+    g_master = std::getenv("SPQR_SAMPLE_MASTER") != nullptr;
+    if (g_master) {  // wall-clock samples of the calling (engine) thread only
+        sigevent se;
+        std::memset(&se, 0, sizeof se);
+        se.sigev_notify = SIGEV_THREAD_ID;
+        se.sigev_signo = SIGPROF;
+        se._sigev_un._tid = static_cast<pid_t>(syscall(SYS_gettid));
+        timer_create(CLOCK_MONOTONIC, &se, &g_timer);
+        itimerspec its{{0, 100000}, {0, 100000}};
+        timer_settime(g_timer, 0, &its, nullptr);
+    } else {
+        itimerval tv{{0, 100}, {0, 100}};
+        setitimer(ITIMER_PROF, &tv, nullptr);
+    }
     g_on = true;
 }
 
 void sampler_stop() {
     if (!g_on) return;
-    itimerval tv{{0, 0}, {0, 0}};
-    setitimer(ITIMER_PROF, &tv, nullptr);
+    if (g_master) {
+        timer_delete(g_timer);
+    } else {
+        itimerval tv{{0, 0}, {0, 0}};
+        setitimer(ITIMER_PROF, &tv, nullptr);
+    }
     g_on = false;
     const char* path = std::getenv("SPQR_SAMPLE");
     FILE* f = std::fopen(path, "w");
