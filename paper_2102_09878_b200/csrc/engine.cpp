@@ -301,14 +301,68 @@ struct Scratch {
     std::vector<PRow> rows;
 };
 
+// Allocator whose value-initialisation is default-initialisation: vectors that
+// receive device downloads are resized without zero-filling them first.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = NoInitAlloc<U>;
+    };
+    NoInitAlloc() = default;
+    template <class U>
+    NoInitAlloc(const NoInitAlloc<U>&) {}
+    template <class U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <class U, class... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+template <class T>
+using dl_vector = std::vector<T, NoInitAlloc<T>>;
+
+// Growable array of trivially copyable elements whose growth does not
+// value-initialise (the row maps are rewritten in parallel right after).
+template <class T>
+struct PodVec {
+    std::unique_ptr<T[]> p;
+    size_t n = 0, cap = 0;
+    void reserve(size_t c) {
+        if (c <= cap) return;
+        const size_t nc = std::max(c, 2 * cap);
+        std::unique_ptr<T[]> q(new T[nc]);
+        if (n) std::memcpy(q.get(), p.get(), n * sizeof(T));
+        p = std::move(q);
+        cap = nc;
+    }
+    void resize_uninit(size_t m) {
+        reserve(m);
+        n = m;
+    }
+    void resize(size_t m, const T& v) {
+        reserve(m);
+        for (size_t i = n; i < m; ++i) p[i] = v;
+        n = m;
+    }
+    void shrink(size_t m) { n = std::min(n, m); }
+    T& operator[](size_t i) { return p[i]; }
+    const T* data() const { return p.get(); }
+    size_t size() const { return n; }
+    void clear() { n = 0; }
+};
+
 // Assemble job builder (generic gather, dev.h).
 struct AsmBuilder {
     std::vector<AsmDst> dst;
-    std::vector<int4> rowref;
+    PodVec<int4> rowref;
     std::vector<int> segoff, kmap;
     std::vector<AsmSrc> src;
     long long elems = 0;
-    int begin(double* p, int ld, int nrows, int ncols, int nsrc, int nseg) {
+    // init_rows = false: the caller writes every row map entry itself
+    int begin(double* p, int ld, int nrows, int ncols, int nsrc, int nseg, bool init_rows = true) {
         AsmDst d;
         d.p = p;
         d.ld = ld;
@@ -323,7 +377,10 @@ struct AsmBuilder {
         d.src_off = static_cast<long long>(src.size());
         d.elem_off = elems;
         elems += static_cast<long long>(nrows) * ncols;
-        rowref.resize(rowref.size() + nrows, int4{-1, 0, -1, 0});
+        if (init_rows)
+            rowref.resize(rowref.size() + nrows, int4{-1, 0, -1, 0});
+        else
+            rowref.resize_uninit(rowref.size() + nrows);
         segoff.resize(segoff.size() + d.nseg + 1, 0);
         segoff[d.seg_off + d.nseg] = ncols;
         kmap.resize(kmap.size() + static_cast<size_t>(d.nseg) * nsrc, -1);
@@ -339,7 +396,7 @@ struct AsmBuilder {
         if (!dst.empty() && (dst.back().nrows == 0 || dst.back().ncols == 0)) {
             const AsmDst d = dst.back();
             elems = d.elem_off;
-            rowref.resize(d.row_off);
+            rowref.shrink(d.row_off);
             segoff.resize(d.seg_off);
             kmap.resize(d.kmap_off);
             src.resize(d.src_off);
@@ -454,8 +511,8 @@ private:
         asm_pool_[i].clear();
         return asm_pool_[i];
     }
-    std::vector<double> pre_sq_, post_sq_;
-    std::vector<unsigned char> pre_nz_, post_nz_;
+    dl_vector<double> pre_sq_, post_sq_;
+    dl_vector<unsigned char> pre_nz_, post_nz_;
     // first error in reference order
     int err_cluster_ = -1;
     std::string err_reason_;
@@ -496,8 +553,8 @@ private:
         size_t bytes;
     };
     std::vector<Pending> dl_;
-    template <class T>
-    void enqueue(std::vector<T>& h, const T* d, size_t n) {
+    template <class T, class A>
+    void enqueue(std::vector<T, A>& h, const T* d, size_t n) {
         if (h.capacity() < n) {  // grow without copying the stale contents
             h.clear();
             h.reserve(n);
@@ -522,8 +579,8 @@ private:
         kt_.resolve(out_.ctr);
         out_.ctr.syncs++;
     }
-    template <class T>
-    void download(std::vector<T>& h, const T* d, size_t n) {
+    template <class T, class A>
+    void download(std::vector<T, A>& h, const T* d, size_t n) {
         if (h.capacity() < n) {
             h.clear();
             h.reserve(n);
@@ -544,7 +601,7 @@ private:
         ProfScope ps(prof_, HostProf::UPLOAD);
         Uploader u = up();
         const AsmDst* d = u.put(b.dst);
-        const int4* rr = u.put(b.rowref);
+        const int4* rr = u.put(b.rowref.data(), b.rowref.size());
         const int* so = u.put(b.segoff);
         const int* km = u.put(b.kmap);
         const AsmSrc* s = u.put(b.src);
@@ -1700,7 +1757,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
             sp.elims++;
         }
         const int nsrc = static_cast<int>(sb_bases_[ei].size());
-        edi[ei] = sb.begin(e.S, e.total_rows, e.total_rows, e.tcols, nsrc, static_cast<int>(e.keys.size()));
+        edi[ei] = sb.begin(e.S, e.total_rows, e.total_rows, e.tcols, nsrc, static_cast<int>(e.keys.size()), false);
         flags_init.push_back(INT_MAX);
         QrDesc q{e.S, e.total_rows, e.total_rows, e.cs, e.tcols, nullptr, nullptr, nullptr, nullptr, 0, 1};
         qd.push_back(q);
@@ -2162,7 +2219,7 @@ void Engine::sparsify_cols_all() {
             const int nsrc = static_cast<int>(j.rparts.size()) + 1;
             j.di = -1;
             if (j.nG > 0) {
-                j.di = gb.begin(j.G, j.cs, j.nG, j.cs, nsrc, 1);
+                j.di = gb.begin(j.G, j.cs, j.nG, j.cs, nsrc, 1, false);
                 gb.dst[j.di].trans = 1;
             }
             j.V = out_.warena->alloc_n<double>(static_cast<size_t>(j.cs) * std::max(j.kmax, 1));
