@@ -2386,7 +2386,7 @@ void Engine::sparsify_cols_all() {
                 const int r2 = rank[ji];
                 if (fm.nrows() > 0) {
                     const int di = mb.begin(fm.mat + static_cast<long long>(fm.keys[mq].col) * fm.ld, fm.ld, fm.nrows(), r2,
-                                            1, 1);
+                                            1, 1, false);
                     mb.source(di, 0) = AsmSrc{j.G + static_cast<long long>(j.seg[s]) * j.cs, j.cs, 1};
                     for (int q = 0; q < fm.nrows(); ++q) mb.row(di, q) = int4{-1, 0, 0, q};
                     mb.km(di, 0, 0) = 0;
