@@ -2552,10 +2552,18 @@ void Engine::merge_level() {
         if (fr_[c].live) fr_[c] = Front();
 #pragma omp parallel for schedule(dynamic, 512)
     for (long long c = 0; c < static_cast<long long>(holders_.size()); ++c) holders_[c].clear();
-    for (int g = 0; g < ng; ++g) {
-        const int P = gp[g];
-        fr_[P] = std::move(plans[g].nf);
-        for (const KeyRef& k : fr_[P].keys) holders_[k.key].add(P);
+    for (int g = 0; g < ng; ++g) fr_[gp[g]] = std::move(plans[g].nf);
+    {  // holder sets: counted first, so each set grows once (ascending P: already sorted)
+        std::vector<int> cnt(holders_.size(), 0);
+        for (int g = 0; g < ng; ++g)
+            for (const KeyRef& k : fr_[gp[g]].keys) ++cnt[k.key];
+#pragma omp parallel for schedule(dynamic, 512)
+        for (long long c = 0; c < static_cast<long long>(holders_.size()); ++c)
+            if (cnt[c]) holders_[c].v.reserve(cnt[c]);
+        for (int g = 0; g < ng; ++g) {
+            const int P = gp[g];
+            for (const KeyRef& k : fr_[P].keys) holders_[k.key].add(P);
+        }
     }
     // everything of this stage lived in arena cur_; the next stage starts clean
     sync();
