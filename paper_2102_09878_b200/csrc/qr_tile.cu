@@ -30,7 +30,7 @@ namespace spqr {
 
 namespace {
 
-constexpr int kNW = 8;  // warps per CTA
+constexpr int kNW = 4;  // warps per CTA
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -249,7 +249,8 @@ __device__ void tile_dmma(const QrDesc& d, const int4& wk, double* sm, int kmax,
             __syncwarp();
         }
     }
-    const int mt = wid & 3, nt = (wid >> 2) * 2;
+    constexpr int NQ = 16 / kNW;  // W column tiles per warp (W is 4 x 4 tiles of 8 x 8)
+    const int mt = wid & 3, nt = (wid >> 2) * NQ;
     for (int c0 = wk.y; c0 < wk.z; c0 += 32) {
         const int nc = min(32, wk.z - c0);
         __syncthreads();  // T ready / previous tile stored
@@ -271,36 +272,36 @@ __device__ void tile_dmma(const QrDesc& d, const int4& wk, double* sm, int kmax,
         }
         __syncthreads();
         // W = V^T X  (32 x 32): warp -> W rows 8 mt.., columns 8 nt.. (two tiles)
-        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        double acc[NQ][2] = {};
 #pragma unroll 8
         for (int k0 = 0; k0 < MP; k0 += 4) {
             const double a = sV[(k0 + t4) + (8 * mt + g) * LV];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) dmma884(acc[q][0], acc[q][1], a, sX[(k0 + t4) + (8 * (nt + q) + g) * LV]);
+            for (int q = 0; q < NQ; ++q) dmma884(acc[q][0], acc[q][1], a, sX[(k0 + t4) + (8 * (nt + q) + g) * LV]);
         }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < NQ; ++q) {
             sW[(8 * mt + g) + (8 * (nt + q) + 2 * t4) * LT] = acc[q][0];
             sW[(8 * mt + g) + (8 * (nt + q) + 2 * t4 + 1) * LT] = acc[q][1];
         }
         __syncthreads();
         // W = T^T W
-        double acc2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        double acc2[NQ][2] = {};
 #pragma unroll
         for (int k0 = 0; k0 < 32; k0 += 4) {
             const double a = sT[(k0 + t4) + (8 * mt + g) * LT];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) dmma884(acc2[q][0], acc2[q][1], a, sW[(k0 + t4) + (8 * (nt + q) + g) * LT]);
+            for (int q = 0; q < NQ; ++q) dmma884(acc2[q][0], acc2[q][1], a, sW[(k0 + t4) + (8 * (nt + q) + g) * LT]);
         }
         __syncthreads();
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < NQ; ++q) {
             sW[(8 * mt + g) + (8 * (nt + q) + 2 * t4) * LT] = acc2[q][0];
             sW[(8 * mt + g) + (8 * (nt + q) + 2 * t4 + 1) * LT] = acc2[q][1];
         }
         __syncthreads();
         // X -= V W: warp -> row tiles wid, wid + 8, ..., all four column tiles
-        for (int m8 = wid; m8 < MP / 8; m8 += 8) {
+        for (int m8 = wid; m8 < MP / 8; m8 += kNW) {
             double o[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
             for (int k0 = 0; k0 < 32; k0 += 4) {
@@ -334,10 +335,10 @@ __device__ void tile_dmma(const QrDesc& d, const int4& wk, double* sm, int kmax,
 // 8 row pairs {2(i*TPC + r), +1} in registers (16*TPC rows per column); one
 // reflector costs 8 shared-memory pair loads, 16 FMAs for the dot product,
 // log2(TPC) shuffles and 16 FMAs for the update, with no block barriers.
-// ~100 registers, so two CTAs share an SM and one's panel factorisation
-// overlaps the other's tile sweep.
+// ~120 registers; 4-warp CTAs, so four share an SM and their panel
+// factorisations overlap the others' tile sweeps.
 template <int TPC, bool WY>
-__global__ void __launch_bounds__(32 * kNW, 2) k_qr_tile(const QrDesc* __restrict__ ds, const int4* __restrict__ work,
+__global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_tile(const QrDesc* __restrict__ ds, const int4* __restrict__ work,
                                                       int* __restrict__ count) {
     constexpr int MP = 16 * TPC;  // padded rows (panel leading dimension)
     const int4 wk = work[blockIdx.x];
