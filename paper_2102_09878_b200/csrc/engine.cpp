@@ -959,6 +959,8 @@ private:
     void elim_pass1(Elim& e, Scratch& S);
     void elim_prep2(Elim& e, Scratch& S);
     void elim_commit2(Elim& e);
+    void flush_holder_removals();
+    std::vector<std::pair<int, int>> hrem_;  // (key, eliminated cluster) removals pending for the wave
     std::vector<Scratch> tscr_;
     std::vector<uint64_t> colmask_;
     void materialize_pending();
@@ -1384,9 +1386,35 @@ void Engine::elim_commit2(Elim& e) {
         fr_[tgt].scaled_ok = false;
         a = b;
     }
-    for (const KW& kw : fc.keys) holders_[kw.key].remove(c);
+    for (const KW& kw : fc.keys) hrem_.emplace_back(kw.key, c);  // removed in one pass per key after the wave
     gone_[c] = 1;
     fr_[c].live = false;
+}
+
+// the commits of one wave only add holders, so the eliminated clusters' removals
+// are batched: each touched set is normalised once and filtered in one pass
+void Engine::flush_holder_removals() {
+    if (hrem_.empty()) return;
+    std::sort(hrem_.begin(), hrem_.end());
+    std::vector<size_t> gs;
+    for (size_t i = 0; i < hrem_.size(); ++i)
+        if (i == 0 || hrem_[i].first != hrem_[i - 1].first) gs.push_back(i);
+    gs.push_back(hrem_.size());
+    const long long ng = static_cast<long long>(gs.size()) - 1;
+#pragma omp parallel for schedule(dynamic, 64) if (ng > 256)
+    for (long long g = 0; g < ng; ++g) {
+        HolderSet& h = holders_[hrem_[gs[g]].first];
+        h.norm();
+        size_t w = 0, q = gs[g];
+        const size_t qe = gs[g + 1];
+        for (size_t i = 0; i < h.v.size(); ++i) {
+            while (q < qe && hrem_[q].second < h.v[i]) ++q;
+            if (q < qe && hrem_[q].second == h.v[i]) continue;
+            h.v[w++] = h.v[i];
+        }
+        h.v.resize(w);
+    }
+    hrem_.clear();
 }
 
 // Materialise every pending (touched, still live) front with one gather.
@@ -1890,6 +1918,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         for (int t = 0; t < nvalid; ++t)
             if (el_[t].logic) throw std::logic_error(el_[t].err);
         for (int t = 0; t < nvalid; ++t) elim_commit2(el_[t]);
+        flush_holder_removals();
     }
     materialize_pending();
 }
