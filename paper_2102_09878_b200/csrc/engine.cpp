@@ -1047,6 +1047,17 @@ void Engine::init_fronts(const std::vector<int>& owner) {
             fr_[c].live = true;
         }
     std::vector<int> local(A_.m);
+    {  // rows (ascending) and a key-count bound per front, counted first so every list grows once
+        std::vector<int> nr(fr_.size(), 0);
+        std::vector<long long> nk(fr_.size(), 0);
+        for (Index r = 0; r < A_.m; ++r) ++nr[owner[r]];
+        for (Index k = 0; k < A_.nnz(); ++k) ++nk[owner[A_.i[k]]];
+#pragma omp parallel for schedule(dynamic, 1024)
+        for (long long c = 0; c < static_cast<long long>(fr_.size()); ++c) {
+            if (nr[c]) fr_[c].rows.reserve(nr[c]);
+            if (nk[c]) fr_[c].keys.reserve(std::min<long long>(nk[c], 64));
+        }
+    }
     for (Index r = 0; r < A_.m; ++r) {
         Front& f = fr_[owner[r]];
         local[r] = f.nrows();
