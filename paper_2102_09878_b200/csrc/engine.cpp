@@ -1495,7 +1495,8 @@ void Engine::materialize_pending() {
         }
         if (nf.nrows() == 0 || nf.ncols == 0) continue;
         const int nsrc = static_cast<int>(pl.bases.size() + pl.stacks.size());
-        pl.di = b.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, std::max(nsrc, 1), static_cast<int>(pl.ord.size()));
+        // every row map entry is written in phase C (one per pending row)
+        pl.di = b.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, std::max(nsrc, 1), static_cast<int>(pl.ord.size()), false);
     }
     // phase C (parallel): fill
 #pragma omp parallel for schedule(dynamic, 32)
@@ -1547,10 +1548,12 @@ void Engine::materialize_pending() {
     flush_assemble(b);
     mt2.reset();
     NScope mt3(nprof_, "mat.swap");
-    for (Plan& pl : plans) {
-        if (pl.f < 0 || pl.same) continue;
-        dfree(fr_[pl.f].mat, fr_[pl.f].big);  // the gather reading it is already enqueued
-        fr_[pl.f] = std::move(pl.nf);
+    for (Plan& pl : plans)
+        if (pl.f >= 0 && !pl.same) dfree(fr_[pl.f].mat, fr_[pl.f].big);  // the gather reading it is already enqueued
+#pragma omp parallel for schedule(dynamic, 64) if (plans.size() > 256)
+    for (long long t = 0; t < static_cast<long long>(plans.size()); ++t) {
+        Plan& pl = plans[t];
+        if (pl.f >= 0 && !pl.same) fr_[pl.f] = std::move(pl.nf);
     }
     // eliminated fronts and this wave's stacks are no longer referenced
     for (int f : pend_list_)
