@@ -1274,7 +1274,9 @@ struct BigWs {
         return p;
     }
 };
-BigWs g_ws_w[2], g_ws_t[2];  // [0]: trailing updates (main stream), [1]: panel phase (side stream)
+// Per-process workspaces of the blocked path (one GPU per process, one host thread per context,
+// as the C ABI requires): [0] trailing updates (main stream), [1] panel phase (side stream)
+BigWs g_ws_w[2], g_ws_t[2];
 
 // block reflector (KB columns at J0, kw valid, T in T_all with ld KB) applied
 // to columns [cbeg, cend) of every problem; gram != 0 computes V^T V instead
