@@ -30,6 +30,7 @@
 #include <omp.h>
 #endif
 #include <map>
+#include <mutex>
 #include <string>
 
 #include "dev.h"
@@ -354,6 +355,20 @@ struct PodVec {
     void clear() { n = 0; }
 };
 
+// Stage arenas and pinned staging buffers outlive one factorization: a new
+// Engine takes them from this pool (per device) and returns them, so repeated
+// factorizations in a process do not pay cudaMalloc / cudaMallocHost again.  The
+// pool is never destroyed (no CUDA calls during process teardown).
+struct ArenaPool {
+    std::mutex mu;
+    std::map<int, std::vector<std::unique_ptr<DeviceArena>>> dev;
+    std::vector<std::unique_ptr<PinnedArena>> pin;
+    static ArenaPool& get() {
+        static ArenaPool* p = new ArenaPool;
+        return *p;
+    }
+};
+
 // Assemble job builder (generic gather, dev.h).
 struct AsmBuilder {
     std::vector<AsmDst> dst;
@@ -450,6 +465,7 @@ public:
         {
             int dev = 0;
             CK(cudaGetDevice(&dev));
+            dev_ = dev;
             cudaMemPool_t pool;
             CK(cudaDeviceGetDefaultMemPool(&pool, dev));
             uint64_t thr = UINT64_MAX;
@@ -457,11 +473,42 @@ public:
         }
         CK(cudaEventCreate(&ev0_));
         CK(cudaEventCreate(&ev1_));
+        {  // stage arenas and pinned staging come from the process-wide pool (kept across factorizations)
+            ArenaPool& P = ArenaPool::get();
+            std::lock_guard<std::mutex> lk(P.mu);
+            auto& dv = P.dev[dev_];
+            for (auto& a : arena_) {
+                if (!dv.empty()) {
+                    a = std::move(dv.back());
+                    dv.pop_back();
+                } else {
+                    a = std::make_unique<DeviceArena>();
+                }
+            }
+            if (!P.pin.empty()) {
+                pin_ = std::move(P.pin.back());
+                P.pin.pop_back();
+            } else {
+                pin_ = std::make_unique<PinnedArena>();
+            }
+        }
         init_fronts(owner);
     }
     ~Engine() {
+        cudaStreamSynchronize(st_);  // nothing may still use the arenas when they go back to the pool
         cudaEventDestroy(ev0_);
         cudaEventDestroy(ev1_);
+        ArenaPool& P = ArenaPool::get();
+        std::lock_guard<std::mutex> lk(P.mu);
+        for (auto& a : arena_)
+            if (a) {
+                a->reset();
+                P.dev[dev_].push_back(std::move(a));
+            }
+        if (pin_) {
+            pin_->reset();
+            P.pin.push_back(std::move(pin_));
+        }
     }
 
     DeviceFactorization run();
@@ -478,9 +525,9 @@ private:
     std::vector<HolderSet> holders_;
     std::vector<std::vector<int>> stage_list_, tree_clusters_;
     DeviceFactorization out_;
-    DeviceArena arena_[2];
-    int cur_ = 0;
-    PinnedArena pin_;
+    std::unique_ptr<DeviceArena> arena_[2];
+    int cur_ = 0, dev_ = 0;
+    std::unique_ptr<PinnedArena> pin_;
     Index npiv_ = 0;
     int batch_ = 0;
     cudaEvent_t ev0_, ev1_;
@@ -517,7 +564,7 @@ private:
     int err_cluster_ = -1;
     std::string err_reason_;
 
-    DeviceArena& arena() { return arena_[cur_]; }
+    DeviceArena& arena() { return *arena_[cur_]; }
     // Large matrices (3D fronts, big stacks) are allocated stream-ordered and
     // released as soon as the launch that consumes them is enqueued, so a
     // stage's peak footprint is its live data, not everything it rebuilt.
@@ -533,7 +580,7 @@ private:
     void dfree(double* p, bool big) {
         if (big && p) CK(cudaFreeAsync(p, st_));
     }
-    Uploader up() { return Uploader{&arena(), &pin_, st_}; }
+    Uploader up() { return Uploader{&arena(), pin_.get(), st_}; }
     int width(int key) const { return static_cast<int>(cols_[key].size()); }
 
     void sync() {
@@ -542,7 +589,7 @@ private:
             CK(cudaStreamSynchronize(st_));
         }
         CK(cudaGetLastError());  // a failed launch must not pass silently
-        pin_.reset();
+        pin_->reset();
         kt_.resolve(out_.ctr);
         out_.ctr.syncs++;
     }
@@ -561,7 +608,7 @@ private:
         }
         h.resize(n);
         if (n == 0) return;
-        void* p = pin_.alloc(sizeof(T) * n);
+        void* p = pin_->alloc(sizeof(T) * n);
         CK(cudaMemcpyAsync(p, d, sizeof(T) * n, cudaMemcpyDeviceToHost, st_));
         dl_.push_back({h.data(), p, sizeof(T) * n});
         out_.ctr.d2h_bytes += sizeof(T) * n;
@@ -575,7 +622,7 @@ private:
         CK(cudaGetLastError());  // a failed launch must not pass silently
         for (auto& q : dl_) par_memcpy(q.host, q.pin, q.bytes);
         dl_.clear();
-        pin_.reset();
+        pin_->reset();
         kt_.resolve(out_.ctr);
         out_.ctr.syncs++;
     }
@@ -587,7 +634,7 @@ private:
         }
         h.resize(n);
         if (n == 0) return;
-        T* p = static_cast<T*>(pin_.alloc(sizeof(T) * n));
+        T* p = static_cast<T*>(pin_->alloc(sizeof(T) * n));
         CK(cudaMemcpyAsync(p, d, sizeof(T) * n, cudaMemcpyDeviceToHost, st_));
         sync();
         par_memcpy(h.data(), p, sizeof(T) * n);
@@ -2498,7 +2545,7 @@ void Engine::merge_level() {
             o += width(c);
         }
     }
-    DeviceArena& next = arena_[cur_ ^ 1];
+    DeviceArena& next = *arena_[cur_ ^ 1];
     std::unique_ptr<NScope> m1 = std::make_unique<NScope>(nprof_, "merge.descriptors");
     AsmBuilder& mb = asm_slot(5);  // keeps its capacity across calls
     struct Plan {
@@ -2610,7 +2657,7 @@ void Engine::merge_level() {
     }
     // everything of this stage lived in arena cur_; the next stage starts clean
     sync();
-    arena_[cur_].reset();
+    arena_[cur_]->reset();
     cur_ ^= 1;
 }
 
