@@ -359,10 +359,12 @@ struct PodVec {
 // Engine takes them from this pool (per device) and returns them, so repeated
 // factorizations in a process do not pay cudaMalloc / cudaMallocHost again.  The
 // pool is never destroyed (no CUDA calls during process teardown).
+struct HostBuilders;
 struct ArenaPool {
     std::mutex mu;
     std::map<int, std::vector<std::unique_ptr<DeviceArena>>> dev;
     std::vector<std::unique_ptr<PinnedArena>> pin;
+    std::vector<std::unique_ptr<HostBuilders>> host;
     static ArenaPool& get() {
         static ArenaPool* p = new ArenaPool;
         return *p;
@@ -428,6 +430,11 @@ struct AsmBuilder {
     }
 };
 
+struct HostBuilders {
+    AsmBuilder wcopy;    // W copies + materialised fronts
+    AsmBuilder slot[6];  // one per gather call site
+};
+
 // key indices of a front in physical column order
 inline void phys_order(const std::vector<KeyRef>& keys, std::vector<int>& ord) {
     ord.resize(keys.size());
@@ -491,6 +498,13 @@ public:
             } else {
                 pin_ = std::make_unique<PinnedArena>();
             }
+            if (!P.host.empty()) {
+                hp_ = std::move(P.host.back());
+                P.host.pop_back();
+            } else {
+                hp_ = std::make_unique<HostBuilders>();
+            }
+            hp_->wcopy.clear();
         }
         init_fronts(owner);
     }
@@ -509,6 +523,7 @@ public:
             pin_->reset();
             P.pin.push_back(std::move(pin_));
         }
+        if (hp_) P.host.push_back(std::move(hp_));
     }
 
     DeviceFactorization run();
@@ -552,11 +567,10 @@ private:
     std::vector<char> mark_;
     std::vector<int> stage_of_;
     std::vector<std::pair<int, int>> dep_;
-    AsmBuilder wcopy_;
-    AsmBuilder asm_pool_[6];  // one per call site: vectors keep their capacity between waves
-    AsmBuilder& asm_slot(int i) {
-        asm_pool_[i].clear();
-        return asm_pool_[i];
+    std::unique_ptr<HostBuilders> hp_;  // assemble builders, pooled across factorizations
+    AsmBuilder& asm_slot(int i) {  // one per call site: vectors keep their capacity
+        hp_->slot[i].clear();
+        return hp_->slot[i];
     }
     dl_vector<double> pre_sq_, post_sq_;
     dl_vector<unsigned char> pre_nz_, post_nz_;
@@ -1395,15 +1409,15 @@ void Engine::elim_commit2(Elim& e) {
         const int kept = e.kept;
         DevWFactor& f = new_factor(0, c, cs, kept, cols_[c], &e.coupled);
         f.a = out_.warena->alloc_n<double>(static_cast<size_t>(cs) * (cs + kept));
-        const int di = wcopy_.begin(f.a, cs, cs, cs + kept, 1, 1 + static_cast<int>(e.keepk.size()));
-        wcopy_.source(di, 0) = AsmSrc{e.S, 1, e.total_rows};
-        for (int i = 0; i < cs; ++i) wcopy_.row(di, i) = int4{-1, 0, 0, i};
-        wcopy_.seg(di, 0, 0);
-        wcopy_.km(di, 0, 0) = 0;
+        const int di = hp_->wcopy.begin(f.a, cs, cs, cs + kept, 1, 1 + static_cast<int>(e.keepk.size()));
+        hp_->wcopy.source(di, 0) = AsmSrc{e.S, 1, e.total_rows};
+        for (int i = 0; i < cs; ++i) hp_->wcopy.row(di, i) = int4{-1, 0, 0, i};
+        hp_->wcopy.seg(di, 0, 0);
+        hp_->wcopy.km(di, 0, 0) = 0;
         int o = cs;
         for (size_t q = 0; q < e.keepk.size(); ++q) {
-            wcopy_.seg(di, static_cast<int>(q) + 1, o);
-            wcopy_.km(di, static_cast<int>(q) + 1, 0) = e.off[e.keepk[q]];
+            hp_->wcopy.seg(di, static_cast<int>(q) + 1, o);
+            hp_->wcopy.km(di, static_cast<int>(q) + 1, 0) = e.off[e.keepk[q]];
             o += width(e.keys[e.keepk[q]]);
         }
     }
@@ -1479,7 +1493,7 @@ void Engine::flush_holder_removals() {
 void Engine::materialize_pending() {
     ProfScope ps_(prof_, HostProf::MATER);
     std::unique_ptr<NScope> mt1 = std::make_unique<NScope>(nprof_, "mat.descriptors");
-    AsmBuilder& b = wcopy_;  // W copies already queued; fronts go in the same launch
+    AsmBuilder& b = hp_->wcopy;  // W copies already queued; fronts go in the same launch
     struct Plan {
         int f = -1;
         bool same = false;
@@ -1896,7 +1910,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
             }
         }
     }
-    wcopy_.clear();
+    hp_->wcopy.clear();
     double *d_psq = nullptr;
     unsigned char* d_pnz = nullptr;
     if (!qd.empty()) {
