@@ -31,6 +31,7 @@
 #endif
 #include <map>
 #include <mutex>
+#include <thread>
 #include <string>
 
 #include "dev.h"
@@ -509,6 +510,19 @@ public:
         init_fronts(owner);
     }
     ~Engine() {
+        {  // the per-cluster host containers (hundreds of thousands of small vectors) are
+           // freed on a background thread instead of on the caller's critical path
+            struct Trash {
+                std::vector<Front> fr;
+                std::vector<std::vector<int>> cols, sl, tc, sb;
+                std::vector<HolderSet> holders;
+                std::deque<PFront> pend;
+                std::vector<Elim> el;
+            };
+            auto* t = new Trash{std::move(fr_),      std::move(cols_),    std::move(stage_list_), std::move(tree_clusters_),
+                                std::move(sb_bases_), std::move(holders_), std::move(pend_),      std::move(el_)};
+            std::thread([t] { delete t; }).detach();
+        }
         cudaStreamSynchronize(st_);  // nothing may still use the arenas when they go back to the pool
         cudaEventDestroy(ev0_);
         cudaEventDestroy(ev1_);
@@ -2762,8 +2776,19 @@ DeviceFactorization gpu_factorize(const Csc& A, const ClusterHierarchy& h, const
     if (A.m < A.n) throw std::invalid_argument("matrix must have at least as many rows as columns");
     if (static_cast<Index>(owner.size()) != A.m) throw std::invalid_argument("row_owner size mismatch");
     sampler_start();
-    Engine e(A, h, owner, opt, st);
-    DeviceFactorization F = e.run();
+    static const bool prof = std::getenv("SPQR_PROF") != nullptr;
+    const double t0 = now_s();
+    DeviceFactorization F;
+    double t1 = 0, t2 = 0;
+    {
+        Engine e(A, h, owner, opt, st);
+        t1 = now_s();
+        F = e.run();
+        t2 = now_s();
+    }
+    if (prof)
+        std::fprintf(stderr, "[spqr prof] engine construct %.3f s  run %.3f s  teardown %.3f s\n", t1 - t0, t2 - t1,
+                     now_s() - t2);
     sampler_stop();
     return F;
 }

@@ -7,13 +7,19 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
 
 namespace spqr {
 
 SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
     SolvePlan P;
     P.mem = std::make_unique<DeviceArena>(size_t(64) << 20);
-    PinnedArena pin;
+    // pinned staging kept across plans (pinning 64 MB per call cost tens of ms)
+    static std::mutex pin_mu;
+    static PinnedArena* pin_cache = new PinnedArena();  // never freed: no CUDA calls at exit
+    std::lock_guard<std::mutex> pin_lock(pin_mu);
+    PinnedArena& pin = *pin_cache;
+    pin.reset();
     Uploader up{P.mem.get(), &pin, st};
     const int* d_idx = up.put(F.idx);
     // group factors by batch (batch ids increase chronologically; within a
@@ -30,7 +36,7 @@ SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
         while (j < ord.size() && F.W[ord[j]].batch == F.W[ord[i]].batch) ++j;
         std::vector<WFac> fac, bfac;
         long long contrib = 0;
-        std::map<int, std::vector<int>> lists;  // coupled column -> contribution indices (chronological)
+        std::vector<std::pair<int, int>> lists;  // (coupled column, contribution index), chronological
         int maxc = 1, bmaxc = 1;
         for (size_t q = i; q < j; ++q) {
             const DevWFactor& w = F.W[ord[q]];
@@ -45,7 +51,7 @@ SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
             f.sign = w.sign;
             f.contrib_off = contrib;
             if (w.kind == 0 && w.k > 0) {
-                for (int t = 0; t < w.k; ++t) lists[F.idx[w.coupled_off + t]].push_back(static_cast<int>(contrib + t));
+                for (int t = 0; t < w.k; ++t) lists.emplace_back(F.idx[w.coupled_off + t], static_cast<int>(contrib + t));
                 contrib += w.k;
             }
             // triangular factors: the warp path's back substitution is c sequential
@@ -67,11 +73,17 @@ SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
         b.nbf = static_cast<int>(bfac.size());
         b.bmaxc = bmaxc;
         if (!lists.empty()) {
+            // per coupled column (ascending), its contributions in chronological order:
+            // the indices increase with time, so sorting the pairs gives exactly that
+            std::sort(lists.begin(), lists.end());
             std::vector<int> ptr{0}, idx, col;
-            for (auto& [c, l] : lists) {
-                col.push_back(c);
-                idx.insert(idx.end(), l.begin(), l.end());
+            idx.reserve(lists.size());
+            for (size_t a = 0; a < lists.size();) {
+                size_t e = a;
+                while (e < lists.size() && lists[e].first == lists[a].first) idx.push_back(lists[e++].second);
+                col.push_back(lists[a].first);
                 ptr.push_back(static_cast<int>(idx.size()));
+                a = e;
             }
             b.rptr = up.put(ptr);
             b.ridx = up.put(idx);
