@@ -116,7 +116,7 @@ private:
 // Large host copies (pinned staging <-> host vectors) split over the OpenMP
 // threads: a single thread's memcpy is memory-latency bound far below DRAM speed.
 inline void par_memcpy(void* dst, const void* src, size_t bytes) {
-    constexpr size_t kChunk = size_t(256) << 10;
+    constexpr size_t kChunk = size_t(64) << 10;
     if (bytes < 4 * kChunk) {
         std::memcpy(dst, src, bytes);
         return;

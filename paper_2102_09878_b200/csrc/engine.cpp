@@ -1661,7 +1661,7 @@ void Engine::compute_stats(const std::vector<int>& P) {
         wcount[t + 1] = wcount[t] + static_cast<long long>(nk) * F.nrows();
     }
     const long long work = wcount[nP];
-    std::vector<StatDesc> sd(dcount[nP]);
+    dl_vector<StatDesc> sd(dcount[nP]);  // every entry is written by the fill below
 #pragma omp parallel for schedule(dynamic, 256)
     for (long long t = 0; t < static_cast<long long>(nP); ++t) {
         Front& F = fr_[P[t]];
@@ -1679,7 +1679,7 @@ void Engine::compute_stats(const std::vector<int>& P) {
     unsigned char* d_nz = arena().alloc_n<unsigned char>(std::max<long long>(work, 1));
     if (!sd.empty()) {
         Uploader u = up();
-        const StatDesc* dd = u.put(sd);
+        const StatDesc* dd = u.put(sd.data(), sd.size());
         out_.ctr.h2d_bytes += u.bytes_h2d;
         double sb = 0;
         for (auto& q : sd) sb += 8.0 * q.nrows * q.ncols + 9.0 * q.nrows;
@@ -1861,6 +1861,14 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         if (el_[ei].cs <= 0) continue;
         for (const PRow& r : el_[ei].srows)
             if (std::find(bases.begin(), bases.end(), r.base) == bases.end()) bases.push_back(r.base);
+    }
+    {
+        size_t npd = 0;
+        for (int ei = 0; ei < nvalid; ++ei)
+            if (el_[ei].cs > 0) npd += 1 + 2 * el_[ei].keys.size();
+        pd.reserve(npd);
+        qd.reserve(nvalid);
+        flags_init.reserve(nvalid);
     }
     for (int ei = 0; ei < nvalid; ++ei) {
         Elim& e = el_[ei];
