@@ -184,18 +184,27 @@ struct NamedProf {
         return v.back().second;
     }
 };
+// the host-profile scopes only read the clock when SPQR_PROF is set (they are on
+// every wave's path)
+inline bool host_prof_on() {
+    static const bool on = std::getenv("SPQR_PROF") != nullptr;
+    return on;
+}
 struct NScope {
     double& t;
     double t0;
-    NScope(NamedProf& p, const char* n) : t(p.slot(n)), t0(now_s()) {}
-    ~NScope() { t += now_s() - t0; }
+    NScope(NamedProf& p, const char* n) : t(p.slot(n)), t0(host_prof_on() ? now_s() : 0.0) {}
+    ~NScope() {
+        if (host_prof_on()) t += now_s() - t0;
+    }
 };
 struct ProfScope {
     HostProf& p;
     int i;
     double t0;
-    ProfScope(HostProf& p_, int i_) : p(p_), i(i_), t0(now_s()) {}
+    ProfScope(HostProf& p_, int i_) : p(p_), i(i_), t0(host_prof_on() ? now_s() : 0.0) {}
     ~ProfScope() {
+        if (!host_prof_on()) return;
         p.t[i] += now_s() - t0;
         p.n[i]++;
     }
