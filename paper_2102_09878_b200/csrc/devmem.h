@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -128,6 +129,18 @@ inline void par_memcpy(void* dst, const void* src, size_t bytes) {
         std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, std::min(kChunk, bytes - off));
     }
 }
+
+// Process-wide pinned staging for one-shot uploads (solve plans, matrices): pinning a fresh
+// 64 MB buffer per call cost tens of ms.  Callers hold `mu` until their copies have completed;
+// never destroyed (no CUDA calls during process teardown).
+struct SharedPinned {
+    std::mutex mu;
+    PinnedArena arena;
+    static SharedPinned& get() {
+        static SharedPinned* s = new SharedPinned;
+        return *s;
+    }
+};
 
 // Uploads host vectors through pinned memory into a device arena.
 struct Uploader {

@@ -14,11 +14,9 @@ namespace spqr {
 SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
     SolvePlan P;
     P.mem = std::make_unique<DeviceArena>(size_t(64) << 20);
-    // pinned staging kept across plans (pinning 64 MB per call cost tens of ms)
-    static std::mutex pin_mu;
-    static PinnedArena* pin_cache = new PinnedArena();  // never freed: no CUDA calls at exit
-    std::lock_guard<std::mutex> pin_lock(pin_mu);
-    PinnedArena& pin = *pin_cache;
+    SharedPinned& sp = SharedPinned::get();
+    std::lock_guard<std::mutex> pin_lock(sp.mu);
+    PinnedArena& pin = sp.arena;
     pin.reset();
     Uploader up{P.mem.get(), &pin, st};
     const int* d_idx = up.put(F.idx);
@@ -144,8 +142,10 @@ DevMatrix upload_matrix(const Csc& A, cudaStream_t st) {
             ri[pos[A.i[k]]] = j;
             rv[pos[A.i[k]]++] = A.x[k];
         }
-    PinnedArena pin;
-    Uploader up{D.mem.get(), &pin, st};
+    SharedPinned& sp = SharedPinned::get();
+    std::lock_guard<std::mutex> pin_lock(sp.mu);
+    sp.arena.reset();
+    Uploader up{D.mem.get(), &sp.arena, st};
     D.rp = up.put(rp);
     D.ri = up.put(ri);
     D.rv = up.put(rv);
