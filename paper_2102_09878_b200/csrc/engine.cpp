@@ -440,6 +440,15 @@ struct AsmBuilder {
     }
 };
 
+// materialize_pending's per-front plan (kept by the engine between calls)
+struct MatPlan {
+    int f = -1;
+    bool same = false;
+    Front nf;
+    std::vector<int> bases, stacks, ord;
+    int di = -1;
+};
+
 struct HostBuilders {
     AsmBuilder wcopy;    // W copies + materialised fronts
     AsmBuilder slot[6];  // one per gather call site
@@ -527,9 +536,11 @@ public:
                 std::vector<HolderSet> holders;
                 std::deque<PFront> pend;
                 std::vector<Elim> el;
+                std::vector<MatPlan> plans;
             };
             auto* t = new Trash{std::move(fr_),      std::move(cols_),    std::move(stage_list_), std::move(tree_clusters_),
-                                std::move(sb_bases_), std::move(holders_), std::move(pend_),      std::move(el_)};
+                                std::move(sb_bases_), std::move(holders_), std::move(pend_),      std::move(el_),
+                                std::move(mplans_)};
             std::thread([t] { delete t; }).detach();
         }
         cudaStreamSynchronize(st_);  // nothing may still use the arenas when they go back to the pool
@@ -591,6 +602,7 @@ private:
     std::vector<int> stage_of_;
     std::vector<std::pair<int, int>> dep_;
     std::unique_ptr<HostBuilders> hp_;  // assemble builders, pooled across factorizations
+    std::vector<MatPlan> mplans_;       // materialize_pending plans, reused between waves
     AsmBuilder& asm_slot(int i) {  // one per call site: vectors keep their capacity
         hp_->slot[i].clear();
         return hp_->slot[i];
@@ -1517,23 +1529,32 @@ void Engine::materialize_pending() {
     ProfScope ps_(prof_, HostProf::MATER);
     std::unique_ptr<NScope> mt1 = std::make_unique<NScope>(nprof_, "mat.descriptors");
     AsmBuilder& b = hp_->wcopy;  // W copies already queued; fronts go in the same launch
-    struct Plan {
-        int f = -1;
-        bool same = false;
-        Front nf;
-        std::vector<int> bases, stacks, ord;
-        int di = -1;
-    };
-    std::vector<Plan> plans(pend_list_.size());
+    // plans persist across calls: a plan's new front is swapped into fr_, so the
+    // superseded front's vectors come back here and are reused next time (no
+    // malloc / free per front and wave)
+    using Plan = MatPlan;
+    const size_t nplan = pend_list_.size();
+    if (mplans_.size() < nplan) mplans_.resize(nplan);
+    std::vector<Plan>& plans = mplans_;
     // phase A (parallel): new row / key lists, layout, sources
 #pragma omp parallel for schedule(dynamic, 32)
-    for (long long t = 0; t < static_cast<long long>(pend_list_.size()); ++t) {
+    for (long long t = 0; t < static_cast<long long>(nplan); ++t) {
         const int f = pend_list_[t];
         Plan& pl = plans[t];
+        pl.f = -1;
+        pl.same = false;
+        pl.di = -1;
+        pl.bases.clear();
+        pl.stacks.clear();
+        pl.ord.clear();
         if (!fr_[f].live) continue;
         pl.f = f;
         const PFront& P = pend_[pend_id_[f]];
         Front& nf = pl.nf;
+        nf.mat = nullptr;
+        nf.big = false;
+        nf.soff.clear();
+        nf.tag.clear();
         nf.live = true;
         nf.scaled_ok = fr_[f].scaled_ok;
         nf.rows.resize(P.rows.size());
@@ -1565,7 +1586,8 @@ void Engine::materialize_pending() {
         phys_order(nf.keys, pl.ord);
     }
     // phase B (sequential): allocation and descriptor reservation
-    for (Plan& pl : plans) {
+    for (size_t t = 0; t < nplan; ++t) {
+        Plan& pl = plans[t];
         if (pl.f < 0 || pl.same) continue;
         Front& nf = pl.nf;
         nf.mat = dalloc(arena(), static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1), nf.big);
@@ -1584,7 +1606,7 @@ void Engine::materialize_pending() {
     }
     // phase C (parallel): fill
 #pragma omp parallel for schedule(dynamic, 32)
-    for (long long t = 0; t < static_cast<long long>(plans.size()); ++t) {
+    for (long long t = 0; t < static_cast<long long>(nplan); ++t) {
         Plan& pl = plans[t];
         if (pl.di < 0) continue;
         const int di = pl.di;
@@ -1632,12 +1654,14 @@ void Engine::materialize_pending() {
     flush_assemble(b);
     mt2.reset();
     NScope mt3(nprof_, "mat.swap");
-    for (Plan& pl : plans)
-        if (pl.f >= 0 && !pl.same) dfree(fr_[pl.f].mat, fr_[pl.f].big);  // the gather reading it is already enqueued
-#pragma omp parallel for schedule(dynamic, 64) if (plans.size() > 256)
-    for (long long t = 0; t < static_cast<long long>(plans.size()); ++t) {
+    for (size_t t = 0; t < nplan; ++t) {
         Plan& pl = plans[t];
-        if (pl.f >= 0 && !pl.same) fr_[pl.f] = std::move(pl.nf);
+        if (pl.f >= 0 && !pl.same) dfree(fr_[pl.f].mat, fr_[pl.f].big);  // the gather reading it is already enqueued
+    }
+#pragma omp parallel for schedule(dynamic, 64) if (nplan > 256)
+    for (long long t = 0; t < static_cast<long long>(nplan); ++t) {
+        Plan& pl = plans[t];
+        if (pl.f >= 0 && !pl.same) std::swap(fr_[pl.f], pl.nf);  // old front's storage is recycled
     }
     // eliminated fronts and this wave's stacks are no longer referenced
     for (int f : pend_list_)
