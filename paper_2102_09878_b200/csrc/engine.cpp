@@ -71,6 +71,19 @@ struct Front {
         return (it != keys.end() && it->key == key) ? static_cast<int>(it - keys.begin()) : -1;
     }
     int nrows() const { return static_cast<int>(rows.size()); }
+    // dead after a merge: emptied but keeps its storage (freed with the engine, off the
+    // critical path) — freeing ~10^5 small vectors per merge contended on malloc's locks
+    void retire() {
+        live = false;
+        rows.clear();
+        keys.clear();
+        mat = nullptr;
+        big = false;
+        ld = ncols = 0;
+        scaled_ok = false;
+        soff.clear();
+        tag.clear();
+    }
 };
 
 // symbolic row: values of old front `base` row `brow`, overridden by stack
@@ -2708,7 +2721,7 @@ void Engine::merge_level() {
         if (fr_[c].live && fr_[c].big) dfree(fr_[c].mat, true);
 #pragma omp parallel for schedule(dynamic, 512)
     for (long long c = 0; c < static_cast<long long>(fr_.size()); ++c)
-        if (fr_[c].live) fr_[c] = Front();
+        if (fr_[c].live) fr_[c].retire();
 #pragma omp parallel for schedule(dynamic, 512)
     for (long long c = 0; c < static_cast<long long>(holders_.size()); ++c) holders_[c].clear();
     for (int g = 0; g < ng; ++g) fr_[gp[g]] = std::move(plans[g].nf);
