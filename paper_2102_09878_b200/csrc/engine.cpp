@@ -2744,18 +2744,32 @@ void Engine::merge_level() {
 }
 
 void Engine::snapshot(StageStats& st) {  // factorize.cpp:731-743
-    for (size_t c = 0; c < fr_.size(); ++c) {
-        const Front& f = fr_[c];
-        if (!f.live) continue;
-        const int cs = width(static_cast<int>(c));
-        if (cs > 0) {
-            st.front_cols.push_back(cs);
-            st.front_aspect.push_back(static_cast<double>(f.nrows()) / cs);
+    // ascending cluster order (the reference iterates its std::map); blocks of clusters
+    // are scanned in parallel and concatenated in order
+    const long long nc = static_cast<long long>(fr_.size());
+    constexpr long long kBlk = 4096;
+    const long long nb = (nc + kBlk - 1) / kBlk;
+    std::vector<std::vector<std::pair<int, double>>> part(nb);
+    std::vector<long long> trows(nb, 0), tcols(nb, 0);
+#pragma omp parallel for schedule(static)
+    for (long long q = 0; q < nb; ++q)
+        for (long long c = q * kBlk; c < std::min(nc, (q + 1) * kBlk); ++c) {
+            const Front& f = fr_[c];
+            if (!f.live) continue;
+            const int cs = width(static_cast<int>(c));
+            if (cs > 0) part[q].emplace_back(cs, static_cast<double>(f.nrows()) / cs);
+            if (h_.clusters[c].tree_node == h_.tree->root) {
+                trows[q] += f.nrows();
+                tcols[q] += cs;
+            }
         }
-        if (h_.clusters[c].tree_node == h_.tree->root) {
-            st.top_rows += f.nrows();
-            st.top_cols += cs;
+    for (long long q = 0; q < nb; ++q) {
+        for (const auto& pc : part[q]) {
+            st.front_cols.push_back(pc.first);
+            st.front_aspect.push_back(pc.second);
         }
+        st.top_rows += trows[q];
+        st.top_cols += tcols[q];
     }
 }
 

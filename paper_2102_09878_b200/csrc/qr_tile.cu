@@ -30,7 +30,9 @@ namespace spqr {
 
 namespace {
 
-constexpr int kNW = 4;  // warps per CTA
+// warps per CTA by row class: 4 for panels of up to 128 rows (four CTAs per SM), 8 above
+template <int TPC>
+constexpr int nw_of() { return TPC <= 8 ? 4 : 8; }
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -79,7 +81,7 @@ __device__ __forceinline__ void apply_panel(double* P, int ldp, int m, int k, in
 // thread forms the same Householder scalars, the owners publish v (barrier),
 // every column reduces its dot product with v across warps (barrier) and
 // updates its rows.  The factored panel is written back to P.
-template <int MP>
+template <int MP, int kNW>
 __device__ void panel_regs(double* P, int m, int n, int kmax, double* s_tau) {
     constexpr int RPT = MP / kNW;
     __shared__ double red[kNW], vsh[MP], part[kNW][32];
@@ -186,7 +188,7 @@ __host__ __device__ constexpr int dmma_tile_doubles(int MP) { return 2 * (MP + 4
 // W = T^T W, X -= V W (apply_raw's blocked branch, dense_kernels.cpp:61-69).
 // Leading dimensions are = 4 (mod 16) doubles so every fragment load is two
 // conflict-free wavefronts.
-template <int MP>
+template <int MP, int kNW>
 __device__ void tile_dmma(const QrDesc& d, const int4& wk, double* sm, int kmax, const double* s_tau,
                           const unsigned char* s_neg) {
     constexpr int LV = MP + 4, LT = 36;
@@ -337,7 +339,7 @@ __device__ void tile_dmma(const QrDesc& d, const int4& wk, double* sm, int kmax,
 // log2(TPC) shuffles and 16 FMAs for the update, with no block barriers.
 // ~120 registers; 4-warp CTAs, so four share an SM and their panel
 // factorisations overlap the others' tile sweeps.
-template <int TPC, bool WY>
+template <int TPC, bool WY, int kNW = nw_of<TPC>()>
 __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_tile(const QrDesc* __restrict__ ds, const int4* __restrict__ work,
                                                       int* __restrict__ count) {
     constexpr int MP = 16 * TPC;  // padded rows (panel leading dimension)
@@ -381,7 +383,7 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_tile(const QrDesc* __
     // ---- panel factorisation
     if (MP <= 256 && n <= 32) {
         __syncthreads();
-        panel_regs<(MP <= 256 ? MP : 256)>(P, m, n, kmax, s_tau);
+        panel_regs<(MP <= 256 ? MP : 256), kNW>(P, m, n, kmax, s_tau);
     } else {  // smem panel, warp per column, one barrier per reflector (look-ahead)
         if (kmax > 0 && wid == 0) make_reflector(P, MP, m, 0, s_tau);
         __syncthreads();
@@ -423,7 +425,7 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_tile(const QrDesc* __
     if (wk.z <= wk.y) return;
     __syncthreads();
     if (WY && MP <= 256 && n <= 32) {  // compact-WY tile phase on DMMA (SPQR_TILE_DMMA=1)
-        tile_dmma<(MP <= 256 ? MP : 256)>(d, wk, P, kmax, s_tau, s_neg);
+        tile_dmma<(MP <= 256 ? MP : 256), kNW>(d, wk, P, kmax, s_tau, s_neg);
         return;
     }
     // ---- explicit reflectors: V(:, k) = [0; 1; v], zero rows >= m
@@ -511,11 +513,11 @@ void launch_tile(const QrDesc* dd, const int4* dw, int nwork, size_t smem, int* 
     if (tile_dmma_enabled()) {
         static size_t configured = 0;
         smem_optin(reinterpret_cast<const void*>(k_qr_tile<TPC, true>), smem, configured);
-        k_qr_tile<TPC, true><<<nwork, 32 * kNW, smem, st>>>(dd, dw, count);
+        k_qr_tile<TPC, true><<<nwork, 32 * nw_of<TPC>(), smem, st>>>(dd, dw, count);
     } else {
         static size_t configured = 0;
         smem_optin(reinterpret_cast<const void*>(k_qr_tile<TPC, false>), smem, configured);
-        k_qr_tile<TPC, false><<<nwork, 32 * kNW, smem, st>>>(dd, dw, count);
+        k_qr_tile<TPC, false><<<nwork, 32 * nw_of<TPC>(), smem, st>>>(dd, dw, count);
     }
 }
 
