@@ -488,6 +488,7 @@ public:
         fr_.resize(nc);
         cols_.resize(nc);
         gone_.assign(nc, 0);
+        alive_.assign(nc, 0);
         holders_.resize(nc);
         pend_id_.assign(nc, -1);
         mark_.assign(nc, 0);
@@ -584,6 +585,7 @@ private:
     std::vector<Front> fr_;
     std::vector<std::vector<int>> cols_;
     std::vector<char> gone_;
+    std::vector<char> alive_;  // mirror of fr_[c].live, scanned instead of the Front objects
     std::vector<HolderSet> holders_;
     std::vector<std::vector<int>> stage_list_, tree_clusters_;
     DeviceFactorization out_;
@@ -1154,6 +1156,7 @@ void Engine::init_fronts(const std::vector<int>& owner) {
         if (h_.clusters[c].level == Lf) {
             cols_[c] = h_.clusters[c].cols;
             fr_[c].live = true;
+            alive_[c] = 1;
         }
     std::vector<int> local(A_.m);
     {  // rows (ascending) and a key-count bound per front, counted first so every list grows once
@@ -1509,6 +1512,7 @@ void Engine::elim_commit2(Elim& e) {
     for (const KW& kw : fc.keys) hrem_.emplace_back(kw.key, c);  // removed in one pass per key after the wave
     gone_[c] = 1;
     fr_[c].live = false;
+    alive_[c] = 0;
 }
 
 // the commits of one wave only add holders, so the eliminated clusters' removals
@@ -1766,7 +1770,8 @@ std::vector<int> Engine::stage_fronts(const std::vector<int>& list) {
 void Engine::eliminate_stage(int k) {
     const auto& list = stage_list_[k];
     if (list.empty()) return;
-    for (size_t f = 0; f < fr_.size(); ++f) fr_[f].tag.clear();
+    for (size_t f = 0; f < fr_.size(); ++f)
+        if (alive_[f]) fr_[f].tag.clear();
     std::vector<int> P = stage_fronts(list);
     compute_stats(P);
     std::vector<int> lvl(fr_.size(), -1);
@@ -2072,6 +2077,7 @@ void Engine::scale_all() {
     std::vector<int> cand;
     std::vector<StatDesc> sd;
     for (size_t p = 0; p < fr_.size(); ++p) {
+        if (!alive_[p]) continue;
         Front& f = fr_[p];
         if (!f.live) continue;
         f.scaled_ok = false;
@@ -2184,6 +2190,7 @@ void Engine::sparsify_rows_all() {
     int maxm = 0;
     for (size_t pp = 0; pp < fr_.size(); ++pp) {
         const int p = static_cast<int>(pp);
+        if (!alive_[p]) continue;
         Front& f = fr_[p];
         if (!f.live) continue;
         const int cs = width(p);
@@ -2292,7 +2299,7 @@ void Engine::sparsify_cols_all() {
     ProfScope ps_(prof_, HostProf::SCOLS);
     std::vector<int> elig;
     for (size_t p = 0; p < fr_.size(); ++p)
-        if (fr_[p].live && width(static_cast<int>(p)) > 0 && fr_[p].scaled_ok) elig.push_back(static_cast<int>(p));
+        if (alive_[p] && fr_[p].live && width(static_cast<int>(p)) > 0 && fr_[p].scaled_ok) elig.push_back(static_cast<int>(p));
     if (elig.empty()) return;
     // Speculative rounds: every pending interface is factored from the
     // current data; in ascending order a result is accepted unless a lower
@@ -2601,7 +2608,7 @@ void Engine::merge_level() {
     {
         std::vector<std::pair<int, int>> pk;  // (parent, kid)
         for (size_t c = 0; c < fr_.size(); ++c)
-            if (fr_[c].live) pk.emplace_back(h_.clusters[c].parent, static_cast<int>(c));
+            if (alive_[c] && fr_[c].live) pk.emplace_back(h_.clusters[c].parent, static_cast<int>(c));
         std::sort(pk.begin(), pk.end());
         for (size_t i = 0; i < pk.size(); ++i) {
             if (pk[i].first < 0) throw std::logic_error("spaqr engine: live front without a parent cluster at merge");
@@ -2718,13 +2725,19 @@ void Engine::merge_level() {
     std::unique_ptr<NScope> m2 = std::make_unique<NScope>(nprof_, "merge.flush+rebuild_host");
     flush_assemble(mb);
     for (size_t c = 0; c < fr_.size(); ++c)
-        if (fr_[c].live && fr_[c].big) dfree(fr_[c].mat, true);
+        if (alive_[c] && fr_[c].live && fr_[c].big) dfree(fr_[c].mat, true);
 #pragma omp parallel for schedule(dynamic, 512)
     for (long long c = 0; c < static_cast<long long>(fr_.size()); ++c)
-        if (fr_[c].live) fr_[c].retire();
+        if (fr_[c].live) {
+            fr_[c].retire();
+            alive_[c] = 0;
+        }
 #pragma omp parallel for schedule(dynamic, 512)
     for (long long c = 0; c < static_cast<long long>(holders_.size()); ++c) holders_[c].clear();
-    for (int g = 0; g < ng; ++g) fr_[gp[g]] = std::move(plans[g].nf);
+    for (int g = 0; g < ng; ++g) {
+        fr_[gp[g]] = std::move(plans[g].nf);
+        alive_[gp[g]] = 1;
+    }
     {  // holder sets: counted first, so each set grows once (ascending P: already sorted)
         std::vector<int> cnt(holders_.size(), 0);
         for (int g = 0; g < ng; ++g)
