@@ -2728,7 +2728,7 @@ void Engine::merge_level() {
         if (alive_[c] && fr_[c].live && fr_[c].big) dfree(fr_[c].mat, true);
 #pragma omp parallel for schedule(dynamic, 512)
     for (long long c = 0; c < static_cast<long long>(fr_.size()); ++c)
-        if (fr_[c].live) {
+        if (alive_[c] && fr_[c].live) {
             fr_[c].retire();
             alive_[c] = 0;
         }
@@ -2767,6 +2767,7 @@ void Engine::snapshot(StageStats& st) {  // factorize.cpp:731-743
 #pragma omp parallel for schedule(static)
     for (long long q = 0; q < nb; ++q)
         for (long long c = q * kBlk; c < std::min(nc, (q + 1) * kBlk); ++c) {
+            if (!alive_[c]) continue;
             const Front& f = fr_[c];
             if (!f.live) continue;
             const int cs = width(static_cast<int>(c));
@@ -2818,7 +2819,7 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         for (int i = 0; i < HostProf::N; ++i) sprof_.back().t[i] = prof_.t[i] - before.t[i];
     }
     for (size_t c = 0; c < fr_.size(); ++c)
-        if (fr_[c].live) out_.trailing_rows.insert(out_.trailing_rows.end(), fr_[c].rows.begin(), fr_[c].rows.end());
+        if (alive_[c] && fr_[c].live) out_.trailing_rows.insert(out_.trailing_rows.end(), fr_[c].rows.begin(), fr_[c].rows.end());
     for (size_t c = 0; c < fr_.size(); ++c) dfree(fr_[c].mat, fr_[c].big);
     sync();
     out_.ctr.t_qr_ms = out_.ctr.k_ms[K_QR];
