@@ -14,7 +14,10 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = os.path.join(_HERE, "liboracle.so")
+# oracle/ref.py re-executes this module with _LIB_OVERRIDE set to oracle/_ref/libspaqr_ref.so:
+# the reference's own sources behind the same orc_* ABI (see oracle/ref_capi.cpp).
+_LIB = globals().get("_LIB_OVERRIDE") or os.path.join(_HERE, "liboracle.so")
+_MAKEFILE = globals().get("_MAKEFILE_OVERRIDE") or "Makefile"
 _lib = None
 
 i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
@@ -30,7 +33,7 @@ class SingularFrontError(RuntimeError):
 
 
 def build():
-    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    subprocess.run(["make", "-s", "-C", _HERE, "-f", _MAKEFILE], check=True)
 
 
 def lib():

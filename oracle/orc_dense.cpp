@@ -3,7 +3,10 @@
 // the unblocked Householder sweep with Eigen's makeHouseholder convention
 // (third-party algorithm, Eigen3 >= 3.3; reflector v = [1; x_tail/(c0-beta)],
 // beta = -sign(c0)*||x|| (beta = -||x|| when c0 >= 0), tau = (beta-c0)/beta,
-// tau = 0 and beta = c0 when ||x_tail||^2 <= DBL_MIN).
+// tau = 0 and beta = c0 when ||x_tail||^2 <= DBL_MIN).  Sign rule shared with the
+// GPU kernels (csrc/dev.h hh_beta_negative): when c0 is roundoff-sized
+// (c0^2 <= 1e-20 ||x_tail||^2) its sign is not a property of the data — Eigen's
+// blocked arithmetic decides it by roundoff — so beta = -||x|| is taken there too.
 #include <algorithm>
 #include <cassert>
 #include <limits>
@@ -28,7 +31,7 @@ void make_householder(Mat& A, Index k, double& tau, double& beta) {
         return;
     }
     beta = std::sqrt(c0 * c0 + tail2);
-    if (c0 >= 0.0) beta = -beta;
+    if (c0 >= 0.0 || c0 * c0 <= 1e-20 * tail2) beta = -beta;
     const double den = c0 - beta;
     for (Index i = k + 1; i < m; ++i) A(i, k) /= den;
     tau = (beta - c0) / beta;

@@ -16,6 +16,19 @@
 
 namespace spqr {
 
+// Householder sign rule.  Eigen's makeHouseholder (the arithmetic
+// behind block_householder_qr, dense_kernels.cpp:11-35) takes beta = -sign(c0)*||x||,
+// beta = -||x|| for c0 >= 0.  When c0 is roundoff-sized next to the tail
+// (c0^2 <= 1e-20 * ||x_tail||^2, i.e. |c0| <= 1e-10 ||x_tail||) its sign is not a
+// property of the data — Eigen's own blocked arithmetic decides it by roundoff — yet
+// it selects which of two valid reflectors is used, and with it the complement rows
+// that move_extras redistributes.  Every restatement (GPU kernels, oracle/orc_dense.cpp,
+// oracle/eigen_shim) therefore takes beta = -||x|| there.
+constexpr double kHhSignTol2 = 1e-20;
+__host__ __device__ __forceinline__ bool hh_beta_negative(double c0, double tail2) {
+    return c0 >= 0.0 || c0 * c0 <= kHhSignTol2 * tail2;
+}
+
 // Opt in to `bytes` of dynamic shared memory for `func`.  The 48 KB default
 // limit covers static + dynamic shared memory together, so the attribute is
 // raised whenever a launch needs more than any earlier one (`configured` is a

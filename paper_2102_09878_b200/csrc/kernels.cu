@@ -206,7 +206,7 @@ __device__ void qr_body(double* A, int ld, int m, int n, int nt, double* tau_out
                 s_sc[1] = 0.0;
             } else {
                 double beta = sqrt(c0 * c0 + tail2);
-                if (c0 >= 0.0) beta = -beta;
+                if (hh_beta_negative(c0, tail2)) beta = -beta;
                 s_sc[1] = c0 - beta;
                 s_sc[0] = (beta - c0) / beta;
                 ak[k] = beta;

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(32 * NWP) k_panel2(double* __restrict__ a, int
         double t = 0.0, den = 0.0, beta = c0;
         if (!(tail2 <= DBL_MIN)) {
             beta = sqrt(c0 * c0 + tail2);
-            if (c0 >= 0.0) beta = -beta;
+            if (hh_beta_negative(c0, tail2)) beta = -beta;
             den = c0 - beta;
             t = (beta - c0) / beta;
         }
@@ -248,7 +248,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(256)
         double t = 0.0, den = 0.0, beta = c0;
         if (!(tail2 <= DBL_MIN)) {
             beta = sqrt(c0 * c0 + tail2);
-            if (c0 >= 0.0) beta = -beta;
+            if (hh_beta_negative(c0, tail2)) beta = -beta;
             den = c0 - beta;
             t = (beta - c0) / beta;
         }
@@ -639,7 +639,7 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
             double t = 0.0, den = 0.0, beta = c0;
             if (!(tail2 <= DBL_MIN)) {
                 beta = sqrt(c0 * c0 + tail2);
-                if (c0 >= 0.0) beta = -beta;
+                if (hh_beta_negative(c0, tail2)) beta = -beta;
                 den = c0 - beta;
                 t = (beta - c0) / beta;
             }

@@ -51,7 +51,7 @@ __device__ __forceinline__ void make_reflector(double* P, int ldp, int m, int k,
     double tau = 0.0, den = 0.0;
     if (!(tail2 <= DBL_MIN)) {
         double beta = sqrt(c0 * c0 + tail2);
-        if (c0 >= 0.0) beta = -beta;
+        if (hh_beta_negative(c0, tail2)) beta = -beta;
         den = c0 - beta;
         tau = (beta - c0) / beta;
         if (lane == 0) pk[k] = beta;
@@ -118,7 +118,7 @@ __device__ void panel_regs(double* P, int m, int n, int kmax, double* s_tau) {
         double tau = 0.0, den = 0.0, beta = c0;
         if (!(tail2 <= DBL_MIN)) {  // Eigen makeHouseholder
             beta = sqrt(c0 * c0 + tail2);
-            if (c0 >= 0.0) beta = -beta;
+            if (hh_beta_negative(c0, tail2)) beta = -beta;
             den = c0 - beta;
             tau = (beta - c0) / beta;
         }

@@ -8,7 +8,8 @@ import pytest
 import scipy.sparse as sp
 
 import oracle as O
-from paper_2102_09878_b200.problems import random_full_rank, tall_grid
+from oracle import ref as R
+from paper_2102_09878_b200.problems import knn_geometric, random_full_rank, tall_grid
 
 pytestmark = pytest.mark.gpu
 
@@ -171,11 +172,76 @@ def test_config4_knn_small_parity():  # BASELINE config 4 construction at N=4096
     _solve_parity(o, g, p)
 
 
+def _rows_equal(o, g):
+    po, do, to = o.rows()
+    pg, dg, tg_ = g.rows()
+    assert np.array_equal(po, pg)
+    assert np.array_equal(np.sort(do), np.sort(dg)) and np.array_equal(np.sort(to), np.sort(tg_))
+
+
 @pytest.mark.timeout(900)
-def test_config2_full_size_parity():  # the headline problem at full size (oracle ~25-60 s)
+def test_config4_knn_65536_parity():
+    """BASELINE config 4 construction at N=65,536 (L=12): the size where round 1's
+    roundoff-sized Householder pivots (c0 = 0 in exact arithmetic) flipped move_extras
+    decisions.  With the shared sign rule (csrc/dev.h hh_beta_negative) every interface
+    width, nW, nnz(W) and every pivot row must equal the oracle's."""
+    p = knn_geometric(65536, seed=0, levels=12)
+    o, g = _pair(p.A, eps=p.eps, levels=p.levels, coords=p.coords)
+    _compare_structure(o, g)
+    assert o.nnz_w == g.nnz_w and o.nW == g.nW
+    _rows_equal(o, g)
+    _solve_parity(o, g, p)
+
+
+@pytest.mark.timeout(900)
+def test_config3_n32_parity():  # BASELINE config 3 construction at n=32 (N=32,768, M=3N, L=9)
+    p = tall_grid(32, dim=3, seed=0)
+    o, g = _pair(p.A, eps=1e-2, levels=9, coords=p.coords)
+    _compare_structure(o, g)
+    assert o.nnz_w == g.nnz_w and o.nW == g.nW
+    _rows_equal(o, g)
+    _solve_parity(o, g, p)
+
+
+@pytest.mark.skipif(not R.available(), reason="reference build (oracle/_ref) unavailable")
+@pytest.mark.parametrize("case", ["c1", "c3_n16", "c4_4096", "exact"])
+def test_gpu_matches_reference_sources(case):
+    """The GPU pipeline against the reference's own sources (oracle/_ref: proj/src compiled
+    unmodified against the Eigen API shim)."""
+    if case == "c1":
+        p = tall_grid(64)
+        A, kw, b = p.A, dict(eps=p.eps, levels=p.levels, coords=p.coords), p.b
+    elif case == "c3_n16":
+        p = tall_grid(16, dim=3, seed=3)
+        A, kw, b = p.A, dict(eps=1e-2, levels=6, coords=p.coords), p.b
+    elif case == "c4_4096":
+        p = knn_geometric(4096, seed=4, levels=6)
+        A, kw, b = p.A, dict(eps=1e-2, levels=6, coords=p.coords), p.b
+    else:
+        A = random_full_rank(160, 90, 4, seed=2)
+        kw, b = dict(eps=0.0, levels=3, skip_levels=0), np.random.default_rng(1).standard_normal(160)
+    r, g = R.Pipeline(A, **kw), _P().Pipeline(A, **kw)
+    _compare_structure(r, g)
+    assert r.nW == g.nW and r.nnz_w == g.nnz_w
+    _rows_equal(r, g)
+    xr, rr = r.solve(b)
+    xg, rg = g.solve(b)
+    assert abs(rr["iterations"] - rg["iterations"]) <= 1 and rr["converged"] == rg["converged"]
+    rel = lambda x: np.linalg.norm(A.T @ (b - A @ x)) / np.linalg.norm(A.T @ b)
+    assert abs(rel(xg) - rel(xr)) <= 1e-10
+
+
+@pytest.mark.timeout(1500)
+def test_config2_full_size_parity():  # the headline problem at full size (oracle ~25-60 s, reference ~30-70 s)
     p = tall_grid(512)
     o, g = _pair(p.A, eps=p.eps, levels=p.levels, coords=p.coords)
     _compare_structure(o, g)
+    if R.available():  # the reference's own engine at full size
+        r = R.Pipeline(p.A, eps=p.eps, levels=p.levels, coords=p.coords)
+        _compare_structure(r, g)
+        assert r.nnz_w == g.nnz_w and r.nW == g.nW
+        _rows_equal(r, g)
+        del r
     assert o.nnz_w == g.nnz_w and o.nW == g.nW
     po, do, to = o.rows()
     pg, dg, tg_ = g.rows()
