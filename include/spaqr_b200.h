@@ -46,12 +46,14 @@ int spqr_pipeline_create(int m, int n, const int* colptr, const int* rowind, con
                          int* err_cluster);
 void spqr_pipeline_destroy(spqr_pipeline* p);
 
-/* info[16]: M, N, L, nclusters, nW, n_dropped, n_trailing, n_stages, nnz_w, nnz(A), n_batches,
+/* info[16]: M, N, L, nclusters, nW, n_dropped, n_trailing, n_stages, nnz_w, nnz(A), W sweep levels,
  *           engine launches, engine syncs, h2d bytes, d2h bytes, solve-plan launches per sweep pair */
 void spqr_pipeline_info(const spqr_pipeline* p, long long* info);
-/* times[16]: t_partition, t_factorize, t_upload, qr_device_ms, qr_flops, qr_bytes, cpqr_flops,
+/* times[24]: t_partition, t_factorize, t_upload, qr_device_ms, qr_flops, qr_bytes, cpqr_flops,
  *            cpqr_bytes, qr_launches, factorize_event_ms, solve_event_ms, solve_launches,
- *            elimination_waves */
+ *            elimination_waves, cpqr_redundant_bytes, cpqr_redundant_flops, sweep_device_ms (last
+ *            solve), sweeps (last solve), sweep_algorithmic_bytes (one sweep), solve_plan_build_s,
+ *            w_solve levels, wt_solve levels (rest 0) */
 void spqr_pipeline_times(const spqr_pipeline* p, double* times);
 /* Device time (CUDA events on the engine stream), algorithmic HBM bytes and launch
  * counts per kernel family: assemble, stats, front_qr, trsm, cpqr, scatter (6 each). */

@@ -68,11 +68,13 @@ class Pipeline:
             self.h = None
 
     def times(self):
-        t = np.zeros(16)
+        t = np.zeros(24)
         lib().spqr_pipeline_times(self.h, t)
         return dict(t_partition=t[0], t_factorize=t[1], t_upload=t[2], qr_ms=t[3], qr_flops=t[4], qr_bytes=t[5],
                     cpqr_flops=t[6], cpqr_bytes=t[7], qr_launches=int(t[8]), factorize_event_ms=t[9],
-                    solve_event_ms=t[10], solve_launches=int(t[11]), elim_waves=int(t[12]))
+                    solve_event_ms=t[10], solve_launches=int(t[11]), elim_waves=int(t[12]),
+                    cpqr_redundant_bytes=t[13], cpqr_redundant_flops=t[14], sweep_ms=t[15], sweeps=int(t[16]),
+                    sweep_bytes=t[17], solve_plan_s=t[18], w_solve_levels=int(t[19]), wt_solve_levels=int(t[20]))
 
     KERNELS = ("assemble", "stats", "front_qr", "trsm", "cpqr", "scatter")
 

@@ -45,6 +45,8 @@ struct spqr_pipeline {
     double t_partition = 0, t_factorize = 0, t_upload = 0;
     double ev_factorize_ms = 0, ev_solve_ms = 0;  // CUDA events on the pipeline stream
     long long solve_launches = 0;
+    double sweep_ms = 0;  // W sweeps of the last solve (CUDA events)
+    int sweeps = 0;
     ~spqr_pipeline() {
         if (st) cudaStreamDestroy(st);
     }
@@ -205,7 +207,7 @@ void spqr_pipeline_info(const spqr_pipeline* p, long long* o) {
     o[7] = static_cast<long long>(p->F.stages.size());
     o[8] = p->F.nnz_w();
     o[9] = p->Aw.nnz();
-    o[10] = static_cast<long long>(p->plan.batches.size());
+    o[10] = static_cast<long long>(p->plan.sched[kWSolve].levels.size());
     o[11] = p->F.ctr.launches;
     o[12] = p->F.ctr.syncs;
     o[13] = p->F.ctr.h2d_bytes;
@@ -214,7 +216,7 @@ void spqr_pipeline_info(const spqr_pipeline* p, long long* o) {
 }
 
 void spqr_pipeline_times(const spqr_pipeline* p, double* t) {
-    std::fill(t, t + 16, 0.0);
+    std::fill(t, t + 24, 0.0);
     t[0] = p->t_partition;
     t[1] = p->t_factorize;
     t[2] = p->t_upload;
@@ -228,6 +230,14 @@ void spqr_pipeline_times(const spqr_pipeline* p, double* t) {
     t[10] = p->ev_solve_ms;
     t[11] = static_cast<double>(p->solve_launches);
     t[12] = static_cast<double>(p->F.ctr.elim_waves);
+    t[13] = p->F.ctr.cpqr_redundant_bytes;
+    t[14] = p->F.ctr.cpqr_redundant_flops;
+    t[15] = p->sweep_ms;
+    t[16] = static_cast<double>(p->sweeps);
+    t[17] = p->plan.sweep_bytes;
+    t[18] = p->plan.t_build;
+    t[19] = static_cast<double>(p->plan.sched[kWSolve].levels.size());
+    t[20] = static_cast<double>(p->plan.sched[kWtSolve].levels.size());
 }
 
 void spqr_pipeline_kernel_stats(const spqr_pipeline* p, double* ms, double* bytes, long long* launches) {
@@ -263,6 +273,8 @@ int spqr_pipeline_solve(spqr_pipeline* p, int direct, const double* b, double* x
         CK(cudaEventElapsedTime(&ms, e0, e1));
         p->ev_solve_ms = ms;
         p->solve_launches = rep.launches;
+        p->sweep_ms = rep.sweep_ms;
+        p->sweeps = rep.sweeps;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         std::vector<double> u(n);

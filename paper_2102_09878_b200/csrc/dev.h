@@ -170,6 +170,8 @@ void launch_wsweep(const WFac* f, int nf, double* z, double* contrib, int mode, 
 // factors with c >= kBigFactorCols: one CTA each (k_wsweep_big)
 constexpr int kBigFactorCols = 192;
 void launch_wsweep_big(const WFac* f, int nf, double* z, double* contrib, int mode, int maxc, cudaStream_t st);
+// opt in to the largest dynamic shared memory any level needs, before graph capture
+void prepare_wsweep(int maxc, int bmaxc);
 // z[col[t]] (+/-)= contrib[idx[ptr[t]..ptr[t+1])] in order
 void launch_wreduce(const int* ptr, const int* idx, const int* col, int ncol, const double* contrib, double* z,
                     double sgn, cudaStream_t st);

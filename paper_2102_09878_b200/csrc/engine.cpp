@@ -146,36 +146,6 @@ void sorted_insert(std::vector<int>& v, int x) {
     if (it == v.end() || *it != x) v.insert(it, x);
 }
 
-// Parity diagnostics (off unless SPQR_TRACE_SCOLS=<path>): one text line per
-// elimination, row move and sparsify decision, in the format the oracle writes,
-// so tools/trace_scols.py can diff the two engines.  SPQR_TRACE_ELIM=<cluster>
-// adds that elimination's stack rows and dumps its stack before the QR;
-// SPQR_TRACE_ROW=<row> prints the move_extras candidates of that row.
-struct ParityTrace {
-    std::string path;
-    int elim = -1, row = -1;
-    ParityTrace() {
-        if (const char* t = std::getenv("SPQR_TRACE_SCOLS")) path = std::string(t).substr(0, std::string(t).find(':'));
-        if (const char* e = std::getenv("SPQR_TRACE_ELIM")) elim = std::atoi(e);
-        if (const char* r = std::getenv("SPQR_TRACE_ROW")) row = std::atoi(r);
-    }
-    bool on() const { return !path.empty(); }
-    void line(const char* fmt, ...) const {
-        if (!on()) return;
-        if (FILE* f = std::fopen(path.c_str(), "a")) {
-            va_list ap;
-            va_start(ap, fmt);
-            std::vfprintf(f, fmt, ap);
-            va_end(ap);
-            std::fclose(f);
-        }
-    }
-};
-const ParityTrace& ptrace() {
-    static const ParityTrace t;
-    return t;
-}
-
 // Host-side profile (SPQR_PROF=1 prints it to stderr after the factorization).
 struct HostProf {
     enum { INIT, STATS, SYNC, PASS1, SBUILD, PASS2, MATER, SCALE, SROWS, SCOLS, MERGE, UPLOAD, DEPS, FETCH, N };
@@ -922,31 +892,9 @@ private:
             if (narrow[c].empty()) continue;
             const int* dn = u.put(narrow[c]);
             double nb = 0;
-            for (int i : narrow[c]) nb += 16.0 * cd[i].m * cd[i].n;
+            for (int i : narrow[c]) nb += 8.0 * cd[i].m * cd[i].n;
             cudaEvent_t e0 = kt_.begin(st_);
-            static const bool nlog = std::getenv("SPQR_BIGLOG") != nullptr;
-            cudaEvent_t b0 = nullptr, b1 = nullptr;
-            if (nlog) {
-                cudaEventCreate(&b0);
-                cudaEventCreate(&b1);
-                cudaEventRecord(b0, st_);
-            }
             launch_cpqr_narrow(c, dc, dn, static_cast<int>(narrow[c].size()), nsmem[c], st_);
-            if (nlog) {
-                cudaEventRecord(b1, st_);
-                cudaEventSynchronize(b1);
-                float ms = 0;
-                cudaEventElapsedTime(&ms, b0, b1);
-                int mm = 0, mn = 0;
-                for (int i : narrow[c]) {
-                    mm = std::max(mm, cd[i].m);
-                    mn = std::max(mn, cd[i].n);
-                }
-                std::fprintf(stderr, "[spqr cpqr narrow] cls %d count %zu max m %d max n %d  %.3f ms\n", c,
-                             narrow[c].size(), mm, mn, ms);
-                cudaEventDestroy(b0);
-                cudaEventDestroy(b1);
-            }
             kt_.end(K_CPQR, e0, st_, nb);
         }
         if (nnar == cd.size()) return;
@@ -982,26 +930,8 @@ private:
                 CpqrDesc d = cd[i];
                 d.work = arena().alloc_n<double>(cpqr_big_work_doubles(d.n));
                 cudaEvent_t e0 = kt_.begin(st_);
-                static const bool biglog = std::getenv("SPQR_BIGLOG") != nullptr;
-                cudaEvent_t b0 = nullptr, b1 = nullptr;
-                if (biglog) {
-                    cudaEventCreate(&b0);
-                    cudaEventCreate(&b1);
-                    cudaEventRecord(b0, st_);
-                }
                 launch_cpqr_big(d, st_);
-                if (biglog) {
-                    cudaEventRecord(b1, st_);
-                    cudaEventSynchronize(b1);
-                    float ms = 0;
-                    cudaEventElapsedTime(&ms, b0, b1);
-                    int rk = 0;
-                    cudaMemcpy(&rk, d.rank, sizeof(int), cudaMemcpyDeviceToHost);
-                    std::fprintf(stderr, "[spqr big cpqr] m %d n %d rank %d  %.3f ms\n", d.m, d.n, rk, ms);
-                    cudaEventDestroy(b0);
-                    cudaEventDestroy(b1);
-                }
-                kt_.end(K_CPQR, e0, st_, 16.0 * d.m * d.n);
+                kt_.end(K_CPQR, e0, st_, 8.0 * d.m * d.n);
                 continue;
             }
             static const bool no_tall = std::getenv("SPQR_NO_TALL") != nullptr;
@@ -1020,7 +950,7 @@ private:
             if (tall[c].empty()) continue;
             const int* dt = u.put(tall[c]);
             double tb = 0;
-            for (int i : tall[c]) tb += 16.0 * cd[i].m * cd[i].n;
+            for (int i : tall[c]) tb += 8.0 * cd[i].m * cd[i].n;
             cudaEvent_t e0 = kt_.begin(st_);
             launch_cpqr_tall(c, dc, dt, static_cast<int>(tall[c].size()), st_);
             kt_.end(K_CPQR, e0, st_, tb);
@@ -1028,39 +958,10 @@ private:
         const int* ds = u.put(small);
         const int* dl = u.put(large);
         double cb = 0;
-        for (int i : small) cb += 16.0 * cd[i].m * cd[i].n;
-        for (int i : large) cb += 16.0 * cd[i].m * cd[i].n;
+        for (int i : small) cb += 8.0 * cd[i].m * cd[i].n;
+        for (int i : large) cb += 8.0 * cd[i].m * cd[i].n;
         cudaEvent_t e0 = kt_.begin(st_);
-        static const bool biglog = std::getenv("SPQR_BIGLOG") != nullptr;
-        cudaEvent_t b0 = nullptr, b1 = nullptr;
-        if (biglog) {
-            cudaEventCreate(&b0);
-            cudaEventCreate(&b1);
-            cudaEventRecord(b0, st_);
-        }
         launch_cpqr_split(dc, ds, static_cast<int>(small.size()), smem, dl, static_cast<int>(large.size()), maxm, st_);
-        if (biglog) {
-            cudaEventRecord(b1, st_);
-            cudaEventSynchronize(b1);
-            float ms = 0;
-            cudaEventElapsedTime(&ms, b0, b1);
-            long long sm_mn = 0, lg_mn = 0;
-            int sm_m = 0, sm_n = 0, lg_m = 0, lg_n = 0;
-            for (int i : small) {
-                sm_mn = std::max<long long>(sm_mn, 1LL * cd[i].m * cd[i].n);
-                sm_m = std::max(sm_m, cd[i].m);
-                sm_n = std::max(sm_n, cd[i].n);
-            }
-            for (int i : large) {
-                lg_mn += 1LL * cd[i].m * cd[i].n;
-                lg_m = std::max(lg_m, cd[i].m);
-                lg_n = std::max(lg_n, cd[i].n);
-            }
-            std::fprintf(stderr, "[spqr cpqr batch] small %zu (max m %d n %d mn %lld) large %zu (max m %d n %d sum mn %lld)  %.3f ms\n",
-                         small.size(), sm_m, sm_n, sm_mn, large.size(), lg_m, lg_n, lg_mn, ms);
-            cudaEventDestroy(b0);
-            cudaEventDestroy(b1);
-        }
         kt_.end(K_CPQR, e0, st_, cb);
     }
     void eliminate_stage(int k);
@@ -1423,14 +1324,8 @@ void Engine::elim_prep2(Elim& e, Scratch& S) {
     S.best.assign(nr, -1);
     S.rv_sq.resize(nr);
     S.rv_nz.resize(nr);
-    const int trace_row = ptrace().row;
     for (int m : cand) {  // strict > in candidate order == the reference's per-row loop
         row_vals(fc, c, m, S.rv_sq.data(), S.rv_nz.data(), true);
-        if (trace_row >= 0)
-            for (size_t q = 0; q < nr; ++q)
-                if (fc.rows[q].gid == trace_row)
-                    std::fprintf(stderr, "[gpu row] c %d row %d cand %d sq %.17g (base %d sidx %d)\n", c, trace_row, m,
-                                 S.rv_sq[q], fc.rows[q].base, fc.rows[q].sidx);
         for (size_t q = 0; q < nr; ++q)
             if (S.rv_sq[q] > S.bw[q]) {
                 S.bw[q] = S.rv_sq[q];
@@ -1473,19 +1368,6 @@ void Engine::elim_commit2(Elim& e) {
         }
     }
     PFront& fc = pend_[pend_id_[c]];
-    if (ptrace().on()) {
-        const ParityTrace& T = ptrace();
-        if (cs > 0) T.line("e %d rows %d tcols %d 0\n", c, e.total_rows, e.tcols);
-        if (c == T.elim && cs > 0) {
-            std::string l = "S " + std::to_string(c) + " rows";
-            for (const PRow& r : e.srows) l += " " + std::to_string(r.gid);
-            l += " keys";
-            for (int k : e.keys) l += " " + std::to_string(k);
-            T.line("%s\n", l.c_str());
-        }
-        for (const auto& d : e.dest) T.line("m %d row %d tgt %d\n", c, fc.rows[d.second].gid, d.first);
-        for (int q : e.trail) T.line("m %d row %d tgt -1\n", c, fc.rows[q].gid);
-    }
     for (int q : e.trail) out_.trailing_rows.push_back(fc.rows[q].gid);
     for (size_t a = 0; a < e.dest.size();) {  // append_rows, factorize.cpp:112-133 (ascending targets)
         size_t b = a;
@@ -1999,22 +1881,6 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
                 ++qi;
             }
         const QrDesc* dq = u.put(qd);
-        if (ptrace().elim >= 0) {  // diagnostics: the traced elimination's stack before its QR
-            const int want = ptrace().elim;
-            for (int i = 0; i < nvalid; ++i)
-                if (el_[i].c == want && el_[i].cs > 0) {
-                    cudaStreamSynchronize(st_);
-                    const Elim& x = el_[i];
-                    std::vector<double> h(static_cast<size_t>(x.total_rows) * x.tcols);
-                    cudaMemcpy(h.data(), x.S, sizeof(double) * h.size(), cudaMemcpyDeviceToHost);
-                    if (FILE* df = std::fopen("gpurun_out/stack_gpu.bin", "wb")) {
-                        const int dims[3] = {x.total_rows, x.tcols, x.cs};
-                        std::fwrite(dims, 4, 3, df);
-                        std::fwrite(h.data(), 8, h.size(), df);
-                        std::fclose(df);
-                    }
-                }
-        }
         d_psq = arena().alloc_n<double>(std::max<long long>(postlen, 1));
         d_pnz = arena().alloc_n<unsigned char>(std::max<long long>(postlen, 1));
         pwork = layout_stats(pd.data(), pd.size());
@@ -2207,7 +2073,6 @@ void Engine::sparsify_rows_all() {
                 ++nseg;
             }
         if (nw == 0) {  // keep = 0: every extra row is dropped
-            ptrace().line("r %d p2 %d nw 0 keep 0\n", static_cast<int>(p), p2);
             for (int i = cs; i < r; ++i) out_.dropped_rows.push_back(f.rows[i]);
             f.rows.resize(cs);
             continue;
@@ -2260,7 +2125,8 @@ void Engine::sparsify_rows_all() {
         const Job& j = jobs[i];
         const int keep = rank[i];
         out_.ctr.cpqr_flops += 4.0 * j.p2 * double(j.nw) * keep + 2.0 * j.p2 * j.nw;
-        ptrace().line("r %d p2 %d nw %d keep %d\n", j.p, j.p2, j.nw, keep);
+        out_.ctr.cpqr_bytes += 8.0 * keep * j.nw;  // R out (8mn + 8rn)
+        out_.ctr.k_bytes[K_CPQR] += 8.0 * keep * j.nw;
         if (keep >= j.p2) continue;
         Front& f = fr_[j.p];
         for (int r = j.cs + keep; r < j.cs + j.p2; ++r) out_.dropped_rows.push_back(f.rows[r]);
@@ -2460,20 +2326,29 @@ void Engine::sparsify_cols_all() {
         for (size_t i = 0; i < nj; ++i) {
             Job& j = jobs[i];
             const int r2 = rank[i];
-            out_.ctr.cpqr_flops += 4.0 * j.cs * double(j.nG) * r2 + 2.0 * j.cs * j.nG;
+            const double jf = 4.0 * j.cs * double(j.nG) * r2 + 2.0 * j.cs * j.nG;
             bool ok = true;
             for (int q : lower[eidx[j.p]])
                 if (bad[q] || changed[q]) {
                     ok = false;
                     break;
                 }
+            if (ok) {
+                out_.ctr.cpqr_flops += jf;
+                out_.ctr.cpqr_bytes += 8.0 * r2 * j.nG;  // R out (8mn + 8rn)
+                out_.ctr.k_bytes[K_CPQR] += 8.0 * r2 * j.nG;
+            } else {  // speculative result discarded: redundant, not algorithmic, work
+                out_.ctr.cpqr_bytes -= 8.0 * j.cs * j.nG;
+                out_.ctr.k_bytes[K_CPQR] -= 8.0 * j.cs * j.nG;
+                out_.ctr.cpqr_redundant_bytes += 8.0 * j.cs * j.nG + 8.0 * r2 * j.nG;
+                out_.ctr.cpqr_redundant_flops += jf;
+            }
             if (!ok) {
                 bad[j.p] = 1;
                 rejected.push_back(j.p);
                 continue;
             }
             done[j.p] = 1;
-            ptrace().line("p %d cs %d nG %d rank %d\n", j.p, j.cs, j.nG, r2);
             if (r2 >= j.cs) continue;
             changed[j.p] = 1;
             const int p = j.p;

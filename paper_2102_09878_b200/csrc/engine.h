@@ -36,7 +36,8 @@ struct EngineCounters {
     double k_bytes[K_NTAGS] = {0};    // algorithmic HBM bytes (read + write) per kernel family
     long long k_launches[K_NTAGS] = {0};
     long long launches = 0, syncs = 0, h2d_bytes = 0, d2h_bytes = 0;
-    double qr_flops = 0, qr_bytes = 0, cpqr_flops = 0, cpqr_bytes = 0;  // algorithmic work (BASELINE.md formulas)
+    double qr_flops = 0, qr_bytes = 0, cpqr_flops = 0, cpqr_bytes = 0;  // algorithmic work (SURVEY 8(d) formulas)
+    double cpqr_redundant_flops = 0, cpqr_redundant_bytes = 0;         // discarded speculative sparsify_cols work
     double t_qr_ms = 0;  // device time of the batched front-QR launches (CUDA events)
     long long qr_launches = 0;
     long long elim_waves = 0;  // dependency waves of eliminations summed over stages

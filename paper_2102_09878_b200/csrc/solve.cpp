@@ -12,6 +12,7 @@
 namespace spqr {
 
 SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
+    const double t0 = now_s();
     SolvePlan P;
     P.mem = std::make_unique<DeviceArena>(size_t(64) << 20);
     SharedPinned& sp = SharedPinned::get();
@@ -20,105 +21,153 @@ SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
     pin.reset();
     Uploader up{P.mem.get(), &pin, st};
     const int* d_idx = up.put(F.idx);
-    // group factors by batch (batch ids increase chronologically; within a
-    // batch the factors commute)
-    std::vector<size_t> ord(F.W.size());
-    for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;
-    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return F.W[a].batch < F.W[b].batch; });
-    long long maxcontrib = 1;
+    const int nfac = static_cast<int>(F.W.size());
     // factors at least this wide run one per CTA (SPQR_BIG_FACTOR overrides, for tests)
     const int big_cols = std::getenv("SPQR_BIG_FACTOR") ? std::atoi(std::getenv("SPQR_BIG_FACTOR")) : kBigFactorCols;
-    size_t i = 0;
-    while (i < ord.size()) {
-        size_t j = i;
-        while (j < ord.size() && F.W[ord[j]].batch == F.W[ord[i]].batch) ++j;
-        std::vector<WFac> fac, bfac;
-        long long contrib = 0;
-        std::vector<std::pair<int, int>> lists;  // (coupled column, contribution index), chronological
-        int maxc = 1, bmaxc = 1;
-        for (size_t q = i; q < j; ++q) {
-            const DevWFactor& w = F.W[ord[q]];
-            WFac f{};
-            f.kind = w.kind;
-            f.c = w.c;
-            f.k = w.k;
-            f.cols = d_idx + w.cols_off;
-            f.coupled = d_idx + w.coupled_off;
-            f.a = w.a;
-            f.tau = w.tau;
-            f.sign = w.sign;
-            f.contrib_off = contrib;
-            if (w.kind == 0 && w.k > 0) {
-                for (int t = 0; t < w.k; ++t) lists.emplace_back(F.idx[w.coupled_off + t], static_cast<int>(contrib + t));
-                contrib += w.k;
-            }
-            // triangular factors: the warp path's back substitution is c sequential
-            // steps of c/32 work; rotations: the CTA path pays two block barriers per
-            // reflector, so only very tall ones move
-            if (w.kind == 0 ? w.c >= big_cols : w.c >= 8 * big_cols) {
-                bmaxc = std::max(bmaxc, w.c);
-                bfac.push_back(f);
+    long long maxcontrib = 1;
+    std::vector<int> lastW(F.N > 0 ? F.N : 1), lastR(F.N > 0 ? F.N : 1), lastA(F.N > 0 ? F.N : 1), level(nfac);
+    for (int mode = 0; mode < 4; ++mode) {
+        const bool forward = (mode == kWtSolve || mode == kWApply);
+        const bool accumulate = (mode == kWtSolve || mode == kWtApply);
+        std::fill(lastW.begin(), lastW.end(), 0);
+        std::fill(lastR.begin(), lastR.end(), 0);
+        std::fill(lastA.begin(), lastA.end(), 0);
+        int nlev = 0;
+        for (int t = 0; t < nfac; ++t) {
+            const int q = forward ? t : nfac - 1 - t;
+            const DevWFactor& w = F.W[q];
+            const int* cols = F.idx.data() + w.cols_off;
+            const int* cp = F.idx.data() + w.coupled_off;
+            const int k = (w.kind == 0) ? w.k : 0;
+            int L = 0;
+            for (int i = 0; i < w.c; ++i) L = std::max({L, lastW[cols[i]], lastR[cols[i]], lastA[cols[i]]});
+            if (accumulate) {
+                int La = 0;
+                for (int j = 0; j < k; ++j) {
+                    L = std::max({L, lastW[cp[j]], lastR[cp[j]]});
+                    La = std::max(La, lastA[cp[j]]);
+                }
+                L = std::max(L + 1, La);
+                for (int j = 0; j < k; ++j) lastA[cp[j]] = std::max(lastA[cp[j]], L);
             } else {
-                maxc = std::max(maxc, w.c);
-                fac.push_back(f);
+                for (int j = 0; j < k; ++j) L = std::max(L, lastW[cp[j]]);
+                ++L;
+                for (int j = 0; j < k; ++j) lastR[cp[j]] = std::max(lastR[cp[j]], L);
             }
-        }
-        SolvePlan::Batch b;
-        b.fac = up.put(fac);
-        b.nf = static_cast<int>(fac.size());
-        b.maxc = maxc;
-        b.bfac = up.put(bfac);
-        b.nbf = static_cast<int>(bfac.size());
-        b.bmaxc = bmaxc;
-        if (!lists.empty()) {
-            // per coupled column (ascending), its contributions in chronological order:
-            // the indices increase with time, so sorting the pairs gives exactly that
-            std::sort(lists.begin(), lists.end());
-            std::vector<int> ptr{0}, idx, col;
-            idx.reserve(lists.size());
-            for (size_t a = 0; a < lists.size();) {
-                size_t e = a;
-                while (e < lists.size() && lists[e].first == lists[a].first) idx.push_back(lists[e++].second);
-                col.push_back(lists[a].first);
-                ptr.push_back(static_cast<int>(idx.size()));
-                a = e;
+            for (int i = 0; i < w.c; ++i) {
+                lastW[cols[i]] = L;
+                lastR[cols[i]] = std::max(lastR[cols[i]], L);
             }
-            b.rptr = up.put(ptr);
-            b.ridx = up.put(idx);
-            b.rcol = up.put(col);
-            b.ncol = static_cast<int>(col.size());
+            level[q] = L;
+            nlev = std::max(nlev, L);
         }
-        maxcontrib = std::max(maxcontrib, contrib);
-        P.batches.push_back(b);
-        i = j;
+        // bucket the factors by level, in walk order
+        std::vector<int> cnt(nlev + 2, 0);
+        for (int q = 0; q < nfac; ++q) ++cnt[level[q] + 1];
+        for (int l = 0; l <= nlev; ++l) cnt[l + 1] += cnt[l];
+        std::vector<int> byl(nfac), pos(cnt.begin(), cnt.end() - 1);
+        for (int t = 0; t < nfac; ++t) {
+            const int q = forward ? t : nfac - 1 - t;
+            byl[pos[level[q]]++] = q;
+        }
+        SolvePlan::Schedule& S = P.sched[mode];
+        for (int l = 1; l <= nlev; ++l) {
+            std::vector<WFac> fac, bfac;
+            std::vector<std::pair<int, int>> lists;  // (coupled column, contribution index) in walk order
+            long long contrib = 0;
+            int maxc = 1, bmaxc = 1;
+            for (int e = cnt[l]; e < cnt[l + 1]; ++e) {
+                const DevWFactor& w = F.W[byl[e]];
+                WFac f{};
+                f.kind = w.kind;
+                f.c = w.c;
+                f.k = w.k;
+                f.cols = d_idx + w.cols_off;
+                f.coupled = d_idx + w.coupled_off;
+                f.a = w.a;
+                f.tau = w.tau;
+                f.sign = w.sign;
+                f.contrib_off = contrib;
+                if (accumulate && w.kind == 0 && w.k > 0) {
+                    for (int t = 0; t < w.k; ++t)
+                        lists.emplace_back(F.idx[w.coupled_off + t], static_cast<int>(contrib + t));
+                    contrib += w.k;
+                }
+                // triangular factors: the warp path's back substitution is c sequential steps of
+                // c/32 work; rotations: the CTA path pays two block barriers per reflector, so only
+                // very tall ones move
+                if (w.kind == 0 ? w.c >= big_cols : w.c >= 8 * big_cols) {
+                    bmaxc = std::max(bmaxc, w.c);
+                    bfac.push_back(f);
+                } else {
+                    maxc = std::max(maxc, w.c);
+                    fac.push_back(f);
+                }
+            }
+            SolvePlan::Level lv;
+            lv.fac = up.put(fac);
+            lv.nf = static_cast<int>(fac.size());
+            lv.maxc = maxc;
+            lv.bfac = up.put(bfac);
+            lv.nbf = static_cast<int>(bfac.size());
+            lv.bmaxc = bmaxc;
+            if (!lists.empty()) {
+                // per coupled column (ascending) its contributions in walk order: indices grow
+                // along the walk, so sorting the pairs gives exactly that
+                std::sort(lists.begin(), lists.end());
+                std::vector<int> ptr{0}, idx, col;
+                idx.reserve(lists.size());
+                for (size_t a = 0; a < lists.size();) {
+                    size_t e = a;
+                    while (e < lists.size() && lists[e].first == lists[a].first) idx.push_back(lists[e++].second);
+                    col.push_back(lists[a].first);
+                    ptr.push_back(static_cast<int>(idx.size()));
+                    a = e;
+                }
+                lv.rptr = up.put(ptr);
+                lv.ridx = up.put(idx);
+                lv.rcol = up.put(col);
+                lv.ncol = static_cast<int>(col.size());
+            }
+            maxcontrib = std::max(maxcontrib, contrib);
+            S.launches += (lv.nf > 0) + (lv.nbf > 0) + (lv.ncol > 0);
+            S.levels.push_back(lv);
+        }
     }
     P.contrib = P.mem->alloc_n<double>(maxcontrib);
-    for (const auto& b : P.batches) {
-        const int k = (b.nf > 0 ? 1 : 0) + (b.nbf > 0 ? 1 : 0);
-        P.launches_per_sweep += k;
-        P.launches_per_sweep_t += k + (b.ncol > 0 ? 1 : 0);
+    int allc = 1, allb = 1;
+    for (const auto& S : P.sched)
+        for (const auto& lv : S.levels) {
+            allc = std::max(allc, lv.maxc);
+            allb = std::max(allb, lv.bmaxc);
+        }
+    prepare_wsweep(allc, allb);
+    {
+        double gathered = 0.0;
+        for (const auto& w : F.W) gathered += w.c + (w.kind == 0 ? w.k : 0);
+        P.sweep_bytes = 8.0 * static_cast<double>(F.nnz_w()) + 16.0 * gathered;
     }
+    P.launches_per_sweep = P.sched[kWSolve].launches;
+    P.launches_per_sweep_t = P.sched[kWtSolve].launches;
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
+    P.t_build = now_s() - t0;
     return P;
 }
 
 long long sweep(const SolvePlan& P, SweepMode mode, double* d_z, cudaStream_t st) {
     long long L = 0;
-    const int nb = static_cast<int>(P.batches.size());
-    const bool forward = (mode == kWtSolve || mode == kWApply);  // chronological order
-    for (int q = 0; q < nb; ++q) {
-        const auto& b = P.batches[forward ? q : nb - 1 - q];
-        if (b.nf > 0) {
-            launch_wsweep(b.fac, b.nf, d_z, P.contrib, static_cast<int>(mode), b.maxc, st);
+    for (const auto& lv : P.sched[mode].levels) {
+        if (lv.nf > 0) {
+            launch_wsweep(lv.fac, lv.nf, d_z, P.contrib, static_cast<int>(mode), lv.maxc, st);
             ++L;
         }
-        if (b.nbf > 0) {  // same batch: the factors commute, the order of the two launches is free
-            launch_wsweep_big(b.bfac, b.nbf, d_z, P.contrib, static_cast<int>(mode), b.bmaxc, st);
+        if (lv.nbf > 0) {  // same level: independent factors, the order of the two launches is free
+            launch_wsweep_big(lv.bfac, lv.nbf, d_z, P.contrib, static_cast<int>(mode), lv.bmaxc, st);
             ++L;
         }
-        if ((mode == kWtSolve || mode == kWtApply) && b.ncol > 0) {
-            launch_wreduce(b.rptr, b.ridx, b.rcol, b.ncol, P.contrib, d_z, mode == kWtSolve ? -1.0 : 1.0, st);
+        if (lv.ncol > 0) {
+            launch_wreduce(lv.rptr, lv.ridx, lv.rcol, lv.ncol, P.contrib, d_z, mode == kWtSolve ? -1.0 : 1.0, st);
             ++L;
         }
     }
@@ -172,6 +221,7 @@ CglsWork make_cgls_work(int m, int n) {
     w.partial = w.mem->alloc_n<double>(w.nblocks);
     w.scal = w.mem->alloc_n<double>(16);
     w.brk = w.mem->alloc_n<int>(4);
+    CK(cudaMallocHost(reinterpret_cast<void**>(&w.hpin), 2 * sizeof(double)));
     return w;
 }
 
@@ -190,6 +240,30 @@ struct Dots {
 
 }  // namespace
 
+namespace {
+
+// One captured CUDA graph per half-iteration of CGLS: the kernel sequence of an
+// iteration is fixed (the W level schedules, the spmvs, the reductions), so it is
+// recorded once per solve and replayed with one launch, instead of ~100 launches.
+struct CapturedGraph {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t x = nullptr;
+    ~CapturedGraph() {
+        if (x) cudaGraphExecDestroy(x);
+        if (g) cudaGraphDestroy(g);
+    }
+    template <class F>
+    void capture(cudaStream_t st, F&& body) {
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        body();
+        CK(cudaStreamEndCapture(st, &g));
+        CK(cudaGraphInstantiate(&x, g, 0));
+    }
+    void launch(cudaStream_t st) const { CK(cudaGraphLaunch(x, st)); }
+};
+
+}  // namespace
+
 SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, double* d_u, double tol, int maxit,
                      const double* d_w, CglsWork& ws, cudaStream_t st) {
     const double t0 = now_s();
@@ -197,11 +271,12 @@ SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, 
     const int m = A.m, n = A.n;
     long long L = 0;
     Dots dots{ws, st, L};
-    // scalars: 0 nres0^2, 1 gamma(a), 2 gamma(b), 3 qq, 4 alpha, 5 tn^2
+    // scalars: 0 nres0^2, 1 gamma, 2 gamma_new, 3 qq, 4 alpha, 5 tn^2
     double* sc = ws.scal;
     launch_copy(m, d_b, ws.r, st);
     launch_spmv_csr(n, A.cp, A.ci, A.cv, ws.r, ws.t, st);  // t = A^T r
     dots.norm2(n, ws.t, d_w ? d_w : nullptr, sc + 0);
+    L += 2;
     double h0 = 0.0;
     CK(cudaMemcpyAsync(&h0, sc + 0, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -212,59 +287,110 @@ SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, 
         rep.converged = true;
         rep.residual_history = {0.0};
         rep.t_solve = now_s() - t0;
+        rep.launches = L;
         return rep;
     }
     rep.residual_history.push_back(1.0);
+    // sweep timing: e[0..1] eager sweeps, e[2..3] inside g1, e[4..5] inside g2
+    cudaEvent_t e[6];
+    for (auto& x : e) CK(cudaEventCreate(&x));
+    auto acc = [&](int a) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e[a], e[a + 1]));
+        rep.sweep_ms += ms;
+        ++rep.sweeps;
+    };
     launch_copy(n, ws.t, ws.s, st);
-    if (W) L += sweep(*W, kWtSolve, ws.s, st);
+    if (W) {
+        CK(cudaEventRecord(e[0], st));
+        L += sweep(*W, kWtSolve, ws.s, st);
+        CK(cudaEventRecord(e[1], st));
+    }
     launch_copy(n, ws.s, ws.p, st);
     CK(cudaMemsetAsync(ws.y, 0, sizeof(double) * n, st));
     double* gamma = sc + 1;
     double* gnew = sc + 2;
     dots.norm2(n, ws.s, nullptr, gamma);
-    struct {
-        double tn2;
-        int brk;
-    } hres;
-    double* hpin = nullptr;
-    CK(cudaMallocHost(reinterpret_cast<void**>(&hpin), 2 * sizeof(double)));
-    for (int it = 1; it <= maxit; ++it) {
+    L += 2;
+    double* hpin = ws.hpin;
+    // half-iteration 1 (solve.cpp:50-62): v = W^{-1} p, q = A v, alpha, y, r, t = A^T r, ||w.t||
+    long long L1 = 0, L2 = 0;
+    CapturedGraph g1, g2;
+    g1.capture(st, [&] {
+        Dots d1{ws, st, L1};
         launch_copy(n, ws.p, ws.v, st);
-        if (W) L += sweep(*W, kWSolve, ws.v, st);
+        if (W) {
+            CK(cudaEventRecord(e[2], st));
+            L1 += sweep(*W, kWSolve, ws.v, st);
+            CK(cudaEventRecord(e[3], st));
+        }
         launch_spmv_csr(m, A.rp, A.ri, A.rv, ws.v, ws.q, st);  // q = A v
-        dots.norm2(m, ws.q, nullptr, sc + 3);
+        d1.norm2(m, ws.q, nullptr, sc + 3);
         launch_cgls_alpha(gamma, sc + 3, sc + 4, ws.brk, st);
         launch_axpy_dev(n, sc + 4, 1.0, ws.p, ws.y, st);
         launch_axpy_dev(m, sc + 4, -1.0, ws.q, ws.r, st);
         launch_spmv_csr(n, A.cp, A.ci, A.cv, ws.r, ws.t, st);
-        dots.norm2(n, ws.t, d_w, sc + 5);
-        L += 7;
+        d1.norm2(n, ws.t, d_w, sc + 5);
+        L1 += 7;
         CK(cudaMemcpyAsync(hpin, sc + 5, sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(hpin + 1, ws.brk, sizeof(int), cudaMemcpyDeviceToHost, st));
+    });
+    // half-iteration 2 (:66-71): s = W^{-T} t, gamma_new, p = s + (gamma_new/gamma) p, gamma = gamma_new
+    g2.capture(st, [&] {
+        Dots d2{ws, st, L2};
+        launch_copy(n, ws.t, ws.s, st);
+        if (W) {
+            CK(cudaEventRecord(e[4], st));
+            L2 += sweep(*W, kWtSolve, ws.s, st);
+            CK(cudaEventRecord(e[5], st));
+        }
+        d2.norm2(n, ws.s, nullptr, gnew);
+        launch_cgls_p_update(n, ws.s, gnew, gamma, ws.p, st);
+        launch_copy(1, gnew, gamma, st);
+        L2 += 3;
+    });
+    if (W) {
+        CK(cudaStreamSynchronize(st));
+        acc(0);
+    }
+    bool g2_pending = false;
+    for (int it = 1; it <= maxit; ++it) {
+        g1.launch(st);
+        L += L1;
         CK(cudaStreamSynchronize(st));
         CK(cudaGetLastError());
-        hres.tn2 = hpin[0];
-        std::memcpy(&hres.brk, hpin + 1, sizeof(int));
-        if (hres.brk) break;
-        const double rel = std::sqrt(hres.tn2) / nres0;
+        if (W) {
+            if (g2_pending) acc(4);
+            acc(2);
+        }
+        g2_pending = false;
+        int brk = 0;
+        std::memcpy(&brk, hpin + 1, sizeof(int));
+        if (brk) break;
+        const double rel = std::sqrt(hpin[0]) / nres0;
         rep.residual_history.push_back(rel);
         rep.iterations = it;
         if (rel <= tol || !std::isfinite(rel)) {
             rep.converged = rel <= tol;
             break;
         }
-        launch_copy(n, ws.t, ws.s, st);
-        if (W) L += sweep(*W, kWtSolve, ws.s, st);
-        dots.norm2(n, ws.s, nullptr, gnew);
-        launch_cgls_p_update(n, ws.s, gnew, gamma, ws.p, st);
-        L += 3;
-        std::swap(gamma, gnew);
+        g2.launch(st);
+        L += L2;
+        g2_pending = true;
     }
-    cudaFreeHost(hpin);
     launch_copy(n, ws.y, d_u, st);
-    if (W) L += sweep(*W, kWSolve, d_u, st);
+    if (W) {
+        CK(cudaEventRecord(e[0], st));
+        L += sweep(*W, kWSolve, d_u, st);
+        CK(cudaEventRecord(e[1], st));
+    }
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
+    if (W) {
+        if (g2_pending) acc(4);
+        acc(0);
+    }
+    for (auto& x : e) cudaEventDestroy(x);
     rep.t_solve = now_s() - t0;
     rep.launches = L;
     return rep;

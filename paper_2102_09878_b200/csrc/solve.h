@@ -12,24 +12,41 @@
 
 namespace spqr {
 
-// Level schedule of W: one batch per engine phase, chronological.
+enum SweepMode { kWSolve = 0, kWtSolve = 1, kWApply = 2, kWtApply = 3 };
+
+// Level schedules of W (transforms.cpp:40-111), one per sweep mode.  A sweep walks W
+// forward (w_apply, wt_solve) or backward (w_solve, wt_apply); each factor reads and
+// writes z[cols] and either reads z[coupled] (w_solve / w_apply) or accumulates into it
+// (wt_solve / wt_apply).  A factor's level is one past the last level of any earlier
+// (in walk order) factor it conflicts with — read-after-write, write-after-read,
+// write-after-write on cols, and a read of an accumulated column — while two
+// accumulations into one column may share a level (the per-level reduction applies
+// them in walk order).  Every level is one launch (+ one for the wide factors, + one
+// reduction): C2 goes from ~400 engine batches per sweep to ~35 levels.
 struct SolvePlan {
-    struct Batch {
+    struct Level {
         const WFac* fac = nullptr;  // warp per factor
         int nf = 0, maxc = 0;
         const WFac* bfac = nullptr;  // CTA per factor (c >= kBigFactorCols)
         int nbf = 0, bmaxc = 0;
-        const int *rptr = nullptr, *ridx = nullptr, *rcol = nullptr;  // wt reduce lists
+        const int *rptr = nullptr, *ridx = nullptr, *rcol = nullptr;  // accumulation lists
         int ncol = 0;
     };
-    std::vector<Batch> batches;
+    struct Schedule {
+        std::vector<Level> levels;
+        long long launches = 0;
+    };
+    Schedule sched[4];  // by SweepMode
     double* contrib = nullptr;
     std::unique_ptr<DeviceArena> mem;
-    long long launches_per_sweep_t = 0, launches_per_sweep = 0;
+    long long launches_per_sweep_t = 0, launches_per_sweep = 0;  // wt_solve / w_solve
+    double t_build = 0.0;
+    // algorithmic HBM bytes of one sweep: 8 nnz(W) + 16 (gathered entries:
+    // z[cols] read + written, z[coupled] read or accumulated)
+    double sweep_bytes = 0.0;
 };
 SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st);
 
-enum SweepMode { kWSolve = 0, kWtSolve = 1, kWApply = 2, kWtApply = 3 };
 long long sweep(const SolvePlan& P, SweepMode mode, double* d_z, cudaStream_t st);  // returns launches
 
 // A on the device in both orientations (row dots for A x and A^T y).
@@ -49,14 +66,29 @@ struct SolveReport {
     std::vector<double> residual_history;
     double t_solve = 0.0;
     long long launches = 0;
+    double sweep_ms = 0.0;  // device time of the W sweeps (CUDA events, also inside the graphs)
+    int sweeps = 0;
 };
 
 // Device workspace for CGLS (vectors of length M and N, scalars).
 struct CglsWork {
-    double *r, *t, *s, *p, *y, *v, *q, *partial, *scal;
-    int* brk;
+    double *r = nullptr, *t = nullptr, *s = nullptr, *p = nullptr, *y = nullptr, *v = nullptr, *q = nullptr;
+    double *partial = nullptr, *scal = nullptr;
+    int* brk = nullptr;
+    double* hpin = nullptr;  // pinned: ||w.t||^2 and the breakdown flag of each iteration
     int nblocks = 0;
     std::unique_ptr<DeviceArena> mem;
+    CglsWork() = default;
+    CglsWork(CglsWork&& o) noexcept { *this = std::move(o); }
+    CglsWork& operator=(CglsWork&& o) noexcept {
+        std::swap(r, o.r), std::swap(t, o.t), std::swap(s, o.s), std::swap(p, o.p), std::swap(y, o.y);
+        std::swap(v, o.v), std::swap(q, o.q), std::swap(partial, o.partial), std::swap(scal, o.scal);
+        std::swap(brk, o.brk), std::swap(hpin, o.hpin), std::swap(nblocks, o.nblocks), std::swap(mem, o.mem);
+        return *this;
+    }
+    ~CglsWork() {
+        if (hpin) cudaFreeHost(hpin);
+    }
 };
 CglsWork make_cgls_work(int m, int n);
 

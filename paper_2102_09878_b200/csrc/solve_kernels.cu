@@ -1,13 +1,14 @@
 // W sweeps and CGLS vector kernels (proj/src/transforms.cpp:40-111,
 // proj/src/solve.cpp:24-76) for B200.
 //
-// A W batch is a run of factors from one engine phase; their column sets are
-// disjoint and no factor's cols meet another's coupled set, so a batch is one
-// launch with one warp per factor.  wt_solve's coupled updates
-// (z[coupled] -= C^T zs) may hit the same column from several factors of a
-// batch: each factor writes its contribution to a scratch vector and a second
-// kernel subtracts them per column in chronological factor order, which is
-// the reference's sequential order and keeps the result deterministic.
+// A sweep runs W's level schedule (solve.cpp build_solve_plan): the factors of one
+// level touch disjoint column sets and no factor's cols meet another's coupled set,
+// so a level is one launch with one warp per factor (one CTA per wide factor).
+// wt_solve's coupled updates (z[coupled] -= C^T zs) may hit the same column from
+// several factors of a level: each factor writes its contribution to a scratch
+// vector and a second kernel subtracts them per column in walk order, which is the
+// reference's sequential order and keeps the result deterministic.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 
@@ -351,11 +352,21 @@ __global__ void k_copy(int n, const double* __restrict__ a, double* __restrict__
 
 }  // namespace
 
+namespace {
+size_t g_wsweep_cfg = 0, g_wsweep_big_cfg = 0;  // dynamic smem opted in so far (see prepare_wsweep)
+}
+
+void prepare_wsweep(int maxc, int bmaxc) {
+    smem_optin(reinterpret_cast<const void*>(k_wsweep), sizeof(double) * static_cast<size_t>(std::max(maxc, 1)) * kWarpsPerBlock,
+               g_wsweep_cfg);
+    smem_optin(reinterpret_cast<const void*>(k_wsweep_big), sizeof(double) * static_cast<size_t>(std::max(bmaxc, 1)),
+               g_wsweep_big_cfg);
+}
+
 static void wsweep(const WFac* f, int nf, double* z, double* contrib, int mode, int maxc, cudaStream_t st) {
     if (nf <= 0) return;
     const size_t smem = sizeof(double) * static_cast<size_t>(maxc > 0 ? maxc : 1) * kWarpsPerBlock;
-    static size_t cfg = 0;
-    smem_optin(reinterpret_cast<const void*>(k_wsweep), smem, cfg);
+    smem_optin(reinterpret_cast<const void*>(k_wsweep), smem, g_wsweep_cfg);
     k_wsweep<<<(nf + kWarpsPerBlock - 1) / kWarpsPerBlock, 32 * kWarpsPerBlock, smem, st>>>(f, nf, z, contrib, mode, maxc);
 }
 
@@ -366,8 +377,7 @@ void launch_wsweep(const WFac* f, int nf, double* z, double* contrib, int mode, 
 void launch_wsweep_big(const WFac* f, int nf, double* z, double* contrib, int mode, int maxc, cudaStream_t st) {
     if (nf <= 0) return;
     const size_t smem = sizeof(double) * static_cast<size_t>(maxc > 0 ? maxc : 1);
-    static size_t cfg = 0;
-    smem_optin(reinterpret_cast<const void*>(k_wsweep_big), smem, cfg);
+    smem_optin(reinterpret_cast<const void*>(k_wsweep_big), smem, g_wsweep_big_cfg);
     k_wsweep_big<<<nf, kBigThreads, smem, st>>>(f, z, contrib, mode);
 }
 
