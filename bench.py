@@ -14,9 +14,10 @@ value    : factorize + solve time measured with CUDA events on the pipeline
 e2e      : the same step through the C ABI from HOST buffers
            (spqr_pipeline_create + spqr_pipeline_solve): partition, upload of A
            and b, factorize, solve, download of x.
---impl reference : the CPU oracle restatement of the reference (the reference
-           itself cannot be built here: Eigen3 is absent), timed on this box's
-           host on the same problem.
+--impl reference : the reference's own sources (proj/src, unmodified) compiled
+           against the in-repo Eigen API shim into oracle/_ref/libspaqr_ref.so
+           (single-threaded, like the reference), timed on this box's host on the
+           same problem; the CPU oracle restatement stands in if that .so is absent.
 Multi-GPU (--gpus N under torchrun): independent replicas, one per GPU
 ("replicas only" in round 1), timed as the max over ranks.
 """
@@ -35,6 +36,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
+
+def config(ws):
+    """The `config` object of both arms' JSON lines (identical keys and values)."""
+    return {"workload": WORKLOAD, "N": 262144, "M": 524288, "levels": 14, "eps": 1e-2, "skip_levels": 3,
+            "cgls_tol": 1e-12, "seed": 0, "parallelism": f"replicas{ws}" if ws > 1 else "1 GPU",
+            "l2_flush": "256 MB write between steps (ours); the CPU arm has no device state"}
+
 
 WORKLOAD = ("C2: 2D tall sparse LS, 512x512 grid, N=262144, M=524288, 5-point rows + 3-nnz random rows, "
             "geometric ND L=14, eps=1e-2, skip_levels=3, CGLS tol 1e-12 (seed 0)")
@@ -158,14 +166,14 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel):
-    """dram bytes (read + write) of one launch of kernel family `kernel` from the committed
-    ncu --set full summary (profiles/ncu_traffic.json), if any."""
+def ncu_traffic(family):
+    """Mean DRAM bytes (read + write) per launch of a kernel family over one C2 step, from the
+    committed ncu launch list summary (profiles/ncu_traffic.json, tools/ncu_traffic.py)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            v = json.load(f).get(kernel)
-        return v.get("dram_bytes") if isinstance(v, dict) else v
+            v = json.load(f).get(family)
+        return v if isinstance(v, dict) else None
     except Exception:
         return None
 
@@ -175,10 +183,21 @@ def make_problem():
     return tall_grid(512, seed=0)
 
 
-def cpu_oracle_step(p):
+def cpu_module():
+    """The CPU implementation timed as the baseline: the reference's own sources built by
+    oracle/Makefile.ref (kind "reference"), else the oracle restatement (kind "port")."""
+    from oracle import ref
+    if os.path.exists(ref.PATH):
+        return ref, "reference"
     import oracle as O
+    return O, "port"
+
+
+def cpu_oracle_step(p, M=None):
+    if M is None:
+        M = cpu_module()[0]
     t0 = time.perf_counter()
-    P = O.Pipeline(p.A, eps=p.eps, levels=p.levels, coords=p.coords)
+    P = M.Pipeline(p.A, eps=p.eps, levels=p.levels, coords=p.coords)
     x, rep = P.solve(p.b)
     wall = time.perf_counter() - t0
     t = P.times()
@@ -322,33 +341,48 @@ def run_ours(args, ws, rank, local):
     g, rep = last
     t = g.times()
     ks = g.kernel_stats()
+    # W-sweep family (solve): device time from CUDA events around every sweep, also inside
+    # the CGLS graphs; algorithmic bytes per sweep = 8 nnz(W) + 16 gathered entries
+    ks["w_sweep"] = {"ms": t["sweep_ms"], "bytes": t["sweep_bytes"] * t["sweeps"],
+                     "launches": int(t["sweeps"] * g.sweep_launches / 2)}
     dom = max(ks, key=lambda k: ks[k]["ms"])
     peak, peak_src = load_peaks()
     d = ks[dom]
     achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
-    per_launch_traffic = ncu_traffic(dom)
+    trf = ncu_traffic(dom)
     # front-QR roofline on its own (the kernel BASELINE.json names)
     q = ks["front_qr"]
     qr_gbs = q["bytes"] / (q["ms"] / 1e3) / 1e9 if q["ms"] > 0 else 0.0
     qr_tflops = t["qr_flops"] / (q["ms"] / 1e3) / 1e12 if q["ms"] > 0 else 0.0
-    x_rel = None
     launches = int(g.launches + t["solve_launches"])
+    fams = {k: {"device_ms": round(v["ms"], 3), "algorithmic_bytes": v["bytes"], "launches": v["launches"],
+                "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 2) if v["ms"] > 0 else None,
+                "frac_hbm": round(v["bytes"] / (v["ms"] / 1e3) / 1e9 / peak, 5) if v["ms"] > 0 else None}
+            for k, v in ks.items()}
     out = {
         "metric": METRIC, "value": round(value, 6), "unit": "s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(value * 1e3, 3), "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "parallelism": f"replicas{ws}", "l2_flush": "256MB write between steps",
-                   "levels": p.levels, "eps": p.eps, "N": int(A.shape[1]), "M": int(A.shape[0])},
+        "config": config(ws),
         "e2e": {"value": round(e2e, 6), "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "note": "spqr_pipeline_create+solve from host CSC/b to host x, incl. host partition "
                         f"({t['t_partition']:.3f}s)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": per_launch_traffic,
+                     "frac": round(achieved / peak, 5),
+                     "traffic": None if trf is None else trf.get("dram_bytes"),
+                     "traffic_note": "mean DRAM bytes (read+write) per launch of the family over one C2 step "
+                                     "(profiles/ncu_traffic.json, tools/ncu_traffic.py); compare with "
+                                     "algorithmic_bytes_per_launch",
+                     "algorithmic_bytes_per_launch": round(d["bytes"] / max(d["launches"], 1), 1),
                      "peak_source": peak_src,
                      "algorithmic_bytes": d["bytes"], "device_ms": round(d["ms"], 3), "launches": d["launches"],
+                     "bytes_formula": "SURVEY 8(d): cpqr 8mn+8rn (discarded speculative rounds apart), "
+                                      "front_qr 16m(n+k), w_sweep 8 nnz(W)+16 gathered, assemble 16/elem",
+                     "cpqr_redundant_bytes": t["cpqr_redundant_bytes"],
                      "front_qr": {"GB/s": round(qr_gbs, 2), "frac_hbm": round(qr_gbs / peak, 4),
                                   "TFLOP/s": round(qr_tflops, 4), "launches": q["launches"],
                                   "device_ms": round(q["ms"], 3)},
+                     "families": fams,
                      "kernel_ms": {k: round(v["ms"], 3) for k, v in ks.items()}},
         "step_values": step_values,
         "gpu_launches": launches,
@@ -357,7 +391,8 @@ def run_ours(args, ws, rank, local):
                   "residual": float(rep["residual_history"][-1]), "nW": g.nW, "nnz_w": g.nnz_w,
                   "factorize_event_s": round(t["factorize_event_ms"] / 1e3, 4),
                   "solve_event_s": round(t["solve_event_ms"] / 1e3, 4), "engine_syncs": g.syncs,
-                  "elim_waves": t["elim_waves"]},
+                  "elim_waves": t["elim_waves"], "w_solve_levels": t["w_solve_levels"],
+                  "solve_plan_s": round(t["solve_plan_s"], 4), "solve_launches": t["solve_launches"]},
     }
     if not args.no_microbench:
         try:
@@ -367,36 +402,49 @@ def run_ours(args, ws, rank, local):
         if rank == 0:
             out["front_qr_microbench"] = mb
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        v, wall, iters, tpart = cpu_oracle_step(p)
-        out["cpu_baseline"] = {"value": round(v, 4), "unit": "s", "cores": 1, "kind": "port",
-                               "sample": "full C2 problem, one factorize+solve of the single-threaded CPU oracle "
-                                         f"(oracle/; {iters} CGLS iterations; partition {tpart:.2f}s excluded)"}
+        M, kind = cpu_module()
+        v, wall, iters, tpart = cpu_oracle_step(p, M)
+        what = ("the reference's own proj/src compiled unmodified against the in-repo Eigen API shim "
+                "(oracle/_ref)" if kind == "reference" else "the CPU oracle restatement (oracle/)")
+        out["cpu_baseline"] = {"value": round(v, 4), "unit": "s", "cores": 1, "kind": kind,
+                               "sample": f"full C2 problem, one factorize+solve (t_factorize + t_solve) of {what}, "
+                                         f"single-threaded like the reference; {iters} CGLS iterations; "
+                                         f"host partition {tpart:.2f}s excluded as in the value"}
     if rank == 0:
         print(json.dumps(out))
 
 
 def run_reference(args, ws, rank):
+    """The reference arm: the reference's CPU implementation (oracle/_ref, else the port) on the
+    same C2 problem.  One step = one full factorize + solve (25-60 s on these hosts); the number
+    of steps is capped so the run ends within ~4 minutes (a bounded sample of --steps)."""
     if rank != 0:
         return
+    M, kind = cpu_module()
     p = make_problem()
     vals, walls, its = [], [], []
-    # the oracle is a pure CPU program: there is no device state to warm up, so
-    # warm-up steps are not repeated; at most 2 timed steps keep the run bounded.
-    for _ in range(max(1, min(args.steps, 2))):
-        v, wall, iters, tpart = cpu_oracle_step(p)
+    budget = 240.0
+    t_start = time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        v, wall, iters, tpart = cpu_oracle_step(p, M)
         vals.append(v)
         walls.append(wall)
         its.append(iters)
+        if time.perf_counter() - t_start + wall > budget:
+            break
     v = sum(vals) / len(vals)
+    what = ("reference proj/src (unmodified) built against the in-repo Eigen API shim, oracle/_ref"
+            if kind == "reference" else "CPU oracle restatement (oracle/); oracle/_ref absent")
     out = {"metric": METRIC, "value": round(v, 4), "unit": "s", "n_gpus": ws, "steps": len(vals),
-           "warmup": 0, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": {"workload": WORKLOAD, "parallelism": "cpu-1-thread"},
-           "cpu_baseline": {"value": round(v, 4), "unit": "s", "cores": 1, "kind": "port",
-                            "sample": "full C2 problem per step (CPU oracle restatement; reference needs Eigen3, "
-                                      "absent)"},
+           "steps_requested": args.steps, "warmup": 0, "ms_per_step": round(v * 1e3, 1),
+           "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "impl": "reference", "config": config(ws),
+           "cpu_baseline": {"value": round(v, 4), "unit": "s", "cores": 1, "kind": kind,
+                            "sample": f"full C2 problem per step, t_factorize + t_solve, {what}; "
+                                      f"{len(vals)} of {args.steps} steps within a {budget:.0f} s budget; "
+                                      "no warm-up (no device state)"},
            "e2e": {"value": round(v, 4), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "iterations": its[-1]}
+           "step_values": [round(x, 3) for x in vals], "iterations": its[-1]}
     print(json.dumps(out))
 
 

@@ -296,7 +296,10 @@ int spqr_pipeline_apply(spqr_pipeline* p, int mode, double* z) {
         const int n = p->Aw.n;
         CK(cudaMemcpyAsync(p->d_u, z, sizeof(double) * n, cudaMemcpyHostToDevice, p->st));
         static const SweepMode map[4] = {kWApply, kWSolve, kWtApply, kWtSolve};
-        if (p->has_f) sweep(p->plan, map[mode & 3], p->d_u, p->st);
+        if (p->has_f) {
+            ensure_schedule(p->plan, p->F, map[mode & 3], p->st);
+            sweep(p->plan, map[mode & 3], p->d_u, p->st);
+        }
         CK(cudaMemcpyAsync(z, p->d_u, sizeof(double) * n, cudaMemcpyDeviceToHost, p->st));
         CK(cudaStreamSynchronize(p->st));
     });

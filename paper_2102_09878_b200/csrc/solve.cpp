@@ -8,154 +8,182 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <stdexcept>
 
 namespace spqr {
 
-SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
-    const double t0 = now_s();
-    SolvePlan P;
-    P.mem = std::make_unique<DeviceArena>(size_t(64) << 20);
+namespace {
+
+// The level schedule of one sweep mode (see solve.h): levels from the walk-order
+// conflicts, factors bucketed per level, descriptors and accumulation lists uploaded.
+void build_schedule(SolvePlan& P, const DeviceFactorization& F, int mode, const int* d_idx, Uploader& up,
+                    std::vector<int>& lastW, std::vector<int>& lastR, std::vector<int>& lastA, long long& maxcontrib) {
+    const int nfac = static_cast<int>(F.W.size());
+    // factors at least this wide run one per CTA (SPQR_BIG_FACTOR overrides, for tests)
+    static const int big_cols =
+        std::getenv("SPQR_BIG_FACTOR") ? std::atoi(std::getenv("SPQR_BIG_FACTOR")) : kBigFactorCols;
+    const bool forward = (mode == kWtSolve || mode == kWApply);
+    const bool accumulate = (mode == kWtSolve || mode == kWtApply);
+    std::fill(lastW.begin(), lastW.end(), 0);
+    std::fill(lastR.begin(), lastR.end(), 0);
+    std::fill(lastA.begin(), lastA.end(), 0);
+    std::vector<int> level(nfac);
+    int nlev = 0;
+    for (int t = 0; t < nfac; ++t) {
+        const int q = forward ? t : nfac - 1 - t;
+        const DevWFactor& w = F.W[q];
+        const int* cols = F.idx.data() + w.cols_off;
+        const int* cp = F.idx.data() + w.coupled_off;
+        const int k = (w.kind == 0) ? w.k : 0;
+        int L = 0;
+        for (int i = 0; i < w.c; ++i) L = std::max({L, lastW[cols[i]], lastR[cols[i]], lastA[cols[i]]});
+        if (accumulate) {
+            int La = 0;
+            for (int j = 0; j < k; ++j) {
+                L = std::max({L, lastW[cp[j]], lastR[cp[j]]});
+                La = std::max(La, lastA[cp[j]]);
+            }
+            L = std::max(L + 1, La);
+            for (int j = 0; j < k; ++j) lastA[cp[j]] = std::max(lastA[cp[j]], L);
+        } else {
+            for (int j = 0; j < k; ++j) L = std::max(L, lastW[cp[j]]);
+            ++L;
+            for (int j = 0; j < k; ++j) lastR[cp[j]] = std::max(lastR[cp[j]], L);
+        }
+        for (int i = 0; i < w.c; ++i) {
+            lastW[cols[i]] = L;
+            lastR[cols[i]] = std::max(lastR[cols[i]], L);
+        }
+        level[q] = L;
+        nlev = std::max(nlev, L);
+    }
+    // bucket the factors by level, in walk order
+    std::vector<int> cnt(nlev + 2, 0);
+    for (int q = 0; q < nfac; ++q) ++cnt[level[q] + 1];
+    for (int l = 0; l <= nlev; ++l) cnt[l + 1] += cnt[l];
+    std::vector<int> byl(nfac), pos(cnt.begin(), cnt.end() - 1);
+    for (int t = 0; t < nfac; ++t) {
+        const int q = forward ? t : nfac - 1 - t;
+        byl[pos[level[q]]++] = q;
+    }
+    SolvePlan::Schedule& S = P.sched[mode];
+    S.levels.clear();
+    S.launches = 0;
+    std::vector<WFac> fac, bfac;
+    std::vector<std::pair<int, int>> lists;  // (coupled column, contribution index) in walk order
+    std::vector<int> rptr, ridx, rcol;
+    for (int l = 1; l <= nlev; ++l) {
+        fac.clear();
+        bfac.clear();
+        lists.clear();
+        long long contrib = 0;
+        int maxc = 1, bmaxc = 1;
+        for (int e = cnt[l]; e < cnt[l + 1]; ++e) {
+            const DevWFactor& w = F.W[byl[e]];
+            WFac f{};
+            f.kind = w.kind;
+            f.c = w.c;
+            f.k = w.k;
+            f.cols = d_idx + w.cols_off;
+            f.coupled = d_idx + w.coupled_off;
+            f.a = w.a;
+            f.tau = w.tau;
+            f.sign = w.sign;
+            f.contrib_off = contrib;
+            if (accumulate && w.kind == 0 && w.k > 0) {
+                for (int t = 0; t < w.k; ++t) lists.emplace_back(F.idx[w.coupled_off + t], static_cast<int>(contrib + t));
+                contrib += w.k;
+            }
+            // triangular factors: the warp path's back substitution is c sequential steps of
+            // c/32 work; rotations: the CTA path pays two block barriers per reflector, so only
+            // very tall ones move
+            if (w.kind == 0 ? w.c >= big_cols : w.c >= 8 * big_cols) {
+                bmaxc = std::max(bmaxc, w.c);
+                bfac.push_back(f);
+            } else {
+                maxc = std::max(maxc, w.c);
+                fac.push_back(f);
+            }
+        }
+        SolvePlan::Level lv;
+        lv.fac = up.put(fac);
+        lv.nf = static_cast<int>(fac.size());
+        lv.maxc = maxc;
+        lv.bfac = up.put(bfac);
+        lv.nbf = static_cast<int>(bfac.size());
+        lv.bmaxc = bmaxc;
+        if (!lists.empty()) {
+            // per coupled column (ascending) its contributions in walk order: indices grow
+            // along the walk, so sorting the pairs gives exactly that
+            std::sort(lists.begin(), lists.end());
+            rptr.assign(1, 0);
+            ridx.clear();
+            rcol.clear();
+            for (size_t a = 0; a < lists.size();) {
+                size_t e = a;
+                while (e < lists.size() && lists[e].first == lists[a].first) ridx.push_back(lists[e++].second);
+                rcol.push_back(lists[a].first);
+                rptr.push_back(static_cast<int>(ridx.size()));
+                a = e;
+            }
+            lv.rptr = up.put(rptr);
+            lv.ridx = up.put(ridx);
+            lv.rcol = up.put(rcol);
+            lv.ncol = static_cast<int>(rcol.size());
+        }
+        maxcontrib = std::max(maxcontrib, contrib);
+        S.launches += (lv.nf > 0) + (lv.nbf > 0) + (lv.ncol > 0);
+        S.levels.push_back(lv);
+    }
+    S.built = true;
+    for (const auto& lv : S.levels) {
+        P.maxc = std::max(P.maxc, lv.maxc);
+        P.bmaxc = std::max(P.bmaxc, lv.bmaxc);
+    }
+}
+
+void build_schedules(SolvePlan& P, const DeviceFactorization& F, cudaStream_t st, std::initializer_list<int> modes) {
     SharedPinned& sp = SharedPinned::get();
     std::lock_guard<std::mutex> pin_lock(sp.mu);
     PinnedArena& pin = sp.arena;
     pin.reset();
     Uploader up{P.mem.get(), &pin, st};
-    const int* d_idx = up.put(F.idx);
-    const int nfac = static_cast<int>(F.W.size());
-    // factors at least this wide run one per CTA (SPQR_BIG_FACTOR overrides, for tests)
-    const int big_cols = std::getenv("SPQR_BIG_FACTOR") ? std::atoi(std::getenv("SPQR_BIG_FACTOR")) : kBigFactorCols;
-    long long maxcontrib = 1;
-    std::vector<int> lastW(F.N > 0 ? F.N : 1), lastR(F.N > 0 ? F.N : 1), lastA(F.N > 0 ? F.N : 1), level(nfac);
-    for (int mode = 0; mode < 4; ++mode) {
-        const bool forward = (mode == kWtSolve || mode == kWApply);
-        const bool accumulate = (mode == kWtSolve || mode == kWtApply);
-        std::fill(lastW.begin(), lastW.end(), 0);
-        std::fill(lastR.begin(), lastR.end(), 0);
-        std::fill(lastA.begin(), lastA.end(), 0);
-        int nlev = 0;
-        for (int t = 0; t < nfac; ++t) {
-            const int q = forward ? t : nfac - 1 - t;
-            const DevWFactor& w = F.W[q];
-            const int* cols = F.idx.data() + w.cols_off;
-            const int* cp = F.idx.data() + w.coupled_off;
-            const int k = (w.kind == 0) ? w.k : 0;
-            int L = 0;
-            for (int i = 0; i < w.c; ++i) L = std::max({L, lastW[cols[i]], lastR[cols[i]], lastA[cols[i]]});
-            if (accumulate) {
-                int La = 0;
-                for (int j = 0; j < k; ++j) {
-                    L = std::max({L, lastW[cp[j]], lastR[cp[j]]});
-                    La = std::max(La, lastA[cp[j]]);
-                }
-                L = std::max(L + 1, La);
-                for (int j = 0; j < k; ++j) lastA[cp[j]] = std::max(lastA[cp[j]], L);
-            } else {
-                for (int j = 0; j < k; ++j) L = std::max(L, lastW[cp[j]]);
-                ++L;
-                for (int j = 0; j < k; ++j) lastR[cp[j]] = std::max(lastR[cp[j]], L);
-            }
-            for (int i = 0; i < w.c; ++i) {
-                lastW[cols[i]] = L;
-                lastR[cols[i]] = std::max(lastR[cols[i]], L);
-            }
-            level[q] = L;
-            nlev = std::max(nlev, L);
-        }
-        // bucket the factors by level, in walk order
-        std::vector<int> cnt(nlev + 2, 0);
-        for (int q = 0; q < nfac; ++q) ++cnt[level[q] + 1];
-        for (int l = 0; l <= nlev; ++l) cnt[l + 1] += cnt[l];
-        std::vector<int> byl(nfac), pos(cnt.begin(), cnt.end() - 1);
-        for (int t = 0; t < nfac; ++t) {
-            const int q = forward ? t : nfac - 1 - t;
-            byl[pos[level[q]]++] = q;
-        }
-        SolvePlan::Schedule& S = P.sched[mode];
-        for (int l = 1; l <= nlev; ++l) {
-            std::vector<WFac> fac, bfac;
-            std::vector<std::pair<int, int>> lists;  // (coupled column, contribution index) in walk order
-            long long contrib = 0;
-            int maxc = 1, bmaxc = 1;
-            for (int e = cnt[l]; e < cnt[l + 1]; ++e) {
-                const DevWFactor& w = F.W[byl[e]];
-                WFac f{};
-                f.kind = w.kind;
-                f.c = w.c;
-                f.k = w.k;
-                f.cols = d_idx + w.cols_off;
-                f.coupled = d_idx + w.coupled_off;
-                f.a = w.a;
-                f.tau = w.tau;
-                f.sign = w.sign;
-                f.contrib_off = contrib;
-                if (accumulate && w.kind == 0 && w.k > 0) {
-                    for (int t = 0; t < w.k; ++t)
-                        lists.emplace_back(F.idx[w.coupled_off + t], static_cast<int>(contrib + t));
-                    contrib += w.k;
-                }
-                // triangular factors: the warp path's back substitution is c sequential steps of
-                // c/32 work; rotations: the CTA path pays two block barriers per reflector, so only
-                // very tall ones move
-                if (w.kind == 0 ? w.c >= big_cols : w.c >= 8 * big_cols) {
-                    bmaxc = std::max(bmaxc, w.c);
-                    bfac.push_back(f);
-                } else {
-                    maxc = std::max(maxc, w.c);
-                    fac.push_back(f);
-                }
-            }
-            SolvePlan::Level lv;
-            lv.fac = up.put(fac);
-            lv.nf = static_cast<int>(fac.size());
-            lv.maxc = maxc;
-            lv.bfac = up.put(bfac);
-            lv.nbf = static_cast<int>(bfac.size());
-            lv.bmaxc = bmaxc;
-            if (!lists.empty()) {
-                // per coupled column (ascending) its contributions in walk order: indices grow
-                // along the walk, so sorting the pairs gives exactly that
-                std::sort(lists.begin(), lists.end());
-                std::vector<int> ptr{0}, idx, col;
-                idx.reserve(lists.size());
-                for (size_t a = 0; a < lists.size();) {
-                    size_t e = a;
-                    while (e < lists.size() && lists[e].first == lists[a].first) idx.push_back(lists[e++].second);
-                    col.push_back(lists[a].first);
-                    ptr.push_back(static_cast<int>(idx.size()));
-                    a = e;
-                }
-                lv.rptr = up.put(ptr);
-                lv.ridx = up.put(idx);
-                lv.rcol = up.put(col);
-                lv.ncol = static_cast<int>(col.size());
-            }
-            maxcontrib = std::max(maxcontrib, contrib);
-            S.launches += (lv.nf > 0) + (lv.nbf > 0) + (lv.ncol > 0);
-            S.levels.push_back(lv);
-        }
+    if (!P.d_idx) P.d_idx = up.put(F.idx);
+    const size_t n = F.N > 0 ? static_cast<size_t>(F.N) : 1;
+    std::vector<int> lastW(n), lastR(n), lastA(n);
+    long long maxcontrib = P.ncontrib;
+    for (int mode : modes) build_schedule(P, F, mode, P.d_idx, up, lastW, lastR, lastA, maxcontrib);
+    if (maxcontrib > P.ncontrib) {
+        P.contrib = P.mem->alloc_n<double>(maxcontrib);
+        P.ncontrib = maxcontrib;
     }
-    P.contrib = P.mem->alloc_n<double>(maxcontrib);
-    int allc = 1, allb = 1;
-    for (const auto& S : P.sched)
-        for (const auto& lv : S.levels) {
-            allc = std::max(allc, lv.maxc);
-            allb = std::max(allb, lv.bmaxc);
-        }
-    prepare_wsweep(allc, allb);
-    {
-        double gathered = 0.0;
-        for (const auto& w : F.W) gathered += w.c + (w.kind == 0 ? w.k : 0);
-        P.sweep_bytes = 8.0 * static_cast<double>(F.nnz_w()) + 16.0 * gathered;
-    }
-    P.launches_per_sweep = P.sched[kWSolve].launches;
-    P.launches_per_sweep_t = P.sched[kWtSolve].launches;
+    prepare_wsweep(P.maxc, P.bmaxc);
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
+}
+
+}  // namespace
+
+SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st) {
+    const double t0 = now_s();
+    SolvePlan P;
+    P.mem = std::make_unique<DeviceArena>(size_t(64) << 20);
+    build_schedules(P, F, st, {kWSolve, kWtSolve});  // the CGLS / CSNE sweeps; apply modes on demand
+    double gathered = 0.0;
+    for (const auto& w : F.W) gathered += w.c + (w.kind == 0 ? w.k : 0);
+    P.sweep_bytes = 8.0 * static_cast<double>(F.nnz_w()) + 16.0 * gathered;
+    P.launches_per_sweep = P.sched[kWSolve].launches;
+    P.launches_per_sweep_t = P.sched[kWtSolve].launches;
     P.t_build = now_s() - t0;
     return P;
 }
 
+void ensure_schedule(SolvePlan& P, const DeviceFactorization& F, SweepMode mode, cudaStream_t st) {
+    if (!P.sched[mode].built) build_schedules(P, F, st, {static_cast<int>(mode)});
+}
+
 long long sweep(const SolvePlan& P, SweepMode mode, double* d_z, cudaStream_t st) {
+    if (!P.sched[mode].built) throw std::logic_error("W sweep schedule not built (ensure_schedule)");
     long long L = 0;
     for (const auto& lv : P.sched[mode].levels) {
         if (lv.nf > 0) {
@@ -320,9 +348,9 @@ SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, 
         Dots d1{ws, st, L1};
         launch_copy(n, ws.p, ws.v, st);
         if (W) {
-            CK(cudaEventRecord(e[2], st));
+            CK(cudaEventRecordWithFlags(e[2], st, cudaEventRecordExternal));  // a record node in the graph
             L1 += sweep(*W, kWSolve, ws.v, st);
-            CK(cudaEventRecord(e[3], st));
+            CK(cudaEventRecordWithFlags(e[3], st, cudaEventRecordExternal));
         }
         launch_spmv_csr(m, A.rp, A.ri, A.rv, ws.v, ws.q, st);  // q = A v
         d1.norm2(m, ws.q, nullptr, sc + 3);
@@ -340,9 +368,9 @@ SolveReport gpu_cgls(const DevMatrix& A, const SolvePlan* W, const double* d_b, 
         Dots d2{ws, st, L2};
         launch_copy(n, ws.t, ws.s, st);
         if (W) {
-            CK(cudaEventRecord(e[4], st));
+            CK(cudaEventRecordWithFlags(e[4], st, cudaEventRecordExternal));  // a record node in the graph
             L2 += sweep(*W, kWtSolve, ws.s, st);
-            CK(cudaEventRecord(e[5], st));
+            CK(cudaEventRecordWithFlags(e[5], st, cudaEventRecordExternal));
         }
         d2.norm2(n, ws.s, nullptr, gnew);
         launch_cgls_p_update(n, ws.s, gnew, gamma, ws.p, st);

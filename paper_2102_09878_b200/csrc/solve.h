@@ -35,9 +35,13 @@ struct SolvePlan {
     struct Schedule {
         std::vector<Level> levels;
         long long launches = 0;
+        bool built = false;
     };
-    Schedule sched[4];  // by SweepMode
+    Schedule sched[4];  // by SweepMode; w_apply / wt_apply are built on first use
+    const int* d_idx = nullptr;
     double* contrib = nullptr;
+    long long ncontrib = 0;
+    int maxc = 1, bmaxc = 1;
     std::unique_ptr<DeviceArena> mem;
     long long launches_per_sweep_t = 0, launches_per_sweep = 0;  // wt_solve / w_solve
     double t_build = 0.0;
@@ -46,6 +50,7 @@ struct SolvePlan {
     double sweep_bytes = 0.0;
 };
 SolvePlan build_solve_plan(const DeviceFactorization& F, cudaStream_t st);
+void ensure_schedule(SolvePlan& P, const DeviceFactorization& F, SweepMode mode, cudaStream_t st);
 
 long long sweep(const SolvePlan& P, SweepMode mode, double* d_z, cudaStream_t st);  // returns launches
 
