@@ -77,6 +77,12 @@ void spqr_pipeline_owner(const spqr_pipeline* p, int* owner);        /* M: row -
 void spqr_pipeline_weights(const spqr_pipeline* p, double* w);       /* N */
 /* pivot_row: N; dropped: n_dropped; trailing: n_trailing (info[5], info[6]) */
 void spqr_pipeline_rows(const spqr_pipeline* p, int* pivot_row, int* dropped, int* trailing);
+/* The SeparatorTree (partition.h:14-27): returns the node count; parent[ntree] and the root
+ * when non-NULL.  finest_of_col: N.  scaled: the scaled, permuted A (Pipeline::scaled,
+ * pipeline.h:62) as CSC (colptr N+1, rowind / vals nnz(A) = info[9]). */
+int spqr_pipeline_tree(const spqr_pipeline* p, int* parent, int* root);
+void spqr_pipeline_finest(const spqr_pipeline* p, int* finest_of_col);
+void spqr_pipeline_scaled(const spqr_pipeline* p, int* colptr, int* rowind, double* vals);
 /* cluster: tree_node, level, parent, stage, interior, ncols */
 void spqr_pipeline_cluster(const spqr_pipeline* p, int c, int* info6);
 void spqr_pipeline_cluster_cols(const spqr_pipeline* p, int c, int* cols);
@@ -93,6 +99,45 @@ int spqr_pipeline_wfactor_data(const spqr_pipeline* p, int i, int* cols, double*
  * SPQRFW01 file readable by the reference's load_factorization (transforms.cpp:242-289).
  * Returns SPQR_OK, or an error code with the message in err. */
 int spqr_pipeline_save(const spqr_pipeline* p, const char* path, char* err, int errlen);
+
+/* ---- engine- and solver-level entry points ------------------------------------------ */
+/* A factorization handle: W resident on one GPU (transforms.h:53-72). */
+typedef struct spqr_factorization spqr_factorization;
+
+/* spaqr_factorize(A, h, row_owner, opt) (factorize.h:51-53; factorize.cpp:795-804) on a
+ * caller-supplied hierarchy.  A: m x n CSC, already column-scaled and permuted (the engine's
+ * input, pipeline.cpp:47-53).  The ClusterHierarchy (partition.h:54-75) as flat arrays:
+ * cluster_info[5*c] = tree_node, level, parent, stage, interior; cluster c's (permuted) columns
+ * cluster_cols[cluster_colptr[c] .. cluster_colptr[c+1]); finest_of_col[n]; the SeparatorTree
+ * nodes' parents tree_parent[ntree] and its root.  row_owner[m]: a stage-(L+1) cluster per row.
+ * Errors: m < n or inconsistent hierarchy / owner arrays -> SPQR_E_SHAPE (std::invalid_argument);
+ * SingularFrontError -> SPQR_E_SINGULAR with *err_cluster. */
+int spqr_factorize(int m, int n, const int* colptr, const int* rowind, const double* vals, int num_levels,
+                   int nclusters, const int* cluster_info, const int* cluster_colptr, const int* cluster_cols,
+                   const int* finest_of_col, int ntree, const int* tree_parent, int tree_root, const int* row_owner,
+                   double eps, int skip_levels, int device, spqr_factorization** out, char* err, int errlen,
+                   int* err_cluster);
+void spqr_factorization_destroy(spqr_factorization* f);
+/* info[8]: M, N, nW, nnz_w, n_dropped, n_trailing, n_stages, w_solve sweep levels */
+void spqr_factorization_info(const spqr_factorization* f, long long* info);
+void spqr_factorization_rows(const spqr_factorization* f, int* pivot_row, int* dropped, int* trailing);
+/* StageStats s (transforms.h:40-47): out5 = stage, nfronts, top_rows, top_cols, nnz_w */
+int spqr_factorization_stage(const spqr_factorization* f, int s, long long* out5);
+int spqr_factorization_stage_fronts(const spqr_factorization* f, int s, int* front_cols);
+/* Factorization::w_apply / w_solve / wt_apply / wt_solve (transforms.h:66-69) on host z (N). */
+int spqr_factorization_apply(spqr_factorization* f, int mode, double* z);
+/* save_factorization / load_factorization (transforms.h:75-76; transforms.cpp:206-289): SPQRFW01
+ * files; a loaded factorization solves on the GPU (factor once, solve many).  Q sections of
+ * store_q files are read and dropped. */
+int spqr_factorization_save(const spqr_factorization* f, const char* path, char* err, int errlen);
+int spqr_factorization_load(const char* path, int device, spqr_factorization** out, char* err, int errlen);
+/* cgls(A, W, b, u, opt, weights) (solve.h:30-31; solve.cpp:24-76) on the GPU: A m x n CSC in W's
+ * column coordinates, W may be NULL (plain CGLS), weights (n) may be NULL; u (n) out;
+ * tol <= 0 / maxit <= 0 take 1e-12 / 500.  hist needs maxit + 2 slots.  device is used when W is
+ * NULL (else W's device). */
+int spqr_cgls(int m, int n, const int* colptr, const int* rowind, const double* vals, spqr_factorization* W,
+              const double* b, double* u, double tol, int maxit, const double* weights, int device, int* iters,
+              int* converged, double* hist, int* nhist, double* t_solve, char* err, int errlen);
 
 /* ---- dense kernels (dense_kernels.h:24-54), batched, one launch each ---- */
 /* block_householder_qr + apply_reflectors_left_t fused: for each of nb problems

@@ -1,25 +1,3 @@
-# INTEGRATION — binding the B200 library from the reference
-
-The reference (`proj/`) is C++20; its public API is `proj/include/spaqr/*.h` and it has no
-FFI layer. The B200 implementation exposes the same operations through a C ABI
-(`include/spaqr_b200.h`, library `paper_2102_09878_b200/libspaqr_b200.so`, built by
-`__graft_entry__.build()` or `make -C paper_2102_09878_b200`).
-
-## C++ shim a maintainer would add to the reference
-
-`integration/pipeline_b200.hpp` (embedded below, kept identical by `tests/test_integration.py`)
-gives the reference drop-in `PipelineB200`, `spaqr_factorize_b200`, `FactorizationB200`
-(w_solve / wt_solve / save / load) and `cgls_b200` with the reference's signatures
-(`pipeline.h:39-52`, `factorize.h:51-53`, `solve.h:30-31`, `transforms.h:66-76`) and error types
-(`types.h:24-31`). It is not just documentation: `integration/Makefile` compiles it against the
-reference's own headers (`/root/reference/proj/include`, with the in-repo Eigen API shim) and links
-`integration/demo.cpp` with both the reference's sources (`oracle/_ref/libspaqr_ref.so`) and
-`libspaqr_b200.so`. The demo runs the reference's `Pipeline`, `spaqr_factorize`, `cgls`,
-`save_factorization` / `load_factorization` and `SingularFrontError` path next to the B200 bindings on
-the same problem and compares them (`tests/test_integration.py`, `-m gpu`); without a GPU it checks
-that the B200 path refuses to run.
-
-```cpp
 // The C++ shim a maintainer would add to the reference (proj/src/pipeline_b200.hpp) to run
 // its Pipeline / spaqr_factorize / cgls on the B200 library through the C ABI
 // (include/spaqr_b200.h).  Same signatures and error types as the reference:
@@ -188,40 +166,3 @@ inline SolveReport cgls_b200(const SparseMatrix& A, const FactorizationB200* W, 
 }
 
 }  // namespace spaqr
-```
-
-Mapping of the remaining reference calls: `Factorization::w_apply / w_solve / wt_apply / wt_solve`
--> `spqr_pipeline_apply(h, SPQR_W_*, z)` or `spqr_factorization_apply(f, SPQR_W_*, z)`;
-`save_factorization(F, path)` -> `spqr_pipeline_save` / `spqr_factorization_save` (SPQRFW01 bytes,
-readable by the reference's `load_factorization`); `load_factorization(path)` ->
-`spqr_factorization_load(path, device, &f)` (W straight onto the GPU); `truncated_cpqr`,
-`block_householder_qr` + `apply_reflectors_left_t`, and `tri_solve_upper(..., Right, false)` -> the
-batched `spqr_cpqr_batched`, `spqr_qr_apply_batched`, `spqr_trsm_right_batched`. For callers that
-already hold device buffers (and for the C5 microbenchmark) `spqr_qr_apply_batched_dev` and
-`spqr_cpqr_batched_dev` run the same kernels in place on device pointers and return the device time
-of the launches. `make_profile` / `validate_profile` are mirrored in
-`paper_2102_09878_b200/profile.py`.
-
-## ctypes (what this repo's Python layer does)
-
-`paper_2102_09878_b200/_lib.py` declares every symbol of the header; `api.py` mirrors the
-reference API:
-
-```python
-import paper_2102_09878_b200 as spaqr
-from paper_2102_09878_b200.problems import tall_grid
-
-p = tall_grid(512)                                   # BASELINE config 2
-pipe = spaqr.Pipeline(p.A, eps=1e-2, levels=14, coords=p.coords)
-x, rep = pipe.solve(p.b)                             # Pipeline::solve -> device CGLS
-print(rep["iterations"], rep["residual_history"][-1])
-```
-
-Engine- and solver-level calls: `spaqr.spaqr_factorize(pipe.scaled(), pipe.hierarchy(), pipe.owner(),
-eps=1e-2)` returns a `spaqr.Factorization` (W on the GPU; `.w_solve`, `.save`,
-`spaqr.Factorization.load(path)`), and `spaqr.cgls(A, W, b, tol, maxit, weights)` runs the reference's
-`cgls` on the device.
-
-Errors: `spaqr.SingularFrontError` carries `.cluster` and `.reason` like the reference's
-`SingularFrontError`; shape errors raise `ValueError` (the reference's `std::invalid_argument`).
-There is no CPU fallback: without a visible GPU the constructor raises.

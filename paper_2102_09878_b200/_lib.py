@@ -46,6 +46,23 @@ SIGNATURES = {
     "spqr_pipeline_wfactor": (None, [vp, C.c_int, i32p]),
     "spqr_pipeline_wfactor_data": (C.c_int, [vp, C.c_int, i32p, f64p, i32p, f64p, f64p]),
     "spqr_pipeline_save": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_int]),
+    "spqr_pipeline_tree": (C.c_int, [vp, vp, vp]),
+    "spqr_pipeline_finest": (None, [vp, i32p]),
+    "spqr_pipeline_scaled": (None, [vp, i32p, i32p, f64p]),
+    "spqr_factorize": (C.c_int, [C.c_int, C.c_int, i32p, i32p, f64p, C.c_int, C.c_int, i32p, i32p, i32p, i32p,
+                                 C.c_int, i32p, C.c_int, i32p, C.c_double, C.c_int, C.c_int, C.POINTER(vp),
+                                 C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
+    "spqr_factorization_destroy": (None, [vp]),
+    "spqr_factorization_info": (None, [vp, i64p]),
+    "spqr_factorization_rows": (None, [vp, i32p, i32p, i32p]),
+    "spqr_factorization_stage": (C.c_int, [vp, C.c_int, i64p]),
+    "spqr_factorization_stage_fronts": (C.c_int, [vp, C.c_int, i32p]),
+    "spqr_factorization_apply": (C.c_int, [vp, C.c_int, f64p]),
+    "spqr_factorization_save": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_int]),
+    "spqr_factorization_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(vp), C.c_char_p, C.c_int]),
+    "spqr_cgls": (C.c_int, [C.c_int, C.c_int, i32p, i32p, f64p, vp, f64p, f64p, C.c_double, C.c_int, vp, C.c_int,
+                            C.POINTER(C.c_int), C.POINTER(C.c_int), f64p, C.POINTER(C.c_int),
+                            C.POINTER(C.c_double), C.c_char_p, C.c_int]),
     "spqr_qr_apply_batched": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, f64p, f64p, f64p, i32p]),
     "spqr_qr_apply_batched_dev": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp,
                                             C.POINTER(C.c_float)]),

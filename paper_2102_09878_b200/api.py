@@ -40,6 +40,10 @@ class Pipeline:
         require_gpu()
         L = lib()
         m, n, p, i, x = _csc(A)
+        if coords is not None and np.asarray(coords).shape[0] != n:  # pipeline.cpp:39-40
+            raise ValueError("coordinate row count does not match column count")
+        if parts is not None and len(parts) != n:
+            raise ValueError("partition length does not match column count")
         cp = None if coords is None else np.ascontiguousarray(coords, np.float64)
         pp = None if parts is None else np.ascontiguousarray(parts, np.int32)
         dim = 0 if cp is None else cp.shape[1]
@@ -85,6 +89,8 @@ class Pipeline:
 
     def solve(self, b, tol=-1.0, maxit=-1, direct=False):
         b = np.ascontiguousarray(b, np.float64)
+        if b.ndim != 1 or b.shape[0] != self.M:  # pipeline.cpp:71,84
+            raise ValueError("right-hand side length mismatch")
         x = np.zeros(self.N)
         hist = np.zeros((maxit if maxit > 0 else 500) + 4)
         it, cv, nh = C.c_int(), C.c_int(), C.c_int()
@@ -99,6 +105,8 @@ class Pipeline:
 
     def _apply(self, mode, z):
         z = np.array(z, dtype=np.float64, copy=True)
+        if z.ndim != 1 or z.shape[0] != self.N:
+            raise ValueError("vector length does not match the factorization")
         if lib().spqr_pipeline_apply(self.h, mode, z):
             raise RuntimeError("spqr_pipeline_apply failed")
         return z
@@ -161,6 +169,26 @@ class Pipeline:
         err = C.create_string_buffer(512)
         if lib().spqr_pipeline_save(self.h, str(path).encode(), err, 512):
             raise RuntimeError(err.value.decode())
+
+    def scaled(self):
+        """Pipeline::scaled() (pipeline.h:62): the column-scaled, permuted A the engine factors."""
+        import scipy.sparse as sp
+        p = np.zeros(self.N + 1, np.int32)
+        i = np.zeros(self.nnz_A, np.int32)
+        x = np.zeros(self.nnz_A)
+        lib().spqr_pipeline_scaled(self.h, p, i, x)
+        return sp.csc_matrix((x, i, p), shape=(self.M, self.N))
+
+    def hierarchy(self):
+        """Pipeline::hierarchy() (pipeline.h:59) as the flat description spaqr_factorize takes."""
+        nt = lib().spqr_pipeline_tree(self.h, None, None)
+        par = np.zeros(nt, np.int32)
+        root = C.c_int()
+        lib().spqr_pipeline_tree(self.h, par.ctypes.data_as(C.c_void_p), C.byref(root))
+        fin = np.zeros(self.N, np.int32)
+        lib().spqr_pipeline_finest(self.h, fin)
+        return dict(num_levels=self.L, clusters=self.clusters(), finest_of_col=fin, tree_parent=par,
+                    tree_root=root.value)
 
     def wfactors(self):
         out = []
@@ -241,3 +269,130 @@ def trsm_right_batched(B, R):
     if rc:
         raise RuntimeError(f"spqr_trsm_right_batched failed ({rc})")
     return bb.reshape(nb, n, nrows).transpose(0, 2, 1).copy()
+
+
+class Factorization:
+    """spaqr::Factorization (transforms.h:53-72) with W resident on the GPU: made by
+    spaqr_factorize or Factorization.load; w_apply / w_solve / wt_apply / wt_solve
+    (transforms.h:66-69), save (transforms.h:75)."""
+
+    def __init__(self, handle):
+        self.h = handle
+        info = np.zeros(8, np.int64)
+        lib().spqr_factorization_info(self.h, info)
+        (self.M, self.N, self.nW, self.nnz_w, self.ndropped, self.ntrailing, self.nstages,
+         self.levels) = [int(v) for v in info]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().spqr_factorization_destroy(self.h)
+            self.h = None
+
+    @classmethod
+    def load(cls, path, device=0):
+        """load_factorization (transforms.cpp:242-289) straight onto the GPU."""
+        require_gpu()
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = lib().spqr_factorization_load(str(path).encode(), int(device), C.byref(h), err, 512)
+        if rc:
+            raise (ValueError if rc == 2 else RuntimeError)(err.value.decode())
+        return cls(h)
+
+    def save(self, path):
+        err = C.create_string_buffer(512)
+        if lib().spqr_factorization_save(self.h, str(path).encode(), err, 512):
+            raise RuntimeError(err.value.decode())
+
+    def rows(self):
+        pr = np.zeros(max(self.N, 1), np.int32)
+        dr = np.zeros(max(self.ndropped, 1), np.int32)
+        tr = np.zeros(max(self.ntrailing, 1), np.int32)
+        lib().spqr_factorization_rows(self.h, pr, dr, tr)
+        return pr[: self.N], dr[: self.ndropped], tr[: self.ntrailing]
+
+    def stages(self):
+        out = []
+        o = np.zeros(5, np.int64)
+        for s in range(self.nstages):
+            lib().spqr_factorization_stage(self.h, s, o)
+            fc = np.zeros(max(int(o[1]), 1), np.int32)
+            lib().spqr_factorization_stage_fronts(self.h, s, fc)
+            out.append(dict(stage=int(o[0]), front_cols=fc[: int(o[1])].copy(), top_rows=int(o[2]),
+                            top_cols=int(o[3]), nnz_w=int(o[4])))
+        return out
+
+    def _apply(self, mode, z):
+        z = np.array(z, dtype=np.float64, copy=True)
+        if z.ndim != 1 or z.shape[0] != self.N:
+            raise ValueError("vector length does not match the factorization")
+        if lib().spqr_factorization_apply(self.h, mode, z):
+            raise RuntimeError("spqr_factorization_apply failed")
+        return z
+
+    def w_apply(self, z): return self._apply(0, z)
+    def w_solve(self, z): return self._apply(1, z)
+    def wt_apply(self, z): return self._apply(2, z)
+    def wt_solve(self, z): return self._apply(3, z)
+
+
+def spaqr_factorize(A, hierarchy, row_owner, eps=1e-2, skip_levels=3, device=0):
+    """spaqr_factorize(A, h, row_owner, opt) (factorize.h:51-53) on the GPU.  A: the scaled,
+    permuted matrix; hierarchy: the dict Pipeline.hierarchy() returns (clusters with tree_node,
+    level, parent, stage, interior, cols; finest_of_col; tree_parent; tree_root; num_levels)."""
+    require_gpu()
+    m, n, p, i, x = _csc(A)
+    owner = np.ascontiguousarray(row_owner, np.int32)
+    if owner.shape[0] != m:  # factorize.cpp:800-801
+        raise ValueError("row_owner size mismatch")
+    cl = hierarchy["clusters"]
+    info = np.ascontiguousarray([[c["tree_node"], c["level"], c["parent"], c["stage"], int(c["interior"])]
+                                 for c in cl], np.int32).ravel()
+    cptr = np.zeros(len(cl) + 1, np.int32)
+    cptr[1:] = np.cumsum([len(c["cols"]) for c in cl])
+    ccols = np.ascontiguousarray(np.concatenate([np.asarray(c["cols"], np.int32) for c in cl])
+                                 if cl else np.zeros(0, np.int32), np.int32)
+    if ccols.size == 0:
+        ccols = np.zeros(1, np.int32)
+    fin = np.ascontiguousarray(hierarchy["finest_of_col"], np.int32)
+    tpar = np.ascontiguousarray(hierarchy["tree_parent"], np.int32)
+    h = C.c_void_p()
+    err = C.create_string_buffer(512)
+    ecl = C.c_int(-1)
+    rc = lib().spqr_factorize(m, n, p, i, x, int(hierarchy["num_levels"]), len(cl), info, cptr, ccols, fin,
+                              len(tpar), tpar, int(hierarchy["tree_root"]), owner, float(eps), int(skip_levels),
+                              int(device), C.byref(h), err, 512, C.byref(ecl))
+    if rc:
+        msg = err.value.decode()
+        if rc == 1:
+            raise SingularFrontError(ecl.value, msg)
+        if rc == 2:
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+    return Factorization(h)
+
+
+def cgls(A, W, b, tol=1e-12, maxit=500, weights=None, device=0):
+    """cgls(A, W, b, u, opt, weights) (solve.h:30-31) on the GPU: right-preconditioned CGLS on A
+    (in W's column coordinates) with W a Factorization or None.  Returns (u, report)."""
+    require_gpu()
+    m, n, p, i, x = _csc(A)
+    b = np.ascontiguousarray(b, np.float64)
+    if b.shape[0] != m:
+        raise ValueError("right-hand side length mismatch")
+    if W is not None and W.N != n:
+        raise ValueError("factorization column count does not match A")
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    if w is not None and w.shape[0] != n:
+        raise ValueError("weights length does not match column count")
+    u = np.zeros(n)
+    hist = np.zeros(int(maxit if maxit > 0 else 500) + 4)
+    it, cv, nh = C.c_int(), C.c_int(), C.c_int()
+    ts = C.c_double()
+    err = C.create_string_buffer(512)
+    rc = lib().spqr_cgls(m, n, p, i, x, None if W is None else W.h, b, u, float(tol), int(maxit), _ptr(w),
+                         int(device), C.byref(it), C.byref(cv), hist, C.byref(nh), C.byref(ts), err, 512)
+    if rc:
+        raise (ValueError if rc == 2 else RuntimeError)(err.value.decode())
+    return u, dict(iterations=it.value, converged=bool(cv.value), residual_history=hist[: nh.value].copy(),
+                   t_solve=ts.value)

@@ -16,6 +16,7 @@
 #include <omp.h>
 #endif
 
+#include "capi_common.h"
 #include "dev.h"
 #include "engine.h"
 #include "solve.h"
@@ -54,31 +55,9 @@ struct spqr_pipeline {
 
 namespace {
 
-void put_err(char* err, int errlen, const std::string& s) {
-    if (!err || errlen <= 0) return;
-    std::strncpy(err, s.c_str(), static_cast<size_t>(errlen - 1));
-    err[errlen - 1] = 0;
-}
-
 template <class F>
 int guarded(char* err, int errlen, int* err_cluster, F&& f) {
-    try {
-        f();
-        return SPQR_OK;
-    } catch (const SingularFrontError& e) {
-        if (err_cluster) *err_cluster = e.cluster;
-        put_err(err, errlen, std::string(e.what()) + " | reason: " + e.reason);
-        return SPQR_E_SINGULAR;
-    } catch (const std::invalid_argument& e) {
-        put_err(err, errlen, e.what());
-        return SPQR_E_SHAPE;
-    } catch (const CudaError& e) {
-        put_err(err, errlen, e.what());
-        return SPQR_E_CUDA;
-    } catch (const std::exception& e) {
-        put_err(err, errlen, e.what());
-        return SPQR_E_OTHER;
-    }
+    return capi_guarded(err, errlen, err_cluster, std::forward<F>(f));
 }
 
 }  // namespace
@@ -99,15 +78,7 @@ int spqr_pipeline_create(int m, int n, const int* colptr, const int* rowind, con
     *out = nullptr;
     auto* P = new spqr_pipeline;
     const int rc = guarded(err, errlen, err_cluster, [&] {
-#ifdef _OPENMP
-        // host bookkeeping threads: all cores but one (measured best on the 16-core
-        // B200 hosts: 15 threads 3.4 s vs 12 threads 3.7 s on C2) unless the user
-        // chose a count
-        if (!std::getenv("OMP_NUM_THREADS")) {
-            const int np = omp_get_num_procs();
-            omp_set_num_threads(std::max(1, np - 1));
-        }
-#endif
+        capi_set_threads();  // 15 host threads on the 16-core hosts: 3.4 s vs 3.7 s at 12 (C2)
         P->device = device;
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
@@ -305,6 +276,24 @@ int spqr_pipeline_apply(spqr_pipeline* p, int mode, double* z) {
     });
 }
 
+int spqr_pipeline_tree(const spqr_pipeline* p, int* parent, int* root) {
+    const int nt = static_cast<int>(p->tree.nodes.size());
+    if (parent)
+        for (int t = 0; t < nt; ++t) parent[t] = p->tree.nodes[t].parent;
+    if (root) *root = p->tree.root;
+    return nt;
+}
+
+void spqr_pipeline_finest(const spqr_pipeline* p, int* finest_of_col) {
+    std::copy(p->h.finest_of_col.begin(), p->h.finest_of_col.end(), finest_of_col);
+}
+
+void spqr_pipeline_scaled(const spqr_pipeline* p, int* colptr, int* rowind, double* vals) {
+    std::copy(p->Aw.p.begin(), p->Aw.p.end(), colptr);
+    std::copy(p->Aw.i.begin(), p->Aw.i.end(), rowind);
+    std::copy(p->Aw.x.begin(), p->Aw.x.end(), vals);
+}
+
 void spqr_pipeline_perm(const spqr_pipeline* p, int* o) { std::copy(p->perm.begin(), p->perm.end(), o); }
 void spqr_pipeline_owner(const spqr_pipeline* p, int* o) { std::copy(p->owner.begin(), p->owner.end(), o); }
 void spqr_pipeline_weights(const spqr_pipeline* p, double* o) { std::copy(p->weights.begin(), p->weights.end(), o); }
@@ -380,68 +369,7 @@ int spqr_pipeline_save(const spqr_pipeline* p, const char* path, char* err, int 
     int cl = -1;
     return guarded(err, errlen, &cl, [&] {
         if (!p->has_f) throw std::logic_error("spqr_pipeline_save: no factorization (solver=direct)");
-        const DeviceFactorization& F = p->F;
-        std::vector<std::pair<const char*, std::vector<char>>> mirror;
-        F.warena->for_each_chunk([&](const char* base, size_t used) {
-            mirror.emplace_back(base, std::vector<char>(used));
-            if (used) CK(cudaMemcpy(mirror.back().second.data(), base, used, cudaMemcpyDeviceToHost));
-        });
-        auto host = [&](const double* d) -> const double* {
-            const char* c = reinterpret_cast<const char*>(d);
-            for (const auto& m : mirror)
-                if (c >= m.first && c < m.first + m.second.size())
-                    return reinterpret_cast<const double*>(m.second.data() + (c - m.first));
-            throw std::logic_error("spqr_pipeline_save: factor data outside the W arena");
-        };
-        std::FILE* f = std::fopen(path, "wb");
-        if (!f) throw std::runtime_error(std::string("cannot open ") + path + " for writing");
-        std::unique_ptr<std::FILE, int (*)(std::FILE*)> guard(f, &std::fclose);
-        auto i64 = [&](long long v) {
-            const int64_t x = v;
-            std::fwrite(&x, 8, 1, f);
-        };
-        auto f64s = [&](const double* v, size_t n) {
-            if (n) std::fwrite(v, 8, n, f);
-        };
-        auto ivec = [&](const int* v, size_t n) {
-            i64(static_cast<long long>(n));
-            for (size_t i = 0; i < n; ++i) i64(v[i]);
-        };
-        std::fwrite("SPQRFW01", 1, 8, f);
-        i64(F.M);
-        i64(F.N);
-        f64s(&F.eps, 1);
-        ivec(F.pivot_row.data(), F.pivot_row.size());
-        ivec(F.dropped_rows.data(), F.dropped_rows.size());
-        ivec(F.trailing_rows.data(), F.trailing_rows.size());
-        i64(static_cast<long long>(F.W.size()));
-        for (const DevWFactor& w : F.W) {
-            const int* cols = F.idx.data() + w.cols_off;
-            if (w.kind == 0) {  // a = [R | C], c x (c + k), column-major
-                const double* a = w.c ? host(w.a) : nullptr;
-                i64(0);
-                ivec(cols, w.c);
-                i64(w.c);
-                i64(w.c);
-                f64s(a, static_cast<size_t>(w.c) * w.c);
-                ivec(F.idx.data() + w.coupled_off, w.k);
-                i64(w.scale_only ? 0 : w.c);  // scale_all's factor keeps the default-constructed C (0 x 0)
-                i64(w.k);
-                f64s(a ? a + static_cast<size_t>(w.c) * w.c : nullptr, static_cast<size_t>(w.c) * w.k);
-            } else {  // V c x k (unit diagonal explicit), tau k, sign k
-                i64(1);
-                ivec(cols, w.c);
-                i64(w.c);
-                i64(w.k);
-                f64s((w.c > 0 && w.k > 0) ? host(w.a) : nullptr, static_cast<size_t>(w.c) * w.k);
-                i64(w.k);
-                f64s(w.k ? host(w.tau) : nullptr, w.k);
-                i64(w.k);
-                f64s(w.k ? host(w.sign) : nullptr, w.k);
-            }
-        }
-        i64(0);  // has_q: the GPU engine does not store Q (store_q is a test-only option)
-        if (std::ferror(f)) throw std::runtime_error(std::string("write failed: ") + path);
+        save_device_factorization(p->F, path);
     });
 }
 

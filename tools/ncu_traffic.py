@@ -17,6 +17,7 @@ FAMILY = [("k_wsweep", "w_sweep"), ("k_wreduce", "w_sweep"), ("k_cpqr", "cpqr"),
           ("k_spmv", "cgls_vec"), ("k_dot", "cgls_vec"), ("k_finish", "cgls_vec"), ("k_axpy", "cgls_vec"),
           ("k_copy", "cgls_vec"), ("k_p_update", "cgls_vec"), ("k_cgls", "cgls_vec")]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+         "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9,
          "second": 1.0}
 
 
