@@ -146,7 +146,9 @@ int spqr_cgls(int m, int n, const int* colptr, const int* rowind, const double* 
  * upper triangle, reflectors (unit diagonal implicit) below, H^T X to the right.
  * info[b] = -1 ok, else the first zero/denormal pivot. */
 int spqr_qr_apply_batched(int nb, int m, int n, int ntot, double* a, double* tau, double* sign, int* info);
-/* Same on device pointers (timed by the caller's stream: 0 = default). Returns device ms. */
+/* Same on device pointers, in place; runs on the legacy default stream (0) and synchronises
+ * before returning.  *ms = device time of the launches (CUDA events around them);
+ * d_info[b] = -1 ok, else the first zero/denormal pivot (as the host entry point). */
 int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, double* d_tau, double* d_sign,
                               int* d_info, float* ms);
 /* truncated_cpqr (dense_kernels.cpp:124-232) for nb m x n problems.  Outputs per

@@ -439,6 +439,8 @@ int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, doubl
         if (ms) *ms = t;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+        launch_info_fixup(d_info, nb, 0);
+        CK(cudaStreamSynchronize(0));
         if (dq) cudaFree(dq);
         if (dwork) cudaFree(dwork);
         if (didx) cudaFree(didx);

@@ -377,7 +377,7 @@ size_t cpqr_big_smem_bytes(int m, int n) {
 void launch_cpqr_big(const CpqrDesc& d, cudaStream_t st) {
     const int G = cpqr_big_grid();
     const size_t smem = cpqr_big_smem_bytes(d.m, d.n);
-    static size_t configured = 0;
+    static SmemCfg configured;
     smem_optin(reinterpret_cast<const void*>(k_cpqr_big), smem, configured);
     BigScratch S;
     S.vn1 = d.work;

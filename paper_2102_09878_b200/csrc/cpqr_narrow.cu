@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_cpqr_tall(const CpqrDesc* __res
 
 template <int RPL, bool GLB, int NC>
 void launch_narrow(const CpqrDesc* d, const int* idx, int cnt, size_t smem, cudaStream_t st) {
-    static size_t configured = 0;
+    static SmemCfg configured;
     if (!GLB) smem_optin(reinterpret_cast<const void*>(k_cpqr_narrow<RPL, GLB, NC>), smem, configured);
     k_cpqr_narrow<RPL, GLB, NC><<<cnt, kThreads, GLB ? 0 : smem, st>>>(d, idx);
 }

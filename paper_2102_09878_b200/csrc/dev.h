@@ -12,6 +12,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <mutex>
 #include <vector>
 
 namespace spqr {
@@ -29,15 +31,26 @@ __host__ __device__ __forceinline__ bool hh_beta_negative(double c0, double tail
     return c0 >= 0.0 || c0 * c0 <= kHhSignTol2 * tail2;
 }
 
-// Opt in to `bytes` of dynamic shared memory for `func`.  The 48 KB default
-// limit covers static + dynamic shared memory together, so the attribute is
-// raised whenever a launch needs more than any earlier one (`configured` is a
-// per-call-site static).
-inline void smem_optin(const void* func, size_t bytes, size_t& configured) {
-    if (bytes > configured) {
-        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
-        configured = bytes;
-    }
+// Opt in to `bytes` of dynamic shared memory for `func` on the current device.  The 48 KB
+// default limit covers static + dynamic shared memory together, so the attribute is raised
+// whenever a launch needs more than any earlier one.  `configured` is a per-call-site static
+// holding the opted-in size per device (the attribute is per device); the slow path is
+// serialised so a concurrent caller never launches before the attribute covers it.
+constexpr int kMaxDevices = 64;
+struct SmemCfg {
+    std::atomic<size_t> v[kMaxDevices] = {};
+};
+inline void smem_optin(const void* func, size_t bytes, SmemCfg& configured) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    if (configured.v[dev].load(std::memory_order_acquire) >= bytes) return;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (configured.v[dev].load(std::memory_order_relaxed) >= bytes) return;
+    if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)) ==
+        cudaSuccess)
+        configured.v[dev].store(bytes, std::memory_order_release);
 }
 
 // ---- generic gather ("assemble"): builds a destination matrix from rows of
@@ -170,6 +183,8 @@ void launch_wsweep(const WFac* f, int nf, double* z, double* contrib, int mode, 
 // factors with c >= kBigFactorCols: one CTA each (k_wsweep_big)
 constexpr int kBigFactorCols = 192;
 void launch_wsweep_big(const WFac* f, int nf, double* z, double* contrib, int mode, int maxc, cudaStream_t st);
+// d_info[i] == INT_MAX (no singular pivot) -> -1, on st
+void launch_info_fixup(int* info, int n, cudaStream_t st);
 // opt in to the largest dynamic shared memory any level needs, before graph capture
 void prepare_wsweep(int maxc, int bmaxc);
 // z[col[t]] (+/-)= contrib[idx[ptr[t]..ptr[t+1])] in order

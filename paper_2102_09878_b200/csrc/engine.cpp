@@ -25,7 +25,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <iterator>
+#include <condition_variable>
 #include <deque>
+#include <functional>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -444,6 +446,72 @@ inline void phys_order(const std::vector<KeyRef>& keys, std::vector<int>& ord) {
     std::sort(ord.begin(), ord.end(), [&](int a, int b) { return keys[a].col < keys[b].col; });
 }
 
+// One persistent background thread frees the engines' host containers (hundreds of thousands
+// of small vectors) off the caller's critical path; it drains its queue and is joined when the
+// library is unloaded / the process exits.
+class Reaper {
+public:
+    static Reaper& get() {
+        static Reaper r;
+        return r;
+    }
+    void post(std::function<void()> f) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            q_.push_back(std::move(f));
+        }
+        cv_.notify_one();
+    }
+    ~Reaper() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_one();
+        if (th_.joinable()) th_.join();
+    }
+
+private:
+    Reaper() : th_([this] { run(); }) {}
+    void run() {
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+            if (q_.empty() && stop_) return;
+            auto f = std::move(q_.front());
+            q_.pop_front();
+            lk.unlock();
+            f();
+            lk.lock();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    bool stop_ = false;
+    std::thread th_;
+};
+
+// The library's own stream-ordered pool per device for big fronts and stacks: it keeps freed
+// memory cached across waves and factorizations (release threshold = max) without touching
+// the device's default pool, which other allocators in the process (torch, the caller) use.
+cudaMemPool_t engine_pool(int dev) {
+    static std::mutex mu;
+    static std::vector<cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lk(mu);
+    if (static_cast<int>(pools.size()) <= dev) pools.resize(dev + 1, nullptr);
+    if (!pools[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        CK(cudaMemPoolCreate(&pools[dev], &props));
+        uint64_t thr = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+    return pools[dev];
+}
+
 class Engine {
 public:
     Engine(const Csc& A, const ClusterHierarchy& h, const std::vector<int>& owner, const FactorizeOptions& opt,
@@ -476,10 +544,7 @@ public:
             int dev = 0;
             CK(cudaGetDevice(&dev));
             dev_ = dev;
-            cudaMemPool_t pool;
-            CK(cudaDeviceGetDefaultMemPool(&pool, dev));
-            uint64_t thr = UINT64_MAX;
-            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+            pool_ = engine_pool(dev);
         }
         CK(cudaEventCreate(&ev0_));
         CK(cudaEventCreate(&ev1_));
@@ -525,7 +590,7 @@ public:
             auto* t = new Trash{std::move(fr_),      std::move(cols_),    std::move(stage_list_), std::move(tree_clusters_),
                                 std::move(sb_bases_), std::move(holders_), std::move(pend_),      std::move(el_),
                                 std::move(mplans_)};
-            std::thread([t] { delete t; }).detach();
+            Reaper::get().post([t] { delete t; });
         }
         cudaStreamSynchronize(st_);  // nothing may still use the arenas when they go back to the pool
         cudaEventDestroy(ev0_);
@@ -561,6 +626,7 @@ private:
     DeviceFactorization out_;
     std::unique_ptr<DeviceArena> arena_[2];
     int cur_ = 0, dev_ = 0;
+    cudaMemPool_t pool_ = nullptr;
     std::unique_ptr<PinnedArena> pin_;
     Index npiv_ = 0;
     int batch_ = 0;
@@ -608,7 +674,7 @@ private:
         big = bytes >= kBig;
         if (!big) return ar.alloc_n<double>(std::max<size_t>(n, 1));
         void* p = nullptr;
-        CK(cudaMallocAsync(&p, bytes, st_));
+        CK(cudaMallocFromPoolAsync(&p, bytes, pool_, st_));
         return static_cast<double*>(p);
     }
     void dfree(double* p, bool big) {

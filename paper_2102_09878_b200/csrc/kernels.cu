@@ -7,6 +7,7 @@
 // place in HBM (L1/L2 resident at these sizes).  Reference semantics per
 // kernel are cited next to each one (proj/src/dense_kernels.cpp).
 #include <cfloat>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 
@@ -650,7 +651,7 @@ void launch_stats(const StatDesc* d, int nd, long long total, double* out_sq, un
 void launch_qr_split(const QrDesc* d_desc, const int* d_small, int n_small, size_t smem_small, const int* d_large,
                      int n_large, cudaStream_t st) {
     if (n_small > 0) {
-        static size_t cfg = 0;
+        static SmemCfg cfg;
         smem_optin(reinterpret_cast<const void*>(k_qr_smem), smem_small, cfg);
         k_qr_smem<<<n_small, 256, smem_small, st>>>(d_desc, d_small);
     }
@@ -666,16 +667,28 @@ void launch_trsm(const TrsmDesc* d, int nd, long long total, cudaStream_t st) {
 void launch_cpqr_split(const CpqrDesc* d_desc, const int* d_small, int n_small, size_t smem_small, const int* d_large,
                        int n_large, int max_m_large, cudaStream_t st) {
     if (n_small > 0) {
-        static size_t cfg = 0;
+        static SmemCfg cfg;
         smem_optin(reinterpret_cast<const void*>(k_cpqr_smem), smem_small, cfg);
         k_cpqr_smem<<<n_small, kCpqrThreads, smem_small, st>>>(d_desc, d_small);
     }
     if (n_large > 0) {
         const size_t smem = sizeof(double) * static_cast<size_t>(max_m_large > 0 ? max_m_large : 1);
-        static size_t cfg = 0;
+        static SmemCfg cfg;
         smem_optin(reinterpret_cast<const void*>(k_cpqr), smem, cfg);
         k_cpqr<<<n_large, kCpqrThreads, smem, st>>>(d_desc, d_large);
     }
+}
+
+namespace {
+__global__ void k_info_fixup(int* info, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && info[i] == INT_MAX) info[i] = -1;
+}
+}  // namespace
+
+// QR flags are atomicMin'd from INT_MAX: map "no singular pivot" to the C ABI's -1
+void launch_info_fixup(int* info, int n, cudaStream_t st) {
+    if (n > 0) k_info_fixup<<<(n + 255) / 256, 256, 0, st>>>(info, n);
 }
 
 }  // namespace spqr

@@ -16,11 +16,14 @@
 #include <cstdlib>
 #include <cstdint>
 #include <algorithm>
+#include <mutex>
 #include <stdexcept>
+#include <string>
 
 #include <cooperative_groups.h>
 
 #include "dev.h"
+#include "devmem.h"
 
 namespace spqr {
 
@@ -1261,22 +1264,43 @@ constexpr size_t kTmergeSmem = sizeof(double) * (KO * (KO + 1) + 2 * 32 * 32 + 2
 size_t vtc_smem(int kb) { return sizeof(double) * (2 * kb * LDS_ + 2 * TCG * LDS_); }
 size_t cvw_smem(int kb) { return sizeof(double) * (TCG * (kb + 4) + 2 * CHG * (kb + 4) + 2 * TCG * LDS_); }
 
-// workspace for the partial W tiles and the outer T (grow-only, per process)
+// workspace for the partial W tiles and the outer T (grow-only)
 struct BigWs {
     double* p = nullptr;
     size_t cap = 0;
     double* get(size_t n) {
         if (n > cap) {
-            if (p) cudaFree(p);
-            cudaMalloc(&p, sizeof(double) * n);
+            if (p) cudaFree(p);  // synchronises: no kernel still uses the old buffer
+            p = nullptr;
+            cap = 0;
+            const cudaError_t e = cudaMalloc(&p, sizeof(double) * n);
+            if (e != cudaSuccess) {
+                p = nullptr;
+                throw CudaError(std::string("blocked QR workspace: ") + cudaGetErrorString(e));
+            }
             cap = n;
         }
         return p;
     }
 };
-// Per-process workspaces of the blocked path (one GPU per process, one host thread per context,
-// as the C ABI requires): [0] trailing updates (main stream), [1] panel phase (side stream)
-BigWs g_ws_w[2], g_ws_t[2];
+// Per-device state of the blocked path: workspaces ([0] trailing updates on the caller's
+// stream, [1] panel phase on the look-ahead side stream), the side stream and its events.
+// Calls on one device are serialised on the host (mutex) and on the GPU (each call's stream
+// waits for the previous call's completion event), so concurrent handles never share a
+// workspace in flight; every device gets its own buffers and stream.
+struct MbqrDev {
+    std::mutex mu;
+    BigWs ws_w[2], ws_t[2];
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, done = nullptr;
+    bool used = false;
+};
+MbqrDev& mbqr_dev() {
+    static MbqrDev s[kMaxDevices];
+    int d = 0;
+    cudaGetDevice(&d);
+    return s[(d >= 0 && d < kMaxDevices) ? d : 0];
+}
 
 // block reflector (KB columns at J0, kw valid, T in T_all with ld KB) applied
 // to columns [cbeg, cend) of every problem; gram != 0 computes V^T V instead
@@ -1306,7 +1330,7 @@ void apply_block(BigWs& ws, int nbatch, int m, int ld, long long stride, double*
     nsl = (rows + rs - 1) / rs;
     double* wp = ws.get(static_cast<size_t>(nbatch) * nsl * ntile * KB * TCG);
     {
-        static size_t cfg = 0;
+        static SmemCfg cfg;
         smem_optin(reinterpret_cast<const void*>(k_vtc<KB>), vtc_smem(KB), cfg);
         k_vtc<KB><<<dim3(ntile, nsl, nbatch), 256, vtc_smem(KB), st>>>(d_a, ld, stride, m, J0, kw, cbeg, cend, rs, gram,
                                                                          wp, (nsl == 1 && !gram) ? T_all : nullptr);
@@ -1316,20 +1340,20 @@ void apply_block(BigWs& ws, int nbatch, int m, int ld, long long stride, double*
         return;
     }
     if (nsl > 1) {  // (one slice: fused into k_vtc)
-        static size_t cfg = 0;
+        static SmemCfg cfg;
         const size_t sm = sizeof(double) * KB * 0 + sizeof(double) * (KB + 4) * TCG;
         smem_optin(reinterpret_cast<const void*>(k_tw<KB>), sm, cfg);
         k_tw<KB><<<dim3(ntile, nbatch), 256, sm, st>>>(wp, nsl, T_all, kw);
     }
     if (!std::getenv("SPQR_CVW1")) {
-        static size_t cfg = 0;
+        static SmemCfg cfg;
         smem_optin(reinterpret_cast<const void*>(k_cvw2<KB>), kCvw2Smem, cfg);
         k_cvw2<KB><<<dim3(ntile, (rows + CM - 1) / CM, nbatch), 256, kCvw2Smem, st>>>(d_a, ld, stride, m, J0, kw, cbeg,
                                                                                    cend, wp, nsl);
     } else {
         const int rt = rows <= 512 ? ((rows + 1) / 2 + CHG - 1) / CHG * CHG : 256;
         const int nrt = (rows + rt - 1) / rt;
-        static size_t cfg = 0;
+        static SmemCfg cfg;
         smem_optin(reinterpret_cast<const void*>(k_cvw<KB>), cvw_smem(KB), cfg);
         k_cvw<KB><<<dim3(ntile, nrt, nbatch), 256, cvw_smem(KB), st>>>(d_a, ld, stride, m, J0, kw, cbeg, cend,
                                                                          std::max(rt, CHG), wp, nsl);
@@ -1348,6 +1372,12 @@ void blocked_qr_post(double* a, int ld, int m, int n, double* rout, int set_iden
 // columns + H^T applied to the rest; tau/sign n per problem; info per problem.
 void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d_tau, double* d_sign, int* d_info,
                       double* d_T, cudaStream_t st, int ld_in) {
+    MbqrDev& D = mbqr_dev();
+    std::lock_guard<std::mutex> lk(D.mu);
+    if (!D.done) CK(cudaEventCreateWithFlags(&D.done, cudaEventDisableTiming));
+    if (D.used) CK(cudaStreamWaitEvent(st, D.done, 0));  // previous call (any stream) has finished
+    BigWs* g_ws_w = D.ws_w;
+    BigWs* g_ws_t = D.ws_t;
     const int ldA = ld_in > 0 ? ld_in : m;
     const long long stride = static_cast<long long>(ldA) * ntot;
     const size_t smem_cap = 160 * 1024;
@@ -1363,15 +1393,15 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
         if (rows > smem_rows && static_cast<size_t>(Rc) * w * sizeof(double) <= 200 * 1024 &&
             !std::getenv("SPQR_NO_CLUSTER_PANEL")) {
             const size_t csmem = sizeof(double) * static_cast<size_t>(Rc) * w;
-            static size_t cfg = 0;
+            static SmemCfg cfg;
             smem_optin(reinterpret_cast<const void*>(k_panel_cluster), csmem, cfg);
             k_panel_cluster<<<nbatch * kCS, 256, csmem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, Rc);
         } else if (rows <= 512) {
-            static size_t cfg = 0;
+            static SmemCfg cfg;
             smem_optin(reinterpret_cast<const void*>(k_panel2<8>), smem, cfg);
             k_panel2<8><<<nbatch, 256, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
         } else {
-            static size_t cfg = 0;
+            static SmemCfg cfg;
             smem_optin(reinterpret_cast<const void*>(k_panel2<16>), smem, cfg);
             k_panel2<16><<<nbatch, 512, smem, st>>>(d_a, ldA, stride, m, j0, w, d_tau, n, d_T, smem_rows);
         }
@@ -1388,7 +1418,7 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
                 dim3 grid((trail + TC2 - 1) / TC2, nbatch);
                 const size_t vsz = std::max(NB * LDV, CH * LDVT);
                 const size_t wsm = sizeof(double) * (2 * vsz + 2 * TC2 * LDC + TC2 * LDW + NB * LDW);
-                static size_t cfg = 0;
+                static SmemCfg cfg;
                 smem_optin(reinterpret_cast<const void*>(k_wy<16>), wsm, cfg);
                 k_wy<16><<<grid, 512, wsm, st>>>(d_a, ldA, stride, m, ntot, j0, w, d_T);
             }
@@ -1403,15 +1433,15 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
         double* Tb[2] = {g_ws_t[0].get(tsz), g_ws_t[1].get(tsz)};
         const bool reg_panel = !std::getenv("SPQR_SMEM_PANEL");
         const bool lookahead = !std::getenv("SPQR_NO_LOOKAHEAD");
-        static cudaStream_t side = nullptr;
-        static cudaEvent_t ev_a = nullptr, ev_b = nullptr;
-        if (lookahead && !side) {
+        if (lookahead && !D.side) {
             int lo = 0, hi = 0;
-            cudaDeviceGetStreamPriorityRange(&lo, &hi);
-            cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi);
-            cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming);
-            cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming);
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CK(cudaStreamCreateWithPriority(&D.side, cudaStreamNonBlocking, hi));
+            CK(cudaEventCreateWithFlags(&D.ev_a, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&D.ev_b, cudaEventDisableTiming));
         }
+        cudaStream_t side = D.side;
+        cudaEvent_t ev_a = D.ev_a, ev_b = D.ev_b;
         // panels + inner updates of block J0, its Gram matrix and merged T into Tout
         auto panel_phase = [&](int J0, double* Tout, cudaStream_t s) {
             const int kw2 = std::min(KO, n - J0);
@@ -1427,7 +1457,7 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
             if (kw2 <= NB || J0 + kw2 >= ntot) return;
             int nsl = 1;
             apply_block<KO>(g_ws_w[1], nbatch, m, ldA, stride, d_a, J0, kw2, J0, J0 + KO, nullptr, s, &nsl, 1);
-            static size_t cfg = 0;
+            static SmemCfg cfg;
             smem_optin(reinterpret_cast<const void*>(k_tmerge), kTmergeSmem, cfg);
             k_tmerge<<<nbatch, 256, kTmergeSmem, s>>>(g_ws_w[1].p, nsl, T_in, slot, (kw2 + NB - 1) / NB, Tout);
         };
@@ -1469,6 +1499,8 @@ void blocked_qr_apply(int nbatch, int m, int n, int ntot, double* d_a, double* d
     dim3 g2((ntot + kFlipCols - 1) / kFlipCols, nbatch);
     k_flip<<<g2, 256, 0, st>>>(d_a, ldA, stride, n, ntot, d_sign, d_info);
     k_flip_diag<<<nbatch, 256, 0, st>>>(d_a, ldA, stride, n);
+    CK(cudaEventRecord(D.done, st));
+    D.used = true;
 }
 
 }  // namespace spqr

@@ -511,11 +511,11 @@ bool tile_dmma_enabled() { return std::getenv("SPQR_TILE_DMMA") != nullptr; }
 template <int TPC>
 void launch_tile(const QrDesc* dd, const int4* dw, int nwork, size_t smem, int* count, cudaStream_t st) {
     if (tile_dmma_enabled()) {
-        static size_t configured = 0;
+        static SmemCfg configured;
         smem_optin(reinterpret_cast<const void*>(k_qr_tile<TPC, true>), smem, configured);
         k_qr_tile<TPC, true><<<nwork, 32 * nw_of<TPC>(), smem, st>>>(dd, dw, count);
     } else {
-        static size_t configured = 0;
+        static SmemCfg configured;
         smem_optin(reinterpret_cast<const void*>(k_qr_tile<TPC, false>), smem, configured);
         k_qr_tile<TPC, false><<<nwork, 32 * nw_of<TPC>(), smem, st>>>(dd, dw, count);
     }

@@ -353,7 +353,7 @@ __global__ void k_copy(int n, const double* __restrict__ a, double* __restrict__
 }  // namespace
 
 namespace {
-size_t g_wsweep_cfg = 0, g_wsweep_big_cfg = 0;  // dynamic smem opted in so far (see prepare_wsweep)
+SmemCfg g_wsweep_cfg, g_wsweep_big_cfg;  // dynamic smem opted in so far (see prepare_wsweep)
 }
 
 void prepare_wsweep(int maxc, int bmaxc) {
