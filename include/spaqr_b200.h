@@ -32,6 +32,33 @@ enum { SPQR_W_APPLY = 0, SPQR_W_SOLVE = 1, SPQR_WT_APPLY = 2, SPQR_WT_SOLVE = 3 
 
 typedef struct spqr_pipeline spqr_pipeline;
 
+/* FactorizeObserver / EngineView (factorize.h:31-43): the engine state after each phase,
+ * materialised on the host (tests, diagnostics).  Front f (cluster front_cluster[f]) has rows
+ * rows[rows_ptr[f] .. rows_ptr[f+1]) and key blocks keys[keys_ptr[f] .. keys_ptr[f+1])
+ * (ascending), block b being key_width[b] columns of nrows values (column-major) at
+ * values + block_off[b].  cols: the active columns of every cluster.  The GPU engine
+ * eliminates a stage in dependency waves: one "eliminate" notification per wave, whose
+ * clusters are wave[0..nwave) (detail = wave[0]); other phases: "scale", "sparsify_rows",
+ * "sparsify_cols", "merge" (detail -1). */
+typedef struct {
+    int nfronts;
+    const int* front_cluster;
+    const int* rows_ptr;
+    const int* rows;
+    const int* keys_ptr;
+    const int* keys;
+    const int* key_width;
+    const long long* block_off;
+    const double* values;
+    int nclusters;
+    const int* cols_ptr;
+    const int* cols;
+    int nwave;
+    const int* wave;
+    long long pivots, dropped, trailing;
+} spqr_engine_view;
+typedef void (*spqr_observer_fn)(void* user, const char* phase, int stage, int detail, const spqr_engine_view* view);
+
 /* Library / device probes. */
 const char* spqr_version(void);
 int spqr_device_count(void);
@@ -44,6 +71,11 @@ int spqr_pipeline_create(int m, int n, const int* colptr, const int* rowind, con
                          const double* coords, int dim, const int* parts, int levels, double eps,
                          int skip_levels, int solver, int device, spqr_pipeline** out, char* err, int errlen,
                          int* err_cluster);
+/* Same with an observer called after every engine phase (Pipeline's obs, pipeline.h:39-41). */
+int spqr_pipeline_create_observed(int m, int n, const int* colptr, const int* rowind, const double* vals,
+                                  const double* coords, int dim, const int* parts, int levels, double eps,
+                                  int skip_levels, int solver, int device, spqr_observer_fn obs, void* obs_user,
+                                  spqr_pipeline** out, char* err, int errlen, int* err_cluster);
 void spqr_pipeline_destroy(spqr_pipeline* p);
 
 /* info[16]: M, N, L, nclusters, nW, n_dropped, n_trailing, n_stages, nnz_w, nnz(A), W sweep levels,
@@ -110,13 +142,14 @@ typedef struct spqr_factorization spqr_factorization;
  * cluster_info[5*c] = tree_node, level, parent, stage, interior; cluster c's (permuted) columns
  * cluster_cols[cluster_colptr[c] .. cluster_colptr[c+1]); finest_of_col[n]; the SeparatorTree
  * nodes' parents tree_parent[ntree] and its root.  row_owner[m]: a stage-(L+1) cluster per row.
+ * obs (may be NULL): the FactorizeObserver (factorize.h:40-43), see spqr_engine_view.
  * Errors: m < n or inconsistent hierarchy / owner arrays -> SPQR_E_SHAPE (std::invalid_argument);
  * SingularFrontError -> SPQR_E_SINGULAR with *err_cluster. */
 int spqr_factorize(int m, int n, const int* colptr, const int* rowind, const double* vals, int num_levels,
                    int nclusters, const int* cluster_info, const int* cluster_colptr, const int* cluster_cols,
                    const int* finest_of_col, int ntree, const int* tree_parent, int tree_root, const int* row_owner,
-                   double eps, int skip_levels, int device, spqr_factorization** out, char* err, int errlen,
-                   int* err_cluster);
+                   double eps, int skip_levels, int device, spqr_observer_fn obs, void* obs_user,
+                   spqr_factorization** out, char* err, int errlen, int* err_cluster);
 void spqr_factorization_destroy(spqr_factorization* f);
 /* info[8]: M, N, nW, nnz_w, n_dropped, n_trailing, n_stages, w_solve sweep levels */
 void spqr_factorization_info(const spqr_factorization* f, long long* info);

@@ -141,7 +141,8 @@ inline FactorizationB200 spaqr_factorize_b200(const SparseMatrix& A, const Clust
     const int rc = spqr_factorize(A.rows(), A.cols(), A.outer(), A.inner(), A.values(), h.num_levels,
                                   int(h.clusters.size()), info.data(), cptr.data(), ccols.data(),
                                   h.finest_of_col.data(), int(tpar.size()), tpar.data(), h.tree->root,
-                                  row_owner.data(), opt.eps, opt.skip_levels, device, &f, err, sizeof err, &cluster);
+                                  row_owner.data(), opt.eps, opt.skip_levels, device, /*obs=*/nullptr, nullptr, &f,
+                                  err, sizeof err, &cluster);
     b200_check(rc, err, cluster);
     return FactorizationB200(f);
 }

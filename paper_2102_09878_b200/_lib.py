@@ -50,8 +50,11 @@ SIGNATURES = {
     "spqr_pipeline_finest": (None, [vp, i32p]),
     "spqr_pipeline_scaled": (None, [vp, i32p, i32p, f64p]),
     "spqr_factorize": (C.c_int, [C.c_int, C.c_int, i32p, i32p, f64p, C.c_int, C.c_int, i32p, i32p, i32p, i32p,
-                                 C.c_int, i32p, C.c_int, i32p, C.c_double, C.c_int, C.c_int, C.POINTER(vp),
-                                 C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
+                                 C.c_int, i32p, C.c_int, i32p, C.c_double, C.c_int, C.c_int, vp, vp,
+                                 C.POINTER(vp), C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
+    "spqr_pipeline_create_observed": (C.c_int, [C.c_int, C.c_int, i32p, i32p, f64p, vp, C.c_int, vp, C.c_int,
+                                                C.c_double, C.c_int, C.c_int, C.c_int, vp, vp, C.POINTER(vp),
+                                                C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
     "spqr_factorization_destroy": (None, [vp]),
     "spqr_factorization_info": (None, [vp, i64p]),
     "spqr_factorization_rows": (None, [vp, i32p, i32p, i32p]),

@@ -33,10 +33,64 @@ def _ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
-class Pipeline:
-    """spqr_pipeline_create / _solve / _apply (include/spaqr_b200.h)."""
+class _EngineView(C.Structure):  # spqr_engine_view (include/spaqr_b200.h)
+    _fields_ = [("nfronts", C.c_int), ("front_cluster", C.POINTER(C.c_int)), ("rows_ptr", C.POINTER(C.c_int)),
+                ("rows", C.POINTER(C.c_int)), ("keys_ptr", C.POINTER(C.c_int)), ("keys", C.POINTER(C.c_int)),
+                ("key_width", C.POINTER(C.c_int)), ("block_off", C.POINTER(C.c_longlong)),
+                ("values", C.POINTER(C.c_double)), ("nclusters", C.c_int), ("cols_ptr", C.POINTER(C.c_int)),
+                ("cols", C.POINTER(C.c_int)), ("nwave", C.c_int), ("wave", C.POINTER(C.c_int)),
+                ("pivots", C.c_longlong), ("dropped", C.c_longlong), ("trailing", C.c_longlong)]
 
-    def __init__(self, A, eps=1e-2, levels=0, skip_levels=3, solver="spaqr", coords=None, parts=None, device=0):
+
+_OBSERVER_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.POINTER(_EngineView))
+
+
+def _arr(p, n, dt):
+    return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True) if n > 0 else np.zeros(0, dt)
+
+
+def _observer(fn):
+    """Wrap fn(phase, stage, detail, view) — FactorizeObserver::on_phase (factorize.h:40-43) —
+    as the C callback; view = dict(fronts={cluster: dict(rows, blocks={key: ndarray})},
+    cols=[active columns per cluster], wave, pivots, dropped, trailing) copied to numpy."""
+    if fn is None:
+        return None
+
+    def cb(user, phase, stage, detail, vp_):
+        v = vp_.contents
+        nf = v.nfronts
+        rp = _arr(v.rows_ptr, nf + 1, np.int64)
+        kp = _arr(v.keys_ptr, nf + 1, np.int64)
+        fc = _arr(v.front_cluster, nf, np.int64)
+        nkeys = int(kp[-1]) if nf else 0
+        rows = _arr(v.rows, int(rp[-1]) if nf else 0, np.int64)
+        keys = _arr(v.keys, nkeys, np.int64)
+        kw = _arr(v.key_width, nkeys, np.int64)
+        bo = _arr(v.block_off, nkeys, np.int64)
+        nval = int(bo[-1] + kw[-1] * (rp[-1] - rp[-2])) if nkeys else 0
+        vals = _arr(v.values, nval, np.float64)
+        fronts = {}
+        for f in range(nf):
+            nr = int(rp[f + 1] - rp[f])
+            blocks = {}
+            for b in range(int(kp[f]), int(kp[f + 1])):
+                w = int(kw[b])
+                blocks[int(keys[b])] = vals[bo[b]: bo[b] + nr * w].reshape(w, nr).T.copy()
+            fronts[int(fc[f])] = dict(rows=rows[rp[f]: rp[f + 1]].copy(), blocks=blocks)
+        cp = _arr(v.cols_ptr, v.nclusters + 1, np.int64)
+        cols_all = _arr(v.cols, int(cp[-1]), np.int64)
+        cols = [cols_all[cp[c]: cp[c + 1]] for c in range(v.nclusters)]
+        fn(phase.decode(), stage, detail, dict(fronts=fronts, cols=cols, wave=_arr(v.wave, v.nwave, np.int64).tolist(),
+                                               pivots=v.pivots, dropped=v.dropped, trailing=v.trailing))
+    return _OBSERVER_FN(cb)
+
+
+class Pipeline:
+    """spqr_pipeline_create / _solve / _apply (include/spaqr_b200.h).  observer: an optional
+    fn(phase, stage, detail, view) called after every engine phase (pipeline.h:39-41)."""
+
+    def __init__(self, A, eps=1e-2, levels=0, skip_levels=3, solver="spaqr", coords=None, parts=None, device=0,
+                 observer=None):
         require_gpu()
         L = lib()
         m, n, p, i, x = _csc(A)
@@ -50,8 +104,11 @@ class Pipeline:
         err = C.create_string_buffer(512)
         cl = C.c_int(-1)
         h = C.c_void_p()
-        rc = L.spqr_pipeline_create(m, n, p, i, x, _ptr(cp), dim, _ptr(pp), int(levels), float(eps), int(skip_levels),
-                                    SOLVERS[solver], int(device), C.byref(h), err, 512, C.byref(cl))
+        cb = _observer(observer)
+        rc = L.spqr_pipeline_create_observed(m, n, p, i, x, _ptr(cp), dim, _ptr(pp), int(levels), float(eps),
+                                             int(skip_levels), SOLVERS[solver], int(device),
+                                             C.cast(cb, C.c_void_p) if cb else None, None, C.byref(h), err, 512,
+                                             C.byref(cl))
         if rc != 0:
             msg = err.value.decode()
             if rc == 1:
@@ -336,7 +393,7 @@ class Factorization:
     def wt_solve(self, z): return self._apply(3, z)
 
 
-def spaqr_factorize(A, hierarchy, row_owner, eps=1e-2, skip_levels=3, device=0):
+def spaqr_factorize(A, hierarchy, row_owner, eps=1e-2, skip_levels=3, device=0, observer=None):
     """spaqr_factorize(A, h, row_owner, opt) (factorize.h:51-53) on the GPU.  A: the scaled,
     permuted matrix; hierarchy: the dict Pipeline.hierarchy() returns (clusters with tree_node,
     level, parent, stage, interior, cols; finest_of_col; tree_parent; tree_root; num_levels)."""
@@ -359,9 +416,11 @@ def spaqr_factorize(A, hierarchy, row_owner, eps=1e-2, skip_levels=3, device=0):
     h = C.c_void_p()
     err = C.create_string_buffer(512)
     ecl = C.c_int(-1)
+    cb = _observer(observer)
     rc = lib().spqr_factorize(m, n, p, i, x, int(hierarchy["num_levels"]), len(cl), info, cptr, ccols, fin,
                               len(tpar), tpar, int(hierarchy["tree_root"]), owner, float(eps), int(skip_levels),
-                              int(device), C.byref(h), err, 512, C.byref(ecl))
+                              int(device), C.cast(cb, C.c_void_p) if cb else None, None, C.byref(h), err, 512,
+                              C.byref(ecl))
     if rc:
         msg = err.value.decode()
         if rc == 1:

@@ -75,6 +75,14 @@ int spqr_device_count(void) {
 int spqr_pipeline_create(int m, int n, const int* colptr, const int* rowind, const double* vals, const double* coords,
                          int dim, const int* parts, int levels, double eps, int skip_levels, int solver, int device,
                          spqr_pipeline** out, char* err, int errlen, int* err_cluster) {
+    return spqr_pipeline_create_observed(m, n, colptr, rowind, vals, coords, dim, parts, levels, eps, skip_levels, solver,
+                                         device, nullptr, nullptr, out, err, errlen, err_cluster);
+}
+
+int spqr_pipeline_create_observed(int m, int n, const int* colptr, const int* rowind, const double* vals,
+                                  const double* coords, int dim, const int* parts, int levels, double eps,
+                                  int skip_levels, int solver, int device, spqr_observer_fn obs, void* obs_user,
+                                  spqr_pipeline** out, char* err, int errlen, int* err_cluster) {
     *out = nullptr;
     auto* P = new spqr_pipeline;
     const int rc = guarded(err, errlen, err_cluster, [&] {
@@ -134,7 +142,8 @@ int spqr_pipeline_create(int m, int n, const int* colptr, const int* rowind, con
             CK(cudaEventCreate(&e0));
             CK(cudaEventCreate(&e1));
             CK(cudaEventRecord(e0, P->st));
-            P->F = gpu_factorize(P->Aw, P->h, P->owner, fo, P->st);
+            const FactorizeObserver ob = make_observer(obs, obs_user);
+            P->F = gpu_factorize(P->Aw, P->h, P->owner, fo, P->st, obs ? &ob : nullptr);
             P->plan = build_solve_plan(P->F, P->st);
             CK(cudaEventRecord(e1, P->st));
             CK(cudaEventSynchronize(e1));

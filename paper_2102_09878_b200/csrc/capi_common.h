@@ -59,6 +59,32 @@ inline void capi_set_threads() {
 #endif
 }
 
+// The engine's observer as the C ABI's callback: the view's arrays point into the EngineView.
+inline FactorizeObserver make_observer(spqr_observer_fn fn, void* user) {
+    if (!fn) return FactorizeObserver();
+    return [fn, user](const char* phase, int stage, int detail, const EngineView& v) {
+        spqr_engine_view cv{};
+        cv.nfronts = static_cast<int>(v.front_cluster.size());
+        cv.front_cluster = v.front_cluster.data();
+        cv.rows_ptr = v.rows_ptr.data();
+        cv.rows = v.rows.data();
+        cv.keys_ptr = v.keys_ptr.data();
+        cv.keys = v.keys.data();
+        cv.key_width = v.key_width.data();
+        cv.block_off = v.block_off.data();
+        cv.values = v.values.data();
+        cv.nclusters = static_cast<int>(v.cols_ptr.size()) - 1;
+        cv.cols_ptr = v.cols_ptr.data();
+        cv.cols = v.cols.data();
+        cv.nwave = static_cast<int>(v.wave.size());
+        cv.wave = v.wave.data();
+        cv.pivots = v.pivots;
+        cv.dropped = v.dropped;
+        cv.trailing = v.trailing;
+        fn(user, phase, stage, detail, &cv);
+    };
+}
+
 // save_factorization (proj/src/transforms.cpp:206-240): SPQRFW01 file of a device W.
 inline void save_device_factorization(const DeviceFactorization& F, const char* path) {
     std::vector<std::pair<const char*, std::vector<char>>> mirror;

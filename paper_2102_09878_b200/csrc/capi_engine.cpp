@@ -94,8 +94,8 @@ extern "C" {
 int spqr_factorize(int m, int n, const int* colptr, const int* rowind, const double* vals, int num_levels,
                    int nclusters, const int* cluster_info, const int* cluster_colptr, const int* cluster_cols,
                    const int* finest_of_col, int ntree, const int* tree_parent, int tree_root, const int* row_owner,
-                   double eps, int skip_levels, int device, spqr_factorization** out, char* err, int errlen,
-                   int* err_cluster) {
+                   double eps, int skip_levels, int device, spqr_observer_fn obs, void* obs_user,
+                   spqr_factorization** out, char* err, int errlen, int* err_cluster) {
     *out = nullptr;
     spqr_factorization* H = nullptr;
     const int rc = capi_guarded(err, errlen, err_cluster, [&] {
@@ -147,7 +147,8 @@ int spqr_factorize(int m, int n, const int* colptr, const int* rowind, const dou
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, H->st));
-        H->F = gpu_factorize(A, h, owner, fo, H->st);
+        const FactorizeObserver ob = make_observer(obs, obs_user);
+        H->F = gpu_factorize(A, h, owner, fo, H->st, obs ? &ob : nullptr);
         finish_handle(H);
         CK(cudaEventRecord(e1, H->st));
         CK(cudaEventSynchronize(e1));

@@ -515,8 +515,8 @@ cudaMemPool_t engine_pool(int dev) {
 class Engine {
 public:
     Engine(const Csc& A, const ClusterHierarchy& h, const std::vector<int>& owner, const FactorizeOptions& opt,
-           cudaStream_t st)
-        : A_(A), h_(h), opt_(opt), st_(st), L_(h.num_levels) {
+           cudaStream_t st, const FactorizeObserver* obs = nullptr)
+        : A_(A), h_(h), opt_(opt), st_(st), L_(h.num_levels), obs_(obs) {
         out_.M = A.m;
         out_.N = A.n;
         out_.eps = opt.eps;
@@ -617,6 +617,42 @@ private:
     FactorizeOptions opt_;
     cudaStream_t st_;
     int L_;
+    const FactorizeObserver* obs_ = nullptr;
+    int cur_stage_ = 0;
+    // factorize.cpp:86-95: the state after a phase, downloaded for the observer (tests only)
+    void notify(const char* phase, int detail, const std::vector<int>* wave = nullptr) {
+        if (!obs_ || !*obs_) return;
+        CK(cudaStreamSynchronize(st_));
+        EngineView v;
+        std::vector<double> buf;
+        for (size_t c = 0; c < fr_.size(); ++c) {
+            if (!alive_[c] || !fr_[c].live) continue;
+            const Front& F = fr_[c];
+            v.front_cluster.push_back(static_cast<int>(c));
+            v.rows.insert(v.rows.end(), F.rows.begin(), F.rows.end());
+            v.rows_ptr.push_back(static_cast<int>(v.rows.size()));
+            const int nr = F.nrows();
+            buf.assign(static_cast<size_t>(F.ld) * std::max(F.ncols, 0), 0.0);
+            if (!buf.empty() && F.mat) CK(cudaMemcpy(buf.data(), F.mat, sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
+            for (const KeyRef& k : F.keys) {  // ascending keys
+                v.keys.push_back(k.key);
+                v.key_width.push_back(k.width);
+                v.block_off.push_back(static_cast<long long>(v.values.size()));
+                for (int j = 0; j < k.width; ++j)
+                    for (int r = 0; r < nr; ++r) v.values.push_back(buf[static_cast<size_t>(k.col + j) * F.ld + r]);
+            }
+            v.keys_ptr.push_back(static_cast<int>(v.keys.size()));
+        }
+        for (const auto& cl : cols_) {
+            v.cols.insert(v.cols.end(), cl.begin(), cl.end());
+            v.cols_ptr.push_back(static_cast<int>(v.cols.size()));
+        }
+        if (wave) v.wave = *wave;
+        v.pivots = npiv_;
+        v.dropped = static_cast<long long>(out_.dropped_rows.size());
+        v.trailing = static_cast<long long>(out_.trailing_rows.size());
+        (*obs_)(phase, cur_stage_, detail, v);
+    }
     std::vector<Front> fr_;
     std::vector<std::vector<int>> cols_;
     std::vector<char> gone_;
@@ -1759,6 +1795,7 @@ void Engine::eliminate_stage(int k) {
         if (w > 0) compute_stats(stage_fronts(waves[w]));
         batch_ = out_.nbatches++;  // a wave's factors touch independent column sets
         eliminate_wave(waves[w]);
+        notify("eliminate", waves[w].front(), &waves[w]);
     }
     // W in the reference's chronological order (ascending cluster); the solve
     // plan regroups by batch, which only reorders independent factors
@@ -2732,6 +2769,7 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
     for (int k = L_ + 1; k >= 1; --k) {
         StageStats st;
         st.stage = k;
+        cur_stage_ = k;
         sprof_.emplace_back();
         sprof_.back().stage = k;
         const HostProf before = prof_;
@@ -2743,17 +2781,21 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
             batch_ = out_.nbatches++;
             scale_all();
             st.t_scale = now_s() - t0;
+            notify("scale", -1);
             t0 = now_s();
             sparsify_rows_all();
+            notify("sparsify_rows", -1);
             batch_ = out_.nbatches++;
             sparsify_cols_all();
             st.t_sparsify = now_s() - t0;
+            notify("sparsify_cols", -1);
         }
         snapshot(st);
         if (k >= 2) {
             t0 = now_s();
             merge_level();
             st.t_merge = now_s() - t0;
+            notify("merge", -1);
         }
         st.nnz_w = out_.nnz_w();
         out_.stages.push_back(st);
@@ -2795,7 +2837,7 @@ void sampler_start();
 void sampler_stop();
 
 DeviceFactorization gpu_factorize(const Csc& A, const ClusterHierarchy& h, const std::vector<int>& owner,
-                                  const FactorizeOptions& opt, cudaStream_t st) {
+                                  const FactorizeOptions& opt, cudaStream_t st, const FactorizeObserver* obs) {
     if (A.m < A.n) throw std::invalid_argument("matrix must have at least as many rows as columns");
     if (static_cast<Index>(owner.size()) != A.m) throw std::invalid_argument("row_owner size mismatch");
     sampler_start();
@@ -2804,7 +2846,7 @@ DeviceFactorization gpu_factorize(const Csc& A, const ClusterHierarchy& h, const
     DeviceFactorization F;
     double t1 = 0, t2 = 0;
     {
-        Engine e(A, h, owner, opt, st);
+        Engine e(A, h, owner, opt, st, obs);
         t1 = now_s();
         F = e.run();
         t2 = now_s();

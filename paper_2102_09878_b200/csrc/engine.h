@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -57,7 +58,24 @@ struct DeviceFactorization {
     long long nnz_w() const;
 };
 
+// Read-only engine state handed to an observer after each phase (EngineView,
+// factorize.h:31-36), materialised on the host: every live front's rows and key blocks
+// (column-major nrows x width each, keys ascending), the active columns per cluster and the
+// row accounting.  The GPU engine eliminates a stage in dependency waves, so one
+// "eliminate" notification covers a whole wave (`wave`, ascending; detail = its first id).
+struct EngineView {
+    std::vector<int> front_cluster, rows_ptr{0}, rows, keys_ptr{0}, keys, key_width;
+    std::vector<long long> block_off;
+    std::vector<double> values;
+    std::vector<int> cols_ptr{0}, cols;
+    std::vector<int> wave;
+    long long pivots = 0, dropped = 0, trailing = 0;
+};
+// FactorizeObserver::on_phase (factorize.h:40-43): phase is "eliminate", "scale",
+// "sparsify_rows", "sparsify_cols" or "merge".
+using FactorizeObserver = std::function<void(const char* phase, int stage, int detail, const EngineView& v)>;
+
 DeviceFactorization gpu_factorize(const Csc& A, const ClusterHierarchy& h, const std::vector<int>& owner,
-                                  const FactorizeOptions& opt, cudaStream_t st);
+                                  const FactorizeOptions& opt, cudaStream_t st, const FactorizeObserver* obs = nullptr);
 
 }  // namespace spqr
