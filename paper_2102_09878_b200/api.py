@@ -67,15 +67,17 @@ def _observer(fn):
         keys = _arr(v.keys, nkeys, np.int64)
         kw = _arr(v.key_width, nkeys, np.int64)
         bo = _arr(v.block_off, nkeys, np.int64)
-        nval = int(bo[-1] + kw[-1] * (rp[-1] - rp[-2])) if nkeys else 0
-        vals = _arr(v.values, nval, np.float64)
+        have_vals = bool(v.values)
+        nval = int(bo[-1] + kw[-1] * (rp[-1] - rp[-2])) if (nkeys and have_vals) else 0
+        vals = _arr(v.values, nval, np.float64) if have_vals else None
         fronts = {}
         for f in range(nf):
             nr = int(rp[f + 1] - rp[f])
             blocks = {}
             for b in range(int(kp[f]), int(kp[f + 1])):
                 w = int(kw[b])
-                blocks[int(keys[b])] = vals[bo[b]: bo[b] + nr * w].reshape(w, nr).T.copy()
+                blocks[int(keys[b])] = (vals[bo[b]: bo[b] + nr * w].reshape(w, nr).T.copy() if vals is not None
+                                        else np.zeros((nr, w)))  # SPQR_OBSERVE_STRUCTURE_ONLY
             fronts[int(fc[f])] = dict(rows=rows[rp[f]: rp[f + 1]].copy(), blocks=blocks)
         cp = _arr(v.cols_ptr, v.nclusters + 1, np.int64)
         cols_all = _arr(v.cols, int(cp[-1]), np.int64)

@@ -619,10 +619,39 @@ private:
     int L_;
     const FactorizeObserver* obs_ = nullptr;
     int cur_stage_ = 0;
+    // SPQR_DUMP_G=<stage>:<cluster>:<path> writes that interface's sparsify_cols input G
+    // (cs x nG, column-major, int32 dims first) before each of its CPQRs (parity diagnostics)
+    struct GDump {
+        int stage = -1, cluster = -1;
+        std::string path;
+        GDump() {
+            if (const char* e = std::getenv("SPQR_DUMP_G")) {
+                const std::string v(e);
+                const size_t a = v.find(':'), b = v.find(':', a + 1);
+                if (a != std::string::npos && b != std::string::npos) {
+                    stage = std::atoi(v.substr(0, a).c_str());
+                    cluster = std::atoi(v.substr(a + 1, b - a - 1).c_str());
+                    path = v.substr(b + 1);
+                }
+            }
+        }
+    } gdump_;
+    void dump_g(const double* dG, int cs, int nG) {
+        CK(cudaStreamSynchronize(st_));
+        std::vector<double> h(static_cast<size_t>(cs) * nG);
+        if (!h.empty()) CK(cudaMemcpy(h.data(), dG, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+        if (std::FILE* f = std::fopen(gdump_.path.c_str(), "wb")) {
+            const int dims[2] = {cs, nG};
+            std::fwrite(dims, 4, 2, f);
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
+    }
     // factorize.cpp:86-95: the state after a phase, downloaded for the observer (tests only)
     void notify(const char* phase, int detail, const std::vector<int>* wave = nullptr) {
         if (!obs_ || !*obs_) return;
         CK(cudaStreamSynchronize(st_));
+        static const bool structure_only = std::getenv("SPQR_OBSERVE_STRUCTURE_ONLY") != nullptr;
         EngineView v;
         std::vector<double> buf;
         for (size_t c = 0; c < fr_.size(); ++c) {
@@ -632,12 +661,16 @@ private:
             v.rows.insert(v.rows.end(), F.rows.begin(), F.rows.end());
             v.rows_ptr.push_back(static_cast<int>(v.rows.size()));
             const int nr = F.nrows();
-            buf.assign(static_cast<size_t>(F.ld) * std::max(F.ncols, 0), 0.0);
-            if (!buf.empty() && F.mat) CK(cudaMemcpy(buf.data(), F.mat, sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
+            if (!structure_only) {
+                buf.assign(static_cast<size_t>(F.ld) * std::max(F.ncols, 0), 0.0);
+                if (!buf.empty() && F.mat)
+                    CK(cudaMemcpy(buf.data(), F.mat, sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
+            }
             for (const KeyRef& k : F.keys) {  // ascending keys
                 v.keys.push_back(k.key);
                 v.key_width.push_back(k.width);
                 v.block_off.push_back(static_cast<long long>(v.values.size()));
+                if (structure_only) continue;  // SPQR_OBSERVE_STRUCTURE_ONLY: rows, keys and widths only
                 for (int j = 0; j < k.width; ++j)
                     for (int r = 0; r < nr; ++r) v.values.push_back(buf[static_cast<size_t>(k.col + j) * F.ld + r]);
             }
@@ -2403,6 +2436,9 @@ void Engine::sparsify_cols_all() {
         std::unique_ptr<NScope> sc2 = std::make_unique<NScope>(nprof_, "scols.upload+cpqr+fetch");
         flush_assemble(gb);
         const size_t nj = jobs.size();
+        if (gdump_.cluster >= 0)  // diagnostics (SPQR_DUMP_G): one interface's G before its CPQR
+            for (const Job& j : jobs)
+                if (j.p == gdump_.cluster && cur_stage_ == gdump_.stage) dump_g(j.G, j.cs, j.nG);
         int* d_rank = arena().alloc_n<int>(nj);
         double* d_r11 = arena().alloc_n<double>(nj);
         for (size_t i = 0; i < nj; ++i) {
