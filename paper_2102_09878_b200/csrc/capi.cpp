@@ -491,7 +491,8 @@ namespace {
 void cpqr_dev_run(DeviceArena& mem, int nb, int m, int n, double* da, double eps, int* dr, double* d11, int* dp,
                   double* dV, double* dt, double* ds, float* ms) {
     const int kmax = std::min(m, n);
-    const bool big = 8ull * m * n > kBigCpqrBytes && m >= 32 && cpqr_big_smem_bytes(m, n) <= 200 * 1024;
+    const bool big = 8ull * m * n > kBigCpqrBytes && m >= 32 && cpqr_big_smem_bytes(m, n) <= 200 * 1024 &&
+                     !(std::getenv("SPQR_CPQR_PATH") && std::string(std::getenv("SPQR_CPQR_PATH")) == "cluster");
     const size_t wstride = big ? cpqr_big_work_doubles(n) : 3 * static_cast<size_t>(n);
     double* work = mem.alloc_n<double>(std::max<size_t>(static_cast<size_t>(nb) * wstride, 1));
     CK(cudaMemset(dV, 0, sizeof(double) * static_cast<size_t>(nb) * m * kmax));
@@ -507,8 +508,9 @@ void cpqr_dev_run(DeviceArena& mem, int nb, int m, int n, double* da, double eps
     int* didx = mem.alloc_n<int>(std::max(nb, 1));
     CK(cudaMemcpy(didx, all.data(), sizeof(int) * nb, cudaMemcpyHostToDevice));
     const size_t sm = cpqr_smem_bytes(m, n);
-    const char* force = std::getenv("SPQR_CPQR_PATH");  // narrow|smem|big (comparisons, tests)
+    const char* force = std::getenv("SPQR_CPQR_PATH");  // narrow|tall|smem|big|cluster (comparisons, tests)
     const std::string fp = force ? force : "";
+    const bool clus = fp == "cluster" && n >= 16 && cpqr_clus_smem_bytes(m, n) <= 200 * 1024;
     const int ncls = (fp.empty() || fp == "narrow") ? cpqr_narrow_class(m, n) : -1;
     const int tcls = (fp.empty() || fp == "tall") ? cpqr_tall_class(m, n) : -1;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -518,7 +520,9 @@ void cpqr_dev_run(DeviceArena& mem, int nb, int m, int n, double* da, double eps
         CK(cudaDeviceSynchronize());
         CK(cudaEventRecord(e0, 0));
     }
-    if (ncls >= 0)
+    if (clus)
+        launch_cpqr_clus(dc, didx, nb, cpqr_clus_smem_bytes(m, n), 0);
+    else if (ncls >= 0)
         launch_cpqr_narrow(ncls, dc, didx, nb, cpqr_narrow_smem(m, n), 0);
     else if (tcls >= 0)
         launch_cpqr_tall(tcls, dc, didx, nb, 0);

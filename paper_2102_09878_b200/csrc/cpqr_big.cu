@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 
 #include "dev.h"
@@ -130,9 +131,11 @@ __device__ void trailing(double* A, long long ld, int m, int k, int kmax, int G,
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_cpqr_big(CpqrDesc d, BigScratch S) {
-    cg::grid_group grid = cg::this_grid();
-    const int G = gridDim.x, cta = blockIdx.x;
+// The cooperative algorithm on G CTAs (rank cta); gsync() is the barrier between them (a
+// grid barrier for the whole-GPU launch, a cluster barrier for thread-block clusters).
+template <class Sync>
+__device__ __forceinline__ void cpqr_coop_body(const CpqrDesc& d, const BigScratch& S, const int G, const int cta,
+                                               Sync&& gsync) {
     const int m = d.m, n = d.n, kmax = min(m, n);
     const long long ld = d.ld;
     double* A = d.a;
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cpqr_big(CpqrDesc d, BigScratch
                 S.pphys[cta] = bp;
             }
         }
-        grid.sync();
+        gsync();
         if (wid == 0) {  // every CTA reduces the same partials to the same answer
             bv = -1.0;
             bj = n;
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cpqr_big(CpqrDesc d, BigScratch
         ++k;
     }
     if (prev_pc >= 0) {  // loop ran to kmax: the last pivot column is still pending
-        grid.sync();
+        gsync();
         finalise(prev_pc, k - 1, prev_alpha, prev_v0, prev_reflect, prev_flip);
     }
     if (cta == 0 && threadIdx.x == 0) {
@@ -355,7 +358,103 @@ __global__ void __launch_bounds__(kThreads, 1) k_cpqr_big(CpqrDesc d, BigScratch
     }
 }
 
+__global__ void __launch_bounds__(kThreads, 1) k_cpqr_big(CpqrDesc d, BigScratch S) {
+    cg::grid_group grid = cg::this_grid();
+    cpqr_coop_body(d, S, static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x), [&] { grid.sync(); });
+}
+
+// One problem per thread-block cluster of CS CTAs (distinct problems run concurrently, one
+// cluster each): the same algorithm with a cluster barrier (~1 us) in place of the grid
+// barrier.  The cluster's partials and the pivot column go through global memory (L2,
+// __ldcg); a fence before every barrier makes the CTAs' global stores visible at cluster scope.
+template <int CS>
+__global__ void __launch_bounds__(kThreads, 1) k_cpqr_clus(const CpqrDesc* __restrict__ ds, const int* __restrict__ idx) {
+    cg::cluster_group cl = cg::this_cluster();
+    const CpqrDesc d = ds[idx[blockIdx.x / CS]];
+    BigScratch S;
+    S.vn1 = d.work;
+    S.pval = d.work + d.n;
+    S.pidx = reinterpret_cast<int*>(S.pval + CS);
+    S.pphys = S.pidx + CS;
+    cpqr_coop_body(d, S, CS, static_cast<int>(cl.block_rank()), [&] {
+        __threadfence();
+        cl.sync();
+    });
+}
+
 }  // namespace
+
+template <int CS>
+void launch_clus_cs(const CpqrDesc* ds, const int* idx, int np, size_t smem, cudaStream_t st);
+
+// cluster size: 16 CTAs (non-portable; C3 CPQR 4.6 s against 5.1 s with 8) when the device can
+// hold such a cluster of 1024-thread CTAs, else the portable 8; SPQR_CPQR_CLUSTER=8|16 forces one
+int cpqr_clus_ctas() {
+    static const int cs = [] {
+        if (const char* e = std::getenv("SPQR_CPQR_CLUSTER")) return std::atoi(e) == 16 ? 16 : 8;
+        if (cudaFuncSetAttribute(reinterpret_cast<const void*>(k_cpqr_clus<16>),
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            cudaGetLastError();
+            return 8;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(16);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = 64 * 1024;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 16;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(k_cpqr_clus<16>),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        int nclus = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclus, reinterpret_cast<const void*>(k_cpqr_clus<16>), &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            return 8;
+        }
+        return nclus >= 4 ? 16 : 8;
+    }();
+    return cs;
+}
+
+size_t cpqr_clus_smem_bytes(int m, int n) {
+    const size_t cs = static_cast<size_t>(cpqr_clus_ctas());
+    const size_t nown = (static_cast<size_t>(n) + cs - 1) / cs;
+    return sizeof(double) * (static_cast<size_t>(m) + 2 * nown) + sizeof(int) * nown;
+}
+
+template <int CS>
+void launch_clus_cs(const CpqrDesc* ds, const int* idx, int np, size_t smem, cudaStream_t st) {
+    static SmemCfg configured;
+    smem_optin(reinterpret_cast<const void*>(k_cpqr_clus<CS>), smem, configured);
+    if (CS > 8) cudaFuncSetAttribute(reinterpret_cast<const void*>(k_cpqr_clus<CS>),
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(np) * CS);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_cpqr_clus<CS>, ds, idx);
+}
+
+// problems idx[0..np) of ds, one cluster each; every problem's d.work holds >= n + 32 doubles
+void launch_cpqr_clus(const CpqrDesc* ds, const int* idx, int np, size_t smem, cudaStream_t st) {
+    if (np <= 0) return;
+    if (cpqr_clus_ctas() == 16)
+        launch_clus_cs<16>(ds, idx, np, smem, st);
+    else
+        launch_clus_cs<8>(ds, idx, np, smem, st);
+}
 
 int cpqr_big_grid() {
     static int g = 0;

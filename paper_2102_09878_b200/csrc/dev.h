@@ -234,6 +234,10 @@ void launch_cpqr_narrow(int cls, const CpqrDesc* d_desc, const int* d_idx, int c
 int cpqr_tall_class(int m, int n);
 void launch_cpqr_tall(int cls, const CpqrDesc* d_desc, const int* d_idx, int cnt, cudaStream_t st);
 void launch_cpqr_big(const CpqrDesc& d, cudaStream_t st);
+// one problem per thread-block cluster of cpqr_clus_ctas() CTAs (cpqr_big.cu k_cpqr_clus)
+int cpqr_clus_ctas();
+size_t cpqr_clus_smem_bytes(int m, int n);
+void launch_cpqr_clus(const CpqrDesc* ds, const int* idx, int np, size_t smem, cudaStream_t st);
 size_t cpqr_big_smem_bytes(int m, int n);  // dynamic smem of one launch (<= 200 KB to be eligible)
 inline size_t cpqr_big_work_doubles(int n) { return 3 * static_cast<size_t>(n) + 2 * 512 + 16; }
 constexpr size_t kBigCpqrBytes = size_t(2) << 20;

@@ -206,10 +206,11 @@ public:
         CK(cudaEventRecord(e, st));
         return e;
     }
-    void end(int tag, cudaEvent_t e0, cudaStream_t st, double bytes) {
+    // route >= 0: also accumulated per CPQR route (SPQR_PROF breakdown), with `probs` problems
+    void end(int tag, cudaEvent_t e0, cudaStream_t st, double bytes, int route = -1, double probs = 0) {
         cudaEvent_t e1 = take();
         CK(cudaEventRecord(e1, st));
-        pend_.push_back({tag, e0, e1, bytes});
+        pend_.push_back({tag, e0, e1, bytes, route, probs});
     }
     void resolve(EngineCounters& c) {
         for (auto& p : pend_) {
@@ -218,6 +219,11 @@ public:
             c.k_ms[p.tag] += ms;
             c.k_bytes[p.tag] += p.bytes;
             c.k_launches[p.tag] += 1;
+            if (p.route >= 0) {
+                c.route_ms[p.route] += ms;
+                c.route_probs[p.route] += p.probs;
+                c.route_launches[p.route] += 1;
+            }
         }
         pend_.clear();
         used_ = 0;
@@ -228,6 +234,8 @@ private:
         int tag;
         cudaEvent_t e0, e1;
         double bytes;
+        int route;
+        double probs;
     };
     std::vector<cudaEvent_t> pool_;
     std::vector<P> pend_;
@@ -1005,7 +1013,8 @@ private:
         // kernel costs ~8 us per pivot plus the trailing traffic at ~6 TB/s.
         // Move the largest problems to the cooperative kernel while that lowers
         // the estimated batch time.
-        std::vector<int> glob;
+        std::vector<int> glob, clus;
+        size_t csmem = 0;
         std::vector<int> tall[2];
         std::vector<std::vector<int>> narrow(12);
         std::vector<char> coop(cd.size(), 0), nar(cd.size(), 0);
@@ -1030,16 +1039,31 @@ private:
             for (int i : narrow[c]) nb += 8.0 * cd[i].m * cd[i].n;
             cudaEvent_t e0 = kt_.begin(st_);
             launch_cpqr_narrow(c, dc, dn, static_cast<int>(narrow[c].size()), nsmem[c], st_);
-            kt_.end(K_CPQR, e0, st_, nb);
+            kt_.end(K_CPQR, e0, st_, nb, 0, static_cast<double>(narrow[c].size()));
         }
         if (nnar == cd.size()) return;
+        // Problems too big for one CTA's shared memory run on a thread-block cluster of
+        // cpqr_clus_ctas() CTAs each (k_cpqr_clus, concurrently), or — the largest — one at a
+        // time on the whole GPU (k_cpqr_big).  SPQR_NO_CPQR_CLUSTER=1: one CTA each in global
+        // memory instead of the clusters (the previous route, for comparison).
+        static const bool use_clus = std::getenv("SPQR_NO_CPQR_CLUSTER") == nullptr;
+        auto clus_ok = [&](int i) {
+            return use_clus && cd[i].n >= 16 && cpqr_clus_smem_bytes(cd[i].m, cd[i].n) <= 200 * 1024;
+        };
         if (!glob.empty()) {
-            auto single = [&](int i) { return 16.0 * std::min(cd[i].m, cd[i].n) * double(cd[i].m) * cd[i].n / 20e9; };
+            // estimated time off the cooperative kernel: one CTA streams ~20 GB/s; a cluster
+            // ~cpqr_clus_ctas() times that plus ~3 us of cluster barriers per pivot
+            static const double clus_bw =  // per-CTA streaming rate assumed for the clusters (GB/s)
+                std::getenv("SPQR_CLUS_BW") ? std::atof(std::getenv("SPQR_CLUS_BW")) : 20.0;
+            auto single = [&](int i) {
+                const double mn = std::min(cd[i].m, cd[i].n), bytes = 16.0 * double(cd[i].m) * cd[i].n;
+                return clus_ok(i) ? mn * (3e-6 + bytes / (cpqr_clus_ctas() * clus_bw * 1e9)) : mn * bytes / 20e9;
+            };
             auto cost = [&](int i) {
                 return std::min(cd[i].m, cd[i].n) * (8e-6 + 16.0 * double(cd[i].m) * cd[i].n / 6e12);
             };
             std::sort(glob.begin(), glob.end(), [&](int a, int b) { return single(a) > single(b); });
-            const double lanes = 2.0 * sm_count();
+            const double lanes = use_clus ? std::max(1.0, double(sm_count()) / cpqr_clus_ctas()) : 2.0 * sm_count();
             std::vector<double> suf(glob.size() + 1, 0.0);
             for (size_t j = glob.size(); j-- > 0;) suf[j] = suf[j + 1] + single(glob[j]);
             double best = 1e300, ccum = 0.0;
@@ -1066,7 +1090,7 @@ private:
                 d.work = arena().alloc_n<double>(cpqr_big_work_doubles(d.n));
                 cudaEvent_t e0 = kt_.begin(st_);
                 launch_cpqr_big(d, st_);
-                kt_.end(K_CPQR, e0, st_, 8.0 * d.m * d.n);
+                kt_.end(K_CPQR, e0, st_, 8.0 * d.m * d.n, 1, 1.0);
                 continue;
             }
             static const bool no_tall = std::getenv("SPQR_NO_TALL") != nullptr;
@@ -1076,10 +1100,21 @@ private:
                 smem = std::max(smem, b);
             } else if (tc >= 0) {  // 128 < m <= 512: warp-per-column kernel, in place
                 tall[tc].push_back(static_cast<int>(i));
+            } else if (clus_ok(static_cast<int>(i))) {
+                clus.push_back(static_cast<int>(i));
+                csmem = std::max(csmem, cpqr_clus_smem_bytes(cd[i].m, cd[i].n));
             } else {
                 large.push_back(static_cast<int>(i));
                 maxm = std::max(maxm, cd[i].m);
             }
+        }
+        if (!clus.empty()) {
+            const int* dcl = u.put(clus);
+            double cbb = 0;
+            for (int i : clus) cbb += 8.0 * cd[i].m * cd[i].n;
+            cudaEvent_t e0 = kt_.begin(st_);
+            launch_cpqr_clus(dc, dcl, static_cast<int>(clus.size()), csmem, st_);
+            kt_.end(K_CPQR, e0, st_, cbb, 4, static_cast<double>(clus.size()));
         }
         for (int c = 0; c < 2; ++c) {
             if (tall[c].empty()) continue;
@@ -1088,7 +1123,7 @@ private:
             for (int i : tall[c]) tb += 8.0 * cd[i].m * cd[i].n;
             cudaEvent_t e0 = kt_.begin(st_);
             launch_cpqr_tall(c, dc, dt, static_cast<int>(tall[c].size()), st_);
-            kt_.end(K_CPQR, e0, st_, tb);
+            kt_.end(K_CPQR, e0, st_, tb, 2, static_cast<double>(tall[c].size()));
         }
         const int* ds = u.put(small);
         const int* dl = u.put(large);
@@ -1097,7 +1132,7 @@ private:
         for (int i : large) cb += 8.0 * cd[i].m * cd[i].n;
         cudaEvent_t e0 = kt_.begin(st_);
         launch_cpqr_split(dc, ds, static_cast<int>(small.size()), smem, dl, static_cast<int>(large.size()), maxm, st_);
-        kt_.end(K_CPQR, e0, st_, cb);
+        kt_.end(K_CPQR, e0, st_, cb, 3, static_cast<double>(small.size() + large.size()));
     }
     void eliminate_stage(int k);
     void eliminate_wave(const std::vector<int>& list);
@@ -2863,6 +2898,10 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         for (int t = 0; t < K_NTAGS; ++t)
             std::fprintf(stderr, "[spqr prof] kernel %-9s %8.2f ms %6lld launches %10.1f MB\n", ktag_name(t), out_.ctr.k_ms[t],
                          out_.ctr.k_launches[t], out_.ctr.k_bytes[t] / 1e6);
+        static const char* rn[5] = {"narrow", "coop", "tall", "smem+large", "cluster"};
+        for (int r = 0; r < 5; ++r)
+            std::fprintf(stderr, "[spqr prof] cpqr route %-10s %8.2f ms %6lld launches %8.0f problems\n", rn[r],
+                         out_.ctr.route_ms[r], out_.ctr.route_launches[r], out_.ctr.route_probs[r]);
     }
     return std::move(out_);
 }

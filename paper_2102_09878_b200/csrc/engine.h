@@ -42,6 +42,8 @@ struct EngineCounters {
     double t_qr_ms = 0;  // device time of the batched front-QR launches (CUDA events)
     long long qr_launches = 0;
     long long elim_waves = 0;  // dependency waves of eliminations summed over stages
+    double route_ms[5] = {0}, route_probs[5] = {0};  // CPQR by route: narrow, coop, tall, smem+large, cluster
+    long long route_launches[5] = {0};
 };
 
 // The outcome of spaqr_factorize (transforms.h:53-72) with W resident in HBM.

@@ -173,6 +173,35 @@ def test_cpqr_large_cooperative_matches_oracle(shape, eps, decay):
     assert np.array_equal(g["sign"][:k], ref["sign"][:k])
 
 
+@pytest.mark.parametrize("shape,eps,decay", [((600, 1200), 1e-2, 0.97), ((1500, 400), 1e-3, 0.98),
+                                             ((700, 900), 0.0, 0.99), ((300, 2500), 1e-2, 0.95),
+                                             ((2000, 300), 1e-2, 0.9), ((257, 64), 1e-8, 0.8)])
+def test_cpqr_cluster_matches_oracle(shape, eps, decay, monkeypatch):
+    """Large interfaces on thread-block clusters (k_cpqr_clus, cpqr_big.cu): one 8-CTA cluster per
+    problem, several problems concurrently, cluster barriers instead of a grid barrier."""
+    monkeypatch.setenv("SPQR_CPQR_PATH", "cluster")
+    m, n = shape
+    rng = np.random.default_rng(m * 3 + n)
+    r = min(m, n)
+    nb = 3
+    A = []
+    for b in range(nb):
+        U, _ = np.linalg.qr(rng.standard_normal((m, r)))
+        W, _ = np.linalg.qr(rng.standard_normal((n, r)))
+        A.append((U * decay ** np.arange(r)) @ W.T)
+    res = _P().cpqr_batched(np.stack(A), eps)
+    for b in range(nb):
+        g, ref = res[b], O.cpqr(A[b], eps)
+        assert g["rank"] == ref["rank"]
+        k = ref["rank"]
+        assert np.array_equal(g["perm"][:k], ref["perm"][:k])
+        assert abs(g["r11"] - ref["r11"]) <= 1e-12 * abs(ref["r11"])
+        assert np.allclose(g["R"], ref["R"], atol=1e-10 * abs(ref["r11"]))
+        assert np.allclose(g["V"], ref["V"], atol=1e-9)
+        assert np.allclose(g["tau"], ref["tau"], atol=1e-12)
+        assert np.array_equal(g["sign"][:k], ref["sign"][:k])
+
+
 def test_cpqr_edge_cases():
     res = _P().cpqr_batched(np.zeros((2, 6, 4)), 1e-8)
     assert all(r["rank"] == 0 and r["r11"] == 0.0 for r in res)
