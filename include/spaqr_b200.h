@@ -29,6 +29,9 @@ extern "C" {
 enum { SPQR_OK = 0, SPQR_E_SINGULAR = 1, SPQR_E_SHAPE = 2, SPQR_E_CUDA = 3, SPQR_E_OTHER = 4 };
 enum { SPQR_SOLVER_SPAQR = 0, SPQR_SOLVER_DIRECT = 1, SPQR_SOLVER_DIAG = 2 };
 enum { SPQR_W_APPLY = 0, SPQR_W_SOLVE = 1, SPQR_WT_APPLY = 2, SPQR_WT_SOLVE = 3 };
+/* Factorization::q_apply_t / q_apply (transforms.h:70-71; transforms.cpp:113-127): y (length M)
+ * <- Q^T y / Q y, for factorizations made with store_q (factorize.h:16). */
+enum { SPQR_Q_APPLY_T = 4, SPQR_Q_APPLY = 5 };
 
 typedef struct spqr_pipeline spqr_pipeline;
 
@@ -76,7 +79,15 @@ int spqr_pipeline_create_observed(int m, int n, const int* colptr, const int* ro
                                   const double* coords, int dim, const int* parts, int levels, double eps,
                                   int skip_levels, int solver, int device, spqr_observer_fn obs, void* obs_user,
                                   spqr_pipeline** out, char* err, int errlen, int* err_cluster);
+/* Same with FactorizeOptions::store_q (factorize.h:16; pipeline.h:18): the engine also keeps Q
+ * (transforms.h:34-37,57) for SPQR_Q_APPLY_T / SPQR_Q_APPLY. */
+int spqr_pipeline_create_ex(int m, int n, const int* colptr, const int* rowind, const double* vals,
+                            const double* coords, int dim, const int* parts, int levels, double eps, int skip_levels,
+                            int solver, int store_q, int device, spqr_observer_fn obs, void* obs_user,
+                            spqr_pipeline** out, char* err, int errlen, int* err_cluster);
 void spqr_pipeline_destroy(spqr_pipeline* p);
+/* |Q| (number of RowReflect factors), or -1 when the factorization keeps no Q. */
+long long spqr_pipeline_nq(const spqr_pipeline* p);
 
 /* info[16]: M, N, L, nclusters, nW, n_dropped, n_trailing, n_stages, nnz_w, nnz(A), W sweep levels,
  *           engine launches, engine syncs, h2d bytes, d2h bytes, solve-plan launches per sweep pair */
@@ -100,7 +111,8 @@ int spqr_pipeline_solve(spqr_pipeline* p, int direct, const double* b, double* x
                         int errlen);
 
 /* Factorization::w_apply / w_solve / wt_apply / wt_solve (transforms.cpp:40-111),
- * applied on the device to a host vector z of length N (permuted coordinates). */
+ * applied on the device to a host vector z of length N (permuted coordinates); modes
+ * SPQR_Q_APPLY_T / SPQR_Q_APPLY act on a vector of length M (store_q pipelines only). */
 int spqr_pipeline_apply(spqr_pipeline* p, int mode, double* z);
 
 /* Structure getters (reference-facing results for parity checks). */
@@ -150,18 +162,26 @@ int spqr_factorize(int m, int n, const int* colptr, const int* rowind, const dou
                    const int* finest_of_col, int ntree, const int* tree_parent, int tree_root, const int* row_owner,
                    double eps, int skip_levels, int device, spqr_observer_fn obs, void* obs_user,
                    spqr_factorization** out, char* err, int errlen, int* err_cluster);
+/* Same with FactorizeOptions::store_q (factorize.h:16). */
+int spqr_factorize_ex(int m, int n, const int* colptr, const int* rowind, const double* vals, int num_levels,
+                      int nclusters, const int* cluster_info, const int* cluster_colptr, const int* cluster_cols,
+                      const int* finest_of_col, int ntree, const int* tree_parent, int tree_root, const int* row_owner,
+                      double eps, int skip_levels, int store_q, int device, spqr_observer_fn obs, void* obs_user,
+                      spqr_factorization** out, char* err, int errlen, int* err_cluster);
 void spqr_factorization_destroy(spqr_factorization* f);
+long long spqr_factorization_nq(const spqr_factorization* f);
 /* info[8]: M, N, nW, nnz_w, n_dropped, n_trailing, n_stages, w_solve sweep levels */
 void spqr_factorization_info(const spqr_factorization* f, long long* info);
 void spqr_factorization_rows(const spqr_factorization* f, int* pivot_row, int* dropped, int* trailing);
 /* StageStats s (transforms.h:40-47): out5 = stage, nfronts, top_rows, top_cols, nnz_w */
 int spqr_factorization_stage(const spqr_factorization* f, int s, long long* out5);
 int spqr_factorization_stage_fronts(const spqr_factorization* f, int s, int* front_cols);
-/* Factorization::w_apply / w_solve / wt_apply / wt_solve (transforms.h:66-69) on host z (N). */
+/* Factorization::w_apply / w_solve / wt_apply / wt_solve (transforms.h:66-69) on host z (N);
+ * SPQR_Q_APPLY_T / SPQR_Q_APPLY (transforms.h:70-71) on host y (M) when the factorization has Q. */
 int spqr_factorization_apply(spqr_factorization* f, int mode, double* z);
 /* save_factorization / load_factorization (transforms.h:75-76; transforms.cpp:206-289): SPQRFW01
- * files; a loaded factorization solves on the GPU (factor once, solve many).  Q sections of
- * store_q files are read and dropped. */
+ * files; a loaded factorization solves on the GPU (factor once, solve many).  Q sections
+ * (store_q) are written and read back. */
 int spqr_factorization_save(const spqr_factorization* f, const char* path, char* err, int errlen);
 int spqr_factorization_load(const char* path, int device, spqr_factorization** out, char* err, int errlen);
 /* cgls(A, W, b, u, opt, weights) (solve.h:30-31; solve.cpp:24-76) on the GPU: A m x n CSC in W's

@@ -455,9 +455,10 @@ def match_rows(A):
 
 def factor_file_apply(path, mode, z=None):
     """load_factorization (transforms.cpp:242-289) of an SPQRFW01 file, then one sweep:
-    mode 'w_apply' | 'w_solve' | 'wt_apply' | 'wt_solve'.  Returns (M, N, nW) and the
-    transformed copy of z (None when z is None)."""
-    md = {"w_apply": 0, "w_solve": 1, "wt_apply": 2, "wt_solve": 3}[mode]
+    mode 'w_apply' | 'w_solve' | 'wt_apply' | 'wt_solve' (z of length N) or 'q_apply_t' | 'q_apply'
+    (length M, store_q files).  Returns (M, N, nW) and the transformed copy of z (None when z is
+    None)."""
+    md = {"w_apply": 0, "w_solve": 1, "wt_apply": 2, "wt_solve": 3, "q_apply_t": 4, "q_apply": 5}[mode]
     dims = np.zeros(3, np.int64)
     err = C.create_string_buffer(512)
     v = None if z is None else np.array(z, np.float64, copy=True)

@@ -46,7 +46,7 @@ Csc make_csc(int m, int n, const int* p, const int* i, const double* x) {
 
 Mat make_mat(int r, int c, const double* a) {
     Mat M(r, c);
-    if (r * c) std::memcpy(M.a.data(), a, sizeof(double) * static_cast<size_t>(r) * c);
+    if (r > 0 && c > 0) std::memcpy(M.a.data(), a, sizeof(double) * static_cast<size_t>(r) * c);
     return M;
 }
 

@@ -35,6 +35,11 @@
 
 namespace orc {
 
+// move_extras roundoff rule (factorize.cpp:141-164): candidate squared row norms at
+// or below kMoveNoise2 x (largest squared row norm of the eliminated cluster's blocks) count as 0.
+constexpr double kMoveNoise2 = (1e3 * 2.220446049250313e-16) * (1e3 * 2.220446049250313e-16);
+
+
 using Index = int;  // proj/include/spaqr/types.h:11
 
 // Column-major dense FP64 matrix (stands in for Eigen::MatrixXd, types.h:12).

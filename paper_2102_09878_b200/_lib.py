@@ -55,6 +55,14 @@ SIGNATURES = {
     "spqr_pipeline_create_observed": (C.c_int, [C.c_int, C.c_int, i32p, i32p, f64p, vp, C.c_int, vp, C.c_int,
                                                 C.c_double, C.c_int, C.c_int, C.c_int, vp, vp, C.POINTER(vp),
                                                 C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
+    "spqr_factorize_ex": (C.c_int, [C.c_int, C.c_int, i32p, i32p, f64p, C.c_int, C.c_int, i32p, i32p, i32p, i32p,
+                                    C.c_int, i32p, C.c_int, i32p, C.c_double, C.c_int, C.c_int, C.c_int, vp, vp,
+                                    C.POINTER(vp), C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
+    "spqr_pipeline_create_ex": (C.c_int, [C.c_int, C.c_int, i32p, i32p, f64p, vp, C.c_int, vp, C.c_int,
+                                          C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.POINTER(vp),
+                                          C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
+    "spqr_pipeline_nq": (C.c_longlong, [vp]),
+    "spqr_factorization_nq": (C.c_longlong, [vp]),
     "spqr_factorization_destroy": (None, [vp]),
     "spqr_factorization_info": (None, [vp, i64p]),
     "spqr_factorization_rows": (None, [vp, i32p, i32p, i32p]),

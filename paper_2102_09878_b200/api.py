@@ -92,7 +92,7 @@ class Pipeline:
     fn(phase, stage, detail, view) called after every engine phase (pipeline.h:39-41)."""
 
     def __init__(self, A, eps=1e-2, levels=0, skip_levels=3, solver="spaqr", coords=None, parts=None, device=0,
-                 observer=None):
+                 observer=None, store_q=False):
         require_gpu()
         L = lib()
         m, n, p, i, x = _csc(A)
@@ -107,10 +107,10 @@ class Pipeline:
         cl = C.c_int(-1)
         h = C.c_void_p()
         cb = _observer(observer)
-        rc = L.spqr_pipeline_create_observed(m, n, p, i, x, _ptr(cp), dim, _ptr(pp), int(levels), float(eps),
-                                             int(skip_levels), SOLVERS[solver], int(device),
-                                             C.cast(cb, C.c_void_p) if cb else None, None, C.byref(h), err, 512,
-                                             C.byref(cl))
+        rc = L.spqr_pipeline_create_ex(m, n, p, i, x, _ptr(cp), dim, _ptr(pp), int(levels), float(eps),
+                                       int(skip_levels), SOLVERS[solver], int(bool(store_q)), int(device),
+                                       C.cast(cb, C.c_void_p) if cb else None, None, C.byref(h), err, 512,
+                                       C.byref(cl))
         if rc != 0:
             msg = err.value.decode()
             if rc == 1:
@@ -124,6 +124,7 @@ class Pipeline:
         (self.M, self.N, self.L, self.nclusters, self.nW, self.ndropped, self.ntrailing, self.nstages, self.nnz_w,
          self.nnz_A, self.nbatches, self.launches, self.syncs, self.h2d_bytes, self.d2h_bytes,
          self.sweep_launches) = [int(v) for v in info]
+        self.nQ = int(L.spqr_pipeline_nq(self.h))  # -1: no Q kept
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -164,11 +165,16 @@ class Pipeline:
 
     def _apply(self, mode, z):
         z = np.array(z, dtype=np.float64, copy=True)
-        if z.ndim != 1 or z.shape[0] != self.N:
+        if z.ndim != 1 or z.shape[0] != (self.M if mode >= 4 else self.N):
             raise ValueError("vector length does not match the factorization")
+        if mode >= 4 and self.nQ < 0:
+            raise RuntimeError("the factorization holds no Q (create the pipeline with store_q=True)")
         if lib().spqr_pipeline_apply(self.h, mode, z):
             raise RuntimeError("spqr_pipeline_apply failed")
         return z
+
+    def q_apply_t(self, y): return self._apply(4, y)  # transforms.cpp:113-119
+    def q_apply(self, y): return self._apply(5, y)    # transforms.cpp:121-127
 
     def w_apply(self, z): return self._apply(0, z)
     def w_solve(self, z): return self._apply(1, z)
@@ -341,6 +347,7 @@ class Factorization:
         lib().spqr_factorization_info(self.h, info)
         (self.M, self.N, self.nW, self.nnz_w, self.ndropped, self.ntrailing, self.nstages,
          self.levels) = [int(v) for v in info]
+        self.nQ = int(lib().spqr_factorization_nq(self.h))  # -1: no Q kept
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -383,11 +390,16 @@ class Factorization:
 
     def _apply(self, mode, z):
         z = np.array(z, dtype=np.float64, copy=True)
-        if z.ndim != 1 or z.shape[0] != self.N:
+        if z.ndim != 1 or z.shape[0] != (self.M if mode >= 4 else self.N):
             raise ValueError("vector length does not match the factorization")
+        if mode >= 4 and self.nQ < 0:
+            raise RuntimeError("the factorization holds no Q (factorize with store_q=True)")
         if lib().spqr_factorization_apply(self.h, mode, z):
             raise RuntimeError("spqr_factorization_apply failed")
         return z
+
+    def q_apply_t(self, y): return self._apply(4, y)  # transforms.cpp:113-119
+    def q_apply(self, y): return self._apply(5, y)    # transforms.cpp:121-127
 
     def w_apply(self, z): return self._apply(0, z)
     def w_solve(self, z): return self._apply(1, z)
@@ -395,7 +407,7 @@ class Factorization:
     def wt_solve(self, z): return self._apply(3, z)
 
 
-def spaqr_factorize(A, hierarchy, row_owner, eps=1e-2, skip_levels=3, device=0, observer=None):
+def spaqr_factorize(A, hierarchy, row_owner, eps=1e-2, skip_levels=3, device=0, observer=None, store_q=False):
     """spaqr_factorize(A, h, row_owner, opt) (factorize.h:51-53) on the GPU.  A: the scaled,
     permuted matrix; hierarchy: the dict Pipeline.hierarchy() returns (clusters with tree_node,
     level, parent, stage, interior, cols; finest_of_col; tree_parent; tree_root; num_levels)."""
@@ -419,10 +431,10 @@ def spaqr_factorize(A, hierarchy, row_owner, eps=1e-2, skip_levels=3, device=0, 
     err = C.create_string_buffer(512)
     ecl = C.c_int(-1)
     cb = _observer(observer)
-    rc = lib().spqr_factorize(m, n, p, i, x, int(hierarchy["num_levels"]), len(cl), info, cptr, ccols, fin,
-                              len(tpar), tpar, int(hierarchy["tree_root"]), owner, float(eps), int(skip_levels),
-                              int(device), C.cast(cb, C.c_void_p) if cb else None, None, C.byref(h), err, 512,
-                              C.byref(ecl))
+    rc = lib().spqr_factorize_ex(m, n, p, i, x, int(hierarchy["num_levels"]), len(cl), info, cptr, ccols, fin,
+                                 len(tpar), tpar, int(hierarchy["tree_root"]), owner, float(eps), int(skip_levels),
+                                 int(bool(store_q)), int(device), C.cast(cb, C.c_void_p) if cb else None, None,
+                                 C.byref(h), err, 512, C.byref(ecl))
     if rc:
         msg = err.value.decode()
         if rc == 1:

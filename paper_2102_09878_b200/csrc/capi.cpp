@@ -38,6 +38,7 @@ struct spqr_pipeline {
     bool has_f = false;
     DeviceFactorization F;
     SolvePlan plan;
+    QSweep qs;  // store_q: q_apply / q_apply_t
     DevMatrix dA;
     CglsWork ws;
     double* d_w = nullptr;
@@ -83,6 +84,14 @@ int spqr_pipeline_create_observed(int m, int n, const int* colptr, const int* ro
                                   const double* coords, int dim, const int* parts, int levels, double eps,
                                   int skip_levels, int solver, int device, spqr_observer_fn obs, void* obs_user,
                                   spqr_pipeline** out, char* err, int errlen, int* err_cluster) {
+    return spqr_pipeline_create_ex(m, n, colptr, rowind, vals, coords, dim, parts, levels, eps, skip_levels, solver, 0,
+                                   device, obs, obs_user, out, err, errlen, err_cluster);
+}
+
+int spqr_pipeline_create_ex(int m, int n, const int* colptr, const int* rowind, const double* vals,
+                            const double* coords, int dim, const int* parts, int levels, double eps, int skip_levels,
+                            int solver, int store_q, int device, spqr_observer_fn obs, void* obs_user,
+                            spqr_pipeline** out, char* err, int errlen, int* err_cluster) {
     *out = nullptr;
     auto* P = new spqr_pipeline;
     const int rc = guarded(err, errlen, err_cluster, [&] {
@@ -138,6 +147,7 @@ int spqr_pipeline_create_observed(int m, int n, const int* colptr, const int* ro
             FactorizeOptions fo;
             fo.eps = P->eps;
             fo.skip_levels = skip_levels;
+            fo.store_q = store_q != 0;
             cudaEvent_t e0, e1;
             CK(cudaEventCreate(&e0));
             CK(cudaEventCreate(&e1));
@@ -194,6 +204,8 @@ void spqr_pipeline_info(const spqr_pipeline* p, long long* o) {
     o[14] = p->F.ctr.d2h_bytes;
     o[15] = p->plan.launches_per_sweep + p->plan.launches_per_sweep_t;
 }
+
+long long spqr_pipeline_nq(const spqr_pipeline* p) { return p->F.has_q ? static_cast<long long>(p->F.Q.size()) : -1; }
 
 void spqr_pipeline_times(const spqr_pipeline* p, double* t) {
     std::fill(t, t + 24, 0.0);
@@ -273,6 +285,12 @@ int spqr_pipeline_apply(spqr_pipeline* p, int mode, double* z) {
     int cl = -1;
     return guarded(nullptr, 0, &cl, [&] {
         CK(cudaSetDevice(p->device));
+        if (mode == SPQR_Q_APPLY_T || mode == SPQR_Q_APPLY) {
+            if (!p->has_f) throw std::logic_error("no factorization");
+            q_sweep(p->F, p->qs, mode, z, p->st);
+            return;
+        }
+        if (mode < 0 || mode > 3) throw std::invalid_argument("unknown apply mode");
         const int n = p->Aw.n;
         CK(cudaMemcpyAsync(p->d_u, z, sizeof(double) * n, cudaMemcpyHostToDevice, p->st));
         static const SweepMode map[4] = {kWApply, kWSolve, kWtApply, kWtSolve};

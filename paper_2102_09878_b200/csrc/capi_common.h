@@ -15,6 +15,7 @@
 
 #include "../../include/spaqr_b200.h"
 #include "engine.h"
+#include "solve.h"
 
 namespace spqr {
 
@@ -85,19 +86,51 @@ inline FactorizeObserver make_observer(spqr_observer_fn fn, void* user) {
     };
 }
 
+// Factorization::q_apply_t / q_apply (transforms.cpp:113-127) on a host vector of length M:
+// the RowReflects (store_q) are rotations on row ids, so they run through the W-sweep level
+// schedules (solve.cpp) with z of length M — q_apply_t as the forward walk applying H^T
+// (wt_solve's rotation step), q_apply as the backward walk applying H (w_solve's).
+struct QSweep {
+    DeviceFactorization view;  // W = the Q factors, idx = their row ids, N = M
+    SolvePlan plan;
+    bool built = false;
+    double* d_y = nullptr;
+    std::unique_ptr<DeviceArena> mem;
+};
+inline void q_sweep(const DeviceFactorization& F, QSweep& qs, int mode, double* y, cudaStream_t st) {
+    if (!F.has_q) throw std::logic_error("the factorization holds no Q (store_q was not set)");
+    if (!qs.built) {
+        qs.view.M = qs.view.N = F.M;
+        qs.view.W = F.Q;
+        qs.view.idx = F.qidx;
+        qs.plan = build_solve_plan(qs.view, st);
+        qs.mem = std::make_unique<DeviceArena>(sizeof(double) * std::max<size_t>(F.M, 1) + 4096);
+        qs.d_y = qs.mem->alloc_n<double>(std::max<size_t>(F.M, 1));
+        qs.built = true;
+    }
+    const SweepMode sm = mode == SPQR_Q_APPLY_T ? kWtSolve : kWSolve;
+    CK(cudaMemcpyAsync(qs.d_y, y, sizeof(double) * F.M, cudaMemcpyHostToDevice, st));
+    ensure_schedule(qs.plan, qs.view, sm, st);
+    sweep(qs.plan, sm, qs.d_y, st);
+    CK(cudaMemcpyAsync(y, qs.d_y, sizeof(double) * F.M, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+}
+
 // save_factorization (proj/src/transforms.cpp:206-240): SPQRFW01 file of a device W.
 inline void save_device_factorization(const DeviceFactorization& F, const char* path) {
     std::vector<std::pair<const char*, std::vector<char>>> mirror;
-    F.warena->for_each_chunk([&](const char* base, size_t used) {
+    auto grab = [&](const char* base, size_t used) {
         mirror.emplace_back(base, std::vector<char>(used));
         if (used) CK(cudaMemcpy(mirror.back().second.data(), base, used, cudaMemcpyDeviceToHost));
-    });
+    };
+    F.warena->for_each_chunk(grab);
+    if (F.has_q && F.qarena) F.qarena->for_each_chunk(grab);
     auto host = [&](const double* d) -> const double* {
         const char* c = reinterpret_cast<const char*>(d);
         for (const auto& m : mirror)
             if (c >= m.first && c < m.first + m.second.size())
                 return reinterpret_cast<const double*>(m.second.data() + (c - m.first));
-        throw std::logic_error("save_factorization: factor data outside the W arena");
+        throw std::logic_error("save_factorization: factor data outside the W / Q arenas");
     };
     std::FILE* f = std::fopen(path, "wb");
     if (!f) throw std::runtime_error(std::string("cannot open ") + path + " for writing");
@@ -121,6 +154,15 @@ inline void save_device_factorization(const DeviceFactorization& F, const char* 
     ivec(F.dropped_rows.data(), F.dropped_rows.size());
     ivec(F.trailing_rows.data(), F.trailing_rows.size());
     i64(static_cast<long long>(F.W.size()));
+    auto reflectors = [&](const DevWFactor& w) {  // put_reflectors: V c x k (unit diagonal explicit), tau, sign
+        i64(w.c);
+        i64(w.k);
+        f64s((w.c > 0 && w.k > 0) ? host(w.a) : nullptr, static_cast<size_t>(w.c) * w.k);
+        i64(w.k);
+        f64s(w.k ? host(w.tau) : nullptr, w.k);
+        i64(w.k);
+        f64s(w.k ? host(w.sign) : nullptr, w.k);
+    };
     for (const DevWFactor& w : F.W) {
         const int* cols = F.idx.data() + w.cols_off;
         if (w.kind == 0) {  // a = [R | C], c x (c + k), column-major
@@ -137,16 +179,17 @@ inline void save_device_factorization(const DeviceFactorization& F, const char* 
         } else {  // V c x k (unit diagonal explicit), tau k, sign k
             i64(1);
             ivec(cols, w.c);
-            i64(w.c);
-            i64(w.k);
-            f64s((w.c > 0 && w.k > 0) ? host(w.a) : nullptr, static_cast<size_t>(w.c) * w.k);
-            i64(w.k);
-            f64s(w.k ? host(w.tau) : nullptr, w.k);
-            i64(w.k);
-            f64s(w.k ? host(w.sign) : nullptr, w.k);
+            reflectors(w);
         }
     }
-    i64(0);  // has_q: the GPU engine does not store Q (store_q is a test-only option)
+    i64(F.has_q ? 1 : 0);  // transforms.cpp:230-237: Q as (rows, reflectors) per RowReflect
+    if (F.has_q) {
+        i64(static_cast<long long>(F.Q.size()));
+        for (const DevWFactor& q : F.Q) {
+            ivec(F.qidx.data() + q.cols_off, q.c);
+            reflectors(q);
+        }
+    }
     if (std::ferror(f)) throw std::runtime_error(std::string("write failed: ") + path);
 }
 

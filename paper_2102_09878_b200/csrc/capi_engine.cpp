@@ -25,6 +25,7 @@ struct spqr_factorization {
     cudaStream_t st = nullptr;
     DeviceFactorization F;
     SolvePlan plan;
+    QSweep qs;  // store_q: q_apply / q_apply_t
     std::unique_ptr<DeviceArena> mem;
     double* d_z = nullptr;
     double ev_factorize_ms = 0.0;
@@ -96,6 +97,16 @@ int spqr_factorize(int m, int n, const int* colptr, const int* rowind, const dou
                    const int* finest_of_col, int ntree, const int* tree_parent, int tree_root, const int* row_owner,
                    double eps, int skip_levels, int device, spqr_observer_fn obs, void* obs_user,
                    spqr_factorization** out, char* err, int errlen, int* err_cluster) {
+    return spqr_factorize_ex(m, n, colptr, rowind, vals, num_levels, nclusters, cluster_info, cluster_colptr,
+                             cluster_cols, finest_of_col, ntree, tree_parent, tree_root, row_owner, eps, skip_levels, 0,
+                             device, obs, obs_user, out, err, errlen, err_cluster);
+}
+
+int spqr_factorize_ex(int m, int n, const int* colptr, const int* rowind, const double* vals, int num_levels,
+                      int nclusters, const int* cluster_info, const int* cluster_colptr, const int* cluster_cols,
+                      const int* finest_of_col, int ntree, const int* tree_parent, int tree_root, const int* row_owner,
+                      double eps, int skip_levels, int store_q, int device, spqr_observer_fn obs, void* obs_user,
+                      spqr_factorization** out, char* err, int errlen, int* err_cluster) {
     *out = nullptr;
     spqr_factorization* H = nullptr;
     const int rc = capi_guarded(err, errlen, err_cluster, [&] {
@@ -143,6 +154,7 @@ int spqr_factorize(int m, int n, const int* colptr, const int* rowind, const dou
         FactorizeOptions fo;
         fo.eps = eps;
         fo.skip_levels = skip_levels;
+        fo.store_q = store_q != 0;
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
@@ -180,6 +192,10 @@ void spqr_factorization_info(const spqr_factorization* f, long long* o) {
     o[7] = static_cast<long long>(f->plan.sched[kWSolve].levels.size());
 }
 
+long long spqr_factorization_nq(const spqr_factorization* f) {
+    return f->F.has_q ? static_cast<long long>(f->F.Q.size()) : -1;
+}
+
 void spqr_factorization_rows(const spqr_factorization* f, int* pivot_row, int* dropped, int* trailing) {
     std::copy(f->F.pivot_row.begin(), f->F.pivot_row.end(), pivot_row);
     std::copy(f->F.dropped_rows.begin(), f->F.dropped_rows.end(), dropped);
@@ -206,8 +222,12 @@ int spqr_factorization_stage_fronts(const spqr_factorization* f, int s, int* fro
 int spqr_factorization_apply(spqr_factorization* f, int mode, double* z) {
     int cl = -1;
     return capi_guarded(nullptr, 0, &cl, [&] {
-        if (mode < 0 || mode > 3) throw std::invalid_argument("mode must be SPQR_W_APPLY..SPQR_WT_SOLVE");
         CK(cudaSetDevice(f->device));
+        if (mode == SPQR_Q_APPLY_T || mode == SPQR_Q_APPLY) {
+            q_sweep(f->F, f->qs, mode, z, f->st);
+            return;
+        }
+        if (mode < 0 || mode > 3) throw std::invalid_argument("mode must be SPQR_W_APPLY..SPQR_Q_APPLY");
         const Index n = f->F.N;
         CK(cudaMemcpyAsync(f->d_z, z, sizeof(double) * n, cudaMemcpyHostToDevice, f->st));
         static const SweepMode map[4] = {kWApply, kWSolve, kWtApply, kWtSolve};
@@ -327,20 +347,50 @@ int spqr_factorization_load(const char* path, int device, spqr_factorization** o
             if (stage.size() > (size_t(32) << 20)) flush();
         }
         flush();
-        // Q (has_q): read and dropped — the GPU path keeps no row factors
-        if (r.i64() != 0) {
+        // Q (has_q, transforms.cpp:277-286): RowReflects kept on the device for q_apply(_t)
+        F.has_q = r.i64() != 0;
+        if (F.has_q) {
+            F.qarena = std::make_unique<DeviceArena>(size_t(64) << 20);
             const int64_t nq = r.size();
+            auto qput = [&](size_t n) -> double* {
+                double* d = F.qarena->alloc_n<double>(std::max<size_t>(n, 1));
+                pending.emplace_back(d, stage.size());
+                return d;
+            };
             for (int64_t q = 0; q < nq; ++q) {
-                r.ivec();
-                int64_t a, b;
-                r.mat(a, b);
+                const std::vector<int> rows = r.ivec();
+                int64_t vr, vc;
+                const std::vector<double> V = r.mat(vr, vc);
                 const int64_t nt = r.size();
-                std::vector<double> t(static_cast<size_t>(nt));
-                r.f64s(t.data(), t.size());
+                std::vector<double> tau(static_cast<size_t>(nt));
+                r.f64s(tau.data(), tau.size());
                 const int64_t ns = r.size();
-                t.resize(static_cast<size_t>(ns));
-                r.f64s(t.data(), t.size());
+                std::vector<double> sg(static_cast<size_t>(ns));
+                r.f64s(sg.data(), sg.size());
+                const int c = static_cast<int>(rows.size());
+                if (vr != c || nt != vc || ns != vc) throw std::runtime_error(std::string(path) + ": inconsistent RowReflect");
+                for (int x : rows)
+                    if (x < 0 || x >= F.M) throw std::runtime_error(std::string(path) + ": row out of range");
+                DevWFactor w;
+                w.kind = 1;
+                w.c = c;
+                w.k = static_cast<int>(vc);
+                w.cols_off = static_cast<long long>(F.qidx.size());
+                F.qidx.insert(F.qidx.end(), rows.begin(), rows.end());
+                w.coupled_off = static_cast<long long>(F.qidx.size());
+                w.a = qput(V.size());
+                stage.insert(stage.end(), V.begin(), V.end());
+                if (V.empty()) stage.push_back(0.0);
+                w.tau = qput(tau.size());
+                stage.insert(stage.end(), tau.begin(), tau.end());
+                if (tau.empty()) stage.push_back(0.0);
+                w.sign = qput(sg.size());
+                stage.insert(stage.end(), sg.begin(), sg.end());
+                if (sg.empty()) stage.push_back(0.0);
+                F.Q.push_back(w);
+                if (stage.size() > (size_t(32) << 20)) flush();
             }
+            flush();
         }
         finish_handle(H);
     });

@@ -163,6 +163,14 @@ void launch_qr_split(const QrDesc* d_desc, const int* d_small, int n_small, size
 void launch_cpqr_split(const CpqrDesc* d_desc, const int* d_small, int n_small, size_t smem_small, const int* d_large,
                        int n_large, int max_m_large, cudaStream_t st);
 void launch_trsm(const TrsmDesc* d, int nd, long long total_rows, cudaStream_t st);
+// store_q: reflectors of an in-place QR copied out (unit diagonal), then the block restored
+enum { VCOPY_ZERO_LOWER = 1, VCOPY_SET_IDENTITY = 2 };
+struct VCopyDesc {
+    double* src;
+    int lds, m, n, mode;
+    double* dst;  // m x n, ld m
+};
+void launch_vcopy(const VCopyDesc* d, int nd, cudaStream_t st);
 void launch_scatter_values(const long long* off, const double* val, long long n, double* base, cudaStream_t st);
 
 // W-sweep kernels (solve) ------------------------------------------------------

@@ -270,9 +270,11 @@ struct Elim {
     std::vector<std::pair<int, int>> dest;  // move_extras: (target, local row), ascending target
     std::vector<int> trail;                 // move_extras: rows to the trailing set
     int color = 0;
+    double cmax2 = 0.0;  // largest squared row norm of the c blocks (move_extras noise floor scale)
     void reset(int c_, int cs_) {
         c = c_;
         cs = cs_;
+        cmax2 = 0.0;
         hadd.clear();
         err.clear();
         logic = false;
@@ -530,6 +532,8 @@ public:
         out_.eps = opt.eps;
         out_.pivot_row.assign(A.n, -1);
         out_.warena = std::make_unique<DeviceArena>(size_t(128) << 20);
+        out_.has_q = opt.store_q;
+        if (opt.store_q) out_.qarena = std::make_unique<DeviceArena>(size_t(64) << 20);
         const size_t nc = h.clusters.size();
         fr_.resize(nc);
         cols_.resize(nc);
@@ -655,8 +659,106 @@ private:
             std::fclose(f);
         }
     }
+    // SPQR_DIGEST=<path> (parity diagnostics, tools/phase_digest.py): after every stage-level
+    // phase, one record per live front: cluster, #rows, #keys, a polynomial hash of its row ids,
+    // of its (key, width) list and — with SPQR_DIGEST_VALUES=1 — of its significance pattern
+    // (row-key blocks whose squared norm exceeds 1e-20 x the front's largest).  The oracle writes
+    // the same records (ORC_DIGEST, oracle/orc_capi.cpp), so the first diverging phase and front
+    // can be found without moving whole states.
+    void digest(int phase_id) {
+        static const char* path = std::getenv("SPQR_DIGEST");
+        if (!path) return;
+        static const bool values = std::getenv("SPQR_DIGEST_VALUES") != nullptr;
+        CK(cudaStreamSynchronize(st_));
+        auto mix = [](uint64_t h, uint64_t x) { return h * 1000003ull + x + 1; };
+        std::vector<int> rec;
+        std::vector<uint64_t> hs;
+        std::vector<double> buf;
+        for (size_t c = 0; c < fr_.size(); ++c) {
+            if (!alive_[c] || !fr_[c].live) continue;
+            const Front& F = fr_[c];
+            uint64_t hr = 0, hk = 0, hv = 0;
+            for (int r : F.rows) hr = mix(hr, static_cast<uint64_t>(r));
+            for (const KeyRef& k : F.keys) hk = mix(mix(hk, static_cast<uint64_t>(k.key)), static_cast<uint64_t>(k.width));
+            if (values && F.nrows() > 0 && F.ncols > 0 && F.mat) {
+                buf.resize(static_cast<size_t>(F.ld) * F.ncols);
+                CK(cudaMemcpy(buf.data(), F.mat, sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
+                std::vector<double> nq(static_cast<size_t>(F.nrows()) * F.keys.size(), 0.0);
+                double mx = 0;
+                for (int r = 0; r < F.nrows(); ++r)
+                    for (size_t q = 0; q < F.keys.size(); ++q) {
+                        double s = 0;
+                        for (int j = 0; j < F.keys[q].width; ++j) {
+                            const double x = buf[static_cast<size_t>(F.keys[q].col + j) * F.ld + r];
+                            s += x * x;
+                        }
+                        nq[r * F.keys.size() + q] = s;
+                        mx = std::max(mx, s);
+                    }
+                for (double s : nq) hv = mix(hv, s > 1e-20 * mx ? 1u : 0u);
+            }
+            rec.push_back(static_cast<int>(c));
+            rec.push_back(F.nrows());
+            rec.push_back(static_cast<int>(F.keys.size()));
+            hs.push_back(hr);
+            hs.push_back(hk);
+            hs.push_back(hv);
+        }
+        // SPQR_DUMP_FRONTS=<c1,c2,...>: those fronts in full (rows, keys, per-row per-key squared
+        // norms) as text (<path>.fronts.txt), the same lines the oracle writes
+        static std::vector<int> dumpc = [] {
+            std::vector<int> v;
+            if (const char* e = std::getenv("SPQR_DUMP_FRONTS"))
+                for (const char* q = e; *q;) {
+                    v.push_back(std::atoi(q));
+                    while (*q && *q != ',') ++q;
+                    if (*q == ',') ++q;
+                }
+            return v;
+        }();
+        if (!dumpc.empty())
+            if (std::FILE* fp = std::fopen((std::string(path) + ".fronts.txt").c_str(), "a")) {
+                for (int c : dumpc) {
+                    if (c < 0 || static_cast<size_t>(c) >= fr_.size() || !alive_[c] || !fr_[c].live) continue;
+                    const Front& F = fr_[c];
+                    std::fprintf(fp, "phase %d stage %d front %d rows %zu keys", phase_id, cur_stage_, c, F.rows.size());
+                    for (const KeyRef& k : F.keys) std::fprintf(fp, " %d:%d", k.key, k.width);
+                    std::fprintf(fp, "\n");
+                    buf.assign(static_cast<size_t>(F.ld) * std::max(F.ncols, 0), 0.0);
+                    if (!buf.empty() && F.mat)
+                        CK(cudaMemcpy(buf.data(), F.mat, sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
+                    for (int r = 0; r < F.nrows(); ++r) {
+                        std::fprintf(fp, "  row %d", F.rows[r]);
+                        for (const KeyRef& k : F.keys) {
+                            double s = 0;
+                            for (int j = 0; j < k.width; ++j) {
+                                const double x = buf[static_cast<size_t>(k.col + j) * F.ld + r];
+                                s += x * x;
+                            }
+                            std::fprintf(fp, " %.6e", s);
+                        }
+                        std::fprintf(fp, "\n");
+                    }
+                }
+                std::fclose(fp);
+            }
+        static bool first = true;
+        if (std::FILE* f = std::fopen(path, first ? "wb" : "ab")) {
+            const int head[3] = {phase_id, cur_stage_, static_cast<int>(hs.size() / 3)};
+            std::fwrite(head, 4, 3, f);
+            std::fwrite(rec.data(), 4, rec.size(), f);
+            std::fwrite(hs.data(), 8, hs.size(), f);
+            std::fclose(f);
+        }
+        first = false;
+    }
     // factorize.cpp:86-95: the state after a phase, downloaded for the observer (tests only)
     void notify(const char* phase, int detail, const std::vector<int>* wave = nullptr) {
+        if (phase[0] != 'e' || wave == nullptr) {
+            static const char* names[5] = {"eliminate", "scale", "sparsify_rows", "sparsify_cols", "merge"};
+            for (int i = 1; i < 5; ++i)
+                if (std::string(phase) == names[i]) digest(i);
+        }
         if (!obs_ || !*obs_) return;
         CK(cudaStreamSynchronize(st_));
         static const bool structure_only = std::getenv("SPQR_OBSERVE_STRUCTURE_ONLY") != nullptr;
@@ -957,7 +1059,8 @@ private:
             const QrDesc& q = qd[i];
             cudaEvent_t e0 = kt_.begin(st_);
             double* scratch = arena().alloc_n<double>(2 * static_cast<size_t>(q.n) + 32 * 32);
-            blocked_qr_apply(1, q.m, q.n, q.ntot, q.a, scratch, scratch + q.n, q.flag, scratch + 2 * q.n, st_, q.ld);
+            blocked_qr_apply(1, q.m, q.n, q.ntot, q.a, q.tau ? q.tau : scratch, q.sign ? q.sign : scratch + q.n, q.flag,
+                             scratch + 2 * q.n, st_, q.ld);
             blocked_qr_post(q.a, q.ld, q.m, q.n, q.rout, q.set_identity, q.zero_lower, st_);
             kt_.end(K_QR, e0, st_, 16.0 * q.m * q.ntot);
         }
@@ -1198,6 +1301,7 @@ private:
     std::vector<unsigned char> rv_nz_;
     std::vector<std::vector<int>> sel_;
     std::vector<int> scr_cand_, scr_best_, scr_keyset_, scr_spos_;
+    std::vector<int> qrows_scratch_;
     std::vector<double> scr_bw_;
     std::vector<std::pair<int, int>> scr_dest_;
     std::vector<PRow> scr_rows_;
@@ -1215,6 +1319,25 @@ private:
         if (coupled) out_.idx.insert(out_.idx.end(), coupled->begin(), coupled->end());
         out_.W.push_back(f);
         return out_.W.back();
+    }
+    // store_q: one RowReflect (transforms.h:34-37) on `rows` with k reflectors; storage for V
+    // (rows x k), tau and sign from the Q arena unless the caller shares a W rotation's
+    DevWFactor& new_qfactor(int cluster, const int* rows, int nrows, int k, bool alloc = true) {
+        DevWFactor f;
+        f.kind = 1;
+        f.cluster = cluster;
+        f.c = nrows;
+        f.k = k;
+        f.cols_off = static_cast<long long>(out_.qidx.size());
+        out_.qidx.insert(out_.qidx.end(), rows, rows + nrows);
+        f.coupled_off = static_cast<long long>(out_.qidx.size());
+        if (alloc) {
+            f.a = out_.qarena->alloc_n<double>(std::max<size_t>(static_cast<size_t>(nrows) * k, 1));
+            f.tau = out_.qarena->alloc_n<double>(std::max(k, 1));
+            f.sign = out_.qarena->alloc_n<double>(std::max(k, 1));
+        }
+        out_.Q.push_back(f);
+        return out_.Q.back();
     }
 };
 
@@ -1368,6 +1491,7 @@ void Engine::elim_pass1(Elim& e, Scratch& S) {
         for (size_t q = S.rv_off[pi]; q < S.rv_off[pi + 1]; ++q) mx = std::max(mx, S.rv_sq[q]);
     }
     const double tau2 = eps > 0.0 ? mx * eps * eps * 1e-4 : 0.0;
+    e.cmax2 = mx;
     if (S.sel.size() < np) S.sel.resize(np);
     auto& sel = S.sel;
     int total = 0;
@@ -1494,13 +1618,18 @@ void Engine::elim_prep2(Elim& e, Scratch& S) {
     S.best.assign(nr, -1);
     S.rv_sq.resize(nr);
     S.rv_nz.resize(nr);
+    // roundoff rule shared with the oracle (spqr.h kMoveNoise2): candidate norms at the noise
+    // floor of the elimination count as exact zeros
+    const double noise2 = kMoveNoise2 * e.cmax2;
     for (int m : cand) {  // strict > in candidate order == the reference's per-row loop
         row_vals(fc, c, m, S.rv_sq.data(), S.rv_nz.data(), true);
-        for (size_t q = 0; q < nr; ++q)
-            if (S.rv_sq[q] > S.bw[q]) {
-                S.bw[q] = S.rv_sq[q];
+        for (size_t q = 0; q < nr; ++q) {
+            const double w = S.rv_sq[q] <= noise2 ? 0.0 : S.rv_sq[q];
+            if (w > S.bw[q]) {
+                S.bw[q] = w;
                 S.best[q] = m;
             }
+        }
     }
     int anc = -2;
     for (size_t q = 0; q < nr; ++q) {
@@ -1858,7 +1987,7 @@ void Engine::eliminate_stage(int k) {
     out_.ctr.elim_waves += nw;
     waves_per_stage_.push_back(nw);
     sprof_.back().waves = nw;
-    const size_t w0 = out_.W.size();
+    const size_t w0 = out_.W.size(), q0 = out_.Q.size();
     for (int w = 0; w < nw; ++w) {
         if (w > 0) compute_stats(stage_fronts(waves[w]));
         batch_ = out_.nbatches++;  // a wave's factors touch independent column sets
@@ -1868,6 +1997,8 @@ void Engine::eliminate_stage(int k) {
     // W in the reference's chronological order (ascending cluster); the solve
     // plan regroups by batch, which only reorders independent factors
     std::stable_sort(out_.W.begin() + w0, out_.W.end(),
+                     [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
+    std::stable_sort(out_.Q.begin() + q0, out_.Q.end(),
                      [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
 }
 
@@ -1951,6 +2082,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
     AsmBuilder& sb = asm_slot(0);  // keeps its capacity across calls
     std::vector<QrDesc> qd;
     std::vector<StatDesc> pd;
+    std::vector<VCopyDesc> vq;  // store_q
     long long pwork = 0, postlen = 0;
     std::vector<int> flags_init;
     // stack descriptors in three phases: source fronts per elimination
@@ -1989,6 +2121,16 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         edi[ei] = sb.begin(e.S, e.total_rows, e.total_rows, e.tcols, nsrc, static_cast<int>(e.keys.size()), false);
         flags_init.push_back(INT_MAX);
         QrDesc q{e.S, e.total_rows, e.total_rows, e.cs, e.tcols, nullptr, nullptr, nullptr, nullptr, 0, 1};
+        if (opt_.store_q) {  // factorize.cpp:324-330: H of the stack on its rows, parts order
+            std::vector<int>& rws = qrows_scratch_;
+            rws.resize(e.total_rows);
+            for (int i = 0; i < e.total_rows; ++i) rws[i] = e.srows[i].gid;
+            DevWFactor& qf = new_qfactor(e.c, rws.data(), e.total_rows, e.cs);
+            q.tau = qf.tau;
+            q.sign = qf.sign;
+            q.zero_lower = 0;
+            vq.push_back(VCopyDesc{e.S, e.total_rows, e.total_rows, e.cs, VCOPY_ZERO_LOWER, qf.a});
+        }
         qd.push_back(q);
         out_.ctr.qr_flops += 2.0 * e.total_rows * double(e.cs) * e.cs - 2.0 / 3.0 * double(e.cs) * e.cs * e.cs +
                              (4.0 * e.total_rows * e.cs - 2.0 * e.cs * double(e.cs)) * (e.tcols - e.cs);
@@ -2062,6 +2204,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         run_qr(qd, dq, u);
         out_.ctr.launches++;
         out_.ctr.qr_launches++;
+        if (!vq.empty()) launch_vcopy(u.put(vq), static_cast<int>(vq.size()), st_);
         double sb = 0;
         for (auto& q : pd) sb += 8.0 * q.nrows * q.ncols + 9.0;
         cudaEvent_t e0 = kt_.begin(st_);
@@ -2153,6 +2296,7 @@ void Engine::scale_all() {
     download(ident, d_nz, cand.size());
     std::vector<QrDesc> qd;
     std::vector<TrsmDesc> td;
+    std::vector<VCopyDesc> vq;  // store_q
     std::vector<int> qp;
     long long trows = 0;
     for (size_t i = 0; i < cand.size(); ++i) {
@@ -2166,6 +2310,13 @@ void Engine::scale_all() {
         DevWFactor& w = new_factor(0, p, cs, 0, cols_[p], nullptr);
         w.a = out_.warena->alloc_n<double>(static_cast<size_t>(cs) * cs);
         qd.push_back(QrDesc{f.mat, f.ld, f.nrows(), cs, f.ncols, nullptr, nullptr, w.a, nullptr, 1, 0});
+        if (opt_.store_q) {  // factorize.cpp:483: U on all of p's rows
+            DevWFactor& qf = new_qfactor(p, f.rows.data(), f.nrows(), cs);
+            qd.back().tau = qf.tau;
+            qd.back().sign = qf.sign;
+            qd.back().set_identity = 0;
+            vq.push_back(VCopyDesc{f.mat, f.ld, f.nrows(), cs, VCOPY_SET_IDENTITY, qf.a});
+        }
         qp.push_back(p);
         out_.ctr.qr_flops += 2.0 * f.nrows() * double(cs) * cs - 2.0 / 3.0 * double(cs) * cs * cs +
                              (4.0 * f.nrows() * cs - 2.0 * cs * double(cs)) * (f.ncols - cs);
@@ -2195,6 +2346,7 @@ void Engine::scale_all() {
         run_qr(qd, dq, u);
         out_.ctr.launches++;
         out_.ctr.qr_launches++;
+        if (!vq.empty()) launch_vcopy(u.put(vq), static_cast<int>(vq.size()), st_);
         cudaEvent_t e0 = kt_.begin(st_);
         launch_trsm(dt, static_cast<int>(td.size()), trows, st_);
         kt_.end(K_TRSM, e0, st_, tb);
@@ -2276,11 +2428,19 @@ void Engine::sparsify_rows_all() {
     const size_t nj = jobs.size();
     int* d_rank = arena().alloc_n<int>(nj);
     double* d_r11 = arena().alloc_n<double>(nj);
+    std::vector<double*> qv(opt_.store_q ? nj * 3 : 0);  // store_q: T.H of every job (V, tau, sign)
     for (size_t i = 0; i < nj; ++i) {
         const Job& j = jobs[i];
         double* work = arena().alloc_n<double>(3 * static_cast<size_t>(j.nw));
         cd.push_back(CpqrDesc{j.B, j.p2, j.p2, j.nw, opt_.eps, d_rank + i, d_r11 + i, nullptr, 0, nullptr, nullptr,
                               nullptr, work});
+        if (opt_.store_q) {
+            const int kmax = std::max(1, std::min(j.p2, j.nw));
+            qv[3 * i] = cd.back().V = out_.qarena->alloc_n<double>(static_cast<size_t>(j.p2) * kmax);
+            cd.back().ldv = j.p2;
+            qv[3 * i + 1] = cd.back().tau = out_.qarena->alloc_n<double>(kmax);
+            qv[3 * i + 2] = cd.back().sign = out_.qarena->alloc_n<double>(kmax);
+        }
     }
     {
         Uploader u = up();
@@ -2300,6 +2460,12 @@ void Engine::sparsify_rows_all() {
         out_.ctr.k_bytes[K_CPQR] += 8.0 * keep * j.nw;
         if (keep >= j.p2) continue;
         Front& f = fr_[j.p];
+        if (opt_.store_q) {  // factorize.cpp:514-519: T.H on the extra rows
+            DevWFactor& qf = new_qfactor(j.p, f.rows.data() + j.cs, j.p2, keep, false);
+            qf.a = qv[3 * i];
+            qf.tau = qv[3 * i + 1];
+            qf.sign = qv[3 * i + 2];
+        }
         for (int r = j.cs + keep; r < j.cs + j.p2; ++r) out_.dropped_rows.push_back(f.rows[r]);
         f.rows.resize(j.cs + keep);
         if (keep == 0) continue;
@@ -2358,7 +2524,7 @@ void Engine::sparsify_cols_all() {
     std::vector<int> pending = elig;
     int rounds = 0;
     const int rot_batch = batch_;
-    const size_t w0 = out_.W.size();
+    const size_t w0 = out_.W.size(), q0 = out_.Q.size();
     std::vector<int> depth(fr_.size(), -1);  // speculation depth of interfaces included in this round
     std::vector<char> done(fr_.size(), 0);
     const int kmax_depth = spec_depth_;
@@ -2533,6 +2699,12 @@ void Engine::sparsify_cols_all() {
                 w.a = j.V;
                 w.tau = j.tau;
                 w.sign = j.sign;
+                if (opt_.store_q) {  // factorize.cpp:583-588: the same T.H on p's first cs rows
+                    DevWFactor& qf = new_qfactor(p, f.rows.data(), j.cs, r2, false);
+                    qf.a = j.V;
+                    qf.tau = j.tau;
+                    qf.sign = j.sign;
+                }
             }
             for (size_t s = 0; s < j.rparts.size(); ++s) {
                 const int m = j.rparts[s];
@@ -2642,6 +2814,8 @@ void Engine::sparsify_cols_all() {
     }
     if (!sprof_.empty()) sprof_.back().scol_waves = rounds;
     std::stable_sort(out_.W.begin() + w0, out_.W.end(),
+                     [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
+    std::stable_sort(out_.Q.begin() + q0, out_.Q.end(),
                      [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
 }
 
@@ -2847,6 +3021,7 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         double t0 = now_s();
         eliminate_stage(k);
         st.t_eliminate = now_s() - t0;
+        digest(0);
         if (opt_.eps > 0.0 && k >= 2 && L_ + 1 - k >= opt_.skip_levels) {
             t0 = now_s();
             batch_ = out_.nbatches++;

@@ -55,6 +55,12 @@ struct DeviceFactorization {
     std::vector<Index> pivot_row, dropped_rows, trailing_rows;
     std::vector<StageStats> stages;
     std::unique_ptr<DeviceArena> warena;
+    // Q (store_q, transforms.h:34-37,57): RowReflect factors as rotations on row ids (kind 1,
+    // cols = rows, chronological); q_apply_t walks them forward, q_apply backward
+    bool has_q = false;
+    std::vector<DevWFactor> Q;
+    std::vector<int> qidx;
+    std::unique_ptr<DeviceArena> qarena;
     int nbatches = 0;
     EngineCounters ctr;
     long long nnz_w() const;

@@ -691,4 +691,27 @@ void launch_info_fixup(int* info, int n, cudaStream_t st) {
     if (n > 0) k_info_fixup<<<(n + 255) / 256, 256, 0, st>>>(info, n);
 }
 
+namespace {
+// store_q (factorize.cpp:324-330, :483, :514-519): copy the reflectors a QR left below the
+// diagonal of src(:, :n) into dst (m x n, ld m, explicit unit diagonal, zeros above — the
+// layout the rotation sweeps read), then restore what the non-store_q launch would have left:
+// the lower part cleared (VCOPY_ZERO_LOWER) or the block set to [I; 0] (VCOPY_SET_IDENTITY).
+// One CTA per block; each element is read, copied and rewritten by one thread.
+__global__ void k_vcopy(const VCopyDesc* __restrict__ ds) {
+    const VCopyDesc d = ds[blockIdx.x];
+    const long long total = static_cast<long long>(d.m) * d.n;
+    for (long long e = threadIdx.x; e < total; e += blockDim.x) {
+        const int j = static_cast<int>(e / d.m), i = static_cast<int>(e - static_cast<long long>(j) * d.m);
+        double* sp = d.src + static_cast<long long>(j) * d.lds + i;
+        d.dst[static_cast<long long>(j) * d.m + i] = i > j ? *sp : (i == j ? 1.0 : 0.0);
+        if ((d.mode & VCOPY_ZERO_LOWER) && i > j) *sp = 0.0;
+        if (d.mode & VCOPY_SET_IDENTITY) *sp = (i == j) ? 1.0 : 0.0;
+    }
+}
+}  // namespace
+
+void launch_vcopy(const VCopyDesc* d, int nd, cudaStream_t st) {
+    if (nd > 0) k_vcopy<<<nd, 256, 0, st>>>(d);
+}
+
 }  // namespace spqr

@@ -16,6 +16,11 @@
 
 namespace spqr {
 
+// move_extras roundoff rule (factorize.cpp:141-164): candidate squared row norms at
+// or below kMoveNoise2 x (largest squared row norm of the eliminated cluster's blocks) count as 0.
+constexpr double kMoveNoise2 = (1e3 * 2.220446049250313e-16) * (1e3 * 2.220446049250313e-16);
+
+
 using Index = int;  // proj/include/spaqr/types.h:11
 
 struct SingularFrontError : std::runtime_error {  // types.h:24-31
@@ -80,7 +85,11 @@ struct RowMatching { std::vector<Index> row_of_col, col_of_row; Index size = 0; 
 RowMatching match_rows(const Csc& A);                                                // :401-463
 std::vector<int> assign_rows(const Csc& A, const ClusterHierarchy& h, const RowMatching& m);  // :465-514
 
-struct FactorizeOptions { double eps = 1e-2; int skip_levels = 3; };  // factorize.h:13-17 (store_q: not on the GPU path)
+struct FactorizeOptions {  // factorize.h:13-17
+    double eps = 1e-2;
+    int skip_levels = 3;
+    bool store_q = false;  // keep the orthogonal row factors Q (tests, diagnostics)
+};
 
 struct StageStats {  // transforms.h:40-47 (+ per-phase device-side timings)
     int stage = 0;

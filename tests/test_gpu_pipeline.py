@@ -228,13 +228,10 @@ def test_config3_full_size_matches_oracle():
 
 @pytest.mark.timeout(900)
 def test_config4_full_size_matches_oracle():
-    """BASELINE config 4 (kNN, N=2^20, L=16) at full size.  Every row decision (pivot, dropped,
-    trailing rows), the ordering, ownership, iterations and residual are identical; one interface
-    (stage 12 cluster 625282, and the same interface after each merge) is one column narrower on
-    the GPU: its sparsify_cols input differs by one holder row's coupling (1.8 % of |R11|), i.e. an
-    upstream row-selection floor decided within roundoff of its threshold, not a CPQR tie
-    (profiles/r02_c4_parity.txt).  The test allows that one interface per stage and no more."""
-    _fingerprint_check("c4", max_width_diffs=1)
+    """BASELINE config 4 (kNN, N=2^20, L=16) at full size: identical structure — ordering, ownership,
+    every row decision, every stage's interface widths, nW, nnz(W), iterations and residual (with
+    the move_extras roundoff rule shared by the oracle and the engine)."""
+    _fingerprint_check("c4")
 
 
 @pytest.mark.skipif(not R.available(), reason="reference build (oracle/_ref) unavailable")
