@@ -65,3 +65,18 @@ for nm, c in self_c.most_common(30):
 print("--- inclusive")
 for nm, c in incl.most_common(40):
     print(f"{100*c/n:6.1f}%  {nm}")
+# SAMPLE_FOCUS=<substring>: for samples whose leaf frames (first 6) match it, the nearest
+# libspaqr_b200.so frame — which engine code pays for it
+focus = os.environ.get("SAMPLE_FOCUS")
+if focus:
+    by = collections.Counter()
+    for st in stacks:
+        nm0 = [names.get(off, obj.split("/")[-1]) if obj.endswith("libspaqr_b200.so") else dyn_name(obj, off)
+               for obj, off in st]
+        if not any(focus in x for x in nm0[:6]):
+            continue
+        own = [x for (obj, _), x in zip(st, nm0) if obj.endswith("libspaqr_b200.so")]
+        by[" < ".join(own[:3]) if own else "?"] += 1
+    print(f"--- '{focus}' by engine caller")
+    for nm, c in by.most_common(25):
+        print(f"{100*c/n:6.1f}%  {nm}")
