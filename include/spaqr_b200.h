@@ -83,11 +83,26 @@ int spqr_pipeline_create_observed(int m, int n, const int* colptr, const int* ro
  * (transforms.h:34-37,57) for SPQR_Q_APPLY_T / SPQR_Q_APPLY. */
 int spqr_pipeline_create_ex(int m, int n, const int* colptr, const int* rowind, const double* vals,
                             const double* coords, int dim, const int* parts, int levels, double eps, int skip_levels,
-                            int solver, int store_q, int device, spqr_observer_fn obs, void* obs_user,
+                            int solver, int store_q, int ranks, int device, spqr_observer_fn obs, void* obs_user,
                             spqr_pipeline** out, char* err, int errlen, int* err_cluster);
 void spqr_pipeline_destroy(spqr_pipeline* p);
 /* |Q| (number of RowReflect factors), or -1 when the factorization keeps no Q. */
 long long spqr_pipeline_nq(const spqr_pipeline* p);
+
+/* ---- subtree split across GPUs ------------------------------ */
+/* The ownership of a G = 2^g GPU split, on the host only: the pipeline's partition of A
+ * (pipeline.cpp:36-53), then the owner rank of every cluster — the subtree below the top g
+ * separator levels holding its tree node; top-g separator pieces at granularity k > g go to the
+ * lowest subtree they border, coarser pieces to rank 0.  Call with NULL arrays to get
+ * *nclusters / *ntree first.  No GPU needed. */
+int spqr_rank_plan(int m, int n, const int* colptr, const int* rowind, const double* vals, const double* coords,
+                   int dim, const int* parts, int levels, int nranks, int* nclusters, int* ntree, int* owner,
+                   int* cluster_node, int* cluster_level, int* tree_parent, int* tree_level, char* err, int errlen);
+/* A pipeline created with ranks = G > 1 accounted, per stage, the flops each rank would own
+ * (flops[stage * G + rank]) and the bytes crossing ranks by phase (cross[stage * 4 + phase]:
+ * stack rows, R to holders, sparsify_cols holder blocks, merges).  Returns G (0 when not
+ * accounted); *nstages stages; owner (nclusters) optional. */
+int spqr_pipeline_rank_stats(const spqr_pipeline* p, int* nstages, double* flops, double* cross, int* owner);
 
 /* info[16]: M, N, L, nclusters, nW, n_dropped, n_trailing, n_stages, nnz_w, nnz(A), W sweep levels,
  *           engine launches, engine syncs, h2d bytes, d2h bytes, solve-plan launches per sweep pair */

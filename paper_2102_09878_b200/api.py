@@ -92,7 +92,7 @@ class Pipeline:
     fn(phase, stage, detail, view) called after every engine phase (pipeline.h:39-41)."""
 
     def __init__(self, A, eps=1e-2, levels=0, skip_levels=3, solver="spaqr", coords=None, parts=None, device=0,
-                 observer=None, store_q=False):
+                 observer=None, store_q=False, ranks=1):
         require_gpu()
         L = lib()
         m, n, p, i, x = _csc(A)
@@ -108,7 +108,7 @@ class Pipeline:
         h = C.c_void_p()
         cb = _observer(observer)
         rc = L.spqr_pipeline_create_ex(m, n, p, i, x, _ptr(cp), dim, _ptr(pp), int(levels), float(eps),
-                                       int(skip_levels), SOLVERS[solver], int(bool(store_q)), int(device),
+                                       int(skip_levels), SOLVERS[solver], int(bool(store_q)), int(ranks), int(device),
                                        C.cast(cb, C.c_void_p) if cb else None, None, C.byref(h), err, 512,
                                        C.byref(cl))
         if rc != 0:
@@ -180,6 +180,22 @@ class Pipeline:
     def w_solve(self, z): return self._apply(1, z)
     def wt_apply(self, z): return self._apply(2, z)
     def wt_solve(self, z): return self._apply(3, z)
+
+    def rank_stats(self):
+        """Subtree-split accounting of a pipeline created with ranks=G > 1:
+        flops[stage, rank], cross[stage, phase] bytes (phases: stack rows, R to holders,
+        sparsify_cols holder blocks, merges), owner per cluster."""
+        L = lib()
+        ns = C.c_int()
+        G = L.spqr_pipeline_rank_stats(self.h, C.byref(ns), None, None, None)
+        if G <= 1:
+            return None
+        fl = np.zeros((ns.value, G))
+        cr = np.zeros((ns.value, 4))
+        ow = np.zeros(self.nclusters, np.int32)
+        L.spqr_pipeline_rank_stats(self.h, C.byref(ns), fl.ctypes.data_as(C.c_void_p), cr.ctypes.data_as(C.c_void_p),
+                                   ow.ctypes.data_as(C.c_void_p))
+        return dict(ranks=G, flops=fl, cross=cr, owner=ow)
 
     def perm(self):
         o = np.zeros(self.N, np.int32)
@@ -469,3 +485,27 @@ def cgls(A, W, b, tol=1e-12, maxit=500, weights=None, device=0):
         raise (ValueError if rc == 2 else RuntimeError)(err.value.decode())
     return u, dict(iterations=it.value, converged=bool(cv.value), residual_history=hist[: nh.value].copy(),
                    t_solve=ts.value)
+
+
+def rank_plan(A, nranks, levels=0, coords=None, parts=None):
+    """spqr_rank_plan (include/spaqr_b200.h): the owner rank of every cluster for an
+    nranks = 2^g GPU subtree split of the pipeline's partition of A (host only, no GPU)."""
+    L = lib()
+    m, n, p, i, x = _csc(A)
+    cp = None if coords is None else np.ascontiguousarray(coords, np.float64)
+    pp = None if parts is None else np.ascontiguousarray(parts, np.int32)
+    dim = 0 if cp is None else cp.shape[1]
+    ncl, nt = C.c_int(), C.c_int()
+    err = C.create_string_buffer(512)
+    args = (m, n, p, i, x, _ptr(cp), dim, _ptr(pp), int(levels), int(nranks), C.byref(ncl), C.byref(nt))
+    rc = L.spqr_rank_plan(*args, None, None, None, None, None, err, 512)
+    if rc:
+        raise (ValueError if rc == 2 else RuntimeError)(err.value.decode())
+    out = dict(owner=np.zeros(ncl.value, np.int32), cluster_node=np.zeros(ncl.value, np.int32),
+               cluster_level=np.zeros(ncl.value, np.int32), tree_parent=np.zeros(nt.value, np.int32),
+               tree_level=np.zeros(nt.value, np.int32))
+    rc = L.spqr_rank_plan(*args, *[out[k].ctypes.data_as(C.c_void_p) for k in ("owner", "cluster_node", "cluster_level",
+                                                                               "tree_parent", "tree_level")], err, 512)
+    if rc:
+        raise RuntimeError(err.value.decode())
+    return out

@@ -85,12 +85,12 @@ int spqr_pipeline_create_observed(int m, int n, const int* colptr, const int* ro
                                   int skip_levels, int solver, int device, spqr_observer_fn obs, void* obs_user,
                                   spqr_pipeline** out, char* err, int errlen, int* err_cluster) {
     return spqr_pipeline_create_ex(m, n, colptr, rowind, vals, coords, dim, parts, levels, eps, skip_levels, solver, 0,
-                                   device, obs, obs_user, out, err, errlen, err_cluster);
+                                   1, device, obs, obs_user, out, err, errlen, err_cluster);
 }
 
 int spqr_pipeline_create_ex(int m, int n, const int* colptr, const int* rowind, const double* vals,
                             const double* coords, int dim, const int* parts, int levels, double eps, int skip_levels,
-                            int solver, int store_q, int device, spqr_observer_fn obs, void* obs_user,
+                            int solver, int store_q, int ranks, int device, spqr_observer_fn obs, void* obs_user,
                             spqr_pipeline** out, char* err, int errlen, int* err_cluster) {
     *out = nullptr;
     auto* P = new spqr_pipeline;
@@ -148,6 +148,7 @@ int spqr_pipeline_create_ex(int m, int n, const int* colptr, const int* rowind, 
             fo.eps = P->eps;
             fo.skip_levels = skip_levels;
             fo.store_q = store_q != 0;
+            fo.ranks = std::max(1, ranks);
             cudaEvent_t e0, e1;
             CK(cudaEventCreate(&e0));
             CK(cudaEventCreate(&e1));
@@ -206,6 +207,49 @@ void spqr_pipeline_info(const spqr_pipeline* p, long long* o) {
 }
 
 long long spqr_pipeline_nq(const spqr_pipeline* p) { return p->F.has_q ? static_cast<long long>(p->F.Q.size()) : -1; }
+
+int spqr_pipeline_rank_stats(const spqr_pipeline* p, int* nstages, double* flops, double* cross, int* owner) {
+    const RankStats& r = p->F.rank;
+    if (r.ranks <= 1) return 0;
+    const int ns = static_cast<int>(std::max(r.flops.size(), r.cross.size()));
+    if (nstages) *nstages = ns;
+    for (int s = 0; s < ns; ++s) {
+        for (int q = 0; q < r.ranks; ++q)
+            if (flops) flops[s * r.ranks + q] = s < static_cast<int>(r.flops.size()) ? r.flops[s][q] : 0.0;
+        for (int q = 0; q < 4; ++q)
+            if (cross) cross[s * 4 + q] = s < static_cast<int>(r.cross.size()) ? r.cross[s][q] : 0.0;
+    }
+    if (owner) std::copy(r.owner.begin(), r.owner.end(), owner);
+    return r.ranks;
+}
+
+int spqr_rank_plan(int m, int n, const int* colptr, const int* rowind, const double* vals, const double* coords, int dim,
+                   const int* parts, int levels, int nranks, int* nclusters, int* ntree, int* owner, int* cluster_node,
+                   int* cluster_level, int* tree_parent, int* tree_level, char* err, int errlen) {
+    int cl = -1;
+    return guarded(err, errlen, &cl, [&] {
+        Csc A = csc_canonical(m, n, colptr, rowind, vals);
+        if (A.m < A.n) throw std::invalid_argument("matrix must have at least as many rows as columns");
+        scale_columns(A);
+        const Graph g = ata_graph(A);
+        const int L = levels > 0 ? levels : default_num_levels(n);
+        if (coords && dim <= 0) throw std::invalid_argument("coordinate dimension must be positive");
+        const SeparatorTree t = parts ? import_partition(g, L, parts) : nested_dissection(g, L, coords, dim);
+        ClusterHierarchy h = build_interfaces(t, g);
+        const std::vector<int> own = rank_owners(h, g, nranks);
+        if (nclusters) *nclusters = static_cast<int>(h.clusters.size());
+        if (ntree) *ntree = static_cast<int>(t.nodes.size());
+        for (size_t c = 0; c < h.clusters.size(); ++c) {
+            if (owner) owner[c] = own[c];
+            if (cluster_node) cluster_node[c] = h.clusters[c].tree_node;
+            if (cluster_level) cluster_level[c] = h.clusters[c].level;
+        }
+        for (size_t v = 0; v < t.nodes.size(); ++v) {
+            if (tree_parent) tree_parent[v] = t.nodes[v].parent;
+            if (tree_level) tree_level[v] = t.nodes[v].level;
+        }
+    });
+}
 
 void spqr_pipeline_times(const spqr_pipeline* p, double* t) {
     std::fill(t, t + 24, 0.0);

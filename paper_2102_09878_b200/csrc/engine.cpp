@@ -533,6 +533,10 @@ public:
         out_.pivot_row.assign(A.n, -1);
         out_.warena = std::make_unique<DeviceArena>(size_t(128) << 20);
         out_.has_q = opt.store_q;
+        if (opt.ranks > 1) {
+            out_.rank.ranks = opt.ranks;
+            out_.rank.owner = rank_owners(h, ata_graph(A), opt.ranks);
+        }
         if (opt.store_q) out_.qarena = std::make_unique<DeviceArena>(size_t(64) << 20);
         const size_t nc = h.clusters.size();
         fr_.resize(nc);
@@ -1339,6 +1343,21 @@ private:
         out_.Q.push_back(f);
         return out_.Q.back();
     }
+    // subtree-split accounting (opt.ranks > 1)
+    bool ranked() const { return out_.rank.ranks > 1; }
+    int own(int c) const { return out_.rank.owner[c]; }
+    void rank_flops(int c, double f) {
+        auto& v = out_.rank.flops;
+        const size_t s = out_.stages.size();
+        if (v.size() <= s) v.resize(s + 1, std::vector<double>(out_.rank.ranks, 0.0));
+        v[s][own(c)] += f;
+    }
+    void rank_cross(int phase, double bytes) {
+        auto& v = out_.rank.cross;
+        const size_t s = out_.stages.size();
+        if (v.size() <= s) v.resize(s + 1, std::vector<double>(4, 0.0));
+        v[s][phase] += bytes;
+    }
 };
 
 // factorize.cpp:32-82 — finest fronts, rows ascending into owners, one block
@@ -2135,6 +2154,13 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         out_.ctr.qr_flops += 2.0 * e.total_rows * double(e.cs) * e.cs - 2.0 / 3.0 * double(e.cs) * e.cs * e.cs +
                              (4.0 * e.total_rows * e.cs - 2.0 * e.cs * double(e.cs)) * (e.tcols - e.cs);
         out_.ctr.qr_bytes += 16.0 * e.total_rows * e.tcols;
+        if (ranked()) {  // rows gathered from (and written back to) fronts of other ranks
+            rank_flops(e.c, 2.0 * e.total_rows * double(e.cs) * e.cs - 2.0 / 3.0 * double(e.cs) * e.cs * e.cs +
+                                (4.0 * e.total_rows * e.cs - 2.0 * e.cs * double(e.cs)) * (e.tcols - e.cs));
+            long long remote = 0;
+            for (int i = 0; i < e.total_rows; ++i) remote += own(e.srows[i].base) != own(e.c);
+            rank_cross(0, 16.0 * remote * e.tcols);
+        }
         // post stats: [max over all neighbour cols][max per key][own non-pivot rows x keys]
         const long long nk = static_cast<long long>(e.keys.size()) - 1;
         e.post_off = postlen;
@@ -2321,12 +2347,16 @@ void Engine::scale_all() {
         out_.ctr.qr_flops += 2.0 * f.nrows() * double(cs) * cs - 2.0 / 3.0 * double(cs) * cs * cs +
                              (4.0 * f.nrows() * cs - 2.0 * cs * double(cs)) * (f.ncols - cs);
         out_.ctr.qr_bytes += 16.0 * f.nrows() * f.ncols;
+        if (ranked())
+            rank_flops(p, 2.0 * f.nrows() * double(cs) * cs - 2.0 / 3.0 * double(cs) * cs * cs +
+                              (4.0 * f.nrows() * cs - 2.0 * cs * double(cs)) * (f.ncols - cs));
         for (int m : holders_[p].get()) {
             if (m == p) continue;
             const Front& fm = fr_[m];
             const int mq = fm.find(p);
             if (fm.nrows() == 0) continue;
             td.push_back(TrsmDesc{fm.mat + static_cast<long long>(fm.keys[mq].col) * fm.ld, fm.ld, fm.nrows(), cs, w.a, cs, trows});
+            if (ranked() && own(m) != own(p)) rank_cross(1, 8.0 * cs * cs);
             trows += fm.nrows();
         }
         f.scaled_ok = true;
@@ -2456,6 +2486,7 @@ void Engine::sparsify_rows_all() {
         const Job& j = jobs[i];
         const int keep = rank[i];
         out_.ctr.cpqr_flops += 4.0 * j.p2 * double(j.nw) * keep + 2.0 * j.p2 * j.nw;
+        if (ranked()) rank_flops(j.p, 4.0 * j.p2 * double(j.nw) * keep + 2.0 * j.p2 * j.nw);
         out_.ctr.cpqr_bytes += 8.0 * keep * j.nw;  // R out (8mn + 8rn)
         out_.ctr.k_bytes[K_CPQR] += 8.0 * keep * j.nw;
         if (keep >= j.p2) continue;
@@ -2593,6 +2624,12 @@ void Engine::sparsify_cols_all() {
             j.nG = wrows + wcols;
             j.kmax = std::min(j.cs, j.nG);
         }
+        if (ranked())
+            for (const Job& j : jobs) {
+                rank_flops(j.p, 4.0 * j.cs * double(j.nG) * j.kmax + 2.0 * j.cs * j.nG);  // upper bound (rank <= kmax)
+                for (int m : j.rparts)
+                    if (own(m) != own(j.p)) rank_cross(2, 16.0 * fr_[m].nrows() * j.cs);
+            }
         for (Job& j : jobs) {
             j.G = dalloc(arena(), static_cast<size_t>(j.cs) * std::max(j.nG, 1), j.gbig);
             // G (cs x nG) built transposed: G column g <- a row of holder m or a column of own block;
@@ -2845,6 +2882,12 @@ void Engine::merge_level() {
         gstart.push_back(static_cast<int>(gkids.size()));
     }
     const int ng = static_cast<int>(gp.size());
+    if (ranked())
+        for (int g = 0; g < ng; ++g)
+            for (int t = gstart[g]; t < gstart[g + 1]; ++t) {
+                const Front& F = fr_[gkids[t]];
+                if (own(gkids[t]) != own(gp[g])) rank_cross(3, 8.0 * F.nrows() * F.ncols);
+            }
     std::vector<int> child_off(fr_.size(), -1);
     for (int g = 0; g < ng; ++g) {
         const int P = gp[g];

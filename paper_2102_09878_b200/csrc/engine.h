@@ -46,6 +46,19 @@ struct EngineCounters {
     long long route_launches[5] = {0};
 };
 
+// Subtree-split accounting (FactorizeOptions::ranks > 1): per stage, the
+// algorithmic flops of the work each rank would own (eliminations, scaling QR, CPQR) and
+// the bytes that would cross ranks, by phase: 0 stack gathers / scatter-backs of rows held by
+// another rank's front, 1 R_p shipped to holders on other ranks (scale_all's B_m R_p^-1),
+// 2 holder blocks gathered into G and written back (sparsify_cols), 3 fronts moved to a
+// parent owned by another rank (merge; the top levels gather onto rank 0).
+struct RankStats {
+    int ranks = 0;
+    std::vector<int> owner;                      // per cluster
+    std::vector<std::vector<double>> flops;      // [stage position][rank]
+    std::vector<std::vector<double>> cross;      // [stage position][phase]
+};
+
 // The outcome of spaqr_factorize (transforms.h:53-72) with W resident in HBM.
 struct DeviceFactorization {
     Index M = 0, N = 0;
@@ -63,6 +76,7 @@ struct DeviceFactorization {
     std::unique_ptr<DeviceArena> qarena;
     int nbatches = 0;
     EngineCounters ctr;
+    RankStats rank;
     long long nnz_w() const;
 };
 

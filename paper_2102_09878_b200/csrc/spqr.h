@@ -82,13 +82,16 @@ struct ClusterHierarchy {  // partition.h:54-75
 ClusterHierarchy build_interfaces(const SeparatorTree& t, const Graph& g);  // :231-346
 std::vector<Index> order_columns(ClusterHierarchy& h);                        // :348-399
 struct RowMatching { std::vector<Index> row_of_col, col_of_row; Index size = 0; };
-RowMatching match_rows(const Csc& A);                                                // :401-463
+RowMatching match_rows(const Csc& A);
+// owner rank of every cluster for a G = 2^g GPU subtree split (ranks.cpp)
+std::vector<int> rank_owners(const ClusterHierarchy& h, const Graph& g, int G);                                                // :401-463
 std::vector<int> assign_rows(const Csc& A, const ClusterHierarchy& h, const RowMatching& m);  // :465-514
 
 struct FactorizeOptions {  // factorize.h:13-17
     double eps = 1e-2;
     int skip_levels = 3;
     bool store_q = false;  // keep the orthogonal row factors Q (tests, diagnostics)
+    int ranks = 1;         // > 1: account work and cross-rank traffic of a ranks-GPU subtree split (ranks.cpp)
 };
 
 struct StageStats {  // transforms.h:40-47 (+ per-phase device-side timings)
