@@ -152,6 +152,32 @@ int main(int argc, char** argv) {
     Fg.w_solve(zr);
     Wr.w_solve(zg);
     check("factor_files", max_rel(zg, zr) <= 1e-10 && Fg.W.size() == F.W.size(), std::to_string(max_rel(zg, zr)));
+    // 4b. store_q (factorize.h:16): the reference's Q against the GPU's, both ways through files
+    {
+        FactorizeOptions fq = fo;
+        fq.store_q = true;
+        const Factorization Fq = spaqr_factorize(Aw, ref.hierarchy(), owner, fq);
+        FactorizationB200 Wq = spaqr_factorize_b200(Aw, ref.hierarchy(), owner, fq);
+        VectorXd y(Aw.rows());
+        for (Index i = 0; i < y.size(); ++i) y(i) = U(rng);
+        VectorXd yr = y, yg = y;
+        Fq.q_apply_t(yr);
+        Wq.q_apply_t(yg);
+        check("q_apply_t", Wq.has_q() && max_rel(yg, yr) <= 1e-10, std::to_string(max_rel(yg, yr)));
+        yr = y;
+        yg = y;
+        Fq.q_apply(yr);
+        Wq.q_apply(yg);
+        check("q_apply", max_rel(yg, yr) <= 1e-10, std::to_string(max_rel(yg, yr)));
+        Wq.save(tmp + "/q_gpu.spqr");
+        const Factorization Fqg = load_factorization(tmp + "/q_gpu.spqr");
+        yr = y;
+        yg = y;
+        Fqg.q_apply_t(yr);
+        Wq.q_apply_t(yg);
+        check("q_factor_file", Fqg.has_q && Fqg.Q.size() == Fq.Q.size() && max_rel(yg, yr) <= 1e-10,
+              std::to_string(Fqg.Q.size()) + " vs " + std::to_string(Fq.Q.size()));
+    }
     // 5. error mapping: a front with fewer coupled rows than columns
     {
         std::vector<Eigen::Triplet<double>> t{{0, 0, 1.0}, {0, 1, 2.0}};

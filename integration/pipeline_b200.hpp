@@ -43,10 +43,11 @@ public:
         }
         char err[512] = {0};
         int cluster = -1;
-        const int rc = spqr_pipeline_create(A.rows(), A.cols(), A.outer(), A.inner(), A.values(),
-                                            coords ? xy.data() : nullptr, coords ? int(coords->cols()) : 0,
-                                            parts ? parts->data() : nullptr, opt.levels, opt.eps, opt.skip_levels,
-                                            int(opt.solver), device, &h_, err, sizeof err, &cluster);
+        const int rc = spqr_pipeline_create_ex(A.rows(), A.cols(), A.outer(), A.inner(), A.values(),
+                                               coords ? xy.data() : nullptr, coords ? int(coords->cols()) : 0,
+                                               parts ? parts->data() : nullptr, opt.levels, opt.eps, opt.skip_levels,
+                                               int(opt.solver), int(opt.store_q), /*ranks=*/1, device,
+                                               /*obs=*/nullptr, nullptr, &h_, err, sizeof err, &cluster);
         b200_check(rc, err, cluster);
     }
     PipelineB200(const PipelineB200&) = delete;
@@ -106,6 +107,10 @@ public:
     void wt_solve(VectorXd& z) const { apply(SPQR_WT_SOLVE, z); }
     void w_apply(VectorXd& z) const { apply(SPQR_W_APPLY, z); }
     void wt_apply(VectorXd& z) const { apply(SPQR_WT_APPLY, z); }
+    // transforms.h:70-71 (factorizations made with FactorizeOptions::store_q); y has length M
+    void q_apply_t(VectorXd& y) const { apply(SPQR_Q_APPLY_T, y); }
+    void q_apply(VectorXd& y) const { apply(SPQR_Q_APPLY, y); }
+    bool has_q() const { return spqr_factorization_nq(h_) >= 0; }
     void save(const std::string& path) const {
         char err[512] = {0};
         b200_check(spqr_factorization_save(h_, path.c_str(), err, sizeof err), err, -1);
@@ -138,11 +143,11 @@ inline FactorizationB200 spaqr_factorize_b200(const SparseMatrix& A, const Clust
     spqr_factorization* f = nullptr;
     char err[512] = {0};
     int cluster = -1;
-    const int rc = spqr_factorize(A.rows(), A.cols(), A.outer(), A.inner(), A.values(), h.num_levels,
-                                  int(h.clusters.size()), info.data(), cptr.data(), ccols.data(),
-                                  h.finest_of_col.data(), int(tpar.size()), tpar.data(), h.tree->root,
-                                  row_owner.data(), opt.eps, opt.skip_levels, device, /*obs=*/nullptr, nullptr, &f,
-                                  err, sizeof err, &cluster);
+    const int rc = spqr_factorize_ex(A.rows(), A.cols(), A.outer(), A.inner(), A.values(), h.num_levels,
+                                     int(h.clusters.size()), info.data(), cptr.data(), ccols.data(),
+                                     h.finest_of_col.data(), int(tpar.size()), tpar.data(), h.tree->root,
+                                     row_owner.data(), opt.eps, opt.skip_levels, int(opt.store_q), device,
+                                     /*obs=*/nullptr, nullptr, &f, err, sizeof err, &cluster);
     b200_check(rc, err, cluster);
     return FactorizationB200(f);
 }
