@@ -1128,8 +1128,16 @@ private:
         static const bool no_narrow = std::getenv("SPQR_NO_NARROW") != nullptr;
         size_t nsmem[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         size_t nnar = 0;
+        // Narrow blocks too large for one CTA's shared memory (the in-place classes, m <= 128 by up
+        // to 2048 columns: the widest sparsify_cols G at C2) go to the thread-block clusters, whose
+        // CTAs each stage a column range: per pivot a cluster barrier instead of one CTA walking
+        // the whole block in L2 (C2: CPQR 105 -> 77 ms).  SPQR_NARROW_IN_PLACE=1 keeps them narrow.
+        static const bool glb_clus =
+            std::getenv("SPQR_NARROW_IN_PLACE") == nullptr && std::getenv("SPQR_NO_CPQR_CLUSTER") == nullptr;
         for (size_t i = 0; i < cd.size(); ++i) {
-            const int nc = no_narrow ? -1 : cpqr_narrow_class(cd[i].m, cd[i].n);
+            int nc = no_narrow ? -1 : cpqr_narrow_class(cd[i].m, cd[i].n);
+            if (glb_clus && nc >= 0 && nc % 6 >= 3 && cd[i].n >= 16 && cpqr_clus_smem_bytes(cd[i].m, cd[i].n) <= 200 * 1024)
+                nc = -1;
             if (nc >= 0) {
                 narrow[nc].push_back(static_cast<int>(i));
                 nar[i] = 1;
@@ -1144,9 +1152,32 @@ private:
             const int* dn = u.put(narrow[c]);
             double nb = 0;
             for (int i : narrow[c]) nb += 8.0 * cd[i].m * cd[i].n;
+            // SPQR_CPQR_LOG=<path>: per narrow launch, its device time and problem shapes
+            // (diagnostics; synchronises after the launch)
+            static const char* clog = std::getenv("SPQR_CPQR_LOG");
+            cudaEvent_t la = nullptr, lb = nullptr;
+            if (clog) {
+                CK(cudaEventCreate(&la));
+                CK(cudaEventCreate(&lb));
+                CK(cudaEventRecord(la, st_));
+            }
             cudaEvent_t e0 = kt_.begin(st_);
             launch_cpqr_narrow(c, dc, dn, static_cast<int>(narrow[c].size()), nsmem[c], st_);
             kt_.end(K_CPQR, e0, st_, nb, 0, static_cast<double>(narrow[c].size()));
+            if (clog) {
+                CK(cudaEventRecord(lb, st_));
+                CK(cudaEventSynchronize(lb));
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, la, lb));
+                cudaEventDestroy(la);
+                cudaEventDestroy(lb);
+                if (std::FILE* f = std::fopen(clog, "a")) {
+                    std::fprintf(f, "L %d %d %.4f %d", cur_stage_, c, ms, static_cast<int>(narrow[c].size()));
+                    for (int i : narrow[c]) std::fprintf(f, " %dx%d", cd[i].m, cd[i].n);
+                    std::fprintf(f, "\n");
+                    std::fclose(f);
+                }
+            }
         }
         if (nnar == cd.size()) return;
         // Problems too big for one CTA's shared memory run on a thread-block cluster of
@@ -1232,6 +1263,7 @@ private:
             launch_cpqr_tall(c, dc, dt, static_cast<int>(tall[c].size()), st_);
             kt_.end(K_CPQR, e0, st_, tb, 2, static_cast<double>(tall[c].size()));
         }
+        if (small.empty() && large.empty()) return;
         const int* ds = u.put(small);
         const int* dl = u.put(large);
         double cb = 0;
