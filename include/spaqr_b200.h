@@ -104,6 +104,25 @@ int spqr_rank_plan(int m, int n, const int* colptr, const int* rowind, const dou
  * accounted); *nstages stages; owner (nclusters) optional. */
 int spqr_pipeline_rank_stats(const spqr_pipeline* p, int* nstages, double* flops, double* cross, int* owner);
 
+/* A factorization across nranks = 2^g processes (one per GPU), the Pipeline of every rank
+ * built from the same A: each rank partitions A (identically), eliminates the leaves of its
+ * own subtree (spqr_rank_plan owners), and ranks > 0 send their leaf-stage effects — eliminated
+ * clusters, W factors, pivot / trailing rows and every front they touched — to rank 0 through
+ * the caller's blocking byte transport; rank 0 merges them exactly as the sequential engine
+ * would have left its state and runs the remaining stages (the top levels gathered onto one
+ * GPU).  Rank 0's pipeline is the factorization (identical to spqr_pipeline_create's); the
+ * other ranks' pipelines hold none (solve returns an error).  Transport callbacks return 0 on
+ * success. */
+typedef int (*spqr_send_fn)(void* user, int dst, const void* buf, long long n);
+typedef int (*spqr_recv_fn)(void* user, int src, void* buf, long long n);
+int spqr_pipeline_create_dist(int m, int n, const int* colptr, const int* rowind, const double* vals,
+                              const double* coords, int dim, const int* parts, int levels, double eps, int skip_levels,
+                              int device, int rank, int nranks, spqr_send_fn send, spqr_recv_fn recv, void* user,
+                              spqr_pipeline** out, char* err, int errlen, int* err_cluster);
+/* out3: 1 if this rank's part went to rank 0 (no factorization here), seconds in the leaf-stage
+ * exchange, bytes sent (ranks > 0) / received (rank 0). */
+void spqr_pipeline_dist_info(const spqr_pipeline* p, double* out3);
+
 /* info[16]: M, N, L, nclusters, nW, n_dropped, n_trailing, n_stages, nnz_w, nnz(A), W sweep levels,
  *           engine launches, engine syncs, h2d bytes, d2h bytes, solve-plan launches per sweep pair */
 void spqr_pipeline_info(const spqr_pipeline* p, long long* info);

@@ -62,6 +62,10 @@ SIGNATURES = {
                                           C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp,
                                           C.POINTER(vp), C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
     "spqr_pipeline_rank_stats": (C.c_int, [vp, C.POINTER(C.c_int), vp, vp, vp]),
+    "spqr_pipeline_create_dist": (C.c_int, [C.c_int, C.c_int, i32p, i32p, f64p, vp, C.c_int, vp, C.c_int, C.c_double,
+                                            C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, C.POINTER(vp),
+                                            C.c_char_p, C.c_int, C.POINTER(C.c_int)]),
+    "spqr_pipeline_dist_info": (None, [vp, f64p]),
     "spqr_rank_plan": (C.c_int, [C.c_int, C.c_int, i32p, i32p, f64p, vp, C.c_int, vp, C.c_int, C.c_int,
                                  C.POINTER(C.c_int), C.POINTER(C.c_int), vp, vp, vp, vp, vp, C.c_char_p, C.c_int]),
     "spqr_pipeline_nq": (C.c_longlong, [vp]),

@@ -87,12 +87,42 @@ def _observer(fn):
     return _OBSERVER_FN(cb)
 
 
+_SEND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_longlong)
+_RECV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_longlong)
+
+
+def _transport(group):
+    """The blocking byte transport of spqr_pipeline_create_dist over a torch.distributed group
+    (CPU tensors: a gloo group; under an NCCL default group pass dist.new_group(backend="gloo"))."""
+    import torch
+    import torch.distributed as dist
+
+    def send(user, dst, buf, n):
+        try:
+            a = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_uint8)), shape=(int(n),))
+            dist.send(torch.from_numpy(a.copy()), dst, group=group)
+            return 0
+        except Exception:
+            return 1
+
+    def recv(user, src, buf, n):
+        try:
+            t = torch.empty(int(n), dtype=torch.uint8)
+            dist.recv(t, src, group=group)
+            C.memmove(buf, t.numpy().ctypes.data, int(n))
+            return 0
+        except Exception:
+            return 1
+
+    return _SEND_FN(send), _RECV_FN(recv)
+
+
 class Pipeline:
     """spqr_pipeline_create / _solve / _apply (include/spaqr_b200.h).  observer: an optional
     fn(phase, stage, detail, view) called after every engine phase (pipeline.h:39-41)."""
 
     def __init__(self, A, eps=1e-2, levels=0, skip_levels=3, solver="spaqr", coords=None, parts=None, device=0,
-                 observer=None, store_q=False, ranks=1):
+                 observer=None, store_q=False, ranks=1, dist_group=None):
         require_gpu()
         L = lib()
         m, n, p, i, x = _csc(A)
@@ -107,10 +137,21 @@ class Pipeline:
         cl = C.c_int(-1)
         h = C.c_void_p()
         cb = _observer(observer)
-        rc = L.spqr_pipeline_create_ex(m, n, p, i, x, _ptr(cp), dim, _ptr(pp), int(levels), float(eps),
-                                       int(skip_levels), SOLVERS[solver], int(bool(store_q)), int(ranks), int(device),
-                                       C.cast(cb, C.c_void_p) if cb else None, None, C.byref(h), err, 512,
-                                       C.byref(cl))
+        if dist_group is not None:  # spqr_pipeline_create_dist: one factorization across the group's ranks
+            if solver != "spaqr" or store_q or observer is not None:
+                raise ValueError("a distributed pipeline takes the spaqr solver without store_q / observer")
+            import torch.distributed as dist
+            rank, size = dist.get_rank(dist_group), dist.get_world_size(dist_group)
+            self._tp = _transport(dist_group)
+            rc = L.spqr_pipeline_create_dist(m, n, p, i, x, _ptr(cp), dim, _ptr(pp), int(levels), float(eps),
+                                             int(skip_levels), int(device), rank, size,
+                                             C.cast(self._tp[0], C.c_void_p), C.cast(self._tp[1], C.c_void_p), None,
+                                             C.byref(h), err, 512, C.byref(cl))
+        else:
+            rc = L.spqr_pipeline_create_ex(m, n, p, i, x, _ptr(cp), dim, _ptr(pp), int(levels), float(eps),
+                                           int(skip_levels), SOLVERS[solver], int(bool(store_q)), int(ranks),
+                                           int(device), C.cast(cb, C.c_void_p) if cb else None, None, C.byref(h),
+                                           err, 512, C.byref(cl))
         if rc != 0:
             msg = err.value.decode()
             if rc == 1:
@@ -125,6 +166,10 @@ class Pipeline:
          self.nnz_A, self.nbatches, self.launches, self.syncs, self.h2d_bytes, self.d2h_bytes,
          self.sweep_launches) = [int(v) for v in info]
         self.nQ = int(L.spqr_pipeline_nq(self.h))  # -1: no Q kept
+        di = np.zeros(3)
+        L.spqr_pipeline_dist_info(self.h, di)
+        self.is_root = di[0] == 0.0  # False on ranks > 0 of a distributed factorization
+        self.dist_exchange_s, self.dist_bytes = float(di[1]), int(di[2])
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -61,6 +61,11 @@ int guarded(char* err, int errlen, int* err_cluster, F&& f) {
     return capi_guarded(err, errlen, err_cluster, std::forward<F>(f));
 }
 
+int create_impl(int m, int n, const int* colptr, const int* rowind, const double* vals, const double* coords, int dim,
+                const int* parts, int levels, double eps, int skip_levels, int solver, int store_q, int ranks, int device,
+                spqr_observer_fn obs, void* obs_user, const DistTransport* dist, spqr_pipeline** out, char* err,
+                int errlen, int* err_cluster);
+
 }  // namespace
 
 extern "C" {
@@ -92,6 +97,42 @@ int spqr_pipeline_create_ex(int m, int n, const int* colptr, const int* rowind, 
                             const double* coords, int dim, const int* parts, int levels, double eps, int skip_levels,
                             int solver, int store_q, int ranks, int device, spqr_observer_fn obs, void* obs_user,
                             spqr_pipeline** out, char* err, int errlen, int* err_cluster) {
+    return create_impl(m, n, colptr, rowind, vals, coords, dim, parts, levels, eps, skip_levels, solver, store_q, ranks,
+                       device, obs, obs_user, nullptr, out, err, errlen, err_cluster);
+}
+
+int spqr_pipeline_create_dist(int m, int n, const int* colptr, const int* rowind, const double* vals,
+                              const double* coords, int dim, const int* parts, int levels, double eps, int skip_levels,
+                              int device, int rank, int nranks, spqr_send_fn send, spqr_recv_fn recv, void* user,
+                              spqr_pipeline** out, char* err, int errlen, int* err_cluster) {
+    DistTransport t;
+    t.user = user;
+    t.rank = rank;
+    t.size = nranks;
+    t.send = send;
+    t.recv = recv;
+    if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && (!send || !recv))) {
+        *out = nullptr;
+        if (err && errlen > 0) std::snprintf(err, errlen, "bad rank / transport");
+        return SPQR_E_SHAPE;
+    }
+    return create_impl(m, n, colptr, rowind, vals, coords, dim, parts, levels, eps, skip_levels, SPQR_SOLVER_SPAQR, 0, 1,
+                       device, nullptr, nullptr, nranks > 1 ? &t : nullptr, out, err, errlen, err_cluster);
+}
+
+void spqr_pipeline_dist_info(const spqr_pipeline* p, double* out3) {
+    out3[0] = p->F.dist_partial ? 1.0 : 0.0;
+    out3[1] = p->F.dist_exchange_s;
+    out3[2] = static_cast<double>(p->F.dist_bytes);
+}
+
+}  // extern "C"
+
+namespace {
+int create_impl(int m, int n, const int* colptr, const int* rowind, const double* vals, const double* coords, int dim,
+                const int* parts, int levels, double eps, int skip_levels, int solver, int store_q, int ranks, int device,
+                spqr_observer_fn obs, void* obs_user, const DistTransport* dist, spqr_pipeline** out, char* err,
+                int errlen, int* err_cluster) {
     *out = nullptr;
     auto* P = new spqr_pipeline;
     const int rc = guarded(err, errlen, err_cluster, [&] {
@@ -149,13 +190,14 @@ int spqr_pipeline_create_ex(int m, int n, const int* colptr, const int* rowind, 
             fo.skip_levels = skip_levels;
             fo.store_q = store_q != 0;
             fo.ranks = std::max(1, ranks);
+            fo.dist = dist;
             cudaEvent_t e0, e1;
             CK(cudaEventCreate(&e0));
             CK(cudaEventCreate(&e1));
             CK(cudaEventRecord(e0, P->st));
             const FactorizeObserver ob = make_observer(obs, obs_user);
             P->F = gpu_factorize(P->Aw, P->h, P->owner, fo, P->st, obs ? &ob : nullptr);
-            P->plan = build_solve_plan(P->F, P->st);
+            if (!P->F.dist_partial) P->plan = build_solve_plan(P->F, P->st);
             CK(cudaEventRecord(e1, P->st));
             CK(cudaEventSynchronize(e1));
             float ms = 0.f;
@@ -163,7 +205,7 @@ int spqr_pipeline_create_ex(int m, int n, const int* colptr, const int* rowind, 
             P->ev_factorize_ms = ms;
             cudaEventDestroy(e0);
             cudaEventDestroy(e1);
-            P->has_f = true;
+            P->has_f = !P->F.dist_partial;  // ranks > 0 of a distributed factorization hold none
             P->t_factorize = now_s() - t0;
         }
         const double t0 = now_s();
@@ -183,6 +225,10 @@ int spqr_pipeline_create_ex(int m, int n, const int* colptr, const int* rowind, 
     *out = P;
     return SPQR_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 void spqr_pipeline_destroy(spqr_pipeline* p) { delete p; }
 
@@ -288,6 +334,7 @@ int spqr_pipeline_solve(spqr_pipeline* p, int direct, const double* b, double* x
                         int* converged, double* hist, int* nhist, double* t_solve, char* err, int errlen) {
     int cl = -1;
     return guarded(err, errlen, &cl, [&] {
+        if (p->F.dist_partial) throw std::logic_error("this rank's part of the factorization was sent to rank 0");
         if (direct && !p->has_f) throw std::logic_error("direct solve requires a factorization");
         CK(cudaSetDevice(p->device));
         const int m = p->Aw.m, n = p->Aw.n;

@@ -24,6 +24,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <iterator>
 #include <condition_variable>
 #include <deque>
@@ -537,6 +538,10 @@ public:
             out_.rank.ranks = opt.ranks;
             out_.rank.owner = rank_owners(h, ata_graph(A), opt.ranks);
         }
+        if (opt.dist && opt.dist->size > 1) {
+            dist_ = opt.dist;
+            dist_owner_ = rank_owners(h, ata_graph(A), dist_->size);
+        }
         if (opt.store_q) out_.qarena = std::make_unique<DeviceArena>(size_t(64) << 20);
         const size_t nc = h.clusters.size();
         fr_.resize(nc);
@@ -806,6 +811,15 @@ private:
     std::vector<char> alive_;  // mirror of fr_[c].live, scanned instead of the Front objects
     std::vector<HolderSet> holders_;
     std::vector<std::vector<int>> stage_list_, tree_clusters_;
+    // distributed leaf stage (opt.dist): owner rank per cluster, the initial row list per front
+    const DistTransport* dist_ = nullptr;
+    std::vector<int> dist_owner_;
+    std::vector<std::vector<int>> init_rows_;
+    std::vector<int> dist_touched_;                 // fronts this rank's leaf eliminations touched
+    std::vector<std::pair<int, int>> dist_tr_;      // (front, row) rows they transformed in place
+    std::vector<char> dist_export();
+    void dist_import(const char* buf, size_t n);
+    void dist_exchange();
     DeviceFactorization out_;
     std::unique_ptr<DeviceArena> arena_[2];
     int cur_ = 0, dev_ = 0;
@@ -1420,6 +1434,11 @@ void Engine::init_fronts(const std::vector<int>& owner) {
         local[r] = f.nrows();
         f.rows.push_back(r);
     }
+    if (dist_) {
+        init_rows_.resize(fr_.size());
+        for (size_t c = 0; c < fr_.size(); ++c)
+            if (fr_[c].live) init_rows_[c] = fr_[c].rows;
+    }
     std::vector<int> colpos(A_.n);
     for (size_t c = 0; c < h_.clusters.size(); ++c)
         if (h_.clusters[c].level == Lf)
@@ -2000,7 +2019,12 @@ std::vector<int> Engine::stage_fronts(const std::vector<int>& list) {
 // stage is split into dependency waves (edge c1 -> c2, c1 < c2, when some row
 // is nonzero in both blocks); each wave is one batched round.
 void Engine::eliminate_stage(int k) {
-    const auto& list = stage_list_[k];
+    std::vector<int> mine;
+    if (dist_ && k == L_ + 1) {  // the leaf stage: this rank's subtree only (ranks.cpp owners)
+        for (int c : stage_list_[k])
+            if (dist_owner_[c] == dist_->rank) mine.push_back(c);
+    }
+    const auto& list = (dist_ && k == L_ + 1) ? mine : stage_list_[k];
     if (list.empty()) return;
     for (size_t f = 0; f < fr_.size(); ++f)
         if (alive_[f]) fr_[f].tag.clear();
@@ -2303,6 +2327,13 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         }
         for (int t = 0; t < nvalid; ++t)
             if (el_[t].logic) throw std::logic_error(el_[t].err);
+        if (dist_ && cur_stage_ == L_ + 1)  // distributed leaf stage: what rank 0 must merge
+            for (int t = 0; t < nvalid; ++t) {
+                const Elim& e = el_[t];
+                for (int m : e.parts) dist_touched_.push_back(m);
+                for (const auto& d : e.dest) dist_touched_.push_back(d.first);
+                for (int i = std::max(e.cs, 0); i < e.total_rows; ++i) dist_tr_.emplace_back(e.srows[i].base, e.srows[i].gid);
+            }
         for (int t = 0; t < nvalid; ++t) elim_commit2(el_[t]);
         flush_holder_removals();
     }
@@ -3085,6 +3116,328 @@ void Engine::snapshot(StageStats& st) {  // factorize.cpp:731-743
     }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Distributed leaf stage (opt.dist).  Every rank builds the same engine; at
+// the leaf stage (L+1) each eliminates only the leaves of its own subtree (ranks.cpp owners).
+// Leaves touch disjoint rows — no row of A couples two subtrees' interiors — so the ranks'
+// eliminations commute; the only fronts two ranks touch are pieces of the top separators, each
+// rank transforming its own side's rows.  Ranks > 0 then send rank 0 their effects: eliminated
+// clusters, W factors, pivot rows, trailing rows, and every front they touched (rows, keys,
+// values, and which rows they transformed); rank 0 merges them into its own state exactly as
+// the sequential engine would have left it (initial rows in order minus every rank's pivots,
+// then appended rows in ascending source-cluster order = rank order), and runs the remaining
+// stages — the top levels gathered onto one GPU.
+namespace {
+struct DistWriter {
+    std::vector<char> b;
+    template <class T>
+    void put(const T* p, size_t n) {
+        const char* c = reinterpret_cast<const char*>(p);
+        b.insert(b.end(), c, c + sizeof(T) * n);
+    }
+    void i64(long long v) { put(&v, 1); }
+    void ivec(const std::vector<int>& v) {
+        i64(static_cast<long long>(v.size()));
+        put(v.data(), v.size());
+    }
+};
+struct DistReader {
+    const char* p;
+    size_t n, o = 0;
+    template <class T>
+    void get(T* d, size_t cnt) {
+        const size_t bytes = sizeof(T) * cnt;
+        if (o + bytes > n) throw std::runtime_error("distributed factorization: truncated message");
+        std::memcpy(d, p + o, bytes);
+        o += bytes;
+    }
+    long long i64() {
+        long long v;
+        get(&v, 1);
+        return v;
+    }
+    std::vector<int> ivec() {
+        const long long k = i64();
+        if (k < 0 || static_cast<size_t>(k) > n) throw std::runtime_error("distributed factorization: bad length");
+        std::vector<int> v(k);
+        get(v.data(), v.size());
+        return v;
+    }
+};
+}  // namespace
+
+std::vector<char> Engine::dist_export() {
+    DistWriter w;
+    w.i64(0x53505144);  // "SPQD"
+    std::vector<int> el;
+    for (int c : stage_list_[L_ + 1])
+        if (dist_owner_[c] == dist_->rank && gone_[c]) el.push_back(c);
+    w.ivec(el);
+    // W factors (every factor so far is this rank's), values from a host mirror of the W arena
+    std::vector<std::pair<const char*, std::vector<char>>> mirror;
+    out_.warena->for_each_chunk([&](const char* base, size_t used) {
+        mirror.emplace_back(base, std::vector<char>(used));
+        if (used) CK(cudaMemcpy(mirror.back().second.data(), base, used, cudaMemcpyDeviceToHost));
+    });
+    auto host = [&](const double* d) -> const double* {
+        const char* c = reinterpret_cast<const char*>(d);
+        for (const auto& m : mirror)
+            if (c >= m.first && c < m.first + m.second.size()) return reinterpret_cast<const double*>(m.second.data() + (c - m.first));
+        throw std::logic_error("distributed factorization: W data outside the W arena");
+    };
+    w.i64(static_cast<long long>(out_.W.size()));
+    for (const DevWFactor& f : out_.W) {
+        if (f.kind != 0) throw std::logic_error("distributed factorization: rotation factor at the leaf stage");
+        const int meta[4] = {f.cluster, f.c, f.k, f.scale_only ? 1 : 0};
+        w.put(meta, 4);
+        w.put(out_.idx.data() + f.cols_off, f.c);
+        w.put(out_.idx.data() + f.coupled_off, f.k);
+        if (f.c > 0) w.put(host(f.a), static_cast<size_t>(f.c) * (f.c + f.k));
+    }
+    std::vector<int> piv;
+    for (int c : el)
+        for (int j : cols_[c]) {
+            piv.push_back(j);
+            piv.push_back(static_cast<int>(out_.pivot_row[j]));
+        }
+    w.ivec(piv);
+    w.i64(npiv_);
+    std::vector<int> trail(out_.trailing_rows.begin(), out_.trailing_rows.end());
+    w.ivec(trail);
+    // touched fronts, their transformed rows, and their values gathered into one buffer
+    std::sort(dist_touched_.begin(), dist_touched_.end());
+    dist_touched_.erase(std::unique(dist_touched_.begin(), dist_touched_.end()), dist_touched_.end());
+    std::vector<int> T;
+    for (int f : dist_touched_)
+        if (!gone_[f] && fr_[f].live) T.push_back(f);
+    std::sort(dist_tr_.begin(), dist_tr_.end());
+    AsmBuilder& gb = asm_slot(0);
+    std::vector<long long> voff(T.size() + 1, 0);
+    for (size_t t = 0; t < T.size(); ++t) voff[t + 1] = voff[t] + static_cast<long long>(fr_[T[t]].nrows()) * fr_[T[t]].ncols;
+    double* dv = arena().alloc_n<double>(std::max<long long>(voff.back(), 1));
+    for (size_t t = 0; t < T.size(); ++t) {  // each front's blocks in ascending key order, ld = rows
+        const Front& F = fr_[T[t]];
+        if (F.nrows() == 0 || F.ncols == 0) continue;
+        const int di = gb.begin(dv + voff[t], F.nrows(), F.nrows(), F.ncols, 1, static_cast<int>(F.keys.size()));
+        gb.source(di, 0) = AsmSrc{F.mat, 1, F.ld};
+        for (int i = 0; i < F.nrows(); ++i) gb.row(di, i) = int4{0, i, -1, 0};
+        int o = 0;
+        for (size_t q = 0; q < F.keys.size(); ++q) {
+            gb.seg(di, static_cast<int>(q), o);
+            gb.km(di, static_cast<int>(q), 0) = F.keys[q].col;
+            o += F.keys[q].width;
+        }
+    }
+    flush_assemble(gb);
+    std::vector<double> hv(voff.back());
+    sync();
+    if (!hv.empty()) CK(cudaMemcpy(hv.data(), dv, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost));
+    w.i64(static_cast<long long>(T.size()));
+    size_t q0 = 0;
+    for (size_t t = 0; t < T.size(); ++t) {
+        const Front& F = fr_[T[t]];
+        w.i64(T[t]);
+        w.ivec(F.rows);
+        std::vector<int> kw;
+        for (const KeyRef& k : F.keys) {
+            kw.push_back(k.key);
+            kw.push_back(k.width);
+        }
+        w.ivec(kw);
+        std::vector<int> tr;
+        while (q0 < dist_tr_.size() && dist_tr_[q0].first < T[t]) ++q0;
+        for (size_t q = q0; q < dist_tr_.size() && dist_tr_[q].first == T[t]; ++q) tr.push_back(dist_tr_[q].second);
+        w.ivec(tr);
+        w.put(hv.data() + voff[t], static_cast<size_t>(voff[t + 1] - voff[t]));
+    }
+    return std::move(w.b);
+}
+
+void Engine::dist_import(const char* buf, size_t n) {
+    DistReader r{buf, n};
+    if (r.i64() != 0x53505144) throw std::runtime_error("distributed factorization: bad message");
+    const std::vector<int> el = r.ivec();
+    for (int c : el) {
+        if (c < 0 || static_cast<size_t>(c) >= fr_.size()) throw std::runtime_error("distributed factorization: bad cluster");
+        for (const KeyRef& k : fr_[c].keys) holders_[k.key].remove(c);
+        holders_[c].clear();
+        gone_[c] = 1;
+        alive_[c] = 0;
+        dfree(fr_[c].mat, fr_[c].big);
+        fr_[c].retire();
+    }
+    // W factors: values uploaded in one copy
+    const long long nw = r.i64();
+    struct WIn {
+        int cl, c, k, so;
+        std::vector<int> cols, cp;
+        size_t off;
+    };
+    std::vector<WIn> ws(nw);
+    std::vector<double> wv;
+    for (auto& f : ws) {
+        int meta[4];
+        r.get(meta, 4);
+        f.cl = meta[0], f.c = meta[1], f.k = meta[2], f.so = meta[3];
+        f.cols.resize(f.c);
+        f.cp.resize(f.k);
+        r.get(f.cols.data(), f.c);
+        r.get(f.cp.data(), f.k);
+        f.off = wv.size();
+        wv.resize(wv.size() + static_cast<size_t>(f.c) * (f.c + f.k));
+        r.get(wv.data() + f.off, static_cast<size_t>(f.c) * (f.c + f.k));
+    }
+    double* dw = out_.warena->alloc_n<double>(std::max<size_t>(wv.size(), 1));
+    if (!wv.empty()) CK(cudaMemcpyAsync(dw, wv.data(), sizeof(double) * wv.size(), cudaMemcpyHostToDevice, st_));
+    for (const auto& f : ws) {
+        DevWFactor& d = new_factor(0, f.cl, f.c, f.k, f.cols, f.so ? nullptr : &f.cp);
+        d.a = dw + f.off;
+    }
+    const std::vector<int> piv = r.ivec();
+    for (size_t i = 0; i + 1 < piv.size(); i += 2) out_.pivot_row[piv[i]] = piv[i + 1];
+    npiv_ += r.i64();
+    const std::vector<int> trail = r.ivec();
+    out_.trailing_rows.insert(out_.trailing_rows.end(), trail.begin(), trail.end());
+    // fronts
+    const long long nf = r.i64();
+    struct FIn {
+        int f;
+        std::vector<int> rows, kw, tr;
+        size_t off;
+    };
+    std::vector<FIn> fs(nf);
+    std::vector<double> fv;
+    for (auto& x : fs) {
+        x.f = static_cast<int>(r.i64());
+        if (x.f < 0 || static_cast<size_t>(x.f) >= fr_.size() || !fr_[x.f].live)
+            throw std::runtime_error("distributed factorization: front not live on rank 0");
+        x.rows = r.ivec();
+        x.kw = r.ivec();
+        x.tr = r.ivec();
+        size_t ncols = 0;
+        for (size_t q = 1; q < x.kw.size(); q += 2) ncols += x.kw[q];
+        x.off = fv.size();
+        fv.resize(fv.size() + x.rows.size() * ncols);
+        r.get(fv.data() + x.off, x.rows.size() * ncols);
+    }
+    double* dv = arena().alloc_n<double>(std::max<size_t>(fv.size(), 1));
+    if (!fv.empty()) CK(cudaMemcpyAsync(dv, fv.data(), sizeof(double) * fv.size(), cudaMemcpyHostToDevice, st_));
+    AsmBuilder& mb = asm_slot(0);
+    std::vector<std::pair<int, Front>> repl;
+    for (const auto& x : fs) {
+        const Front& C = fr_[x.f];
+        const std::vector<int>& init = init_rows_[x.f];
+        std::vector<int> sinit(init), sr(x.rows), str(x.tr);
+        std::sort(sinit.begin(), sinit.end());
+        std::sort(sr.begin(), sr.end());
+        std::sort(str.begin(), str.end());
+        auto in = [](const std::vector<int>& v, int a) { return std::binary_search(v.begin(), v.end(), a); };
+        Front nf;
+        nf.live = true;
+        std::vector<int2> src;  // (source 0 = rank 0's front / 1 = imported, row)
+        for (int i = 0; i < C.nrows(); ++i) {
+            const int g = C.rows[i];
+            const bool initial = in(sinit, g);
+            if (initial && !in(sr, g)) continue;  // taken as a pivot by the sending rank
+            nf.rows.push_back(g);
+            src.push_back(int2{0, i});
+        }
+        std::vector<int> pos_r(x.rows.size());
+        for (size_t i = 0; i < x.rows.size(); ++i) {
+            const int g = x.rows[i];
+            if (!in(sinit, g)) {  // appended by the sending rank: after everything rank 0 holds
+                nf.rows.push_back(g);
+                src.push_back(int2{1, static_cast<int>(i)});
+            }
+        }
+        {  // rows the sending rank transformed in place take its values
+            std::vector<std::pair<int, int>> rp;
+            for (size_t i = 0; i < x.rows.size(); ++i) rp.emplace_back(x.rows[i], static_cast<int>(i));
+            std::sort(rp.begin(), rp.end());
+            for (size_t i = 0; i < nf.rows.size(); ++i)
+                if (src[i].x == 0 && in(str, nf.rows[i])) {
+                    auto it = std::lower_bound(rp.begin(), rp.end(), std::make_pair(nf.rows[i], INT_MIN));
+                    if (it == rp.end() || it->first != nf.rows[i]) throw std::logic_error("distributed factorization: transformed row missing");
+                    src[i] = int2{1, it->second};
+                }
+        }
+        // keys: both versions', minus the clusters the sending rank eliminated
+        std::vector<std::pair<int, int>> ks;
+        for (const KeyRef& k : C.keys)
+            if (!gone_[k.key]) ks.emplace_back(k.key, k.width);
+        std::vector<int> roff;  // imported column offset per imported key (ascending)
+        int o = 0;
+        for (size_t q = 0; q + 1 < x.kw.size(); q += 2) {
+            roff.push_back(o);
+            o += x.kw[q + 1];
+            if (!gone_[x.kw[q]]) ks.emplace_back(x.kw[q], x.kw[q + 1]);  // eliminated by any rank: gone
+        }
+        std::sort(ks.begin(), ks.end());
+        ks.erase(std::unique(ks.begin(), ks.end(), [](const auto& a, const auto& b) { return a.first == b.first; }), ks.end());
+        for (const auto& k : ks) nf.keys.push_back(KeyRef{k.first, k.second, 0});
+        layout(x.f, nf.keys, nf.ncols);
+        nf.ld = std::max(1, nf.nrows());
+        nf.mat = dalloc(arena(), static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1), nf.big);
+        std::vector<int> ord;
+        phys_order(nf.keys, ord);
+        const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, 2, static_cast<int>(ord.size()));
+        mb.source(di, 0) = AsmSrc{C.mat, 1, C.ld};
+        mb.source(di, 1) = AsmSrc{dv + x.off, 1, static_cast<long long>(std::max<size_t>(x.rows.size(), 1))};
+        for (int i = 0; i < nf.nrows(); ++i) mb.row(di, i) = int4{src[i].x, src[i].y, -1, 0};
+        for (size_t q = 0; q < ord.size(); ++q) {
+            const KeyRef& k = nf.keys[ord[q]];
+            mb.seg(di, static_cast<int>(q), k.col);
+            const int ci = C.find(k.key);
+            mb.km(di, static_cast<int>(q), 0) = ci >= 0 ? C.keys[ci].col : -1;
+            int ri = -1;
+            for (size_t t = 0; t + 1 < x.kw.size(); t += 2)
+                if (x.kw[t] == k.key) ri = roff[t / 2];
+            mb.km(di, static_cast<int>(q), 1) = ri;
+            if (ci < 0) holders_[k.key].add(x.f);
+        }
+        mb.drop_if_empty();
+        repl.emplace_back(x.f, std::move(nf));
+    }
+    flush_assemble(mb);
+    for (auto& pr : repl) {
+        Front& F = fr_[pr.first];
+        dfree(F.mat, F.big);
+        F.rows = std::move(pr.second.rows);
+        F.keys = std::move(pr.second.keys);
+        F.mat = pr.second.mat;
+        F.big = pr.second.big;
+        F.ld = pr.second.ld;
+        F.ncols = pr.second.ncols;
+        F.scaled_ok = false;
+        F.tag.clear();
+        F.soff.clear();
+    }
+}
+
+void Engine::dist_exchange() {
+    const double t0 = now_s();
+    if (dist_->rank != 0) {
+        const std::vector<char> b = dist_export();
+        const long long n = static_cast<long long>(b.size());
+        if (dist_->send(dist_->user, 0, &n, sizeof n) || dist_->send(dist_->user, 0, b.data(), n))
+            throw std::runtime_error("distributed factorization: send to rank 0 failed");
+        out_.dist_bytes += n;
+    } else {
+        for (int q = 1; q < dist_->size; ++q) {  // ascending ranks = ascending source clusters
+            long long n = 0;
+            if (dist_->recv(dist_->user, q, &n, sizeof n)) throw std::runtime_error("distributed factorization: receive failed");
+            std::vector<char> b(static_cast<size_t>(std::max<long long>(n, 0)));
+            if (n > 0 && dist_->recv(dist_->user, q, b.data(), n)) throw std::runtime_error("distributed factorization: receive failed");
+            dist_import(b.data(), b.size());
+            out_.dist_bytes += n;
+        }
+        // W in the reference's chronological order (ascending cluster) within the leaf stage
+        std::stable_sort(out_.W.begin(), out_.W.end(), [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
+    }
+    out_.dist_exchange_s = now_s() - t0;
+}
+
 DeviceFactorization Engine::run() {  // factorize.cpp:745-790
     for (int k = L_ + 1; k >= 1; --k) {
         StageStats st;
@@ -3095,6 +3448,13 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         const HostProf before = prof_;
         double t0 = now_s();
         eliminate_stage(k);
+        if (dist_ && k == L_ + 1) {
+            dist_exchange();
+            if (dist_->rank != 0) {  // this rank's part is with rank 0
+                out_.dist_partial = true;
+                break;
+            }
+        }
         st.t_eliminate = now_s() - t0;
         digest(0);
         if (opt_.eps > 0.0 && k >= 2 && L_ + 1 - k >= opt_.skip_levels) {
@@ -3122,8 +3482,9 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         out_.stages.push_back(st);
         for (int i = 0; i < HostProf::N; ++i) sprof_.back().t[i] = prof_.t[i] - before.t[i];
     }
-    for (size_t c = 0; c < fr_.size(); ++c)
-        if (alive_[c] && fr_[c].live) out_.trailing_rows.insert(out_.trailing_rows.end(), fr_[c].rows.begin(), fr_[c].rows.end());
+    if (!out_.dist_partial)
+        for (size_t c = 0; c < fr_.size(); ++c)
+            if (alive_[c] && fr_[c].live) out_.trailing_rows.insert(out_.trailing_rows.end(), fr_[c].rows.begin(), fr_[c].rows.end());
     for (size_t c = 0; c < fr_.size(); ++c) dfree(fr_[c].mat, fr_[c].big);
     sync();
     out_.ctr.t_qr_ms = out_.ctr.k_ms[K_QR];

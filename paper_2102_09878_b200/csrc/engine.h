@@ -77,6 +77,11 @@ struct DeviceFactorization {
     int nbatches = 0;
     EngineCounters ctr;
     RankStats rank;
+    // distributed factorization: on ranks > 0 the result stops after the leaf stage, whose
+    // effects were sent to rank 0 (which holds the whole factorization)
+    bool dist_partial = false;
+    double dist_exchange_s = 0.0;   // time in the leaf-stage exchange (export / receive + import)
+    long long dist_bytes = 0;       // bytes sent (ranks > 0) or received (rank 0)
     long long nnz_w() const;
 };
 

@@ -87,11 +87,21 @@ RowMatching match_rows(const Csc& A);
 std::vector<int> rank_owners(const ClusterHierarchy& h, const Graph& g, int G);                                                // :401-463
 std::vector<int> assign_rows(const Csc& A, const ClusterHierarchy& h, const RowMatching& m);  // :465-514
 
+// Byte transport between the ranks of a distributed factorization (one process per GPU; the
+// Python layer binds it to torch.distributed).  Blocking; returns 0 on success.
+struct DistTransport {
+    void* user = nullptr;
+    int rank = 0, size = 1;
+    int (*send)(void* user, int dst, const void* buf, long long n) = nullptr;
+    int (*recv)(void* user, int src, void* buf, long long n) = nullptr;
+};
+
 struct FactorizeOptions {  // factorize.h:13-17
     double eps = 1e-2;
     int skip_levels = 3;
     bool store_q = false;  // keep the orthogonal row factors Q (tests, diagnostics)
     int ranks = 1;         // > 1: account work and cross-rank traffic of a ranks-GPU subtree split (ranks.cpp)
+    const DistTransport* dist = nullptr;  // size > 1: the leaf stage runs subtree-parallel
 };
 
 struct StageStats {  // transforms.h:40-47 (+ per-phase device-side timings)
