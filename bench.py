@@ -40,7 +40,9 @@ import numpy as np  # noqa: E402
 def config(ws):
     """The `config` object of both arms' JSON lines (identical keys and values)."""
     return {"workload": WORKLOAD, "N": 262144, "M": 524288, "levels": 14, "eps": 1e-2, "skip_levels": 3,
-            "cgls_tol": 1e-12, "seed": 0, "parallelism": f"replicas{ws}" if ws > 1 else "1 GPU",
+            "cgls_tol": 1e-12, "seed": 0,
+            "parallelism": (f"subtree split over {ws} GPUs: leaf stage per rank, then gathered on rank 0 "
+                            "(spqr_pipeline_create_dist)") if ws > 1 else "1 GPU",
             "l2_flush": "256 MB write between steps (ours); the CPU arm has no device state"}
 
 
@@ -53,16 +55,15 @@ def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # the engine's host bookkeeping is multi-threaded: replicas on one node split the
-    # host cores instead of oversubscribing them (one core left per replica's driver thread)
-    nloc = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
-    if nloc > 1 and "OMP_NUM_THREADS" not in os.environ:
-        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or nloc) // nloc - 1))
+    # N > 1 runs ONE factorization across the ranks (spqr_pipeline_create_dist): the ranks
+    # share the leaf stage, then rank 0 works alone, so every rank keeps the host's threads
     if ws > 1:
         import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if os.environ.get("BENCH_SAME_GPU"):  # functional check of the N > 1 path with one GPU: every
+            local, backend = 0, "gloo"        # rank on cuda:0, collectives on the host (not a measurement)
         if backend == "nccl":
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
@@ -80,7 +81,8 @@ def allmax(ws, v):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([float(v)], device="cuda" if torch.cuda.is_available() else "cpu", dtype=torch.float64)
+    dev = "cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v)], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -309,10 +311,17 @@ def run_ours(args, ws, rank, local):
     h2d = A.indptr.nbytes + A.indices.nbytes + A.data.nbytes + p.b.nbytes + p.coords.nbytes
     d2h = 8 * A.shape[1]
 
+    group = None
+    if ws > 1:  # one factorization across the ranks; its transport is a gloo group on the host
+        import torch.distributed as dist
+        group = dist.new_group(backend="gloo")
+
     def step():
         t0 = time.perf_counter()
-        g = P.Pipeline(A, eps=p.eps, levels=p.levels, coords=p.coords, device=local)
-        x, rep = g.solve(p.b)
+        g = P.Pipeline(A, eps=p.eps, levels=p.levels, coords=p.coords, device=local, dist_group=group)
+        rep = None
+        if g.is_root:
+            x, rep = g.solve(p.b)
         wall = time.perf_counter() - t0
         t = g.times()
         return g, rep, (t["factorize_event_ms"] + t["solve_event_ms"]) / 1e3, wall
@@ -339,6 +348,10 @@ def run_ours(args, ws, rank, local):
     value = allmax(ws, sum(dev_t) / len(dev_t))
     e2e = allmax(ws, sum(e2e_t) / len(e2e_t))
     g, rep = last
+    if not g.is_root:  # this rank's leaf stage went to rank 0, which reports the step
+        if not args.no_microbench:
+            front_qr_microbench(local, ws, rank)
+        return
     t = g.times()
     ks = g.kernel_stats()
     # W-sweep family (solve): device time from CUDA events around every sweep, also inside
@@ -362,7 +375,7 @@ def run_ours(args, ws, rank, local):
     out = {
         "metric": METRIC, "value": round(value, 6), "unit": "s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(value * 1e3, 3), "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config(ws),
         "e2e": {"value": round(e2e, 6), "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "note": "spqr_pipeline_create+solve from host CSC/b to host x, incl. host partition "
@@ -394,6 +407,10 @@ def run_ours(args, ws, rank, local):
                   "elim_waves": t["elim_waves"], "w_solve_levels": t["w_solve_levels"],
                   "solve_plan_s": round(t["solve_plan_s"], 4), "solve_launches": t["solve_launches"]},
     }
+    if ws > 1:
+        out["distributed"] = {"exchange_s_rank0": round(g.dist_exchange_s, 4), "bytes_to_rank0": g.dist_bytes,
+                              "note": "each rank eliminates its subtree's leaves; ranks > 0 send their effects "
+                                      "to rank 0, which finishes; value = max over ranks"}
     if not args.no_microbench:
         try:
             mb = front_qr_microbench(local, ws, rank)
