@@ -1,7 +1,8 @@
 """N>1 plumbing of bench.py on CPU (gloo, world_size 2): process-group init from
 torchrun-style env, barrier, max-over-ranks timing, and rank-0-only reporting of
-the reference arm, and the split of the C5 microbenchmark batch across ranks.  The C2
-factorization is "replicas only"."""
+the reference arm, the split of the C5 microbenchmark batch across ranks, and the subtree
+ownership plan of the distributed factorization (the factorization itself needs
+GPUs: tests/test_gpu_dist.py)."""
 import os
 import socket
 import subprocess
