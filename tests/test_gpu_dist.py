@@ -24,7 +24,8 @@ from paper_2102_09878_b200.problems import tall_grid, knn_geometric
 dist.init_process_group("gloo", init_method="env://")
 rank, ws = dist.get_rank(), dist.get_world_size()
 cases = {"grid64": lambda: tall_grid(64), "knn": lambda: knn_geometric(8192, seed=2, levels=8),
-         "grid3d": lambda: tall_grid(20, dim=3, seed=1), "c2": lambda: tall_grid(512)}
+         "grid3d": lambda: tall_grid(20, dim=3, seed=1), "c2": lambda: tall_grid(512),
+         "c3": lambda: tall_grid(48, dim=3, seed=0), "c4": lambda: knn_geometric(1 << 20, seed=0, levels=16)}
 p = cases[os.environ["CASE"]]()
 kw = dict(eps=p.eps, levels=p.levels, coords=p.coords)
 g = P.Pipeline(p.A, dist_group=dist.group.WORLD, **kw)
@@ -95,3 +96,10 @@ def test_distributed_factorization_matches_single_process(ws, case):
 def test_distributed_c2_full_size():
     """BASELINE config 2 at full size across 2 ranks: identical to the single-process run."""
     print(_run(2, "c2", 850))
+
+
+@pytest.mark.timeout(1500)
+@pytest.mark.parametrize("case,ws", [("c3", 4), ("c4", 2)])
+def test_distributed_full_size_3d_and_knn(case, ws):
+    """BASELINE configs 3 (4 ranks) and 4 (2 ranks) at full size: identical to the single-process run."""
+    print(_run(ws, case, 1400))
