@@ -1,6 +1,7 @@
 // W sweep plan + device CGLS / CSNE drivers.
 #include "solve.h"
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <algorithm>
@@ -14,19 +15,29 @@ namespace spqr {
 
 namespace {
 
-// The level schedule of one sweep mode (see solve.h): levels from the walk-order
-// conflicts, factors bucketed per level, descriptors and accumulation lists uploaded.
-void build_schedule(SolvePlan& P, const DeviceFactorization& F, int mode, const int* d_idx, Uploader& up,
-                    std::vector<int>& lastW, std::vector<int>& lastR, std::vector<int>& lastA, long long& maxcontrib) {
+// The level schedule of one sweep mode (see solve.h), host side: levels from the walk-order
+// conflicts, factors bucketed per level, descriptors (device pointers into W) and the
+// accumulation lists.  Pure host work, so the schedules of several modes are built
+// concurrently and uploaded afterwards.
+struct HostLevel {
+    std::vector<WFac> fac, bfac;
+    std::vector<int> rptr, ridx, rcol;
+    int maxc = 1, bmaxc = 1;
+};
+struct HostSchedule {
+    std::vector<HostLevel> levels;
+    long long maxcontrib = 0;
+};
+
+HostSchedule host_schedule(const DeviceFactorization& F, int mode, const int* d_idx) {
     const int nfac = static_cast<int>(F.W.size());
     // factors at least this wide run one per CTA (SPQR_BIG_FACTOR overrides, for tests)
     static const int big_cols =
         std::getenv("SPQR_BIG_FACTOR") ? std::atoi(std::getenv("SPQR_BIG_FACTOR")) : kBigFactorCols;
     const bool forward = (mode == kWtSolve || mode == kWApply);
     const bool accumulate = (mode == kWtSolve || mode == kWtApply);
-    std::fill(lastW.begin(), lastW.end(), 0);
-    std::fill(lastR.begin(), lastR.end(), 0);
-    std::fill(lastA.begin(), lastA.end(), 0);
+    const size_t n = F.N > 0 ? static_cast<size_t>(F.N) : 1;
+    std::vector<int> lastW(n, 0), lastR(n, 0), lastA(n, 0);
     std::vector<int> level(nfac);
     int nlev = 0;
     for (int t = 0; t < nfac; ++t) {
@@ -66,18 +77,14 @@ void build_schedule(SolvePlan& P, const DeviceFactorization& F, int mode, const 
         const int q = forward ? t : nfac - 1 - t;
         byl[pos[level[q]]++] = q;
     }
-    SolvePlan::Schedule& S = P.sched[mode];
-    S.levels.clear();
-    S.launches = 0;
-    std::vector<WFac> fac, bfac;
+    HostSchedule H;
+    H.levels.resize(nlev);
     std::vector<std::pair<int, int>> lists;  // (coupled column, contribution index) in walk order
-    std::vector<int> rptr, ridx, rcol;
+    std::vector<int> colcnt(n, 0), touched;
     for (int l = 1; l <= nlev; ++l) {
-        fac.clear();
-        bfac.clear();
+        HostLevel& hl = H.levels[l - 1];
         lists.clear();
         long long contrib = 0;
-        int maxc = 1, bmaxc = 1;
         for (int e = cnt[l]; e < cnt[l + 1]; ++e) {
             const DevWFactor& w = F.W[byl[e]];
             WFac f{};
@@ -98,48 +105,59 @@ void build_schedule(SolvePlan& P, const DeviceFactorization& F, int mode, const 
             // c/32 work; rotations: the CTA path pays two block barriers per reflector, so only
             // very tall ones move
             if (w.kind == 0 ? w.c >= big_cols : w.c >= 8 * big_cols) {
-                bmaxc = std::max(bmaxc, w.c);
-                bfac.push_back(f);
+                hl.bmaxc = std::max(hl.bmaxc, w.c);
+                hl.bfac.push_back(f);
             } else {
-                maxc = std::max(maxc, w.c);
-                fac.push_back(f);
+                hl.maxc = std::max(hl.maxc, w.c);
+                hl.fac.push_back(f);
             }
         }
-        SolvePlan::Level lv;
-        lv.fac = up.put(fac);
-        lv.nf = static_cast<int>(fac.size());
-        lv.maxc = maxc;
-        lv.bfac = up.put(bfac);
-        lv.nbf = static_cast<int>(bfac.size());
-        lv.bmaxc = bmaxc;
         if (!lists.empty()) {
-            // per coupled column (ascending) its contributions in walk order: indices grow
-            // along the walk, so sorting the pairs gives exactly that
-            std::sort(lists.begin(), lists.end());
-            rptr.assign(1, 0);
-            ridx.clear();
-            rcol.clear();
-            for (size_t a = 0; a < lists.size();) {
-                size_t e = a;
-                while (e < lists.size() && lists[e].first == lists[a].first) ridx.push_back(lists[e++].second);
-                rcol.push_back(lists[a].first);
-                rptr.push_back(static_cast<int>(ridx.size()));
-                a = e;
+            // per coupled column (ascending) its contributions in walk order: a counting sort
+            // by column, stable, so each column's indices keep their (ascending) walk order
+            touched.clear();
+            for (const auto& pr : lists)
+                if (colcnt[pr.first]++ == 0) touched.push_back(pr.first);
+            std::sort(touched.begin(), touched.end());
+            hl.rcol = touched;
+            hl.rptr.assign(touched.size() + 1, 0);
+            for (size_t c = 0; c < touched.size(); ++c) {
+                hl.rptr[c + 1] = hl.rptr[c] + colcnt[touched[c]];
+                colcnt[touched[c]] = hl.rptr[c];  // becomes the next write position
             }
-            lv.rptr = up.put(rptr);
-            lv.ridx = up.put(ridx);
-            lv.rcol = up.put(rcol);
-            lv.ncol = static_cast<int>(rcol.size());
+            hl.ridx.resize(lists.size());
+            for (const auto& pr : lists) hl.ridx[colcnt[pr.first]++] = pr.second;
+            for (int c : touched) colcnt[c] = 0;
         }
-        maxcontrib = std::max(maxcontrib, contrib);
+        H.maxcontrib = std::max(H.maxcontrib, contrib);
+    }
+    return H;
+}
+
+void upload_schedule(SolvePlan& P, int mode, const HostSchedule& H, Uploader& up) {
+    SolvePlan::Schedule& S = P.sched[mode];
+    S.levels.clear();
+    S.launches = 0;
+    for (const HostLevel& hl : H.levels) {
+        SolvePlan::Level lv;
+        lv.fac = up.put(hl.fac);
+        lv.nf = static_cast<int>(hl.fac.size());
+        lv.maxc = hl.maxc;
+        lv.bfac = up.put(hl.bfac);
+        lv.nbf = static_cast<int>(hl.bfac.size());
+        lv.bmaxc = hl.bmaxc;
+        if (!hl.rcol.empty()) {
+            lv.rptr = up.put(hl.rptr);
+            lv.ridx = up.put(hl.ridx);
+            lv.rcol = up.put(hl.rcol);
+            lv.ncol = static_cast<int>(hl.rcol.size());
+        }
         S.launches += (lv.nf > 0) + (lv.nbf > 0) + (lv.ncol > 0);
         S.levels.push_back(lv);
-    }
-    S.built = true;
-    for (const auto& lv : S.levels) {
         P.maxc = std::max(P.maxc, lv.maxc);
         P.bmaxc = std::max(P.bmaxc, lv.bmaxc);
     }
+    S.built = true;
 }
 
 void build_schedules(SolvePlan& P, const DeviceFactorization& F, cudaStream_t st, std::initializer_list<int> modes) {
@@ -147,19 +165,32 @@ void build_schedules(SolvePlan& P, const DeviceFactorization& F, cudaStream_t st
     std::lock_guard<std::mutex> pin_lock(sp.mu);
     PinnedArena& pin = sp.arena;
     pin.reset();
+    static const bool prof = std::getenv("SPQR_PROF") != nullptr;
+    const double t0 = prof ? now_s() : 0.0;
     Uploader up{P.mem.get(), &pin, st};
     if (!P.d_idx) P.d_idx = up.put(F.idx);
-    const size_t n = F.N > 0 ? static_cast<size_t>(F.N) : 1;
-    std::vector<int> lastW(n), lastR(n), lastA(n);
+    const double t1 = prof ? now_s() : 0.0;
+    const std::vector<int> ms(modes);
+    std::vector<HostSchedule> hs(ms.size());
+#pragma omp parallel for num_threads(static_cast<int>(ms.size())) if (ms.size() > 1)
+    for (int i = 0; i < static_cast<int>(ms.size()); ++i) hs[i] = host_schedule(F, ms[i], P.d_idx);
+    const double t2 = prof ? now_s() : 0.0;
     long long maxcontrib = P.ncontrib;
-    for (int mode : modes) build_schedule(P, F, mode, P.d_idx, up, lastW, lastR, lastA, maxcontrib);
+    for (size_t i = 0; i < ms.size(); ++i) {
+        upload_schedule(P, ms[i], hs[i], up);
+        maxcontrib = std::max(maxcontrib, hs[i].maxcontrib);
+    }
     if (maxcontrib > P.ncontrib) {
         P.contrib = P.mem->alloc_n<double>(maxcontrib);
         P.ncontrib = maxcontrib;
     }
     prepare_wsweep(P.maxc, P.bmaxc);
+    const double t3 = prof ? now_s() : 0.0;
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
+    if (prof)
+        std::fprintf(stderr, "[spqr prof] solve plan: idx upload %.4f schedules %.4f upload %.4f sync %.4f s (%zu idx)\n",
+                     t1 - t0, t2 - t1, t3 - t2, now_s() - t3, F.idx.size());
 }
 
 }  // namespace
