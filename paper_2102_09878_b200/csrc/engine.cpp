@@ -819,7 +819,7 @@ private:
     std::vector<std::pair<int, int>> dist_tr_;      // (front, row) rows they transformed in place
     std::vector<char> dist_export();
     void dist_import(const char* buf, size_t n);
-    void dist_exchange();
+    void dist_exchange(int err_cluster, const std::string& err_reason);
     DeviceFactorization out_;
     std::unique_ptr<DeviceArena> arena_[2];
     int cur_ = 0, dev_ = 0;
@@ -2934,7 +2934,12 @@ void Engine::merge_level() {
             if (alive_[c] && fr_[c].live) pk.emplace_back(h_.clusters[c].parent, static_cast<int>(c));
         std::sort(pk.begin(), pk.end());
         for (size_t i = 0; i < pk.size(); ++i) {
-            if (pk[i].first < 0) throw std::logic_error("spaqr engine: live front without a parent cluster at merge");
+            if (pk[i].first < 0)
+                throw std::logic_error("spaqr engine: live front without a parent cluster at merge (cluster " +
+                                       std::to_string(pk[i].second) + ", level " +
+                                       std::to_string(h_.clusters[pk[i].second].level) + ", stage " +
+                                       std::to_string(cur_stage_) + ", rows " + std::to_string(fr_[pk[i].second].nrows()) +
+                                       ", width " + std::to_string(width(pk[i].second)) + ")");
             if (i == 0 || pk[i].first != pk[i - 1].first) {
                 gp.push_back(pk[i].first);
                 gstart.push_back(static_cast<int>(gkids.size()));
@@ -3415,23 +3420,47 @@ void Engine::dist_import(const char* buf, size_t n) {
     }
 }
 
-void Engine::dist_exchange() {
+void Engine::dist_exchange(int err_cluster, const std::string& err_reason) {
     const double t0 = now_s();
     if (dist_->rank != 0) {
+        if (err_cluster >= 0) {  // length -1: an error record (cluster, reason) instead of the effects
+            const long long n = -1;
+            const int cl = err_cluster, len = static_cast<int>(err_reason.size());
+            if (dist_->send(dist_->user, 0, &n, sizeof n) || dist_->send(dist_->user, 0, &cl, sizeof cl) ||
+                dist_->send(dist_->user, 0, &len, sizeof len) ||
+                (len > 0 && dist_->send(dist_->user, 0, err_reason.data(), len)))
+                throw std::runtime_error("distributed factorization: send to rank 0 failed");
+            throw SingularFrontError(err_cluster, err_reason);
+        }
         const std::vector<char> b = dist_export();
         const long long n = static_cast<long long>(b.size());
         if (dist_->send(dist_->user, 0, &n, sizeof n) || dist_->send(dist_->user, 0, b.data(), n))
             throw std::runtime_error("distributed factorization: send to rank 0 failed");
         out_.dist_bytes += n;
     } else {
+        int ecl = err_cluster;
+        std::string why = err_reason;
         for (int q = 1; q < dist_->size; ++q) {  // ascending ranks = ascending source clusters
             long long n = 0;
             if (dist_->recv(dist_->user, q, &n, sizeof n)) throw std::runtime_error("distributed factorization: receive failed");
-            std::vector<char> b(static_cast<size_t>(std::max<long long>(n, 0)));
+            if (n < 0) {
+                int cl = -1, len = 0;
+                if (dist_->recv(dist_->user, q, &cl, sizeof cl) || dist_->recv(dist_->user, q, &len, sizeof len))
+                    throw std::runtime_error("distributed factorization: receive failed");
+                std::string r(static_cast<size_t>(std::max(len, 0)), '\0');
+                if (len > 0 && dist_->recv(dist_->user, q, r.data(), len)) throw std::runtime_error("distributed factorization: receive failed");
+                if (ecl < 0 || cl < ecl) {
+                    ecl = cl;
+                    why = r;
+                }
+                continue;
+            }
+            std::vector<char> b(static_cast<size_t>(n));
             if (n > 0 && dist_->recv(dist_->user, q, b.data(), n)) throw std::runtime_error("distributed factorization: receive failed");
-            dist_import(b.data(), b.size());
+            if (ecl < 0) dist_import(b.data(), b.size());  // after an error only the error matters
             out_.dist_bytes += n;
         }
+        if (ecl >= 0) throw SingularFrontError(ecl, why);
         // W in the reference's chronological order (ascending cluster) within the leaf stage
         std::stable_sort(out_.W.begin(), out_.W.end(), [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
     }
@@ -3447,13 +3476,24 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         sprof_.back().stage = k;
         const HostProf before = prof_;
         double t0 = now_s();
-        eliminate_stage(k);
         if (dist_ && k == L_ + 1) {
-            dist_exchange();
+            // a rank whose leaves fail still reports to rank 0, which raises the first failing
+            // cluster of all ranks (ascending ids: what the sequential engine would raise)
+            int ecl = -1;
+            std::string why;
+            try {
+                eliminate_stage(k);
+            } catch (const SingularFrontError& e) {
+                ecl = e.cluster;
+                why = e.reason;
+            }
+            dist_exchange(ecl, why);
             if (dist_->rank != 0) {  // this rank's part is with rank 0
                 out_.dist_partial = true;
                 break;
             }
+        } else {
+            eliminate_stage(k);
         }
         st.t_eliminate = now_s() - t0;
         digest(0);

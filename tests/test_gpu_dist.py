@@ -26,6 +26,41 @@ rank, ws = dist.get_rank(), dist.get_world_size()
 cases = {"grid64": lambda: tall_grid(64), "knn": lambda: knn_geometric(8192, seed=2, levels=8),
          "grid3d": lambda: tall_grid(20, dim=3, seed=1), "c2": lambda: tall_grid(512),
          "c3": lambda: tall_grid(48, dim=3, seed=0), "c4": lambda: knn_geometric(1 << 20, seed=0, levels=16)}
+if os.environ["CASE"].startswith("sing"):  # singular leaf fronts (test_gpu_pipeline's matrices)
+    import scipy.sparse as sp
+    case = os.environ["CASE"]
+    if case in ("singA", "singB"):  # one row couples the two columns of one leaf: "rows couple"
+        D = np.zeros((9, 6))
+        D[0, 0], D[0, 1] = 1.0, 2.0
+        for j in range(2, 6):
+            D[2 * j - 3, j] = 3.0
+            D[2 * j - 2, j] = 0.5
+        parts = [0, 0, 1, 1, 1, 1] if case == "singA" else [1, 1, 0, 0, 0, 0]
+    else:  # a leaf whose stack QR meets an exactly zero pivot
+        D = np.zeros((11, 7))
+        D[0, 0], D[0, 1], D[1, 2], D[2, 2] = 1.5, -2.25, 2.0, 0.5
+        for j in range(3, 7):
+            D[2 * j - 3, j] = 3.0
+            D[2 * j - 2, j] = -0.75
+        parts = [0, 0, 0, 1, 1, 1, 1]
+    A = sp.csc_matrix(D)
+    kw = dict(eps=0.0, levels=1, parts=parts)
+    try:
+        P.Pipeline(A, dist_group=dist.group.WORLD, **kw)
+        got = None
+    except P.SingularFrontError as e:
+        got = (e.cluster, str(e))
+    if rank == 0:
+        try:
+            P.Pipeline(A, **kw)
+            want = None
+        except P.SingularFrontError as e:
+            want = (e.cluster, str(e))
+        assert want is not None and got == want, (got, want)
+    dist.barrier()
+    print(json.dumps({"rank": rank, "error": got}))
+    dist.destroy_process_group()
+    sys.exit(0)
 p = cases[os.environ["CASE"]]()
 kw = dict(eps=p.eps, levels=p.levels, coords=p.coords)
 g = P.Pipeline(p.A, dist_group=dist.group.WORLD, **kw)
@@ -103,3 +138,11 @@ def test_distributed_c2_full_size():
 def test_distributed_full_size_3d_and_knn(case, ws):
     """BASELINE configs 3 (4 ranks) and 4 (2 ranks) at full size: identical to the single-process run."""
     print(_run(ws, case, 1400))
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("case", ["singA", "singB", "singP"])
+def test_distributed_singular_front_error(case):
+    """A singular leaf on rank 0's side (singA, singP) or on rank 1's (singB): rank 0 raises the
+    SingularFrontError — cluster and reason — the single-process factorization raises."""
+    print(_run(2, case, 280))
