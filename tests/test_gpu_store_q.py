@@ -115,3 +115,18 @@ def test_q_survives_the_factor_file(tmp_path):
     # the oracle's restated reader sees the same Q section
     _, v = O.factor_file_apply(str(path), "q_apply_t", y)
     assert np.linalg.norm(v - g.q_apply_t(y)) <= 1e-12 * np.linalg.norm(y)
+
+
+@pytest.mark.timeout(900)
+def test_q_matches_oracle_3d_blocked_fronts():
+    """A 3D problem whose top fronts exceed the tile kernels (> 2 MB: the blocked QR path,
+    mbqr.cu) and whose large interfaces run on the cluster CPQR: Q still matches the oracle."""
+    p = tall_grid(24, dim=3, seed=3)
+    kw = dict(eps=p.eps, levels=p.levels, coords=p.coords)
+    g = _P().Pipeline(p.A, store_q=True, **kw)
+    o = O.Pipeline(p.A, store_q=True, **kw)
+    assert g.nW == o.nW and g.nQ == o.nQ > 0
+    y = np.random.default_rng(7).standard_normal(g.M)
+    for f in ("q_apply_t", "q_apply"):
+        a, b = getattr(g, f)(y), getattr(o, f)(y)
+        assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(y), f
