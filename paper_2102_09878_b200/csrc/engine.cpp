@@ -818,7 +818,8 @@ private:
     std::vector<int> dist_touched_;                 // fronts this rank's leaf eliminations touched
     std::vector<std::pair<int, int>> dist_tr_;      // (front, row) rows they transformed in place
     std::vector<char> dist_export();
-    void dist_import(const char* buf, size_t n);
+    bool dist_import(const char* buf, size_t n);
+    double* dist_vbuf_ = nullptr;  // exported values (CUDA IPC) until rank 0 acknowledges
     void dist_exchange(int err_cluster, const std::string& err_reason);
     DeviceFactorization out_;
     std::unique_ptr<DeviceArena> arena_[2];
@@ -3172,56 +3173,42 @@ struct DistReader {
 };
 }  // namespace
 
+// Values (front blocks and W factors) travel device to device: the sending rank gathers them
+// into one cudaMalloc'ed buffer and sends its CUDA IPC handle with the metadata; rank 0 opens
+// it (peer memory over NVLink on a multi-GPU node, the same memory when the ranks share a
+// GPU) and its gather kernels read the values in place; an acknowledgement releases the
+// buffer.  SPQR_DIST_HOST=1 sends the values inline through the host transport instead.
 std::vector<char> Engine::dist_export() {
+    static const bool host_mode = std::getenv("SPQR_DIST_HOST") != nullptr;
     DistWriter w;
     w.i64(0x53505144);  // "SPQD"
+    w.i64(host_mode ? 0 : 1);
     std::vector<int> el;
     for (int c : stage_list_[L_ + 1])
         if (dist_owner_[c] == dist_->rank && gone_[c]) el.push_back(c);
-    w.ivec(el);
-    // W factors (every factor so far is this rank's), values from a host mirror of the W arena
-    std::vector<std::pair<const char*, std::vector<char>>> mirror;
-    out_.warena->for_each_chunk([&](const char* base, size_t used) {
-        mirror.emplace_back(base, std::vector<char>(used));
-        if (used) CK(cudaMemcpy(mirror.back().second.data(), base, used, cudaMemcpyDeviceToHost));
-    });
-    auto host = [&](const double* d) -> const double* {
-        const char* c = reinterpret_cast<const char*>(d);
-        for (const auto& m : mirror)
-            if (c >= m.first && c < m.first + m.second.size()) return reinterpret_cast<const double*>(m.second.data() + (c - m.first));
-        throw std::logic_error("distributed factorization: W data outside the W arena");
-    };
-    w.i64(static_cast<long long>(out_.W.size()));
-    for (const DevWFactor& f : out_.W) {
-        if (f.kind != 0) throw std::logic_error("distributed factorization: rotation factor at the leaf stage");
-        const int meta[4] = {f.cluster, f.c, f.k, f.scale_only ? 1 : 0};
-        w.put(meta, 4);
-        w.put(out_.idx.data() + f.cols_off, f.c);
-        w.put(out_.idx.data() + f.coupled_off, f.k);
-        if (f.c > 0) w.put(host(f.a), static_cast<size_t>(f.c) * (f.c + f.k));
-    }
-    std::vector<int> piv;
-    for (int c : el)
-        for (int j : cols_[c]) {
-            piv.push_back(j);
-            piv.push_back(static_cast<int>(out_.pivot_row[j]));
-        }
-    w.ivec(piv);
-    w.i64(npiv_);
-    std::vector<int> trail(out_.trailing_rows.begin(), out_.trailing_rows.end());
-    w.ivec(trail);
-    // touched fronts, their transformed rows, and their values gathered into one buffer
+    // touched fronts and their transformed rows
     std::sort(dist_touched_.begin(), dist_touched_.end());
     dist_touched_.erase(std::unique(dist_touched_.begin(), dist_touched_.end()), dist_touched_.end());
     std::vector<int> T;
     for (int f : dist_touched_)
         if (!gone_[f] && fr_[f].live) T.push_back(f);
     std::sort(dist_tr_.begin(), dist_tr_.end());
-    AsmBuilder& gb = asm_slot(0);
-    std::vector<long long> voff(T.size() + 1, 0);
+    // value space: every touched front's blocks in ascending key order (ld = rows), then every
+    // W factor's [R | C] (ld = c)
+    std::vector<long long> voff(T.size() + 1, 0), woff(out_.W.size() + 1, 0);
     for (size_t t = 0; t < T.size(); ++t) voff[t + 1] = voff[t] + static_cast<long long>(fr_[T[t]].nrows()) * fr_[T[t]].ncols;
-    double* dv = arena().alloc_n<double>(std::max<long long>(voff.back(), 1));
-    for (size_t t = 0; t < T.size(); ++t) {  // each front's blocks in ascending key order, ld = rows
+    woff[0] = voff.back();
+    for (size_t q = 0; q < out_.W.size(); ++q) {
+        const DevWFactor& f = out_.W[q];
+        if (f.kind != 0) throw std::logic_error("distributed factorization: rotation factor at the leaf stage");
+        woff[q + 1] = woff[q] + static_cast<long long>(f.c) * (f.c + f.k);
+    }
+    const long long total = woff.back();
+    double* dv = nullptr;
+    CK(cudaMalloc(&dv, sizeof(double) * std::max<long long>(total, 1)));
+    dist_vbuf_ = dv;
+    AsmBuilder& gb = asm_slot(0);
+    for (size_t t = 0; t < T.size(); ++t) {
         const Front& F = fr_[T[t]];
         if (F.nrows() == 0 || F.ncols == 0) continue;
         const int di = gb.begin(dv + voff[t], F.nrows(), F.nrows(), F.ncols, 1, static_cast<int>(F.keys.size()));
@@ -3234,10 +3221,43 @@ std::vector<char> Engine::dist_export() {
             o += F.keys[q].width;
         }
     }
+    for (size_t q = 0; q < out_.W.size(); ++q) {
+        const DevWFactor& f = out_.W[q];
+        if (f.c == 0) continue;
+        const int di = gb.begin(dv + woff[q], f.c, f.c, f.c + f.k, 1, 1);
+        gb.source(di, 0) = AsmSrc{f.a, 1, f.c};
+        for (int i = 0; i < f.c; ++i) gb.row(di, i) = int4{0, i, -1, 0};
+        gb.seg(di, 0, 0);
+        gb.km(di, 0, 0) = 0;
+    }
     flush_assemble(gb);
-    std::vector<double> hv(voff.back());
     sync();
-    if (!hv.empty()) CK(cudaMemcpy(hv.data(), dv, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost));
+    if (!host_mode) {
+        cudaIpcMemHandle_t hnd;
+        CK(cudaIpcGetMemHandle(&hnd, dv));
+        w.put(reinterpret_cast<const char*>(&hnd), sizeof hnd);
+        w.i64(total);
+    }
+    w.ivec(el);
+    w.i64(static_cast<long long>(out_.W.size()));
+    for (size_t q = 0; q < out_.W.size(); ++q) {
+        const DevWFactor& f = out_.W[q];
+        const int meta[4] = {f.cluster, f.c, f.k, f.scale_only ? 1 : 0};
+        w.put(meta, 4);
+        w.put(out_.idx.data() + f.cols_off, f.c);
+        w.put(out_.idx.data() + f.coupled_off, f.k);
+        w.i64(woff[q]);
+    }
+    std::vector<int> piv;
+    for (int c : el)
+        for (int j : cols_[c]) {
+            piv.push_back(j);
+            piv.push_back(static_cast<int>(out_.pivot_row[j]));
+        }
+    w.ivec(piv);
+    w.i64(npiv_);
+    std::vector<int> trail(out_.trailing_rows.begin(), out_.trailing_rows.end());
+    w.ivec(trail);
     w.i64(static_cast<long long>(T.size()));
     size_t q0 = 0;
     for (size_t t = 0; t < T.size(); ++t) {
@@ -3254,14 +3274,36 @@ std::vector<char> Engine::dist_export() {
         while (q0 < dist_tr_.size() && dist_tr_[q0].first < T[t]) ++q0;
         for (size_t q = q0; q < dist_tr_.size() && dist_tr_[q].first == T[t]; ++q) tr.push_back(dist_tr_[q].second);
         w.ivec(tr);
-        w.put(hv.data() + voff[t], static_cast<size_t>(voff[t + 1] - voff[t]));
+        w.i64(voff[t]);
+    }
+    if (host_mode) {  // the values inline
+        std::vector<double> hv(total);
+        if (total > 0) CK(cudaMemcpy(hv.data(), dv, sizeof(double) * total, cudaMemcpyDeviceToHost));
+        w.i64(total);
+        w.put(hv.data(), hv.size());
+        CK(cudaFree(dv));
+        dist_vbuf_ = nullptr;
     }
     return std::move(w.b);
 }
 
-void Engine::dist_import(const char* buf, size_t n) {
+// returns true when the sender's values came through CUDA IPC (the sender waits for an ack)
+bool Engine::dist_import(const char* buf, size_t n) {
     DistReader r{buf, n};
     if (r.i64() != 0x53505144) throw std::runtime_error("distributed factorization: bad message");
+    const bool ipc = r.i64() == 1;
+    const double* vp = nullptr;
+    double* peer = nullptr;
+    long long total = 0;
+    if (ipc) {
+        cudaIpcMemHandle_t hnd;
+        r.get(reinterpret_cast<char*>(&hnd), sizeof hnd);
+        total = r.i64();
+        void* p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, hnd, cudaIpcMemLazyEnablePeerAccess));
+        peer = static_cast<double*>(p);
+        vp = peer;
+    }
     const std::vector<int> el = r.ivec();
     for (int c : el) {
         if (c < 0 || static_cast<size_t>(c) >= fr_.size()) throw std::runtime_error("distributed factorization: bad cluster");
@@ -3272,15 +3314,14 @@ void Engine::dist_import(const char* buf, size_t n) {
         dfree(fr_[c].mat, fr_[c].big);
         fr_[c].retire();
     }
-    // W factors: values uploaded in one copy
     const long long nw = r.i64();
     struct WIn {
         int cl, c, k, so;
         std::vector<int> cols, cp;
-        size_t off;
+        long long off;
     };
     std::vector<WIn> ws(nw);
-    std::vector<double> wv;
+    long long wtot = 0;
     for (auto& f : ws) {
         int meta[4];
         r.get(meta, 4);
@@ -3289,30 +3330,19 @@ void Engine::dist_import(const char* buf, size_t n) {
         f.cp.resize(f.k);
         r.get(f.cols.data(), f.c);
         r.get(f.cp.data(), f.k);
-        f.off = wv.size();
-        wv.resize(wv.size() + static_cast<size_t>(f.c) * (f.c + f.k));
-        r.get(wv.data() + f.off, static_cast<size_t>(f.c) * (f.c + f.k));
-    }
-    double* dw = out_.warena->alloc_n<double>(std::max<size_t>(wv.size(), 1));
-    if (!wv.empty()) CK(cudaMemcpyAsync(dw, wv.data(), sizeof(double) * wv.size(), cudaMemcpyHostToDevice, st_));
-    for (const auto& f : ws) {
-        DevWFactor& d = new_factor(0, f.cl, f.c, f.k, f.cols, f.so ? nullptr : &f.cp);
-        d.a = dw + f.off;
+        f.off = r.i64();
+        wtot += static_cast<long long>(f.c) * (f.c + f.k);
     }
     const std::vector<int> piv = r.ivec();
-    for (size_t i = 0; i + 1 < piv.size(); i += 2) out_.pivot_row[piv[i]] = piv[i + 1];
-    npiv_ += r.i64();
+    const long long npiv = r.i64();
     const std::vector<int> trail = r.ivec();
-    out_.trailing_rows.insert(out_.trailing_rows.end(), trail.begin(), trail.end());
-    // fronts
     const long long nf = r.i64();
     struct FIn {
         int f;
         std::vector<int> rows, kw, tr;
-        size_t off;
+        long long off;
     };
     std::vector<FIn> fs(nf);
-    std::vector<double> fv;
     for (auto& x : fs) {
         x.f = static_cast<int>(r.i64());
         if (x.f < 0 || static_cast<size_t>(x.f) >= fr_.size() || !fr_[x.f].live)
@@ -3320,15 +3350,37 @@ void Engine::dist_import(const char* buf, size_t n) {
         x.rows = r.ivec();
         x.kw = r.ivec();
         x.tr = r.ivec();
-        size_t ncols = 0;
-        for (size_t q = 1; q < x.kw.size(); q += 2) ncols += x.kw[q];
-        x.off = fv.size();
-        fv.resize(fv.size() + x.rows.size() * ncols);
-        r.get(fv.data() + x.off, x.rows.size() * ncols);
+        x.off = r.i64();
     }
-    double* dv = arena().alloc_n<double>(std::max<size_t>(fv.size(), 1));
-    if (!fv.empty()) CK(cudaMemcpyAsync(dv, fv.data(), sizeof(double) * fv.size(), cudaMemcpyHostToDevice, st_));
+    if (!ipc) {  // values inline: onto the device
+        total = r.i64();
+        std::vector<double> hv(static_cast<size_t>(std::max<long long>(total, 0)));
+        r.get(hv.data(), hv.size());
+        double* d = arena().alloc_n<double>(std::max<long long>(total, 1));
+        if (total > 0) CK(cudaMemcpyAsync(d, hv.data(), sizeof(double) * total, cudaMemcpyHostToDevice, st_));
+        vp = d;
+        sync();  // hv is released on return
+    }
     AsmBuilder& mb = asm_slot(0);
+    // W factors: gathered into one W-arena block
+    double* dw = out_.warena->alloc_n<double>(std::max<long long>(wtot, 1));
+    long long o = 0;
+    for (const auto& f : ws) {
+        DevWFactor& d = new_factor(0, f.cl, f.c, f.k, f.cols, f.so ? nullptr : &f.cp);
+        d.a = dw + o;
+        if (f.c > 0) {
+            const int di = mb.begin(d.a, f.c, f.c, f.c + f.k, 1, 1);
+            mb.source(di, 0) = AsmSrc{vp + f.off, 1, f.c};
+            for (int i = 0; i < f.c; ++i) mb.row(di, i) = int4{0, i, -1, 0};
+            mb.seg(di, 0, 0);
+            mb.km(di, 0, 0) = 0;
+        }
+        o += static_cast<long long>(f.c) * (f.c + f.k);
+    }
+    for (size_t i = 0; i + 1 < piv.size(); i += 2) out_.pivot_row[piv[i]] = piv[i + 1];
+    npiv_ += npiv;
+    out_.trailing_rows.insert(out_.trailing_rows.end(), trail.begin(), trail.end());
+    // fronts: rank 0's version (source 0) merged with the sender's (source 1, read in place)
     std::vector<std::pair<int, Front>> repl;
     for (const auto& x : fs) {
         const Front& C = fr_[x.f];
@@ -3340,22 +3392,18 @@ void Engine::dist_import(const char* buf, size_t n) {
         auto in = [](const std::vector<int>& v, int a) { return std::binary_search(v.begin(), v.end(), a); };
         Front nf;
         nf.live = true;
-        std::vector<int2> src;  // (source 0 = rank 0's front / 1 = imported, row)
+        std::vector<int2> src;  // (source, row)
         for (int i = 0; i < C.nrows(); ++i) {
             const int g = C.rows[i];
-            const bool initial = in(sinit, g);
-            if (initial && !in(sr, g)) continue;  // taken as a pivot by the sending rank
+            if (in(sinit, g) && !in(sr, g)) continue;  // taken as a pivot by the sending rank
             nf.rows.push_back(g);
             src.push_back(int2{0, i});
         }
-        std::vector<int> pos_r(x.rows.size());
-        for (size_t i = 0; i < x.rows.size(); ++i) {
-            const int g = x.rows[i];
-            if (!in(sinit, g)) {  // appended by the sending rank: after everything rank 0 holds
-                nf.rows.push_back(g);
+        for (size_t i = 0; i < x.rows.size(); ++i)
+            if (!in(sinit, x.rows[i])) {  // appended by the sending rank: after everything rank 0 holds
+                nf.rows.push_back(x.rows[i]);
                 src.push_back(int2{1, static_cast<int>(i)});
             }
-        }
         {  // rows the sending rank transformed in place take its values
             std::vector<std::pair<int, int>> rp;
             for (size_t i = 0; i < x.rows.size(); ++i) rp.emplace_back(x.rows[i], static_cast<int>(i));
@@ -3367,16 +3415,16 @@ void Engine::dist_import(const char* buf, size_t n) {
                     src[i] = int2{1, it->second};
                 }
         }
-        // keys: both versions', minus the clusters the sending rank eliminated
+        // keys: both versions', minus the clusters eliminated by any rank
         std::vector<std::pair<int, int>> ks;
         for (const KeyRef& k : C.keys)
             if (!gone_[k.key]) ks.emplace_back(k.key, k.width);
-        std::vector<int> roff;  // imported column offset per imported key (ascending)
-        int o = 0;
+        std::vector<int> roff;  // sender's column offset per key (ascending)
+        int oc = 0;
         for (size_t q = 0; q + 1 < x.kw.size(); q += 2) {
-            roff.push_back(o);
-            o += x.kw[q + 1];
-            if (!gone_[x.kw[q]]) ks.emplace_back(x.kw[q], x.kw[q + 1]);  // eliminated by any rank: gone
+            roff.push_back(oc);
+            oc += x.kw[q + 1];
+            if (!gone_[x.kw[q]]) ks.emplace_back(x.kw[q], x.kw[q + 1]);
         }
         std::sort(ks.begin(), ks.end());
         ks.erase(std::unique(ks.begin(), ks.end(), [](const auto& a, const auto& b) { return a.first == b.first; }), ks.end());
@@ -3388,7 +3436,7 @@ void Engine::dist_import(const char* buf, size_t n) {
         phys_order(nf.keys, ord);
         const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, 2, static_cast<int>(ord.size()));
         mb.source(di, 0) = AsmSrc{C.mat, 1, C.ld};
-        mb.source(di, 1) = AsmSrc{dv + x.off, 1, static_cast<long long>(std::max<size_t>(x.rows.size(), 1))};
+        mb.source(di, 1) = AsmSrc{vp + x.off, 1, static_cast<long long>(std::max<size_t>(x.rows.size(), 1))};
         for (int i = 0; i < nf.nrows(); ++i) mb.row(di, i) = int4{src[i].x, src[i].y, -1, 0};
         for (size_t q = 0; q < ord.size(); ++q) {
             const KeyRef& k = nf.keys[ord[q]];
@@ -3405,6 +3453,8 @@ void Engine::dist_import(const char* buf, size_t n) {
         repl.emplace_back(x.f, std::move(nf));
     }
     flush_assemble(mb);
+    sync();  // every read of the sender's values done (its buffer may go)
+    if (peer) CK(cudaIpcCloseMemHandle(peer));
     for (auto& pr : repl) {
         Front& F = fr_[pr.first];
         dfree(F.mat, F.big);
@@ -3418,6 +3468,8 @@ void Engine::dist_import(const char* buf, size_t n) {
         F.tag.clear();
         F.soff.clear();
     }
+    (void)total;
+    return ipc;
 }
 
 void Engine::dist_exchange(int err_cluster, const std::string& err_reason) {
@@ -3437,6 +3489,12 @@ void Engine::dist_exchange(int err_cluster, const std::string& err_reason) {
         if (dist_->send(dist_->user, 0, &n, sizeof n) || dist_->send(dist_->user, 0, b.data(), n))
             throw std::runtime_error("distributed factorization: send to rank 0 failed");
         out_.dist_bytes += n;
+        if (dist_vbuf_) {  // rank 0 has read the values in place: release them
+            long long ack = 0;
+            if (dist_->recv(dist_->user, 0, &ack, sizeof ack)) throw std::runtime_error("distributed factorization: receive failed");
+            CK(cudaFree(dist_vbuf_));
+            dist_vbuf_ = nullptr;
+        }
     } else {
         int ecl = err_cluster;
         std::string why = err_reason;
@@ -3447,18 +3505,25 @@ void Engine::dist_exchange(int err_cluster, const std::string& err_reason) {
                 int cl = -1, len = 0;
                 if (dist_->recv(dist_->user, q, &cl, sizeof cl) || dist_->recv(dist_->user, q, &len, sizeof len))
                     throw std::runtime_error("distributed factorization: receive failed");
-                std::string r(static_cast<size_t>(std::max(len, 0)), '\0');
-                if (len > 0 && dist_->recv(dist_->user, q, r.data(), len)) throw std::runtime_error("distributed factorization: receive failed");
+                std::string rs(static_cast<size_t>(std::max(len, 0)), '\0');
+                if (len > 0 && dist_->recv(dist_->user, q, rs.data(), len)) throw std::runtime_error("distributed factorization: receive failed");
                 if (ecl < 0 || cl < ecl) {
                     ecl = cl;
-                    why = r;
+                    why = rs;
                 }
                 continue;
             }
             std::vector<char> b(static_cast<size_t>(n));
             if (n > 0 && dist_->recv(dist_->user, q, b.data(), n)) throw std::runtime_error("distributed factorization: receive failed");
-            if (ecl < 0) dist_import(b.data(), b.size());  // after an error only the error matters
             out_.dist_bytes += n;
+            // after an error only the error matters, but an IPC sender still waits for its ack
+            DistReader hdr{b.data(), b.size()};
+            const bool ipc = b.size() >= 16 && (hdr.i64(), hdr.i64() == 1);
+            if (ecl < 0) dist_import(b.data(), b.size());
+            if (ipc) {
+                const long long ack = 1;
+                if (dist_->send(dist_->user, q, &ack, sizeof ack)) throw std::runtime_error("distributed factorization: send failed");
+            }
         }
         if (ecl >= 0) throw SingularFrontError(ecl, why);
         // W in the reference's chronological order (ascending cluster) within the leaf stage
