@@ -598,6 +598,7 @@ public:
         init_fronts(owner);
     }
     ~Engine() {
+        if (dist_vbuf_) cudaFree(dist_vbuf_);  // an exchange that failed before rank 0's ack
         {  // the per-cluster host containers (hundreds of thousands of small vectors) are
            // freed on a background thread instead of on the caller's critical path
             struct Trash {
@@ -3304,6 +3305,12 @@ bool Engine::dist_import(const char* buf, size_t n) {
         peer = static_cast<double*>(p);
         vp = peer;
     }
+    struct PeerGuard {  // the mapping is closed on every exit path
+        double*& p;
+        ~PeerGuard() {
+            if (p) cudaIpcCloseMemHandle(p);
+        }
+    } guard{peer};
     const std::vector<int> el = r.ivec();
     for (int c : el) {
         if (c < 0 || static_cast<size_t>(c) >= fr_.size()) throw std::runtime_error("distributed factorization: bad cluster");
@@ -3454,7 +3461,10 @@ bool Engine::dist_import(const char* buf, size_t n) {
     }
     flush_assemble(mb);
     sync();  // every read of the sender's values done (its buffer may go)
-    if (peer) CK(cudaIpcCloseMemHandle(peer));
+    if (peer) {
+        CK(cudaIpcCloseMemHandle(peer));
+        peer = nullptr;
+    }
     for (auto& pr : repl) {
         Front& F = fr_[pr.first];
         dfree(F.mat, F.big);
