@@ -40,9 +40,29 @@ __device__ double block_sum(double v, double* red) {
 // ------------------------------------------------------------------ assemble
 __global__ void k_assemble(const AsmDst* __restrict__ dst, int ndst, long long total, const int4* __restrict__ rowref,
                            const int* __restrict__ segoff, const int* __restrict__ kmap, const AsmSrc* __restrict__ src) {
-    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    // the destinations this block's elements fall in, found once per block; each thread then
+    // searches only that (usually short) range
+    __shared__ int s_lo, s_hi;
+    const long long b0 = blockIdx.x * static_cast<long long>(blockDim.x);
+    if (threadIdx.x < 2) {
+        const long long t = threadIdx.x == 0 ? b0 : min(total - 1, b0 + blockDim.x - 1);
+        int lo = 0, hi = ndst - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (dst[mid].elem_off <= t)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        if (threadIdx.x == 0)
+            s_lo = lo;
+        else
+            s_hi = lo;
+    }
+    __syncthreads();
+    const long long e = b0 + threadIdx.x;
     if (e >= total) return;
-    int lo = 0, hi = ndst - 1;
+    int lo = s_lo, hi = s_hi;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (dst[mid].elem_off <= e)
@@ -51,9 +71,10 @@ __global__ void k_assemble(const AsmDst* __restrict__ dst, int ndst, long long t
             hi = mid - 1;
     }
     const AsmDst d = dst[lo];
-    const long long loc = e - d.elem_off;
-    const int i = static_cast<int>(loc % d.nrows);
-    const int j = static_cast<int>(loc / d.nrows);
+    // 32-bit index arithmetic: one destination holds fewer than 2^31 elements
+    const unsigned loc = static_cast<unsigned>(e - d.elem_off), nr = static_cast<unsigned>(d.nrows);
+    const int j = static_cast<int>(loc / nr);
+    const int i = static_cast<int>(loc - static_cast<unsigned>(j) * nr);
     const int* so = segoff + d.seg_off;
     int q = 0, qh = d.nseg - 1;
     while (q < qh) {

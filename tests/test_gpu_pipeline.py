@@ -283,3 +283,18 @@ def test_config2_full_size_parity():  # the headline problem at full size (oracl
     z = np.random.default_rng(0).uniform(-1, 1, g.N)
     assert np.linalg.norm(g.w_solve(g.w_apply(z)) - z) <= 1e-12 * np.linalg.norm(z)
     assert np.linalg.norm(g.wt_solve(g.wt_apply(z)) - z) <= 1e-12 * np.linalg.norm(z)
+
+
+def test_factorization_is_bitwise_reproducible():
+    """Two factorizations of the same problem in one process give bitwise-identical W sweeps and
+    solves: every reduction on the path (statistics, block reflectors, sweep accumulations) has
+    a fixed order, and the host's parallel passes commit in cluster order."""
+    p = tall_grid(128, seed=3)
+    kw = dict(eps=p.eps, levels=p.levels, coords=p.coords)
+    a = _P().Pipeline(p.A, **kw)
+    b = _P().Pipeline(p.A, **kw)
+    z = np.random.default_rng(5).standard_normal(a.N)
+    assert np.array_equal(a.w_solve(z), b.w_solve(z)) and np.array_equal(a.wt_solve(z), b.wt_solve(z))
+    xa, ra = a.solve(p.b)
+    xb, rb = b.solve(p.b)
+    assert np.array_equal(xa, xb) and ra["iterations"] == rb["iterations"]
