@@ -541,6 +541,12 @@ public:
         if (opt.dist && opt.dist->size > 1) {
             dist_ = opt.dist;
             dist_owner_ = rank_owners(h, ata_graph(A), dist_->size);
+            // the split stages: from the leaves down to the first stage that sparsifies (its
+            // eliminations still precede any scale_all) and above the top lg levels
+            int lg = 0;
+            while ((1 << lg) < dist_->size) ++lg;
+            const int ksp = (opt.eps > 0.0 && L_ + 1 - opt.skip_levels >= 2) ? L_ + 1 - opt.skip_levels : 0;
+            dist_kend_ = std::max(lg + 1, ksp);
         }
         if (opt.store_q) out_.qarena = std::make_unique<DeviceArena>(size_t(64) << 20);
         const size_t nc = h.clusters.size();
@@ -812,16 +818,21 @@ private:
     std::vector<char> alive_;  // mirror of fr_[c].live, scanned instead of the Front objects
     std::vector<HolderSet> holders_;
     std::vector<std::vector<int>> stage_list_, tree_clusters_;
-    // distributed leaf stage (opt.dist): owner rank per cluster, the initial row list per front
+    // distributed stages (opt.dist): owner rank per cluster; the stages L+1 ..
+    // dist_kend_ split their eliminations by subtree
     const DistTransport* dist_ = nullptr;
     std::vector<int> dist_owner_;
-    std::vector<std::vector<int>> init_rows_;
-    std::vector<int> dist_touched_;                 // fronts this rank's leaf eliminations touched
+    int dist_kend_ = 0;
+    bool dist_stage(int k) const { return dist_ && k >= dist_kend_; }
+    std::vector<std::vector<int>> start_rows_;      // every front's rows at the start of the stage
+    size_t dist_w0_ = 0, dist_t0_ = 0;              // W / trailing-row counts at the start of the stage
+    long long dist_npiv0_ = 0;
+    std::vector<int> dist_touched_;                 // fronts this rank's eliminations touched
     std::vector<std::pair<int, int>> dist_tr_;      // (front, row) rows they transformed in place
-    std::vector<char> dist_export();
-    bool dist_import(const char* buf, size_t n);
-    double* dist_vbuf_ = nullptr;  // exported values (CUDA IPC) until rank 0 acknowledges
-    void dist_exchange(int err_cluster, const std::string& err_reason);
+    std::vector<char> dist_export(int k);
+    void dist_apply(const std::vector<std::vector<char>>& msgs);
+    double* dist_vbuf_ = nullptr;  // exported values (CUDA IPC) until every peer acknowledges
+    void dist_exchange(int k, int err_cluster, const std::string& err_reason);
     DeviceFactorization out_;
     std::unique_ptr<DeviceArena> arena_[2];
     int cur_ = 0, dev_ = 0;
@@ -1436,11 +1447,6 @@ void Engine::init_fronts(const std::vector<int>& owner) {
         local[r] = f.nrows();
         f.rows.push_back(r);
     }
-    if (dist_) {
-        init_rows_.resize(fr_.size());
-        for (size_t c = 0; c < fr_.size(); ++c)
-            if (fr_[c].live) init_rows_[c] = fr_[c].rows;
-    }
     std::vector<int> colpos(A_.n);
     for (size_t c = 0; c < h_.clusters.size(); ++c)
         if (h_.clusters[c].level == Lf)
@@ -2022,11 +2028,11 @@ std::vector<int> Engine::stage_fronts(const std::vector<int>& list) {
 // is nonzero in both blocks); each wave is one batched round.
 void Engine::eliminate_stage(int k) {
     std::vector<int> mine;
-    if (dist_ && k == L_ + 1) {  // the leaf stage: this rank's subtree only (ranks.cpp owners)
+    if (dist_stage(k)) {  // a split stage: this rank's subtree only (ranks.cpp owners)
         for (int c : stage_list_[k])
             if (dist_owner_[c] == dist_->rank) mine.push_back(c);
     }
-    const auto& list = (dist_ && k == L_ + 1) ? mine : stage_list_[k];
+    const auto& list = dist_stage(k) ? mine : stage_list_[k];
     if (list.empty()) return;
     for (size_t f = 0; f < fr_.size(); ++f)
         if (alive_[f]) fr_[f].tag.clear();
@@ -2329,7 +2335,7 @@ void Engine::eliminate_wave(const std::vector<int>& list) {
         }
         for (int t = 0; t < nvalid; ++t)
             if (el_[t].logic) throw std::logic_error(el_[t].err);
-        if (dist_ && cur_stage_ == L_ + 1)  // distributed leaf stage: what rank 0 must merge
+        if (dist_stage(cur_stage_))  // split stage: what the other ranks must merge
             for (int t = 0; t < nvalid; ++t) {
                 const Elim& e = el_[t];
                 for (int m : e.parts) dist_touched_.push_back(m);
@@ -3174,34 +3180,34 @@ struct DistReader {
 };
 }  // namespace
 
-// Values (front blocks and W factors) travel device to device: the sending rank gathers them
-// into one cudaMalloc'ed buffer and sends its CUDA IPC handle with the metadata; rank 0 opens
-// it (peer memory over NVLink on a multi-GPU node, the same memory when the ranks share a
-// GPU) and its gather kernels read the values in place; an acknowledgement releases the
-// buffer.  SPQR_DIST_HOST=1 sends the values inline through the host transport instead.
-std::vector<char> Engine::dist_export() {
+// Values (front blocks and W factors) travel device to device: each rank gathers them into
+// one cudaMalloc'ed buffer and sends its CUDA IPC handle with the metadata; the other ranks open
+// it (peer memory over NVLink on a multi-GPU node, the same memory when the ranks share a GPU)
+// and their gather kernels read the values in place; acknowledgements release the buffer.
+// SPQR_DIST_HOST=1 sends the values inline through the host transport instead.
+std::vector<char> Engine::dist_export(int k) {
     static const bool host_mode = std::getenv("SPQR_DIST_HOST") != nullptr;
     DistWriter w;
     w.i64(0x53505144);  // "SPQD"
     w.i64(host_mode ? 0 : 1);
     std::vector<int> el;
-    for (int c : stage_list_[L_ + 1])
+    for (int c : stage_list_[k])
         if (dist_owner_[c] == dist_->rank && gone_[c]) el.push_back(c);
-    // touched fronts and their transformed rows
     std::sort(dist_touched_.begin(), dist_touched_.end());
     dist_touched_.erase(std::unique(dist_touched_.begin(), dist_touched_.end()), dist_touched_.end());
     std::vector<int> T;
     for (int f : dist_touched_)
         if (!gone_[f] && fr_[f].live) T.push_back(f);
     std::sort(dist_tr_.begin(), dist_tr_.end());
-    // value space: every touched front's blocks in ascending key order (ld = rows), then every
-    // W factor's [R | C] (ld = c)
-    std::vector<long long> voff(T.size() + 1, 0), woff(out_.W.size() + 1, 0);
+    // value space: every touched front's blocks in ascending key order (ld = rows), then this
+    // stage's W factors' [R | C] (ld = c)
+    std::vector<long long> voff(T.size() + 1, 0);
     for (size_t t = 0; t < T.size(); ++t) voff[t + 1] = voff[t] + static_cast<long long>(fr_[T[t]].nrows()) * fr_[T[t]].ncols;
-    woff[0] = voff.back();
-    for (size_t q = 0; q < out_.W.size(); ++q) {
-        const DevWFactor& f = out_.W[q];
-        if (f.kind != 0) throw std::logic_error("distributed factorization: rotation factor at the leaf stage");
+    const size_t nw = out_.W.size() - dist_w0_;
+    std::vector<long long> woff(nw + 1, voff.back());
+    for (size_t q = 0; q < nw; ++q) {
+        const DevWFactor& f = out_.W[dist_w0_ + q];
+        if (f.kind != 0) throw std::logic_error("distributed factorization: rotation factor in a split stage");
         woff[q + 1] = woff[q] + static_cast<long long>(f.c) * (f.c + f.k);
     }
     const long long total = woff.back();
@@ -3222,8 +3228,8 @@ std::vector<char> Engine::dist_export() {
             o += F.keys[q].width;
         }
     }
-    for (size_t q = 0; q < out_.W.size(); ++q) {
-        const DevWFactor& f = out_.W[q];
+    for (size_t q = 0; q < nw; ++q) {
+        const DevWFactor& f = out_.W[dist_w0_ + q];
         if (f.c == 0) continue;
         const int di = gb.begin(dv + woff[q], f.c, f.c, f.c + f.k, 1, 1);
         gb.source(di, 0) = AsmSrc{f.a, 1, f.c};
@@ -3240,9 +3246,9 @@ std::vector<char> Engine::dist_export() {
         w.i64(total);
     }
     w.ivec(el);
-    w.i64(static_cast<long long>(out_.W.size()));
-    for (size_t q = 0; q < out_.W.size(); ++q) {
-        const DevWFactor& f = out_.W[q];
+    w.i64(static_cast<long long>(nw));
+    for (size_t q = 0; q < nw; ++q) {
+        const DevWFactor& f = out_.W[dist_w0_ + q];
         const int meta[4] = {f.cluster, f.c, f.k, f.scale_only ? 1 : 0};
         w.put(meta, 4);
         w.put(out_.idx.data() + f.cols_off, f.c);
@@ -3256,8 +3262,8 @@ std::vector<char> Engine::dist_export() {
             piv.push_back(static_cast<int>(out_.pivot_row[j]));
         }
     w.ivec(piv);
-    w.i64(npiv_);
-    std::vector<int> trail(out_.trailing_rows.begin(), out_.trailing_rows.end());
+    w.i64(npiv_ - dist_npiv0_);
+    std::vector<int> trail(out_.trailing_rows.begin() + dist_t0_, out_.trailing_rows.end());
     w.ivec(trail);
     w.i64(static_cast<long long>(T.size()));
     size_t q0 = 0;
@@ -3266,9 +3272,9 @@ std::vector<char> Engine::dist_export() {
         w.i64(T[t]);
         w.ivec(F.rows);
         std::vector<int> kw;
-        for (const KeyRef& k : F.keys) {
-            kw.push_back(k.key);
-            kw.push_back(k.width);
+        for (const KeyRef& kr : F.keys) {
+            kw.push_back(kr.key);
+            kw.push_back(kr.width);
         }
         w.ivec(kw);
         std::vector<int> tr;
@@ -3288,183 +3294,250 @@ std::vector<char> Engine::dist_export() {
     return std::move(w.b);
 }
 
-// returns true when the sender's values came through CUDA IPC (the sender waits for an ack)
-bool Engine::dist_import(const char* buf, size_t n) {
-    DistReader r{buf, n};
-    if (r.i64() != 0x53505144) throw std::runtime_error("distributed factorization: bad message");
-    const bool ipc = r.i64() == 1;
-    const double* vp = nullptr;
-    double* peer = nullptr;
-    long long total = 0;
-    if (ipc) {
-        cudaIpcMemHandle_t hnd;
-        r.get(reinterpret_cast<char*>(&hnd), sizeof hnd);
-        total = r.i64();
-        void* p = nullptr;
-        CK(cudaIpcOpenMemHandle(&p, hnd, cudaIpcMemLazyEnablePeerAccess));
-        peer = static_cast<double*>(p);
-        vp = peer;
-    }
-    struct PeerGuard {  // the mapping is closed on every exit path
-        double*& p;
-        ~PeerGuard() {
-            if (p) cudaIpcCloseMemHandle(p);
-        }
-    } guard{peer};
-    const std::vector<int> el = r.ivec();
-    for (int c : el) {
-        if (c < 0 || static_cast<size_t>(c) >= fr_.size()) throw std::runtime_error("distributed factorization: bad cluster");
-        for (const KeyRef& k : fr_[c].keys) holders_[k.key].remove(c);
-        holders_[c].clear();
-        gone_[c] = 1;
-        alive_[c] = 0;
-        dfree(fr_[c].mat, fr_[c].big);
-        fr_[c].retire();
-    }
-    const long long nw = r.i64();
+// Apply the other ranks' effects of this stage (msgs[rank]; this rank's own entry is empty, its
+// effects are already in place): every rank ends with the state the sequential engine would
+// have after the stage.  Each touched front becomes: its rows at the start of the stage in order,
+// minus every rank's pivots, then the rows each rank appended in rank order (= ascending source
+// cluster); a row's values come from the rank that transformed or appended it, else from this
+// rank's copy; its keys are the union minus the eliminated clusters.
+void Engine::dist_apply(const std::vector<std::vector<char>>& msgs) {
+    const int G = dist_->size, me = dist_->rank;
     struct WIn {
         int cl, c, k, so;
         std::vector<int> cols, cp;
         long long off;
     };
-    std::vector<WIn> ws(nw);
-    long long wtot = 0;
-    for (auto& f : ws) {
-        int meta[4];
-        r.get(meta, 4);
-        f.cl = meta[0], f.c = meta[1], f.k = meta[2], f.so = meta[3];
-        f.cols.resize(f.c);
-        f.cp.resize(f.k);
-        r.get(f.cols.data(), f.c);
-        r.get(f.cp.data(), f.k);
-        f.off = r.i64();
-        wtot += static_cast<long long>(f.c) * (f.c + f.k);
-    }
-    const std::vector<int> piv = r.ivec();
-    const long long npiv = r.i64();
-    const std::vector<int> trail = r.ivec();
-    const long long nf = r.i64();
     struct FIn {
         int f;
         std::vector<int> rows, kw, tr;
         long long off;
     };
-    std::vector<FIn> fs(nf);
-    for (auto& x : fs) {
-        x.f = static_cast<int>(r.i64());
-        if (x.f < 0 || static_cast<size_t>(x.f) >= fr_.size() || !fr_[x.f].live)
-            throw std::runtime_error("distributed factorization: front not live on rank 0");
-        x.rows = r.ivec();
-        x.kw = r.ivec();
-        x.tr = r.ivec();
-        x.off = r.i64();
-    }
-    if (!ipc) {  // values inline: onto the device
-        total = r.i64();
-        std::vector<double> hv(static_cast<size_t>(std::max<long long>(total, 0)));
-        r.get(hv.data(), hv.size());
-        double* d = arena().alloc_n<double>(std::max<long long>(total, 1));
-        if (total > 0) CK(cudaMemcpyAsync(d, hv.data(), sizeof(double) * total, cudaMemcpyHostToDevice, st_));
-        vp = d;
-        sync();  // hv is released on return
-    }
-    AsmBuilder& mb = asm_slot(0);
-    // W factors: gathered into one W-arena block
-    double* dw = out_.warena->alloc_n<double>(std::max<long long>(wtot, 1));
-    long long o = 0;
-    for (const auto& f : ws) {
-        DevWFactor& d = new_factor(0, f.cl, f.c, f.k, f.cols, f.so ? nullptr : &f.cp);
-        d.a = dw + o;
-        if (f.c > 0) {
-            const int di = mb.begin(d.a, f.c, f.c, f.c + f.k, 1, 1);
-            mb.source(di, 0) = AsmSrc{vp + f.off, 1, f.c};
-            for (int i = 0; i < f.c; ++i) mb.row(di, i) = int4{0, i, -1, 0};
-            mb.seg(di, 0, 0);
-            mb.km(di, 0, 0) = 0;
+    struct Msg {
+        std::vector<int> el, piv, trail;
+        long long npiv = 0;
+        std::vector<WIn> ws;
+        std::vector<FIn> fs;
+        const double* vp = nullptr;
+        double* peer = nullptr;
+        std::vector<double> inline_vals;
+    };
+    std::vector<Msg> M(G);
+    struct PeerClose {
+        std::vector<Msg>& m;
+        ~PeerClose() {
+            for (auto& x : m)
+                if (x.peer) cudaIpcCloseMemHandle(x.peer);
         }
-        o += static_cast<long long>(f.c) * (f.c + f.k);
+    } closer{M};
+    for (int r = 0; r < G; ++r) {
+        if (r == me) continue;
+        DistReader rd{msgs[r].data(), msgs[r].size()};
+        if (rd.i64() != 0x53505144) throw std::runtime_error("distributed factorization: bad message");
+        const bool ipc = rd.i64() == 1;
+        Msg& m = M[r];
+        if (ipc) {
+            cudaIpcMemHandle_t hnd;
+            rd.get(reinterpret_cast<char*>(&hnd), sizeof hnd);
+            rd.i64();
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, hnd, cudaIpcMemLazyEnablePeerAccess));
+            m.peer = static_cast<double*>(p);
+            m.vp = m.peer;
+        }
+        m.el = rd.ivec();
+        const long long nw = rd.i64();
+        m.ws.resize(nw);
+        for (auto& f : m.ws) {
+            int meta[4];
+            rd.get(meta, 4);
+            f.cl = meta[0], f.c = meta[1], f.k = meta[2], f.so = meta[3];
+            f.cols.resize(f.c);
+            f.cp.resize(f.k);
+            rd.get(f.cols.data(), f.c);
+            rd.get(f.cp.data(), f.k);
+            f.off = rd.i64();
+        }
+        m.piv = rd.ivec();
+        m.npiv = rd.i64();
+        m.trail = rd.ivec();
+        const long long nf = rd.i64();
+        m.fs.resize(nf);
+        for (auto& x : m.fs) {
+            x.f = static_cast<int>(rd.i64());
+            if (x.f < 0 || static_cast<size_t>(x.f) >= fr_.size()) throw std::runtime_error("distributed factorization: bad front");
+            x.rows = rd.ivec();
+            x.kw = rd.ivec();
+            x.tr = rd.ivec();
+            x.off = rd.i64();
+        }
+        if (!ipc) {
+            const long long total = rd.i64();
+            m.inline_vals.resize(static_cast<size_t>(std::max<long long>(total, 0)));
+            rd.get(m.inline_vals.data(), m.inline_vals.size());
+            double* d = arena().alloc_n<double>(std::max<long long>(total, 1));
+            if (total > 0) CK(cudaMemcpyAsync(d, m.inline_vals.data(), sizeof(double) * total, cudaMemcpyHostToDevice, st_));
+            m.vp = d;
+        }
     }
-    for (size_t i = 0; i + 1 < piv.size(); i += 2) out_.pivot_row[piv[i]] = piv[i + 1];
-    npiv_ += npiv;
-    out_.trailing_rows.insert(out_.trailing_rows.end(), trail.begin(), trail.end());
-    // fronts: rank 0's version (source 0) merged with the sender's (source 1, read in place)
+    // eliminated clusters of every other rank
+    for (int r = 0; r < G; ++r)
+        for (int c : M[r].el) {
+            if (c < 0 || static_cast<size_t>(c) >= fr_.size()) throw std::runtime_error("distributed factorization: bad cluster");
+            for (const KeyRef& kr : fr_[c].keys) holders_[kr.key].remove(c);
+            holders_[c].clear();
+            gone_[c] = 1;
+            alive_[c] = 0;
+            dfree(fr_[c].mat, fr_[c].big);
+            fr_[c].retire();
+        }
+    AsmBuilder& mb = asm_slot(0);
+    // W factors, pivots, trailing rows (this stage's trailing rows rebuilt in rank order)
+    std::vector<int> own_trail(out_.trailing_rows.begin() + dist_t0_, out_.trailing_rows.end());
+    out_.trailing_rows.resize(dist_t0_);
+    for (int r = 0; r < G; ++r) {
+        if (r == me) {
+            out_.trailing_rows.insert(out_.trailing_rows.end(), own_trail.begin(), own_trail.end());
+            continue;
+        }
+        const Msg& m = M[r];
+        long long wtot = 0;
+        for (const auto& f : m.ws) wtot += static_cast<long long>(f.c) * (f.c + f.k);
+        double* dw = out_.warena->alloc_n<double>(std::max<long long>(wtot, 1));
+        long long o = 0;
+        for (const auto& f : m.ws) {
+            DevWFactor& d = new_factor(0, f.cl, f.c, f.k, f.cols, f.so ? nullptr : &f.cp);
+            d.a = dw + o;
+            if (f.c > 0) {
+                const int di = mb.begin(d.a, f.c, f.c, f.c + f.k, 1, 1);
+                mb.source(di, 0) = AsmSrc{m.vp + f.off, 1, f.c};
+                for (int i = 0; i < f.c; ++i) mb.row(di, i) = int4{0, i, -1, 0};
+                mb.seg(di, 0, 0);
+                mb.km(di, 0, 0) = 0;
+            }
+            o += static_cast<long long>(f.c) * (f.c + f.k);
+        }
+        for (size_t i = 0; i + 1 < m.piv.size(); i += 2) out_.pivot_row[m.piv[i]] = m.piv[i + 1];
+        npiv_ += m.npiv;
+        out_.trailing_rows.insert(out_.trailing_rows.end(), m.trail.begin(), m.trail.end());
+    }
+    // touched fronts: versions by front
+    std::map<int, std::vector<std::pair<int, const FIn*>>> byf;
+    for (int r = 0; r < G; ++r)
+        for (const auto& x : M[r].fs) byf[x.f].emplace_back(r, &x);
     std::vector<std::pair<int, Front>> repl;
-    for (const auto& x : fs) {
-        const Front& C = fr_[x.f];
-        const std::vector<int>& init = init_rows_[x.f];
-        std::vector<int> sinit(init), sr(x.rows), str(x.tr);
-        std::sort(sinit.begin(), sinit.end());
-        std::sort(sr.begin(), sr.end());
-        std::sort(str.begin(), str.end());
-        auto in = [](const std::vector<int>& v, int a) { return std::binary_search(v.begin(), v.end(), a); };
+    auto in = [](const std::vector<int>& v, int a) { return std::binary_search(v.begin(), v.end(), a); };
+    for (const auto& [f, vers] : byf) {
+        if (gone_[f] || !fr_[f].live) throw std::runtime_error("distributed factorization: touched front not live");
+        const Front& C = fr_[f];
+        const std::vector<int>& start = start_rows_[f];
+        std::vector<int> sstart(start), sc(C.rows);
+        std::sort(sstart.begin(), sstart.end());
+        std::sort(sc.begin(), sc.end());
+        const int nv = static_cast<int>(vers.size());
+        std::vector<std::vector<int>> sr(nv), str(nv);
+        std::vector<std::vector<std::pair<int, int>>> pos(nv);
+        for (int v = 0; v < nv; ++v) {
+            const FIn& x = *vers[v].second;
+            sr[v] = x.rows;
+            std::sort(sr[v].begin(), sr[v].end());
+            str[v] = x.tr;
+            std::sort(str[v].begin(), str[v].end());
+            for (size_t i = 0; i < x.rows.size(); ++i) pos[v].emplace_back(x.rows[i], static_cast<int>(i));
+            std::sort(pos[v].begin(), pos[v].end());
+        }
+        std::vector<std::pair<int, int>> cpos;
+        for (int i = 0; i < C.nrows(); ++i) cpos.emplace_back(C.rows[i], i);
+        std::sort(cpos.begin(), cpos.end());
+        auto find = [](const std::vector<std::pair<int, int>>& pv, int g) {
+            auto it = std::lower_bound(pv.begin(), pv.end(), std::make_pair(g, INT_MIN));
+            if (it == pv.end() || it->first != g) throw std::logic_error("distributed factorization: row missing");
+            return it->second;
+        };
         Front nf;
         nf.live = true;
-        std::vector<int2> src;  // (source, row)
-        for (int i = 0; i < C.nrows(); ++i) {
-            const int g = C.rows[i];
-            if (in(sinit, g) && !in(sr, g)) continue;  // taken as a pivot by the sending rank
-            nf.rows.push_back(g);
-            src.push_back(int2{0, i});
-        }
-        for (size_t i = 0; i < x.rows.size(); ++i)
-            if (!in(sinit, x.rows[i])) {  // appended by the sending rank: after everything rank 0 holds
-                nf.rows.push_back(x.rows[i]);
-                src.push_back(int2{1, static_cast<int>(i)});
-            }
-        {  // rows the sending rank transformed in place take its values
-            std::vector<std::pair<int, int>> rp;
-            for (size_t i = 0; i < x.rows.size(); ++i) rp.emplace_back(x.rows[i], static_cast<int>(i));
-            std::sort(rp.begin(), rp.end());
-            for (size_t i = 0; i < nf.rows.size(); ++i)
-                if (src[i].x == 0 && in(str, nf.rows[i])) {
-                    auto it = std::lower_bound(rp.begin(), rp.end(), std::make_pair(nf.rows[i], INT_MIN));
-                    if (it == rp.end() || it->first != nf.rows[i]) throw std::logic_error("distributed factorization: transformed row missing");
-                    src[i] = int2{1, it->second};
+        std::vector<int2> src;  // (source: 0 = this rank's front, 1 + v = version v; row)
+        for (int g : start) {
+            if (!in(sc, g)) continue;  // a pivot of this rank
+            bool kept = true;
+            for (int v = 0; v < nv && kept; ++v) kept = in(sr[v], g);
+            if (!kept) continue;  // a pivot of another rank
+            int s0 = 0, row = find(cpos, g);
+            for (int v = 0; v < nv; ++v)
+                if (in(str[v], g)) {
+                    s0 = 1 + v;
+                    row = find(pos[v], g);
                 }
+            nf.rows.push_back(g);
+            src.push_back(int2{s0, row});
         }
-        // keys: both versions', minus the clusters eliminated by any rank
+        int vi = 0;
+        for (int r = 0; r < G; ++r) {  // appended rows in rank order
+            if (r == me) {
+                for (int i = 0; i < C.nrows(); ++i)
+                    if (!in(sstart, C.rows[i])) {
+                        nf.rows.push_back(C.rows[i]);
+                        src.push_back(int2{0, i});
+                    }
+                continue;
+            }
+            while (vi < nv && vers[vi].first < r) ++vi;
+            if (vi < nv && vers[vi].first == r) {
+                const FIn& x = *vers[vi].second;
+                for (size_t i = 0; i < x.rows.size(); ++i)
+                    if (!in(sstart, x.rows[i])) {
+                        nf.rows.push_back(x.rows[i]);
+                        src.push_back(int2{1 + vi, static_cast<int>(i)});
+                    }
+            }
+        }
+        // keys: every version's, minus the clusters eliminated by any rank
         std::vector<std::pair<int, int>> ks;
-        for (const KeyRef& k : C.keys)
-            if (!gone_[k.key]) ks.emplace_back(k.key, k.width);
-        std::vector<int> roff;  // sender's column offset per key (ascending)
-        int oc = 0;
-        for (size_t q = 0; q + 1 < x.kw.size(); q += 2) {
-            roff.push_back(oc);
-            oc += x.kw[q + 1];
-            if (!gone_[x.kw[q]]) ks.emplace_back(x.kw[q], x.kw[q + 1]);
+        for (const KeyRef& kr : C.keys)
+            if (!gone_[kr.key]) ks.emplace_back(kr.key, kr.width);
+        std::vector<std::vector<int>> roff(nv);
+        for (int v = 0; v < nv; ++v) {
+            const FIn& x = *vers[v].second;
+            int o = 0;
+            for (size_t q = 0; q + 1 < x.kw.size(); q += 2) {
+                roff[v].push_back(o);
+                o += x.kw[q + 1];
+                if (!gone_[x.kw[q]]) ks.emplace_back(x.kw[q], x.kw[q + 1]);
+            }
         }
         std::sort(ks.begin(), ks.end());
         ks.erase(std::unique(ks.begin(), ks.end(), [](const auto& a, const auto& b) { return a.first == b.first; }), ks.end());
-        for (const auto& k : ks) nf.keys.push_back(KeyRef{k.first, k.second, 0});
-        layout(x.f, nf.keys, nf.ncols);
+        for (const auto& kk : ks) nf.keys.push_back(KeyRef{kk.first, kk.second, 0});
+        layout(f, nf.keys, nf.ncols);
         nf.ld = std::max(1, nf.nrows());
         nf.mat = dalloc(arena(), static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1), nf.big);
         std::vector<int> ord;
         phys_order(nf.keys, ord);
-        const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, 2, static_cast<int>(ord.size()));
+        const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, 1 + nv, static_cast<int>(ord.size()));
         mb.source(di, 0) = AsmSrc{C.mat, 1, C.ld};
-        mb.source(di, 1) = AsmSrc{vp + x.off, 1, static_cast<long long>(std::max<size_t>(x.rows.size(), 1))};
+        for (int v = 0; v < nv; ++v) {
+            const FIn& x = *vers[v].second;
+            mb.source(di, 1 + v) = AsmSrc{M[vers[v].first].vp + x.off, 1, static_cast<long long>(std::max<size_t>(x.rows.size(), 1))};
+        }
         for (int i = 0; i < nf.nrows(); ++i) mb.row(di, i) = int4{src[i].x, src[i].y, -1, 0};
         for (size_t q = 0; q < ord.size(); ++q) {
-            const KeyRef& k = nf.keys[ord[q]];
-            mb.seg(di, static_cast<int>(q), k.col);
-            const int ci = C.find(k.key);
+            const KeyRef& kr = nf.keys[ord[q]];
+            mb.seg(di, static_cast<int>(q), kr.col);
+            const int ci = C.find(kr.key);
             mb.km(di, static_cast<int>(q), 0) = ci >= 0 ? C.keys[ci].col : -1;
-            int ri = -1;
-            for (size_t t = 0; t + 1 < x.kw.size(); t += 2)
-                if (x.kw[t] == k.key) ri = roff[t / 2];
-            mb.km(di, static_cast<int>(q), 1) = ri;
-            if (ci < 0) holders_[k.key].add(x.f);
+            for (int v = 0; v < nv; ++v) {
+                const FIn& x = *vers[v].second;
+                int ri = -1;
+                for (size_t t = 0; t + 1 < x.kw.size(); t += 2)
+                    if (x.kw[t] == kr.key) ri = roff[v][t / 2];
+                mb.km(di, static_cast<int>(q), 1 + v) = ri;
+            }
+            if (ci < 0) holders_[kr.key].add(f);
         }
         mb.drop_if_empty();
-        repl.emplace_back(x.f, std::move(nf));
+        repl.emplace_back(f, std::move(nf));
     }
     flush_assemble(mb);
-    sync();  // every read of the sender's values done (its buffer may go)
-    if (peer) {
-        CK(cudaIpcCloseMemHandle(peer));
-        peer = nullptr;
-    }
+    sync();  // every read of the other ranks' values is done
     for (auto& pr : repl) {
         Front& F = fr_[pr.first];
         dfree(F.mat, F.big);
@@ -3478,68 +3551,80 @@ bool Engine::dist_import(const char* buf, size_t n) {
         F.tag.clear();
         F.soff.clear();
     }
-    (void)total;
-    return ipc;
 }
 
-void Engine::dist_exchange(int err_cluster, const std::string& err_reason) {
+// One split stage's exchange: every rank's effects (or its first failing cluster) to every
+// other rank, in rank order (rank r sends while the others receive from r), then all apply.
+void Engine::dist_exchange(int k, int err_cluster, const std::string& err_reason) {
     const double t0 = now_s();
-    if (dist_->rank != 0) {
-        if (err_cluster >= 0) {  // length -1: an error record (cluster, reason) instead of the effects
-            const long long n = -1;
-            const int cl = err_cluster, len = static_cast<int>(err_reason.size());
-            if (dist_->send(dist_->user, 0, &n, sizeof n) || dist_->send(dist_->user, 0, &cl, sizeof cl) ||
-                dist_->send(dist_->user, 0, &len, sizeof len) ||
-                (len > 0 && dist_->send(dist_->user, 0, err_reason.data(), len)))
-                throw std::runtime_error("distributed factorization: send to rank 0 failed");
-            throw SingularFrontError(err_cluster, err_reason);
-        }
-        const std::vector<char> b = dist_export();
-        const long long n = static_cast<long long>(b.size());
-        if (dist_->send(dist_->user, 0, &n, sizeof n) || dist_->send(dist_->user, 0, b.data(), n))
-            throw std::runtime_error("distributed factorization: send to rank 0 failed");
-        out_.dist_bytes += n;
-        if (dist_vbuf_) {  // rank 0 has read the values in place: release them
-            long long ack = 0;
-            if (dist_->recv(dist_->user, 0, &ack, sizeof ack)) throw std::runtime_error("distributed factorization: receive failed");
-            CK(cudaFree(dist_vbuf_));
-            dist_vbuf_ = nullptr;
-        }
+    const int G = dist_->size, me = dist_->rank;
+    std::vector<char> own;
+    if (err_cluster >= 0) {  // an error record: magic, -1, cluster, reason
+        DistWriter w;
+        w.i64(0x53505144);
+        w.i64(-1);
+        w.i64(err_cluster);
+        w.ivec(std::vector<int>(err_reason.begin(), err_reason.end()));
+        own = std::move(w.b);
     } else {
-        int ecl = err_cluster;
-        std::string why = err_reason;
-        for (int q = 1; q < dist_->size; ++q) {  // ascending ranks = ascending source clusters
+        own = dist_export(k);
+    }
+    auto fail = [] { throw std::runtime_error("distributed factorization: transport failed"); };
+    std::vector<std::vector<char>> msgs(G);
+    for (int r = 0; r < G; ++r) {
+        if (r == me) {
+            const long long n = static_cast<long long>(own.size());
+            for (int q = 0; q < G; ++q)
+                if (q != me && (dist_->send(dist_->user, q, &n, sizeof n) || dist_->send(dist_->user, q, own.data(), n))) fail();
+            out_.dist_bytes += n * (G - 1);
+        } else {
             long long n = 0;
-            if (dist_->recv(dist_->user, q, &n, sizeof n)) throw std::runtime_error("distributed factorization: receive failed");
-            if (n < 0) {
-                int cl = -1, len = 0;
-                if (dist_->recv(dist_->user, q, &cl, sizeof cl) || dist_->recv(dist_->user, q, &len, sizeof len))
-                    throw std::runtime_error("distributed factorization: receive failed");
-                std::string rs(static_cast<size_t>(std::max(len, 0)), '\0');
-                if (len > 0 && dist_->recv(dist_->user, q, rs.data(), len)) throw std::runtime_error("distributed factorization: receive failed");
-                if (ecl < 0 || cl < ecl) {
-                    ecl = cl;
-                    why = rs;
-                }
-                continue;
-            }
-            std::vector<char> b(static_cast<size_t>(n));
-            if (n > 0 && dist_->recv(dist_->user, q, b.data(), n)) throw std::runtime_error("distributed factorization: receive failed");
-            out_.dist_bytes += n;
-            // after an error only the error matters, but an IPC sender still waits for its ack
-            DistReader hdr{b.data(), b.size()};
-            const bool ipc = b.size() >= 16 && (hdr.i64(), hdr.i64() == 1);
-            if (ecl < 0) dist_import(b.data(), b.size());
-            if (ipc) {
-                const long long ack = 1;
-                if (dist_->send(dist_->user, q, &ack, sizeof ack)) throw std::runtime_error("distributed factorization: send failed");
+            if (dist_->recv(dist_->user, r, &n, sizeof n)) fail();
+            msgs[r].resize(static_cast<size_t>(std::max<long long>(n, 0)));
+            if (n > 0 && dist_->recv(dist_->user, r, msgs[r].data(), n)) fail();
+        }
+    }
+    auto mode = [](const std::vector<char>& b) {  // -1 error, 0 inline values, 1 IPC values
+        DistReader rd{b.data(), b.size()};
+        rd.i64();
+        return static_cast<int>(rd.i64());
+    };
+    int ecl = err_cluster;
+    std::string why = err_reason;
+    for (int r = 0; r < G; ++r)
+        if (r != me && mode(msgs[r]) == -1) {
+            DistReader rd{msgs[r].data(), msgs[r].size()};
+            rd.i64();
+            rd.i64();
+            const int cl = static_cast<int>(rd.i64());
+            const std::vector<int> rv = rd.ivec();
+            if (ecl < 0 || cl < ecl) {
+                ecl = cl;
+                why.assign(rv.begin(), rv.end());
             }
         }
-        if (ecl >= 0) throw SingularFrontError(ecl, why);
-        // W in the reference's chronological order (ascending cluster) within the leaf stage
-        std::stable_sort(out_.W.begin(), out_.W.end(), [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
+    if (ecl < 0) dist_apply(msgs);
+    // acknowledgements: rank r's IPC buffer is released once every other rank has read it
+    for (int r = 0; r < G; ++r) {
+        const long long ack = 1;
+        if (r == me) {
+            if (dist_vbuf_) {
+                for (int q = 0; q < G; ++q) {
+                    long long a = 0;
+                    if (q != me && dist_->recv(dist_->user, q, &a, sizeof a)) fail();
+                }
+                CK(cudaFree(dist_vbuf_));
+                dist_vbuf_ = nullptr;
+            }
+        } else if (mode(msgs[r]) == 1) {
+            if (dist_->send(dist_->user, r, &ack, sizeof ack)) fail();
+        }
     }
-    out_.dist_exchange_s = now_s() - t0;
+    if (ecl >= 0) throw SingularFrontError(ecl, why);
+    // W in the reference's chronological order (ascending cluster) within the stage
+    std::stable_sort(out_.W.begin() + dist_w0_, out_.W.end(),
+                     [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
+    out_.dist_exchange_s += now_s() - t0;
 }
 
 DeviceFactorization Engine::run() {  // factorize.cpp:745-790
@@ -3551,9 +3636,18 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         sprof_.back().stage = k;
         const HostProf before = prof_;
         double t0 = now_s();
-        if (dist_ && k == L_ + 1) {
-            // a rank whose leaves fail still reports to rank 0, which raises the first failing
-            // cluster of all ranks (ascending ids: what the sequential engine would raise)
+        if (dist_stage(k)) {
+            // a split stage: every rank eliminates its own subtree's clusters from the same state,
+            // then all exchange their effects; a rank whose elimination fails still reports, and
+            // every rank raises the first failing cluster of all ranks (the sequential error)
+            start_rows_.assign(fr_.size(), std::vector<int>());
+            for (size_t c = 0; c < fr_.size(); ++c)
+                if (alive_[c] && fr_[c].live) start_rows_[c] = fr_[c].rows;
+            dist_w0_ = out_.W.size();
+            dist_t0_ = out_.trailing_rows.size();
+            dist_npiv0_ = npiv_;
+            dist_touched_.clear();
+            dist_tr_.clear();
             int ecl = -1;
             std::string why;
             try {
@@ -3562,8 +3656,8 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
                 ecl = e.cluster;
                 why = e.reason;
             }
-            dist_exchange(ecl, why);
-            if (dist_->rank != 0) {  // this rank's part is with rank 0
+            dist_exchange(k, ecl, why);
+            if (k == dist_kend_ && dist_->rank != 0) {  // the rest runs on rank 0
                 out_.dist_partial = true;
                 break;
             }
