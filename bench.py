@@ -41,8 +41,9 @@ def config(ws):
     """The `config` object of both arms' JSON lines (identical keys and values)."""
     return {"workload": WORKLOAD, "N": 262144, "M": 524288, "levels": 14, "eps": 1e-2, "skip_levels": 3,
             "cgls_tol": 1e-12, "seed": 0,
-            "parallelism": (f"subtree split over {ws} GPUs: leaf stage per rank, then gathered on rank 0 "
-                            "(spqr_pipeline_create_dist)") if ws > 1 else "1 GPU",
+            "parallelism": (f"subtree split over {ws} GPUs: the stages before the first scale_all run per rank on "
+                            "its own subtree (top-separator fronts re-merged after every stage), then gathered "
+                            "on rank 0 (spqr_pipeline_create_dist)") if ws > 1 else "1 GPU",
             "l2_flush": "256 MB write between steps (ours); the CPU arm has no device state"}
 
 
@@ -56,8 +57,13 @@ def dist_init():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # N > 1 runs ONE factorization across the ranks (spqr_pipeline_create_dist): the ranks
-    # share the leaf stage, then rank 0 works alone, so every rank keeps the host's threads
+    # share the host's cores during the split stages, then rank 0 works alone with all of them
+    # (torchrun's OMP_NUM_THREADS=1 would serialise the host bookkeeping)
     if ws > 1:
+        ncpu = len(os.sched_getaffinity(0))
+        lws = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
+        os.environ.setdefault("SPQR_HOST_THREADS", str(max(1, (ncpu - 1) // lws)))
+        os.environ.setdefault("SPQR_HOST_THREADS_ROOT", str(max(1, ncpu - 1)))
         import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -348,7 +354,7 @@ def run_ours(args, ws, rank, local):
     value = allmax(ws, sum(dev_t) / len(dev_t))
     e2e = allmax(ws, sum(e2e_t) / len(e2e_t))
     g, rep = last
-    if not g.is_root:  # this rank's leaf stage went to rank 0, which reports the step
+    if not g.is_root:  # this rank's subtree went to rank 0, which reports the step
         if not args.no_microbench:
             front_qr_microbench(local, ws, rank)
         return
@@ -408,9 +414,12 @@ def run_ours(args, ws, rank, local):
                   "solve_plan_s": round(t["solve_plan_s"], 4), "solve_launches": t["solve_launches"]},
     }
     if ws > 1:
-        out["distributed"] = {"exchange_s_rank0": round(g.dist_exchange_s, 4), "bytes_to_rank0": g.dist_bytes,
-                              "note": "each rank eliminates its subtree's leaves; ranks > 0 send their effects "
-                                      "to rank 0, which finishes; value = max over ranks"}
+        out["distributed"] = {"exchange_s_rank0": round(g.dist_exchange_s, 4), "exchange_bytes_rank0": g.dist_bytes,
+                              "host_threads": [os.environ.get("SPQR_HOST_THREADS"), os.environ.get("SPQR_HOST_THREADS_ROOT")],
+                              "note": "each rank eliminates its subtree's clusters through the split stages; the "
+                                      "top-separator fronts are re-merged after every stage; ranks > 0 then send "
+                                      "their subtree to rank 0, which finishes; exchange bytes = host metadata + "
+                                      "values read over peer memory (CUDA IPC); value = max over ranks"}
     if not args.no_microbench:
         try:
             mb = front_qr_microbench(local, ws, rank)

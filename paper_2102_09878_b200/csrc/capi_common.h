@@ -49,11 +49,15 @@ int capi_guarded(char* err, int errlen, int* err_cluster, F&& f) {
     }
 }
 
-// Host bookkeeping threads: all cores but one (measured best on the 16-core B200 hosts)
-// unless the user chose a count.
+// Host bookkeeping threads: SPQR_HOST_THREADS if set (one process per GPU shares the host's
+// cores: torchrun exports OMP_NUM_THREADS=1), else all cores but one (measured best on the
+// 16-core B200 hosts) unless the user chose an OpenMP count.
 inline void capi_set_threads() {
 #ifdef _OPENMP
-    if (!std::getenv("OMP_NUM_THREADS")) {
+    if (const char* s = std::getenv("SPQR_HOST_THREADS")) {
+        const int n = std::atoi(s);
+        if (n > 0) omp_set_num_threads(n);
+    } else if (!std::getenv("OMP_NUM_THREADS")) {
         const int np = omp_get_num_procs();
         omp_set_num_threads(np > 1 ? np - 1 : 1);
     }

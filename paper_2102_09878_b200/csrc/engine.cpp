@@ -547,6 +547,16 @@ public:
             while ((1 << lg) < dist_->size) ++lg;
             const int ksp = (opt.eps > 0.0 && L_ + 1 - opt.skip_levels >= 2) ? L_ + 1 - opt.skip_levels : 0;
             dist_kend_ = std::max(lg + 1, ksp);
+            dist_top_.assign(h.clusters.size(), 0);  // pieces of the top lg separators: every rank keeps them
+            for (size_t c = 0; c < h.clusters.size(); ++c) dist_top_[c] = h.tree->nodes[h.clusters[c].tree_node].level <= lg;
+            // merges stay inside one subtree (or among the top pieces): a parent cluster has its
+            // children's tree node, so the partitioned state is closed under merge_level
+            for (size_t c = 0; c < h.clusters.size(); ++c) {
+                const int P = h.clusters[c].parent;
+                if (P >= 0 && (dist_top_[P] != dist_top_[c] || (!dist_top_[c] && dist_owner_[P] != dist_owner_[c])))
+                    throw std::logic_error("distributed factorization: a merge crosses subtrees (cluster " + std::to_string(c) + ")");
+            }
+            if (opt.store_q) throw std::invalid_argument("a distributed factorization does not record Q");
         }
         if (opt.store_q) out_.qarena = std::make_unique<DeviceArena>(size_t(64) << 20);
         const size_t nc = h.clusters.size();
@@ -825,14 +835,28 @@ private:
     int dist_kend_ = 0;
     bool dist_stage(int k) const { return dist_ && k >= dist_kend_; }
     std::vector<std::vector<int>> start_rows_;      // every front's rows at the start of the stage
-    size_t dist_w0_ = 0, dist_t0_ = 0;              // W / trailing-row counts at the start of the stage
-    long long dist_npiv0_ = 0;
+    std::vector<char> dist_ghost_;                  // other subtrees' clusters alive on their ranks (columns tracked here)
     std::vector<int> dist_touched_;                 // fronts this rank's eliminations touched
     std::vector<std::pair<int, int>> dist_tr_;      // (front, row) rows they transformed in place
-    std::vector<char> dist_export(int k);
-    void dist_apply(const std::vector<std::vector<char>>& msgs);
+    std::vector<char> dist_top_;                    // 1: a top-separator piece (kept by every rank)
+    struct SnapE {
+        int c, cs;
+        double asp;
+    };
+    std::map<int, std::vector<SnapE>> dist_snap_;  // split stage -> its snapshot entries by cluster
+    std::vector<std::pair<int, size_t>> dist_tseg_; // (stage, end) of this rank's trailing rows per split stage
+    bool dist_mine(int c) const { return !dist_top_[c] && dist_owner_[c] == dist_->rank; }
+    void dist_partition_state();
+    std::vector<char> dist_export(int k, bool final_to_root);
+    void dist_apply(const std::vector<std::vector<char>>& msgs, bool final_to_root);
     double* dist_vbuf_ = nullptr;  // exported values (CUDA IPC) until every peer acknowledges
     void dist_exchange(int k, int err_cluster, const std::string& err_reason);
+    void rebuild_holders() {
+        for (auto& hs : holders_) hs.clear();
+        for (size_t c = 0; c < fr_.size(); ++c)
+            if (alive_[c] && fr_[c].live)
+                for (const KeyRef& kr : fr_[c].keys) holders_[kr.key].add(static_cast<int>(c));
+    }
     DeviceFactorization out_;
     std::unique_ptr<DeviceArena> arena_[2];
     int cur_ = 0, dev_ = 0;
@@ -2030,7 +2054,7 @@ void Engine::eliminate_stage(int k) {
     std::vector<int> mine;
     if (dist_stage(k)) {  // a split stage: this rank's subtree only (ranks.cpp owners)
         for (int c : stage_list_[k])
-            if (dist_owner_[c] == dist_->rank) mine.push_back(c);
+            if (dist_mine(c)) mine.push_back(c);
     }
     const auto& list = dist_stage(k) ? mine : stage_list_[k];
     if (list.empty()) return;
@@ -2976,6 +3000,33 @@ void Engine::merge_level() {
             o += width(c);
         }
     }
+    if (!dist_ghost_.empty()) {
+        // the other subtrees' merges, columns only (their ranks merge the fronts): groups ng..
+        // hold them, so a top-separator front's keys on those clusters split like any other
+        std::vector<std::pair<int, int>> gk;
+        for (size_t c = 0; c < dist_ghost_.size(); ++c)
+            if (dist_ghost_[c]) gk.emplace_back(h_.clusters[c].parent, static_cast<int>(c));
+        std::sort(gk.begin(), gk.end());
+        int o = 0;
+        for (size_t i = 0; i < gk.size(); ++i) {
+            const int P = gk[i].first, c = gk[i].second;
+            if (P < 0) throw std::logic_error("distributed factorization: subtree cluster without a parent");
+            if (i == 0 || P != gk[i - 1].first) {
+                if (i > 0) gstart.push_back(static_cast<int>(gkids.size()));
+                gp.push_back(P);
+                group_of[P] = static_cast<int>(gp.size()) - 1;
+                cols_[P].clear();
+                o = 0;
+            }
+            gkids.push_back(c);
+            child_off[c] = o;
+            o += width(c);
+            cols_[P].insert(cols_[P].end(), cols_[c].begin(), cols_[c].end());
+            dist_ghost_[c] = 0;
+        }
+        if (!gk.empty()) gstart.push_back(static_cast<int>(gkids.size()));
+        for (const auto& pc : gk) dist_ghost_[pc.first] = 1;
+    }
     DeviceArena& next = *arena_[cur_ ^ 1];
     std::unique_ptr<NScope> m1 = std::make_unique<NScope>(nprof_, "merge.descriptors");
     AsmBuilder& mb = asm_slot(5);  // keeps its capacity across calls
@@ -3127,6 +3178,14 @@ void Engine::snapshot(StageStats& st) {  // factorize.cpp:731-743
         st.top_rows += trows[q];
         st.top_cols += tcols[q];
     }
+    if (dist_stage(cur_stage_)) {  // split stage: the entries by cluster, merged on rank 0 at the end
+        auto& v = dist_snap_[cur_stage_];
+        v.clear();
+        for (long long c = 0; c < nc; ++c)
+            if (alive_[c] && fr_[c].live && width(static_cast<int>(c)) > 0 && (dist_->rank == 0 || !dist_top_[c]))
+                v.push_back(SnapE{static_cast<int>(c), width(static_cast<int>(c)),
+                                  static_cast<double>(fr_[c].nrows()) / width(static_cast<int>(c))});
+    }
 }
 
 
@@ -3180,33 +3239,62 @@ struct DistReader {
 };
 }  // namespace
 
-// Values (front blocks and W factors) travel device to device: each rank gathers them into
-// one cudaMalloc'ed buffer and sends its CUDA IPC handle with the metadata; the other ranks open
-// it (peer memory over NVLink on a multi-GPU node, the same memory when the ranks share a GPU)
-// and their gather kernels read the values in place; acknowledgements release the buffer.
-// SPQR_DIST_HOST=1 sends the values inline through the host transport instead.
-std::vector<char> Engine::dist_export(int k) {
+// Partitioned state of a distributed factorization: each rank keeps the fronts of its own
+// subtree and the pieces of the top separators (every rank, kept identical stage by stage); the
+// other subtrees' fronts are released here and reach rank 0 at the end of the split stages.
+void Engine::dist_partition_state() {
+    dist_ghost_.assign(fr_.size(), 0);
+    for (size_t c = 0; c < fr_.size(); ++c)
+        if (!dist_top_[c] && dist_owner_[c] != dist_->rank && fr_[c].live) {
+            dfree(fr_[c].mat, fr_[c].big);
+            fr_[c].retire();
+            alive_[c] = 0;
+            dist_ghost_[c] = 1;
+        }
+    rebuild_holders();
+}
+
+// Values travel device to device: each rank gathers the values it sends into one cudaMalloc'ed
+// buffer and sends its CUDA IPC handle with the metadata; the receivers open it (peer memory
+// over NVLink on a multi-GPU node, the same memory when the ranks share a GPU) and their gather
+// kernels read the values in place; acknowledgements release the buffer.  SPQR_DIST_HOST=1 sends
+// the values inline through the host transport instead.
+//
+// Per split stage (all ranks to all): the clusters this rank eliminated and the top-separator
+// fronts it touched (rows, keys, values, rows transformed in place).  At the last split stage
+// (ranks > 0 to rank 0) also: every front of its subtree, their clusters' columns, all its W
+// factors, pivot rows, trailing rows per stage and snapshot entries per stage.
+std::vector<char> Engine::dist_export(int k, bool final_to_root) {
     static const bool host_mode = std::getenv("SPQR_DIST_HOST") != nullptr;
     DistWriter w;
     w.i64(0x53505144);  // "SPQD"
     w.i64(host_mode ? 0 : 1);
-    std::vector<int> el;
+    std::vector<int> el, all_el;
     for (int c : stage_list_[k])
-        if (dist_owner_[c] == dist_->rank && gone_[c]) el.push_back(c);
+        if (dist_mine(c) && gone_[c]) el.push_back(c);
     std::sort(dist_touched_.begin(), dist_touched_.end());
     dist_touched_.erase(std::unique(dist_touched_.begin(), dist_touched_.end()), dist_touched_.end());
-    std::vector<int> T;
+    std::vector<int> T, S;  // touched top fronts; (final) this subtree's live fronts
     for (int f : dist_touched_)
-        if (!gone_[f] && fr_[f].live) T.push_back(f);
+        if (dist_top_[f] && !gone_[f] && fr_[f].live) T.push_back(f);
+    if (final_to_root)
+        for (size_t c = 0; c < fr_.size(); ++c) {
+            if (dist_top_[c] || dist_owner_[c] != dist_->rank) continue;
+            if (gone_[c])
+                all_el.push_back(static_cast<int>(c));
+            else if (alive_[c] && fr_[c].live)
+                S.push_back(static_cast<int>(c));
+        }
     std::sort(dist_tr_.begin(), dist_tr_.end());
-    // value space: every touched front's blocks in ascending key order (ld = rows), then this
-    // stage's W factors' [R | C] (ld = c)
-    std::vector<long long> voff(T.size() + 1, 0);
-    for (size_t t = 0; t < T.size(); ++t) voff[t + 1] = voff[t] + static_cast<long long>(fr_[T[t]].nrows()) * fr_[T[t]].ncols;
-    const size_t nw = out_.W.size() - dist_w0_;
+    // value space: T's blocks, then S's (ascending keys, ld = rows), then (final) W's [R | C]
+    std::vector<int> TS(T);
+    TS.insert(TS.end(), S.begin(), S.end());
+    std::vector<long long> voff(TS.size() + 1, 0);
+    for (size_t t = 0; t < TS.size(); ++t) voff[t + 1] = voff[t] + static_cast<long long>(fr_[TS[t]].nrows()) * fr_[TS[t]].ncols;
+    const size_t nw = final_to_root ? out_.W.size() : 0;
     std::vector<long long> woff(nw + 1, voff.back());
     for (size_t q = 0; q < nw; ++q) {
-        const DevWFactor& f = out_.W[dist_w0_ + q];
+        const DevWFactor& f = out_.W[q];
         if (f.kind != 0) throw std::logic_error("distributed factorization: rotation factor in a split stage");
         woff[q + 1] = woff[q] + static_cast<long long>(f.c) * (f.c + f.k);
     }
@@ -3215,8 +3303,8 @@ std::vector<char> Engine::dist_export(int k) {
     CK(cudaMalloc(&dv, sizeof(double) * std::max<long long>(total, 1)));
     dist_vbuf_ = dv;
     AsmBuilder& gb = asm_slot(0);
-    for (size_t t = 0; t < T.size(); ++t) {
-        const Front& F = fr_[T[t]];
+    for (size_t t = 0; t < TS.size(); ++t) {
+        const Front& F = fr_[TS[t]];
         if (F.nrows() == 0 || F.ncols == 0) continue;
         const int di = gb.begin(dv + voff[t], F.nrows(), F.nrows(), F.ncols, 1, static_cast<int>(F.keys.size()));
         gb.source(di, 0) = AsmSrc{F.mat, 1, F.ld};
@@ -3229,7 +3317,7 @@ std::vector<char> Engine::dist_export(int k) {
         }
     }
     for (size_t q = 0; q < nw; ++q) {
-        const DevWFactor& f = out_.W[dist_w0_ + q];
+        const DevWFactor& f = out_.W[q];
         if (f.c == 0) continue;
         const int di = gb.begin(dv + woff[q], f.c, f.c, f.c + f.k, 1, 1);
         gb.source(di, 0) = AsmSrc{f.a, 1, f.c};
@@ -3246,30 +3334,9 @@ std::vector<char> Engine::dist_export(int k) {
         w.i64(total);
     }
     w.ivec(el);
-    w.i64(static_cast<long long>(nw));
-    for (size_t q = 0; q < nw; ++q) {
-        const DevWFactor& f = out_.W[dist_w0_ + q];
-        const int meta[4] = {f.cluster, f.c, f.k, f.scale_only ? 1 : 0};
-        w.put(meta, 4);
-        w.put(out_.idx.data() + f.cols_off, f.c);
-        w.put(out_.idx.data() + f.coupled_off, f.k);
-        w.i64(woff[q]);
-    }
-    std::vector<int> piv;
-    for (int c : el)
-        for (int j : cols_[c]) {
-            piv.push_back(j);
-            piv.push_back(static_cast<int>(out_.pivot_row[j]));
-        }
-    w.ivec(piv);
-    w.i64(npiv_ - dist_npiv0_);
-    std::vector<int> trail(out_.trailing_rows.begin() + dist_t0_, out_.trailing_rows.end());
-    w.ivec(trail);
-    w.i64(static_cast<long long>(T.size()));
-    size_t q0 = 0;
-    for (size_t t = 0; t < T.size(); ++t) {
-        const Front& F = fr_[T[t]];
-        w.i64(T[t]);
+    auto put_front = [&](size_t t, bool with_tr) {
+        const Front& F = fr_[TS[t]];
+        w.i64(TS[t]);
         w.ivec(F.rows);
         std::vector<int> kw;
         for (const KeyRef& kr : F.keys) {
@@ -3277,11 +3344,51 @@ std::vector<char> Engine::dist_export(int k) {
             kw.push_back(kr.width);
         }
         w.ivec(kw);
-        std::vector<int> tr;
-        while (q0 < dist_tr_.size() && dist_tr_[q0].first < T[t]) ++q0;
-        for (size_t q = q0; q < dist_tr_.size() && dist_tr_[q].first == T[t]; ++q) tr.push_back(dist_tr_[q].second);
-        w.ivec(tr);
+        if (with_tr) {
+            std::vector<int> tr;
+            auto it = std::lower_bound(dist_tr_.begin(), dist_tr_.end(), std::make_pair(TS[t], INT_MIN));
+            for (; it != dist_tr_.end() && it->first == TS[t]; ++it) tr.push_back(it->second);
+            w.ivec(tr);
+        }
         w.i64(voff[t]);
+    };
+    w.i64(static_cast<long long>(T.size()));
+    for (size_t t = 0; t < T.size(); ++t) put_front(t, true);
+    if (final_to_root) {
+        w.i64(static_cast<long long>(S.size()));
+        for (size_t t = T.size(); t < TS.size(); ++t) put_front(t, false);
+        for (int c : S) w.ivec(cols_[c]);
+        w.ivec(all_el);
+        w.i64(static_cast<long long>(nw));
+        for (size_t q = 0; q < nw; ++q) {
+            const DevWFactor& f = out_.W[q];
+            const int meta[5] = {f.cluster, f.c, f.k, f.scale_only ? 1 : 0, f.batch};
+            w.put(meta, 5);
+            w.put(out_.idx.data() + f.cols_off, f.c);
+            w.put(out_.idx.data() + f.coupled_off, f.k);
+            w.i64(woff[q]);
+        }
+        std::vector<int> piv;
+        for (int c : all_el)
+            for (int j : cols_[c]) {
+                piv.push_back(j);
+                piv.push_back(static_cast<int>(out_.pivot_row[j]));
+            }
+        w.ivec(piv);
+        w.i64(npiv_);
+        w.i64(static_cast<long long>(dist_tseg_.size()));
+        size_t t0 = 0;
+        for (const auto& sg : dist_tseg_) {
+            w.i64(sg.first);
+            w.ivec(std::vector<int>(out_.trailing_rows.begin() + t0, out_.trailing_rows.begin() + sg.second));
+            t0 = sg.second;
+        }
+        w.i64(static_cast<long long>(dist_snap_.size()));
+        for (const auto& [st, v] : dist_snap_) {
+            w.i64(st);
+            w.i64(static_cast<long long>(v.size()));
+            w.put(v.data(), v.size());
+        }
     }
     if (host_mode) {  // the values inline
         std::vector<double> hv(total);
@@ -3294,29 +3401,33 @@ std::vector<char> Engine::dist_export(int k) {
     return std::move(w.b);
 }
 
-// Apply the other ranks' effects of this stage (msgs[rank]; this rank's own entry is empty, its
-// effects are already in place): every rank ends with the state the sequential engine would
-// have after the stage.  Each touched front becomes: its rows at the start of the stage in order,
-// minus every rank's pivots, then the rows each rank appended in rank order (= ascending source
-// cluster); a row's values come from the rank that transformed or appended it, else from this
-// rank's copy; its keys are the union minus the eliminated clusters.
-void Engine::dist_apply(const std::vector<std::vector<char>>& msgs) {
+// Apply the other ranks' messages (msgs[rank]; this rank's own entry is empty, its effects are
+// in place).  Each touched top-separator front becomes what the sequential engine would hold
+// after the stage: its rows at the start of the stage in order, minus every rank's pivots, then
+// the rows each rank appended in rank order (= ascending source cluster); a row's values come
+// from the rank that transformed or appended it, else from this rank's copy; its keys are the
+// union minus the eliminated clusters.  The final messages (on rank 0) add the other subtrees'
+// fronts, columns, W factors, pivot and trailing rows and snapshot entries.
+void Engine::dist_apply(const std::vector<std::vector<char>>& msgs, bool final_to_root) {
     const int G = dist_->size, me = dist_->rank;
     struct WIn {
-        int cl, c, k, so;
+        int cl, c, k, so, batch;
         std::vector<int> cols, cp;
         long long off;
     };
     struct FIn {
         int f;
-        std::vector<int> rows, kw, tr;
+        std::vector<int> rows, kw, tr, cols;
         long long off;
     };
     struct Msg {
-        std::vector<int> el, piv, trail;
+        bool present = false;
+        std::vector<int> el, all_el, piv;
         long long npiv = 0;
         std::vector<WIn> ws;
-        std::vector<FIn> fs;
+        std::vector<FIn> fs, sub;
+        std::vector<std::pair<int, std::vector<int>>> tsegs;
+        std::vector<std::pair<int, std::vector<SnapE>>> snaps;
         const double* vp = nullptr;
         double* peer = nullptr;
         std::vector<double> inline_vals;
@@ -3330,45 +3441,61 @@ void Engine::dist_apply(const std::vector<std::vector<char>>& msgs) {
         }
     } closer{M};
     for (int r = 0; r < G; ++r) {
-        if (r == me) continue;
+        if (r == me || msgs[r].empty()) continue;
         DistReader rd{msgs[r].data(), msgs[r].size()};
         if (rd.i64() != 0x53505144) throw std::runtime_error("distributed factorization: bad message");
         const bool ipc = rd.i64() == 1;
         Msg& m = M[r];
+        m.present = true;
         if (ipc) {
             cudaIpcMemHandle_t hnd;
             rd.get(reinterpret_cast<char*>(&hnd), sizeof hnd);
-            rd.i64();
+            out_.dist_bytes += 8 * rd.i64();  // the values, read over peer memory
             void* p = nullptr;
             CK(cudaIpcOpenMemHandle(&p, hnd, cudaIpcMemLazyEnablePeerAccess));
             m.peer = static_cast<double*>(p);
             m.vp = m.peer;
         }
         m.el = rd.ivec();
-        const long long nw = rd.i64();
-        m.ws.resize(nw);
-        for (auto& f : m.ws) {
-            int meta[4];
-            rd.get(meta, 4);
-            f.cl = meta[0], f.c = meta[1], f.k = meta[2], f.so = meta[3];
-            f.cols.resize(f.c);
-            f.cp.resize(f.k);
-            rd.get(f.cols.data(), f.c);
-            rd.get(f.cp.data(), f.k);
-            f.off = rd.i64();
-        }
-        m.piv = rd.ivec();
-        m.npiv = rd.i64();
-        m.trail = rd.ivec();
-        const long long nf = rd.i64();
-        m.fs.resize(nf);
-        for (auto& x : m.fs) {
+        auto get_front = [&](FIn& x, bool with_tr) {
             x.f = static_cast<int>(rd.i64());
             if (x.f < 0 || static_cast<size_t>(x.f) >= fr_.size()) throw std::runtime_error("distributed factorization: bad front");
             x.rows = rd.ivec();
             x.kw = rd.ivec();
-            x.tr = rd.ivec();
+            if (with_tr) x.tr = rd.ivec();
             x.off = rd.i64();
+        };
+        m.fs.resize(rd.i64());
+        for (auto& x : m.fs) get_front(x, true);
+        if (final_to_root) {
+            m.sub.resize(rd.i64());
+            for (auto& x : m.sub) get_front(x, false);
+            for (auto& x : m.sub) x.cols = rd.ivec();
+            m.all_el = rd.ivec();
+            m.ws.resize(rd.i64());
+            for (auto& f : m.ws) {
+                int meta[5];
+                rd.get(meta, 5);
+                f.cl = meta[0], f.c = meta[1], f.k = meta[2], f.so = meta[3], f.batch = meta[4];
+                f.cols.resize(f.c);
+                f.cp.resize(f.k);
+                rd.get(f.cols.data(), f.c);
+                rd.get(f.cp.data(), f.k);
+                f.off = rd.i64();
+            }
+            m.piv = rd.ivec();
+            m.npiv = rd.i64();
+            m.tsegs.resize(rd.i64());
+            for (auto& sg : m.tsegs) {
+                sg.first = static_cast<int>(rd.i64());
+                sg.second = rd.ivec();
+            }
+            m.snaps.resize(rd.i64());
+            for (auto& sn : m.snaps) {
+                sn.first = static_cast<int>(rd.i64());
+                sn.second.resize(rd.i64());
+                rd.get(sn.second.data(), sn.second.size());
+            }
         }
         if (!ipc) {
             const long long total = rd.i64();
@@ -3379,53 +3506,22 @@ void Engine::dist_apply(const std::vector<std::vector<char>>& msgs) {
             m.vp = d;
         }
     }
-    // eliminated clusters of every other rank
+    // clusters the other ranks eliminated (their fronts are not held here)
     for (int r = 0; r < G; ++r)
-        for (int c : M[r].el) {
-            if (c < 0 || static_cast<size_t>(c) >= fr_.size()) throw std::runtime_error("distributed factorization: bad cluster");
-            for (const KeyRef& kr : fr_[c].keys) holders_[kr.key].remove(c);
-            holders_[c].clear();
-            gone_[c] = 1;
-            alive_[c] = 0;
-            dfree(fr_[c].mat, fr_[c].big);
-            fr_[c].retire();
-        }
-    AsmBuilder& mb = asm_slot(0);
-    // W factors, pivots, trailing rows (this stage's trailing rows rebuilt in rank order)
-    std::vector<int> own_trail(out_.trailing_rows.begin() + dist_t0_, out_.trailing_rows.end());
-    out_.trailing_rows.resize(dist_t0_);
-    for (int r = 0; r < G; ++r) {
-        if (r == me) {
-            out_.trailing_rows.insert(out_.trailing_rows.end(), own_trail.begin(), own_trail.end());
-            continue;
-        }
-        const Msg& m = M[r];
-        long long wtot = 0;
-        for (const auto& f : m.ws) wtot += static_cast<long long>(f.c) * (f.c + f.k);
-        double* dw = out_.warena->alloc_n<double>(std::max<long long>(wtot, 1));
-        long long o = 0;
-        for (const auto& f : m.ws) {
-            DevWFactor& d = new_factor(0, f.cl, f.c, f.k, f.cols, f.so ? nullptr : &f.cp);
-            d.a = dw + o;
-            if (f.c > 0) {
-                const int di = mb.begin(d.a, f.c, f.c, f.c + f.k, 1, 1);
-                mb.source(di, 0) = AsmSrc{m.vp + f.off, 1, f.c};
-                for (int i = 0; i < f.c; ++i) mb.row(di, i) = int4{0, i, -1, 0};
-                mb.seg(di, 0, 0);
-                mb.km(di, 0, 0) = 0;
+        for (const std::vector<int>* v : {&M[r].el, &M[r].all_el})
+            for (int c : *v) {
+                if (c < 0 || static_cast<size_t>(c) >= fr_.size()) throw std::runtime_error("distributed factorization: bad cluster");
+                holders_[c].clear();
+                gone_[c] = 1;
+                dist_ghost_[c] = 0;
             }
-            o += static_cast<long long>(f.c) * (f.c + f.k);
-        }
-        for (size_t i = 0; i + 1 < m.piv.size(); i += 2) out_.pivot_row[m.piv[i]] = m.piv[i + 1];
-        npiv_ += m.npiv;
-        out_.trailing_rows.insert(out_.trailing_rows.end(), m.trail.begin(), m.trail.end());
-    }
-    // touched fronts: versions by front
+    AsmBuilder& mb = asm_slot(0);
+    auto in = [](const std::vector<int>& v, int a) { return std::binary_search(v.begin(), v.end(), a); };
+    // touched top-separator fronts: versions by front
     std::map<int, std::vector<std::pair<int, const FIn*>>> byf;
     for (int r = 0; r < G; ++r)
         for (const auto& x : M[r].fs) byf[x.f].emplace_back(r, &x);
     std::vector<std::pair<int, Front>> repl;
-    auto in = [](const std::vector<int>& v, int a) { return std::binary_search(v.begin(), v.end(), a); };
     for (const auto& [f, vers] : byf) {
         if (gone_[f] || !fr_[f].live) throw std::runtime_error("distributed factorization: touched front not live");
         const Front& C = fr_[f];
@@ -3490,7 +3586,6 @@ void Engine::dist_apply(const std::vector<std::vector<char>>& msgs) {
                     }
             }
         }
-        // keys: every version's, minus the clusters eliminated by any rank
         std::vector<std::pair<int, int>> ks;
         for (const KeyRef& kr : C.keys)
             if (!gone_[kr.key]) ks.emplace_back(kr.key, kr.width);
@@ -3536,6 +3631,66 @@ void Engine::dist_apply(const std::vector<std::vector<char>>& msgs) {
         mb.drop_if_empty();
         repl.emplace_back(f, std::move(nf));
     }
+    if (final_to_root) {
+        // the other subtrees' fronts and columns
+        for (int r = 0; r < G; ++r)
+            for (const auto& x : M[r].sub) {
+                cols_[x.f] = x.cols;
+                Front nf;
+                nf.live = true;
+                nf.rows = x.rows;
+                std::vector<int> roff;
+                int o = 0;
+                for (size_t q = 0; q + 1 < x.kw.size(); q += 2) {
+                    roff.push_back(o);
+                    o += x.kw[q + 1];
+                    nf.keys.push_back(KeyRef{x.kw[q], x.kw[q + 1], 0});
+                }
+                layout(x.f, nf.keys, nf.ncols);
+                nf.ld = std::max(1, nf.nrows());
+                nf.mat = dalloc(arena(), static_cast<size_t>(nf.ld) * std::max(nf.ncols, 1), nf.big);
+                std::vector<int> ord;
+                phys_order(nf.keys, ord);
+                const int di = mb.begin(nf.mat, nf.ld, nf.nrows(), nf.ncols, 1, static_cast<int>(ord.size()));
+                mb.source(di, 0) = AsmSrc{M[r].vp + x.off, 1, static_cast<long long>(std::max<size_t>(x.rows.size(), 1))};
+                for (int i = 0; i < nf.nrows(); ++i) mb.row(di, i) = int4{0, i, -1, 0};
+                for (size_t q = 0; q < ord.size(); ++q) {
+                    mb.seg(di, static_cast<int>(q), nf.keys[ord[q]].col);
+                    mb.km(di, static_cast<int>(q), 0) = roff[ord[q]];
+                }
+                mb.drop_if_empty();
+                if (!dist_ghost_[x.f]) throw std::runtime_error("distributed factorization: unexpected subtree front");
+                dist_ghost_[x.f] = 0;
+                alive_[x.f] = 1;
+                repl.emplace_back(x.f, std::move(nf));
+            }
+        // W factors (values gathered into the W arena), pivot rows
+        for (int r = 0; r < G; ++r) {
+            const Msg& m = M[r];
+            long long wtot = 0;
+            for (const auto& f : m.ws) wtot += static_cast<long long>(f.c) * (f.c + f.k);
+            double* dw = out_.warena->alloc_n<double>(std::max<long long>(wtot, 1));
+            long long o = 0;
+            int nb = 0;
+            for (const auto& f : m.ws) {
+                DevWFactor& d = new_factor(0, f.cl, f.c, f.k, f.cols, f.so ? nullptr : &f.cp);
+                d.batch = out_.nbatches + f.batch;  // the sending rank's waves, after this rank's
+                nb = std::max(nb, f.batch + 1);
+                d.a = dw + o;
+                if (f.c > 0) {
+                    const int di = mb.begin(d.a, f.c, f.c, f.c + f.k, 1, 1);
+                    mb.source(di, 0) = AsmSrc{m.vp + f.off, 1, f.c};
+                    for (int i = 0; i < f.c; ++i) mb.row(di, i) = int4{0, i, -1, 0};
+                    mb.seg(di, 0, 0);
+                    mb.km(di, 0, 0) = 0;
+                }
+                o += static_cast<long long>(f.c) * (f.c + f.k);
+            }
+            out_.nbatches += nb;
+            for (size_t i = 0; i + 1 < m.piv.size(); i += 2) out_.pivot_row[m.piv[i]] = m.piv[i + 1];
+            npiv_ += m.npiv;
+        }
+    }
     flush_assemble(mb);
     sync();  // every read of the other ranks' values is done
     for (auto& pr : repl) {
@@ -3547,17 +3702,77 @@ void Engine::dist_apply(const std::vector<std::vector<char>>& msgs) {
         F.big = pr.second.big;
         F.ld = pr.second.ld;
         F.ncols = pr.second.ncols;
+        F.live = true;
         F.scaled_ok = false;
         F.tag.clear();
         F.soff.clear();
     }
+    if (!final_to_root) return;
+    for (size_t c = 0; c < dist_ghost_.size(); ++c)
+        if (dist_ghost_[c]) throw std::runtime_error("distributed factorization: subtree front " + std::to_string(c) + " not received");
+    dist_ghost_.clear();
+    // chronological order of the split stages' results: W by (stage, cluster), trailing rows by
+    // (stage, rank), every split stage's snapshot by cluster, nnz(W) per stage
+    auto stage_of = [&](int c) { return h_.clusters[c].stage; };
+    std::stable_sort(out_.W.begin(), out_.W.end(), [&](const DevWFactor& a, const DevWFactor& b) {
+        const int sa = stage_of(a.cluster), sb = stage_of(b.cluster);
+        return sa != sb ? sa > sb : a.cluster < b.cluster;
+    });
+    std::map<int, std::vector<std::vector<int>>> tby;  // stage -> per rank
+    {
+        size_t t0 = 0;
+        for (const auto& sg : dist_tseg_) {
+            auto& v = tby[sg.first];
+            v.resize(G);
+            v[me].assign(out_.trailing_rows.begin() + t0, out_.trailing_rows.begin() + sg.second);
+            t0 = sg.second;
+        }
+    }
+    for (int r = 0; r < G; ++r)
+        for (const auto& sg : M[r].tsegs) {
+            auto& v = tby[sg.first];
+            v.resize(G);
+            v[r] = sg.second;
+        }
+    out_.trailing_rows.clear();
+    for (auto it = tby.rbegin(); it != tby.rend(); ++it)  // stages descending
+        for (const auto& v : it->second) out_.trailing_rows.insert(out_.trailing_rows.end(), v.begin(), v.end());
+    for (int r = 0; r < G; ++r)
+        for (const auto& sn : M[r].snaps) {
+            auto& v = dist_snap_[sn.first];
+            v.insert(v.end(), sn.second.begin(), sn.second.end());
+        }
+    for (auto& st : out_.stages) {
+        auto it = dist_snap_.find(st.stage);
+        if (it == dist_snap_.end()) continue;
+        auto v = it->second;
+        std::sort(v.begin(), v.end(), [](const SnapE& a, const SnapE& b) { return a.c < b.c; });
+        st.front_cols.clear();
+        st.front_aspect.clear();
+        for (const auto& e : v) {
+            st.front_cols.push_back(e.cs);
+            st.front_aspect.push_back(e.asp);
+        }
+        long long nnz = 0;  // cumulative nnz(W) after the stage (transforms.cpp:25-38)
+        for (const auto& f : out_.W) {
+            if (stage_of(f.cluster) < st.stage) continue;
+            const long long c = f.c, kk = f.k;
+            nnz += f.kind == 0 ? c * (c + 1) / 2 + c * kk : kk * c - kk * (kk - 1) / 2 + kk;
+        }
+        st.nnz_w = nnz;
+    }
+    rebuild_holders();
 }
 
-// One split stage's exchange: every rank's effects (or its first failing cluster) to every
-// other rank, in rank order (rank r sends while the others receive from r), then all apply.
+// One split stage's exchange.  Before the last split stage every rank's message goes to every
+// other rank (rank r sends while the others receive from r) and all apply them; at the last one
+// ranks > 0 send to rank 0 only, which applies them and continues alone.  A rank whose
+// elimination failed sends its first failing cluster instead; the first of all ranks is raised
+// (the sequential engine's error), by every rank before the last split stage, by rank 0 at it.
 void Engine::dist_exchange(int k, int err_cluster, const std::string& err_reason) {
     const double t0 = now_s();
     const int G = dist_->size, me = dist_->rank;
+    const bool final_stage = k == dist_kend_;
     std::vector<char> own;
     if (err_cluster >= 0) {  // an error record: magic, -1, cluster, reason
         DistWriter w;
@@ -3566,25 +3781,30 @@ void Engine::dist_exchange(int k, int err_cluster, const std::string& err_reason
         w.i64(err_cluster);
         w.ivec(std::vector<int>(err_reason.begin(), err_reason.end()));
         own = std::move(w.b);
-    } else {
-        own = dist_export(k);
+    } else if (!(final_stage && me == 0)) {
+        own = dist_export(k, final_stage);
     }
     auto fail = [] { throw std::runtime_error("distributed factorization: transport failed"); };
     std::vector<std::vector<char>> msgs(G);
     for (int r = 0; r < G; ++r) {
+        if (final_stage && r == 0) continue;  // nothing goes out of rank 0 at the last split stage
         if (r == me) {
             const long long n = static_cast<long long>(own.size());
-            for (int q = 0; q < G; ++q)
-                if (q != me && (dist_->send(dist_->user, q, &n, sizeof n) || dist_->send(dist_->user, q, own.data(), n))) fail();
-            out_.dist_bytes += n * (G - 1);
-        } else {
+            for (int q = 0; q < G; ++q) {
+                if (q == me || (final_stage && q != 0)) continue;
+                if (dist_->send(dist_->user, q, &n, sizeof n) || dist_->send(dist_->user, q, own.data(), n)) fail();
+                out_.dist_bytes += n;
+            }
+        } else if (!final_stage || me == 0) {
             long long n = 0;
             if (dist_->recv(dist_->user, r, &n, sizeof n)) fail();
             msgs[r].resize(static_cast<size_t>(std::max<long long>(n, 0)));
             if (n > 0 && dist_->recv(dist_->user, r, msgs[r].data(), n)) fail();
+            out_.dist_bytes += n;
         }
     }
     auto mode = [](const std::vector<char>& b) {  // -1 error, 0 inline values, 1 IPC values
+        if (b.size() < 16) return -2;
         DistReader rd{b.data(), b.size()};
         rd.i64();
         return static_cast<int>(rd.i64());
@@ -3603,15 +3823,16 @@ void Engine::dist_exchange(int k, int err_cluster, const std::string& err_reason
                 why.assign(rv.begin(), rv.end());
             }
         }
-    if (ecl < 0) dist_apply(msgs);
-    // acknowledgements: rank r's IPC buffer is released once every other rank has read it
+    if (ecl < 0 && (!final_stage || me == 0)) dist_apply(msgs, final_stage);
+    // acknowledgements: a rank's IPC buffer is released once its receivers have read it
     for (int r = 0; r < G; ++r) {
         const long long ack = 1;
         if (r == me) {
             if (dist_vbuf_) {
                 for (int q = 0; q < G; ++q) {
+                    if (q == me || (final_stage && q != 0)) continue;
                     long long a = 0;
-                    if (q != me && dist_->recv(dist_->user, q, &a, sizeof a)) fail();
+                    if (dist_->recv(dist_->user, q, &a, sizeof a)) fail();
                 }
                 CK(cudaFree(dist_vbuf_));
                 dist_vbuf_ = nullptr;
@@ -3621,9 +3842,6 @@ void Engine::dist_exchange(int k, int err_cluster, const std::string& err_reason
         }
     }
     if (ecl >= 0) throw SingularFrontError(ecl, why);
-    // W in the reference's chronological order (ascending cluster) within the stage
-    std::stable_sort(out_.W.begin() + dist_w0_, out_.W.end(),
-                     [](const DevWFactor& a, const DevWFactor& b) { return a.cluster < b.cluster; });
     out_.dist_exchange_s += now_s() - t0;
 }
 
@@ -3637,15 +3855,13 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
         const HostProf before = prof_;
         double t0 = now_s();
         if (dist_stage(k)) {
-            // a split stage: every rank eliminates its own subtree's clusters from the same state,
-            // then all exchange their effects; a rank whose elimination fails still reports, and
-            // every rank raises the first failing cluster of all ranks (the sequential error)
+            // a split stage: every rank eliminates its own subtree's clusters; the top-separator
+            // fronts they share are re-merged after every stage, and at the last split stage the
+            // other subtrees' state goes to rank 0 (a rank whose elimination fails still reports)
+            if (k == L_ + 1) dist_partition_state();
             start_rows_.assign(fr_.size(), std::vector<int>());
             for (size_t c = 0; c < fr_.size(); ++c)
-                if (alive_[c] && fr_[c].live) start_rows_[c] = fr_[c].rows;
-            dist_w0_ = out_.W.size();
-            dist_t0_ = out_.trailing_rows.size();
-            dist_npiv0_ = npiv_;
+                if (dist_top_[c] && alive_[c] && fr_[c].live) start_rows_[c] = fr_[c].rows;
             dist_touched_.clear();
             dist_tr_.clear();
             int ecl = -1;
@@ -3656,10 +3872,17 @@ DeviceFactorization Engine::run() {  // factorize.cpp:745-790
                 ecl = e.cluster;
                 why = e.reason;
             }
+            dist_tseg_.emplace_back(k, out_.trailing_rows.size());
             dist_exchange(k, ecl, why);
-            if (k == dist_kend_ && dist_->rank != 0) {  // the rest runs on rank 0
-                out_.dist_partial = true;
-                break;
+            if (k == dist_kend_) {  // the rest runs on rank 0
+                if (dist_->rank != 0) {
+                    out_.dist_partial = true;
+                    break;
+                }
+#ifdef _OPENMP
+                if (const char* s = std::getenv("SPQR_HOST_THREADS_ROOT"))  // alone on the host now
+                    if (std::atoi(s) > 0) omp_set_num_threads(std::atoi(s));
+#endif
             }
         } else {
             eliminate_stage(k);

@@ -81,7 +81,7 @@ struct DeviceFactorization {
     // effects were sent to rank 0 (which holds the whole factorization)
     bool dist_partial = false;
     double dist_exchange_s = 0.0;   // time in the leaf-stage exchange (export / receive + import)
-    long long dist_bytes = 0;       // bytes sent (ranks > 0) or received (rank 0)
+    long long dist_bytes = 0;       // host-transport bytes sent + received, plus value bytes read over peer memory
     long long nnz_w() const;
 };
 
