@@ -105,12 +105,13 @@ int spqr_rank_plan(int m, int n, const int* colptr, const int* rowind, const dou
 int spqr_pipeline_rank_stats(const spqr_pipeline* p, int* nstages, double* flops, double* cross, int* owner);
 
 /* A factorization across nranks = 2^g processes (one per GPU), the Pipeline of every rank
- * built from the same A: each rank partitions A (identically), eliminates the leaves of its
- * own subtree (spqr_rank_plan owners), and ranks > 0 send their leaf-stage effects — eliminated
- * clusters, W factors, pivot / trailing rows and every front they touched — to rank 0 through
- * the caller's blocking byte transport; rank 0 merges them exactly as the sequential engine
- * would have left its state and runs the remaining stages (the top levels gathered onto one
- * GPU).  Rank 0's pipeline is the factorization (identical to spqr_pipeline_create's); the
+ * built from the same A: each rank partitions A (identically) and keeps only its own subtree
+ * (spqr_rank_plan owners) plus the top-g separator pieces; through every stage before the first
+ * scale_all it eliminates its subtree's clusters, and after each such stage the ranks exchange
+ * the eliminated clusters and the top-separator fronts they touched (each rank re-merges them as
+ * the sequential engine leaves them); after the last one ranks > 0 send rank 0 their subtree —
+ * fronts, W factors, pivot / trailing rows — and rank 0 runs the remaining stages.  Metadata
+ * goes through the caller's blocking byte transport, values device to device (CUDA IPC).  Rank 0's pipeline is the factorization (identical to spqr_pipeline_create's); the
  * other ranks' pipelines hold none (solve returns an error).  Transport callbacks return 0 on
  * success. */
 typedef int (*spqr_send_fn)(void* user, int dst, const void* buf, long long n);
@@ -119,8 +120,8 @@ int spqr_pipeline_create_dist(int m, int n, const int* colptr, const int* rowind
                               const double* coords, int dim, const int* parts, int levels, double eps, int skip_levels,
                               int device, int rank, int nranks, spqr_send_fn send, spqr_recv_fn recv, void* user,
                               spqr_pipeline** out, char* err, int errlen, int* err_cluster);
-/* out3: 1 if this rank's part went to rank 0 (no factorization here), seconds in the leaf-stage
- * exchange, bytes sent (ranks > 0) / received (rank 0). */
+/* out3: 1 if this rank's part went to rank 0 (no factorization here), seconds in the
+ * exchanges, bytes exchanged (host transport sent + received, values read over peer memory). */
 void spqr_pipeline_dist_info(const spqr_pipeline* p, double* out3);
 
 /* info[16]: M, N, L, nclusters, nW, n_dropped, n_trailing, n_stages, nnz_w, nnz(A), W sweep levels,

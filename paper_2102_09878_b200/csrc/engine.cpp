@@ -3190,16 +3190,15 @@ void Engine::snapshot(StageStats& st) {  // factorize.cpp:731-743
 
 
 // ---------------------------------------------------------------------------------------
-// Distributed leaf stage (opt.dist).  Every rank builds the same engine; at
-// the leaf stage (L+1) each eliminates only the leaves of its own subtree (ranks.cpp owners).
-// Leaves touch disjoint rows — no row of A couples two subtrees' interiors — so the ranks'
-// eliminations commute; the only fronts two ranks touch are pieces of the top separators, each
-// rank transforming its own side's rows.  Ranks > 0 then send rank 0 their effects: eliminated
-// clusters, W factors, pivot rows, trailing rows, and every front they touched (rows, keys,
-// values, and which rows they transformed); rank 0 merges them into its own state exactly as
-// the sequential engine would have left it (initial rows in order minus every rank's pivots,
-// then appended rows in ascending source-cluster order = rank order), and runs the remaining
-// stages — the top levels gathered onto one GPU.
+// Distributed split stages (opt.dist).  Every rank builds the same engine; in
+// the stages L+1 .. dist_kend_ (before any scale_all: rows are still pure) each eliminates only
+// its own subtree's clusters (ranks.cpp owners).  No row of A couples two subtrees' interiors,
+// so the ranks' eliminations commute; the only fronts two ranks touch are pieces of the top
+// separators, each rank transforming its own side's rows.  After each split stage the ranks
+// exchange their effects on those fronts and re-merge them exactly as the sequential engine
+// leaves them (rows at the start of the stage in order minus every rank's pivots, then appended
+// rows in ascending source-cluster order = rank order); after the last one ranks > 0 hand their
+// subtree to rank 0, which runs the remaining stages.
 namespace {
 struct DistWriter {
     std::vector<char> b;

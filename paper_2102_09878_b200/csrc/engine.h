@@ -77,10 +77,10 @@ struct DeviceFactorization {
     int nbatches = 0;
     EngineCounters ctr;
     RankStats rank;
-    // distributed factorization: on ranks > 0 the result stops after the leaf stage, whose
-    // effects were sent to rank 0 (which holds the whole factorization)
+    // distributed factorization: on ranks > 0 the result stops after the split stages, whose
+    // subtree was sent to rank 0 (which holds the whole factorization)
     bool dist_partial = false;
-    double dist_exchange_s = 0.0;   // time in the leaf-stage exchange (export / receive + import)
+    double dist_exchange_s = 0.0;   // time in the split stages' exchanges (export / receive + import)
     long long dist_bytes = 0;       // host-transport bytes sent + received, plus value bytes read over peer memory
     long long nnz_w() const;
 };

@@ -101,7 +101,7 @@ struct FactorizeOptions {  // factorize.h:13-17
     int skip_levels = 3;
     bool store_q = false;  // keep the orthogonal row factors Q (tests, diagnostics)
     int ranks = 1;         // > 1: account work and cross-rank traffic of a ranks-GPU subtree split (ranks.cpp)
-    const DistTransport* dist = nullptr;  // size > 1: the leaf stage runs subtree-parallel
+    const DistTransport* dist = nullptr;  // size > 1: the stages before the first scale_all run subtree-parallel
 };
 
 struct StageStats {  // transforms.h:40-47 (+ per-phase device-side timings)

@@ -1,7 +1,8 @@
 """The distributed factorization (spqr_pipeline_create_dist): 2 and 4 processes,
 each with its own CUDA context (here all on GPU 0 — no kernel of one rank waits on another;
-the ranks exchange over a gloo group on the host), each eliminating the leaves of its own
-subtree; rank 0 merges the other ranks' effects and finishes.  Rank 0's factorization must be
+the ranks exchange over a gloo group on the host), each holding and eliminating its own
+subtree through the stages before the first scale_all, the top-separator fronts re-merged on
+every rank after each stage; rank 0 receives the other subtrees and finishes.  Rank 0's factorization must be
 the single-process one: same ordering, W factor count, nnz(W), pivot / dropped / trailing rows,
 every stage's widths, the same W sweeps and the same CGLS solve."""
 import os
