@@ -22,6 +22,7 @@
 #include <climits>
 #include <cmath>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "dev.h"
@@ -168,6 +169,154 @@ __device__ void panel_regs(double* P, int m, int n, int kmax, double* s_tau) {
     if (lane < n) {
 #pragma unroll
         for (int i = 0; i < RPT; ++i) P[(r0 + i) + lane * MP] = x[i];
+    }
+    __syncthreads();
+}
+
+// Panel factorisation without block barriers inside a reflector (n <= 32, MP <= 128):
+// the panel is swept in sub-panels of eight columns.  One warp factors a sub-panel
+// entirely in registers - lane l holds rows l, l + 32, ... of the eight columns, so
+// the tail norm of the pivot column and its dot products with the columns to its
+// right are one shuffle butterfly, and the pivot row is one shuffle broadcast; no
+// shared memory and no barrier per reflector.  Then every warp applies the eight
+// new reflectors to one of the eight-column chunks to the right (reflector vectors
+// from shared memory, the chunk in registers).  Two block barriers per sub-panel
+// instead of three per reflector.  With v = tail / (c0 - beta) the products
+// v^T x_j are formed as (tail^T x_j) / (c0 - beta): same arithmetic as
+// make_reflector / apply_panel up to rounding.
+template <int N>
+__device__ __forceinline__ void wsum_n(double (&p)[8], int first) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+            if (j >= first) p[j] += __shfl_xor_sync(0xffffffffu, p[j], o);
+    }
+}
+
+// XOR swizzle of the row index per column used by k_qr_wy's shared-memory panel (see there)
+__device__ __forceinline__ int wy_swz(int j) { return (((j >> 1) & 3) ^ ((j & 1) << 1)) << 2; }
+
+// One warp factors the eight panel columns c0..c0+7 in registers (straight-line code:
+// reflectors beyond kmax and zero reflectors run as no-ops).  SWZ: rows stored at
+// (row ^ wy_swz(column)); vtop (optional, SWZ only): the explicit reflectors' top 32 rows
+// (unit diagonal, zeros above, zero columns beyond kmax), ld 32, same swizzle.
+template <int MP, bool SWZ>
+__device__ __forceinline__ void subpanel_factor(double* P, int c0, int n, int kmax, double* s_tau, int lane, double* vtop) {
+    constexpr int RPL = MP / 32;  // rows per lane
+    double x[RPL][8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int sw = SWZ ? wy_swz(c0 + j) : 0;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) x[i][j] = (c0 + j < n) ? P[((lane + 32 * i) ^ sw) + (c0 + j) * MP] : 0.0;
+    }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const int k = c0 + kk;
+        const bool act = k < kmax;
+        const bool t0 = lane > k;  // row `lane` lies below the pivot row (k < 32)
+        double p[8], rk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j < kk) continue;
+            double a = t0 ? x[0][kk] * x[0][j] : 0.0;
+#pragma unroll
+            for (int i = 1; i < RPL; ++i) a = fma(x[i][kk], x[i][j], a);
+            p[j] = a;
+            rk[j] = __shfl_sync(0xffffffffu, x[0][j], k);  // pivot row
+        }
+        wsum_n<8>(p, kk);
+        const double c = rk[kk], tail2 = p[kk];
+        const bool nz = act && !(tail2 <= DBL_MIN);  // Eigen makeHouseholder
+        double bt = sqrt(fma(c, c, tail2));
+        if (hh_beta_negative(c, tail2)) bt = -bt;
+        const double beta = nz ? bt : c;
+        const double tau = nz ? (bt - c) / bt : 0.0;
+        const double rden = nz ? 1.0 / (c - bt) : 0.0;
+        const double sc = act ? rden : 1.0;  // tau == 0: the tail is cleared
+#pragma unroll
+        for (int i = 1; i < RPL; ++i) x[i][kk] *= sc;
+        x[0][kk] = t0 ? x[0][kk] * sc : ((lane == k && act) ? beta : x[0][kk]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j <= kk) continue;
+            const double w = tau * fma(p[j], rden, rk[j]);
+#pragma unroll
+            for (int i = 1; i < RPL; ++i) x[i][j] = fma(-w, x[i][kk], x[i][j]);
+            x[0][j] = t0 ? fma(-w, x[0][kk], x[0][j]) : (lane == k ? x[0][j] - w : x[0][j]);
+        }
+        if (lane == 0 && act) s_tau[k] = tau;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int sw = SWZ ? wy_swz(c0 + j) : 0;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i)
+            if (c0 + j < n) P[((lane + 32 * i) ^ sw) + (c0 + j) * MP] = x[i][j];
+        if (SWZ && vtop) {
+            const int k = c0 + j;
+            vtop[(lane ^ sw) + k * 32] = k < kmax ? (lane > k ? x[0][j] : (lane == k ? 1.0 : 0.0)) : 0.0;
+        }
+    }
+}
+
+template <int MP, int kNW>
+__device__ void panel_warp(double* P, int m_, int n_, int kmax_, double* s_tau) {
+    constexpr int RPL = MP / 32;  // rows per lane
+    // warp-uniform values are broadcast from lane 0 so that the compiler sees every branch
+    // around the shuffles as convergent (plain SHFL instead of per-shuffle warp collectives)
+    const int lane = threadIdx.x & 31;
+    const int wid = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+    const int n = __shfl_sync(0xffffffffu, n_, 0), kmax = __shfl_sync(0xffffffffu, kmax_, 0);
+    (void)m_;
+    const int nchunks = (n + 7) >> 3;
+    for (int s = 0; 8 * s < kmax; ++s) {
+        const int c0 = 8 * s;
+        if (wid == 0) subpanel_factor<MP, false>(P, c0, n, kmax, s_tau, lane, nullptr);
+        __syncthreads();
+        if (s + 1 >= nchunks) break;  // uniform
+        for (int q = s + 1 + wid; q < nchunks; q += kNW) {
+            const int d0 = 8 * q;
+            double y[RPL][8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                for (int i = 0; i < RPL; ++i) y[i][j] = (d0 + j < n) ? P[lane + 32 * i + (d0 + j) * MP] : 0.0;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const int k = c0 + kk;
+                const double tau = k < kmax ? s_tau[k] : 0.0;
+                const int kc = min(k, n - 1);  // a column that exists (its values are unused when tau = 0)
+                double v[RPL], p[8];
+                {
+                    const double t = P[lane + kc * MP];
+                    v[0] = lane > k ? t : (lane == k ? 1.0 : 0.0);
+                }
+#pragma unroll
+                for (int i = 1; i < RPL; ++i) v[i] = P[lane + 32 * i + kc * MP];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    double a = v[0] * y[0][j];
+#pragma unroll
+                    for (int i = 1; i < RPL; ++i) a = fma(v[i], y[i][j], a);
+                    p[j] = a;
+                }
+                wsum_n<8>(p, 0);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const double w = -tau * p[j];
+#pragma unroll
+                    for (int i = 0; i < RPL; ++i) y[i][j] = fma(w, v[i], y[i][j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                for (int i = 0; i < RPL; ++i)
+                    if (d0 + j < n) P[lane + 32 * i + (d0 + j) * MP] = y[i][j];
+        }
+        __syncthreads();
     }
     __syncthreads();
 }
@@ -341,7 +490,7 @@ __device__ void tile_dmma(const QrDesc& d, const int4& wk, double* sm, int kmax,
 // factorisations overlap the others' tile sweeps.
 template <int TPC, bool WY, int kNW = nw_of<TPC>()>
 __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_tile(const QrDesc* __restrict__ ds, const int4* __restrict__ work,
-                                                      int* __restrict__ count) {
+                                                      int* __restrict__ count, int panel_regs_only) {
     constexpr int MP = 16 * TPC;  // padded rows (panel leading dimension)
     const int4 wk = work[blockIdx.x];
     const QrDesc d = ds[wk.x];
@@ -383,7 +532,12 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_tile(const QrDesc* __
     // ---- panel factorisation
     if (MP <= 256 && n <= 32) {
         __syncthreads();
-        panel_regs<(MP <= 256 ? MP : 256), kNW>(P, m, n, kmax, s_tau);
+        if (panel_regs_only == 2) {  // timing probe: no factorisation
+            for (int i = threadIdx.x; i < kmax; i += blockDim.x) s_tau[i] = 0.5;
+        } else if (MP <= 128 && !panel_regs_only)
+            panel_warp<(MP <= 128 ? MP : 128), kNW>(P, m, n, kmax, s_tau);
+        else
+            panel_regs<(MP <= 256 ? MP : 256), kNW>(P, m, n, kmax, s_tau);
     } else {  // smem panel, warp per column, one barrier per reflector (look-ahead)
         if (kmax > 0 && wid == 0) make_reflector(P, MP, m, 0, s_tau);
         __syncthreads();
@@ -503,25 +657,310 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_tile(const QrDesc* __
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Fronts of 65..128 rows with panels of up to 32 columns and a wide trailing block (the
+// C5 128x32+256 shape).  The panel is swept in sub-panels of eight columns; a sub-panel's
+// reflectors are kept in compact-WY form H_7..H_0 = I - V_s T_s^T V_s^T (T_s 8 x 8, from the
+// Gram matrix V_s^T V_s as accumulate_wy, dense_kernels.cpp:41-53) and applied on the FP64
+// tensor cores (m8n8k4) to the panel's own later columns and to the trailing block, both held
+// in REGISTERS.  A warp owns eight columns at a time; lane (g, t4) holds rows
+// {8b + 2 t4, 8b + 2 t4 + 1}, b = 0..15, of column g, which is at once
+//   * the A fragment of  W^T  = X^T V_s  (contraction over rows: k-lane t4 carries row
+//     8b + 2 t4 + e in step (b, e) - a permutation of the contraction index that A and B share),
+//   * and the C fragment of  X^T -= W'^T V_s^T  (C columns 2 t4, 2 t4 + 1 = those same rows).
+// W^T leaves product 1 as a C fragment (reflectors 2 t4 + e), which is the A fragment of
+// W'^T = W^T T_s under the same index permutation, and W'^T likewise feeds product 3.  So
+// applying a block reflector needs no shuffles, no barriers and no shared-memory traffic for
+// X or W; shared memory only serves the V and T_s operands.  The panel (R and raw reflectors)
+// is stored 128 x 32 unpadded with the row index XOR-swizzled per column (wy_swz), so that both
+// operand patterns are conflict-free: row pairs {8b + 2 t4, +1} of columns g, g + 1 as 16-byte
+// loads (product 1, Gram matrix) and rows 8b + g of columns 2 t4 + e as 8-byte loads (product
+// 3); the explicit form of the top 32 rows (unit diagonal, zeros above) is a second 32 x 32
+// block.  The sub-panels themselves are factored by one warp in registers (subpanel_factor).
+// 43 KB of shared memory and 128 registers: four 4-warp CTAs per SM, so the latency-bound
+// sub-panel sweeps of some fronts overlap the tensor-core phase of others.
+constexpr int kWyP = 128 * 32, kWyTop = 32 * 32;
+constexpr size_t kWySmem = sizeof(double) * (kWyP + kWyTop + 4 * 64 + 64);
+
+// x (eight columns in the register layout above) <- H_7..H_0 of sub-panel S applied
+template <int S>
+__device__ __forceinline__ void wy_apply(double2 (&x)[16], const double* P, const double* vtop, const double* sTs, int g, int t4,
+                                         int sg) {
+    // product 1: W^T = X^T V_s (rows above 8 S are zero in V_s); four accumulation chains
+    double w[4][2] = {};
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        if (b < S) continue;
+        double2 v;
+        if (b < 4)
+            v = *reinterpret_cast<const double2*>(vtop + (8 * S + g) * 32 + ((8 * b + 2 * t4) ^ sg));
+        else
+            v = *reinterpret_cast<const double2*>(P + (8 * S + g) * 128 + ((8 * b + 2 * t4) ^ sg));
+        dmma884(w[2 * (b & 1)][0], w[2 * (b & 1)][1], x[b].x, v.x);
+        dmma884(w[2 * (b & 1) + 1][0], w[2 * (b & 1) + 1][1], x[b].y, v.y);
+    }
+    const double w0 = (w[0][0] + w[1][0]) + (w[2][0] + w[3][0]);
+    const double w1 = (w[0][1] + w[1][1]) + (w[2][1] + w[3][1]);
+    // product 2: W'^T = W^T T_s, negated for product 3
+    double u0 = 0.0, u1 = 0.0;
+    dmma884(u0, u1, w0, sTs[S * 64 + (2 * t4) * 8 + g]);
+    dmma884(u0, u1, w1, sTs[S * 64 + (2 * t4 + 1) * 8 + g]);
+    u0 = -u0;
+    u1 = -u1;
+    // product 3: X^T -= W'^T V_s^T
+    const int ca = 8 * S + 2 * t4, sa = t4 << 2, sb = (t4 ^ 2) << 2;  // swizzles of columns ca, ca + 1
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        if (b < S) continue;
+        const double va = (b < 4) ? vtop[ca * 32 + ((8 * b + g) ^ sa)] : P[ca * 128 + ((8 * b + g) ^ sa)];
+        dmma884(x[b].x, x[b].y, u0, va);
+    }
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        if (b < S) continue;
+        const double vb = (b < 4) ? vtop[(ca + 1) * 32 + ((8 * b + g) ^ sb)] : P[(ca + 1) * 128 + ((8 * b + g) ^ sb)];
+        dmma884(x[b].x, x[b].y, u1, vb);
+    }
+}
+
+// T_s of sub-panel S by one warp: Gram matrix on DMMA, then row i of T_s by lane i
+// (T(i, j) = -tau_j sum_{q = i..j-1} T(i, q) G(q, j): a row only needs its own earlier entries)
+__device__ __forceinline__ void wy_subpanel_t(int S, const double* P, const double* vtop, double* sTs, double* Gs,
+                                              const double* s_tau, int lane) {
+    const int g = lane >> 2, t4 = lane & 3, sg = wy_swz(g);
+    double c[2][2] = {};
+    for (int b = S; b < 16; ++b) {  // V_s is zero above row 8 S
+        double2 v;
+        if (b < 4)
+            v = *reinterpret_cast<const double2*>(vtop + (8 * S + g) * 32 + ((8 * b + 2 * t4) ^ sg));
+        else
+            v = *reinterpret_cast<const double2*>(P + (8 * S + g) * 128 + ((8 * b + 2 * t4) ^ sg));
+        dmma884(c[0][0], c[0][1], v.x, v.x);
+        dmma884(c[1][0], c[1][1], v.y, v.y);
+    }
+    Gs[g * 8 + 2 * t4] = c[0][0] + c[1][0];
+    Gs[g * 8 + 2 * t4 + 1] = c[0][1] + c[1][1];
+    __syncwarp();
+    if (lane < 8) {
+        double t[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const double tj = s_tau[8 * S + j];
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < j; ++q)
+                if (q >= lane) acc = fma(t[q], Gs[q * 8 + j], acc);
+            t[j] = j < lane ? 0.0 : (j == lane ? tj : -tj * acc);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sTs[S * 64 + lane * 8 + j] = t[j];
+    }
+    __syncwarp();
+}
+
+template <int kNW>
+__global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_wy(const QrDesc* __restrict__ ds, const int4* __restrict__ work,
+                                                              int* __restrict__ count, long long* __restrict__ prof, int dbg) {
+    constexpr int MP = 128;
+    const int4 wk = work[blockIdx.x];
+    const QrDesc d = ds[wk.x];
+    const int m = d.m, n = d.n;  // 64 < m <= 128, n <= 32 < m: every column carries a reflector
+    const long long ld = d.ld;
+    extern __shared__ double sm[];
+    double* P = sm;  // panel, swizzled: (r, j) at j * 128 + (r ^ wy_swz(j))
+    double* vtop = sm + kWyP;
+    double* sTs = vtop + kWyTop;
+    double* Gs = sTs + 4 * 64;
+    __shared__ double s_tau[32];
+    __shared__ unsigned char s_neg[32];
+    __shared__ int s_writer;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+    const int wid = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+    long long tc[4];
+    tc[0] = prof ? clock64() : 0;
+
+    {  // stage the panel (zero padding rows and columns)
+        constexpr int NE = MP * 32 / (32 * kNW);
+        double v[NE];
+#pragma unroll
+        for (int u = 0; u < NE; ++u) {
+            const int e = threadIdx.x + u * 32 * kNW;
+            const int j = e >> 7, i = e & 127;
+            v[u] = (j < n && i < m) ? d.a[i + j * ld] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < NE; ++u) {
+            const int e = threadIdx.x + u * 32 * kNW;
+            const int j = e >> 7, i = e & 127;
+            P[j * MP + (i ^ wy_swz(j))] = v[u];
+        }
+    }
+    if (threadIdx.x < 32) s_tau[threadIdx.x] = 0.0;
+    for (int e = threadIdx.x; e < kWyTop + 4 * 64; e += blockDim.x) vtop[e] = 0.0;  // vtop and T_s
+    __syncthreads();
+    if (threadIdx.x == 0) {  // the last CTA of the front to finish staging writes the panel
+        int writer = 1;
+        if (wk.w > 1) {
+            writer = atomicAdd(count + wk.x, 1) == wk.w - 1;
+            if (writer) count[wk.x] = 0;
+        }
+        s_writer = writer;
+    }
+    tc[1] = prof ? clock64() : 0;
+    // ---- panel: factor sub-panel S (warp 0), T_s, block-apply to the later chunks (one per warp)
+    const int nchunks = __shfl_sync(0xffffffffu, (n + 7) >> 3, 0);
+    const int sg = wy_swz(g);  // swizzle of columns 8 q + g
+    for (int S = 0; S < nchunks; ++S) {
+        if (wid == 0 && !(dbg & 1)) {
+            subpanel_factor<MP, true>(P, 8 * S, n, n, s_tau, lane, vtop);
+            __syncwarp();
+            wy_subpanel_t(S, P, vtop, sTs, Gs, s_tau, lane);
+        }
+        __syncthreads();
+        if (S + 1 >= nchunks) break;
+        for (int q = S + 1 + wid; q < nchunks; q += kNW) {
+            double* yp = P + (8 * q + g) * MP;
+            double2 y[16];
+#pragma unroll
+            for (int b = 0; b < 16; ++b) y[b] = *reinterpret_cast<const double2*>(yp + ((8 * b + 2 * t4) ^ sg));
+            if (S == 0)
+                wy_apply<0>(y, P, vtop, sTs, g, t4, sg);
+            else if (S == 1)
+                wy_apply<1>(y, P, vtop, sTs, g, t4, sg);
+            else
+                wy_apply<2>(y, P, vtop, sTs, g, t4, sg);
+#pragma unroll
+            for (int b = 0; b < 16; ++b) *reinterpret_cast<double2*>(yp + ((8 * b + 2 * t4) ^ sg)) = y[b];
+        }
+        __syncthreads();
+    }
+    tc[2] = prof ? clock64() : 0;
+    for (int i = threadIdx.x; i < 32; i += blockDim.x) s_neg[i] = i < n && P[i * MP + (i ^ wy_swz(i))] < 0.0;
+    __syncthreads();
+    if (s_writer) {
+        const int tot = m * n;
+        for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+            const int j = e / m, i = e - j * m;
+            double v = P[j * MP + (i ^ wy_swz(j))];
+            if (i <= j && s_neg[i]) v = -v;
+            if (d.rout && i < n) d.rout[i + static_cast<long long>(j) * n] = (i <= j) ? v : 0.0;
+            if (d.set_identity)
+                v = (i == j) ? 1.0 : 0.0;
+            else if (d.zero_lower && i > j)
+                v = 0.0;
+            d.a[i + j * ld] = v;
+        }
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const double r = fabs(P[i * MP + (i ^ wy_swz(i))]);
+            if (d.sign) d.sign[i] = s_neg[i] ? -1.0 : 1.0;
+            if (d.tau) d.tau[i] = s_tau[i];
+            if (d.flag && !(r >= DBL_MIN)) atomicMin(d.flag, i);
+        }
+    }
+    // ---- trailing block: eight columns per warp pass, the four block reflectors in turn
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(d.a) | static_cast<uintptr_t>(ld * 8)) & 15) == 0;
+    for (int n0 = wk.y + 8 * wid; n0 < wk.z; n0 += 8 * kNW) {
+        const int col = n0 + g;
+        const bool cok = col < wk.z;
+        double* xp = d.a + static_cast<long long>(cok ? col : wk.y) * ld;
+        double2 x[16];
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            const int row = 8 * b + 2 * t4;
+            if (dbg & 2) {
+                x[b] = make_double2(1.0, 2.0);
+            } else if (cok && vec_ok && row + 1 < m) {
+                x[b] = *reinterpret_cast<const double2*>(xp + row);
+            } else {
+                x[b].x = (cok && row < m) ? xp[row] : 0.0;
+                x[b].y = (cok && row + 1 < m) ? xp[row + 1] : 0.0;
+            }
+        }
+        wy_apply<0>(x, P, vtop, sTs, g, t4, sg);
+        if (nchunks > 1) wy_apply<1>(x, P, vtop, sTs, g, t4, sg);
+        if (nchunks > 2) wy_apply<2>(x, P, vtop, sTs, g, t4, sg);
+        if (nchunks > 3) wy_apply<3>(x, P, vtop, sTs, g, t4, sg);
+        if (cok && !((dbg & 2) && x[0].x != 12345.0)) {
+#pragma unroll
+            for (int b = 0; b < 16; ++b) {
+                const int row = 8 * b + 2 * t4;
+                if (b < 4) {  // rows of negative R diagonals are flipped
+                    if (s_neg[row]) x[b].x = -x[b].x;
+                    if (s_neg[row + 1]) x[b].y = -x[b].y;
+                }
+                if (vec_ok && row + 1 < m) {
+                    *reinterpret_cast<double2*>(xp + row) = x[b];
+                } else {
+                    if (row < m) xp[row] = x[b].x;
+                    if (row + 1 < m) xp[row + 1] = x[b].y;
+                }
+            }
+        }
+    }
+    if (prof) {
+        tc[3] = clock64();
+        if (threadIdx.x == 0) {
+            for (int i = 0; i < 3; ++i) atomicAdd(reinterpret_cast<unsigned long long*>(prof) + i, static_cast<unsigned long long>(tc[i + 1] - tc[i]));
+            atomicAdd(reinterpret_cast<unsigned long long*>(prof) + 3, 1ull);
+        }
+    }
+}
+
 // The register/FMA tile phase is the default: measured on C5 128x32+256 x 4096 it
 // takes 1.85 ms against 2.16 ms for the DMMA compact-WY variant (32-column
 // passes, five barriers each); SPQR_TILE_DMMA=1 selects the latter.
 bool tile_dmma_enabled() { return std::getenv("SPQR_TILE_DMMA") != nullptr; }
+// SPQR_PANEL_REGS=1: the barrier-per-reflector register panel for every row class
+// (comparisons); default is the warp-local sub-panel sweep up to 128 rows.
+static int panel_regs_only() {
+    static const int v = std::getenv("SPQR_PANEL_REGS") ? std::atoi(std::getenv("SPQR_PANEL_REGS")) : 0;
+    return v;
+}
 
 template <int TPC>
 void launch_tile(const QrDesc* dd, const int4* dw, int nwork, size_t smem, int* count, cudaStream_t st) {
     if (tile_dmma_enabled()) {
         static SmemCfg configured;
         smem_optin(reinterpret_cast<const void*>(k_qr_tile<TPC, true>), smem, configured);
-        k_qr_tile<TPC, true><<<nwork, 32 * nw_of<TPC>(), smem, st>>>(dd, dw, count);
+        k_qr_tile<TPC, true><<<nwork, 32 * nw_of<TPC>(), smem, st>>>(dd, dw, count, panel_regs_only());
     } else {
         static SmemCfg configured;
         smem_optin(reinterpret_cast<const void*>(k_qr_tile<TPC, false>), smem, configured);
-        k_qr_tile<TPC, false><<<nwork, 32 * nw_of<TPC>(), smem, st>>>(dd, dw, count);
+        k_qr_tile<TPC, false><<<nwork, 32 * nw_of<TPC>(), smem, st>>>(dd, dw, count, panel_regs_only());
     }
 }
 
 }  // namespace
+
+bool qr_wy_ok(int m, int n, int ntot) {
+    const bool off = std::getenv("SPQR_NO_WY") != nullptr;
+    return !off && m > 64 && m <= 128 && n >= 1 && n <= 32 && ntot - n >= 64;
+}
+
+void launch_qr_wy(const QrDesc* d_desc, const int4* d_work, int nwork, int* d_count, cudaStream_t st) {
+    if (nwork <= 0) return;
+    static SmemCfg configured;
+    smem_optin(reinterpret_cast<const void*>(k_qr_wy<4>), kWySmem, configured);
+    // SPQR_WY_PROF=1: per-phase clock64 totals of thread 0 of every CTA (stage, panel, output + tiles), printed after the launch (diagnostic; synchronises)
+    static const bool prof = std::getenv("SPQR_WY_PROF") != nullptr;
+    long long* dp = nullptr;
+    if (prof) {
+        cudaMalloc(&dp, 8 * sizeof(long long));
+        cudaMemsetAsync(dp, 0, 8 * sizeof(long long), st);
+    }
+    // SPQR_WY_DBG (timing probes, wrong results): 1 = no sub-panel factorisation, 2 = no trailing loads / stores
+    static const int dbg = std::getenv("SPQR_WY_DBG") ? std::atoi(std::getenv("SPQR_WY_DBG")) : 0;
+    k_qr_wy<4><<<nwork, 128, kWySmem, st>>>(d_desc, d_work, d_count, dp, dbg);
+    if (prof) {
+        long long h[8];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, dp, sizeof(h), cudaMemcpyDeviceToHost);
+        cudaFree(dp);
+        const double c = h[3] ? double(h[3]) : 1.0;
+        std::fprintf(stderr, "[wy prof] %lld CTAs, mean cycles: stage %.0f panel %.0f output+tiles %.0f\n", h[3], h[0] / c,
+                     h[1] / c, h[2] / c);
+    }
+}
 
 int qr_tile_class(int m, int n) {
     static const int maxm = std::getenv("SPQR_TILE_MAXM") ? std::atoi(std::getenv("SPQR_TILE_MAXM")) : 512;

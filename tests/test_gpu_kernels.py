@@ -57,6 +57,35 @@ def test_qr_apply_matches_oracle(shape, path, monkeypatch):
             assert np.allclose(out[b, :, n:], X, atol=1e-12 * (1 + np.abs(X).max()))
 
 
+@pytest.mark.parametrize("shape", [(128, 32, 288), (100, 20, 150), (65, 1, 70), (127, 31, 131), (128, 32, 101),
+                                   (66, 9, 400), (120, 25, 89), (128, 8, 72), (96, 32, 2000)])
+@pytest.mark.parametrize("wy", [True, False])
+def test_qr_wy_tensor_core_path(shape, wy, monkeypatch):
+    """Fronts of 65..128 rows, panels of <= 32 columns, >= 64 trailing columns: warp-local panel
+    sweep + compact-WY on DMMA with the trailing block in registers (k_qr_wy, qr_tile.cu); odd
+    row counts (unaligned columns), ragged last column group, kmax < 32, several tiles per
+    front.  wy=False: the same shapes through the column-tiled kernel (warp-local panel)."""
+    if not wy:
+        monkeypatch.setenv("SPQR_NO_WY", "1")
+    m, n, ntot = shape
+    rng = np.random.default_rng(7 * m + n)
+    nb = 5
+    A = rng.standard_normal((nb, m, ntot))
+    if n > 3:
+        A[2, :, 3] = 0.0  # tau = 0 in the middle of a sub-panel
+    out, tau, sg, info = _P().qr_apply_batched(A, n)
+    for b in range(nb):
+        assert info[b] == (3 if (b == 2 and n > 3) else -1)
+        V, t, s, R = O.householder_qr(A[b, :, :n])
+        assert np.allclose(np.triu(out[b, :n, :n]), R, rtol=0, atol=1e-12 * (1 + np.abs(R).max()))
+        assert np.allclose(tau[b], t, atol=1e-13)
+        assert np.array_equal(sg[b], s)
+        Vg = np.tril(out[b, :, :n], -1) + np.eye(m, n)
+        assert np.allclose(Vg, V, atol=1e-12)
+        X = O.apply_reflectors(V, t, s, A[b, :, n:], "left_t")
+        assert np.allclose(out[b, :, n:], X, atol=1e-12 * (1 + np.abs(X).max()))
+
+
 @pytest.mark.parametrize("shape", [(512, 128, 384), (1024, 256, 300)])
 def test_qr_blocked_large_batch(shape):
     """Large batches: one row slice per trailing tile, so k_vtc applies T^T itself (mbqr.cu);
