@@ -562,15 +562,16 @@ __global__ void k_qr_post(double* __restrict__ a, int ld, int m, int n, double* 
 // CTA rank r of a CS-CTA cluster holds panel rows [r NW 32 RR, (r+1) NW 32 RR);
 // thread (warp g, lane l) holds rows base + g 32 RR + l + 32 q (q < RR), all w <= 32
 // panel columns, in registers.  The reflector loop is fully unrolled, so column
-// indices are compile-time.  Per reflector: tail norm of column k (warp
-// shuffles, barrier), the same Householder scalars in every thread (Eigen
-// makeHouseholder), v formed in place, the dot products of v with all columns
-// (transpose reduction: lane j ends with column j, barrier), broadcast by
-// shuffles and the rank-1 update of the columns right of k.  Lanes left of k
-// carry V^T v_k, which builds the panel's compact-WY T (accumulate_wy,
-// dense_kernels.cpp:41-53).  With CS > 1 each CTA pushes its partial sums into
-// every CTA's shared memory (remote stores), one cluster barrier per reduction,
-// and every CTA adds the CS partials in rank order (double-buffered by parity).
+// indices are compile-time.  Per reflector ONE reduction round: the products of the
+// pivot column's tail with every column (its own: the tail norm) by a transpose
+// reduction (lane j ends with column j) and the pivot row, one block barrier; the same
+// Householder scalars in every thread (Eigen makeHouseholder), v formed in place,
+// v^T x_j = x_j(k) + (tail^T x_j) / (c0 - beta) broadcast by shuffles and the rank-1
+// update of the columns right of k.  Lanes left of k carry V^T v_k, which builds the
+// panel's compact-WY T (accumulate_wy, dense_kernels.cpp:41-53).  With CS > 1 each CTA
+// pushes its column sums (rank 0: and the pivot row) into every CTA's shared memory
+// (remote stores), one cluster barrier per reflector, and every CTA adds the CS partials
+// in rank order (double-buffered by parity).
 template <int NW, int RR, int CS, bool UNR>
 __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, long long stride, int m, int j0, int w,
                                                double* __restrict__ tau_all, int tau_stride,
@@ -580,9 +581,11 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
     const int rank = CS > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
     const int b = blockIdx.x / CS;
     double* A = a + b * stride;
-    __shared__ double red[NW], part[NW][32];
-    __shared__ double s_c0;
-    __shared__ double nrm[2][CS][2], dots[2][CS][32];
+    // one reduction round per reflector (double-buffered by parity): per-warp column sums,
+    // the pivot row, and with CS > 1 every CTA's column sums and rank 0's pivot row pushed to
+    // all CTAs of the cluster
+    __shared__ double part[2][NW][32], prow[2][32];
+    __shared__ double dots[2][CS][32], crow[2][32];
     __shared__ double Ts[NB * NB], gv[NB];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int rows = m - j0;
@@ -604,41 +607,72 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
     for (int k = 0; k < NB; ++k) {
         if (k < kmax) {
             const int par = k & 1;
-            double s = 0.0;
             double xk[RR];
 #pragma unroll
             for (int q = 0; q < RR; ++q) {
                 xk[q] = x[q][0];
 #pragma unroll
                 for (int j = 1; j < NB; ++j) xk[q] = (j == k) ? x[q][j] : xk[q];
-                if (row[q] > k) s = fma(xk[q], xk[q], s);
-                if (row[q] == k) s_c0 = xk[q];
+            }
+            // p[j] = sum over this thread's rows below the pivot row of x_k x_j for every column
+            // (j = k: the tail norm), then a transpose reduction: lane j ends with column j's
+            // warp total.  The first butterfly level is folded into the products so that only
+            // 16 partials are live at a time.  With v = tail / (c0 - beta), v^T x_j is
+            // x_j(k) + (tail^T x_j) / (c0 - beta): the norm and the dot products share one round.
+            double p[16];
+            const bool up16 = lane & 16;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                double lo = 0.0, hi = 0.0;
+#pragma unroll
+                for (int q = 0; q < RR; ++q) {
+                    const double t = row[q] > k ? xk[q] : 0.0;
+                    lo = fma(t, x[q][i], lo);
+                    hi = fma(t, x[q][i + 16], hi);
+                }
+                const double send = up16 ? lo : hi;
+                const double keep = up16 ? hi : lo;
+                p[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) red[wid] = s;
+            for (int o = 8, cnt = 8; o >= 1; o >>= 1, cnt >>= 1) {
+                const bool up = lane & o;
+#pragma unroll
+                for (int i = 0; i < cnt; ++i) {
+                    const double send = up ? p[i] : p[i + cnt];
+                    const double keep = up ? p[i + cnt] : p[i];
+                    p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            part[par][wid][lane] = p[0];
+#pragma unroll
+            for (int q = 0; q < RR; ++q)
+                if (row[q] == k) {  // the pivot row (one thread of rank 0)
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) prow[par][j] = x[q][j];
+                }
             __syncthreads();
-            double tail2 = 0.0, c0 = 0.0;
+            double wl = 0.0, pr = 0.0;
             if constexpr (CS == 1) {
 #pragma unroll
-                for (int g = 0; g < NW; ++g) tail2 += red[g];
-                c0 = s_c0;
+                for (int g = 0; g < NW; ++g) wl += part[par][g][lane];
+                pr = prow[par][lane];
             } else {
-                if (threadIdx.x < CS) {  // push this CTA's partials to rank threadIdx.x
-                    double t2 = 0.0;
+                if (wid < CS) {  // warp q pushes this CTA's column sums (rank 0: and the pivot row) to ranks q, q + NW, ...
+                    double s2 = 0.0;
 #pragma unroll
-                    for (int g = 0; g < NW; ++g) t2 += red[g];
-                    double* dst = cg::this_cluster().map_shared_rank(&nrm[par][rank][0], static_cast<int>(threadIdx.x));
-                    dst[0] = t2;
-                    dst[1] = rank == 0 ? s_c0 : 0.0;
+                    for (int g = 0; g < NW; ++g) s2 += part[par][g][lane];
+                    for (int r = wid; r < CS; r += NW) {
+                        cg::this_cluster().map_shared_rank(&dots[par][rank][0], r)[lane] = s2;
+                        if (rank == 0) cg::this_cluster().map_shared_rank(&crow[par][0], r)[lane] = prow[par][lane];
+                    }
                 }
                 cg::this_cluster().sync();
 #pragma unroll
-                for (int r = 0; r < CS; ++r) {
-                    tail2 += nrm[par][r][0];
-                    c0 += nrm[par][r][1];
-                }
+                for (int r = 0; r < CS; ++r) wl += dots[par][r][lane];
+                pr = crow[par][lane];
             }
+            const double tail2 = __shfl_sync(0xffffffffu, wl, k), c0 = __shfl_sync(0xffffffffu, pr, k);
             double t = 0.0, den = 0.0, beta = c0;
             if (!(tail2 <= DBL_MIN)) {
                 beta = sqrt(c0 * c0 + tail2);
@@ -656,53 +690,9 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
                 v[q] = row[q] > k ? nv : (row[q] == k ? 1.0 : 0.0);
             }
             if (rank == 0 && threadIdx.x == 0) tau_all[static_cast<long long>(b) * tau_stride + j0 + k] = t;
-            // p[j] = sum over this thread's rows of v x_j (column k itself is not needed),
-            // then a transpose reduction: lane j ends with column j's warp total.  The
-            // first butterfly level is folded into the dot products so that only 16
-            // partials are live at a time.
-            double p[16];
-            const bool up16 = lane & 16;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                double lo = 0.0, hi = 0.0;
-#pragma unroll
-                for (int q = 0; q < RR; ++q) {
-                    lo = fma(v[q], x[q][i], lo);  // column k's own sum is never used
-                    hi = fma(v[q], x[q][i + 16], hi);
-                }
-                const double send = up16 ? lo : hi;
-                const double keep = up16 ? hi : lo;
-                p[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-            }
-#pragma unroll
-            for (int o = 8, cnt = 8; o >= 1; o >>= 1, cnt >>= 1) {
-                const bool up = lane & o;
-#pragma unroll
-                for (int i = 0; i < cnt; ++i) {
-                    const double send = up ? p[i] : p[i + cnt];
-                    const double keep = up ? p[i + cnt] : p[i];
-                    p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                }
-            }
-            part[wid][lane] = p[0];
-            __syncthreads();
-            double wl = 0.0;
-            if constexpr (CS == 1) {
-#pragma unroll
-                for (int g = 0; g < NW; ++g) wl += part[g][lane];
-            } else {
-                if (wid < CS) {  // warp q pushes this CTA's column sums to ranks q, q + NW, ...
-                    double s2 = 0.0;
-#pragma unroll
-                    for (int g = 0; g < NW; ++g) s2 += part[g][lane];
-                    for (int r = wid; r < CS; r += NW) cg::this_cluster().map_shared_rank(&dots[par][rank][0], r)[lane] = s2;
-                }
-                cg::this_cluster().sync();
-#pragma unroll
-                for (int r = 0; r < CS; ++r) wl += dots[par][r][lane];
-            }
+            const double vx = fma(wl, rden, pr);  // lane j: v^T x_j
             if (t != 0.0) {
-                const double twl = lane > k ? -t * wl : 0.0;
+                const double twl = lane > k ? -t * vx : 0.0;
 #pragma unroll
                 for (int j = UNR ? k + 1 : 1; j < NB; ++j) {
                     const double tw = __shfl_sync(0xffffffffu, twl, j);
@@ -711,7 +701,7 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
                 }
             }
             if (rank == 0 && wid == 0) {  // V^T v_k and tau_k for T, built after the loop
-                if (lane < k) Ts[lane + k * NB] = wl;
+                if (lane < k) Ts[lane + k * NB] = t != 0.0 ? vx : 0.0;
                 if (lane == 0) gv[k] = t;
             }
         }

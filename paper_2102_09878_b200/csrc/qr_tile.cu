@@ -680,7 +680,8 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_tile(const QrDesc* __
 // 43 KB of shared memory and 128 registers: four 4-warp CTAs per SM, so the latency-bound
 // sub-panel sweeps of some fronts overlap the tensor-core phase of others.
 constexpr int kWyP = 128 * 32, kWyTop = 32 * 32;
-constexpr size_t kWySmem = sizeof(double) * (kWyP + kWyTop + 4 * 64 + 64);
+constexpr int kWyLT = 10, kWyT = 8 * kWyLT;  // T_s row-major with padded rows: the (2 t4 + e, g) loads are conflict-free
+constexpr size_t kWySmem = sizeof(double) * (kWyP + kWyTop + 4 * kWyT + 64);
 
 // x (eight columns in the register layout above) <- H_7..H_0 of sub-panel S applied
 template <int S>
@@ -703,8 +704,8 @@ __device__ __forceinline__ void wy_apply(double2 (&x)[16], const double* P, cons
     const double w1 = (w[0][1] + w[1][1]) + (w[2][1] + w[3][1]);
     // product 2: W'^T = W^T T_s, negated for product 3
     double u0 = 0.0, u1 = 0.0;
-    dmma884(u0, u1, w0, sTs[S * 64 + (2 * t4) * 8 + g]);
-    dmma884(u0, u1, w1, sTs[S * 64 + (2 * t4 + 1) * 8 + g]);
+    dmma884(u0, u1, w0, sTs[S * kWyT + (2 * t4) * kWyLT + g]);
+    dmma884(u0, u1, w1, sTs[S * kWyT + (2 * t4 + 1) * kWyLT + g]);
     u0 = -u0;
     u1 = -u1;
     // product 3: X^T -= W'^T V_s^T
@@ -753,7 +754,7 @@ __device__ __forceinline__ void wy_subpanel_t(int S, const double* P, const doub
             t[j] = j < lane ? 0.0 : (j == lane ? tj : -tj * acc);
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) sTs[S * 64 + lane * 8 + j] = t[j];
+        for (int j = 0; j < 8; ++j) sTs[S * kWyT + lane * kWyLT + j] = t[j];
     }
     __syncwarp();
 }
@@ -770,7 +771,7 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_wy(const QrDesc* __re
     double* P = sm;  // panel, swizzled: (r, j) at j * 128 + (r ^ wy_swz(j))
     double* vtop = sm + kWyP;
     double* sTs = vtop + kWyTop;
-    double* Gs = sTs + 4 * 64;
+    double* Gs = sTs + 4 * kWyT;
     __shared__ double s_tau[32];
     __shared__ unsigned char s_neg[32];
     __shared__ int s_writer;
@@ -796,7 +797,7 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_wy(const QrDesc* __re
         }
     }
     if (threadIdx.x < 32) s_tau[threadIdx.x] = 0.0;
-    for (int e = threadIdx.x; e < kWyTop + 4 * 64; e += blockDim.x) vtop[e] = 0.0;  // vtop and T_s
+    for (int e = threadIdx.x; e < kWyTop + 4 * kWyT; e += blockDim.x) vtop[e] = 0.0;  // vtop and T_s
     __syncthreads();
     if (threadIdx.x == 0) {  // the last CTA of the front to finish staging writes the panel
         int writer = 1;
