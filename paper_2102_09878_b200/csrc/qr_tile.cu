@@ -683,20 +683,42 @@ constexpr int kWyP = 128 * 32, kWyTop = 32 * 32;
 constexpr int kWyLT = 10, kWyT = 8 * kWyLT;  // T_s row-major with padded rows: the (2 t4 + e, g) loads are conflict-free
 constexpr size_t kWySmem = sizeof(double) * (kWyP + kWyTop + 4 * kWyT + 64);
 
-// x (eight columns in the register layout above) <- H_7..H_0 of sub-panel S applied
+// global-memory accesses of the trailing block (the pointer comes out of a descriptor, so the
+// compiler would otherwise emit generic loads and stores)
+__device__ __forceinline__ double2 wy_ldg2(const double* p) {
+    double2 v;
+    asm("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double wy_ldg(const double* p) {
+    double v;
+    asm("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void wy_stg2(double* p, double2 v) {
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void wy_stg(double* p, double v) { asm volatile("st.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory"); }
+
+// x (eight columns in the register layout above) <- H_7..H_0 of sub-panel S applied.
+// Operand addresses: the swizzle only touches bits 2 and 3 of the row index, so
+// (8b + r) ^ s = (r ^ (s & 4)) + 8 (b ^ (s >> 3 & 1)): one base pointer for even b and one
+// for odd b per operand, and every load is base + constant.
 template <int S>
 __device__ __forceinline__ void wy_apply(double2 (&x)[16], const double* P, const double* vtop, const double* sTs, int g, int t4,
                                          int sg) {
     // product 1: W^T = X^T V_s (rows above 8 S are zero in V_s); four accumulation chains
+    const int o1 = ((2 * t4) ^ (sg & 4)), h1 = 8 * ((sg >> 3) & 1);
+    const double* p1e = P + (8 * S + g) * 128 + o1 + h1;
+    const double* p1o = P + (8 * S + g) * 128 + o1 - h1;
+    const double* q1e = vtop + (8 * S + g) * 32 + o1 + h1;
+    const double* q1o = vtop + (8 * S + g) * 32 + o1 - h1;
     double w[4][2] = {};
 #pragma unroll
     for (int b = 0; b < 16; ++b) {
         if (b < S) continue;
-        double2 v;
-        if (b < 4)
-            v = *reinterpret_cast<const double2*>(vtop + (8 * S + g) * 32 + ((8 * b + 2 * t4) ^ sg));
-        else
-            v = *reinterpret_cast<const double2*>(P + (8 * S + g) * 128 + ((8 * b + 2 * t4) ^ sg));
+        const double* src = (b < 4) ? ((b & 1) ? q1o : q1e) : ((b & 1) ? p1o : p1e);
+        const double2 v = *reinterpret_cast<const double2*>(src + 8 * b);
         dmma884(w[2 * (b & 1)][0], w[2 * (b & 1)][1], x[b].x, v.x);
         dmma884(w[2 * (b & 1) + 1][0], w[2 * (b & 1) + 1][1], x[b].y, v.y);
     }
@@ -708,18 +730,24 @@ __device__ __forceinline__ void wy_apply(double2 (&x)[16], const double* P, cons
     dmma884(u0, u1, w1, sTs[S * kWyT + (2 * t4 + 1) * kWyLT + g]);
     u0 = -u0;
     u1 = -u1;
-    // product 3: X^T -= W'^T V_s^T
-    const int ca = 8 * S + 2 * t4, sa = t4 << 2, sb = (t4 ^ 2) << 2;  // swizzles of columns ca, ca + 1
+    // product 3: X^T -= W'^T V_s^T; columns ca = 8 S + 2 t4 and ca + 1 (swizzles t4 << 2, (t4 ^ 2) << 2)
+    const int ca = 8 * S + 2 * t4;
+    const int oa = g ^ ((t4 << 2) & 4), ha = 8 * ((t4 >> 1) & 1);
+    const int ob = g ^ (((t4 ^ 2) << 2) & 4), hb = 8 * (((t4 ^ 2) >> 1) & 1);
+    const double* p3a[2] = {P + ca * 128 + oa + ha, P + ca * 128 + oa - ha};
+    const double* q3a[2] = {vtop + ca * 32 + oa + ha, vtop + ca * 32 + oa - ha};
+    const double* p3b[2] = {P + (ca + 1) * 128 + ob + hb, P + (ca + 1) * 128 + ob - hb};
+    const double* q3b[2] = {vtop + (ca + 1) * 32 + ob + hb, vtop + (ca + 1) * 32 + ob - hb};
 #pragma unroll
     for (int b = 0; b < 16; ++b) {
         if (b < S) continue;
-        const double va = (b < 4) ? vtop[ca * 32 + ((8 * b + g) ^ sa)] : P[ca * 128 + ((8 * b + g) ^ sa)];
+        const double va = (b < 4) ? q3a[b & 1][8 * b] : p3a[b & 1][8 * b];
         dmma884(x[b].x, x[b].y, u0, va);
     }
 #pragma unroll
     for (int b = 0; b < 16; ++b) {
         if (b < S) continue;
-        const double vb = (b < 4) ? vtop[(ca + 1) * 32 + ((8 * b + g) ^ sb)] : P[(ca + 1) * 128 + ((8 * b + g) ^ sb)];
+        const double vb = (b < 4) ? q3b[b & 1][8 * b] : p3b[b & 1][8 * b];
         dmma884(x[b].x, x[b].y, u1, vb);
     }
 }
@@ -833,8 +861,12 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_wy(const QrDesc* __re
 #pragma unroll
             for (int b = 0; b < 16; ++b) *reinterpret_cast<double2*>(yp + ((8 * b + 2 * t4) ^ sg)) = y[b];
         }
-        __syncthreads();
+        // no barrier here: warp 0 has just updated chunk S + 1 itself and goes on to factor it
+        // while the other warps finish theirs (they touch neither that chunk nor T_{S+1}); the
+        // barrier after the next factorisation orders their updates before the next round
+        __syncwarp();
     }
+    __syncthreads();
     tc[2] = prof ? clock64() : 0;
     for (int i = threadIdx.x; i < 32; i += blockDim.x) s_neg[i] = i < n && P[i * MP + (i ^ wy_swz(i))] < 0.0;
     __syncthreads();
@@ -871,10 +903,10 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_wy(const QrDesc* __re
             if (dbg & 2) {
                 x[b] = make_double2(1.0, 2.0);
             } else if (cok && vec_ok && row + 1 < m) {
-                x[b] = *reinterpret_cast<const double2*>(xp + row);
+                x[b] = wy_ldg2(xp + row);
             } else {
-                x[b].x = (cok && row < m) ? xp[row] : 0.0;
-                x[b].y = (cok && row + 1 < m) ? xp[row + 1] : 0.0;
+                x[b].x = (cok && row < m) ? wy_ldg(xp + row) : 0.0;
+                x[b].y = (cok && row + 1 < m) ? wy_ldg(xp + row + 1) : 0.0;
             }
         }
         wy_apply<0>(x, P, vtop, sTs, g, t4, sg);
@@ -890,10 +922,10 @@ __global__ void __launch_bounds__(32 * kNW, 16 / kNW) k_qr_wy(const QrDesc* __re
                     if (s_neg[row + 1]) x[b].y = -x[b].y;
                 }
                 if (vec_ok && row + 1 < m) {
-                    *reinterpret_cast<double2*>(xp + row) = x[b];
+                    wy_stg2(xp + row, x[b]);
                 } else {
-                    if (row < m) xp[row] = x[b].x;
-                    if (row + 1 < m) xp[row + 1] = x[b].y;
+                    if (row < m) wy_stg(xp + row, x[b].x);
+                    if (row + 1 < m) wy_stg(xp + row + 1, x[b].y);
                 }
             }
         }
