@@ -543,7 +543,7 @@ int spqr_qr_apply_batched_dev(int nb, int m, int n, int ntot, double* d_a, doubl
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, 0));
-        if (tile && qr_wy_ok(m, n, ntot))
+        if (tile && qr_wy_enabled() && qr_wy_ok(m, n, ntot))
             launch_qr_wy(dq, dwork, nwork, reinterpret_cast<int*>(dwork + std::max(nwork, 1)), 0);
         else if (tile)
             launch_qr_tile(tcls, dq, dwork, nwork, qr_tile_smem(tcls, n), reinterpret_cast<int*>(dwork + std::max(nwork, 1)), 0);

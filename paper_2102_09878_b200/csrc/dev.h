@@ -232,7 +232,8 @@ void launch_qr_tile(int cls, const QrDesc* d_desc, const int4* d_work, int nwork
 std::vector<int4> qr_tile_plan(const QrDesc* hq, const int* idx, int cnt, int sms);
 // compact-WY tensor-core variant for fronts of 65..128 rows, panels of <= 32 columns and a
 // trailing block of >= 64 columns (same work plan and election counter as the tiled kernel)
-bool qr_wy_ok(int m, int n, int ntot);
+bool qr_wy_ok(int m, int n, int ntot);  // shape test
+bool qr_wy_enabled();                  // SPQR_NO_WY=1 keeps every front on the column-tiled kernel (comparisons, tests)
 void launch_qr_wy(const QrDesc* d_desc, const int4* d_work, int nwork, int* d_count, cudaStream_t st);
 
 // grid-cooperative CPQR of one large problem (cpqr_big.cu); d.work needs

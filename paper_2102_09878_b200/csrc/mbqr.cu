@@ -572,7 +572,8 @@ __global__ void k_qr_post(double* __restrict__ a, int ld, int m, int n, double* 
 // pushes its column sums (rank 0: and the pivot row) into every CTA's shared memory
 // (remote stores), one cluster barrier per reflector, and every CTA adds the CS partials
 // in rank order (double-buffered by parity).
-template <int NW, int RR, int CS, bool UNR>
+constexpr int kPanelUB = 8;  // reflectors unrolled per group (NB must be a multiple)
+template <int NW, int RR, int CS, int UB>
 __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, long long stride, int m, int j0, int w,
                                                double* __restrict__ tau_all, int tau_stride,
                                                double* __restrict__ T_all) {
@@ -584,7 +585,7 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
     // one reduction round per reflector (double-buffered by parity): per-warp column sums,
     // the pivot row, and with CS > 1 every CTA's column sums and rank 0's pivot row pushed to
     // all CTAs of the cluster
-    __shared__ double part[2][NW][32], prow[2][32];
+    __shared__ double part[2][NW][32], prow[2][32], tws[NW][32];
     __shared__ double dots[2][CS][32], crow[2][32];
     __shared__ double Ts[NB * NB], gv[NB];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -600,20 +601,21 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
             x[q][j] = (row[q] < rows && j < w) ? A[(j0 + row[q]) + static_cast<long long>(j0 + j) * ld] : 0.0;
     for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) Ts[e] = 0.0;
     const int kmax = min(w, rows);
-    // UNR: reflector loop fully unrolled (column k static).  Otherwise column k is
-    // read and written through select chains (a much smaller loop body: the
-    // unrolled one overflows the instruction cache)
-#pragma unroll UNR ? NB : 1
-    for (int k = 0; k < NB; ++k) {
-        if (k < kmax) {
-            const int par = k & 1;
+    // The reflector loop is unrolled UB at a time and the register columns are rotated by UB
+    // after every group, so the pivot column always sits at a static position kk < UB: column
+    // indices stay compile-time without unrolling all 32 reflectors (whose code overflowed the
+    // instruction cache: 44 % of the stall samples were instruction fetches) and without
+    // select chains.  Position p holds panel column (p + k0) mod 32; lanes map the same way.
+#pragma unroll 1
+    for (int k0 = 0; k0 < NB; k0 += UB) {
+#pragma unroll
+        for (int kk = 0; kk < UB; ++kk) {
+            const int k = k0 + kk;
+            if (k < kmax) {
+            const int par = kk & 1;
             double xk[RR];
 #pragma unroll
-            for (int q = 0; q < RR; ++q) {
-                xk[q] = x[q][0];
-#pragma unroll
-                for (int j = 1; j < NB; ++j) xk[q] = (j == k) ? x[q][j] : xk[q];
-            }
+            for (int q = 0; q < RR; ++q) xk[q] = x[q][kk];
             // p[j] = sum over this thread's rows below the pivot row of x_k x_j for every column
             // (j = k: the tail norm), then a transpose reduction: lane j ends with column j's
             // warp total.  The first butterfly level is folded into the products so that only
@@ -672,7 +674,7 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
                 for (int r = 0; r < CS; ++r) wl += dots[par][r][lane];
                 pr = crow[par][lane];
             }
-            const double tail2 = __shfl_sync(0xffffffffu, wl, k), c0 = __shfl_sync(0xffffffffu, pr, k);
+            const double tail2 = __shfl_sync(0xffffffffu, wl, kk), c0 = __shfl_sync(0xffffffffu, pr, kk);
             double t = 0.0, den = 0.0, beta = c0;
             if (!(tail2 <= DBL_MIN)) {
                 beta = sqrt(c0 * c0 + tail2);
@@ -685,25 +687,39 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
 #pragma unroll
             for (int q = 0; q < RR; ++q) {
                 const double nv = row[q] > k ? xk[q] * rden : (row[q] == k ? beta : xk[q]);
-#pragma unroll
-                for (int j = 0; j < NB; ++j) x[q][j] = (j == k) ? nv : x[q][j];
+                x[q][kk] = nv;
                 v[q] = row[q] > k ? nv : (row[q] == k ? 1.0 : 0.0);
             }
             if (rank == 0 && threadIdx.x == 0) tau_all[static_cast<long long>(b) * tau_stride + j0 + k] = t;
-            const double vx = fma(wl, rden, pr);  // lane j: v^T x_j
-            if (t != 0.0) {
-                const double twl = lane > k ? -t * vx : 0.0;
+            const double vx = fma(wl, rden, pr);  // lane p: v^T x of the column at position p
+            const int oc = (lane + k0) & (NB - 1);  // that column
+            // -tau v^T x_j to every lane through the warp's own shared-memory row (broadcast
+            // loads); zero for the columns already factored (rotated to the high positions)
+            tws[wid][lane] = (t != 0.0 && oc > k) ? -t * vx : 0.0;
+            __syncwarp();
 #pragma unroll
-                for (int j = UNR ? k + 1 : 1; j < NB; ++j) {
-                    const double tw = __shfl_sync(0xffffffffu, twl, j);
+            for (int pp = kk + 1; pp < NB; ++pp) {
+                const double tw = tws[wid][pp];
 #pragma unroll
-                    for (int q = 0; q < RR; ++q) x[q][j] = fma(tw, v[q], x[q][j]);
-                }
+                for (int q = 0; q < RR; ++q) x[q][pp] = fma(tw, v[q], x[q][pp]);
             }
+            __syncwarp();
             if (rank == 0 && wid == 0) {  // V^T v_k and tau_k for T, built after the loop
-                if (lane < k) Ts[lane + k * NB] = t != 0.0 ? vx : 0.0;
+                if (oc < k) Ts[oc + k * NB] = t != 0.0 ? vx : 0.0;
                 if (lane == 0) gv[k] = t;
             }
+            }
+        }
+        // rotate the columns by UB positions
+#pragma unroll
+        for (int q = 0; q < RR; ++q) {
+            double tmp[UB];
+#pragma unroll
+            for (int i = 0; i < UB; ++i) tmp[i] = x[q][i];
+#pragma unroll
+            for (int pp = 0; pp + UB < NB; ++pp) x[q][pp] = x[q][pp + UB];
+#pragma unroll
+            for (int i = 0; i < UB; ++i) x[q][NB - UB + i] = tmp[i];
         }
     }
     if constexpr (CS > 1) cg::this_cluster().sync();  // no remote store may target an exited CTA
@@ -743,14 +759,14 @@ template <int NW, int RR>
 __global__ void __launch_bounds__(32 * NW, NW * RR <= 8 ? 2 : 1) k_panel_row(double* a, int ld, long long stride,
                                                                            int m, int j0, int w, double* tau_all,
                                                                            int tau_stride, double* T_all) {
-    panel_row_body<NW, RR, 1, true>(a, ld, stride, m, j0, w, tau_all, tau_stride, T_all);
+    panel_row_body<NW, RR, 1, kPanelUB>(a, ld, stride, m, j0, w, tau_all, tau_stride, T_all);
 }
 
 template <int NW, int RR>
 __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(32 * NW, NW * RR <= 8 ? 2 : 1)
     k_panel_rowc(double* a, int ld, long long stride, int m, int j0, int w, double* tau_all, int tau_stride,
                  double* T_all) {
-    panel_row_body<NW, RR, kCS, true>(a, ld, stride, m, j0, w, tau_all, tau_stride, T_all);
+    panel_row_body<NW, RR, kCS, kPanelUB>(a, ld, stride, m, j0, w, tau_all, tau_stride, T_all);
 }
 
 // register-resident panel launch; false when the panel is too tall

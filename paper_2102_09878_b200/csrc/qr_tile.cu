@@ -965,10 +965,8 @@ void launch_tile(const QrDesc* dd, const int4* dw, int nwork, size_t smem, int* 
 
 }  // namespace
 
-bool qr_wy_ok(int m, int n, int ntot) {
-    const bool off = std::getenv("SPQR_NO_WY") != nullptr;
-    return !off && m > 64 && m <= 128 && n >= 1 && n <= 32 && ntot - n >= 64;
-}
+bool qr_wy_ok(int m, int n, int ntot) { return m > 64 && m <= 128 && n >= 1 && n <= 32 && ntot - n >= 64; }
+bool qr_wy_enabled() { return std::getenv("SPQR_NO_WY") == nullptr; }
 
 void launch_qr_wy(const QrDesc* d_desc, const int4* d_work, int nwork, int* d_count, cudaStream_t st) {
     if (nwork <= 0) return;
