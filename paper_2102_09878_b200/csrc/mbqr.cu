@@ -736,17 +736,24 @@ __device__ __forceinline__ void panel_row_body(double* __restrict__ a, int ld, l
     // compact-WY T from the recorded V^T v_k (strict upper part of Ts) and tau
     // (accumulate_wy, dense_kernels.cpp:41-53): T(0:k, k) = -tau_k T(0:k, 0:k) (V^T v_k),
     // T(k, k) = tau_k; one warp, off the per-reflector critical path
+    // Lane i keeps row i of T in registers (fully unrolled: the recorded V^T v_k are independent
+    // broadcast loads, the recurrence itself is ~500 FMAs in four chains per step) - this tail
+    // runs while every other warp of the CTA (and cluster) has finished, so it is serial time.
     if (rank == 0 && wid == 0) {
         __syncwarp();
-        for (int k = 0; k < kmax; ++k) {
-            double sacc = 0.0;
-            if (lane < k)
-                for (int l = lane; l < k; ++l) sacc = fma(Ts[lane + l * NB], Ts[l + k * NB], sacc);
-            __syncwarp();
-            if (lane < k) Ts[lane + k * NB] = -gv[k] * sacc;
-            if (lane == k) Ts[k + k * NB] = gv[k];
-            __syncwarp();
+        double trow[NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+            const double tk = k < kmax ? gv[k] : 0.0;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int l = 0; l < k; ++l) acc[l & 3] = fma(trow[l], Ts[l + k * NB], acc[l & 3]);  // trow[l] = 0 for l < lane
+            trow[k] = lane < k ? -tk * ((acc[0] + acc[1]) + (acc[2] + acc[3])) : (lane == k ? tk : 0.0);
         }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+            if (lane <= k) Ts[lane + k * NB] = trow[k];
     }
     __syncthreads();
     if (rank == 0) {
