@@ -1155,7 +1155,7 @@ __global__ void __launch_bounds__(256, 2) k_cvw2(double* __restrict__ a, int ld,
         const double* sV = sV0 + (s & 1) * (KC * LDM);
         const double* sW = sW0 + (s & 1) * (TCG * LDK);
         const int kend = min(KC, ((kw - s * KC) + 3) & ~3);
-#pragma unroll 2
+#pragma unroll 4
         for (int k0 = 0; k0 < kend; k0 += 4) {
             double av[4], bv[4];
 #pragma unroll
