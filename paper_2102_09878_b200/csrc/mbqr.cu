@@ -561,13 +561,14 @@ __global__ void k_qr_post(double* __restrict__ a, int ld, int m, int n, double* 
 // Register-resident panel factorisation for the two-level path, row layout:
 // CTA rank r of a CS-CTA cluster holds panel rows [r NW 32 RR, (r+1) NW 32 RR);
 // thread (warp g, lane l) holds rows base + g 32 RR + l + 32 q (q < RR), all w <= 32
-// panel columns, in registers.  The reflector loop is fully unrolled, so column
-// indices are compile-time.  Per reflector ONE reduction round: the products of the
+// panel columns, in registers.  The reflector loop is unrolled UB at a time with the register
+// columns rotated after every group (see below), so column indices are compile-time.  Per
+// reflector ONE reduction round: the products of the
 // pivot column's tail with every column (its own: the tail norm) by a transpose
 // reduction (lane j ends with column j) and the pivot row, one block barrier; the same
 // Householder scalars in every thread (Eigen makeHouseholder), v formed in place,
-// v^T x_j = x_j(k) + (tail^T x_j) / (c0 - beta) broadcast by shuffles and the rank-1
-// update of the columns right of k.  Lanes left of k carry V^T v_k, which builds the
+// v^T x_j = x_j(k) + (tail^T x_j) / (c0 - beta) broadcast through a per-warp shared-memory
+// row and the rank-1 update of the columns right of k.  Lanes left of k carry V^T v_k, which builds the
 // panel's compact-WY T (accumulate_wy, dense_kernels.cpp:41-53).  With CS > 1 each CTA
 // pushes its column sums (rank 0: and the pivot row) into every CTA's shared memory
 // (remote stores), one cluster barrier per reflector, and every CTA adds the CS partials
