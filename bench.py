@@ -72,6 +72,12 @@ def dist_init():
             local, backend = 0, "gloo"        # rank on cuda:0, collectives on the host (not a measurement)
         if backend == "nccl":
             torch.cuda.set_device(local)
+            # the ranks read each other's values over CUDA IPC peer mappings; a node whose GPUs
+            # cannot map one another's memory sends the values through the host transport instead
+            # (every rank sees the same devices, so every rank decides the same way)
+            n = min(lws, torch.cuda.device_count())
+            if not all(torch.cuda.can_device_access_peer(i, j) for i in range(n) for j in range(n) if i != j):
+                os.environ.setdefault("SPQR_DIST_HOST", "1")
         dist.init_process_group(backend)
     return ws, rank, local
 
