@@ -1194,6 +1194,131 @@ __global__ void __launch_bounds__(256, 2) k_cvw2(double* __restrict__ a, int ld,
 }
 constexpr size_t kCvw2Smem = sizeof(double) * (2 * KC * LDM + 2 * TCG * LDK);
 
+// k_cvw2 with 64-row tiles, 4-warp CTAs and KCT-reflector stages: four CTAs per SM (38 KB of
+// shared memory and 16 K registers each at KCT = 16) instead of two.  Measured on C5 4096x1024:
+// 39.2 ms against 40.3 ms with k_cvw2, although a tile moves 18 % more bytes through L2 per flop
+// — the barrier-synchronised phases of a CTA (stage wait, DMMA stage, C read-modify-write) leave
+// the FP64 tensor pipe idle unless enough INDEPENDENT CTAs share the SM; the opposite change
+// (one 16-warp CTA per SM, W2 resident, 40 % fewer bytes per flop) ran 44.1 ms (DESIGN 6).
+template <int KB, int KCT>
+__global__ void __launch_bounds__(128, 4) k_cvw4(double* __restrict__ a, int ld, long long stride, int m, int J0,
+                                                 int kw, int cbeg, int cend, const double* __restrict__ wp, int nsl) {
+    constexpr int CMT = 64, LDM4 = CMT + 4, LDK4 = KCT + 4, NT = 128;
+    const int t = blockIdx.x, rtile = blockIdx.y, b = blockIdx.z, ntile = gridDim.x;
+    double* A = a + b * stride;
+    const int rows = m - J0;
+    const int c0 = cbeg + t * TCG, nc = min(TCG, cend - c0);
+    const int r0 = rtile * CMT;
+    const double* W2 = wp + (static_cast<long long>(b) * nsl * ntile + t) * (KB * TCG);
+    extern __shared__ double dsm[];
+    double* const sV0 = dsm;                    // two stages of CMT x KCT
+    double* const sW0 = dsm + 2 * KCT * LDM4;   // two stages of KCT x TCG
+    const int nst = (kw + KCT - 1) / KCT;
+    {
+        const int e = threadIdx.x;  // 128 threads: column e / 2, 32-row half e % 2
+        const int c = e >> 1, rq = (e & 1) * 32;
+        if (c < nc && r0 + rq < rows) {
+            const double* pc = A + (J0 + r0 + rq) + static_cast<long long>(c0 + c) * ld;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pc));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + 16));
+        }
+    }
+    const bool vec = ((ld & 1) == 0) && ((J0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+                     r0 >= KB && r0 + CMT <= rows;
+    auto issue = [&](int s) {
+        double* vb = sV0 + (s & 1) * (KCT * LDM4);
+        double* wb = sW0 + (s & 1) * (TCG * LDK4);
+        const int k0 = s * KCT;
+        if (vec) {
+            for (int e = threadIdx.x; e < CMT * KCT / 2; e += NT) {
+                const int i = 2 * (e % (CMT / 2)), j = e / (CMT / 2), jj = k0 + j;
+                if (jj < kw)
+                    cp_async16(vb + i + j * LDM4, A + (J0 + r0 + i) + static_cast<long long>(J0 + jj) * ld);
+                else
+                    vb[i + j * LDM4] = vb[i + 1 + j * LDM4] = 0.0;
+            }
+        } else {
+            for (int e = threadIdx.x; e < CMT * KCT; e += NT) {
+                const int i = e % CMT, j = e / CMT, r = r0 + i, jj = k0 + j;
+                double* dst = vb + i + j * LDM4;
+                double v;
+                if (r >= rows) *dst = 0.0;
+                else if (v_direct(r, jj, kw, v)) *dst = v;
+                else cp_async8(dst, A + (J0 + r) + static_cast<long long>(J0 + jj) * ld, true);
+            }
+        }
+        for (int e = threadIdx.x; e < KCT * TCG / 2; e += NT) {
+            const int j = 2 * (e % (KCT / 2)), c = e / (KCT / 2);
+            if (k0 + j < KB)
+                cp_async16(wb + j + c * LDK4, W2 + (k0 + j) + c * KB);
+            else
+                wb[j + c * LDK4] = wb[j + 1 + c * LDK4] = 0.0;
+        }
+        cp_commit();
+    };
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int mw = wid & 1, nw = wid >> 1;
+    double acc[4][4][2] = {};
+    issue(0);
+    for (int s = 0; s < nst; ++s) {
+        if (s + 1 < nst) {
+            issue(s + 1);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        const double* sV = sV0 + (s & 1) * (KCT * LDM4);
+        const double* sW = sW0 + (s & 1) * (TCG * LDK4);
+        const int kend = min(KCT, ((kw - s * KCT) + 3) & ~3);
+#pragma unroll 4
+        for (int k0 = 0; k0 < kend; k0 += 4) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = sV[(mw * 32 + i * 8 + g) + (k0 + t4) * LDM4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) bv[q] = sW[(k0 + t4) + (nw * 32 + q * 8 + g) * LDK4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) dmma(acc[i][q][0], acc[i][q][1], av[i], bv[q]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = r0 + mw * 32 + i * 8 + g;
+        double* crow = A + (J0 + r) + static_cast<long long>(c0) * ld;
+        double cv[4][2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = nw * 32 + q * 8 + 2 * t4 + h;
+                cv[q][h] = (r < rows && c < nc) ? crow[static_cast<long long>(c) * ld] : 0.0;
+            }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = nw * 32 + q * 8 + 2 * t4 + h;
+                if (r < rows && c < nc) crow[static_cast<long long>(c) * ld] = cv[q][h] - acc[i][q][h];
+            }
+    }
+}
+template <int KCT>
+constexpr size_t cvw4_smem() {
+    return sizeof(double) * (2 * KCT * (64 + 4) + 2 * TCG * (KCT + 4));
+}
+template <int KB, int KCT>
+void launch_cvw4(dim3 grid, cudaStream_t st, double* d_a, int ld, long long stride, int m, int J0, int kw, int cbeg,
+                 int cend, const double* wp, int nsl) {
+    static SmemCfg cfg;
+    smem_optin(reinterpret_cast<const void*>(k_cvw4<KB, KCT>), cvw4_smem<KCT>(), cfg);
+    k_cvw4<KB, KCT><<<grid, 128, cvw4_smem<KCT>(), st>>>(d_a, ld, stride, m, J0, kw, cbeg, cend, wp, nsl);
+}
+
 // Outer T (KO x KO) of an outer block whose four NB-column panels have compact-WY
 // factors T_q (written by the panel kernels), composed pairwise:
 //   H_A H_B = I - [V_A V_B] [T_A, -T_A (V_A^T V_B) T_B; 0, T_B] [V_A V_B]^T
@@ -1359,7 +1484,18 @@ void apply_block(BigWs& ws, int nbatch, int m, int ld, long long stride, double*
         smem_optin(reinterpret_cast<const void*>(k_tw<KB>), sm, cfg);
         k_tw<KB><<<dim3(ntile, nbatch), 256, sm, st>>>(wp, nsl, T_all, kw);
     }
-    if (!std::getenv("SPQR_CVW1")) {
+    // k_cvw4 (64-row tiles, 4-warp CTAs) for the KO-wide block reflectors and the NB-wide inner
+    // updates; SPQR_CVW4=0 keeps k_cvw2, =32 takes 32-reflector stages, SPQR_CVW4_INNER=0 leaves the
+    // inner updates on k_cvw2 (comparisons)
+    static const int cvw4 = std::getenv("SPQR_CVW4") ? std::atoi(std::getenv("SPQR_CVW4")) : 16;
+    static const bool cvw4_inner = !std::getenv("SPQR_CVW4_INNER") || std::atoi(std::getenv("SPQR_CVW4_INNER")) != 0;
+    if (cvw4 && (KB > NB || cvw4_inner)) {
+        const dim3 grid(ntile, (rows + 63) / 64, nbatch);
+        if (cvw4 == 16)
+            launch_cvw4<KB, 16>(grid, st, d_a, ld, stride, m, J0, kw, cbeg, cend, wp, nsl);
+        else
+            launch_cvw4<KB, 32>(grid, st, d_a, ld, stride, m, J0, kw, cbeg, cend, wp, nsl);
+    } else if (!std::getenv("SPQR_CVW1")) {
         static SmemCfg cfg;
         smem_optin(reinterpret_cast<const void*>(k_cvw2<KB>), kCvw2Smem, cfg);
         k_cvw2<KB><<<dim3(ntile, (rows + CM - 1) / CM, nbatch), 256, kCvw2Smem, st>>>(d_a, ld, stride, m, J0, kw, cbeg,
