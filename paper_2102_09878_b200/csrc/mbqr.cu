@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(256) k_vtc(const double* __restrict__ a, int l
                                              double* __restrict__ wp, const double* __restrict__ T_all) {
     constexpr int PM = KB / 32, PN = TCG / 16;
     const int t = blockIdx.x, s = blockIdx.y, b = blockIdx.z;
-    const int ntile = gridDim.x, nsl = gridDim.y;
+    const int ntile = gram ? KB / TCG : gridDim.x, nsl = gridDim.y;  // Gram: one CTA per slice, KB / TCG tiles in the layout
     const double* A = a + b * stride;
     const int rows = m - J0;
     const int c0 = cbeg + t * TCG, nc = min(TCG, cend - c0);
@@ -857,7 +857,7 @@ __global__ void __launch_bounds__(256) k_vtc(const double* __restrict__ a, int l
                 else
                     vb[i + j * LDS_] = vb[i + 1 + j * LDS_] = 0.0;
             }
-            for (int e = threadIdx.x; e < CHG * TCG / 2; e += 256) {
+            for (int e = threadIdx.x; e < (gram ? 0 : CHG * TCG / 2); e += 256) {  // Gram: B operand is the V chunk
                 const int i = 2 * (e % (CHG / 2)), j = e / (CHG / 2);
                 if (j < nc && (!gram || c0 - cbeg + j < kw))  // Gram: V's columns beyond kw are zero
                     cp_async16(cb + i + j * LDS_, A + (J0 + r0 + i) + static_cast<long long>(c0 + j) * ld);
@@ -875,7 +875,7 @@ __global__ void __launch_bounds__(256) k_vtc(const double* __restrict__ a, int l
             else if (v_direct(r, j, kw, v)) *dst = v;
             else cp_async8(dst, A + (J0 + r) + static_cast<long long>(J0 + j) * ld, true);
         }
-        for (int e = threadIdx.x; e < CHG * TCG; e += 256) {
+        for (int e = threadIdx.x; e < (gram ? 0 : CHG * TCG); e += 256) {
             const int i = e % CHG, j = e / CHG, r = r0 + i;
             double* dst = cb + i + j * LDS_;
             double v;
@@ -885,6 +885,14 @@ __global__ void __launch_bounds__(256) k_vtc(const double* __restrict__ a, int l
         }
         cp_commit();
     };
+    // Gram mode (KB = KO): k_tmerge reads only the six 32 x 32 blocks above the block diagonal
+    // (G01, G23, GAB), so warps 0..5 take one each (two per scheduler at most) with both operands
+    // from the V chunk; rbk / gcb = the block's row / column index
+    int rbk = mw, gcb = 0;
+    if (gram) {
+        rbk = wid < 3 ? 0 : (wid < 5 ? 1 : 2);
+        gcb = wid < 3 ? wid + 1 : (wid < 5 ? wid - 1 : 3);
+    }
     double acc[PM][PN][2] = {};
     if (nchunk > 0) issue(0);
     for (int c = 0; c < nchunk; ++c) {
@@ -896,14 +904,15 @@ __global__ void __launch_bounds__(256) k_vtc(const double* __restrict__ a, int l
         }
         __syncthreads();
         const double* sV = sV0 + (c & 1) * (KB * LDS_);
-        const double* sC = sC0 + (c & 1) * (TCG * LDS_);
+        const double* sC = gram ? sV + (gcb * PN * 8) * LDS_ : sC0 + (c & 1) * (TCG * LDS_) + (nw * PN * 8) * LDS_;
+        if (!gram || wid < 6)
 #pragma unroll
         for (int k0 = 0; k0 < CHG; k0 += 4) {
             double av[PM], bv[PN];
 #pragma unroll
-            for (int i = 0; i < PM; ++i) av[i] = sV[(k0 + t4) + ((mw * PM + i) * 8 + g) * LDS_];
+            for (int i = 0; i < PM; ++i) av[i] = sV[(k0 + t4) + ((rbk * PM + i) * 8 + g) * LDS_];
 #pragma unroll
-            for (int q = 0; q < PN; ++q) bv[q] = sC[(k0 + t4) + ((nw * PN + q) * 8 + g) * LDS_];
+            for (int q = 0; q < PN; ++q) bv[q] = sC[(k0 + t4) + (q * 8 + g) * LDS_];
 #pragma unroll
             for (int i = 0; i < PM; ++i)
 #pragma unroll
@@ -942,6 +951,19 @@ __global__ void __launch_bounds__(256) k_vtc(const double* __restrict__ a, int l
         for (int i = 0; i < PM; ++i)
 #pragma unroll
             for (int q = 0; q < PN; ++q) acc[i][q][0] = acc2[i][q][0], acc[i][q][1] = acc2[i][q][1];
+    }
+    if (gram) {
+        if (wid < 6)
+#pragma unroll
+            for (int i = 0; i < PM; ++i)
+#pragma unroll
+                for (int q = 0; q < PN; ++q) {
+                    const int row = (rbk * PM + i) * 8 + g, colg = (gcb * PN + q) * 8 + 2 * t4;
+                    double* Wt = W + static_cast<long long>(colg / TCG) * (KB * TCG);
+                    Wt[row + (colg % TCG) * KB] = acc[i][q][0];
+                    Wt[row + (colg % TCG + 1) * KB] = acc[i][q][1];
+                }
+        return;
     }
 #pragma unroll
     for (int i = 0; i < PM; ++i)
@@ -1458,7 +1480,7 @@ void apply_block(BigWs& ws, int nbatch, int m, int ld, long long stride, double*
     long long best = -1;
     for (int cand = 1; cand <= std::min(64, std::max(1, nchunks / 2)); ++cand) {
         const int per = (nchunks + cand - 1) / cand;
-        const long long waves = (static_cast<long long>(ntile) * cand * nbatch + resident - 1) / resident;
+        const long long waves = (static_cast<long long>(gram ? 1 : ntile) * cand * nbatch + resident - 1) / resident;
         const long long cost = waves * (per + 2);  // +2: fixed cost per CTA (prologue, partial write)
         if (best < 0 || cost < best) {
             best = cost;
@@ -1471,7 +1493,7 @@ void apply_block(BigWs& ws, int nbatch, int m, int ld, long long stride, double*
     {
         static SmemCfg cfg;
         smem_optin(reinterpret_cast<const void*>(k_vtc<KB>), vtc_smem(KB), cfg);
-        k_vtc<KB><<<dim3(ntile, nsl, nbatch), 256, vtc_smem(KB), st>>>(d_a, ld, stride, m, J0, kw, cbeg, cend, rs, gram,
+        k_vtc<KB><<<dim3(gram ? 1 : ntile, nsl, nbatch), 256, vtc_smem(KB), st>>>(d_a, ld, stride, m, J0, kw, cbeg, cend, rs, gram,
                                                                          wp, (nsl == 1 && !gram) ? T_all : nullptr);
     }
     if (gram) {
